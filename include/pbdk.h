@@ -1,0 +1,75 @@
+/*
+ * pbdk.h — C-ABI of the B200 (sm_100a) blockwise-distillation kernels.
+ *
+ * The reference (Pipe-BD, /root/reference) has no device code: it models each
+ * of these operations as a cost term of Algorithm 1.  The
+ * entry points below are the device implementation of those terms:
+ *
+ *   pbdk_conv_fprop   teacher T_i.forward / student S_i.forward convolutions,
+ *                     and the student dgrad (conv with flipped weights)
+ *                     — "teacher_fwd" / "student_fwd_bwd", simulate.cpp:217-235
+ *   pbdk_conv_wgrad   student weight gradient — inside S_k (cost_model.cpp:38-66)
+ *   pbdk_bn_*         training-mode BatchNorm of the student (forward/backward)
+ *   pbdk_mse_*        fused distillation loss L(s,t) + dL/ds
+ *   pbdk_sgd_momentum S_i.update_weight() (simulate.cpp:243-261)
+ *   pbdk_philox_*     load_data() for the first partition
+ *
+ * Conventions: POD descriptors, caller-owned device memory,
+ * no allocation inside the calls, explicit stream (a cudaStream_t passed as
+ * void*), int status.  Activations are NHWC bf16; channel counts are the
+ * STORED (padded) counts — the image's 3 channels are stored as 16.
+ * Weights are [K][R][S][C] bf16 (K-major for the implicit GEMM).
+ */
+#ifndef PBDK_H_
+#define PBDK_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define PBDK_OK 0
+#define PBDK_EINVAL 1  /* unsupported / inconsistent shape: maps to pbd::ValidationError */
+#define PBDK_ECUDA 2   /* CUDA launch or driver error: maps to pbd::DeviceError */
+
+/* convolution epilogues (fprop) */
+#define PBDK_EPI_STORE 0          /* y = acc                                   */
+#define PBDK_EPI_BIAS 1           /* y = acc + bias[k]                         */
+#define PBDK_EPI_BIAS_RELU 2      /* y = relu(acc + bias[k])                   */
+#define PBDK_EPI_BIAS_RES_RELU 3  /* y = relu(acc + bias[k] + aux[m][k])       */
+#define PBDK_EPI_RELU_MASK 4      /* y = aux[m][k] > 0 ? acc : 0   (relu bwd)  */
+
+typedef struct pbdk_conv_desc {
+  int n, h, w, c;  /* input NHWC, c = stored channels (multiple of 16) */
+  int k;           /* output channels (multiple of 16)                */
+  int r, s;        /* filter height / width                           */
+  int stride, pad; /* symmetric                                       */
+  int p, q;        /* output height / width                           */
+} pbdk_conv_desc;
+
+/* Library identity: returns "sm_100a" build tag; used by loaders to fail loudly. */
+const char* pbdk_build_info(void);
+
+/* y[n,p,q,k] = epi( sum_{r,s,c} x[n, p*st+r-pad, q*st+s-pad, c] * w[k,r,s,c] )
+ * tcgen05 implicit GEMM: M = n*p*q pixels (128 per tile), N = k, K = r*s*c. */
+int pbdk_conv_fprop(const pbdk_conv_desc* d, const void* x, const void* w, void* y, const float* bias,
+                    const void* aux, int epilogue, void* stream);
+
+/* dw[k,r,s,c] = sum_{n,p,q} dy[n,p,q,k] * x[n, p*st+r-pad, q*st+s-pad, c]   (fp32 out)
+ * tcgen05 GEMM with MN-major operands, split-K over pixels; `workspace` must hold
+ * pbdk_conv_wgrad_workspace_bytes(d) bytes (may be 0 => no workspace needed). */
+size_t pbdk_conv_wgrad_workspace_bytes(const pbdk_conv_desc* d);
+int pbdk_conv_wgrad(const pbdk_conv_desc* d, const void* x, const void* dy, float* dw, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
+/* wt[c,r',s',k] = w[k,R-1-r',S-1-s',c]  (bf16 -> bf16): weights of the dgrad conv. */
+int pbdk_weight_flip(const void* w, void* wt, int k, int r, int s, int c, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PBDK_H_ */

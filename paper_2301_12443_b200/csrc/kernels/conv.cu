@@ -1,0 +1,655 @@
+// tcgen05 implicit-GEMM convolutions for sm_100a.
+//
+//   fprop: D[m, k] = sum_{tap, c} X[pix(m, tap), c] * W[k, tap, c]
+//          A = X tile (128 output pixels x BKC channels, K-major) via one 4D TMA box per
+//          (tap, channel chunk); out-of-image taps are zero-filled by TMA OOB handling,
+//          stride-2 convs use TMA element strides. B = W tile (BN x BKC, K-major).
+//          Accumulator in TMEM (128 lanes x BN fp32 columns); fused epilogue.
+//   wgrad: D[k, c] (per tap) = sum_m dY[m, k] * X[pix(m, tap), c]
+//          A = dY tile, B = X tile, both MN-major (pixels are the reduction dim),
+//          split-K over output-pixel tiles, deterministic fixed-order reduction.
+//
+// Warp roles (192 threads): warp 0 TMA producer, warp 1 MMA issuer (one thread),
+// warps 2-5 epilogue (TMEM lane quarter = warp % 4); warp 2 owns TMEM alloc.
+#include "conv.hpp"
+#include "sm100.cuh"
+#include "tmap.hpp"
+
+#include <algorithm>
+
+namespace pbdk {
+
+namespace {
+
+constexpr int kThreads = 192;
+constexpr int kSmemBudget = 200 * 1024;
+
+__host__ __device__ constexpr int layout_for_sw(int sw) { return sw == 128 ? 2 : (sw == 64 ? 4 : 6); }
+__host__ __device__ constexpr int round_up(int a, int b) { return (a + b - 1) / b * b; }
+__host__ __device__ constexpr int tmem_cols_for(int n) { return n <= 32 ? 32 : (n <= 64 ? 64 : (n <= 128 ? 128 : 256)); }
+
+template <int BN, int BKC>
+struct FpropCfg {
+  static constexpr int SW = BKC * 2;  // bytes per smem row == swizzle span
+  static constexpr int LAYOUT = layout_for_sw(SW);
+  static constexpr int A_BYTES = 128 * SW;
+  static constexpr int B_BYTES = BN * SW;
+  static constexpr int STAGE = round_up(A_BYTES + B_BYTES, 1024);
+  static constexpr int STAGES = (kSmemBudget / STAGE) > 8 ? 8 : (kSmemBudget / STAGE);
+  static constexpr int TMEM_COLS = tmem_cols_for(BN);
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+};
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+
+template <int BN, int BKC>
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_fprop_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
+                      const FpropArgs a) {
+  using C = FpropCfg<BN, BKC>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int k0 = blockIdx.x * BN;
+  const int m_tile = blockIdx.y;
+  const int tq = m_tile % a.tiles_q;
+  const int t2 = m_tile / a.tiles_q;
+  const int tp = t2 % a.tiles_p;
+  const int tn = t2 / a.tiles_p;
+  const int ow0 = tq * a.bw, oh0 = tp * a.bh, n0 = tn * a.bn;
+  const int num_kb = a.r * a.s * a.c_chunks;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmx);
+    tma_prefetch(&tmw);
+    for (int i = 0; i < C::STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(tfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int cin_stored = a.c_chunks * BKC;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int st = kb % C::STAGES;
+        if (kb >= C::STAGES) mbar_wait(&empty[st], ((kb / C::STAGES) - 1) & 1);
+        const int tap = kb / a.c_chunks;
+        const int cc = kb - tap * a.c_chunks;
+        const int rr = tap / a.s;
+        const int ss = tap - rr * a.s;
+        uint8_t* sa = smem + st * C::STAGE;
+        uint8_t* sb = sa + C::A_BYTES;
+        mbar_arrive_expect_tx(&full[st], C::A_BYTES + C::B_BYTES);
+        tma_load_4d(sa, &tmx, &full[st], cc * BKC, ow0 * a.stride + ss - a.pad, oh0 * a.stride + rr - a.pad, n0);
+        tma_load_2d(sb, &tmw, &full[st], tap * cin_stored + cc * BKC, k0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(128, BN, 0, 0);
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int st = kb % C::STAGES;
+        mbar_wait(&full[st], (kb / C::STAGES) & 1);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + st * C::STAGE);
+        const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < BKC / 16; ++kk) {
+          const uint64_t ad = umma_smem_desc(sa + kk * 32, 16, 8 * C::SW, C::LAYOUT);
+          const uint64_t bd = umma_smem_desc(sb + kk * 32, 16, 8 * C::SW, C::LAYOUT);
+          umma_bf16(tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+        }
+        umma_commit(&empty[st]);
+      }
+      umma_commit(tfull);
+    }
+  } else {
+    // epilogue: warps 2..5, TMEM lane quarter = warp % 4
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const int iw = row % a.bw;
+    const int ih = (row / a.bw) % a.bh;
+    const int in = row / (a.bw * a.bh);
+    const int nn = n0 + in;
+    const bool valid = nn < a.n;
+    const size_t m = (static_cast<size_t>(nn) * a.p + (oh0 + ih)) * a.q + (ow0 + iw);
+    const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      float v[16];
+      tmem_ld16(trow + c0, v);
+      if (valid) {
+        const int col = k0 + c0;
+        if (a.epi == PBDK_EPI_BIAS || a.epi == PBDK_EPI_BIAS_RELU || a.epi == PBDK_EPI_BIAS_RES_RELU) {
+          const float4* b4 = reinterpret_cast<const float4*>(a.bias + col);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float4 b = __ldg(b4 + j);
+            v[4 * j + 0] += b.x;
+            v[4 * j + 1] += b.y;
+            v[4 * j + 2] += b.z;
+            v[4 * j + 3] += b.w;
+          }
+        }
+        if (a.epi == PBDK_EPI_BIAS_RES_RELU || a.epi == PBDK_EPI_RELU_MASK) {
+          const uint4* r4 = reinterpret_cast<const uint4*>(a.aux + m * a.k + col);
+          const uint4 ra = __ldg(r4);
+          const uint4 rb = __ldg(r4 + 1);
+          const uint32_t rw[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+          if (a.epi == PBDK_EPI_BIAS_RES_RELU) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              v[2 * j] += bf16_lo(rw[j]);
+              v[2 * j + 1] += bf16_hi(rw[j]);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              v[2 * j] = bf16_lo(rw[j]) > 0.f ? v[2 * j] : 0.f;
+              v[2 * j + 1] = bf16_hi(rw[j]) > 0.f ? v[2 * j + 1] : 0.f;
+            }
+          }
+        }
+        if (a.epi == PBDK_EPI_BIAS_RELU || a.epi == PBDK_EPI_BIAS_RES_RELU) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j], 0.f);
+        }
+        uint4 o0, o1;
+        o0.x = pack_bf16x2(v[0], v[1]);
+        o0.y = pack_bf16x2(v[2], v[3]);
+        o0.z = pack_bf16x2(v[4], v[5]);
+        o0.w = pack_bf16x2(v[6], v[7]);
+        o1.x = pack_bf16x2(v[8], v[9]);
+        o1.y = pack_bf16x2(v[10], v[11]);
+        o1.z = pack_bf16x2(v[12], v[13]);
+        o1.w = pack_bf16x2(v[14], v[15]);
+        uint4* dst = reinterpret_cast<uint4*>(a.y + m * a.k + col);
+        dst[0] = o0;
+        dst[1] = o1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+template <int BN, int BKC>
+cudaError_t launch_fprop(const FpropPlan& p, cudaStream_t stream) {
+  using C = FpropCfg<BN, BKC>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(conv_fprop_kernel<BN, BKC>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  conv_fprop_kernel<BN, BKC><<<p.grid, kThreads, C::SMEM, stream>>>(p.tmx, p.tmw, p.args);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ wgrad
+
+template <int BN, int SWA, int SWB>
+struct WgradCfg {
+  static constexpr int KT = 128;                       // pixels per stage
+  static constexpr int A_ATOM = KT * SWA;              // one MN atom of A (SWA/2 channels of k)
+  static constexpr int A_BYTES = 128 * KT * 2;         // full M=128 region
+  static constexpr int B_ATOM = KT * SWB;
+  static constexpr int B_ATOMS = BN / (SWB / 2);
+  static constexpr int B_BYTES = B_ATOMS * B_ATOM;
+  static constexpr int STAGE = round_up(A_BYTES + B_BYTES, 1024);
+  static constexpr int STAGES = (kSmemBudget / STAGE) > 6 ? 6 : (kSmemBudget / STAGE);
+  static constexpr int TMEM_COLS = tmem_cols_for(BN);
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+};
+
+template <int BN, int SWA, int SWB>
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_wgrad_kernel(const __grid_constant__ CUtensorMap tmdy, const __grid_constant__ CUtensorMap tmx,
+                      const WgradArgs a) {
+  using C = WgradCfg<BN, SWA, SWB>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  int t = blockIdx.x;
+  const int ci_t = t % a.ci_tiles;
+  t /= a.ci_tiles;
+  const int co_t = t % a.co_tiles;
+  const int tap = t / a.co_tiles;
+  const int rr = tap / a.s;
+  const int ss = tap - rr * a.s;
+  const int co0 = co_t * 128;
+  const int ci0 = ci_t * BN;
+  const int split = blockIdx.y;
+  const int mt0 = split * a.tiles_per_split;
+  const int mt1 = min(a.m_tiles, mt0 + a.tiles_per_split);
+  const int num_kb = max(0, mt1 - mt0);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmdy);
+    tma_prefetch(&tmx);
+    for (int i = 0; i < C::STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(tfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t bytes = static_cast<uint32_t>(a.a_atoms * C::A_ATOM + C::B_BYTES);
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int st = kb % C::STAGES;
+        if (kb >= C::STAGES) mbar_wait(&empty[st], ((kb / C::STAGES) - 1) & 1);
+        const int mt = mt0 + kb;
+        const int tq = mt % a.tiles_q;
+        const int t2 = mt / a.tiles_q;
+        const int tp = t2 % a.tiles_p;
+        const int tn = t2 / a.tiles_p;
+        const int ow0 = tq * a.bw, oh0 = tp * a.bh, n0 = tn * a.bn;
+        uint8_t* sa = smem + st * C::STAGE;
+        uint8_t* sb = sa + C::A_BYTES;
+        mbar_arrive_expect_tx(&full[st], bytes);
+        for (int i = 0; i < a.a_atoms; ++i)
+          tma_load_4d(sa + i * C::A_ATOM, &tmdy, &full[st], co0 + i * (SWA / 2), ow0, oh0, n0);
+#pragma unroll
+        for (int i = 0; i < C::B_ATOMS; ++i)
+          tma_load_4d(sb + i * C::B_ATOM, &tmx, &full[st], ci0 + i * (SWB / 2), ow0 * a.stride + ss - a.pad,
+                      oh0 * a.stride + rr - a.pad, n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(128, BN, 1, 1);
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int st = kb % C::STAGES;
+        mbar_wait(&full[st], (kb / C::STAGES) & 1);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + st * C::STAGE);
+        const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < C::KT / 16; ++kk) {
+          // MN-major canonical layout: LBO = stride between MN atoms, SBO = 8 K-rows.
+          const uint64_t ad = umma_smem_desc(sa + kk * 16 * SWA, C::A_ATOM, 8 * SWA, layout_for_sw(SWA));
+          const uint64_t bd = umma_smem_desc(sb + kk * 16 * SWB, C::B_ATOM, 8 * SWB, layout_for_sw(SWB));
+          umma_bf16(tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+        }
+        umma_commit(&empty[st]);
+      }
+      if (num_kb > 0) umma_commit(tfull);
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int co = co0 + quarter * 32 + lane;
+    const int taps = a.r * a.s;
+    float* dst_row = a.out + static_cast<size_t>(split) * a.k * taps * a.c +
+                     (static_cast<size_t>(co) * taps + tap) * a.c + ci0;
+    if (num_kb > 0) {
+      mbar_wait(tfull, 0);
+      tc_fence_after();
+      const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        float v[16];
+        tmem_ld16(trow + c0, v);
+        if (co < a.k) {
+          float4* d4 = reinterpret_cast<float4*>(dst_row + c0);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        }
+      }
+    } else if (co < a.k) {
+      for (int c0 = 0; c0 < BN; c0 += 4)
+        *reinterpret_cast<float4*>(dst_row + c0) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+template <int BN, int SWA, int SWB>
+cudaError_t launch_wgrad(const WgradPlan& p, cudaStream_t stream) {
+  using C = WgradCfg<BN, SWA, SWB>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e =
+        cudaFuncSetAttribute(conv_wgrad_kernel<BN, SWA, SWB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  conv_wgrad_kernel<BN, SWA, SWB><<<p.grid, kThreads, C::SMEM, stream>>>(p.tmdy, p.tmx, p.args);
+  return cudaGetLastError();
+}
+
+// Fixed-order split reduction: dw[i] = sum_s ws[s][i]  (deterministic).
+__global__ void split_reduce_kernel(const float4* __restrict__ ws, float4* __restrict__ dw, size_t n4, int splits) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
+    float4 acc = ws[i];
+    for (int s = 1; s < splits; ++s) {
+      const float4 v = ws[s * n4 + i];
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    dw[i] = acc;
+  }
+}
+
+__global__ void weight_flip_kernel(const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ wt, int k, int r,
+                                   int s, int c) {
+  const size_t total = static_cast<size_t>(k) * r * s * c;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    // i indexes wt[ci][r'][s'][co]
+    const int co = static_cast<int>(i % k);
+    size_t t = i / k;
+    const int sp = static_cast<int>(t % s);
+    t /= s;
+    const int rp = static_cast<int>(t % r);
+    const int ci = static_cast<int>(t / r);
+    wt[i] = w[((static_cast<size_t>(co) * r + (r - 1 - rp)) * s + (s - 1 - sp)) * c + ci];
+  }
+}
+
+bool chan_ok(int c) { return c == 16 || c == 32 || (c >= 64 && c % 64 == 0); }
+int chan_block(int c) { return c >= 64 ? 64 : c; }
+
+}  // namespace
+
+bool make_geom(const pbdk_conv_desc& d, ConvGeom* g) {
+  if (d.n < 1 || d.h < 1 || d.w < 1 || d.r < 1 || d.s < 1 || d.stride < 1 || d.pad < 0) return false;
+  if (d.p != (d.h + 2 * d.pad - d.r) / d.stride + 1) return false;
+  if (d.q != (d.w + 2 * d.pad - d.s) / d.stride + 1) return false;
+  if (d.q > 128 || 128 % d.q != 0) return false;
+  g->d = d;
+  g->bw = d.q;
+  const int rows = 128 / d.q;
+  g->bh = std::min(d.p, rows);
+  if (rows % g->bh != 0 || d.p % g->bh != 0) return false;
+  g->bn = rows / g->bh;
+  if (g->bw * d.stride > 256 || g->bh * d.stride > 256 || g->bn > 256) return false;
+  g->tiles_q = d.q / g->bw;
+  g->tiles_p = d.p / g->bh;
+  g->tiles_n = (d.n + g->bn - 1) / g->bn;
+  g->m_tiles = g->tiles_q * g->tiles_p * g->tiles_n;
+  return true;
+}
+
+namespace {
+
+// 4D map over an NHWC bf16 activation, box = one 128-pixel tile of `chan` channels.
+bool act_map(CUtensorMap* m, const void* base, int n, int h, int w, int c, int chan, int bw, int bh, int bn,
+             int stride) {
+  const uint64_t dims[4] = {static_cast<uint64_t>(c), static_cast<uint64_t>(w), static_cast<uint64_t>(h),
+                            static_cast<uint64_t>(n)};
+  const uint64_t strides[3] = {static_cast<uint64_t>(c) * 2, static_cast<uint64_t>(w) * c * 2,
+                               static_cast<uint64_t>(h) * w * c * 2};
+  const uint32_t box[4] = {static_cast<uint32_t>(chan), static_cast<uint32_t>(bw * stride),
+                           static_cast<uint32_t>(bh * stride), static_cast<uint32_t>(bn)};
+  const uint32_t es[4] = {1, static_cast<uint32_t>(stride), static_cast<uint32_t>(stride), 1};
+  return encode_tmap_bf16(m, base, 4, dims, strides, box, es, chan * 2);
+}
+
+using FpropLauncher = cudaError_t (*)(const FpropPlan&, cudaStream_t);
+
+template <int BKC>
+FpropLauncher pick_fprop(int bn) {
+  switch (bn) {
+    case 16: return launch_fprop<16, BKC>;
+    case 32: return launch_fprop<32, BKC>;
+    case 64: return launch_fprop<64, BKC>;
+    case 128: return launch_fprop<128, BKC>;
+    case 256: return launch_fprop<256, BKC>;
+    default: return nullptr;
+  }
+}
+
+int fprop_smem(int bn, int bkc) {
+  const int sw = bkc * 2;
+  const int stage = round_up(128 * sw + bn * sw, 1024);
+  const int stages = std::min(8, kSmemBudget / stage);
+  return stages * stage + 1024 + 256;
+}
+
+using WgradLauncher = cudaError_t (*)(const WgradPlan&, cudaStream_t);
+
+template <int SWA>
+WgradLauncher pick_wgrad_b(int bn, int swb) {
+  if (swb == 32 && bn == 16) return launch_wgrad<16, SWA, 32>;
+  if (swb == 64 && bn == 32) return launch_wgrad<32, SWA, 64>;
+  if (swb == 128 && bn == 64) return launch_wgrad<64, SWA, 128>;
+  if (swb == 128 && bn == 128) return launch_wgrad<128, SWA, 128>;
+  return nullptr;
+}
+
+WgradLauncher pick_wgrad(int bn, int swa, int swb) {
+  switch (swa) {
+    case 32: return pick_wgrad_b<32>(bn, swb);
+    case 64: return pick_wgrad_b<64>(bn, swb);
+    case 128: return pick_wgrad_b<128>(bn, swb);
+    default: return nullptr;
+  }
+}
+
+int wgrad_bn(int c) { return c >= 128 ? 128 : c; }
+
+}  // namespace
+
+int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, const float* bias, const void* aux,
+               int epi, FpropPlan* plan) {
+  ConvGeom g;
+  if (!make_geom(d, &g) || !chan_ok(d.c) || d.k % 16 != 0 || d.k < 16) return PBDK_EINVAL;
+  if (epi < PBDK_EPI_STORE || epi > PBDK_EPI_RELU_MASK) return PBDK_EINVAL;
+  if ((epi == PBDK_EPI_BIAS || epi == PBDK_EPI_BIAS_RELU || epi == PBDK_EPI_BIAS_RES_RELU) && bias == nullptr)
+    return PBDK_EINVAL;
+  if ((epi == PBDK_EPI_BIAS_RES_RELU || epi == PBDK_EPI_RELU_MASK) && aux == nullptr) return PBDK_EINVAL;
+  const int bkc = chan_block(d.c);
+  int bn = 16;
+  for (int cand : {256, 128, 64, 32, 16}) {
+    if (d.k % cand == 0) {
+      bn = cand;
+      break;
+    }
+  }
+  FpropLauncher l = nullptr;
+  switch (bkc) {
+    case 16: l = pick_fprop<16>(bn); break;
+    case 32: l = pick_fprop<32>(bn); break;
+    case 64: l = pick_fprop<64>(bn); break;
+    default: break;
+  }
+  if (l == nullptr) return PBDK_EINVAL;
+  if (!act_map(&plan->tmx, x, d.n, d.h, d.w, d.c, bkc, g.bw, g.bh, g.bn, d.stride)) return PBDK_ECUDA;
+  {
+    const uint64_t ktot = static_cast<uint64_t>(d.r) * d.s * d.c;
+    const uint64_t dims[2] = {ktot, static_cast<uint64_t>(d.k)};
+    const uint64_t strides[1] = {ktot * 2};
+    const uint32_t box[2] = {static_cast<uint32_t>(bkc), static_cast<uint32_t>(bn)};
+    const uint32_t es[2] = {1, 1};
+    if (!encode_tmap_bf16(&plan->tmw, w, 2, dims, strides, box, es, bkc * 2)) return PBDK_ECUDA;
+  }
+  FpropArgs& a = plan->args;
+  a.n = d.n;
+  a.p = d.p;
+  a.q = d.q;
+  a.k = d.k;
+  a.stride = d.stride;
+  a.pad = d.pad;
+  a.r = d.r;
+  a.s = d.s;
+  a.bw = g.bw;
+  a.bh = g.bh;
+  a.bn = g.bn;
+  a.tiles_q = g.tiles_q;
+  a.tiles_p = g.tiles_p;
+  a.c_chunks = d.c / bkc;
+  a.epi = epi;
+  a.y = static_cast<__nv_bfloat16*>(y);
+  a.bias = bias;
+  a.aux = static_cast<const __nv_bfloat16*>(aux);
+  plan->grid = dim3(static_cast<unsigned>(d.k / bn), static_cast<unsigned>(g.m_tiles), 1);
+  plan->bn_tile = bn;
+  plan->bkc = bkc;
+  plan->smem_bytes = fprop_smem(bn, bkc);
+  plan->launch = l;
+  return PBDK_OK;
+}
+
+int fprop_run(const FpropPlan& plan, cudaStream_t stream) {
+  if (plan.launch == nullptr) return PBDK_EINVAL;
+  return plan.launch(plan, stream) == cudaSuccess ? PBDK_OK : PBDK_ECUDA;
+}
+
+int wgrad_splits(const ConvGeom& g) {
+  const int co_tiles = (g.d.k + 127) / 128;
+  const int ci_tiles = g.d.c / wgrad_bn(g.d.c);
+  const int tiles = co_tiles * ci_tiles * g.d.r * g.d.s;
+  const int target = 2 * 148;
+  int splits = std::max(1, target / tiles);
+  splits = std::min(splits, std::max(1, g.m_tiles / 4));  // >= 4 pixel tiles per split
+  return splits;
+}
+
+size_t wgrad_workspace_bytes(const pbdk_conv_desc& d) {
+  ConvGeom g;
+  if (!make_geom(d, &g)) return 0;
+  const int splits = wgrad_splits(g);
+  if (splits <= 1) return 0;
+  return static_cast<size_t>(splits) * d.k * d.r * d.s * d.c * sizeof(float);
+}
+
+int wgrad_plan(const pbdk_conv_desc& d, const void* x, const void* dy, float* dw, void* ws, size_t ws_bytes,
+               WgradPlan* plan) {
+  ConvGeom g;
+  if (!make_geom(d, &g) || !chan_ok(d.c) || !chan_ok(d.k)) return PBDK_EINVAL;
+  const int swa = chan_block(d.k) * 2;
+  const int swb = chan_block(d.c) * 2;
+  const int bn = wgrad_bn(d.c);
+  WgradLauncher l = pick_wgrad(bn, swa, swb);
+  if (l == nullptr) return PBDK_EINVAL;
+  const int splits = wgrad_splits(g);
+  const size_t slab = static_cast<size_t>(d.k) * d.r * d.s * d.c;
+  if (splits > 1 && (ws == nullptr || ws_bytes < splits * slab * sizeof(float))) return PBDK_EINVAL;
+  if (!act_map(&plan->tmdy, dy, d.n, d.p, d.q, d.k, swa / 2, g.bw, g.bh, g.bn, 1)) return PBDK_ECUDA;
+  if (!act_map(&plan->tmx, x, d.n, d.h, d.w, d.c, swb / 2, g.bw, g.bh, g.bn, d.stride)) return PBDK_ECUDA;
+  WgradArgs& a = plan->args;
+  a.n = d.n;
+  a.p = d.p;
+  a.q = d.q;
+  a.k = d.k;
+  a.c = d.c;
+  a.stride = d.stride;
+  a.pad = d.pad;
+  a.r = d.r;
+  a.s = d.s;
+  a.bw = g.bw;
+  a.bh = g.bh;
+  a.bn = g.bn;
+  a.tiles_q = g.tiles_q;
+  a.tiles_p = g.tiles_p;
+  a.m_tiles = g.m_tiles;
+  a.co_tiles = (d.k + 127) / 128;
+  a.ci_tiles = d.c / bn;
+  a.tiles_per_split = (g.m_tiles + splits - 1) / splits;
+  a.a_atoms = (std::min(128, d.k) + swa / 2 - 1) / (swa / 2);
+  a.out = splits > 1 ? static_cast<float*>(ws) : dw;
+  plan->grid = dim3(static_cast<unsigned>(a.co_tiles * a.ci_tiles * d.r * d.s), static_cast<unsigned>(splits), 1);
+  plan->splits = splits;
+  plan->bn_tile = bn;
+  plan->dw = dw;
+  plan->slab = slab;
+  plan->launch = l;
+  return PBDK_OK;
+}
+
+int wgrad_run(const WgradPlan& plan, cudaStream_t stream) {
+  if (plan.launch == nullptr) return PBDK_EINVAL;
+  if (plan.launch(plan, stream) != cudaSuccess) return PBDK_ECUDA;
+  if (plan.splits > 1) {
+    const size_t n4 = plan.slab / 4;
+    const int blocks = static_cast<int>(std::min<size_t>((n4 + 255) / 256, 148 * 8));
+    split_reduce_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<const float4*>(plan.args.out),
+                                                    reinterpret_cast<float4*>(plan.dw), n4, plan.splits);
+    if (cudaGetLastError() != cudaSuccess) return PBDK_ECUDA;
+  }
+  return PBDK_OK;
+}
+
+}  // namespace pbdk
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+const char* pbdk_build_info(void) { return "pbdk sm_100a tcgen05"; }
+
+int pbdk_conv_fprop(const pbdk_conv_desc* d, const void* x, const void* w, void* y, const float* bias,
+                    const void* aux, int epilogue, void* stream) {
+  if (d == nullptr) return PBDK_EINVAL;
+  pbdk::FpropPlan plan;
+  const int rc = pbdk::fprop_plan(*d, x, w, y, bias, aux, epilogue, &plan);
+  if (rc != PBDK_OK) return rc;
+  return pbdk::fprop_run(plan, static_cast<cudaStream_t>(stream));
+}
+
+size_t pbdk_conv_wgrad_workspace_bytes(const pbdk_conv_desc* d) {
+  return d == nullptr ? 0 : pbdk::wgrad_workspace_bytes(*d);
+}
+
+int pbdk_conv_wgrad(const pbdk_conv_desc* d, const void* x, const void* dy, float* dw, void* workspace,
+                    size_t workspace_bytes, void* stream) {
+  if (d == nullptr) return PBDK_EINVAL;
+  pbdk::WgradPlan plan;
+  const int rc = pbdk::wgrad_plan(*d, x, dy, dw, workspace, workspace_bytes, &plan);
+  if (rc != PBDK_OK) return rc;
+  return pbdk::wgrad_run(plan, static_cast<cudaStream_t>(stream));
+}
+
+int pbdk_weight_flip(const void* w, void* wt, int k, int r, int s, int c, void* stream) {
+  if (w == nullptr || wt == nullptr || k < 1 || r < 1 || s < 1 || c < 1) return PBDK_EINVAL;
+  const size_t total = static_cast<size_t>(k) * r * s * c;
+  const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 16));
+  pbdk::weight_flip_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(w), static_cast<__nv_bfloat16*>(wt), k, r, s, c);
+  return cudaGetLastError() == cudaSuccess ? PBDK_OK : PBDK_ECUDA;
+}
+
+}  // extern "C"
