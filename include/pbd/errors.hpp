@@ -1,0 +1,3 @@
+// Forwarding header: the reference API of proj/core/include/pbd/errors.hpp lives in pbd/core.hpp.
+#pragma once
+#include "pbd/core.hpp"
