@@ -68,6 +68,65 @@ int pbdk_conv_wgrad(const pbdk_conv_desc* d, const void* x, const void* dy, floa
 /* wt[c,r',s',k] = w[k,R-1-r',S-1-s',c]  (bf16 -> bf16): weights of the dgrad conv. */
 int pbdk_weight_flip(const void* w, void* wt, int k, int r, int s, int c, void* stream);
 
+
+/* ------------------------------------------------------------------ K12: synthetic input (load_data) */
+/* x[n][32][32][16] bf16 (3 Philox channels + 13 zero pad channels) for global samples
+ * first_sample + (*step_counter)*global_batch + i  (step_counter may be NULL). */
+int pbdk_philox_image(void* x, int n, long long first_sample, const long long* step_counter, int global_batch,
+                      uint32_t seed, void* stream);
+/* device fp32 NHWC [n][32][32][3] -> padded bf16 [n][32][32][16] */
+int pbdk_pack_image(const float* src, void* x, int n, void* stream);
+/* weights: dst[k][r][s][c_stored] = c < c_true ? U(-1,1)*bound : 0 (Philox counter = (flat unpadded idx, tensor_id)) */
+int pbdk_init_uniform(void* dst, int bf16_out, int k, int r, int s, int c_stored, int c_true, uint32_t seed,
+                      uint32_t tensor_id, float bound, void* stream);
+
+/* ------------------------------------------------------------------ K2/K3/K5: training-mode BatchNorm */
+/* workspace bytes for any of the [m][c] reductions below */
+size_t pbdk_reduce_workspace_bytes(int m, int c);
+/* mean_rstd[0:c] = batch mean, mean_rstd[c:2c] = 1/sqrt(biased var + 1e-5) */
+int pbdk_bn_stats(const void* y, int m, int c, void* workspace, float* mean_rstd, void* stream);
+/* a = bf16(relu(gamma*(y-mean)*rstd + beta)) */
+int pbdk_bn_apply_relu(const void* y, const float* mean_rstd, const float* gamma, const float* beta, void* a, int m,
+                       int c, void* stream);
+/* BN backward given dL/d(bn out) g: red[0:c]=sum g, red[c:2c]=sum g*xhat (also written to dbeta/dgamma),
+ * dy = gamma*rstd/m * (m*g - sum g - xhat*sum g*xhat) in bf16 */
+int pbdk_bn_bwd(const void* g, const void* y, const float* mean_rstd, const float* gamma, int m, int c,
+                void* workspace, float* red, float* dgamma, float* dbeta, void* dy, void* stream);
+
+/* ------------------------------------------------------------------ K4: fused distillation loss + backward */
+/* s = relu(BN2(y2) + BNsc(ysc)); loss = sum (s-t)^2 / norm; g = [s>0] (s-t)*gscale (gscale = 2/norm);
+ * writes dgamma/dbeta of both BNs, red[3c] = {sum g, sum g*xhat2, sum g*xhatsc}, and dy2 / dysc (bf16). */
+typedef struct pbdk_mse_args {
+  const void* y2;
+  const void* ysc;
+  const void* t;
+  const float* stats2;
+  const float* statssc;
+  const float* gamma2;
+  const float* beta2;
+  const float* gammasc;
+  const float* betasc;
+  int m, c;
+  float gscale;
+  double norm;
+  void* workspace;
+  float* red;
+  float* dgamma2;
+  float* dbeta2;
+  float* dgammasc;
+  float* dbetasc;
+  double* loss;
+  void* dy2;
+  void* dysc;
+} pbdk_mse_args;
+int pbdk_mse_bn_loss(const pbdk_mse_args* a, void* stream);
+
+/* ------------------------------------------------------------------ K10: SGD-momentum update */
+/* v = mu*v + g; w = w - lr*v (fmaf); w_bf16 (may be NULL) = bf16(w); ++*step_counter (may be NULL).
+ * n must be a multiple of 4. */
+int pbdk_sgd_momentum(float* w, float* v, const float* g, void* w_bf16, size_t n, float lr, float momentum,
+                      long long* step_counter, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,99 @@
+/*
+ * pbdx.h — C-ABI of the per-GPU partition executor (libpbd.so).
+ *
+ * One executor = one device's share of a Pipe-BD schedule: the contiguous
+ * block range [block_lo, block_hi] of a PartitionSpec (schedule.hpp:28-38)
+ * at a shard of `n` samples of each global batch.  It runs the per-device body
+ * of Algorithm 1 as three phases so the host driver can
+ * put the relay and the gradient allreduce between them:
+ *
+ *   pbdx_teacher_forward   load_data() (block 0) + T_i.forward          (lines 8,10)
+ *                          -> the boundary activation is ready to send   (line 11)
+ *   pbdx_student_step      S_i.forward, L(s,t), S_i.backward            (lines 12-13)
+ *                          -> gradients ready for share_gradient()       (line 14)
+ *   pbdx_apply_update      S_i.update_weight() (fused SGD-momentum)      (line 15)
+ *
+ * Its simulated counterpart is the step loop of simulate.cpp:193-262; the
+ * executor reports the same per-block teacher / student times (CUDA events)
+ * that profile.hpp:30-42 BlockProfile holds, so the partitioner can run on
+ * device-measured T_k(b), S_k(b).
+ *
+ * All device memory is owned by the executor (cudaMalloc).  Buffers that the
+ * driver moves with NCCL are exposed as raw device pointers (pbdx_buffer).
+ * Return codes are pbdk.h's (0 ok, 1 invalid, 2 CUDA error).
+ */
+#ifndef PBDX_H_
+#define PBDX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pbdx_desc {
+  int block_lo, block_hi; /* inclusive range of the 4-block CIFAR ResNet chain  */
+  int n_max;              /* largest shard this executor will run               */
+  int global_batch;       /* b: MSE normalisation + synthetic sample indexing   */
+  uint32_t seed_data, seed_teacher, seed_student;
+  float lr, momentum;
+} pbdx_desc;
+
+/* buffers for pbdx_buffer */
+#define PBDX_BUF_INPUT 0        /* input activation of block_lo (bf16 NHWC; block 0: padded image [n,32,32,16]) */
+#define PBDX_BUF_TEACHER_OUT 1  /* teacher output of block_hi (bf16 NHWC) — the relayed activation */
+#define PBDX_BUF_GRADS 2        /* fp32 flat student gradients of the partition (allreduce target) */
+#define PBDX_BUF_PARAMS 3       /* fp32 flat student master weights */
+#define PBDX_BUF_MOMENTUM 4     /* fp32 flat momentum */
+#define PBDX_BUF_LOSSES 5       /* double[num_blocks]: per-block partial loss of the last step */
+#define PBDX_BUF_STEP 6         /* int64 step counter (advanced by apply_update) */
+#define PBDX_BUF_TEACHER_PARAMS 7 /* bf16 teacher conv weights of block_lo..hi (flat, program order) */
+
+int pbdx_create(const pbdx_desc* d, void** handle);
+void pbdx_destroy(void* handle);
+
+/* Deterministic Philox initialisation of teacher and student parameters. */
+int pbdx_init_params(void* handle, void* stream);
+
+/* Current shard: n samples starting at offset `first` inside the global batch. */
+int pbdx_set_shard(void* handle, int n, int first);
+
+/* 0: block 0 input generated on device by Philox (synthetic data);
+ * 1: block 0 input comes from pbdx_upload_images (host data, e2e path). */
+int pbdx_set_input_mode(void* handle, int external);
+/* host fp32 NHWC [n][32][32][3] (pinned for async) -> device padded bf16 input */
+int pbdx_upload_images(void* handle, const float* host, int n, void* stream);
+
+int pbdx_teacher_forward(void* handle, void* stream);
+int pbdx_student_step(void* handle, void* stream);
+int pbdx_apply_update(void* handle, void* stream);
+/* teacher_forward + student_step + apply_update */
+int pbdx_step(void* handle, void* stream);
+
+/* Capture teacher_forward + student_step + apply_update as one CUDA graph (single-GPU path) and replay it. */
+int pbdx_capture(void* handle, void* stream);
+int pbdx_replay(void* handle, void* stream);
+
+int pbdx_buffer(void* handle, int which, void** ptr, size_t* bytes);
+int pbdx_num_blocks(void* handle);
+/* teacher output t_k (bf16 NHWC [n_max][H][W][C]) of block k inside the partition */
+int pbdx_teacher_act(void* handle, int block, void** ptr, size_t* bytes);
+
+/* Per-block CUDA-event timing of the last step (ms): teacher[k], student[k] for k in the range. */
+int pbdx_set_timing(void* handle, int enabled);
+int pbdx_block_times(void* handle, float* teacher_ms, float* student_ms);
+
+/* Flat student-parameter layout of one block (element offsets, padded storage):
+ * out[9] = {w1, w2, wsc, g1, b1, g2, b2, gsc, bsc}; returns the block's element count
+ * (negative on error).  Block 0 stores its 3 input channels padded to 16. */
+long pbdx_student_layout(int block, long* offsets);
+
+/* Kernel launches issued per step by this executor (for the bench's gpu_launches claim). */
+int pbdx_launches_per_step(void* handle);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PBDX_H_ */

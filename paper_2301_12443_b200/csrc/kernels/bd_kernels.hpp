@@ -1,0 +1,50 @@
+// Internal C++ interface of the HBM-bound blockwise-distillation kernels (bd_kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace pbdk {
+
+struct MseArgs {
+  const void* y2;
+  const void* ysc;
+  const void* t;
+  const float* stats2;
+  const float* statssc;
+  const float* gamma2;
+  const float* beta2;
+  const float* gammasc;
+  const float* betasc;
+  int m, c;
+  float gscale;
+  double norm;
+  float* ws;
+  float* red;
+  float* dgamma2;
+  float* dbeta2;
+  float* dgammasc;
+  float* dbetasc;
+  double* loss;
+  void* dy2;
+  void* dysc;
+};
+
+size_t reduce_workspace_floats(int m, int c, int nv);
+int philox_image(void* x, int n, long long first, const long long* counter, int gb, uint32_t seed, cudaStream_t st);
+int pack_image(const float* src, void* x, int n, cudaStream_t st);
+int init_uniform(void* dst, int bf16_out, int k, int r, int s, int cs, int ct, uint32_t seed, uint32_t tensor,
+                 float bound, cudaStream_t st);
+int fill(float* dst, size_t n, float v, cudaStream_t st);
+int bn_stats(const void* y, int m, int c, float* ws, float* mean_rstd, cudaStream_t st);
+int bn_apply_relu(const void* y, const float* mean_rstd, const float* gamma, const float* beta, void* a, int m, int c,
+                  cudaStream_t st);
+int mse_bn_loss(const MseArgs& a, cudaStream_t st);
+int bn_bwd(const void* g, const void* y, const float* mean_rstd, const float* gamma, int m, int c, float* ws,
+           float* red, float* dgamma, float* dbeta, void* dy, cudaStream_t st);
+int sgd_momentum(float* w, float* v, const float* g, void* shadow, size_t n, float lr, float mu, long long* counter,
+                 cudaStream_t st);
+
+}  // namespace pbdk

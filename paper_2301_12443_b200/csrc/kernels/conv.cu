@@ -198,11 +198,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int BN, int BKC>
 cudaError_t launch_fprop(const FpropPlan& p, cudaStream_t stream) {
   using C = FpropCfg<BN, BKC>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(conv_fprop_kernel<BN, BKC>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
+  if (stream == reinterpret_cast<cudaStream_t>(-1)) {  // prepare: set the smem attribute outside any capture
+    return cudaFuncSetAttribute(conv_fprop_kernel<BN, BKC>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   }
   conv_fprop_kernel<BN, BKC><<<p.grid, kThreads, C::SMEM, stream>>>(p.tmx, p.tmw, p.args);
   return cudaGetLastError();
@@ -347,12 +344,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int BN, int SWA, int SWB>
 cudaError_t launch_wgrad(const WgradPlan& p, cudaStream_t stream) {
   using C = WgradCfg<BN, SWA, SWB>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e =
-        cudaFuncSetAttribute(conv_wgrad_kernel<BN, SWA, SWB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
+  if (stream == reinterpret_cast<cudaStream_t>(-1)) {
+    return cudaFuncSetAttribute(conv_wgrad_kernel<BN, SWA, SWB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                C::SMEM);
   }
   conv_wgrad_kernel<BN, SWA, SWB><<<p.grid, kThreads, C::SMEM, stream>>>(p.tmdy, p.tmx, p.args);
   return cudaGetLastError();
@@ -531,6 +525,7 @@ int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, c
   plan->bkc = bkc;
   plan->smem_bytes = fprop_smem(bn, bkc);
   plan->launch = l;
+  if (l(*plan, reinterpret_cast<cudaStream_t>(-1)) != cudaSuccess) return PBDK_ECUDA;
   return PBDK_OK;
 }
 
@@ -598,6 +593,7 @@ int wgrad_plan(const pbdk_conv_desc& d, const void* x, const void* dy, float* dw
   plan->dw = dw;
   plan->slab = slab;
   plan->launch = l;
+  if (l(*plan, reinterpret_cast<cudaStream_t>(-1)) != cudaSuccess) return PBDK_ECUDA;
   return PBDK_OK;
 }
 

@@ -1,0 +1,228 @@
+"""Python face of the per-GPU partition executor (include/pbdx.h).
+
+``Partition`` owns one device's share of a Pipe-BD schedule: blocks
+[block_lo, block_hi] of the CIFAR ResNet-18 teacher / slim student chain at a
+shard of the global batch.  It exposes the three phases of Algorithm 1's
+per-device body so that the multi-GPU driver (runtime.py)
+can put the activation relay and the gradient allreduce between them, and
+wraps the executor's device buffers as torch tensors (zero copy, through
+``__cuda_array_interface__``) so torch.distributed/NCCL can move them.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Dict, List, Optional, Tuple
+
+import torch
+
+from . import _lib
+
+BUF_INPUT, BUF_TEACHER_OUT, BUF_GRADS, BUF_PARAMS, BUF_MOMENTUM, BUF_LOSSES, BUF_STEP, BUF_TEACHER_PARAMS = range(8)
+BLOCKS = 4
+T_CH = (3, 64, 128, 256, 512)
+T_HW = (32, 32, 16, 8, 4)
+STUDENT_TENSORS = ("w1", "w2", "wsc", "g1", "b1", "g2", "b2", "gsc", "bsc")
+
+
+class PbdxDesc(ctypes.Structure):
+    _fields_ = [("block_lo", ctypes.c_int), ("block_hi", ctypes.c_int), ("n_max", ctypes.c_int),
+                ("global_batch", ctypes.c_int), ("seed_data", ctypes.c_uint32), ("seed_teacher", ctypes.c_uint32),
+                ("seed_student", ctypes.c_uint32), ("lr", ctypes.c_float), ("momentum", ctypes.c_float)]
+
+
+def _bind(L):
+    if getattr(L, "_pbdx_bound", False):
+        return L
+    V, I, P = ctypes.c_void_p, ctypes.c_int, ctypes.POINTER
+    L.pbdx_create.argtypes = [P(PbdxDesc), P(V)]
+    L.pbdx_destroy.argtypes = [V]
+    L.pbdx_destroy.restype = None
+    for name in ("pbdx_init_params", "pbdx_teacher_forward", "pbdx_student_step", "pbdx_apply_update", "pbdx_step",
+                 "pbdx_capture", "pbdx_replay"):
+        getattr(L, name).argtypes = [V, V]
+    L.pbdx_set_shard.argtypes = [V, I, I]
+    L.pbdx_set_input_mode.argtypes = [V, I]
+    L.pbdx_upload_images.argtypes = [V, V, I, V]
+    L.pbdx_buffer.argtypes = [V, I, P(V), P(ctypes.c_size_t)]
+    L.pbdx_num_blocks.argtypes = [V]
+    L.pbdx_teacher_act.argtypes = [V, I, P(V), P(ctypes.c_size_t)]
+    L.pbdx_set_timing.argtypes = [V, I]
+    L.pbdx_block_times.argtypes = [V, P(ctypes.c_float), P(ctypes.c_float)]
+    L.pbdx_student_layout.argtypes = [I, P(ctypes.c_long)]
+    L.pbdx_student_layout.restype = ctypes.c_long
+    L.pbdx_launches_per_step.argtypes = [V]
+    L._pbdx_bound = True
+    return L
+
+
+def lib():
+    return _bind(_lib.lib())
+
+
+class DeviceError(RuntimeError):
+    pass
+
+
+def _check(rc: int, what: str):
+    if rc == 1:
+        raise ValueError(f"{what}: invalid argument / unsupported shape")
+    if rc != 0:
+        raise DeviceError(f"{what}: CUDA error (rc={rc})")
+
+
+class _CudaArray:
+    """Minimal __cuda_array_interface__ exporter for a raw device pointer."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def student_layout(block: int) -> Tuple[Dict[str, Tuple[int, int]], int]:
+    """{tensor: (offset, count)} of a block's flat (padded) student parameters."""
+    offs = (ctypes.c_long * 9)()
+    total = lib().pbdx_student_layout(block, offs)
+    if total < 0:
+        raise ValueError("bad block")
+    bounds = list(offs) + [total]
+    return {name: (bounds[i], bounds[i + 1] - bounds[i]) for i, name in enumerate(STUDENT_TENSORS)}, total
+
+
+def stored_channels(c: int) -> int:
+    return 16 if c == 3 else c
+
+
+class Partition:
+    def __init__(self, block_lo: int, block_hi: int, n_max: int, global_batch: int, seed_data: int = 1234,
+                 seed_teacher: int = 1, seed_student: int = 2, lr: float = 0.1, momentum: float = 0.9,
+                 device: Optional[torch.device] = None):
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.block_lo, self.block_hi, self.n_max, self.global_batch = block_lo, block_hi, n_max, global_batch
+        self.n = n_max
+        self.first = 0
+        d = PbdxDesc(block_lo, block_hi, n_max, global_batch, seed_data, seed_teacher, seed_student, lr, momentum)
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _check(lib().pbdx_create(ctypes.byref(d), ctypes.byref(h)), "pbdx_create")
+        self.handle = h
+        self.blocks = list(range(block_lo, block_hi + 1))
+        self.layouts = {}
+        off = 0
+        for k in self.blocks:
+            lay, total = student_layout(k)
+            self.layouts[k] = (off, lay, total)
+            off += total
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            try:
+                lib().pbdx_destroy(h)
+            except Exception:  # pragma: no cover - interpreter shutdown
+                pass
+            self.handle = None
+
+    # -- plumbing
+    def _stream(self, stream=None) -> ctypes.c_void_p:
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        return ctypes.c_void_p(s.cuda_stream)
+
+    def buffer_ptr(self, which: int) -> Tuple[int, int]:
+        p, n = ctypes.c_void_p(), ctypes.c_size_t()
+        _check(lib().pbdx_buffer(self.handle, which, ctypes.byref(p), ctypes.byref(n)), "pbdx_buffer")
+        return p.value, n.value
+
+    def tensor(self, which: int, shape=None, dtype=torch.float32) -> torch.Tensor:
+        ptr, nbytes = self.buffer_ptr(which)
+        typestr = {torch.float32: "<f4", torch.bfloat16: "<V2", torch.float64: "<f8", torch.int64: "<i8"}[dtype]
+        itemsize = torch.empty((), dtype=dtype).element_size()
+        shape = shape or (nbytes // itemsize,)
+        if dtype == torch.bfloat16:
+            raw = torch.as_tensor(_CudaArray(ptr, tuple(shape), "<i2"), device=self.device)
+            return raw.view(torch.bfloat16)
+        return torch.as_tensor(_CudaArray(ptr, tuple(shape), typestr), device=self.device)
+
+    # -- views the driver moves with NCCL
+    def input_act(self) -> torch.Tensor:
+        k = self.block_lo
+        return self.tensor(BUF_INPUT, (self.n_max, T_HW[k], T_HW[k], stored_channels(T_CH[k])), torch.bfloat16)
+
+    def teacher_out(self) -> torch.Tensor:
+        k = self.block_hi + 1
+        return self.tensor(BUF_TEACHER_OUT, (self.n_max, T_HW[k], T_HW[k], T_CH[k]), torch.bfloat16)
+
+    def teacher_act(self, k: int) -> torch.Tensor:
+        """Teacher output t_k of a block inside the partition (bf16 NHWC, n_max rows)."""
+        p, n = ctypes.c_void_p(), ctypes.c_size_t()
+        _check(lib().pbdx_teacher_act(self.handle, k, ctypes.byref(p), ctypes.byref(n)), "pbdx_teacher_act")
+        shape = (self.n_max, T_HW[k + 1], T_HW[k + 1], T_CH[k + 1])
+        return torch.as_tensor(_CudaArray(p.value, shape, "<i2"), device=self.device).view(torch.bfloat16)
+
+    def grads(self) -> torch.Tensor:
+        return self.tensor(BUF_GRADS)
+
+    def params(self) -> torch.Tensor:
+        return self.tensor(BUF_PARAMS)
+
+    def momentum(self) -> torch.Tensor:
+        return self.tensor(BUF_MOMENTUM)
+
+    def losses_tensor(self) -> torch.Tensor:
+        return self.tensor(BUF_LOSSES, (len(self.blocks),), torch.float64)
+
+    def step_counter(self) -> torch.Tensor:
+        return self.tensor(BUF_STEP, (1,), torch.int64)
+
+    def block_params(self, k: int, which: str = "params") -> Dict[str, torch.Tensor]:
+        base, lay, _ = self.layouts[k]
+        flat = {"params": self.params, "grads": self.grads, "momentum": self.momentum}[which]()
+        return {name: flat[base + o: base + o + n] for name, (o, n) in lay.items()}
+
+    # -- phases of Algorithm 1
+    def init_params(self, stream=None):
+        _check(lib().pbdx_init_params(self.handle, self._stream(stream)), "init_params")
+
+    def set_shard(self, n: int, first: int):
+        _check(lib().pbdx_set_shard(self.handle, n, first), "set_shard")
+        self.n, self.first = n, first
+
+    def set_external_input(self, external: bool):
+        _check(lib().pbdx_set_input_mode(self.handle, int(external)), "set_input_mode")
+
+    def upload_images(self, host: torch.Tensor, stream=None):
+        assert host.dtype == torch.float32 and not host.is_cuda and host.is_contiguous()
+        _check(lib().pbdx_upload_images(self.handle, ctypes.c_void_p(host.data_ptr()), host.shape[0],
+                                        self._stream(stream)), "upload_images")
+
+    def teacher_forward(self, stream=None):
+        _check(lib().pbdx_teacher_forward(self.handle, self._stream(stream)), "teacher_forward")
+
+    def student_step(self, stream=None):
+        _check(lib().pbdx_student_step(self.handle, self._stream(stream)), "student_step")
+
+    def apply_update(self, stream=None):
+        _check(lib().pbdx_apply_update(self.handle, self._stream(stream)), "apply_update")
+
+    def step(self, stream=None):
+        _check(lib().pbdx_step(self.handle, self._stream(stream)), "step")
+
+    def capture(self, stream=None):
+        _check(lib().pbdx_capture(self.handle, self._stream(stream)), "capture")
+
+    def replay(self, stream=None):
+        _check(lib().pbdx_replay(self.handle, self._stream(stream)), "replay")
+
+    def set_timing(self, on: bool):
+        _check(lib().pbdx_set_timing(self.handle, int(on)), "set_timing")
+
+    def block_times(self) -> Tuple[List[float], List[float]]:
+        nb = len(self.blocks)
+        t, s = (ctypes.c_float * nb)(), (ctypes.c_float * nb)()
+        _check(lib().pbdx_block_times(self.handle, t, s), "block_times")
+        return list(t), list(s)
+
+    def launches_per_step(self) -> int:
+        return int(lib().pbdx_launches_per_step(self.handle))
+
+    def losses(self) -> List[float]:
+        return self.losses_tensor().cpu().tolist()

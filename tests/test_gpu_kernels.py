@@ -1,0 +1,98 @@
+"""GPU kernel-level checks through the C-ABI (include/pbdk.h).
+
+Convolutions are floating point: checked against torch fp32 on the same
+bf16-valued operands with tolerance |err| <= 2e-2 * max|ref| (fprop: one bf16
+rounding of the output) and 1e-3 * max|ref| (wgrad, fp32 output).
+"""
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2301_12443_b200 import _lib
+    return _lib
+
+
+def desc(L, n, h, c, k, r, stride):
+    pad = r // 2
+    p = (h + 2 * pad - r) // stride + 1
+    return L.ConvDesc(n, h, h, c, k, r, r, stride, pad, p, p)
+
+
+CASES = [(2, 32, 64, 64, 3, 1), (2, 32, 16, 64, 3, 1), (2, 32, 16, 32, 3, 1), (2, 32, 32, 64, 3, 1),
+         (3, 32, 64, 128, 3, 2), (3, 32, 64, 128, 1, 2), (4, 16, 128, 128, 3, 1), (4, 8, 256, 512, 3, 2),
+         (5, 4, 512, 512, 3, 1), (2, 16, 128, 256, 3, 2), (3, 16, 32, 64, 3, 2), (9, 4, 64, 32, 3, 1)]
+
+
+def stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("epi", [0, 1, 2, 3, 4])
+def test_conv_fprop_epilogues(L, case, epi):
+    n, h, c, k, r, st = case
+    d = desc(L, n, h, c, k, r, st)
+    torch.manual_seed(hash(case) % 1000 + epi)
+    x = (torch.rand(n, h, h, c, device="cuda") * 2 - 1).bfloat16()
+    w = ((torch.rand(k, r, r, c, device="cuda") * 2 - 1) / (r * r * c) ** 0.5).bfloat16()
+    bias = torch.rand(k, device="cuda") - 0.5
+    aux = (torch.rand(n, d.p, d.q, k, device="cuda") * 2 - 1).bfloat16()
+    y = torch.empty(n, d.p, d.q, k, device="cuda", dtype=torch.bfloat16)
+    rc = L.lib().pbdk_conv_fprop(ctypes.byref(d), x.data_ptr(), w.data_ptr(), y.data_ptr(), bias.data_ptr(),
+                                 aux.data_ptr(), epi, stream())
+    assert rc == 0
+    ref = F.conv2d(x.float().permute(0, 3, 1, 2), w.float().permute(0, 3, 1, 2), stride=st,
+                   padding=r // 2).permute(0, 2, 3, 1)
+    if epi in (1, 2, 3):
+        ref = ref + bias
+    if epi == 3:
+        ref = ref + aux.float()
+    if epi in (2, 3):
+        ref = ref.clamp_min(0)
+    if epi == 4:
+        ref = torch.where(aux.float() > 0, ref, torch.zeros_like(ref))
+    torch.cuda.synchronize()
+    err = (y.float() - ref).abs().max().item()
+    assert err <= 2e-2 * ref.abs().max().item() + 1e-3
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_conv_wgrad(L, case):
+    n, h, c, k, r, st = case
+    d = desc(L, n, h, c, k, r, st)
+    torch.manual_seed(hash(case) % 997)
+    x = (torch.rand(n, h, h, c, device="cuda") * 2 - 1).bfloat16()
+    dy = (torch.rand(n, d.p, d.q, k, device="cuda") * 2 - 1).bfloat16()
+    dw = torch.empty(k, r, r, c, device="cuda")
+    wsb = L.lib().pbdk_conv_wgrad_workspace_bytes(ctypes.byref(d))
+    ws = torch.empty(max(wsb, 16), device="cuda", dtype=torch.uint8)
+    rc = L.lib().pbdk_conv_wgrad(ctypes.byref(d), x.data_ptr(), dy.data_ptr(), dw.data_ptr(), ws.data_ptr(), wsb,
+                                 stream())
+    assert rc == 0
+    ref = torch.nn.grad.conv2d_weight(x.float().permute(0, 3, 1, 2), (k, c, r, r), dy.float().permute(0, 3, 1, 2),
+                                      stride=st, padding=r // 2).permute(0, 2, 3, 1)
+    torch.cuda.synchronize()
+    assert (dw - ref).abs().max().item() <= 1e-3 * ref.abs().max().item() + 1e-4
+
+
+def test_weight_flip(L):
+    w = torch.randn(64, 3, 3, 32, device="cuda").bfloat16()
+    wt = torch.empty(32, 3, 3, 64, device="cuda", dtype=torch.bfloat16)
+    assert L.lib().pbdk_weight_flip(w.data_ptr(), wt.data_ptr(), 64, 3, 3, 32, stream()) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(wt, w.flip(1, 2).permute(3, 1, 2, 0).contiguous())
+
+
+def test_unsupported_shapes_fail_loudly(L):
+    d = L.ConvDesc(2, 30, 30, 64, 64, 3, 3, 1, 1, 30, 30)  # 30x30 output does not tile 128 rows
+    x = torch.zeros(2, 30, 30, 64, device="cuda", dtype=torch.bfloat16)
+    assert L.lib().pbdk_conv_fprop(ctypes.byref(d), x.data_ptr(), x.data_ptr(), x.data_ptr(), None, None, 0,
+                                   stream()) == 1

@@ -1,0 +1,192 @@
+"""GPU parity: the sm_100a path through the C-ABI (libpbd.so) vs the CPU oracle.
+
+Tolerances (north_star: "bf16 tolerance where used").  The GPU and the oracle
+round the same tensors to bf16 at the same points; they differ only in fp32
+accumulation order inside the tensor cores, which flips an occasional bf16
+rounding (one ulp = 2^-8 relative).  Such flips compound through stacked
+layers, so parity is asserted per stage on IDENTICAL inputs:
+  * teacher block k (4-5 convs) on the GPU's own t_{k-1}: bf16 values, max diff
+    <= depth * 2^-7 * max|t|, mean <= depth * 2^-11 (tests/gpu_helpers.py);
+  * student block k fwd+bwd on the GPU's own (t_{k-1}, t_k): loss rel 1e-4,
+    every gradient tensor within 5e-3 relative L2 of the oracle's (2.5e-2 for
+    w1, which sits behind the cancellation-prone BN backward);
+  * SGD-momentum on identical gradients: exact up to fma rounding (1e-6 rel).
+End to end (3 steps, all blocks chained) the losses agree to 2e-3 relative and
+the weight updates within 2e-2 (block 0) ... 2.5e-1 (block 3) relative L2 —
+the teacher-chain compounding above, not a student-path error.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import bd
+from tests.gpu_helpers import compare_bf16_tensors, pad_image, partition_params, to_oracle_layout
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ex():
+    from paper_2301_12443_b200 import executor
+    return executor
+
+
+def run_partition(ex, lo, hi, b, steps, input_fn=None, graph=False):
+    p = ex.Partition(lo, hi, b, b)
+    p.init_params()
+    losses = []
+    outs = []
+    for s in range(steps):
+        if input_fn is not None:
+            p.input_act().copy_(input_fn(s))
+        if graph:
+            if s == 0:
+                p.capture()
+            p.replay()
+        else:
+            p.step()
+        torch.cuda.synchronize()
+        losses.append(p.losses())
+        outs.append(p.teacher_out().float().cpu().numpy())
+    return p, losses, outs
+
+
+def test_ir_partition_matches_oracle(ex):
+    """All 4 blocks on one GPU (the IR point), b=4, 3 steps: losses, teacher output, weights."""
+    b, steps = 4, 3
+    p, losses, outs = run_partition(ex, 0, 3, b, steps)
+    tr = bd.Trainer(b, bf16_mode=1)
+    p0 = {k: tr.sp[k].copy() for k in range(4)}
+    for s in range(steps):
+        want = tr.step(s)
+        for k in range(4):
+            assert losses[s][k] == pytest.approx(want[k], rel=2e-3), (s, k)
+    # teacher output of the last step (block 3)
+    x = bd.make_input(b, (steps - 1) * b, 1)
+    act = x
+    for k in range(4):
+        act = bd.teacher_fwd(k, tr.tp[k], act, 1)
+    compare_bf16_tensors(outs[-1], act, depth=17)
+    # updated student weights after `steps` SGD-momentum steps (compounded teacher noise)
+    for k, tol in zip(range(4), (2e-2, 6e-2, 1.5e-1, 2.5e-1)):
+        got = partition_params(p, k)
+        dw_g, dw_o = got - p0[k], tr.sp[k] - p0[k]
+        assert np.linalg.norm(dw_g - dw_o) <= tol * np.linalg.norm(dw_o), k
+
+
+@pytest.mark.parametrize("b", [4, 24])
+def test_per_stage_parity_on_identical_inputs(ex, b):
+    """Each teacher block and each student fwd/bwd vs the oracle on the GPU's own inputs."""
+    p = ex.Partition(0, 3, b, b)
+    p.init_params()
+    p.teacher_forward()
+    p.student_step()
+    torch.cuda.synchronize()
+    x = bd.make_input(b, 0, 1)
+    prev = x
+    depth = {0: 5, 1: 5, 2: 5, 3: 5}
+    for k in range(4):
+        gpu_t = p.teacher_act(k)[:b].float().cpu().numpy()
+        want_t = bd.teacher_fwd(k, bd.teacher_params(k, 1), prev, 1)
+        compare_bf16_tensors(gpu_t, want_t, depth=depth[k])
+        loss, g = bd.student_fwd_bwd(k, bd.student_params(k), prev, gpu_t, b, 1)
+        assert p.losses()[k] == pytest.approx(loss, rel=1e-4), k
+        base, _, total = p.layouts[k]
+        gg = to_oracle_layout(k, p.grads()[base:base + total].cpu().numpy())
+        for name, (o, n) in bd.student_layout(k).items():
+            a, w = gg[o:o + n], g[o:o + n]
+            # w1 sits behind the BN1 backward, whose m*g - sum(g) - xhat*sum(g*xhat) cancels most
+            # of g when m is small (block 3 at b=4: m = 64), amplifying the one-ulp bf16 flips of
+            # the dgrad output g1 -> looser bound for that tensor only.
+            tol = 2.5e-2 if name == "w1" else 5e-3
+            assert np.linalg.norm(a - w) <= tol * np.linalg.norm(w) + 1e-12, (k, name)
+        prev = gpu_t
+
+
+def test_sgd_update_exact(ex):
+    b = 4
+    p = ex.Partition(0, 3, b, b)
+    p.init_params()
+    p.teacher_forward()
+    p.student_step()
+    torch.cuda.synchronize()
+    w0 = p.params().cpu().numpy().copy()
+    v0 = p.momentum().cpu().numpy().copy()
+    g = p.grads().cpu().numpy().copy()
+    p.apply_update()
+    torch.cuda.synchronize()
+    w, v = w0.copy(), v0.copy()
+    bd.sgd(w, v, g)
+    np.testing.assert_allclose(p.momentum().cpu().numpy(), v, rtol=1e-6, atol=1e-12)
+    np.testing.assert_allclose(p.params().cpu().numpy(), w, rtol=1e-6, atol=1e-9)
+
+
+def test_initial_params_bit_exact(ex):
+    p = ex.Partition(0, 3, 2, 2)
+    p.init_params()
+    torch.cuda.synchronize()
+    for k in range(4):
+        np.testing.assert_array_equal(partition_params(p, k), bd.student_params(k))
+
+
+def test_relay_partition_with_external_input(ex):
+    """Partition (2,3) fed the oracle's t_1 through its input buffer (as the relay would)."""
+    b = 8
+    tr = bd.Trainer(b, bf16_mode=1)
+    x = bd.make_input(b, 0, 1)
+    t0 = bd.teacher_fwd(0, tr.tp[0], x, 1)
+    t1 = bd.teacher_fwd(1, tr.tp[1], t0, 1)
+    p, losses, outs = run_partition(ex, 2, 3, b, 1,
+                                    input_fn=lambda s: torch.from_numpy(t1).to(torch.bfloat16).cuda())
+    t2 = bd.teacher_fwd(2, tr.tp[2], t1, 1)
+    t3 = bd.teacher_fwd(3, tr.tp[3], t2, 1)
+    compare_bf16_tensors(outs[0], t3, depth=8)
+    for i, k in enumerate((2, 3)):
+        tin = t1 if k == 2 else t2
+        tout = t2 if k == 2 else t3
+        want, _ = bd.student_fwd_bwd(k, tr.sp[k], tin, tout, b, 1)
+        assert losses[0][i] == pytest.approx(want, rel=2e-3)
+
+
+def test_synthetic_input_bit_exact(ex):
+    p = ex.Partition(0, 0, 6, 12)
+    p.init_params()
+    p.set_shard(6, 6)   # second half of a 12-sample global batch
+    p.teacher_forward()
+    torch.cuda.synchronize()
+    got = p.input_act().float().cpu().numpy()[:6]
+    want = pad_image(bd.make_input(6, 6, 1))
+    np.testing.assert_array_equal(got, want)
+
+
+def test_graph_replay_bitwise_equals_eager(ex):
+    b = 8
+    _, l_eager, o_eager = run_partition(ex, 0, 3, b, 3)
+    _, l_graph, o_graph = run_partition(ex, 0, 3, b, 3, graph=True)
+    assert l_eager == l_graph
+    for a, g in zip(o_eager, o_graph):
+        np.testing.assert_array_equal(a, g)
+
+
+def test_deterministic_across_runs(ex):
+    p1, l1, _ = run_partition(ex, 0, 3, 16, 2)
+    p2, l2, _ = run_partition(ex, 0, 3, 16, 2)
+    assert l1 == l2
+    assert torch.equal(p1.params(), p2.params())
+
+
+def test_full_size_teacher_sample_independence(ex):
+    """b=256 (BASELINE configs[1] batch): the first 4 samples' teacher output equals the b=4 run."""
+    big = ex.Partition(0, 3, 256, 256)
+    big.init_params()
+    big.teacher_forward()
+    small = ex.Partition(0, 3, 4, 256)
+    small.init_params()
+    small.set_shard(4, 0)
+    small.teacher_forward()
+    torch.cuda.synchronize()
+    assert torch.equal(big.teacher_out()[:4], small.teacher_out()[:4])
+    big.student_step()
+    torch.cuda.synchronize()
+    losses = big.losses()
+    assert all(np.isfinite(losses)) and all(0 < l < 10 for l in losses)
