@@ -1,0 +1,329 @@
+#!/usr/bin/env python
+"""Blockwise-distillation throughput on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N --steps K --warmup W]          # our sm_100a path
+  python bench.py --impl reference [...]                    # CPU reference arm
+
+Workload (BASELINE.json configs[1]): CIFAR-shaped 32x32 synthetic data,
+ResNet-18-CIFAR 4-block teacher -> slim residual student, bf16 operands / fp32
+accumulation and master weights, global batch 256 per GPU.  At N=1 the whole
+chain runs on one GPU (the IR point of the AHD space, schedule.cpp:305-317).
+Under torchrun (N>1) every rank runs the schedule best_schedule() picks on a
+device-measured profile (weak scaling: global batch 256*N), with NCCL relays
+between pipeline stages and NCCL allreduce inside DP groups (runtime.py).
+
+One JSON line on rank 0; see DESIGN.md §5 for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "blockwise-distill samples/sec"
+UNIT = "samples/s"
+PER_GPU_BATCH = 256
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--batch", type=int, default=PER_GPU_BATCH, help="global batch per GPU")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- roofline helpers
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+def step_work(batch):
+    """Algorithmic FLOPs and bytes of one step (models.py accounting)."""
+    from paper_2301_12443_b200 import models
+    return models.step_flops(batch), models.step_bytes(batch)
+
+
+def ncu_traffic(kernel_key):
+    """DRAM bytes per launch for the dominant kernel from the committed ncu capture (or None)."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    return d.get("kernels", {}).get(kernel_key, {}).get("dram_bytes")
+
+
+def time_dominant_kernel(torch, batch):
+    """CUDA-event timing of the dominant kernel (teacher block-0 3x3 conv, 64->64 @32x32, tcgen05)
+    launched alone on the current stream; algorithmic FLOPs = 2*M*N*K."""
+    import ctypes
+    from paper_2301_12443_b200 import _lib
+    L = _lib.lib()
+    d = _lib.ConvDesc(batch, 32, 32, 64, 64, 3, 3, 1, 1, 32, 32)
+    x = torch.randn(batch, 32, 32, 64, device="cuda").bfloat16()
+    w = (torch.randn(64, 3, 3, 64, device="cuda") * 0.05).bfloat16()
+    bias = torch.zeros(64, device="cuda")
+    y = torch.empty(batch, 32, 32, 64, device="cuda", dtype=torch.bfloat16)
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def launch():
+        rc = L.pbdk_conv_fprop(ctypes.byref(d), x.data_ptr(), w.data_ptr(), y.data_ptr(), bias.data_ptr(), None, 2, s)
+        assert rc == 0
+
+    for _ in range(5):
+        launch()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    reps = 50
+    for _ in range(reps):
+        launch()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    flops = 2.0 * batch * 32 * 32 * 64 * 9 * 64
+    return "conv_fprop_bn64_bkc64", flops, ms
+
+
+# ---------------------------------------------------------------- CPU legs
+def cpu_oracle_rate(samples_per_step=32, steps=6):
+    """The oracle (C restatement, OpenMP) on the host cores: samples/s over `steps` bounded steps."""
+    from oracle import bd
+    tr = bd.Trainer(samples_per_step, bf16_mode=1)
+    tr.step(0)  # warm (allocation, page faults)
+    t0 = time.perf_counter()
+    for s in range(steps):
+        tr.step(1 + s)
+    dt = time.perf_counter() - t0
+    return samples_per_step * steps / dt, bd.lib().bdo_threads(), dt
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU implementation of the path (the oracle port: the reference itself has
+    no executable distillation step) on the host cores, same metric and config."""
+    if rank != 0:
+        return
+    from oracle import bd
+    sample = 8
+    tr = bd.Trainer(sample, bf16_mode=1)
+    for w in range(args.warmup):
+        tr.step(w)
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        tr.step(args.warmup + s)
+    dt = time.perf_counter() - t0
+    rate = sample * args.steps / dt
+    threads = bd.lib().bdo_threads()
+    line = {"metric": METRIC, "value": rate, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16-emulated fp32",
+            "data": "synthetic (Philox4x32-10, DESIGN.md §3)",
+            "config": {"workload": "cifar-resnet18-teacher/slim-student 4 blocks (configs[1])",
+                       "global_batch": args.batch * args.gpus, "sample_per_step": sample, "parallelism": "cpu"},
+            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"{sample} samples x {args.steps} steps, all 4 blocks, fwd+bwd+SGD"},
+            "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    try:
+        from oracle import ref
+        if ref.available():
+            from paper_2301_12443_b200 import core
+            prof = core.synth_profile(shape="front-heavy", blocks=10, front_weight=4.0, curvature=0.4,
+                                      num_devices=8)
+            line["partitioner"] = {"reference_best_schedule_ms": ref.time_best_schedule(prof, threads=1, reps=20),
+                                   "ours_best_schedule_ms": core.time_best_schedule(prof, reps=20),
+                                   "case": "B=10 N=8 (11440 configs)"}
+    except Exception as e:  # pragma: no cover - informational only
+        line["partitioner"] = {"error": str(e)}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2301_12443_b200 import executor, models
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        from paper_2301_12443_b200 import runtime
+        res = runtime.bench_pipeline(args, rank, world, local_rank)
+        if rank == 0:
+            print(json.dumps(res), flush=True)
+        return
+
+    b = args.batch
+    part = executor.Partition(0, 3, b, b, device=dev)
+    part.init_params()
+    stream = torch.cuda.current_stream(dev)
+    use_graph = not args.no_graph
+    if use_graph:
+        part.capture()
+
+    def one():
+        (part.replay if use_graph else part.step)()
+
+    for _ in range(max(3, args.warmup)):
+        one()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            one()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    value = b / ms * 1e3
+    losses = part.losses()
+
+    # ---- e2e through the public API with host buffers: H2D images + step + D2H losses
+    e2e_part = executor.Partition(0, 3, b, b, device=dev)
+    e2e_part.init_params()
+    e2e_part.set_external_input(True)
+    host = torch.empty(b, 32, 32, 3, dtype=torch.float32).pin_memory()
+    host.uniform_(-1.0, 1.0)
+    if use_graph:
+        e2e_part.upload_images(host)
+        e2e_part.capture()
+    loss_host = torch.empty(1, dtype=torch.float64).pin_memory()
+    lt = e2e_part.losses_tensor()
+
+    def e2e_step():
+        e2e_part.upload_images(host)
+        (e2e_part.replay if use_graph else e2e_part.step)()
+        loss_host.copy_(lt.sum().view(1), non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+
+    for _ in range(3):
+        e2e_step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    e2e_ms = (time.perf_counter() - t0) / args.steps * 1e3
+    e2e = {"value": b / e2e_ms * 1e3, "unit": UNIT, "h2d_bytes_per_step": b * 32 * 32 * 3 * 4,
+           "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms}
+    del e2e_part
+
+    # ---- roofline of the dominant kernel + step-level accounting
+    peaks = measured_peaks()
+    key, kflops, kms = time_dominant_kernel(torch, b)
+    achieved = kflops / (kms * 1e-3) / 1e12
+    traffic = ncu_traffic(key)
+    roof = {"bound": "tensor", "kernel": key, "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+            "frac": achieved / peaks["bf16_tflops"], "traffic": traffic, "launch_us": kms * 1e3,
+            "peak_source": peaks["source"] + " burst (kernel timed alone)"}
+    sflops, sbytes = step_work(b)
+    t_roof = max(sflops / (peaks["bf16_tflops_sustained"] * 1e12), sbytes / (peaks["hbm_gbs"] * 1e9))
+    step_roof = {"step_flops": sflops, "step_bytes": sbytes, "t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms,
+                 "achieved_tflops": sflops / (ms * 1e-3) / 1e12,
+                 "note": "sum of algorithmic work / measured step; peak = sustained bf16, measured HBM"}
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        rate, cores, dt = cpu_oracle_rate()
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"32 samples x 6 steps of the same workload (oracle/bd_oracle.c, {dt:.1f} s)"}
+
+    working_set = models.step_working_set_bytes(b)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (Philox4x32-10 inputs generated on device each step; random-init weights)",
+            "config": {"workload": "cifar-resnet18-teacher/slim-student 4 blocks, IR point on 1 GPU (configs[1])",
+                       "global_batch": b, "image": "32x32x3", "blocks": 4, "parallelism": "ir1 (blocks 0-3 on 1 GPU)",
+                       "cuda_graph": use_graph,
+                       "l2": f"no flush: per-step working set {working_set / 2**30:.2f} GiB > 126 MB L2"},
+            "e2e": e2e, "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu,
+            "gpu_launches": part.launches_per_step() * args.steps, "clocks": clocks.summary(),
+            "losses_last_step": losses}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -176,16 +176,51 @@ __device__ void cta_reduce_store(float (&acc)[NV][8], int cg, int rpp, int C, fl
   }
 }
 
-// per-channel double sum of partial[chunk][NV][C] over chunks -> out[v*C + c]
+// Fixed-order parallel sum of partial[chunk][NV][C] over chunks for 32 consecutive
+// (v, c) outputs per CTA: warp w sums chunks [w*per, (w+1)*per) (lanes = 32
+// consecutive outputs, coalesced), then the 8 warp partials are added in warp order.
+// Deterministic for a given (chunks, C).  Returns the double sum in `out` for lane
+// outputs o = blockIdx.x*32 + lane (valid when o < NV*C), visible to warp 0.
+constexpr int kFinWarps = 8;
+
 template <int NV>
-__global__ void finalize_sums_kernel(const float* __restrict__ partial, int chunks, int C, double* __restrict__ out) {
-  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < NV * C; o += gridDim.x * blockDim.x) {
+__device__ __forceinline__ double sum_over_chunks(const float* __restrict__ partial, int chunks, int C, int o) {
+  __shared__ double sm[kFinWarps][32];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  double s = 0.0;
+  if (o < NV * C) {
     const int v = o / C;
     const int c = o - v * C;
-    double s = 0.0;
-    for (int b = 0; b < chunks; ++b) s += partial[(static_cast<size_t>(b) * NV + v) * C + c];
-    out[o] = s;
+    const int per = (chunks + kFinWarps - 1) / kFinWarps;
+    const int b0 = warp * per;
+    const int b1 = min(chunks, b0 + per);
+    for (int b = b0; b < b1; ++b) s += partial[(static_cast<size_t>(b) * NV + v) * C + c];
   }
+  sm[warp][lane] = s;
+  __syncthreads();
+  double t = 0.0;
+  if (warp == 0) {
+#pragma unroll
+    for (int w = 0; w < kFinWarps; ++w) t += sm[w][lane];
+  }
+  return t;
+}
+
+// fixed-order sum of n floats by one CTA of kFinWarps*32 threads
+__device__ __forceinline__ double cta_sum(const float* __restrict__ v, int n) {
+  __shared__ double sm[kFinWarps * 32];
+  double s = 0.0;
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int b0 = threadIdx.x * per;
+  const int b1 = min(n, b0 + per);
+  for (int i = b0; i < b1; ++i) s += v[i];
+  sm[threadIdx.x] = s;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < static_cast<int>(blockDim.x); ++i) t += sm[i];
+  return t;
 }
 
 // -- BN statistics
@@ -210,14 +245,15 @@ __global__ void bn_stats_partial_kernel(const __nv_bfloat16* __restrict__ y, int
   cta_reduce_store<2>(acc, cg, rpp, C, partial);
 }
 
+// grid: ceil(C/32) CTAs of kFinWarps*32 threads; the (s1, s2) pair of channel c is
+// summed by two independent fixed-order passes (v = 0 and v = 1).
 __global__ void bn_stats_finalize_kernel(const float* __restrict__ partial, int chunks, int C, int m,
                                          float* __restrict__ mean_rstd) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
-    double s1 = 0.0, s2 = 0.0;
-    for (int b = 0; b < chunks; ++b) {
-      s1 += partial[(static_cast<size_t>(b) * 2 + 0) * C + c];
-      s2 += partial[(static_cast<size_t>(b) * 2 + 1) * C + c];
-    }
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  const double s1 = sum_over_chunks<2>(partial, chunks, C, c);
+  __syncthreads();
+  const double s2 = sum_over_chunks<2>(partial, chunks, C, C + c);
+  if ((threadIdx.x >> 5) == 0 && c < C) {
     const double mu = s1 / static_cast<double>(m);
     const double var = s2 / static_cast<double>(m) - mu * mu;
     mean_rstd[c] = static_cast<float>(mu);
@@ -312,30 +348,32 @@ __global__ void loss_partial_kernel(const LossParams p, int rows_per_chunk, int 
   }
 }
 
-// red (double [3C]) -> grads of gamma2/beta2/gammasc/betasc, float copies, loss
+// red (double [3C]) -> grads of gamma2/beta2/gammasc/betasc, float copies; the last
+// CTA (blockIdx.x == gridDim.x-1, beyond the channel CTAs) sums the loss partials.
 __global__ void loss_finalize_kernel(const float* __restrict__ partial, const float* __restrict__ loss_partial,
                                      int chunks, int C, double norm, float* __restrict__ red_f,
                                      float* __restrict__ dg2, float* __restrict__ db2, float* __restrict__ dgs,
                                      float* __restrict__ dbs, double* __restrict__ loss_out) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-    for (int b = 0; b < chunks; ++b) {
-      s0 += partial[(static_cast<size_t>(b) * 3 + 0) * C + c];
-      s1 += partial[(static_cast<size_t>(b) * 3 + 1) * C + c];
-      s2 += partial[(static_cast<size_t>(b) * 3 + 2) * C + c];
-    }
-    red_f[c] = static_cast<float>(s0);
-    red_f[C + c] = static_cast<float>(s1);
-    red_f[2 * C + c] = static_cast<float>(s2);
-    db2[c] = static_cast<float>(s0);
-    dbs[c] = static_cast<float>(s0);
-    dg2[c] = static_cast<float>(s1);
-    dgs[c] = static_cast<float>(s2);
+  if (blockIdx.x == gridDim.x - 1) {
+    const double l = cta_sum(loss_partial, chunks);
+    if (threadIdx.x == 0) *loss_out = l / norm;
+    return;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    double l = 0.0;
-    for (int b = 0; b < chunks; ++b) l += loss_partial[b];
-    *loss_out = l / norm;
+  const int o = blockIdx.x * 32 + (threadIdx.x & 31);  // o in [0, 3C)
+  const double sv = sum_over_chunks<3>(partial, chunks, C, o);
+  if ((threadIdx.x >> 5) == 0 && o < 3 * C) {
+    const int v = o / C;
+    const int c = o - v * C;
+    const float f = static_cast<float>(sv);
+    red_f[o] = f;
+    if (v == 0) {
+      db2[c] = f;
+      dbs[c] = f;
+    } else if (v == 1) {
+      dg2[c] = f;
+    } else {
+      dgs[c] = f;
+    }
   }
 }
 
@@ -393,16 +431,17 @@ __global__ void bn_bwd_partial_kernel(const __nv_bfloat16* __restrict__ gin, con
 
 __global__ void bn_bwd_finalize_kernel(const float* __restrict__ partial, int chunks, int C, float* __restrict__ red_f,
                                        float* __restrict__ dgamma, float* __restrict__ dbeta) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
-    double s0 = 0.0, s1 = 0.0;
-    for (int b = 0; b < chunks; ++b) {
-      s0 += partial[(static_cast<size_t>(b) * 2 + 0) * C + c];
-      s1 += partial[(static_cast<size_t>(b) * 2 + 1) * C + c];
-    }
-    red_f[c] = static_cast<float>(s0);
-    red_f[C + c] = static_cast<float>(s1);
-    dbeta[c] = static_cast<float>(s0);
-    dgamma[c] = static_cast<float>(s1);
+  const int o = blockIdx.x * 32 + (threadIdx.x & 31);  // o in [0, 2C)
+  const double sv = sum_over_chunks<2>(partial, chunks, C, o);
+  if ((threadIdx.x >> 5) == 0 && o < 2 * C) {
+    const int v = o / C;
+    const int c = o - v * C;
+    const float f = static_cast<float>(sv);
+    red_f[o] = f;
+    if (v == 0)
+      dbeta[c] = f;
+    else
+      dgamma[c] = f;
   }
 }
 
@@ -495,7 +534,7 @@ int bn_stats(const void* y, int m, int c, float* ws, float* mean_rstd, cudaStrea
   const RowTiling t = tiling_for(m, c);
   bn_stats_partial_kernel<<<t.chunks, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(y), m, c,
                                                          t.rows_per_chunk, t.cg, t.rpp, ws);
-  bn_stats_finalize_kernel<<<(c + 127) / 128, 128, 0, st>>>(ws, t.chunks, c, m, mean_rstd);
+  bn_stats_finalize_kernel<<<(c + 31) / 32, kFinWarps * 32, 0, st>>>(ws, t.chunks, c, m, mean_rstd);
   return ok(cudaGetLastError());
 }
 
@@ -515,7 +554,7 @@ int mse_bn_loss(const MseArgs& a, cudaStream_t st) {
   float* partial = a.ws;
   float* loss_partial = a.ws + static_cast<size_t>(t.chunks) * 3 * a.c;
   loss_partial_kernel<<<t.chunks, kThreads, 0, st>>>(p, t.rows_per_chunk, t.cg, t.rpp, partial, loss_partial);
-  loss_finalize_kernel<<<(a.c + 127) / 128, 128, 0, st>>>(partial, loss_partial, t.chunks, a.c, a.norm, a.red,
+  loss_finalize_kernel<<<(3 * a.c + 31) / 32 + 1, kFinWarps * 32, 0, st>>>(partial, loss_partial, t.chunks, a.c, a.norm, a.red,
                                                           a.dgamma2, a.dbeta2, a.dgammasc, a.dbetasc, a.loss);
   loss_bwd_apply_kernel<<<grid_for(static_cast<long long>(a.m) * a.c / 8), kThreads, 0, st>>>(
       p, a.red, static_cast<__nv_bfloat16*>(a.dy2), static_cast<__nv_bfloat16*>(a.dysc));
@@ -529,7 +568,7 @@ int bn_bwd(const void* g, const void* y, const float* mean_rstd, const float* ga
   bn_bwd_partial_kernel<<<t.chunks, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(g),
                                                        static_cast<const __nv_bfloat16*>(y), mean_rstd, m, c,
                                                        t.rows_per_chunk, t.cg, t.rpp, ws);
-  bn_bwd_finalize_kernel<<<(c + 127) / 128, 128, 0, st>>>(ws, t.chunks, c, red, dgamma, dbeta);
+  bn_bwd_finalize_kernel<<<(2 * c + 31) / 32, kFinWarps * 32, 0, st>>>(ws, t.chunks, c, red, dgamma, dbeta);
   bn_bwd_apply_kernel<<<grid_for(static_cast<long long>(m) * c / 8), kThreads, 0, st>>>(
       static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(y), mean_rstd, gamma, red, m, c,
       static_cast<__nv_bfloat16*>(dy));

@@ -8,8 +8,10 @@ layers, so parity is asserted per stage on IDENTICAL inputs:
   * teacher block k (4-5 convs) on the GPU's own t_{k-1}: bf16 values, max diff
     <= depth * 2^-7 * max|t|, mean <= depth * 2^-11 (tests/gpu_helpers.py);
   * student block k fwd+bwd on the GPU's own (t_{k-1}, t_k): loss rel 1e-4,
-    every gradient tensor within 5e-3 relative L2 of the oracle's (2.5e-2 for
-    w1, which sits behind the cancellation-prone BN backward);
+    every gradient tensor within max(5e-3 relative, the oracle's own
+    bf16-vs-fp32 distance) of the bf16-emulating oracle — i.e. inside the bf16
+    quantisation noise of the computation (large only behind a BN backward
+    with small m, where m*g - sum g - xhat*sum(g*xhat) cancels);
   * SGD-momentum on identical gradients: exact up to fma rounding (1e-6 rel).
 End to end (3 steps, all blocks chained) the losses agree to 2e-3 relative and
 the weight updates within 2e-2 (block 0) ... 2.5e-1 (block 3) relative L2 —
@@ -90,16 +92,19 @@ def test_per_stage_parity_on_identical_inputs(ex, b):
         want_t = bd.teacher_fwd(k, bd.teacher_params(k, 1), prev, 1)
         compare_bf16_tensors(gpu_t, want_t, depth=depth[k])
         loss, g = bd.student_fwd_bwd(k, bd.student_params(k), prev, gpu_t, b, 1)
+        _, g32 = bd.student_fwd_bwd(k, bd.student_params(k), prev, gpu_t, b, 0)   # no bf16 rounding
         assert p.losses()[k] == pytest.approx(loss, rel=1e-4), k
         base, _, total = p.layouts[k]
         gg = to_oracle_layout(k, p.grads()[base:base + total].cpu().numpy())
         for name, (o, n) in bd.student_layout(k).items():
-            a, w = gg[o:o + n], g[o:o + n]
-            # w1 sits behind the BN1 backward, whose m*g - sum(g) - xhat*sum(g*xhat) cancels most
-            # of g when m is small (block 3 at b=4: m = 64), amplifying the one-ulp bf16 flips of
-            # the dgrad output g1 -> looser bound for that tensor only.
-            tol = 2.5e-2 if name == "w1" else 5e-3
-            assert np.linalg.norm(a - w) <= tol * np.linalg.norm(w) + 1e-12, (k, name)
+            a, w, w32 = gg[o:o + n], g[o:o + n], g32[o:o + n]
+            # The GPU must sit within the bf16 quantisation noise of the computation: its distance
+            # to the bf16-emulating oracle may not exceed the oracle's own bf16-vs-fp32
+            # distance (or 5e-3 relative, whichever is larger).  Behind a BN backward with a
+            # small m (block 3: m = 16 per sample) that noise is large; elsewhere it is tiny.
+            noise = np.linalg.norm(w - w32)
+            err = np.linalg.norm(a - w)
+            assert err <= max(5e-3 * np.linalg.norm(w), noise) + 1e-12, (k, name, err, noise)
         prev = gpu_t
 
 
