@@ -1,0 +1,282 @@
+"""Multi-GPU Pipe-BD driver: one process per GPU over torch.distributed.
+
+Each rank owns one device slot of a schedule document (best_schedule output,
+schedule.cpp:361-373): partition j = contiguous blocks [lo, hi] replicated over
+the device group G_j, every member running its shard of the global batch
+(remainder rule SPEC.md:231).  Per step, rank r in partition j runs the
+per-device body of Algorithm 1:
+
+    j == 0 : load_data()                       (synthetic on device, or host upload)
+    j  > 0 : receive(t_{lo-1} shard)           relay from the ranks of G_{j-1}     [TR]
+    T.forward                                   pbdx_teacher_forward
+    j < P-1: send(t_hi shards)                  relay to the ranks of G_{j+1}       [TR]
+    S.forward / S.backward(L(s,t))              pbdx_student_step
+    |G_j| > 1: share_gradient()                 all_reduce(SUM) inside G_j          [AHD]
+    (dpu=False: wait_all_devices())             barrier                             [DPU]
+    S.update_weight()                           pbdx_apply_update
+
+The relay reshards when |G_{j-1}| != |G_j|: every (sender, receiver) pair whose
+sample ranges overlap exchanges exactly the overlapping rows (NHWC rows are
+sample-major, so a shard slice is contiguous).  All P2P ops of one boundary
+are issued as one batch_isend_irecv group (NCCL group semantics, no deadlock).
+
+The stage object is pluggable: ``executor.Partition`` on B200s (the product
+path), and an oracle-backed stage in tests/ to exercise this host logic with
+the gloo backend on CPU (world size 2+).
+"""
+from __future__ import annotations
+
+import json
+import time
+from dataclasses import dataclass
+from typing import Callable, Dict, List, Optional, Tuple
+
+import torch
+import torch.distributed as dist
+
+from . import core
+
+
+def shard(global_batch: int, group: int, index: int) -> Tuple[int, int]:
+    """(first, count) of member `index` of a group of `group` devices."""
+    base, extra = divmod(global_batch, group)
+    count = base + (1 if index < extra else 0)
+    return index * base + min(index, extra), count
+
+
+@dataclass
+class Placement:
+    partition: int
+    block_lo: int
+    block_hi: int
+    group: List[int]
+    index: int
+    first: int
+    count: int
+    per_device_batch: int
+
+
+def placements(schedule: dict, global_batch: int) -> Dict[int, Placement]:
+    out = {}
+    for j, p in enumerate(schedule["partitions"]):
+        lo, hi = p["blocks"]
+        devs = list(p["devices"])
+        for i, d in enumerate(devs):
+            f, c = shard(global_batch, len(devs), i)
+            out[d] = Placement(j, lo, hi, devs, i, f, c, p["per_device_batch"])
+    return out
+
+
+def relay_plan(schedule: dict, global_batch: int, boundary: int) -> List[Tuple[int, int, int, int, int]]:
+    """Messages across boundary (partition boundary-1 -> boundary):
+    (sender rank, receiver rank, sender row offset, receiver row offset, rows)."""
+    up = schedule["partitions"][boundary - 1]["devices"]
+    down = schedule["partitions"][boundary]["devices"]
+    msgs = []
+    for a, ra in enumerate(up):
+        fa, ca = shard(global_batch, len(up), a)
+        for c, rc in enumerate(down):
+            fc, cc = shard(global_batch, len(down), c)
+            lo, hi = max(fa, fc), min(fa + ca, fc + cc)
+            if hi > lo:
+                msgs.append((ra, rc, lo - fa, lo - fc, hi - lo))
+    return msgs
+
+
+class PipeBD:
+    """This rank's share of a Pipe-BD schedule.
+
+    make_stage(block_lo, block_hi, n, first) -> stage with the executor.Partition interface:
+      input_act(), teacher_out(), grads(), teacher_forward(), student_step(), apply_update(), losses().
+    """
+
+    def __init__(self, schedule: dict, global_batch: int, make_stage: Callable, dpu: bool = True,
+                 groups: Optional[Dict[int, object]] = None):
+        self.schedule = schedule
+        self.b = global_batch
+        self.dpu = dpu
+        self.rank = dist.get_rank()
+        self.world = dist.get_world_size()
+        self.place = placements(schedule, global_batch)
+        if self.rank not in self.place:
+            raise ValueError(f"rank {self.rank} has no device slot in the schedule")
+        me = self.place[self.rank]
+        self.me = me
+        self.nparts = len(schedule["partitions"])
+        # one communicator per multi-device group (every rank must take part in new_group)
+        self.groups = groups if groups is not None else {}
+        if groups is None:
+            for j, p in enumerate(schedule["partitions"]):
+                devs = list(p["devices"])
+                g = dist.new_group(devs) if len(devs) > 1 else None
+                self.groups[j] = g
+        self.stage = make_stage(me.block_lo, me.block_hi, me.count, me.first)
+        self.recv_msgs = [m for m in relay_plan(schedule, global_batch, me.partition) if m[1] == self.rank] \
+            if me.partition > 0 else []
+        self.send_msgs = [m for m in relay_plan(schedule, global_batch, me.partition + 1) if m[0] == self.rank] \
+            if me.partition + 1 < self.nparts else []
+        self._pending_sends: List = []
+
+    # -- relay
+    def _recv_input(self):
+        if not self.recv_msgs:
+            return
+        buf = self.stage.input_act()
+        ops = [dist.P2POp(dist.irecv, buf[dst_off:dst_off + rows], src) for src, _, _, dst_off, rows in self.recv_msgs]
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
+    def _send_output(self):
+        if not self.send_msgs:
+            return
+        out = self.stage.teacher_out()
+        ops = [dist.P2POp(dist.isend, out[src_off:src_off + rows], dst) for _, dst, src_off, _, rows in self.send_msgs]
+        self._pending_sends = dist.batch_isend_irecv(ops)
+
+    def _finish_sends(self):
+        for w in self._pending_sends:
+            w.wait()
+        self._pending_sends = []
+
+    # -- Algorithm 1, one step
+    def step(self):
+        self._recv_input()
+        self._finish_sends()  # the previous step's send must drain before t_hi is overwritten
+        self.stage.teacher_forward()
+        self._send_output()
+        self.stage.student_step()
+        g = self.groups.get(self.me.partition)
+        if g is not None:
+            dist.all_reduce(self.stage.grads(), op=dist.ReduceOp.SUM, group=g)
+        if not self.dpu:
+            dist.barrier()
+        self.stage.apply_update()
+
+    def end_epoch(self):
+        """Full synchronisation at the epoch boundary (simulate.cpp:263)."""
+        self._finish_sends()
+        dist.barrier()
+
+    def block_losses(self) -> Dict[int, float]:
+        """Per-block loss of the last step summed over each DP group (the global-batch MSE)."""
+        local = self.stage.losses()
+        g = self.groups.get(self.me.partition)
+        t = torch.tensor(local, dtype=torch.float64, device=_dev_of(self.stage))
+        if g is not None:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=g)
+        return {k: float(v) for k, v in zip(range(self.me.block_lo, self.me.block_hi + 1), t.tolist())}
+
+
+def _dev_of(stage):
+    return getattr(stage, "device", torch.device("cpu"))
+
+
+# ---------------------------------------------------------------- device profiler + AHD on B200
+
+def profile_blocks(global_batch: int, world: int, keys: Optional[List[int]] = None, reps: int = 5,
+                   device: Optional[torch.device] = None) -> dict:
+    """Measure T_k(b), S_k(b) of every block on this GPU with CUDA events ("runs steps
+    of each block with feasible batch sizes") and emit a profile document (profile.hpp:30-86)."""
+    from . import executor, models
+    keys = keys or sorted({max(1, global_batch // d) for d in (16, 8, 4, 2, 1)})
+    blocks = []
+    for k in range(models.BLOCKS):
+        tms, sms = {}, {}
+        for n in keys:
+            p = executor.Partition(k, k, n, max(n, global_batch), device=device)
+            p.init_params()
+            p.set_timing(True)
+            t_samples, s_samples = [], []
+            for r in range(reps + 2):
+                p.step()
+                tt, ss = p.block_times()
+                if r >= 2:
+                    t_samples.append(tt[0])
+                    s_samples.append(ss[0])
+            tms[n] = sorted(t_samples)[len(t_samples) // 2]
+            sms[n] = sorted(s_samples)[len(s_samples) // 2]
+            del p
+        # the profile format requires non-decreasing times in batch (profile.cpp:37-55)
+        run_t = run_s = 0.0
+        for n in keys:
+            run_t = max(run_t, tms[n])
+            run_s = max(run_s, sms[n])
+            tms[n], sms[n] = run_t, run_s
+        g = models.student_geom(k)
+        act = models.T_HW[k + 1] ** 2 * models.T_CH[k + 1] * 2
+        tparams = sum(c[1] * c[2] * c[2] * (16 if c[0] == 3 else c[0]) * 2 for c, _ in models.teacher_convs(k))
+        blocks.append({"id": k, "teacher_ms": {str(n): tms[n] for n in keys},
+                       "student_ms": {str(n): sms[n] for n in keys}, "act_bytes_per_sample": float(act),
+                       "param_bytes": float(models.student_param_count(k) * 4), "teacher_param_bytes": float(tparams)})
+    return {"blocks": blocks, "global_batch": global_batch,
+            "hardware": {"num_devices": world, "link_bytes_per_ms": 7.7e8, "allreduce_bytes_per_ms": 7.25e8,
+                         "mem_bytes_per_device": 1.8e11, "data_load_ms_per_batch": 0.0,
+                         "min_utilization_floor": 1.0}}
+
+
+def observed_profile(reference: dict, measured: Dict[int, Tuple[int, float, float]]) -> dict:
+    """Monitoring (schedule.cpp:319-359): a running partition only observes its
+    blocks at its own per-device batch b_j.  The observed document rescales every key of block k
+    by observed/predicted at b_j, preserving the key structure profile_drift() requires."""
+    obs = json.loads(json.dumps(reference))
+    for k, (bj, t_ms, s_ms) in measured.items():
+        bt = core.exec_time(reference, k, "teacher", bj)
+        bs = core.exec_time(reference, k, "student", bj)
+        blk = obs["blocks"][k]
+        blk["teacher_ms"] = {key: v * (t_ms / bt) for key, v in blk["teacher_ms"].items()}
+        blk["student_ms"] = {key: v * (s_ms / bs) for key, v in blk["student_ms"].items()}
+    return obs
+
+
+# ---------------------------------------------------------------- bench entry (torchrun, N > 1)
+
+def bench_pipeline(args, rank: int, world: int, local_rank: int) -> dict:
+    from . import executor, models
+    dev = torch.device("cuda", local_rank)
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=dev)
+    gb = args.batch * world
+    # profile on every rank's own GPU, schedule on rank 0, broadcast the document
+    prof = profile_blocks(gb, world, device=dev) if rank == 0 else None
+    obj = [None, None]
+    if rank == 0:
+        sched, meta = core.best_schedule(prof)
+        obj = [sched, {"profile": prof, "meta": meta}]
+    dist.broadcast_object_list(obj, src=0)
+    sched, info = obj
+
+    def make_stage(lo, hi, n, first):
+        p = executor.Partition(lo, hi, n, gb, device=dev)
+        p.init_params()
+        p.set_shard(n, first)
+        return p
+
+    pipe = PipeBD(sched, gb, make_stage)
+    for _ in range(max(3, args.warmup)):
+        pipe.step()
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        pipe.step()
+    pipe._finish_sends()
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    losses = pipe.block_losses()
+    all_losses = [None] * world
+    dist.all_gather_object(all_losses, losses)
+    pred = core.predicted_step_time(info["profile"], sched)
+    return {"metric": "blockwise-distill samples/sec", "value": gb / ms * 1e3, "unit": "samples/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (Philox4x32-10 on device)",
+            "config": {"workload": "cifar-resnet18-teacher/slim-student 4 blocks (configs[1])", "global_batch": gb,
+                       "parallelism": "ahd " + ";".join(f"{p['blocks']}x{len(p['devices'])}"
+                                                        for p in sched["partitions"])},
+            "schedule": sched, "predicted_step_ms": pred["step_ms"],
+            "block_losses": {k: v for d in all_losses for k, v in d.items()},
+            "gpu_launches": pipe.stage.launches_per_step() * args.steps}

@@ -1,0 +1,107 @@
+"""Multi-rank host logic of runtime.py on CPU (gloo, world size 2 and 3).
+
+The stages are oracle-backed (tests/oracle_stage.py); the placement, the
+relay resharding between groups of different sizes, the group allreduce and
+the DPU / barrier paths are the product's.  The distributed run must equal a
+single-process run of the same schedule (the oracle Trainer with the same DP
+shards): identical per-block losses and student weights.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2301_12443_b200 import runtime
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def sched(parts, b):
+    return {"flags": {"tr": True, "dpu": True, "ahd": True},
+            "partitions": [{"blocks": [lo, hi], "devices": devs, "per_device_batch": -(-b // len(devs))}
+                           for lo, hi, devs in parts],
+            "predicted": {"partition_ms": [0.0] * len(parts), "step_ms": 0.0}}
+
+
+def _worker(rank, world, port, schedule, b, steps, dpu, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    torch.set_num_threads(2)
+    os.environ["OMP_NUM_THREADS"] = "2"
+    from tests.oracle_stage import OracleStage
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        pipe = runtime.PipeBD(schedule, b, lambda lo, hi, n, first: OracleStage(lo, hi, n, first, b), dpu=dpu)
+        for _ in range(steps):
+            pipe.step()
+        pipe.end_epoch()
+        losses = pipe.block_losses()
+        q.put((rank, losses, {k: pipe.stage.sp[k] for k in pipe.stage.blocks}, pipe.me.index))
+    finally:
+        dist.destroy_process_group()
+
+
+def run_dist(schedule, world, b, steps, dpu=True):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, schedule, b, steps, dpu, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return out
+
+
+@pytest.mark.parametrize("parts,world,dpu", [
+    ([(0, 1, [0]), (2, 3, [1])], 2, True),          # pure pipeline (teacher relaying)
+    ([(0, 3, [0, 1])], 2, True),                     # internal relaying: one DP group of 2
+    ([(0, 0, [0, 1]), (1, 3, [2])], 3, False),       # hybrid: resharding 2 -> 1, TR without DPU
+    ([(0, 1, [0]), (2, 3, [1, 2])], 3, True),        # hybrid: resharding 1 -> 2
+])
+def test_distributed_equals_single_process(parts, world, dpu):
+    from oracle import bd
+    b, steps = 5, 2   # odd batch: uneven shards (remainder rule)
+    s = sched(parts, b)
+    out = run_dist(s, world, b, steps, dpu)
+    groups = {}
+    for lo, hi, devs in parts:
+        for k in range(lo, hi + 1):
+            groups[k] = len(devs)
+    tr = bd.Trainer(b, bf16_mode=1)
+    for st in range(steps):
+        want = tr.step(st, groups)
+    for rank, losses, params, index in out:
+        for k, v in losses.items():
+            assert v == pytest.approx(want[k], rel=1e-12, abs=1e-15), (rank, k)
+        for k, p in params.items():
+            np.testing.assert_allclose(p, tr.sp[k], rtol=1e-6, atol=1e-9)
+
+
+def test_relay_plan_covers_every_row_once():
+    for b in (5, 7, 64, 255):
+        for g_up in range(1, 5):
+            for g_dn in range(1, 5):
+                ups = list(range(g_up))
+                dns = list(range(g_up, g_up + g_dn))
+                s = sched([(0, 0, ups), (1, 3, dns)], b)
+                msgs = runtime.relay_plan(s, b, 1)
+                got = np.zeros(b, int)
+                for src, dst, so, do, rows in msgs:
+                    fs, cs = runtime.shard(b, g_up, ups.index(src))
+                    fd, cd = runtime.shard(b, g_dn, dns.index(dst))
+                    assert 0 <= so and so + rows <= cs and 0 <= do and do + rows <= cd
+                    assert fs + so == fd + do
+                    got[fd + do: fd + do + rows] += 1
+                assert (got == 1).all()
