@@ -26,46 +26,120 @@ constexpr int kSmemBudget = 200 * 1024;
 
 __host__ __device__ constexpr int layout_for_sw(int sw) { return sw == 128 ? 2 : (sw == 64 ? 4 : 6); }
 __host__ __device__ constexpr int round_up(int a, int b) { return (a + b - 1) / b * b; }
-__host__ __device__ constexpr int tmem_cols_for(int n) { return n <= 32 ? 32 : (n <= 64 ? 64 : (n <= 128 ? 128 : 256)); }
+__host__ __device__ constexpr int tmem_cols_for(int n) {
+  return n <= 32 ? 32 : (n <= 64 ? 64 : (n <= 128 ? 128 : (n <= 256 ? 256 : 512)));
+}
 
-template <int BN, int BKC>
+// Persistent fprop: grid = min(tiles, #SMs); each CTA walks tiles t = blockIdx.x + i*gridDim.x
+// (N tile fastest, so CTAs working on one M tile at the same time share its A boxes in L2).
+// Two TMEM accumulators (2*BN columns): the epilogue of tile i overlaps the MMAs of tile i+1.
+// BRES: the whole filter (all K blocks of the single N tile) is loaded into shared memory once
+// per CTA and stays resident; the ring then carries only the activation boxes.
+template <int BN, int BKC, bool BRES>
 struct FpropCfg {
   static constexpr int SW = BKC * 2;  // bytes per smem row == swizzle span
   static constexpr int LAYOUT = layout_for_sw(SW);
   static constexpr int A_BYTES = 128 * SW;
   static constexpr int B_BYTES = BN * SW;
-  static constexpr int STAGE = round_up(A_BYTES + B_BYTES, 1024);
-  static constexpr int STAGES = (kSmemBudget / STAGE) > 8 ? 8 : (kSmemBudget / STAGE);
-  static constexpr int TMEM_COLS = tmem_cols_for(BN);
-  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+  static constexpr int B_RES_MAX = 96 * 1024;  // resident filter budget
+  static constexpr int STAGE = round_up(A_BYTES + (BRES ? 0 : B_BYTES), 1024);
+  static constexpr int RING = (BRES ? kSmemBudget - B_RES_MAX : kSmemBudget);
+  static constexpr int STAGES = (RING / STAGE) > 8 ? 8 : (RING / STAGE);
+  static constexpr int ACC_COLS = BN < 32 ? 32 : BN;
+  static constexpr int TMEM_COLS = tmem_cols_for(2 * ACC_COLS);
+  static constexpr int SMEM = STAGES * STAGE + (BRES ? B_RES_MAX : 0) + 1024 + 256;
 };
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
 
-template <int BN, int BKC>
-__global__ void __launch_bounds__(kThreads, 1)
-    conv_fprop_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
-                      const FpropArgs a) {
-  using C = FpropCfg<BN, BKC>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = align1024(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
-  uint64_t* empty = full + C::STAGES;
-  uint64_t* tfull = empty + C::STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
-
-  const int warp = warp_id();
-  const int lane = lane_id();
-  const int k0 = blockIdx.x * BN;
-  const int m_tile = blockIdx.y;
+template <int BN>
+__device__ __forceinline__ void fprop_epilogue(const FpropArgs& a, uint32_t trow, int row, int m_tile, int k0) {
   const int tq = m_tile % a.tiles_q;
   const int t2 = m_tile / a.tiles_q;
   const int tp = t2 % a.tiles_p;
   const int tn = t2 / a.tiles_p;
-  const int ow0 = tq * a.bw, oh0 = tp * a.bh, n0 = tn * a.bn;
+  const int iw = row % a.bw;
+  const int ih = (row / a.bw) % a.bh;
+  const int in = row / (a.bw * a.bh);
+  const int nn = tn * a.bn + in;
+  const bool valid = nn < a.n;
+  const size_t m = (static_cast<size_t>(nn) * a.p + (tp * a.bh + ih)) * a.q + (tq * a.bw + iw);
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN; c0 += 16) {
+    float v[16];
+    tmem_ld16(trow + c0, v);
+    if (!valid) continue;
+    const int col = k0 + c0;
+    if (a.epi == PBDK_EPI_BIAS || a.epi == PBDK_EPI_BIAS_RELU || a.epi == PBDK_EPI_BIAS_RES_RELU) {
+      const float4* b4 = reinterpret_cast<const float4*>(a.bias + col);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float4 b = __ldg(b4 + j);
+        v[4 * j + 0] += b.x;
+        v[4 * j + 1] += b.y;
+        v[4 * j + 2] += b.z;
+        v[4 * j + 3] += b.w;
+      }
+    }
+    if (a.epi == PBDK_EPI_BIAS_RES_RELU || a.epi == PBDK_EPI_RELU_MASK) {
+      const uint4* r4 = reinterpret_cast<const uint4*>(a.aux + m * a.k + col);
+      const uint4 ra = __ldg(r4);
+      const uint4 rb = __ldg(r4 + 1);
+      const uint32_t rw[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+      if (a.epi == PBDK_EPI_BIAS_RES_RELU) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          v[2 * j] += bf16_lo(rw[j]);
+          v[2 * j + 1] += bf16_hi(rw[j]);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          v[2 * j] = bf16_lo(rw[j]) > 0.f ? v[2 * j] : 0.f;
+          v[2 * j + 1] = bf16_hi(rw[j]) > 0.f ? v[2 * j + 1] : 0.f;
+        }
+      }
+    }
+    if (a.epi == PBDK_EPI_BIAS_RELU || a.epi == PBDK_EPI_BIAS_RES_RELU) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j], 0.f);
+    }
+    uint4 o0, o1;
+    o0.x = pack_bf16x2(v[0], v[1]);
+    o0.y = pack_bf16x2(v[2], v[3]);
+    o0.z = pack_bf16x2(v[4], v[5]);
+    o0.w = pack_bf16x2(v[6], v[7]);
+    o1.x = pack_bf16x2(v[8], v[9]);
+    o1.y = pack_bf16x2(v[10], v[11]);
+    o1.z = pack_bf16x2(v[12], v[13]);
+    o1.w = pack_bf16x2(v[14], v[15]);
+    uint4* dst = reinterpret_cast<uint4*>(a.y + m * a.k + col);
+    dst[0] = o0;
+    dst[1] = o1;
+  }
+}
+
+template <int BN, int BKC, bool BRES>
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_fprop_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
+                      const FpropArgs a) {
+  using C = FpropCfg<BN, BKC, BRES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* bres = smem + C::STAGES * C::STAGE;  // resident filter (BRES)
+  uint64_t* full = reinterpret_cast<uint64_t*>(bres + (BRES ? C::B_RES_MAX : 0));
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;         // [2]
+  uint64_t* bfull = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
   const int num_kb = a.r * a.s * a.c_chunks;
+  const int total = a.m_tiles * a.n_tiles;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmx);
@@ -74,7 +148,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    mbar_init(tfull, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    mbar_init(bfull, 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -86,105 +164,80 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       const int cin_stored = a.c_chunks * BKC;
-      for (int kb = 0; kb < num_kb; ++kb) {
-        const int st = kb % C::STAGES;
-        if (kb >= C::STAGES) mbar_wait(&empty[st], ((kb / C::STAGES) - 1) & 1);
-        const int tap = kb / a.c_chunks;
-        const int cc = kb - tap * a.c_chunks;
-        const int rr = tap / a.s;
-        const int ss = tap - rr * a.s;
-        uint8_t* sa = smem + st * C::STAGE;
-        uint8_t* sb = sa + C::A_BYTES;
-        mbar_arrive_expect_tx(&full[st], C::A_BYTES + C::B_BYTES);
-        tma_load_4d(sa, &tmx, &full[st], cc * BKC, ow0 * a.stride + ss - a.pad, oh0 * a.stride + rr - a.pad, n0);
-        tma_load_2d(sb, &tmw, &full[st], tap * cin_stored + cc * BKC, k0);
+      if (BRES) {
+        mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(num_kb * C::B_BYTES));
+        for (int kb = 0; kb < num_kb; ++kb) {
+          const int tap = kb / a.c_chunks;
+          const int cc = kb - tap * a.c_chunks;
+          tma_load_2d(bres + kb * C::B_BYTES, &tmw, bfull, tap * cin_stored + cc * BKC, 0);
+        }
+      }
+      int it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int m_tile = t / a.n_tiles;
+        const int k0 = (t - m_tile * a.n_tiles) * BN;
+        const int tq = m_tile % a.tiles_q;
+        const int t2 = m_tile / a.tiles_q;
+        const int tp = t2 % a.tiles_p;
+        const int tn = t2 / a.tiles_p;
+        const int ow0 = tq * a.bw, oh0 = tp * a.bh, n0 = tn * a.bn;
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int st = it % C::STAGES;
+          if (it >= C::STAGES) mbar_wait(&empty[st], ((it / C::STAGES) - 1) & 1);
+          const int tap = kb / a.c_chunks;
+          const int cc = kb - tap * a.c_chunks;
+          const int rr = tap / a.s;
+          const int ss = tap - rr * a.s;
+          uint8_t* sa = smem + st * C::STAGE;
+          mbar_arrive_expect_tx(&full[st], C::A_BYTES + (BRES ? 0 : C::B_BYTES));
+          tma_load_4d(sa, &tmx, &full[st], cc * BKC, ow0 * a.stride + ss - a.pad, oh0 * a.stride + rr - a.pad, n0);
+          if (!BRES) tma_load_2d(sa + C::A_BYTES, &tmw, &full[st], tap * cin_stored + cc * BKC, k0);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc_bf16(128, BN, 0, 0);
-      for (int kb = 0; kb < num_kb; ++kb) {
-        const int st = kb % C::STAGES;
-        mbar_wait(&full[st], (kb / C::STAGES) & 1);
+      if (BRES) mbar_wait(bfull, 0);
+      int it = 0, lt = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+        const int acc = lt & 1;
+        if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
         tc_fence_after();
-        const uint32_t sa = smem_u32(smem + st * C::STAGE);
-        const uint32_t sb = sa + C::A_BYTES;
+        const uint32_t dacc = tmem + static_cast<uint32_t>(acc * C::ACC_COLS);
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int st = it % C::STAGES;
+          mbar_wait(&full[st], (it / C::STAGES) & 1);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + st * C::STAGE);
+          const uint32_t sb = BRES ? smem_u32(bres + kb * C::B_BYTES) : sa + C::A_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < BKC / 16; ++kk) {
-          const uint64_t ad = umma_smem_desc(sa + kk * 32, 16, 8 * C::SW, C::LAYOUT);
-          const uint64_t bd = umma_smem_desc(sb + kk * 32, 16, 8 * C::SW, C::LAYOUT);
-          umma_bf16(tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+          for (int kk = 0; kk < BKC / 16; ++kk) {
+            const uint64_t ad = umma_smem_desc(sa + kk * 32, 16, 8 * C::SW, C::LAYOUT);
+            const uint64_t bd = umma_smem_desc(sb + kk * 32, 16, 8 * C::SW, C::LAYOUT);
+            umma_bf16(dacc, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty[st]);
         }
-        umma_commit(&empty[st]);
+        umma_commit(&tfull[acc]);
       }
-      umma_commit(tfull);
     }
   } else {
     // epilogue: warps 2..5, TMEM lane quarter = warp % 4
-    mbar_wait(tfull, 0);
-    tc_fence_after();
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
-    const int iw = row % a.bw;
-    const int ih = (row / a.bw) % a.bh;
-    const int in = row / (a.bw * a.bh);
-    const int nn = n0 + in;
-    const bool valid = nn < a.n;
-    const size_t m = (static_cast<size_t>(nn) * a.p + (oh0 + ih)) * a.q + (ow0 + iw);
-    const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      float v[16];
-      tmem_ld16(trow + c0, v);
-      if (valid) {
-        const int col = k0 + c0;
-        if (a.epi == PBDK_EPI_BIAS || a.epi == PBDK_EPI_BIAS_RELU || a.epi == PBDK_EPI_BIAS_RES_RELU) {
-          const float4* b4 = reinterpret_cast<const float4*>(a.bias + col);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float4 b = __ldg(b4 + j);
-            v[4 * j + 0] += b.x;
-            v[4 * j + 1] += b.y;
-            v[4 * j + 2] += b.z;
-            v[4 * j + 3] += b.w;
-          }
-        }
-        if (a.epi == PBDK_EPI_BIAS_RES_RELU || a.epi == PBDK_EPI_RELU_MASK) {
-          const uint4* r4 = reinterpret_cast<const uint4*>(a.aux + m * a.k + col);
-          const uint4 ra = __ldg(r4);
-          const uint4 rb = __ldg(r4 + 1);
-          const uint32_t rw[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
-          if (a.epi == PBDK_EPI_BIAS_RES_RELU) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              v[2 * j] += bf16_lo(rw[j]);
-              v[2 * j + 1] += bf16_hi(rw[j]);
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              v[2 * j] = bf16_lo(rw[j]) > 0.f ? v[2 * j] : 0.f;
-              v[2 * j + 1] = bf16_hi(rw[j]) > 0.f ? v[2 * j + 1] : 0.f;
-            }
-          }
-        }
-        if (a.epi == PBDK_EPI_BIAS_RELU || a.epi == PBDK_EPI_BIAS_RES_RELU) {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j], 0.f);
-        }
-        uint4 o0, o1;
-        o0.x = pack_bf16x2(v[0], v[1]);
-        o0.y = pack_bf16x2(v[2], v[3]);
-        o0.z = pack_bf16x2(v[4], v[5]);
-        o0.w = pack_bf16x2(v[6], v[7]);
-        o1.x = pack_bf16x2(v[8], v[9]);
-        o1.y = pack_bf16x2(v[10], v[11]);
-        o1.z = pack_bf16x2(v[12], v[13]);
-        o1.w = pack_bf16x2(v[14], v[15]);
-        uint4* dst = reinterpret_cast<uint4*>(a.y + m * a.k + col);
-        dst[0] = o0;
-        dst[1] = o1;
-      }
+    int lt = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+      const int acc = lt & 1;
+      mbar_wait(&tfull[acc], (lt >> 1) & 1);
+      tc_fence_after();
+      const int m_tile = t / a.n_tiles;
+      const int k0 = (t - m_tile * a.n_tiles) * BN;
+      const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * C::ACC_COLS);
+      fprop_epilogue<BN>(a, trow, row, m_tile, k0);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
     }
   }
   tc_fence_before();
@@ -195,13 +248,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int BN, int BKC>
+template <int BN, int BKC, bool BRES>
 cudaError_t launch_fprop(const FpropPlan& p, cudaStream_t stream) {
-  using C = FpropCfg<BN, BKC>;
+  using C = FpropCfg<BN, BKC, BRES>;
   if (stream == reinterpret_cast<cudaStream_t>(-1)) {  // prepare: set the smem attribute outside any capture
-    return cudaFuncSetAttribute(conv_fprop_kernel<BN, BKC>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    return cudaFuncSetAttribute(conv_fprop_kernel<BN, BKC, BRES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                C::SMEM);
   }
-  conv_fprop_kernel<BN, BKC><<<p.grid, kThreads, C::SMEM, stream>>>(p.tmx, p.tmw, p.args);
+  conv_fprop_kernel<BN, BKC, BRES><<<p.grid, kThreads, C::SMEM, stream>>>(p.tmx, p.tmw, p.args);
   return cudaGetLastError();
 }
 
@@ -425,24 +479,28 @@ bool act_map(CUtensorMap* m, const void* base, int n, int h, int w, int c, int c
 
 using FpropLauncher = cudaError_t (*)(const FpropPlan&, cudaStream_t);
 
-template <int BKC>
+template <int BKC, bool BRES>
 FpropLauncher pick_fprop(int bn) {
   switch (bn) {
-    case 16: return launch_fprop<16, BKC>;
-    case 32: return launch_fprop<32, BKC>;
-    case 64: return launch_fprop<64, BKC>;
-    case 128: return launch_fprop<128, BKC>;
-    case 256: return launch_fprop<256, BKC>;
+    case 16: return launch_fprop<16, BKC, BRES>;
+    case 32: return launch_fprop<32, BKC, BRES>;
+    case 64: return launch_fprop<64, BKC, BRES>;
+    case 128: return launch_fprop<128, BKC, BRES>;
+    case 256: return launch_fprop<256, BKC, BRES>;
     default: return nullptr;
   }
 }
 
-int fprop_smem(int bn, int bkc) {
-  const int sw = bkc * 2;
-  const int stage = round_up(128 * sw + bn * sw, 1024);
-  const int stages = std::min(8, kSmemBudget / stage);
-  return stages * stage + 1024 + 256;
+int num_sms() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
+  return n;
 }
+
+
 
 using WgradLauncher = cudaError_t (*)(const WgradPlan&, cudaStream_t);
 
@@ -484,11 +542,13 @@ int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, c
       break;
     }
   }
+  const int num_kb = d.r * d.s * (d.c / bkc);
+  const bool bres = (d.k == bn) && num_kb * bn * bkc * 2 <= 96 * 1024;
   FpropLauncher l = nullptr;
   switch (bkc) {
-    case 16: l = pick_fprop<16>(bn); break;
-    case 32: l = pick_fprop<32>(bn); break;
-    case 64: l = pick_fprop<64>(bn); break;
+    case 16: l = bres ? pick_fprop<16, true>(bn) : pick_fprop<16, false>(bn); break;
+    case 32: l = bres ? pick_fprop<32, true>(bn) : pick_fprop<32, false>(bn); break;
+    case 64: l = bres ? pick_fprop<64, true>(bn) : pick_fprop<64, false>(bn); break;
     default: break;
   }
   if (l == nullptr) return PBDK_EINVAL;
@@ -520,10 +580,13 @@ int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, c
   a.y = static_cast<__nv_bfloat16*>(y);
   a.bias = bias;
   a.aux = static_cast<const __nv_bfloat16*>(aux);
-  plan->grid = dim3(static_cast<unsigned>(d.k / bn), static_cast<unsigned>(g.m_tiles), 1);
+  a.n_tiles = d.k / bn;
+  a.m_tiles = g.m_tiles;
+  const int tiles = a.n_tiles * a.m_tiles;
+  plan->grid = dim3(static_cast<unsigned>(std::min(tiles, num_sms())), 1, 1);
   plan->bn_tile = bn;
   plan->bkc = bkc;
-  plan->smem_bytes = fprop_smem(bn, bkc);
+  plan->smem_bytes = 0;
   plan->launch = l;
   if (l(*plan, reinterpret_cast<cudaStream_t>(-1)) != cudaSuccess) return PBDK_ECUDA;
   return PBDK_OK;

@@ -30,6 +30,7 @@ struct FpropArgs {
   int stride, pad, r, s;
   int bw, bh, bn, tiles_q, tiles_p;
   int c_chunks;
+  int n_tiles, m_tiles;
   int epi;
   __nv_bfloat16* y;
   const float* bias;
