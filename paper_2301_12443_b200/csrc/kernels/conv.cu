@@ -16,13 +16,15 @@
 #include "tmap.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace pbdk {
 
 namespace {
 
 constexpr int kThreads = 192;
-constexpr int kSmemBudget = 200 * 1024;
+constexpr int kSmemBudget = 200 * 1024;      // wgrad pipeline
+constexpr int kFpropBudget = 220 * 1024;     // fprop ring + resident filter
 
 __host__ __device__ constexpr int layout_for_sw(int sw) { return sw == 128 ? 2 : (sw == 64 ? 4 : 6); }
 __host__ __device__ constexpr int round_up(int a, int b) { return (a + b - 1) / b * b; }
@@ -43,7 +45,7 @@ struct FpropCfg {
   static constexpr int B_BYTES = BN * SW;
   static constexpr int B_RES_MAX = 96 * 1024;  // resident filter budget
   static constexpr int STAGE = round_up(A_BYTES + (BRES ? 0 : B_BYTES), 1024);
-  static constexpr int RING = (BRES ? kSmemBudget - B_RES_MAX : kSmemBudget);
+  static constexpr int RING = (BRES ? kFpropBudget - B_RES_MAX : kFpropBudget);
   static constexpr int STAGES = (RING / STAGE) > 8 ? 8 : (RING / STAGE);
   static constexpr int ACC_COLS = BN < 32 ? 32 : BN;
   static constexpr int TMEM_COLS = tmem_cols_for(2 * ACC_COLS);
@@ -54,25 +56,27 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
 
-template <int BN>
-__device__ __forceinline__ void fprop_epilogue(const FpropArgs& a, uint32_t trow, int row, int m_tile, int k0) {
-  const int tq = m_tile % a.tiles_q;
-  const int t2 = m_tile / a.tiles_q;
-  const int tp = t2 % a.tiles_p;
-  const int tn = t2 / a.tiles_p;
-  const int iw = row % a.bw;
-  const int ih = (row / a.bw) % a.bh;
-  const int in = row / (a.bw * a.bh);
-  const int nn = tn * a.bn + in;
-  const bool valid = nn < a.n;
-  const size_t m = (static_cast<size_t>(nn) * a.p + (tp * a.bh + ih)) * a.q + (tq * a.bw + iw);
+// Epilogue: thread = accumulator row (TMEM lane).  tcgen05.ld 16 columns at a time, fused
+// bias / residual / ReLU / ReLU-mask in fp32, one bf16 rounding, 2 x 16 B stores straight
+// from registers.  No shared-memory staging on purpose: for N <= 128 the tensor core is
+// bound by its shared-memory read port (SS operands), so the epilogue must not compete
+// for it.  RowMap(r) -> (valid, output pixel index) of tile row r.
+template <int BN, class RowMap>
+__device__ __forceinline__ void fprop_epilogue(const FpropArgs& a, uint32_t trow, int row, int k0,
+                                               const RowMap& rowmap) {
+  bool valid;
+  size_t m;
+  rowmap(row, valid, m);
+  const bool has_bias = a.epi == PBDK_EPI_BIAS || a.epi == PBDK_EPI_BIAS_RELU || a.epi == PBDK_EPI_BIAS_RES_RELU;
+  const bool relu = a.epi == PBDK_EPI_BIAS_RELU || a.epi == PBDK_EPI_BIAS_RES_RELU;
+  if (a.debug == 3) return;
 #pragma unroll 1
   for (int c0 = 0; c0 < BN; c0 += 16) {
     float v[16];
     tmem_ld16(trow + c0, v);
-    if (!valid) continue;
+    if (!valid || a.debug == 1) continue;
     const int col = k0 + c0;
-    if (a.epi == PBDK_EPI_BIAS || a.epi == PBDK_EPI_BIAS_RELU || a.epi == PBDK_EPI_BIAS_RES_RELU) {
+    if (has_bias) {
       const float4* b4 = reinterpret_cast<const float4*>(a.bias + col);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -102,7 +106,7 @@ __device__ __forceinline__ void fprop_epilogue(const FpropArgs& a, uint32_t trow
         }
       }
     }
-    if (a.epi == PBDK_EPI_BIAS_RELU || a.epi == PBDK_EPI_BIAS_RES_RELU) {
+    if (relu) {
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j], 0.f);
     }
@@ -120,6 +124,31 @@ __device__ __forceinline__ void fprop_epilogue(const FpropArgs& a, uint32_t trow
     dst[1] = o1;
   }
 }
+
+struct TileRows {  // regular tiles: a (bn images) x (bh rows) x (bw cols) box of output pixels
+  const FpropArgs* a;
+  int n0, oh0, ow0;
+  __device__ __forceinline__ void operator()(int row, bool& valid, size_t& m) const {
+    const int iw = row % a->bw;
+    const int ih = (row / a->bw) % a->bh;
+    const int in = row / (a->bw * a->bh);
+    const int nn = n0 + in;
+    valid = nn < a->n;
+    m = (static_cast<size_t>(nn) * a->p + (oh0 + ih)) * a->q + (ow0 + iw);
+  }
+};
+
+struct HaloRows {  // halo tiles: 128 consecutive positions of a (W+2)-wide padded image
+  const FpropArgs* a;
+  int img, p0, wp;
+  __device__ __forceinline__ void operator()(int row, bool& valid, size_t& m) const {
+    const int p = p0 + row;
+    const int h = p / wp;
+    const int w = p - h * wp;
+    valid = h < a->p && w < a->q;
+    m = (static_cast<size_t>(img) * a->p + h) * a->q + w;
+  }
+};
 
 template <int BN, int BKC, bool BRES>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -211,11 +240,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + st * C::STAGE);
           const uint32_t sb = BRES ? smem_u32(bres + kb * C::B_BYTES) : sa + C::A_BYTES;
+          const uint64_t a0 = umma_smem_desc(sa, 16, 8 * C::SW, C::LAYOUT);
+          const uint64_t b0 = umma_smem_desc(sb, 16, 8 * C::SW, C::LAYOUT);
 #pragma unroll
           for (int kk = 0; kk < BKC / 16; ++kk) {
-            const uint64_t ad = umma_smem_desc(sa + kk * 32, 16, 8 * C::SW, C::LAYOUT);
-            const uint64_t bd = umma_smem_desc(sb + kk * 32, 16, 8 * C::SW, C::LAYOUT);
-            umma_bf16(dacc, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+            if (a.debug != 2) umma_bf16(dacc, a0 + 2 * kk, b0 + 2 * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
           }
           umma_commit(&empty[st]);
         }
@@ -225,7 +254,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // epilogue: warps 2..5, TMEM lane quarter = warp % 4
     const int quarter = warp & 3;
-    const int row = quarter * 32 + lane;
     int lt = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
       const int acc = lt & 1;
@@ -234,7 +262,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m_tile = t / a.n_tiles;
       const int k0 = (t - m_tile * a.n_tiles) * BN;
       const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * C::ACC_COLS);
-      fprop_epilogue<BN>(a, trow, row, m_tile, k0);
+      const int tq = m_tile % a.tiles_q;
+      const int t2 = m_tile / a.tiles_q;
+      const TileRows rows{&a, (t2 / a.tiles_p) * a.bn, (t2 % a.tiles_p) * a.bh, tq * a.bw};
+      fprop_epilogue<BN>(a, trow, quarter * 32 + lane, k0, rows);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -246,6 +277,193 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc(tmem, C::TMEM_COLS);
   }
+}
+
+// ------------------------------------------------------------------ halo fprop (3x3, stride 1, pad 1)
+// For wide images (W = 32) the per-tap boxes re-read every input pixel 9 times through L2.
+// Here the GEMM rows index a zero-padded image: output position p = h*(W+2) + w' (w' in
+// [0, W+2), w' >= W are discarded), and the input tile is ONE TMA box of padded rows
+// (columns -1..W, rows from p0/(W+2)-1, OOB zero = padding).  Tap (r, s) is then the same
+// smem tile read from row offset (p0 % (W+2)) + r*(W+2) + s: all 9 taps come from a single
+// load, so activation traffic drops ~5x for a ~6% row overhead (32x32: 9 tiles of 128 rows
+// cover the 1088 padded positions of an image).  Filters stay resident in shared memory.
+template <int BN, int BKC>
+struct HaloCfg {
+  static constexpr int SW = BKC * 2;
+  static constexpr int LAYOUT = layout_for_sw(SW);
+  static constexpr int B_BYTES = BN * SW;
+  static constexpr int B_RES_MAX = 96 * 1024;
+  static constexpr int ACC_COLS = BN < 32 ? 32 : BN;
+  static constexpr int TMEM_COLS = tmem_cols_for(2 * ACC_COLS);
+  static constexpr int SMEM = kFpropBudget + 1024 + 256;
+};
+
+template <int BN, int BKC>
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_fprop_halo_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
+                           const FpropArgs a) {
+  using C = HaloCfg<BN, BKC>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  const int stages = a.halo_stages;
+  const int stage_bytes = a.halo_stage_bytes;
+  uint8_t* bres = smem + stages * stage_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(bres + C::B_RES_MAX);
+  uint64_t* empty = full + 8;
+  uint64_t* tfull = empty + 8;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* bfull = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int wp = a.q + 2;
+  const int taps = a.r * a.s;
+  const int total = a.m_tiles;  // single N tile
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmx);
+    tma_prefetch(&tmw);
+    for (int i = 0; i < stages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    mbar_init(bfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int cin_stored = a.c_chunks * BKC;
+      const int num_kb = taps * a.c_chunks;
+      mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(num_kb * C::B_BYTES));
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int tap = kb / a.c_chunks;
+        const int cc = kb - tap * a.c_chunks;
+        tma_load_2d(bres + kb * C::B_BYTES, &tmw, bfull, tap * cin_stored + cc * BKC, 0);
+      }
+      const uint32_t box_bytes = static_cast<uint32_t>(a.halo_rows * wp * C::SW);
+      int it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int img = t / a.tiles_img;
+        const int p0 = (t - img * a.tiles_img) * 128;
+        for (int cc = 0; cc < a.c_chunks; ++cc, ++it) {
+          const int st = it % stages;
+          if (it >= stages) mbar_wait(&empty[st], ((it / stages) - 1) & 1);
+          mbar_arrive_expect_tx(&full[st], box_bytes);
+          tma_load_4d(smem + st * stage_bytes, &tmx, &full[st], cc * BKC, -1, p0 / wp - 1, img);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(128, BN, 0, 0);
+      mbar_wait(bfull, 0);
+      int it = 0, lt = 0;
+      long long c_start = clock64(), c_tempty = 0, c_full = 0, c_issue = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+        const int acc = lt & 1;
+        long long c0 = clock64();
+        if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
+        c_tempty += clock64() - c0;
+        tc_fence_after();
+        const uint32_t dacc = tmem + static_cast<uint32_t>(acc * C::ACC_COLS);
+        const int img = t / a.tiles_img;
+        const int p0 = (t - img * a.tiles_img) * 128;
+        const int j0 = p0 % wp;
+        // Descriptors are advanced by adding (byte offset >> 4) to the start-address field
+        // (smem addresses < 256 KB never carry out of the 14-bit field): no per-MMA rebuild.
+        const uint32_t row_step = static_cast<uint32_t>(wp * C::SW) >> 4;     // +1 filter row (r)
+        const uint32_t tap_step = static_cast<uint32_t>(a.c_chunks * C::B_BYTES) >> 4;
+        for (int cc = 0; cc < a.c_chunks; ++cc, ++it) {
+          const int st = it % stages;
+          long long c1 = clock64();
+          mbar_wait(&full[st], (it / stages) & 1);
+          long long c2 = clock64();
+          c_full += c2 - c1;
+          tc_fence_after();
+          const uint64_t a0 =
+              umma_smem_desc(smem_u32(smem + st * stage_bytes) + static_cast<uint32_t>(j0 * C::SW), 16, 8 * C::SW,
+                             C::LAYOUT);
+          const uint64_t b0 = umma_smem_desc(smem_u32(bres + cc * C::B_BYTES), 16, 8 * C::SW, C::LAYOUT);
+#pragma unroll
+          for (int rr = 0; rr < 3; ++rr) {
+#pragma unroll
+            for (int ss = 0; ss < 3; ++ss) {
+#pragma unroll
+              for (int kk = 0; kk < BKC / 16; ++kk) {
+                const uint64_t ad = a0 + rr * row_step + static_cast<uint32_t>((ss * C::SW + kk * 32) >> 4);
+                const uint64_t bd = b0 + (rr * 3 + ss) * tap_step + static_cast<uint32_t>((kk * 32) >> 4);
+                const uint32_t accum = (cc != 0 || rr != 0 || ss != 0 || kk != 0) ? 1u : 0u;
+                if (a.debug != 2) umma_bf16(dacc, ad, bd, idesc, accum);
+              }
+            }
+          }
+          umma_commit(&empty[st]);
+          c_issue += clock64() - c2;
+        }
+        umma_commit(&tfull[acc]);
+      }
+      if (a.debug == 4) {
+        long long* d = a.dbg_buf + blockIdx.x * 8;
+        d[0] = clock64() - c_start;
+        d[1] = c_tempty;
+        d[2] = c_full;
+        d[3] = c_issue;
+        d[6] = lt;
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    int lt = 0;
+    long long e_wait = 0, e_work = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+      const int acc = lt & 1;
+      long long c0 = clock64();
+      mbar_wait(&tfull[acc], (lt >> 1) & 1);
+      long long c1 = clock64();
+      e_wait += c1 - c0;
+      tc_fence_after();
+      const int img = t / a.tiles_img;
+      const HaloRows rows{&a, img, (t - img * a.tiles_img) * 128, wp};
+      const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * C::ACC_COLS);
+      fprop_epilogue<BN>(a, trow, quarter * 32 + lane, 0, rows);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      e_work += clock64() - c1;
+    }
+    if (a.debug == 4 && quarter == 0 && lane == 0) {
+      a.dbg_buf[blockIdx.x * 8 + 4] = e_wait;
+      a.dbg_buf[blockIdx.x * 8 + 5] = e_work;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+template <int BN, int BKC>
+cudaError_t launch_fprop_halo(const FpropPlan& p, cudaStream_t stream) {
+  using C = HaloCfg<BN, BKC>;
+  if (stream == reinterpret_cast<cudaStream_t>(-1)) {
+    return cudaFuncSetAttribute(conv_fprop_halo_kernel<BN, BKC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                C::SMEM);
+  }
+  conv_fprop_halo_kernel<BN, BKC><<<p.grid, kThreads, C::SMEM, stream>>>(p.tmx, p.tmw, p.args);
+  return cudaGetLastError();
 }
 
 template <int BN, int BKC, bool BRES>
@@ -491,6 +709,25 @@ FpropLauncher pick_fprop(int bn) {
   }
 }
 
+template <int BKC>
+FpropLauncher pick_halo(int bn) {
+  switch (bn) {
+    case 16: return launch_fprop_halo<16, BKC>;
+    case 32: return launch_fprop_halo<32, BKC>;
+    case 64: return launch_fprop_halo<64, BKC>;
+    case 128: return launch_fprop_halo<128, BKC>;
+    default: return nullptr;
+  }
+}
+
+bool halo_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PBDK_NO_HALO");
+    return e == nullptr || e[0] == '0';
+  }();
+  return on;
+}
+
 int num_sms() {
   static int n = [] {
     int dev = 0, v = 148;
@@ -544,6 +781,8 @@ int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, c
   }
   const int num_kb = d.r * d.s * (d.c / bkc);
   const bool bres = (d.k == bn) && num_kb * bn * bkc * 2 <= 96 * 1024;
+  const bool halo = halo_enabled() && bres && bn <= 128 && d.r == 3 && d.s == 3 && d.stride == 1 && d.pad == 1 &&
+                    d.q >= 32 && d.q + 2 <= 256;
   FpropLauncher l = nullptr;
   switch (bkc) {
     case 16: l = bres ? pick_fprop<16, true>(bn) : pick_fprop<16, false>(bn); break;
@@ -551,8 +790,34 @@ int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, c
     case 64: l = bres ? pick_fprop<64, true>(bn) : pick_fprop<64, false>(bn); break;
     default: break;
   }
+  if (halo) {
+    switch (bkc) {
+      case 16: l = pick_halo<16>(bn); break;
+      case 32: l = pick_halo<32>(bn); break;
+      case 64: l = pick_halo<64>(bn); break;
+      default: l = nullptr; break;
+    }
+  }
   if (l == nullptr) return PBDK_EINVAL;
-  if (!act_map(&plan->tmx, x, d.n, d.h, d.w, d.c, bkc, g.bw, g.bh, g.bn, d.stride)) return PBDK_ECUDA;
+  FpropArgs& a0 = plan->args;
+  if (halo) {
+    const int wp = d.q + 2;
+    a0.halo_rows = 3 + (129 + wp - 1) / wp;
+    a0.halo_stage_bytes = round_up(a0.halo_rows * wp * bkc * 2, 1024);
+    a0.halo_stages = std::min(8, (kFpropBudget - 96 * 1024) / a0.halo_stage_bytes);
+    a0.tiles_img = (d.p * wp + 127) / 128;
+    if (a0.halo_stages < 2) return PBDK_EINVAL;
+    const uint64_t dims[4] = {static_cast<uint64_t>(d.c), static_cast<uint64_t>(d.w), static_cast<uint64_t>(d.h),
+                              static_cast<uint64_t>(d.n)};
+    const uint64_t strides[3] = {static_cast<uint64_t>(d.c) * 2, static_cast<uint64_t>(d.w) * d.c * 2,
+                                 static_cast<uint64_t>(d.h) * d.w * d.c * 2};
+    const uint32_t box[4] = {static_cast<uint32_t>(bkc), static_cast<uint32_t>(wp),
+                             static_cast<uint32_t>(a0.halo_rows), 1};
+    const uint32_t es[4] = {1, 1, 1, 1};
+    if (!encode_tmap_bf16(&plan->tmx, x, 4, dims, strides, box, es, bkc * 2)) return PBDK_ECUDA;
+  } else if (!act_map(&plan->tmx, x, d.n, d.h, d.w, d.c, bkc, g.bw, g.bh, g.bn, d.stride)) {
+    return PBDK_ECUDA;
+  }
   {
     const uint64_t ktot = static_cast<uint64_t>(d.r) * d.s * d.c;
     const uint64_t dims[2] = {ktot, static_cast<uint64_t>(d.k)};
@@ -577,11 +842,16 @@ int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, c
   a.tiles_p = g.tiles_p;
   a.c_chunks = d.c / bkc;
   a.epi = epi;
+  {
+    const char* dbg = std::getenv("PBDK_CONV_DEBUG");
+    a.debug = dbg != nullptr ? std::atoi(dbg) : 0;
+    a.dbg_buf = a.debug == 4 ? static_cast<long long*>(const_cast<void*>(aux)) : nullptr;
+  }
   a.y = static_cast<__nv_bfloat16*>(y);
   a.bias = bias;
   a.aux = static_cast<const __nv_bfloat16*>(aux);
   a.n_tiles = d.k / bn;
-  a.m_tiles = g.m_tiles;
+  a.m_tiles = halo ? d.n * a.tiles_img : g.m_tiles;
   const int tiles = a.n_tiles * a.m_tiles;
   plan->grid = dim3(static_cast<unsigned>(std::min(tiles, num_sms())), 1, 1);
   plan->bn_tile = bn;
