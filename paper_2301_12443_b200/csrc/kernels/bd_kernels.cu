@@ -134,126 +134,143 @@ __global__ void fill_kernel(float* __restrict__ dst, size_t n, float v) {
     dst[i] = v;
 }
 
-// ------------------------------------------------------------------ reductions
-// Geometry of a row-chunked reduction over [M][C]: cg = C/8 channel groups per
-// row, rpp = 256/cg rows per pass; CTA b covers rows [b*rows_per_chunk, ...).
+// ------------------------------------------------------------------ row-wise kernels over [M][C]
+// Thread (g, slot): g = tid % cg owns V consecutive channels for the whole kernel (its
+// per-channel BN parameters are loaded once, into registers), slot = tid / cg picks rows.
+// Partial reductions: CTA b covers the contiguous rows [b*rows_per_chunk, ...), fp32 sums
+// per thread, fixed-order CTA combine into partial[chunk][NV][C]; finalize kernels add the
+// chunk partials in a fixed strided order in fp64.  Deterministic for a given (M, C).
+
+template <int V>
+struct Vec;
+template <>
+struct Vec<8> {
+  using T = uint4;
+  __device__ static void load(const __nv_bfloat16* p, float (&f)[8]) { unpack8(*reinterpret_cast<const uint4*>(p), f); }
+  __device__ static void store(__nv_bfloat16* p, const float (&f)[8]) { *reinterpret_cast<uint4*>(p) = pack8(f); }
+};
+template <>
+struct Vec<4> {
+  __device__ static void load(const __nv_bfloat16* p, float (&f)[4]) {
+    const uint2 v = *reinterpret_cast<const uint2*>(p);
+    f[0] = __uint_as_float(v.x << 16);
+    f[1] = __uint_as_float(v.x & 0xFFFF0000u);
+    f[2] = __uint_as_float(v.y << 16);
+    f[3] = __uint_as_float(v.y & 0xFFFF0000u);
+  }
+  __device__ static void store(__nv_bfloat16* p, const float (&f)[4]) {
+    *reinterpret_cast<uint2*>(p) = make_uint2(pack2(f[0], f[1]), pack2(f[2], f[3]));
+  }
+};
 
 struct RowTiling {
   int cg, rpp, chunks, rows_per_chunk;
 };
 
-RowTiling tiling_for(int m, int c) {
+RowTiling tiling_for(int m, int c, int v) {
   RowTiling t;
-  t.cg = c / 8;
+  t.cg = c / v;
   t.rpp = std::max(1, kThreads / t.cg);
-  const int target = 148 * 4;
-  int rpc = std::max(t.rpp, (m + target - 1) / target);
-  rpc = (rpc + t.rpp - 1) / t.rpp * t.rpp;
-  t.rows_per_chunk = rpc;
-  t.chunks = (m + rpc - 1) / rpc;
+  const int target = 148 * 2;
+  const int passes = (m + t.rpp - 1) / t.rpp;
+  const int chunks = std::max(1, std::min(target, passes));
+  t.rows_per_chunk = (passes + chunks - 1) / chunks * t.rpp;
+  t.chunks = (m + t.rows_per_chunk - 1) / t.rows_per_chunk;
   return t;
 }
 
-// CTA-level fixed-order reduction of NV*8 floats per thread into partial[chunk][NV][C].
-template <int NV>
-__device__ void cta_reduce_store(float (&acc)[NV][8], int cg, int rpp, int C, float* __restrict__ partial) {
-  __shared__ float sm[kThreads * NV * 8];
+int apply_grid(int m, int rpp) { return std::max(1, std::min((m + rpp - 1) / rpp, 148 * 8)); }
+
+// CTA-level fixed-order reduction of NV*V floats per thread into partial[chunk][NV][C].
+template <int NV, int V>
+__device__ void cta_reduce_store(float (&acc)[NV][V], int cg, int rpp, int C, float* __restrict__ partial) {
+  __shared__ float sm[kThreads * NV * V];
   const int t = threadIdx.x;
 #pragma unroll
   for (int v = 0; v < NV; ++v)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) sm[(v * 8 + j) * kThreads + t] = acc[v][j];
+    for (int j = 0; j < V; ++j) sm[(v * V + j) * kThreads + t] = acc[v][j];
   __syncthreads();
-  // thread t < cg*8*NV reduces one (v, channel) over the rpp row slots in order
-  for (int o = t; o < NV * cg * 8; o += kThreads) {
-    const int v = o / (cg * 8);
-    const int rem = o - v * cg * 8;
-    const int g = rem / 8;
-    const int j = rem - g * 8;
+  for (int o = t; o < NV * cg * V; o += kThreads) {
+    const int v = o / (cg * V);
+    const int rem = o - v * cg * V;
+    const int g = rem / V;
+    const int j = rem - g * V;
     float s = 0.0f;
-    for (int r = 0; r < rpp; ++r) s += sm[(v * 8 + j) * kThreads + r * cg + g];
-    partial[(static_cast<size_t>(blockIdx.x) * NV + v) * C + g * 8 + j] = s;
+    for (int r = 0; r < rpp; ++r) s += sm[(v * V + j) * kThreads + r * cg + g];
+    partial[(static_cast<size_t>(blockIdx.x) * NV + v) * C + g * V + j] = s;
   }
 }
 
-// Fixed-order parallel sum of partial[chunk][NV][C] over chunks for 32 consecutive
-// (v, c) outputs per CTA: warp w sums chunks [w*per, (w+1)*per) (lanes = 32
-// consecutive outputs, coalesced), then the 8 warp partials are added in warp order.
-// Deterministic for a given (chunks, C).  Returns the double sum in `out` for lane
-// outputs o = blockIdx.x*32 + lane (valid when o < NV*C), visible to warp 0.
 constexpr int kFinWarps = 8;
 
+// fp64 sum over chunks of partial[chunk][NV][C] for output o = v*C + c: one warp per output,
+// lane l adds chunks l, l+32, ... (independent loads), then a fixed xor-shuffle tree.
+// Deterministic for a given (chunks, C); every lane returns the total.
 template <int NV>
-__device__ __forceinline__ double sum_over_chunks(const float* __restrict__ partial, int chunks, int C, int o) {
-  __shared__ double sm[kFinWarps][32];
+__device__ __forceinline__ double warp_sum_chunks(const float* __restrict__ partial, int chunks, int C, int o) {
   const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
+  const int v = o / C;
+  const int c = o - v * C;
+  const float* base = partial + static_cast<size_t>(v) * C + c;
+  const size_t stride = static_cast<size_t>(NV) * C;
   double s = 0.0;
-  if (o < NV * C) {
-    const int v = o / C;
-    const int c = o - v * C;
-    const int per = (chunks + kFinWarps - 1) / kFinWarps;
-    const int b0 = warp * per;
-    const int b1 = min(chunks, b0 + per);
-    for (int b = b0; b < b1; ++b) s += partial[(static_cast<size_t>(b) * NV + v) * C + c];
-  }
-  sm[warp][lane] = s;
-  __syncthreads();
-  double t = 0.0;
-  if (warp == 0) {
+  for (int b = lane; b < chunks; b += 32) s += base[b * stride];
 #pragma unroll
-    for (int w = 0; w < kFinWarps; ++w) t += sm[w][lane];
-  }
-  return t;
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  return s;
 }
 
-// fixed-order sum of n floats by one CTA of kFinWarps*32 threads
+// fixed-order sum of n floats by one CTA of kFinWarps warps (strided per-thread sums,
+// xor-shuffle tree per warp, warps added in order by thread 0).
 __device__ __forceinline__ double cta_sum(const float* __restrict__ v, int n) {
-  __shared__ double sm[kFinWarps * 32];
+  __shared__ double sm[kFinWarps];
   double s = 0.0;
-  const int per = (n + blockDim.x - 1) / blockDim.x;
-  const int b0 = threadIdx.x * per;
-  const int b1 = min(n, b0 + per);
-  for (int i = b0; i < b1; ++i) s += v[i];
-  sm[threadIdx.x] = s;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += v[i];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
   __syncthreads();
   double t = 0.0;
   if (threadIdx.x == 0)
-    for (int i = 0; i < static_cast<int>(blockDim.x); ++i) t += sm[i];
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += sm[w];
   return t;
 }
 
 // -- BN statistics
-__global__ void bn_stats_partial_kernel(const __nv_bfloat16* __restrict__ y, int m, int C, int rows_per_chunk, int cg,
-                                        int rpp, float* __restrict__ partial) {
+template <int V>
+__global__ void __launch_bounds__(kThreads) bn_stats_partial_kernel(const __nv_bfloat16* __restrict__ y, int m, int C,
+                                                                    int rows_per_chunk, int cg, int rpp,
+                                                                    float* __restrict__ partial) {
   const int g = threadIdx.x % cg;
   const int slot = threadIdx.x / cg;
-  float acc[2][8] = {};
+  float acc[2][V] = {};
   if (slot < rpp) {
     const int r0 = blockIdx.x * rows_per_chunk;
     const int r1 = min(m, r0 + rows_per_chunk);
-    for (int r = r0 + slot; r < r1; r += rpp) {
-      float f[8];
-      unpack8(*reinterpret_cast<const uint4*>(y + static_cast<size_t>(r) * C + g * 8), f);
+    const __nv_bfloat16* p = y + static_cast<size_t>(r0 + slot) * C + g * V;
+#pragma unroll 4
+    for (int r = r0 + slot; r < r1; r += rpp, p += static_cast<size_t>(rpp) * C) {
+      float f[V];
+      Vec<V>::load(p, f);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < V; ++j) {
         acc[0][j] += f[j];
         acc[1][j] += f[j] * f[j];
       }
     }
   }
-  cta_reduce_store<2>(acc, cg, rpp, C, partial);
+  cta_reduce_store<2, V>(acc, cg, rpp, C, partial);
 }
 
-// grid: ceil(C/32) CTAs of kFinWarps*32 threads; the (s1, s2) pair of channel c is
-// summed by two independent fixed-order passes (v = 0 and v = 1).
+// grid: ceil(C / 8) CTAs of 8 warps; warp = channel.
 __global__ void bn_stats_finalize_kernel(const float* __restrict__ partial, int chunks, int C, int m,
                                          float* __restrict__ mean_rstd) {
-  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
-  const double s1 = sum_over_chunks<2>(partial, chunks, C, c);
-  __syncthreads();
-  const double s2 = sum_over_chunks<2>(partial, chunks, C, C + c);
-  if ((threadIdx.x >> 5) == 0 && c < C) {
+  const int c = blockIdx.x * kFinWarps + (threadIdx.x >> 5);
+  if (c >= C) return;
+  const double s1 = warp_sum_chunks<2>(partial, chunks, C, c);
+  const double s2 = warp_sum_chunks<2>(partial, chunks, C, C + c);
+  if ((threadIdx.x & 31) == 0) {
     const double mu = s1 / static_cast<double>(m);
     const double var = s2 / static_cast<double>(m) - mu * mu;
     mean_rstd[c] = static_cast<float>(mu);
@@ -262,23 +279,37 @@ __global__ void bn_stats_finalize_kernel(const float* __restrict__ partial, int 
 }
 
 // -- BN apply + ReLU: a = bf16(relu(fmaf(gamma, (y-mu)*rstd, beta)))
-__global__ void bn_apply_relu_kernel(const __nv_bfloat16* __restrict__ y, const float* __restrict__ mean_rstd,
-                                     const float* __restrict__ gamma, const float* __restrict__ beta,
-                                     __nv_bfloat16* __restrict__ a, int m, int C) {
-  const int cg = C / 8;
-  const long long total = static_cast<long long>(m) * cg;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int c0 = static_cast<int>(i % cg) * 8;
-    float f[8];
-    unpack8(reinterpret_cast<const uint4*>(y)[i], f);
+template <int V>
+__global__ void __launch_bounds__(kThreads) bn_apply_relu_kernel(const __nv_bfloat16* __restrict__ y,
+                                                                 const float* __restrict__ mean_rstd,
+                                                                 const float* __restrict__ gamma,
+                                                                 const float* __restrict__ beta,
+                                                                 __nv_bfloat16* __restrict__ a, int m, int C, int cg,
+                                                                 int rpp) {
+  const int g = threadIdx.x % cg;
+  const int slot = threadIdx.x / cg;
+  if (slot >= rpp) return;
+  const int c0 = g * V;
+  float mu[V], rs[V], ga[V], be[V];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float xh = (f[j] - mean_rstd[c0 + j]) * mean_rstd[C + c0 + j];
-      const float z = fmaf(gamma[c0 + j], xh, beta[c0 + j]);
+  for (int j = 0; j < V; ++j) {
+    mu[j] = mean_rstd[c0 + j];
+    rs[j] = mean_rstd[C + c0 + j];
+    ga[j] = gamma[c0 + j];
+    be[j] = beta[c0 + j];
+  }
+  const int step = gridDim.x * rpp;
+#pragma unroll 2
+  for (int r = blockIdx.x * rpp + slot; r < m; r += step) {
+    const size_t off = static_cast<size_t>(r) * C + c0;
+    float f[V];
+    Vec<V>::load(y + off, f);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const float z = fmaf(ga[j], (f[j] - mu[j]) * rs[j], be[j]);
       f[j] = z > 0.0f ? z : 0.0f;
     }
-    reinterpret_cast<uint4*>(a)[i] = pack8(f);
+    Vec<V>::store(a + off, f);
   }
 }
 
@@ -297,38 +328,63 @@ struct LossParams {
   float gscale;
 };
 
-__device__ __forceinline__ void loss_point(const LossParams& p, size_t off, int c0, float (&g)[8], float (&xh2)[8],
-                                           float (&xhs)[8], float (&d)[8]) {
-  float fy2[8], fys[8], ft[8];
-  unpack8(*reinterpret_cast<const uint4*>(p.y2 + off), fy2);
-  unpack8(*reinterpret_cast<const uint4*>(p.ys + off), fys);
-  unpack8(*reinterpret_cast<const uint4*>(p.t + off), ft);
+template <int V>
+struct LossChan {  // per-channel constants of the loss kernels, held in registers
+  float m2[V], r2[V], g2[V], b2[V], ms[V], rs[V], gs[V], bs[V];
+  __device__ void load(const LossParams& p, int c0) {
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const int c = c0 + j;
-    xh2[j] = (fy2[j] - p.st2[c]) * p.st2[p.C + c];
-    xhs[j] = (fys[j] - p.sts[c]) * p.sts[p.C + c];
-    const float z = fmaf(p.g2[c], xh2[j], p.b2[c]) + fmaf(p.gs[c], xhs[j], p.bs[c]);
-    const float sv = z > 0.0f ? z : 0.0f;
-    d[j] = sv - ft[j];
-    g[j] = z > 0.0f ? d[j] * p.gscale : 0.0f;
+    for (int j = 0; j < V; ++j) {
+      const int c = c0 + j;
+      m2[j] = p.st2[c];
+      r2[j] = p.st2[p.C + c];
+      ms[j] = p.sts[c];
+      rs[j] = p.sts[p.C + c];
+      g2[j] = p.g2[c];
+      b2[j] = p.b2[c];
+      gs[j] = p.gs[c];
+      bs[j] = p.bs[c];
+    }
   }
-}
+  // g (dL/dz), xhat2, xhatsc, d = s - t for V channels of one row
+  __device__ __forceinline__ void point(const LossParams& p, size_t off, float (&g)[V], float (&xh2)[V],
+                                        float (&xhs)[V], float (&d)[V]) const {
+    float fy2[V], fys[V], ft[V];
+    Vec<V>::load(p.y2 + off, fy2);
+    Vec<V>::load(p.ys + off, fys);
+    Vec<V>::load(p.t + off, ft);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      xh2[j] = (fy2[j] - m2[j]) * r2[j];
+      xhs[j] = (fys[j] - ms[j]) * rs[j];
+      const float z = fmaf(g2[j], xh2[j], b2[j]) + fmaf(gs[j], xhs[j], bs[j]);
+      const float sv = z > 0.0f ? z : 0.0f;
+      d[j] = sv - ft[j];
+      g[j] = z > 0.0f ? d[j] * p.gscale : 0.0f;
+    }
+  }
+};
 
-__global__ void loss_partial_kernel(const LossParams p, int rows_per_chunk, int cg, int rpp,
-                                    float* __restrict__ partial, float* __restrict__ loss_partial) {
+constexpr int kLossV = 4;
+
+__global__ void __launch_bounds__(kThreads) loss_partial_kernel(const LossParams p, int rows_per_chunk, int cg, int rpp,
+                                                                float* __restrict__ partial,
+                                                                float* __restrict__ loss_partial) {
+  constexpr int V = kLossV;
   const int gi = threadIdx.x % cg;
   const int slot = threadIdx.x / cg;
-  float acc[3][8] = {};
+  float acc[3][V] = {};
   float lsum = 0.0f;
   if (slot < rpp) {
+    LossChan<V> ch;
+    ch.load(p, gi * V);
     const int r0 = blockIdx.x * rows_per_chunk;
     const int r1 = min(p.m, r0 + rows_per_chunk);
+#pragma unroll 2
     for (int r = r0 + slot; r < r1; r += rpp) {
-      float g[8], xh2[8], xhs[8], d[8];
-      loss_point(p, static_cast<size_t>(r) * p.C + gi * 8, gi * 8, g, xh2, xhs, d);
+      float g[V], xh2[V], xhs[V], d[V];
+      ch.point(p, static_cast<size_t>(r) * p.C + gi * V, g, xh2, xhs, d);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < V; ++j) {
         lsum += d[j] * d[j];
         acc[0][j] += g[j];
         acc[1][j] += g[j] * xh2[j];
@@ -336,20 +392,21 @@ __global__ void loss_partial_kernel(const LossParams p, int rows_per_chunk, int 
       }
     }
   }
-  // loss: block reduction in fixed order
-  __shared__ float lred[kThreads];
-  lred[threadIdx.x] = lsum;
-  cta_reduce_store<3>(acc, cg, rpp, p.C, partial);
+  __shared__ float lred[kThreads / 32];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, off);
+  if ((threadIdx.x & 31) == 0) lred[threadIdx.x >> 5] = lsum;
+  cta_reduce_store<3, V>(acc, cg, rpp, p.C, partial);
   __syncthreads();
   if (threadIdx.x == 0) {
     float s = 0.0f;
-    for (int i = 0; i < kThreads; ++i) s += lred[i];
+    for (int i = 0; i < kThreads / 32; ++i) s += lred[i];
     loss_partial[blockIdx.x] = s;
   }
 }
 
-// red (double [3C]) -> grads of gamma2/beta2/gammasc/betasc, float copies; the last
-// CTA (blockIdx.x == gridDim.x-1, beyond the channel CTAs) sums the loss partials.
+// red (double [3C]) -> grads of gamma2/beta2/gammasc/betasc, float copies; warp = output o in
+// [0, 3C); the last CTA sums the loss partials.
 __global__ void loss_finalize_kernel(const float* __restrict__ partial, const float* __restrict__ loss_partial,
                                      int chunks, int C, double norm, float* __restrict__ red_f,
                                      float* __restrict__ dg2, float* __restrict__ db2, float* __restrict__ dgs,
@@ -359,9 +416,10 @@ __global__ void loss_finalize_kernel(const float* __restrict__ partial, const fl
     if (threadIdx.x == 0) *loss_out = l / norm;
     return;
   }
-  const int o = blockIdx.x * 32 + (threadIdx.x & 31);  // o in [0, 3C)
-  const double sv = sum_over_chunks<3>(partial, chunks, C, o);
-  if ((threadIdx.x >> 5) == 0 && o < 3 * C) {
+  const int o = blockIdx.x * kFinWarps + (threadIdx.x >> 5);
+  if (o >= 3 * C) return;
+  const double sv = warp_sum_chunks<3>(partial, chunks, C, o);
+  if ((threadIdx.x & 31) == 0) {
     const int v = o / C;
     const int c = o - v * C;
     const float f = static_cast<float>(sv);
@@ -377,63 +435,87 @@ __global__ void loss_finalize_kernel(const float* __restrict__ partial, const fl
   }
 }
 
-__global__ void loss_bwd_apply_kernel(const LossParams p, const float* __restrict__ red_f,
-                                      __nv_bfloat16* __restrict__ dy2, __nv_bfloat16* __restrict__ dys) {
-  const int cg = p.C / 8;
-  const long long total = static_cast<long long>(p.m) * cg;
+__global__ void __launch_bounds__(kThreads) loss_bwd_apply_kernel(const LossParams p, const float* __restrict__ red_f,
+                                                                  int cg, int rpp, __nv_bfloat16* __restrict__ dy2,
+                                                                  __nv_bfloat16* __restrict__ dys) {
+  constexpr int V = kLossV;
+  const int gi = threadIdx.x % cg;
+  const int slot = threadIdx.x / cg;
+  if (slot >= rpp) return;
+  const int c0 = gi * V;
   const float mf = static_cast<float>(p.m);
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int c0 = static_cast<int>(i % cg) * 8;
-    float g[8], xh2[8], xhs[8], d[8], o2[8], os[8];
-    loss_point(p, static_cast<size_t>(i) * 8, c0, g, xh2, xhs, d);
+  LossChan<V> ch;
+  ch.load(p, c0);
+  float sg[V], sgx2[V], sgxs[V], k2[V], ks[V];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int c = c0 + j;
-      const float sg = red_f[c];
-      const float k2 = (p.g2[c] * p.st2[p.C + c]) / mf;
-      const float ks = (p.gs[c] * p.sts[p.C + c]) / mf;
-      const float base = fmaf(mf, g[j], -sg);
-      o2[j] = k2 * fmaf(-xh2[j], red_f[p.C + c], base);
-      os[j] = ks * fmaf(-xhs[j], red_f[2 * p.C + c], base);
+  for (int j = 0; j < V; ++j) {
+    const int c = c0 + j;
+    sg[j] = red_f[c];
+    sgx2[j] = red_f[p.C + c];
+    sgxs[j] = red_f[2 * p.C + c];
+    k2[j] = (ch.g2[j] * ch.r2[j]) / mf;
+    ks[j] = (ch.gs[j] * ch.rs[j]) / mf;
+  }
+  const int step = gridDim.x * rpp;
+#pragma unroll 2
+  for (int r = blockIdx.x * rpp + slot; r < p.m; r += step) {
+    const size_t off = static_cast<size_t>(r) * p.C + c0;
+    float g[V], xh2[V], xhs[V], d[V], o2[V], os[V];
+    ch.point(p, off, g, xh2, xhs, d);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const float base = fmaf(mf, g[j], -sg[j]);
+      o2[j] = k2[j] * fmaf(-xh2[j], sgx2[j], base);
+      os[j] = ks[j] * fmaf(-xhs[j], sgxs[j], base);
     }
-    reinterpret_cast<uint4*>(dy2)[i] = pack8(o2);
-    reinterpret_cast<uint4*>(dys)[i] = pack8(os);
+    Vec<V>::store(dy2 + off, o2);
+    Vec<V>::store(dys + off, os);
   }
 }
 
 // -- BN backward (first BN of the unit): reductions and apply
-__global__ void bn_bwd_partial_kernel(const __nv_bfloat16* __restrict__ gin, const __nv_bfloat16* __restrict__ y,
-                                      const float* __restrict__ st, int m, int C, int rows_per_chunk, int cg, int rpp,
-                                      float* __restrict__ partial) {
+template <int V>
+__global__ void __launch_bounds__(kThreads) bn_bwd_partial_kernel(const __nv_bfloat16* __restrict__ gin,
+                                                                  const __nv_bfloat16* __restrict__ y,
+                                                                  const float* __restrict__ st, int m, int C,
+                                                                  int rows_per_chunk, int cg, int rpp,
+                                                                  float* __restrict__ partial) {
   const int gi = threadIdx.x % cg;
   const int slot = threadIdx.x / cg;
-  float acc[2][8] = {};
+  float acc[2][V] = {};
   if (slot < rpp) {
+    const int c0 = gi * V;
+    float mu[V], rs[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      mu[j] = st[c0 + j];
+      rs[j] = st[C + c0 + j];
+    }
     const int r0 = blockIdx.x * rows_per_chunk;
     const int r1 = min(m, r0 + rows_per_chunk);
+#pragma unroll 2
     for (int r = r0 + slot; r < r1; r += rpp) {
-      const size_t off = static_cast<size_t>(r) * C + gi * 8;
-      float fg[8], fy[8];
-      unpack8(*reinterpret_cast<const uint4*>(gin + off), fg);
-      unpack8(*reinterpret_cast<const uint4*>(y + off), fy);
+      const size_t off = static_cast<size_t>(r) * C + c0;
+      float fg[V], fy[V];
+      Vec<V>::load(gin + off, fg);
+      Vec<V>::load(y + off, fy);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int c = gi * 8 + j;
-        const float xh = (fy[j] - st[c]) * st[C + c];
+      for (int j = 0; j < V; ++j) {
+        const float xh = (fy[j] - mu[j]) * rs[j];
         acc[0][j] += fg[j];
         acc[1][j] += fg[j] * xh;
       }
     }
   }
-  cta_reduce_store<2>(acc, cg, rpp, C, partial);
+  cta_reduce_store<2, V>(acc, cg, rpp, C, partial);
 }
 
 __global__ void bn_bwd_finalize_kernel(const float* __restrict__ partial, int chunks, int C, float* __restrict__ red_f,
                                        float* __restrict__ dgamma, float* __restrict__ dbeta) {
-  const int o = blockIdx.x * 32 + (threadIdx.x & 31);  // o in [0, 2C)
-  const double sv = sum_over_chunks<2>(partial, chunks, C, o);
-  if ((threadIdx.x >> 5) == 0 && o < 2 * C) {
+  const int o = blockIdx.x * kFinWarps + (threadIdx.x >> 5);  // o in [0, 2C)
+  if (o >= 2 * C) return;
+  const double sv = warp_sum_chunks<2>(partial, chunks, C, o);
+  if ((threadIdx.x & 31) == 0) {
     const int v = o / C;
     const int c = o - v * C;
     const float f = static_cast<float>(sv);
@@ -445,26 +527,41 @@ __global__ void bn_bwd_finalize_kernel(const float* __restrict__ partial, int ch
   }
 }
 
-__global__ void bn_bwd_apply_kernel(const __nv_bfloat16* __restrict__ gin, const __nv_bfloat16* __restrict__ y,
-                                    const float* __restrict__ st, const float* __restrict__ gamma,
-                                    const float* __restrict__ red_f, int m, int C, __nv_bfloat16* __restrict__ dy) {
-  const int cg = C / 8;
-  const long long total = static_cast<long long>(m) * cg;
+template <int V>
+__global__ void __launch_bounds__(kThreads) bn_bwd_apply_kernel(const __nv_bfloat16* __restrict__ gin,
+                                                                const __nv_bfloat16* __restrict__ y,
+                                                                const float* __restrict__ st,
+                                                                const float* __restrict__ gamma,
+                                                                const float* __restrict__ red_f, int m, int C, int cg,
+                                                                int rpp, __nv_bfloat16* __restrict__ dy) {
+  const int gi = threadIdx.x % cg;
+  const int slot = threadIdx.x / cg;
+  if (slot >= rpp) return;
+  const int c0 = gi * V;
   const float mf = static_cast<float>(m);
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int c0 = static_cast<int>(i % cg) * 8;
-    float fg[8], fy[8], o[8];
-    unpack8(reinterpret_cast<const uint4*>(gin)[i], fg);
-    unpack8(reinterpret_cast<const uint4*>(y)[i], fy);
+  float mu[V], rs[V], k1[V], sg[V], sgx[V];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int c = c0 + j;
-      const float xh = (fy[j] - st[c]) * st[C + c];
-      const float k1 = (gamma[c] * st[C + c]) / mf;
-      o[j] = k1 * fmaf(-xh, red_f[C + c], fmaf(mf, fg[j], -red_f[c]));
+  for (int j = 0; j < V; ++j) {
+    const int c = c0 + j;
+    mu[j] = st[c];
+    rs[j] = st[C + c];
+    k1[j] = (gamma[c] * rs[j]) / mf;
+    sg[j] = red_f[c];
+    sgx[j] = red_f[C + c];
+  }
+  const int step = gridDim.x * rpp;
+#pragma unroll 2
+  for (int r = blockIdx.x * rpp + slot; r < m; r += step) {
+    const size_t off = static_cast<size_t>(r) * C + c0;
+    float fg[V], fy[V], o[V];
+    Vec<V>::load(gin + off, fg);
+    Vec<V>::load(y + off, fy);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const float xh = (fy[j] - mu[j]) * rs[j];
+      o[j] = k1[j] * fmaf(-xh, sgx[j], fmaf(mf, fg[j], -sg[j]));
     }
-    reinterpret_cast<uint4*>(dy)[i] = pack8(o);
+    Vec<V>::store(dy + off, o);
   }
 }
 
@@ -501,8 +598,10 @@ inline int ok(cudaError_t e) { return e == cudaSuccess ? PBDK_OK : PBDK_ECUDA; }
 }  // namespace
 
 size_t reduce_workspace_floats(int m, int c, int nv) {
-  const RowTiling t = tiling_for(m, c);
-  return static_cast<size_t>(t.chunks) * nv * c + t.chunks;
+  const RowTiling t = tiling_for(m, c, 4);  // the finest tiling any of the reductions uses
+  const RowTiling t8 = tiling_for(m, c, 8);
+  const int chunks = std::max(t.chunks, t8.chunks);
+  return static_cast<size_t>(chunks) * nv * c + chunks;
 }
 
 int philox_image(void* x, int n, long long first, const long long* counter, int gb, uint32_t seed, cudaStream_t st) {
@@ -530,48 +629,52 @@ int fill(float* dst, size_t n, float v, cudaStream_t st) {
 }
 
 int bn_stats(const void* y, int m, int c, float* ws, float* mean_rstd, cudaStream_t st) {
-  if (c % 8 != 0 || c > 8 * kThreads) return PBDK_EINVAL;
-  const RowTiling t = tiling_for(m, c);
-  bn_stats_partial_kernel<<<t.chunks, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(y), m, c,
-                                                         t.rows_per_chunk, t.cg, t.rpp, ws);
-  bn_stats_finalize_kernel<<<(c + 31) / 32, kFinWarps * 32, 0, st>>>(ws, t.chunks, c, m, mean_rstd);
+  if (c % 8 != 0 || c / 8 > kThreads) return PBDK_EINVAL;
+  const RowTiling t = tiling_for(m, c, 8);
+  bn_stats_partial_kernel<8><<<t.chunks, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(y), m, c,
+                                                            t.rows_per_chunk, t.cg, t.rpp, ws);
+  bn_stats_finalize_kernel<<<(c + kFinWarps - 1) / kFinWarps, kFinWarps * 32, 0, st>>>(ws, t.chunks, c, m, mean_rstd);
   return ok(cudaGetLastError());
 }
 
 int bn_apply_relu(const void* y, const float* mean_rstd, const float* gamma, const float* beta, void* a, int m, int c,
                   cudaStream_t st) {
-  bn_apply_relu_kernel<<<grid_for(static_cast<long long>(m) * c / 8), kThreads, 0, st>>>(
-      static_cast<const __nv_bfloat16*>(y), mean_rstd, gamma, beta, static_cast<__nv_bfloat16*>(a), m, c);
+  if (c % 8 != 0 || c / 8 > kThreads) return PBDK_EINVAL;
+  const RowTiling t = tiling_for(m, c, 8);
+  bn_apply_relu_kernel<8><<<apply_grid(m, t.rpp), kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(y), mean_rstd,
+                                                                     gamma, beta, static_cast<__nv_bfloat16*>(a), m, c,
+                                                                     t.cg, t.rpp);
   return ok(cudaGetLastError());
 }
 
 int mse_bn_loss(const MseArgs& a, cudaStream_t st) {
-  if (a.c % 8 != 0) return PBDK_EINVAL;
+  if (a.c % kLossV != 0 || a.c / kLossV > kThreads) return PBDK_EINVAL;
   LossParams p{static_cast<const __nv_bfloat16*>(a.y2), static_cast<const __nv_bfloat16*>(a.ysc),
                static_cast<const __nv_bfloat16*>(a.t), a.stats2, a.statssc, a.gamma2, a.beta2, a.gammasc, a.betasc,
                a.m, a.c, a.gscale};
-  const RowTiling t = tiling_for(a.m, a.c);
+  const RowTiling t = tiling_for(a.m, a.c, kLossV);
   float* partial = a.ws;
   float* loss_partial = a.ws + static_cast<size_t>(t.chunks) * 3 * a.c;
   loss_partial_kernel<<<t.chunks, kThreads, 0, st>>>(p, t.rows_per_chunk, t.cg, t.rpp, partial, loss_partial);
-  loss_finalize_kernel<<<(3 * a.c + 31) / 32 + 1, kFinWarps * 32, 0, st>>>(partial, loss_partial, t.chunks, a.c, a.norm, a.red,
-                                                          a.dgamma2, a.dbeta2, a.dgammasc, a.dbetasc, a.loss);
-  loss_bwd_apply_kernel<<<grid_for(static_cast<long long>(a.m) * a.c / 8), kThreads, 0, st>>>(
-      p, a.red, static_cast<__nv_bfloat16*>(a.dy2), static_cast<__nv_bfloat16*>(a.dysc));
+  loss_finalize_kernel<<<(3 * a.c + kFinWarps - 1) / kFinWarps + 1, kFinWarps * 32, 0, st>>>(
+      partial, loss_partial, t.chunks, a.c, a.norm, a.red, a.dgamma2, a.dbeta2, a.dgammasc, a.dbetasc, a.loss);
+  loss_bwd_apply_kernel<<<apply_grid(a.m, t.rpp), kThreads, 0, st>>>(p, a.red, t.cg, t.rpp,
+                                                                     static_cast<__nv_bfloat16*>(a.dy2),
+                                                                     static_cast<__nv_bfloat16*>(a.dysc));
   return ok(cudaGetLastError());
 }
 
 int bn_bwd(const void* g, const void* y, const float* mean_rstd, const float* gamma, int m, int c, float* ws,
            float* red, float* dgamma, float* dbeta, void* dy, cudaStream_t st) {
-  if (c % 8 != 0) return PBDK_EINVAL;
-  const RowTiling t = tiling_for(m, c);
-  bn_bwd_partial_kernel<<<t.chunks, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(g),
-                                                       static_cast<const __nv_bfloat16*>(y), mean_rstd, m, c,
-                                                       t.rows_per_chunk, t.cg, t.rpp, ws);
-  bn_bwd_finalize_kernel<<<(2 * c + 31) / 32, kFinWarps * 32, 0, st>>>(ws, t.chunks, c, red, dgamma, dbeta);
-  bn_bwd_apply_kernel<<<grid_for(static_cast<long long>(m) * c / 8), kThreads, 0, st>>>(
-      static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(y), mean_rstd, gamma, red, m, c,
-      static_cast<__nv_bfloat16*>(dy));
+  if (c % 8 != 0 || c / 8 > kThreads) return PBDK_EINVAL;
+  const RowTiling t = tiling_for(m, c, 8);
+  bn_bwd_partial_kernel<8><<<t.chunks, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(g),
+                                                          static_cast<const __nv_bfloat16*>(y), mean_rstd, m, c,
+                                                          t.rows_per_chunk, t.cg, t.rpp, ws);
+  bn_bwd_finalize_kernel<<<(2 * c + kFinWarps - 1) / kFinWarps, kFinWarps * 32, 0, st>>>(ws, t.chunks, c, red, dgamma, dbeta);
+  bn_bwd_apply_kernel<8><<<apply_grid(m, t.rpp), kThreads, 0, st>>>(
+      static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(y), mean_rstd, gamma, red, m, c, t.cg,
+      t.rpp, static_cast<__nv_bfloat16*>(dy));
   return ok(cudaGetLastError());
 }
 

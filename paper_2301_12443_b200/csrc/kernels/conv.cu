@@ -629,12 +629,20 @@ __global__ void split_reduce_kernel(const float4* __restrict__ ws, float4* __res
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
     float4 acc = ws[i];
-    for (int s = 1; s < splits; ++s) {
+    int s = 1;
+    for (; s + 3 < splits; s += 4) {  // 4 loads in flight, added in split order
+      const float4 v0 = ws[s * n4 + i];
+      const float4 v1 = ws[(s + 1) * n4 + i];
+      const float4 v2 = ws[(s + 2) * n4 + i];
+      const float4 v3 = ws[(s + 3) * n4 + i];
+      acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
+      acc.x += v1.x; acc.y += v1.y; acc.z += v1.z; acc.w += v1.w;
+      acc.x += v2.x; acc.y += v2.y; acc.z += v2.z; acc.w += v2.w;
+      acc.x += v3.x; acc.y += v3.y; acc.z += v3.z; acc.w += v3.w;
+    }
+    for (; s < splits; ++s) {
       const float4 v = ws[s * n4 + i];
-      acc.x += v.x;
-      acc.y += v.y;
-      acc.z += v.z;
-      acc.w += v.w;
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
     }
     dw[i] = acc;
   }
@@ -935,8 +943,8 @@ int wgrad_run(const WgradPlan& plan, cudaStream_t stream) {
   if (plan.launch(plan, stream) != cudaSuccess) return PBDK_ECUDA;
   if (plan.splits > 1) {
     const size_t n4 = plan.slab / 4;
-    const int blocks = static_cast<int>(std::min<size_t>((n4 + 255) / 256, 148 * 8));
-    split_reduce_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<const float4*>(plan.args.out),
+    const int blocks = static_cast<int>(std::max<size_t>(1, std::min<size_t>((n4 + 127) / 128, 148 * 8)));
+    split_reduce_kernel<<<blocks, 128, 0, stream>>>(reinterpret_cast<const float4*>(plan.args.out),
                                                     reinterpret_cast<float4*>(plan.dw), n4, plan.splits);
     if (cudaGetLastError() != cudaSuccess) return PBDK_ECUDA;
   }
