@@ -151,6 +151,14 @@ struct SBlock {
   float *st1, *st2, *sts, *red, *red1;
   pbdk::FpropPlan p_conv1, p_sc, p_conv2, p_dgrad;
   pbdk::WgradPlan p_w2, p_wsc, p_w1;
+  // per-block scratch + stream: student blocks only depend on teacher outputs, so each runs
+  // on its own stream as soon as its teacher block is done (overlaps teacher k+1 and the
+  // other student blocks; the late blocks alone do not fill 148 SMs).
+  float* rws = nullptr;
+  void* wws = nullptr;
+  size_t wws_bytes = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t done = nullptr;
 };
 
 }  // namespace
@@ -233,37 +241,44 @@ class Partition {
       if (timing_) cuda(cudaEventRecord(ev_t_[2 * i], st), "event");
       for (TConv& c : tblocks_[i].convs) check(pbdk::fprop_run(c.plan, st), "teacher conv");
       if (timing_) cuda(cudaEventRecord(ev_t_[2 * i + 1], st), "event");
+      cuda(cudaEventRecord(tdone_[i], st), "event");
     }
   }
 
-  void student_step(cudaStream_t st) {
+  // Student block k runs on its own stream once teacher block k is done (event recorded by
+  // teacher_forward); the caller's stream joins all of them before returning.
+  void student_step(cudaStream_t caller) {
     for (size_t i = 0; i < sblocks_.size(); ++i) {
       SBlock& s = sblocks_[i];
+      cudaStream_t st = s.stream;
+      cuda(cudaStreamWaitEvent(st, tdone_[i], 0), "wait teacher");
       if (timing_) cuda(cudaEventRecord(ev_s_[2 * i], st), "event");
       const float* p = params_ + s.base;
       float* g = grads_ + s.base;
       const int m = n_ * s.hout * s.hout;
       check(pbdk::fprop_run(s.p_conv1, st), "conv1");
       check(pbdk::fprop_run(s.p_sc, st), "shortcut");
-      check(pbdk::bn_stats(s.y1, m, s.mid, rws_, s.st1, st), "bn1 stats");
+      check(pbdk::bn_stats(s.y1, m, s.mid, s.rws, s.st1, st), "bn1 stats");
       check(pbdk::bn_apply_relu(s.y1, s.st1, p + s.lay.g1, p + s.lay.b1, s.a1, m, s.mid, st), "bn1 apply");
       check(pbdk::fprop_run(s.p_conv2, st), "conv2");
-      check(pbdk::bn_stats(s.y2, m, s.cout, rws_, s.st2, st), "bn2 stats");
-      check(pbdk::bn_stats(s.ys, m, s.cout, rws_, s.sts, st), "bnsc stats");
+      check(pbdk::bn_stats(s.y2, m, s.cout, s.rws, s.st2, st), "bn2 stats");
+      check(pbdk::bn_stats(s.ys, m, s.cout, s.rws, s.sts, st), "bnsc stats");
       const double norm = static_cast<double>(d_.global_batch) * s.cout * s.hout * s.hout;
       pbdk::MseArgs a{s.y2, s.ys, s.target, s.st2, s.sts, p + s.lay.g2, p + s.lay.b2, p + s.lay.gsc, p + s.lay.bsc,
-                      m, s.cout, static_cast<float>(2.0 / norm), norm, rws_, s.red, g + s.lay.g2, g + s.lay.b2,
+                      m, s.cout, static_cast<float>(2.0 / norm), norm, s.rws, s.red, g + s.lay.g2, g + s.lay.b2,
                       g + s.lay.gsc, g + s.lay.bsc, losses_ + i, s.dy2, s.dys};
       check(pbdk::mse_bn_loss(a, st), "mse");
       check(pbdk::wgrad_run(s.p_w2, st), "wgrad2");
       check(pbdk::wgrad_run(s.p_wsc, st), "wgrad sc");
       check(pbdk::fprop_run(s.p_dgrad, st), "dgrad2");
-      check(pbdk::bn_bwd(s.g1, s.y1, s.st1, p + s.lay.g1, m, s.mid, rws_, s.red1, g + s.lay.g1, g + s.lay.b1, s.dy1,
+      check(pbdk::bn_bwd(s.g1, s.y1, s.st1, p + s.lay.g1, m, s.mid, s.rws, s.red1, g + s.lay.g1, g + s.lay.b1, s.dy1,
                          st),
             "bn1 bwd");
       check(pbdk::wgrad_run(s.p_w1, st), "wgrad1");
       if (timing_) cuda(cudaEventRecord(ev_s_[2 * i + 1], st), "event");
+      cuda(cudaEventRecord(s.done, st), "event");
     }
+    for (SBlock& s : sblocks_) cuda(cudaStreamWaitEvent(caller, s.done, 0), "join");
   }
 
   void apply_update(cudaStream_t st) {
@@ -365,6 +380,11 @@ class Partition {
   ~Partition() {
     if (graph_exec_ != nullptr) cudaGraphExecDestroy(graph_exec_);
     if (cap_stream_ != nullptr) cudaStreamDestroy(cap_stream_);
+    for (SBlock& s : sblocks_) {
+      if (s.stream != nullptr) cudaStreamDestroy(s.stream);
+      if (s.done != nullptr) cudaEventDestroy(s.done);
+    }
+    for (auto e : tdone_) cudaEventDestroy(e);
     for (auto e : ev_t_) cudaEventDestroy(e);
     for (auto e : ev_s_) cudaEventDestroy(e);
   }
@@ -504,18 +524,21 @@ class Partition {
     losses_ = arena_.get<double>(kBlocks * sizeof(double));
     step_ = arena_.get<long long>(sizeof(long long));
 
-    // ---- shared scratch sized for n_max
-    size_t rws = 0, wws = 0;
-    for (const SBlock& s : sblocks_) {
+    // ---- per-block scratch sized for n_max, streams and events
+    for (SBlock& s : sblocks_) {
       const int m = d_.n_max * s.hout * s.hout;
-      rws = std::max(rws, pbdk::reduce_workspace_floats(m, s.cout, 3));
-      rws = std::max(rws, pbdk::reduce_workspace_floats(m, s.mid, 3));
+      size_t rws = std::max(pbdk::reduce_workspace_floats(m, s.cout, 3), pbdk::reduce_workspace_floats(m, s.mid, 3));
+      size_t wws = 0;
       for (const pbdk_conv_desc& cd : {conv1_desc(s, d_.n_max), sc_desc(s, d_.n_max), conv2_desc(s, d_.n_max)})
         wws = std::max(wws, pbdk::wgrad_workspace_bytes(cd));
+      s.rws = arena_.get<float>(rws * sizeof(float));
+      s.wws_bytes = wws;
+      s.wws = arena_.get<void>(wws);
+      cuda(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "stream");
+      cuda(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming), "event");
     }
-    rws_ = arena_.get<float>(rws * sizeof(float));
-    wws_bytes_ = wws;
-    wws_ = arena_.get<void>(wws);
+    tdone_.resize(tblocks_.size());
+    for (auto& e : tdone_) cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   }
 
   static pbdk_conv_desc conv1_desc(const SBlock& s, int n) {
@@ -547,9 +570,9 @@ class Partition {
             "conv2 plan");
       const pbdk_conv_desc dg{n_, s.hout, s.hout, s.cout, s.mid, 3, 3, 1, 1, s.hout, s.hout};
       check(pbdk::fprop_plan(dg, s.dy2, s.w2flip, s.g1, nullptr, s.a1, PBDK_EPI_RELU_MASK, &s.p_dgrad), "dgrad plan");
-      check(pbdk::wgrad_plan(conv2_desc(s, n_), s.a1, s.dy2, g + s.lay.w2, wws_, wws_bytes_, &s.p_w2), "wgrad2 plan");
-      check(pbdk::wgrad_plan(sc_desc(s, n_), s.in, s.dys, g + s.lay.wsc, wws_, wws_bytes_, &s.p_wsc), "wgradsc plan");
-      check(pbdk::wgrad_plan(conv1_desc(s, n_), s.in, s.dy1, g + s.lay.w1, wws_, wws_bytes_, &s.p_w1), "wgrad1 plan");
+      check(pbdk::wgrad_plan(conv2_desc(s, n_), s.a1, s.dy2, g + s.lay.w2, s.wws, s.wws_bytes, &s.p_w2), "wgrad2 plan");
+      check(pbdk::wgrad_plan(sc_desc(s, n_), s.in, s.dys, g + s.lay.wsc, s.wws, s.wws_bytes, &s.p_wsc), "wgradsc plan");
+      check(pbdk::wgrad_plan(conv1_desc(s, n_), s.in, s.dy1, g + s.lay.w1, s.wws, s.wws_bytes, &s.p_w1), "wgrad1 plan");
     }
   }
 
@@ -575,9 +598,7 @@ class Partition {
   bf16* shadow_ = nullptr;
   double* losses_ = nullptr;
   long long* step_ = nullptr;
-  float* rws_ = nullptr;
-  void* wws_ = nullptr;
-  size_t wws_bytes_ = 0;
+  std::vector<cudaEvent_t> tdone_;
   std::vector<cudaEvent_t> ev_t_, ev_s_;
 };
 
