@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--batch", type=int, default=PER_GPU_BATCH, help="global batch per GPU")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--pipeline", action="store_true",
+                    help="use the multi-GPU runtime (profile -> best_schedule -> PipeBD) even at N=1")
     return ap.parse_args()
 
 
@@ -219,10 +221,13 @@ def run_ours(args, rank, world, local_rank):
     from paper_2301_12443_b200 import executor, models
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if world > 1:
+    if world > 1 or args.pipeline:
         from paper_2301_12443_b200 import runtime
-        res = runtime.bench_pipeline(args, rank, world, local_rank)
+        with ClockSampler(local_rank) as clocks:
+            res = runtime.bench_pipeline(args, rank, world, local_rank)
         if rank == 0:
+            res["clocks"] = clocks.summary()
+            res["cpu_baseline"] = None
             print(json.dumps(res), flush=True)
         return
 

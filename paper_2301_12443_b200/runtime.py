@@ -231,15 +231,23 @@ def observed_profile(reference: dict, measured: Dict[int, Tuple[int, float, floa
 # ---------------------------------------------------------------- bench entry (torchrun, N > 1)
 
 def bench_pipeline(args, rank: int, world: int, local_rank: int) -> dict:
-    from . import executor, models
+    """torchrun entry of bench.py for N GPUs (also usable at N=1 with --pipeline): measure the block
+    profile on the GPU, pick the schedule with best_schedule, run Algorithm 1 across the ranks."""
+    import os
+    import time as _time
+    from . import executor
     dev = torch.device("cuda", local_rank)
     if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         dist.init_process_group("nccl", device_id=dev)
     gb = args.batch * world
-    # profile on every rank's own GPU, schedule on rank 0, broadcast the document
-    prof = profile_blocks(gb, world, device=dev) if rank == 0 else None
+    # profile on rank 0's GPU, schedule on rank 0, broadcast the documents
     obj = [None, None]
     if rank == 0:
+        prof = profile_blocks(gb, world, device=dev)
         sched, meta = core.best_schedule(prof)
         obj = [sched, {"profile": prof, "meta": meta}]
     dist.broadcast_object_list(obj, src=0)
@@ -251,32 +259,63 @@ def bench_pipeline(args, rank: int, world: int, local_rank: int) -> dict:
         p.set_shard(n, first)
         return p
 
+    def timed(pipe, steps, e2e_hook=None):
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = _time.perf_counter()
+        e0.record()
+        for _ in range(steps):
+            if e2e_hook is not None:
+                e2e_hook(pipe, "pre")
+            pipe.step()
+            if e2e_hook is not None:
+                e2e_hook(pipe, "post")
+        pipe._finish_sends()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        wall = (_time.perf_counter() - t0) / steps * 1e3
+        t = torch.tensor([e0.elapsed_time(e1) / steps, wall], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t[0]), float(t[1])
+
     pipe = PipeBD(sched, gb, make_stage)
     for _ in range(max(3, args.warmup)):
         pipe.step()
-    torch.cuda.synchronize(dev)
-    dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(args.steps):
-        pipe.step()
-    pipe._finish_sends()
-    e1.record()
-    torch.cuda.synchronize(dev)
-    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item())
+    ms, _ = timed(pipe, args.steps)
     losses = pipe.block_losses()
+
+    # e2e: partition-0 ranks upload their images from pinned host memory every step; the last
+    # partition reads its losses back to the host every step.
+    me = pipe.me
+    host = None
+    if me.partition == 0:
+        pipe.stage.set_external_input(True)
+        host = torch.empty(me.count, 32, 32, 3, dtype=torch.float32).pin_memory().uniform_(-1, 1)
+    loss_host = torch.empty(len(pipe.stage.blocks), dtype=torch.float64).pin_memory()
+
+    def hook(p, when):
+        if when == "pre" and host is not None:
+            p.stage.upload_images(host)
+        elif when == "post" and me.partition == pipe.nparts - 1:
+            loss_host.copy_(p.stage.losses_tensor(), non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+
+    _, e2e_ms = timed(pipe, args.steps, hook)
     all_losses = [None] * world
     dist.all_gather_object(all_losses, losses)
     pred = core.predicted_step_time(info["profile"], sched)
+    h2d = (me.count * 32 * 32 * 3 * 4) if host is not None else 0
     return {"metric": "blockwise-distill samples/sec", "value": gb / ms * 1e3, "unit": "samples/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (Philox4x32-10 on device)",
             "config": {"workload": "cifar-resnet18-teacher/slim-student 4 blocks (configs[1])", "global_batch": gb,
                        "parallelism": "ahd " + ";".join(f"{p['blocks']}x{len(p['devices'])}"
-                                                        for p in sched["partitions"])},
-            "schedule": sched, "predicted_step_ms": pred["step_ms"],
+                                                        for p in sched["partitions"]),
+                       "l2": "no flush: per-step working set > 126 MB L2"},
+            "e2e": {"value": gb / e2e_ms * 1e3, "unit": "samples/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": 8 * len(pipe.stage.blocks), "ms_per_step": e2e_ms},
+            "schedule": sched, "predicted_step_ms": pred["step_ms"], "profile": info["profile"],
             "block_losses": {k: v for d in all_losses for k, v in d.items()},
             "gpu_launches": pipe.stage.launches_per_step() * args.steps}
