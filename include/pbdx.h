@@ -74,6 +74,12 @@ int pbdx_step(void* handle, void* stream);
 /* Capture teacher_forward + student_step + apply_update as one CUDA graph (single-GPU path) and replay it. */
 int pbdx_capture(void* handle, void* stream);
 int pbdx_replay(void* handle, void* stream);
+/* Capture the three phases as separate graphs (0 teacher_forward, 1 student_step, 2 apply_update)
+ * so a multi-GPU driver can put the NCCL relay / allreduce between replays.  fuse_ts != 0: phase 0
+ * holds teacher_forward + student_step (overlapped per block) and phase 1 is empty — for ranks
+ * that relay nothing downstream. */
+int pbdx_capture_phases(void* handle, int fuse_ts, void* stream);
+int pbdx_replay_phase(void* handle, int phase, void* stream);
 
 int pbdx_buffer(void* handle, int which, void** ptr, size_t* bytes);
 int pbdx_num_blocks(void* handle);

@@ -217,12 +217,14 @@ class Partition {
       n_ = n;
       build_plans();
       graph_valid_ = false;
+      phases_valid_ = false;
     }
   }
 
   void set_external_input(bool ext) {
     external_ = ext;
     graph_valid_ = false;
+    phases_valid_ = false;
   }
 
   void upload_images(const float* host, int n, cudaStream_t st) {
@@ -245,13 +247,18 @@ class Partition {
     }
   }
 
-  // Student block k runs on its own stream once teacher block k is done (event recorded by
-  // teacher_forward); the caller's stream joins all of them before returning.
-  void student_step(cudaStream_t caller) {
+  // Student block k runs on its own stream.  Fused step(): it starts once teacher block k is
+  // done (event recorded by teacher_forward).  Standalone phase (multi-GPU driver, phase
+  // graphs): the student streams fork from the caller's stream at entry.  The caller's
+  // stream joins all of them before returning.
+  void student_step(cudaStream_t caller) { student_step_impl(caller, true); }
+
+  void student_step_impl(cudaStream_t caller, bool fork) {
+    if (fork) cuda(cudaEventRecord(fork_, caller), "event");
     for (size_t i = 0; i < sblocks_.size(); ++i) {
       SBlock& s = sblocks_[i];
       cudaStream_t st = s.stream;
-      cuda(cudaStreamWaitEvent(st, tdone_[i], 0), "wait teacher");
+      cuda(cudaStreamWaitEvent(st, fork ? fork_ : tdone_[i], 0), "wait teacher");
       if (timing_) cuda(cudaEventRecord(ev_s_[2 * i], st), "event");
       const float* p = params_ + s.base;
       float* g = grads_ + s.base;
@@ -288,8 +295,52 @@ class Partition {
 
   void step(cudaStream_t st) {
     teacher_forward(st);
-    student_step(st);
+    student_step_impl(st, false);
     apply_update(st);
+  }
+
+  // Three graphs (teacher_forward / student_step / apply_update) for the multi-GPU driver, which
+  // interleaves NCCL relay and allreduce between them.
+  // fuse_ts: phase 0 = teacher_forward + student_step with the per-block teacher->student
+  // overlap of step(), phase 1 empty (ranks that send no relay: nothing to put in between).
+  void capture_phases(cudaStream_t caller, bool fuse_ts) {
+    if (cap_stream_ == nullptr) cuda(cudaStreamCreateWithFlags(&cap_stream_, cudaStreamNonBlocking), "stream");
+    cuda(cudaStreamSynchronize(caller), "sync");
+    const bool was_timing = timing_;
+    timing_ = false;
+    for (int ph = 0; ph < 3; ++ph) {
+      if (phase_exec_[ph] != nullptr) {
+        cudaGraphExecDestroy(phase_exec_[ph]);
+        phase_exec_[ph] = nullptr;
+      }
+      cudaGraph_t g = nullptr;
+      cuda(cudaStreamBeginCapture(cap_stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
+      try {
+        if (ph == 0) {
+          teacher_forward(cap_stream_);
+          if (fuse_ts) student_step_impl(cap_stream_, false);
+        }
+        if (ph == 1 && !fuse_ts) student_step_impl(cap_stream_, true);
+        if (ph == 2) apply_update(cap_stream_);
+      } catch (...) {
+        cudaStreamEndCapture(cap_stream_, &g);
+        if (g) cudaGraphDestroy(g);
+        timing_ = was_timing;
+        throw;
+      }
+      cuda(cudaStreamEndCapture(cap_stream_, &g), "end capture");
+      size_t nodes = 0;
+      cuda(cudaGraphGetNodes(g, nullptr, &nodes), "graph nodes");
+      if (nodes > 0) cuda(cudaGraphInstantiate(&phase_exec_[ph], g, 0), "instantiate");
+      cudaGraphDestroy(g);
+    }
+    timing_ = was_timing;
+    phases_valid_ = true;
+  }
+
+  void replay_phase(int ph, cudaStream_t st) {
+    if (ph < 0 || ph > 2 || !phases_valid_) throw BadArg("no captured phase graph");
+    if (phase_exec_[ph] != nullptr) cuda(cudaGraphLaunch(phase_exec_[ph], st), "graph launch");
   }
 
   // Captures on a private non-blocking stream (the legacy default stream cannot be
@@ -385,6 +436,9 @@ class Partition {
       if (s.done != nullptr) cudaEventDestroy(s.done);
     }
     for (auto e : tdone_) cudaEventDestroy(e);
+    for (auto g : phase_exec_)
+      if (g != nullptr) cudaGraphExecDestroy(g);
+    if (fork_ != nullptr) cudaEventDestroy(fork_);
     for (auto e : ev_t_) cudaEventDestroy(e);
     for (auto e : ev_s_) cudaEventDestroy(e);
   }
@@ -539,6 +593,7 @@ class Partition {
     }
     tdone_.resize(tblocks_.size());
     for (auto& e : tdone_) cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    cuda(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming), "event");
   }
 
   static pbdk_conv_desc conv1_desc(const SBlock& s, int n) {
@@ -583,6 +638,9 @@ class Partition {
   bool timing_ = false;
   bool graph_valid_ = false;
   cudaGraphExec_t graph_exec_ = nullptr;
+  cudaGraphExec_t phase_exec_[3] = {nullptr, nullptr, nullptr};
+  bool phases_valid_ = false;
+  cudaEvent_t fork_ = nullptr;
   cudaStream_t cap_stream_ = nullptr;
   Arena arena_;
   bf16* input_ = nullptr;
@@ -649,6 +707,10 @@ int pbdx_apply_update(void* h, void* st) { return guard([&] { P(h)->apply_update
 int pbdx_step(void* h, void* st) { return guard([&] { P(h)->step(S(st)); }); }
 int pbdx_capture(void* h, void* st) { return guard([&] { P(h)->capture(S(st)); }); }
 int pbdx_replay(void* h, void* st) { return guard([&] { P(h)->replay(S(st)); }); }
+int pbdx_capture_phases(void* h, int fuse_ts, void* st) {
+  return guard([&] { P(h)->capture_phases(S(st), fuse_ts != 0); });
+}
+int pbdx_replay_phase(void* h, int phase, void* st) { return guard([&] { P(h)->replay_phase(phase, S(st)); }); }
 int pbdx_buffer(void* h, int which, void** ptr, size_t* bytes) {
   return guard([&] { P(h)->buffer(which, ptr, bytes); });
 }

@@ -40,6 +40,8 @@ def _bind(L):
     for name in ("pbdx_init_params", "pbdx_teacher_forward", "pbdx_student_step", "pbdx_apply_update", "pbdx_step",
                  "pbdx_capture", "pbdx_replay"):
         getattr(L, name).argtypes = [V, V]
+    L.pbdx_capture_phases.argtypes = [V, I, V]
+    L.pbdx_replay_phase.argtypes = [V, I, V]
     L.pbdx_set_shard.argtypes = [V, I, I]
     L.pbdx_set_input_mode.argtypes = [V, I]
     L.pbdx_upload_images.argtypes = [V, V, I, V]
@@ -211,6 +213,16 @@ class Partition:
 
     def replay(self, stream=None):
         _check(lib().pbdx_replay(self.handle, self._stream(stream)), "replay")
+
+    def capture_phases(self, fuse_teacher_student: bool = False, stream=None):
+        """Capture teacher_forward / student_step / apply_update as three CUDA graphs (phase 0 holds
+        both forward phases when fuse_teacher_student)."""
+        _check(lib().pbdx_capture_phases(self.handle, int(fuse_teacher_student), self._stream(stream)),
+               "capture_phases")
+        self._phased = True
+
+    def replay_phase(self, phase: int, stream=None):
+        _check(lib().pbdx_replay_phase(self.handle, phase, self._stream(stream)), "replay_phase")
 
     def set_timing(self, on: bool):
         _check(lib().pbdx_set_timing(self.handle, int(on)), "set_timing")

@@ -139,18 +139,31 @@ class PipeBD:
         self._pending_sends = []
 
     # -- Algorithm 1, one step
+    def use_graphs(self):
+        """Replay each phase as a CUDA graph (stages that support capture_phases)."""
+        if hasattr(self.stage, "capture_phases"):
+            # a rank that relays nothing downstream keeps the teacher->student overlap in one graph
+            self.stage.capture_phases(fuse_teacher_student=not self.send_msgs)
+            self._graphs = True
+
+    def _phase(self, i, fn):
+        if getattr(self, "_graphs", False):
+            self.stage.replay_phase(i)
+        else:
+            fn()
+
     def step(self):
         self._recv_input()
         self._finish_sends()  # the previous step's send must drain before t_hi is overwritten
-        self.stage.teacher_forward()
+        self._phase(0, self.stage.teacher_forward)
         self._send_output()
-        self.stage.student_step()
+        self._phase(1, self.stage.student_step)
         g = self.groups.get(self.me.partition)
         if g is not None:
             dist.all_reduce(self.stage.grads(), op=dist.ReduceOp.SUM, group=g)
         if not self.dpu:
             dist.barrier()
-        self.stage.apply_update()
+        self._phase(2, self.stage.apply_update)
 
     def end_epoch(self):
         """Full synchronisation at the epoch boundary (simulate.cpp:263)."""
@@ -280,6 +293,8 @@ def bench_pipeline(args, rank: int, world: int, local_rank: int) -> dict:
         return float(t[0]), float(t[1])
 
     pipe = PipeBD(sched, gb, make_stage)
+    if not getattr(args, "no_graph", False):
+        pipe.use_graphs()
     for _ in range(max(3, args.warmup)):
         pipe.step()
     ms, _ = timed(pipe, args.steps)
@@ -292,6 +307,8 @@ def bench_pipeline(args, rank: int, world: int, local_rank: int) -> dict:
     if me.partition == 0:
         pipe.stage.set_external_input(True)
         host = torch.empty(me.count, 32, 32, 3, dtype=torch.float32).pin_memory().uniform_(-1, 1)
+        if getattr(pipe, "_graphs", False):
+            pipe.use_graphs()  # re-capture without the on-device data generation
     loss_host = torch.empty(len(pipe.stage.blocks), dtype=torch.float64).pin_memory()
 
     def hook(p, when):
@@ -306,6 +323,8 @@ def bench_pipeline(args, rank: int, world: int, local_rank: int) -> dict:
     dist.all_gather_object(all_losses, losses)
     pred = core.predicted_step_time(info["profile"], sched)
     h2d = (me.count * 32 * 32 * 3 * 4) if host is not None else 0
+    dist.barrier()
+    dist.destroy_process_group()
     return {"metric": "blockwise-distill samples/sec", "value": gb / ms * 1e3, "unit": "samples/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",

@@ -195,3 +195,23 @@ def test_full_size_teacher_sample_independence(ex):
     torch.cuda.synchronize()
     losses = big.losses()
     assert all(np.isfinite(losses)) and all(0 < l < 10 for l in losses)
+
+
+def test_phase_graphs_bitwise_equal_eager(ex):
+    """capture_phases (the multi-GPU driver's three graphs) == eager phases, bit for bit."""
+    b = 8
+    outs = []
+    for phased in (False, True):
+        p = ex.Partition(0, 3, b, b)
+        p.init_params()
+        if phased:
+            p.capture_phases()
+        losses = []
+        for _ in range(3):
+            for i, fn in enumerate((p.teacher_forward, p.student_step, p.apply_update)):
+                p.replay_phase(i) if phased else fn()
+            torch.cuda.synchronize()
+            losses.append(p.losses())
+        outs.append((losses, p.params().cpu()))
+    assert outs[0][0] == outs[1][0]
+    assert torch.equal(outs[0][1], outs[1][1])
