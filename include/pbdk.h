@@ -88,14 +88,16 @@ int pbdk_bn_stats(const void* y, int m, int c, void* workspace, float* mean_rstd
 /* a = bf16(relu(gamma*(y-mean)*rstd + beta)) */
 int pbdk_bn_apply_relu(const void* y, const float* mean_rstd, const float* gamma, const float* beta, void* a, int m,
                        int c, void* stream);
-/* BN backward given dL/d(bn out) g: red[0:c]=sum g, red[c:2c]=sum g*xhat (also written to dbeta/dgamma),
- * dy = gamma*rstd/m * (m*g - sum g - xhat*sum g*xhat) in bf16 */
+/* BN backward given dL/d(bn out) g: dbeta = sum g, dgamma = sum g*xhat (= rstd*(sum g*y - mean*sum g)),
+ * dy = gamma*rstd/m * (m*g - sum g - xhat*sum g*xhat) evaluated as dy = A*g + Q*y + R (A = gamma*rstd);
+ * red receives {Q[c], R[c]} (2c floats). */
 int pbdk_bn_bwd(const void* g, const void* y, const float* mean_rstd, const float* gamma, int m, int c,
                 void* workspace, float* red, float* dgamma, float* dbeta, void* dy, void* stream);
 
 /* ------------------------------------------------------------------ K4: fused distillation loss + backward */
 /* s = relu(BN2(y2) + BNsc(ysc)); loss = sum (s-t)^2 / norm; g = [s>0] (s-t)*gscale (gscale = 2/norm);
- * writes dgamma/dbeta of both BNs, red[3c] = {sum g, sum g*xhat2, sum g*xhatsc}, and dy2 / dysc (bf16). */
+ * writes dgamma/dbeta of both BNs, red[4c] = {Q2, R2, Qsc, Rsc} (the coefficients of dy = A*g + Q*y + R)
+ * and dy2 / dysc (bf16). */
 typedef struct pbdk_mse_args {
   const void* y2;
   const void* ysc;

@@ -408,7 +408,6 @@ int bdo_student_fwd_bwd(int k, const float* sp, int n, const float* in, const fl
   const student_geom g = sgeom(k);
   const int P = g.hout;
   const size_t m = (size_t)n * P * P;
-  const float mf = (float)m;
   float* w1 = shadow(sp + g.w1, (size_t)g.mid * 9 * g.cin, bf16);
   float* w2 = shadow(sp + g.w2, (size_t)g.cout * 9 * g.mid, bf16);
   float* wsc = shadow(sp + g.wsc, (size_t)g.cout * g.cin, bf16);
@@ -429,11 +428,17 @@ int bdo_student_fwd_bwd(int k, const float* sp, int n, const float* in, const fl
   bn_stats(y1, m, g.mid, mu1, r1);
   const float* G1 = sp + g.g1;
   const float* B1 = sp + g.b1;
+  /* BN as a per-channel affine map: A = gamma*rstd, B = beta - A*mean */
+  float* A1 = (float*)malloc(sizeof(float) * g.mid);
+  float* C1 = (float*)malloc(sizeof(float) * g.mid);
+  for (int c = 0; c < g.mid; ++c) {
+    A1[c] = G1[c] * r1[c];
+    C1[c] = fmaf(-A1[c], mu1[c], B1[c]);
+  }
 #pragma omp parallel for schedule(static)
   for (long long i = 0; i < (long long)m; ++i)
     for (int c = 0; c < g.mid; ++c) {
-      const float xh = (y1[i * g.mid + c] - mu1[c]) * r1[c];
-      const float z = fmaf(G1[c], xh, B1[c]);
+      const float z = fmaf(A1[c], y1[i * g.mid + c], C1[c]);
       a1[i * g.mid + c] = rnd(z > 0.0f ? z : 0.0f, bf16);
     }
   conv_fwd(a1, n, P, P, g.mid, w2, g.cout, 3, 1, 1, P, P, y2);
@@ -445,11 +450,19 @@ int bdo_student_fwd_bwd(int k, const float* sp, int n, const float* in, const fl
   bn_stats(y2, m, g.cout, mu2, r2);
   bn_stats(ys, m, g.cout, mus, rs);
 
-  /* loss + relu backward + BN2/BNsc reductions (fp32 g recomputed identically later) */
+  /* loss + relu backward + BN2/BNsc backward.  Both BNs are per-channel affine maps
+   * z = A2*y2 + As*ysc + (B2 + Bsc); the backward needs sum g, sum g*y2, sum g*ysc, from which
+   * sum g*xhat = rstd * (sum g*y - mean * sum g), and dy = A*g + Q*y + R. */
   const float* G2 = sp + g.g2;
   const float* B2 = sp + g.b2;
   const float* Gs = sp + g.gsc;
   const float* Bs = sp + g.bsc;
+  float *A2 = malloc(sizeof(float) * g.cout), *As = malloc(sizeof(float) * g.cout), *Bz = malloc(sizeof(float) * g.cout);
+  for (int c = 0; c < g.cout; ++c) {
+    A2[c] = G2[c] * r2[c];
+    As[c] = Gs[c] * rs[c];
+    Bz[c] = fmaf(-A2[c], mu2[c], B2[c]) + fmaf(-As[c], mus[c], Bs[c]);
+  }
   const float gscale = (float)(2.0 / norm);
   double* part = (double*)calloc((size_t)n * (1 + 3 * (size_t)g.cout), sizeof(double));
 #pragma omp parallel for schedule(static)
@@ -458,16 +471,15 @@ int bdo_student_fwd_bwd(int k, const float* sp, int n, const float* in, const fl
     for (int pq = 0; pq < P * P; ++pq) {
       const size_t i = (size_t)s * P * P + pq;
       for (int c = 0; c < g.cout; ++c) {
-        const float xh2 = (y2[i * g.cout + c] - mu2[c]) * r2[c];
-        const float xhs = (ys[i * g.cout + c] - mus[c]) * rs[c];
-        const float z = fmaf(G2[c], xh2, B2[c]) + fmaf(Gs[c], xhs, Bs[c]);
+        const float v2 = y2[i * g.cout + c], vs = ys[i * g.cout + c];
+        const float z = fmaf(A2[c], v2, fmaf(As[c], vs, Bz[c]));
         const float sv = z > 0.0f ? z : 0.0f;
         const float d = sv - t_out[i * g.cout + c];
         ps[0] += (double)d * (double)d;
         const float gg = z > 0.0f ? d * gscale : 0.0f;
         ps[1 + c] += gg;
-        ps[1 + g.cout + c] += (double)gg * xh2;
-        ps[1 + 2 * g.cout + c] += (double)gg * xhs;
+        ps[1 + g.cout + c] += (double)gg * v2;
+        ps[1 + 2 * g.cout + c] += (double)gg * vs;
       }
     }
   }
@@ -481,27 +493,40 @@ int bdo_student_fwd_bwd(int k, const float* sp, int n, const float* in, const fl
   *loss_out = loss / norm;
   float* gr = grads;
   memset(gr, 0, sizeof(float) * g.total);
+  float *Q2 = malloc(sizeof(float) * g.cout), *R2 = malloc(sizeof(float) * g.cout);
+  float *Qs = malloc(sizeof(float) * g.cout), *Rs = malloc(sizeof(float) * g.cout);
   for (int c = 0; c < g.cout; ++c) {
-    gr[g.b2 + c] = (float)red[c];
-    gr[g.bsc + c] = (float)red[c];
-    gr[g.g2 + c] = (float)red[g.cout + c];
-    gr[g.gsc + c] = (float)red[2 * g.cout + c];
+    const double sgv = red[c];
+    const double sgx2 = (double)r2[c] * (red[g.cout + c] - (double)mu2[c] * sgv);
+    const double sgxs = (double)rs[c] * (red[2 * g.cout + c] - (double)mus[c] * sgv);
+    gr[g.b2 + c] = (float)sgv;
+    gr[g.bsc + c] = (float)sgv;
+    gr[g.g2 + c] = (float)sgx2;
+    gr[g.gsc + c] = (float)sgxs;
+    const double c2 = (double)A2[c] / (double)m, cs = (double)As[c] / (double)m;
+    Q2[c] = (float)(-c2 * sgx2 * (double)r2[c]);
+    R2[c] = (float)(-c2 * (sgv - sgx2 * (double)r2[c] * (double)mu2[c]));
+    Qs[c] = (float)(-cs * sgxs * (double)rs[c]);
+    Rs[c] = (float)(-cs * (sgv - sgxs * (double)rs[c] * (double)mus[c]));
   }
 #pragma omp parallel for schedule(static)
   for (long long i = 0; i < (long long)m; ++i)
     for (int c = 0; c < g.cout; ++c) {
-      const float xh2 = (y2[i * g.cout + c] - mu2[c]) * r2[c];
-      const float xhs = (ys[i * g.cout + c] - mus[c]) * rs[c];
-      const float z = fmaf(G2[c], xh2, B2[c]) + fmaf(Gs[c], xhs, Bs[c]);
+      const float v2 = y2[i * g.cout + c], vs = ys[i * g.cout + c];
+      const float z = fmaf(A2[c], v2, fmaf(As[c], vs, Bz[c]));
       const float sv = z > 0.0f ? z : 0.0f;
       const float d = sv - t_out[i * g.cout + c];
       const float gg = z > 0.0f ? d * gscale : 0.0f;
-      const float sg = (float)red[c];
-      const float k2 = (G2[c] * r2[c]) / mf;
-      const float ks = (Gs[c] * rs[c]) / mf;
-      dy2[i * g.cout + c] = rnd(k2 * fmaf(-xh2, (float)red[g.cout + c], fmaf(mf, gg, -sg)), bf16);
-      dys[i * g.cout + c] = rnd(ks * fmaf(-xhs, (float)red[2 * g.cout + c], fmaf(mf, gg, -sg)), bf16);
+      dy2[i * g.cout + c] = rnd(fmaf(A2[c], gg, fmaf(Q2[c], v2, R2[c])), bf16);
+      dys[i * g.cout + c] = rnd(fmaf(As[c], gg, fmaf(Qs[c], vs, Rs[c])), bf16);
     }
+  free(A2);
+  free(As);
+  free(Bz);
+  free(Q2);
+  free(R2);
+  free(Qs);
+  free(Rs);
 
   /* conv2 / shortcut weight gradients, conv2 dgrad with the relu mask of a1 */
   conv_wgrad(a1, n, P, P, g.mid, dy2, g.cout, 3, 1, 1, P, P, gr + g.w2);
@@ -509,33 +534,38 @@ int bdo_student_fwd_bwd(int k, const float* sp, int n, const float* in, const fl
   conv_dgrad_s1(dy2, n, P, P, g.cout, w2, g.mid, 3, 1, g1);
   for (size_t i = 0; i < m * g.mid; ++i) g1[i] = rnd(a1[i] > 0.0f ? g1[i] : 0.0f, bf16);
 
-  /* BN1 backward */
+  /* BN1 backward: sums of g1 and g1*y1, then dy1 = A1*g1 + Q1*y1 + R1 */
   double* red1 = (double*)calloc(2 * (size_t)g.mid, sizeof(double));
 #pragma omp parallel for schedule(static)
   for (int c = 0; c < g.mid; ++c) {
-    double sg = 0.0, sgx = 0.0;
+    double sg = 0.0, sgy = 0.0;
     for (size_t i = 0; i < m; ++i) {
-      const float xh = (y1[i * g.mid + c] - mu1[c]) * r1[c];
       const double gv = g1[i * g.mid + c];
       sg += gv;
-      sgx += gv * xh;
+      sgy += gv * y1[i * g.mid + c];
     }
     red1[c] = sg;
-    red1[g.mid + c] = sgx;
+    red1[g.mid + c] = sgy;
   }
+  float *Q1 = malloc(sizeof(float) * g.mid), *R1 = malloc(sizeof(float) * g.mid);
   for (int c = 0; c < g.mid; ++c) {
-    gr[g.b1 + c] = (float)red1[c];
-    gr[g.g1 + c] = (float)red1[g.mid + c];
+    const double sgv = red1[c];
+    const double sgx = (double)r1[c] * (red1[g.mid + c] - (double)mu1[c] * sgv);
+    gr[g.b1 + c] = (float)sgv;
+    gr[g.g1 + c] = (float)sgx;
+    const double c1 = (double)A1[c] / (double)m;
+    Q1[c] = (float)(-c1 * sgx * (double)r1[c]);
+    R1[c] = (float)(-c1 * (sgv - sgx * (double)r1[c] * (double)mu1[c]));
   }
   float* dy1 = a1; /* reuse */
 #pragma omp parallel for schedule(static)
   for (long long i = 0; i < (long long)m; ++i)
-    for (int c = 0; c < g.mid; ++c) {
-      const float xh = (y1[i * g.mid + c] - mu1[c]) * r1[c];
-      const float k1 = (G1[c] * r1[c]) / mf;
-      dy1[i * g.mid + c] =
-          rnd(k1 * fmaf(-xh, (float)red1[g.mid + c], fmaf(mf, g1[i * g.mid + c], -(float)red1[c])), bf16);
-    }
+    for (int c = 0; c < g.mid; ++c)
+      dy1[i * g.mid + c] = rnd(fmaf(A1[c], g1[i * g.mid + c], fmaf(Q1[c], y1[i * g.mid + c], R1[c])), bf16);
+  free(Q1);
+  free(R1);
+  free(A1);
+  free(C1);
   conv_wgrad(in, n, g.hin, g.hin, g.cin, dy1, g.mid, 3, g.stride, 1, P, P, gr + g.w1);
 
   free(w1);

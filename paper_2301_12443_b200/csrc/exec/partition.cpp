@@ -268,8 +268,7 @@ class Partition {
       check(pbdk::bn_stats(s.y1, m, s.mid, s.rws, s.st1, st), "bn1 stats");
       check(pbdk::bn_apply_relu(s.y1, s.st1, p + s.lay.g1, p + s.lay.b1, s.a1, m, s.mid, st), "bn1 apply");
       check(pbdk::fprop_run(s.p_conv2, st), "conv2");
-      check(pbdk::bn_stats(s.y2, m, s.cout, s.rws, s.st2, st), "bn2 stats");
-      check(pbdk::bn_stats(s.ys, m, s.cout, s.rws, s.sts, st), "bnsc stats");
+      check(pbdk::bn_stats2(s.y2, s.ys, m, s.cout, s.rws, s.st2, s.sts, st), "bn2/bnsc stats");
       const double norm = static_cast<double>(d_.global_batch) * s.cout * s.hout * s.hout;
       pbdk::MseArgs a{s.y2, s.ys, s.target, s.st2, s.sts, p + s.lay.g2, p + s.lay.b2, p + s.lay.gsc, p + s.lay.bsc,
                       m, s.cout, static_cast<float>(2.0 / norm), norm, s.rws, s.red, g + s.lay.g2, g + s.lay.b2,
@@ -421,7 +420,7 @@ class Partition {
     int n = (d_.block_lo == 0 && !external_) ? 1 : 0;
     for (const TBlock& tb : tblocks_) n += static_cast<int>(tb.convs.size());
     for (const SBlock& s : sblocks_) {
-      n += 3 + 2 + 2 * 2 + 3 + 1 + 3;  // convs, bn1 stats(2)+apply, bn2/bnsc stats, mse(3), dgrad, bn_bwd(3)
+      n += 3 + 3 + 2 + 3 + 1 + 3;  // convs, bn1 stats(2)+apply, bn2+bnsc stats(2), mse(3), dgrad, bn_bwd(3)
       n += (s.p_w2.splits > 1 ? 2 : 1) + (s.p_wsc.splits > 1 ? 2 : 1) + (s.p_w1.splits > 1 ? 2 : 1);
     }
     n += 1 + static_cast<int>(sblocks_.size());  // sgd + flips
@@ -568,7 +567,7 @@ class Partition {
       s.red1 = arena_.get<float>(2 * s.mid * sizeof(float));
       s.st2 = arena_.get<float>(2 * s.cout * sizeof(float));
       s.sts = arena_.get<float>(2 * s.cout * sizeof(float));
-      s.red = arena_.get<float>(3 * s.cout * sizeof(float));
+      s.red = arena_.get<float>(4 * s.cout * sizeof(float));
       sblocks_.push_back(s);
     }
     params_ = arena_.get<float>(total_ * sizeof(float));

@@ -237,48 +237,57 @@ __device__ __forceinline__ double cta_sum(const float* __restrict__ v, int n) {
   return t;
 }
 
-// -- BN statistics
-template <int V>
-__global__ void __launch_bounds__(kThreads) bn_stats_partial_kernel(const __nv_bfloat16* __restrict__ y, int m, int C,
-                                                                    int rows_per_chunk, int cg, int rpp,
+// -- BN statistics: per-channel (sum y, sum y^2) of one or two tensors of the same shape
+template <int V, int NT>
+__global__ void __launch_bounds__(kThreads) bn_stats_partial_kernel(const __nv_bfloat16* __restrict__ y0,
+                                                                    const __nv_bfloat16* __restrict__ y1, int m,
+                                                                    int C, int rows_per_chunk, int cg, int rpp,
                                                                     float* __restrict__ partial) {
   const int g = threadIdx.x % cg;
   const int slot = threadIdx.x / cg;
-  float acc[2][V] = {};
+  float acc[2 * NT][V] = {};
   if (slot < rpp) {
     const int r0 = blockIdx.x * rows_per_chunk;
     const int r1 = min(m, r0 + rows_per_chunk);
-    const __nv_bfloat16* p = y + static_cast<size_t>(r0 + slot) * C + g * V;
-#pragma unroll 4
-    for (int r = r0 + slot; r < r1; r += rpp, p += static_cast<size_t>(rpp) * C) {
-      float f[V];
-      Vec<V>::load(p, f);
+#pragma unroll 2
+    for (int r = r0 + slot; r < r1; r += rpp) {
+      const size_t off = static_cast<size_t>(r) * C + g * V;
+      float f[NT][V];
+      Vec<V>::load(y0 + off, f[0]);
+      if (NT == 2) Vec<V>::load(y1 + off, f[NT - 1]);
 #pragma unroll
-      for (int j = 0; j < V; ++j) {
-        acc[0][j] += f[j];
-        acc[1][j] += f[j] * f[j];
-      }
+      for (int t = 0; t < NT; ++t)
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          acc[2 * t][j] += f[t][j];
+          acc[2 * t + 1][j] += f[t][j] * f[t][j];
+        }
     }
   }
-  cta_reduce_store<2, V>(acc, cg, rpp, C, partial);
+  cta_reduce_store<2 * NT, V>(acc, cg, rpp, C, partial);
 }
 
-// grid: ceil(C / 8) CTAs of 8 warps; warp = channel.
+// grid: ceil(NT*C / 8) CTAs of 8 warps; warp = (tensor, channel).
+template <int NT>
 __global__ void bn_stats_finalize_kernel(const float* __restrict__ partial, int chunks, int C, int m,
-                                         float* __restrict__ mean_rstd) {
-  const int c = blockIdx.x * kFinWarps + (threadIdx.x >> 5);
-  if (c >= C) return;
-  const double s1 = warp_sum_chunks<2>(partial, chunks, C, c);
-  const double s2 = warp_sum_chunks<2>(partial, chunks, C, C + c);
+                                         float* __restrict__ mr0, float* __restrict__ mr1) {
+  const int o = blockIdx.x * kFinWarps + (threadIdx.x >> 5);
+  if (o >= NT * C) return;
+  const int t = o / C;
+  const int c = o - t * C;
+  const double s1 = warp_sum_chunks<2 * NT>(partial, chunks, C, 2 * t * C + c);
+  const double s2 = warp_sum_chunks<2 * NT>(partial, chunks, C, (2 * t + 1) * C + c);
   if ((threadIdx.x & 31) == 0) {
+    float* mr = t == 0 ? mr0 : mr1;
     const double mu = s1 / static_cast<double>(m);
     const double var = s2 / static_cast<double>(m) - mu * mu;
-    mean_rstd[c] = static_cast<float>(mu);
-    mean_rstd[C + c] = 1.0f / sqrtf(static_cast<float>(var) + 1e-5f);
+    mr[c] = static_cast<float>(mu);
+    mr[C + c] = 1.0f / sqrtf(static_cast<float>(var) + 1e-5f);
   }
 }
 
-// -- BN apply + ReLU: a = bf16(relu(fmaf(gamma, (y-mu)*rstd, beta)))
+// -- BN apply + ReLU as a per-channel affine map: a = bf16(relu(fmaf(A, y, B))),
+//    A = gamma*rstd, B = fmaf(-A, mean, beta)
 template <int V>
 __global__ void __launch_bounds__(kThreads) bn_apply_relu_kernel(const __nv_bfloat16* __restrict__ y,
                                                                  const float* __restrict__ mean_rstd,
@@ -290,13 +299,11 @@ __global__ void __launch_bounds__(kThreads) bn_apply_relu_kernel(const __nv_bflo
   const int slot = threadIdx.x / cg;
   if (slot >= rpp) return;
   const int c0 = g * V;
-  float mu[V], rs[V], ga[V], be[V];
+  float A[V], B[V];
 #pragma unroll
   for (int j = 0; j < V; ++j) {
-    mu[j] = mean_rstd[c0 + j];
-    rs[j] = mean_rstd[C + c0 + j];
-    ga[j] = gamma[c0 + j];
-    be[j] = beta[c0 + j];
+    A[j] = gamma[c0 + j] * mean_rstd[C + c0 + j];
+    B[j] = fmaf(-A[j], mean_rstd[c0 + j], beta[c0 + j]);
   }
   const int step = gridDim.x * rpp;
 #pragma unroll 2
@@ -306,14 +313,15 @@ __global__ void __launch_bounds__(kThreads) bn_apply_relu_kernel(const __nv_bflo
     Vec<V>::load(y + off, f);
 #pragma unroll
     for (int j = 0; j < V; ++j) {
-      const float z = fmaf(ga[j], (f[j] - mu[j]) * rs[j], be[j]);
+      const float z = fmaf(A[j], f[j], B[j]);
       f[j] = z > 0.0f ? z : 0.0f;
     }
     Vec<V>::store(a + off, f);
   }
 }
 
-// -- fused distillation loss: s = relu(BN2(y2) + BNsc(ysc)); L += (s-t)^2; g = [z>0] (s-t)*gscale
+// -- fused distillation loss.  z = A2*y2 + As*ysc + Bz (both BNs as affine maps), s = relu(z),
+//    L += (s-t)^2, g = [z>0] (s-t)*gscale; partial sums of g, g*y2, g*ysc.
 struct LossParams {
   const __nv_bfloat16* y2;
   const __nv_bfloat16* ys;
@@ -329,66 +337,49 @@ struct LossParams {
 };
 
 template <int V>
-struct LossChan {  // per-channel constants of the loss kernels, held in registers
-  float m2[V], r2[V], g2[V], b2[V], ms[V], rs[V], gs[V], bs[V];
-  __device__ void load(const LossParams& p, int c0) {
+__device__ __forceinline__ void loss_affine(const LossParams& p, int c0, float (&A2)[V], float (&As)[V],
+                                            float (&Bz)[V]) {
 #pragma unroll
-    for (int j = 0; j < V; ++j) {
-      const int c = c0 + j;
-      m2[j] = p.st2[c];
-      r2[j] = p.st2[p.C + c];
-      ms[j] = p.sts[c];
-      rs[j] = p.sts[p.C + c];
-      g2[j] = p.g2[c];
-      b2[j] = p.b2[c];
-      gs[j] = p.gs[c];
-      bs[j] = p.bs[c];
-    }
+  for (int j = 0; j < V; ++j) {
+    const int c = c0 + j;
+    A2[j] = p.g2[c] * p.st2[p.C + c];
+    As[j] = p.gs[c] * p.sts[p.C + c];
+    Bz[j] = fmaf(-A2[j], p.st2[c], p.b2[c]) + fmaf(-As[j], p.sts[c], p.bs[c]);
   }
-  // g (dL/dz), xhat2, xhatsc, d = s - t for V channels of one row
-  __device__ __forceinline__ void point(const LossParams& p, size_t off, float (&g)[V], float (&xh2)[V],
-                                        float (&xhs)[V], float (&d)[V]) const {
-    float fy2[V], fys[V], ft[V];
-    Vec<V>::load(p.y2 + off, fy2);
-    Vec<V>::load(p.ys + off, fys);
-    Vec<V>::load(p.t + off, ft);
-#pragma unroll
-    for (int j = 0; j < V; ++j) {
-      xh2[j] = (fy2[j] - m2[j]) * r2[j];
-      xhs[j] = (fys[j] - ms[j]) * rs[j];
-      const float z = fmaf(g2[j], xh2[j], b2[j]) + fmaf(gs[j], xhs[j], bs[j]);
-      const float sv = z > 0.0f ? z : 0.0f;
-      d[j] = sv - ft[j];
-      g[j] = z > 0.0f ? d[j] * p.gscale : 0.0f;
-    }
-  }
-};
+}
 
-constexpr int kLossV = 4;
+constexpr int kLossPartialV = 8;
+constexpr int kLossApplyV = 4;
 
 __global__ void __launch_bounds__(kThreads) loss_partial_kernel(const LossParams p, int rows_per_chunk, int cg, int rpp,
                                                                 float* __restrict__ partial,
                                                                 float* __restrict__ loss_partial) {
-  constexpr int V = kLossV;
+  constexpr int V = kLossPartialV;
   const int gi = threadIdx.x % cg;
   const int slot = threadIdx.x / cg;
   float acc[3][V] = {};
   float lsum = 0.0f;
   if (slot < rpp) {
-    LossChan<V> ch;
-    ch.load(p, gi * V);
+    float A2[V], As[V], Bz[V];
+    loss_affine<V>(p, gi * V, A2, As, Bz);
     const int r0 = blockIdx.x * rows_per_chunk;
     const int r1 = min(p.m, r0 + rows_per_chunk);
 #pragma unroll 2
     for (int r = r0 + slot; r < r1; r += rpp) {
-      float g[V], xh2[V], xhs[V], d[V];
-      ch.point(p, static_cast<size_t>(r) * p.C + gi * V, g, xh2, xhs, d);
+      const size_t off = static_cast<size_t>(r) * p.C + gi * V;
+      float y2[V], ys[V], t[V];
+      Vec<V>::load(p.y2 + off, y2);
+      Vec<V>::load(p.ys + off, ys);
+      Vec<V>::load(p.t + off, t);
 #pragma unroll
       for (int j = 0; j < V; ++j) {
-        lsum += d[j] * d[j];
-        acc[0][j] += g[j];
-        acc[1][j] += g[j] * xh2[j];
-        acc[2][j] += g[j] * xhs[j];
+        const float z = fmaf(A2[j], y2[j], fmaf(As[j], ys[j], Bz[j]));
+        const float d = (z > 0.0f ? z : 0.0f) - t[j];
+        const float g = z > 0.0f ? d * p.gscale : 0.0f;
+        lsum += d * d;
+        acc[0][j] += g;
+        acc[1][j] += g * y2[j];
+        acc[2][j] += g * ys[j];
       }
     }
   }
@@ -405,125 +396,125 @@ __global__ void __launch_bounds__(kThreads) loss_partial_kernel(const LossParams
   }
 }
 
-// red (double [3C]) -> grads of gamma2/beta2/gammasc/betasc, float copies; warp = output o in
-// [0, 3C); the last CTA sums the loss partials.
-__global__ void loss_finalize_kernel(const float* __restrict__ partial, const float* __restrict__ loss_partial,
-                                     int chunks, int C, double norm, float* __restrict__ red_f,
-                                     float* __restrict__ dg2, float* __restrict__ db2, float* __restrict__ dgs,
-                                     float* __restrict__ dbs, double* __restrict__ loss_out) {
+// Finalize (fp64): sum g*xhat = rstd*(sum g*y - mean*sum g); gamma/beta grads; the coefficients
+// of dy = A*g + Q*y + R: coef[0:C]=Q2, [C:2C]=R2, [2C:3C]=Qs, [3C:4C]=Rs.  Warp = channel; the
+// last CTA sums the loss partials.
+__global__ void loss_finalize_kernel(const LossParams p, const float* __restrict__ partial,
+                                     const float* __restrict__ loss_partial, int chunks, double norm,
+                                     float* __restrict__ coef, float* __restrict__ dg2, float* __restrict__ db2,
+                                     float* __restrict__ dgs, float* __restrict__ dbs, double* __restrict__ loss_out) {
+  const int C = p.C;
   if (blockIdx.x == gridDim.x - 1) {
     const double l = cta_sum(loss_partial, chunks);
     if (threadIdx.x == 0) *loss_out = l / norm;
     return;
   }
-  const int o = blockIdx.x * kFinWarps + (threadIdx.x >> 5);
-  if (o >= 3 * C) return;
-  const double sv = warp_sum_chunks<3>(partial, chunks, C, o);
+  const int c = blockIdx.x * kFinWarps + (threadIdx.x >> 5);
+  if (c >= C) return;
+  const double sg = warp_sum_chunks<3>(partial, chunks, C, c);
+  const double sgy2 = warp_sum_chunks<3>(partial, chunks, C, C + c);
+  const double sgys = warp_sum_chunks<3>(partial, chunks, C, 2 * C + c);
   if ((threadIdx.x & 31) == 0) {
-    const int v = o / C;
-    const int c = o - v * C;
-    const float f = static_cast<float>(sv);
-    red_f[o] = f;
-    if (v == 0) {
-      db2[c] = f;
-      dbs[c] = f;
-    } else if (v == 1) {
-      dg2[c] = f;
-    } else {
-      dgs[c] = f;
-    }
+    const float m2 = p.st2[c], r2 = p.st2[C + c], ms = p.sts[c], rs = p.sts[C + c];
+    const float A2 = p.g2[c] * r2, As = p.gs[c] * rs;
+    const double sgx2 = static_cast<double>(r2) * (sgy2 - static_cast<double>(m2) * sg);
+    const double sgxs = static_cast<double>(rs) * (sgys - static_cast<double>(ms) * sg);
+    db2[c] = static_cast<float>(sg);
+    dbs[c] = static_cast<float>(sg);
+    dg2[c] = static_cast<float>(sgx2);
+    dgs[c] = static_cast<float>(sgxs);
+    const double c2 = static_cast<double>(A2) / p.m, cs = static_cast<double>(As) / p.m;
+    coef[c] = static_cast<float>(-c2 * sgx2 * r2);
+    coef[C + c] = static_cast<float>(-c2 * (sg - sgx2 * r2 * m2));
+    coef[2 * C + c] = static_cast<float>(-cs * sgxs * rs);
+    coef[3 * C + c] = static_cast<float>(-cs * (sg - sgxs * rs * ms));
   }
 }
 
-__global__ void __launch_bounds__(kThreads) loss_bwd_apply_kernel(const LossParams p, const float* __restrict__ red_f,
+__global__ void __launch_bounds__(kThreads) loss_bwd_apply_kernel(const LossParams p, const float* __restrict__ coef,
                                                                   int cg, int rpp, __nv_bfloat16* __restrict__ dy2,
                                                                   __nv_bfloat16* __restrict__ dys) {
-  constexpr int V = kLossV;
+  constexpr int V = kLossApplyV;
   const int gi = threadIdx.x % cg;
   const int slot = threadIdx.x / cg;
   if (slot >= rpp) return;
   const int c0 = gi * V;
-  const float mf = static_cast<float>(p.m);
-  LossChan<V> ch;
-  ch.load(p, c0);
-  float sg[V], sgx2[V], sgxs[V], k2[V], ks[V];
+  float A2[V], As[V], Bz[V], Q2[V], R2[V], Qs[V], Rs[V];
+  loss_affine<V>(p, c0, A2, As, Bz);
 #pragma unroll
   for (int j = 0; j < V; ++j) {
-    const int c = c0 + j;
-    sg[j] = red_f[c];
-    sgx2[j] = red_f[p.C + c];
-    sgxs[j] = red_f[2 * p.C + c];
-    k2[j] = (ch.g2[j] * ch.r2[j]) / mf;
-    ks[j] = (ch.gs[j] * ch.rs[j]) / mf;
+    Q2[j] = coef[c0 + j];
+    R2[j] = coef[p.C + c0 + j];
+    Qs[j] = coef[2 * p.C + c0 + j];
+    Rs[j] = coef[3 * p.C + c0 + j];
   }
   const int step = gridDim.x * rpp;
 #pragma unroll 2
   for (int r = blockIdx.x * rpp + slot; r < p.m; r += step) {
     const size_t off = static_cast<size_t>(r) * p.C + c0;
-    float g[V], xh2[V], xhs[V], d[V], o2[V], os[V];
-    ch.point(p, off, g, xh2, xhs, d);
+    float y2[V], ys[V], t[V], o2[V], os[V];
+    Vec<V>::load(p.y2 + off, y2);
+    Vec<V>::load(p.ys + off, ys);
+    Vec<V>::load(p.t + off, t);
 #pragma unroll
     for (int j = 0; j < V; ++j) {
-      const float base = fmaf(mf, g[j], -sg[j]);
-      o2[j] = k2[j] * fmaf(-xh2[j], sgx2[j], base);
-      os[j] = ks[j] * fmaf(-xhs[j], sgxs[j], base);
+      const float z = fmaf(A2[j], y2[j], fmaf(As[j], ys[j], Bz[j]));
+      const float d = (z > 0.0f ? z : 0.0f) - t[j];
+      const float g = z > 0.0f ? d * p.gscale : 0.0f;
+      o2[j] = fmaf(A2[j], g, fmaf(Q2[j], y2[j], R2[j]));
+      os[j] = fmaf(As[j], g, fmaf(Qs[j], ys[j], Rs[j]));
     }
     Vec<V>::store(dy2 + off, o2);
     Vec<V>::store(dys + off, os);
   }
 }
 
-// -- BN backward (first BN of the unit): reductions and apply
+// -- BN backward (first BN of the unit): partial sums of g and g*y, finalize, apply
 template <int V>
 __global__ void __launch_bounds__(kThreads) bn_bwd_partial_kernel(const __nv_bfloat16* __restrict__ gin,
-                                                                  const __nv_bfloat16* __restrict__ y,
-                                                                  const float* __restrict__ st, int m, int C,
+                                                                  const __nv_bfloat16* __restrict__ y, int m, int C,
                                                                   int rows_per_chunk, int cg, int rpp,
                                                                   float* __restrict__ partial) {
   const int gi = threadIdx.x % cg;
   const int slot = threadIdx.x / cg;
   float acc[2][V] = {};
   if (slot < rpp) {
-    const int c0 = gi * V;
-    float mu[V], rs[V];
-#pragma unroll
-    for (int j = 0; j < V; ++j) {
-      mu[j] = st[c0 + j];
-      rs[j] = st[C + c0 + j];
-    }
     const int r0 = blockIdx.x * rows_per_chunk;
     const int r1 = min(m, r0 + rows_per_chunk);
 #pragma unroll 2
     for (int r = r0 + slot; r < r1; r += rpp) {
-      const size_t off = static_cast<size_t>(r) * C + c0;
+      const size_t off = static_cast<size_t>(r) * C + gi * V;
       float fg[V], fy[V];
       Vec<V>::load(gin + off, fg);
       Vec<V>::load(y + off, fy);
 #pragma unroll
       for (int j = 0; j < V; ++j) {
-        const float xh = (fy[j] - mu[j]) * rs[j];
         acc[0][j] += fg[j];
-        acc[1][j] += fg[j] * xh;
+        acc[1][j] += fg[j] * fy[j];
       }
     }
   }
   cta_reduce_store<2, V>(acc, cg, rpp, C, partial);
 }
 
-__global__ void bn_bwd_finalize_kernel(const float* __restrict__ partial, int chunks, int C, float* __restrict__ red_f,
-                                       float* __restrict__ dgamma, float* __restrict__ dbeta) {
-  const int o = blockIdx.x * kFinWarps + (threadIdx.x >> 5);  // o in [0, 2C)
-  if (o >= 2 * C) return;
-  const double sv = warp_sum_chunks<2>(partial, chunks, C, o);
+// coef[0:C] = Q, coef[C:2C] = R of dy = A*g + Q*y + R
+__global__ void bn_bwd_finalize_kernel(const float* __restrict__ partial, int chunks, int C, int m,
+                                       const float* __restrict__ st, const float* __restrict__ gamma,
+                                       float* __restrict__ coef, float* __restrict__ dgamma,
+                                       float* __restrict__ dbeta) {
+  const int c = blockIdx.x * kFinWarps + (threadIdx.x >> 5);
+  if (c >= C) return;
+  const double sg = warp_sum_chunks<2>(partial, chunks, C, c);
+  const double sgy = warp_sum_chunks<2>(partial, chunks, C, C + c);
   if ((threadIdx.x & 31) == 0) {
-    const int v = o / C;
-    const int c = o - v * C;
-    const float f = static_cast<float>(sv);
-    red_f[o] = f;
-    if (v == 0)
-      dbeta[c] = f;
-    else
-      dgamma[c] = f;
+    const float mu = st[c], rs = st[C + c];
+    const float A = gamma[c] * rs;
+    const double sgx = static_cast<double>(rs) * (sgy - static_cast<double>(mu) * sg);
+    dbeta[c] = static_cast<float>(sg);
+    dgamma[c] = static_cast<float>(sgx);
+    const double k = static_cast<double>(A) / m;
+    coef[c] = static_cast<float>(-k * sgx * rs);
+    coef[C + c] = static_cast<float>(-k * (sg - sgx * rs * mu));
   }
 }
 
@@ -532,22 +523,18 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_apply_kernel(const __nv_bfloa
                                                                 const __nv_bfloat16* __restrict__ y,
                                                                 const float* __restrict__ st,
                                                                 const float* __restrict__ gamma,
-                                                                const float* __restrict__ red_f, int m, int C, int cg,
+                                                                const float* __restrict__ coef, int m, int C, int cg,
                                                                 int rpp, __nv_bfloat16* __restrict__ dy) {
   const int gi = threadIdx.x % cg;
   const int slot = threadIdx.x / cg;
   if (slot >= rpp) return;
   const int c0 = gi * V;
-  const float mf = static_cast<float>(m);
-  float mu[V], rs[V], k1[V], sg[V], sgx[V];
+  float A[V], Q[V], R[V];
 #pragma unroll
   for (int j = 0; j < V; ++j) {
-    const int c = c0 + j;
-    mu[j] = st[c];
-    rs[j] = st[C + c];
-    k1[j] = (gamma[c] * rs[j]) / mf;
-    sg[j] = red_f[c];
-    sgx[j] = red_f[C + c];
+    A[j] = gamma[c0 + j] * st[C + c0 + j];
+    Q[j] = coef[c0 + j];
+    R[j] = coef[C + c0 + j];
   }
   const int step = gridDim.x * rpp;
 #pragma unroll 2
@@ -557,10 +544,7 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_apply_kernel(const __nv_bfloa
     Vec<V>::load(gin + off, fg);
     Vec<V>::load(y + off, fy);
 #pragma unroll
-    for (int j = 0; j < V; ++j) {
-      const float xh = (fy[j] - mu[j]) * rs[j];
-      o[j] = k1[j] * fmaf(-xh, sgx[j], fmaf(mf, fg[j], -sg[j]));
-    }
+    for (int j = 0; j < V; ++j) o[j] = fmaf(A[j], fg[j], fmaf(Q[j], fy[j], R[j]));
     Vec<V>::store(dy + off, o);
   }
 }
@@ -598,10 +582,9 @@ inline int ok(cudaError_t e) { return e == cudaSuccess ? PBDK_OK : PBDK_ECUDA; }
 }  // namespace
 
 size_t reduce_workspace_floats(int m, int c, int nv) {
-  const RowTiling t = tiling_for(m, c, 4);  // the finest tiling any of the reductions uses
-  const RowTiling t8 = tiling_for(m, c, 8);
-  const int chunks = std::max(t.chunks, t8.chunks);
-  return static_cast<size_t>(chunks) * nv * c + chunks;
+  int chunks = 1;
+  for (int v : {4, 8}) chunks = std::max(chunks, tiling_for(m, c, v).chunks);
+  return static_cast<size_t>(chunks) * std::max(nv, 4) * c + chunks;
 }
 
 int philox_image(void* x, int n, long long first, const long long* counter, int gb, uint32_t seed, cudaStream_t st) {
@@ -631,9 +614,21 @@ int fill(float* dst, size_t n, float v, cudaStream_t st) {
 int bn_stats(const void* y, int m, int c, float* ws, float* mean_rstd, cudaStream_t st) {
   if (c % 8 != 0 || c / 8 > kThreads) return PBDK_EINVAL;
   const RowTiling t = tiling_for(m, c, 8);
-  bn_stats_partial_kernel<8><<<t.chunks, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(y), m, c,
-                                                            t.rows_per_chunk, t.cg, t.rpp, ws);
-  bn_stats_finalize_kernel<<<(c + kFinWarps - 1) / kFinWarps, kFinWarps * 32, 0, st>>>(ws, t.chunks, c, m, mean_rstd);
+  bn_stats_partial_kernel<8, 1><<<t.chunks, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(y), nullptr, m, c,
+                                                               t.rows_per_chunk, t.cg, t.rpp, ws);
+  bn_stats_finalize_kernel<1><<<(c + kFinWarps - 1) / kFinWarps, kFinWarps * 32, 0, st>>>(ws, t.chunks, c, m,
+                                                                                          mean_rstd, nullptr);
+  return ok(cudaGetLastError());
+}
+
+int bn_stats2(const void* y0, const void* y1, int m, int c, float* ws, float* mr0, float* mr1, cudaStream_t st) {
+  if (c % 8 != 0 || c / 8 > kThreads) return PBDK_EINVAL;
+  const RowTiling t = tiling_for(m, c, 8);
+  bn_stats_partial_kernel<8, 2><<<t.chunks, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(y0),
+                                                               static_cast<const __nv_bfloat16*>(y1), m, c,
+                                                               t.rows_per_chunk, t.cg, t.rpp, ws);
+  bn_stats_finalize_kernel<2><<<(2 * c + kFinWarps - 1) / kFinWarps, kFinWarps * 32, 0, st>>>(ws, t.chunks, c, m, mr0,
+                                                                                              mr1);
   return ok(cudaGetLastError());
 }
 
@@ -648,19 +643,20 @@ int bn_apply_relu(const void* y, const float* mean_rstd, const float* gamma, con
 }
 
 int mse_bn_loss(const MseArgs& a, cudaStream_t st) {
-  if (a.c % kLossV != 0 || a.c / kLossV > kThreads) return PBDK_EINVAL;
+  if (a.c % 8 != 0 || a.c / kLossApplyV > kThreads) return PBDK_EINVAL;
   LossParams p{static_cast<const __nv_bfloat16*>(a.y2), static_cast<const __nv_bfloat16*>(a.ysc),
                static_cast<const __nv_bfloat16*>(a.t), a.stats2, a.statssc, a.gamma2, a.beta2, a.gammasc, a.betasc,
                a.m, a.c, a.gscale};
-  const RowTiling t = tiling_for(a.m, a.c, kLossV);
+  const RowTiling t = tiling_for(a.m, a.c, kLossPartialV);
   float* partial = a.ws;
   float* loss_partial = a.ws + static_cast<size_t>(t.chunks) * 3 * a.c;
   loss_partial_kernel<<<t.chunks, kThreads, 0, st>>>(p, t.rows_per_chunk, t.cg, t.rpp, partial, loss_partial);
-  loss_finalize_kernel<<<(3 * a.c + kFinWarps - 1) / kFinWarps + 1, kFinWarps * 32, 0, st>>>(
-      partial, loss_partial, t.chunks, a.c, a.norm, a.red, a.dgamma2, a.dbeta2, a.dgammasc, a.dbetasc, a.loss);
-  loss_bwd_apply_kernel<<<apply_grid(a.m, t.rpp), kThreads, 0, st>>>(p, a.red, t.cg, t.rpp,
-                                                                     static_cast<__nv_bfloat16*>(a.dy2),
-                                                                     static_cast<__nv_bfloat16*>(a.dysc));
+  loss_finalize_kernel<<<(a.c + kFinWarps - 1) / kFinWarps + 1, kFinWarps * 32, 0, st>>>(
+      p, partial, loss_partial, t.chunks, a.norm, a.red, a.dgamma2, a.dbeta2, a.dgammasc, a.dbetasc, a.loss);
+  const RowTiling ta = tiling_for(a.m, a.c, kLossApplyV);
+  loss_bwd_apply_kernel<<<apply_grid(a.m, ta.rpp), kThreads, 0, st>>>(p, a.red, ta.cg, ta.rpp,
+                                                                      static_cast<__nv_bfloat16*>(a.dy2),
+                                                                      static_cast<__nv_bfloat16*>(a.dysc));
   return ok(cudaGetLastError());
 }
 
@@ -669,9 +665,10 @@ int bn_bwd(const void* g, const void* y, const float* mean_rstd, const float* ga
   if (c % 8 != 0 || c / 8 > kThreads) return PBDK_EINVAL;
   const RowTiling t = tiling_for(m, c, 8);
   bn_bwd_partial_kernel<8><<<t.chunks, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(g),
-                                                          static_cast<const __nv_bfloat16*>(y), mean_rstd, m, c,
+                                                          static_cast<const __nv_bfloat16*>(y), m, c,
                                                           t.rows_per_chunk, t.cg, t.rpp, ws);
-  bn_bwd_finalize_kernel<<<(2 * c + kFinWarps - 1) / kFinWarps, kFinWarps * 32, 0, st>>>(ws, t.chunks, c, red, dgamma, dbeta);
+  bn_bwd_finalize_kernel<<<(c + kFinWarps - 1) / kFinWarps, kFinWarps * 32, 0, st>>>(ws, t.chunks, c, m, mean_rstd,
+                                                                                    gamma, red, dgamma, dbeta);
   bn_bwd_apply_kernel<8><<<apply_grid(m, t.rpp), kThreads, 0, st>>>(
       static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(y), mean_rstd, gamma, red, m, c, t.cg,
       t.rpp, static_cast<__nv_bfloat16*>(dy));

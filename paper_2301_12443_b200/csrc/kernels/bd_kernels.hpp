@@ -39,6 +39,8 @@ int init_uniform(void* dst, int bf16_out, int k, int r, int s, int cs, int ct, u
                  float bound, cudaStream_t st);
 int fill(float* dst, size_t n, float v, cudaStream_t st);
 int bn_stats(const void* y, int m, int c, float* ws, float* mean_rstd, cudaStream_t st);
+// statistics of two same-shape tensors in one pass (the student's y2 and shortcut y)
+int bn_stats2(const void* y0, const void* y1, int m, int c, float* ws, float* mr0, float* mr1, cudaStream_t st);
 int bn_apply_relu(const void* y, const float* mean_rstd, const float* gamma, const float* beta, void* a, int m, int c,
                   cudaStream_t st);
 int mse_bn_loss(const MseArgs& a, cudaStream_t st);
