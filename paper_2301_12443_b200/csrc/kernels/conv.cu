@@ -879,9 +879,11 @@ int wgrad_splits(const ConvGeom& g) {
   const int co_tiles = (g.d.k + 127) / 128;
   const int ci_tiles = g.d.c / wgrad_bn(g.d.c);
   const int tiles = co_tiles * ci_tiles * g.d.r * g.d.s;
-  const int target = 2 * 148;
+  // one wave of CTAs: the student streams run concurrently, so the wgrads need not fill the
+  // GPU alone, and every split costs a partial slab in the fixed-order reduction.
+  const int target = 148;
   int splits = std::max(1, target / tiles);
-  splits = std::min(splits, std::max(1, g.m_tiles / 4));  // >= 4 pixel tiles per split
+  splits = std::min(splits, std::max(1, g.m_tiles / 8));  // >= 8 pixel tiles per split
   return splits;
 }
 
