@@ -86,6 +86,11 @@ int pbdx_num_blocks(void* handle);
 /* teacher output t_k (bf16 NHWC [n_max][H][W][C]) of block k inside the partition */
 int pbdx_teacher_act(void* handle, int block, void** ptr, size_t* bytes);
 
+/* Re-derive the bf16 GEMM shadows (and flipped dgrad weights) from the fp32 master weights after
+ * the driver overwrote PBDX_BUF_PARAMS / PBDX_BUF_MOMENTUM (state migration on reconfiguration).
+ * Requires PBDX_BUF_GRADS to be zero (momentum is kept unchanged). */
+int pbdx_refresh_shadows(void* handle, void* stream);
+
 /* Per-block CUDA-event timing of the last step (ms): teacher[k], student[k] for k in the range. */
 int pbdx_set_timing(void* handle, int enabled);
 int pbdx_block_times(void* handle, float* teacher_ms, float* student_ms);

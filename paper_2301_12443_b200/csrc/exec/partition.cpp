@@ -287,6 +287,12 @@ class Partition {
     for (SBlock& s : sblocks_) cuda(cudaStreamWaitEvent(caller, s.done, 0), "join");
   }
 
+  // bf16 shadows + flipped dgrad weights from the fp32 master weights (after a state migration)
+  void refresh_shadows(cudaStream_t st) {
+    check(pbdk::sgd_momentum(params_, mom_, grads_, shadow_, total_, 0.0f, 1.0f, nullptr, st), "shadow");
+    refresh_flips(st);
+  }
+
   void apply_update(cudaStream_t st) {
     check(pbdk::sgd_momentum(params_, mom_, grads_, shadow_, total_, d_.lr, d_.momentum, step_, st), "sgd");
     refresh_flips(st);
@@ -717,6 +723,7 @@ int pbdx_num_blocks(void* h) { return P(h)->nblocks(); }
 int pbdx_teacher_act(void* h, int block, void** ptr, size_t* bytes) {
   return guard([&] { P(h)->teacher_act(block, ptr, bytes); });
 }
+int pbdx_refresh_shadows(void* h, void* st) { return guard([&] { P(h)->refresh_shadows(S(st)); }); }
 int pbdx_set_timing(void* h, int enabled) { return guard([&] { P(h)->set_timing(enabled != 0); }); }
 int pbdx_block_times(void* h, float* t, float* s) { return guard([&] { P(h)->block_times(t, s); }); }
 int pbdx_launches_per_step(void* h) { return P(h)->launches_per_step(); }

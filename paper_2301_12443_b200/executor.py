@@ -53,6 +53,7 @@ def _bind(L):
     L.pbdx_student_layout.argtypes = [I, P(ctypes.c_long)]
     L.pbdx_student_layout.restype = ctypes.c_long
     L.pbdx_launches_per_step.argtypes = [V]
+    L.pbdx_refresh_shadows.argtypes = [V, V]
     L._pbdx_bound = True
     return L
 
@@ -238,3 +239,32 @@ class Partition:
 
     def losses(self) -> List[float]:
         return self.losses_tensor().cpu().tolist()
+
+    # -- state migration (runtime.PipeBD.migrate)
+    def block_state(self, k: int) -> List[torch.Tensor]:
+        """[weights, momentum] of student block k (fp32, padded layout) — views into device memory."""
+        base, _, total = self.layouts[k]
+        return [self.params()[base:base + total], self.momentum()[base:base + total]]
+
+    def block_state_like(self, k: int) -> List[torch.Tensor]:
+        """Receive buffers for any block's state (owned by this partition or not)."""
+        _, total = student_layout(k)
+        return [torch.empty(total, dtype=torch.float32, device=self.device) for _ in range(2)]
+
+    def set_block_state(self, k: int, weights: torch.Tensor, momentum: torch.Tensor):
+        """Overwrite block k's master weights and momentum, then refresh the bf16 shadows (an SGD
+        launch with zero gradient and lr 0 is an exact cast)."""
+        w, v = self.block_state(k)
+        w.copy_(weights)
+        v.copy_(momentum)
+        self.grads().zero_()
+        self._refresh_shadows()
+
+    def _refresh_shadows(self):
+        _check(lib().pbdx_refresh_shadows(self.handle, self._stream(None)), "refresh_shadows")
+
+    def step_index(self) -> int:
+        return int(self.step_counter().item())
+
+    def set_step_index(self, step: int):
+        self.step_counter().fill_(int(step))

@@ -170,6 +170,88 @@ class PipeBD:
         self._finish_sends()
         dist.barrier()
 
+    # -- reconfiguration (schedule.cpp:347-359): at an epoch boundary
+    def measured_block_times(self) -> Dict[int, Tuple[int, float, float]]:
+        """{block: (per-device batch, teacher ms, student ms)} of this rank's blocks (needs timing on)."""
+        if not hasattr(self.stage, "block_times"):
+            return {}
+        t, s = self.stage.block_times()
+        return {k: (self.me.per_device_batch, t[i], s[i]) for i, k in enumerate(range(self.me.block_lo,
+                                                                                     self.me.block_hi + 1))}
+
+    def maybe_reconfigure(self, profile: dict, threshold: float, make_stage: Callable,
+                          measured: Optional[Dict[int, Tuple[int, float, float]]] = None) -> Optional[dict]:
+        """Gather the monitored block times, re-plan on rank 0 with reconfigure(), broadcast the
+        decision and migrate if the schedule changed.  Returns the new schedule or None."""
+        mine = measured if measured is not None else self.measured_block_times()
+        gathered = [None] * self.world
+        dist.all_gather_object(gathered, mine)
+        obj = [None]
+        if self.rank == 0:
+            merged = {}
+            for d in gathered:
+                for k, v in (d or {}).items():
+                    merged.setdefault(int(k), v)
+            observed = observed_profile(profile, merged)
+            obj = [core.reconfigure(profile, self.schedule, observed, threshold)]
+        dist.broadcast_object_list(obj, src=0)
+        new = obj[0]
+        if new is not None and new["partitions"] != self.schedule["partitions"]:
+            self.migrate(new, make_stage)
+            return new
+        return None
+
+    def migrate(self, new_schedule: dict, make_stage: Callable):
+        """Move every student block's weights and momentum from its old owners to its new owners
+        (P2P from the first member of the old group), rebuild the stage, communicators and relay
+        plan, and keep the data stream's step index."""
+        self._finish_sends()
+        old_place, new_place = self.place, placements(new_schedule, self.b)
+        step_index = self.stage.step_index()
+        B = len({k for p in self.schedule["partitions"] for k in range(p["blocks"][0], p["blocks"][1] + 1)})
+        # current state of the blocks this rank owns (identical across its DP group after sync)
+        state = {k: self.stage.block_state(k) for k in range(self.me.block_lo, self.me.block_hi + 1)}
+        nme = new_place[self.rank]
+        incoming = {}
+        ops = []
+        for k in range(B):
+            src = next(r for r, pl in sorted(old_place.items()) if pl.block_lo <= k <= pl.block_hi)
+            owners = [r for r, pl in sorted(new_place.items()) if pl.block_lo <= k <= pl.block_hi]
+            if self.rank == src:
+                for dst in owners:
+                    if dst != src:
+                        ops += [dist.P2POp(dist.isend, t, dst) for t in state[k]]
+            if self.rank in owners and self.rank != src:
+                bufs = self.stage.block_state_like(k)
+                incoming[k] = bufs
+                ops += [dist.P2POp(dist.irecv, b_, src) for b_ in bufs]
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        for k in range(nme.block_lo, nme.block_hi + 1):
+            if k not in incoming:
+                incoming[k] = state[k]
+        # rebuild this rank's share of the new schedule
+        self.schedule = new_schedule
+        self.place = new_place
+        self.me = nme
+        self.nparts = len(new_schedule["partitions"])
+        self.groups = {}
+        for j, p in enumerate(new_schedule["partitions"]):
+            devs = list(p["devices"])
+            self.groups[j] = dist.new_group(devs) if len(devs) > 1 else None
+        self.stage = make_stage(nme.block_lo, nme.block_hi, nme.count, nme.first)
+        for k, (w, v) in incoming.items():
+            self.stage.set_block_state(k, w, v)
+        self.stage.set_step_index(step_index)
+        self.recv_msgs = [m for m in relay_plan(new_schedule, self.b, nme.partition) if m[1] == self.rank] \
+            if nme.partition > 0 else []
+        self.send_msgs = [m for m in relay_plan(new_schedule, self.b, nme.partition + 1) if m[0] == self.rank] \
+            if nme.partition + 1 < self.nparts else []
+        self._pending_sends = []
+        if getattr(self, "_graphs", False):
+            self.use_graphs()
+
     def block_losses(self) -> Dict[int, float]:
         """Per-block loss of the last step summed over each DP group (the global-batch MSE)."""
         local = self.stage.losses()

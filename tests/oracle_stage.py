@@ -67,3 +67,21 @@ class OracleStage:
 
     def losses(self):
         return list(self._losses)
+
+    # state migration (runtime.PipeBD.migrate)
+    def block_state(self, k):
+        return [torch.from_numpy(self.sp[k]), torch.from_numpy(self.mom[k])]
+
+    def block_state_like(self, k):  # any block, owned or not
+        n = int(bd.lib().bdo_student_param_count(k))
+        return [torch.empty(n), torch.empty(n)]
+
+    def set_block_state(self, k, w, v):
+        self.sp[k][:] = w.numpy()
+        self.mom[k][:] = v.numpy()
+
+    def step_index(self):
+        return self.step_idx
+
+    def set_step_index(self, step):
+        self.step_idx = int(step)

@@ -215,3 +215,25 @@ def test_phase_graphs_bitwise_equal_eager(ex):
         outs.append((losses, p.params().cpu()))
     assert outs[0][0] == outs[1][0]
     assert torch.equal(outs[0][1], outs[1][1])
+
+
+def test_state_migration_resumes_bitwise(ex):
+    """Reconfiguration support: a fresh executor given another's weights, momentum and step index
+    (block_state / set_block_state / set_step_index) continues bit-identically."""
+    b = 8
+    a = ex.Partition(0, 3, b, b)
+    a.init_params()
+    for _ in range(2):
+        a.step()
+    fresh = ex.Partition(0, 3, b, b)
+    fresh.init_params()
+    for k in range(4):
+        w, v = a.block_state(k)
+        fresh.set_block_state(k, w.clone(), v.clone())
+    fresh.set_step_index(a.step_index())
+    a.step()
+    fresh.step()
+    torch.cuda.synchronize()
+    assert a.losses() == fresh.losses()
+    assert torch.equal(a.params(), fresh.params())
+    assert torch.equal(a.momentum(), fresh.momentum())

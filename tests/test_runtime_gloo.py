@@ -57,7 +57,7 @@ def run_dist(schedule, world, b, steps, dpu=True):
     procs = [ctx.Process(target=_worker, args=(r, world, port, schedule, b, steps, dpu, q)) for r in range(world)]
     for p in procs:
         p.start()
-    out = [q.get(timeout=600) for _ in range(world)]
+    out = [q.get(timeout=240) for _ in range(world)]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -105,3 +105,60 @@ def test_relay_plan_covers_every_row_once():
                     assert fs + so == fd + do
                     got[fd + do: fd + do + rows] += 1
                 assert (got == 1).all()
+
+
+def _migrate_worker(rank, world, port, sched_a, sched_b, b, steps, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    torch.set_num_threads(2)
+    from tests.oracle_stage import OracleStage
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        make = lambda lo, hi, n, first: OracleStage(lo, hi, n, first, b)  # noqa: E731
+        pipe = runtime.PipeBD(sched_a, b, make)
+        for _ in range(steps):
+            pipe.step()
+        pipe.end_epoch()
+        pipe.migrate(sched_b, make)
+        for _ in range(steps):
+            pipe.step()
+        pipe.end_epoch()
+        losses = pipe.block_losses()
+        q.put((rank, losses, {k: pipe.stage.sp[k] for k in pipe.stage.blocks}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_reconfiguration_migrates_state_exactly():
+    """Epoch-boundary re-plan (schedule.cpp:347-359): 2 steps on schedule A, migrate
+    weights + momentum to schedule B, 2 more steps == single process with A's then B's DP shards."""
+    from oracle import bd
+    b, steps, world = 5, 2, 3
+    parts_a = [(0, 0, [0, 1]), (1, 3, [2])]
+    parts_b = [(0, 1, [0]), (2, 3, [1, 2])]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_migrate_worker, args=(r, world, port, sched(parts_a, b), sched(parts_b, b), b, steps, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+
+    def groups(parts):
+        return {k: len(devs) for lo, hi, devs in parts for k in range(lo, hi + 1)}
+
+    tr = bd.Trainer(b, bf16_mode=1)
+    for st in range(steps):
+        tr.step(st, groups(parts_a))
+    for st in range(steps, 2 * steps):
+        want = tr.step(st, groups(parts_b))
+    for rank, losses, params in out:
+        for k, v in losses.items():
+            assert v == pytest.approx(want[k], rel=1e-12, abs=1e-15), (rank, k)
+        for k, p in params.items():
+            np.testing.assert_allclose(p, tr.sp[k], rtol=1e-6, atol=1e-9)
