@@ -69,7 +69,7 @@ __device__ __forceinline__ void fprop_epilogue(const FpropArgs& a, uint32_t trow
   rowmap(row, valid, m);
   const bool has_bias = a.epi == PBDK_EPI_BIAS || a.epi == PBDK_EPI_BIAS_RELU || a.epi == PBDK_EPI_BIAS_RES_RELU;
   const bool relu = a.epi == PBDK_EPI_BIAS_RELU || a.epi == PBDK_EPI_BIAS_RES_RELU;
-  if (a.debug == 3) return;
+  if (a.debug == 3 || a.debug == 9) return;
 #pragma unroll 1
   for (int c0 = 0; c0 < BN; c0 += 16) {
     float v[16];
@@ -279,6 +279,388 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ------------------------------------------------------------------ split-K fprop (clusters + DSMEM)
+// For convs with too few output tiles to fill the GPU (4x4 / 8x8 maps at 256-512 channels) a
+// cluster of S CTAs shares one 128 x BN output tile: CTA s accumulates the K blocks
+// [s*kb/S, (s+1)*kb/S) in its TMEM and stages the fp32 partial in its (by then idle) pipeline
+// shared memory; after a cluster barrier CTA s reduces rows [s*128/S, (s+1)*128/S) over DSMEM,
+// adding the S partials in split order (deterministic), applies the fused epilogue and stores
+// bf16.  No global workspace and no second kernel.
+template <int BN, int BKC>
+struct SplitCfg {
+  using F = FpropCfg<BN, BKC, false>;
+  static constexpr int PITCH = BN + 4;  // floats per staged row; the 16 B pad makes row stores conflict-free
+  static constexpr int TMEM_COLS = tmem_cols_for(BN < 32 ? 32 : BN);
+  static_assert(128 * PITCH * 4 <= F::STAGES * F::STAGE, "partial tile does not fit the ring");
+};
+
+__device__ __forceinline__ void epi_store4(const FpropArgs& a, size_t m, int col, float4 v) {
+  float x[4] = {v.x, v.y, v.z, v.w};
+  const int epi = a.epi;
+  if (epi == PBDK_EPI_BIAS || epi == PBDK_EPI_BIAS_RELU || epi == PBDK_EPI_BIAS_RES_RELU) {
+    const float4 b = __ldg(reinterpret_cast<const float4*>(a.bias + col));
+    x[0] += b.x;
+    x[1] += b.y;
+    x[2] += b.z;
+    x[3] += b.w;
+  }
+  if (epi == PBDK_EPI_BIAS_RES_RELU || epi == PBDK_EPI_RELU_MASK) {
+    const uint2 r = __ldg(reinterpret_cast<const uint2*>(a.aux + m * a.k + col));
+    const float rv[4] = {bf16_lo(r.x), bf16_hi(r.x), bf16_lo(r.y), bf16_hi(r.y)};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (epi == PBDK_EPI_BIAS_RES_RELU) x[j] += rv[j];
+      else x[j] = rv[j] > 0.f ? x[j] : 0.f;
+    }
+  }
+  if (epi == PBDK_EPI_BIAS_RELU || epi == PBDK_EPI_BIAS_RES_RELU) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) x[j] = fmaxf(x[j], 0.f);
+  }
+  uint2 o;
+  o.x = pack_bf16x2(x[0], x[1]);
+  o.y = pack_bf16x2(x[2], x[3]);
+  *reinterpret_cast<uint2*>(a.y + m * a.k + col) = o;
+}
+
+template <int BN, int BKC>
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_fprop_splitk_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
+                             const FpropArgs a) {
+  using F = FpropCfg<BN, BKC, false>;
+  using C = SplitCfg<BN, BKC>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + F::STAGES * F::STAGE);
+  uint64_t* empty = full + F::STAGES;
+  uint64_t* tfull = empty + F::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  float* part = reinterpret_cast<float*>(smem);  // staged partial, reuses the ring
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int splits = static_cast<int>(gridDim.x);
+  const int rank = static_cast<int>(cluster_rank());
+  const int t = blockIdx.y;
+  const int m_tile = t / a.n_tiles;
+  const int k0 = (t - m_tile * a.n_tiles) * BN;
+  const int tq = m_tile % a.tiles_q;
+  const int t2 = m_tile / a.tiles_q;
+  const int tp = t2 % a.tiles_p;
+  const int tn = t2 / a.tiles_p;
+  const int num_kb = a.r * a.s * a.c_chunks;
+  const int kb_lo = rank * num_kb / splits;
+  const int kb_hi = (rank + 1) * num_kb / splits;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmx);
+    tma_prefetch(&tmw);
+    for (int i = 0; i < F::STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(tfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int cin_stored = a.c_chunks * BKC;
+      const int ow0 = tq * a.bw, oh0 = tp * a.bh, n0 = tn * a.bn;
+      int st = 0;
+      uint32_t ph = 0;
+      for (int kb = kb_lo; kb < kb_hi; ++kb) {
+        if (kb - kb_lo >= F::STAGES) mbar_wait(&empty[st], ph ^ 1);
+        const int tap = kb / a.c_chunks;
+        const int cc = kb - tap * a.c_chunks;
+        const int rr = tap / a.s;
+        const int ss = tap - rr * a.s;
+        uint8_t* sa = smem + st * F::STAGE;
+        mbar_arrive_expect_tx(&full[st], F::A_BYTES + F::B_BYTES);
+        tma_load_4d(sa, &tmx, &full[st], cc * BKC, ow0 * a.stride + ss - a.pad, oh0 * a.stride + rr - a.pad, n0);
+        tma_load_2d(sa + F::A_BYTES, &tmw, &full[st], tap * cin_stored + cc * BKC, k0);
+        if (++st == F::STAGES) {
+          st = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(128, BN, 0, 0);
+      const uint64_t adesc0 = umma_smem_desc(smem_u32(smem), 16, 8 * F::SW, F::LAYOUT);
+      int st = 0;
+      uint32_t ph = 0;
+      for (int kb = kb_lo; kb < kb_hi; ++kb) {
+        mbar_wait(&full[st], ph);
+        tc_fence_after();
+        const uint64_t a0 = adesc0 + static_cast<uint32_t>((st * F::STAGE) >> 4);
+        const uint64_t b0 = a0 + static_cast<uint32_t>(F::A_BYTES >> 4);
+#pragma unroll
+        for (int kk = 0; kk < BKC / 16; ++kk)
+          umma_bf16(tmem, a0 + 2 * kk, b0 + 2 * kk, idesc, (kb != kb_lo || kk != 0) ? 1u : 0u);
+        umma_commit(&empty[st]);
+        if (++st == F::STAGES) {
+          st = 0;
+          ph ^= 1;
+        }
+      }
+      umma_commit(tfull);
+    }
+  } else {
+    // stage this CTA's fp32 partial: thread = accumulator row
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+    float4* dst = reinterpret_cast<float4*>(part + row * C::PITCH);
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      float v[16];
+      tmem_ld16(trow + c0, v);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dst[c0 / 4 + j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    }
+    tc_fence_before();
+  }
+  __syncwarp();
+  cluster_sync();
+
+  // reduce rows [rank*128/S, (rank+1)*128/S) across the cluster, fixed split order
+  {
+    const int rows_per = 128 / splits;
+    const TileRows rows{&a, tn * a.bn, tp * a.bh, tq * a.bw};
+    const uint32_t part_u32 = smem_u32(part);
+    for (int r = rank * rows_per + warp; r < (rank + 1) * rows_per; r += kThreads / 32) {
+      bool valid;
+      size_t m;
+      rows(r, valid, m);
+      if (!valid) continue;
+#pragma unroll
+      for (int c4 = lane; c4 < BN / 4; c4 += 32) {
+        const uint32_t off = part_u32 + static_cast<uint32_t>((r * C::PITCH + 4 * c4) * 4);
+        float4 v[8];
+#pragma unroll
+        for (int sp = 0; sp < 8; ++sp)
+          if (sp < splits) v[sp] = dsmem_ld4(dsmem_addr(off, static_cast<uint32_t>(sp)));
+        float4 acc = v[0];
+#pragma unroll
+        for (int sp = 1; sp < 8; ++sp) {
+          if (sp < splits) {
+            acc.x += v[sp].x;
+            acc.y += v[sp].y;
+            acc.z += v[sp].z;
+            acc.w += v[sp].w;
+          }
+        }
+        epi_store4(a, m, k0 + 4 * c4, acc);
+      }
+    }
+  }
+  cluster_sync();  // every CTA's partial stays alive until all reads are done
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+template <int BN, int BKC>
+cudaError_t launch_fprop_splitk(const FpropPlan& p, cudaStream_t stream) {
+  using F = FpropCfg<BN, BKC, false>;
+  if (stream == reinterpret_cast<cudaStream_t>(-1)) {
+    return cudaFuncSetAttribute(conv_fprop_splitk_kernel<BN, BKC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                F::SMEM);
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = p.grid;
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = F::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = p.grid.x;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, conv_fprop_splitk_kernel<BN, BKC>, p.tmx, p.tmw, p.args);
+}
+
+// ------------------------------------------------------------------ 2-CTA fprop (cta_group::2)
+// Each SM ingests at most ~100 B/clk from L2, and a 128 x BN tile with BKC = 64 needs
+// (16 KB A + BN*128 B of B) per K block: 94 B/clk at the MMA rate for BN = 256, 125 for
+// BN = 128, so one-CTA tiles are load-bound.  A CTA pair computes a 256 x BN tile (two
+// consecutive M tiles) with 256 x BN x 16 MMAs issued by the even CTA: each CTA loads its own
+// A box and HALF of the filter tile, so per-SM traffic drops to 16 KB + BN*64 B per K block.
+// Persistent over pair tiles, double-buffered TMEM accumulators, fused register epilogue.
+template <int BN, int BKC>
+struct PairCfg {
+  static constexpr int SW = BKC * 2;
+  static constexpr int LAYOUT = layout_for_sw(SW);
+  static constexpr int A_BYTES = 128 * SW;
+  static constexpr int B_BYTES = (BN / 2) * SW;  // this CTA's half of the filter tile
+  static constexpr int STAGE = round_up(A_BYTES + B_BYTES, 1024);
+  static constexpr int STAGES = (kFpropBudget / STAGE) > 8 ? 8 : (kFpropBudget / STAGE);
+  static constexpr int TMEM_COLS = tmem_cols_for(2 * BN);
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+};
+
+template <int BN, int BKC>
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_fprop_pair_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
+                           const FpropArgs a) {
+  using C = PairCfg<BN, BKC>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);  // leader's are used
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;         // [2], leader's: 4 epilogue warps x 2 CTAs
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int rank = static_cast<int>(cluster_rank());
+  const int pair = blockIdx.x >> 1;
+  const int pairs = gridDim.x >> 1;
+  const int num_kb = a.r * a.s * a.c_chunks;
+  const int total = (a.m_tiles >> 1) * a.n_tiles;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmx);
+    tma_prefetch(&tmw);
+    for (int i = 0; i < C::STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_pair(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int cin_stored = a.c_chunks * BKC;
+      int it = 0, st = 0;
+      uint32_t ph = 0;
+      for (int t = pair; t < total; t += pairs) {
+        const int mp = t / a.n_tiles;
+        const int k0 = (t - mp * a.n_tiles) * BN;
+        const int m_tile = 2 * mp + rank;
+        const int tq = m_tile % a.tiles_q;
+        const int t2 = m_tile / a.tiles_q;
+        const int tp = t2 % a.tiles_p;
+        const int tn = t2 / a.tiles_p;
+        const int ow0 = tq * a.bw, oh0 = tp * a.bh, n0 = tn * a.bn;
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          if (it >= C::STAGES) mbar_wait(&empty[st], ph ^ 1);
+          const uint32_t fb = dsmem_addr(smem_u32(&full[st]), 0);  // leader's full barrier
+          if (rank == 0) mbar_arrive_expect_tx(&full[st], 2 * (C::A_BYTES + C::B_BYTES));
+          const int tap = kb / a.c_chunks;
+          const int cc = kb - tap * a.c_chunks;
+          const int rr = tap / a.s;
+          const int ss = tap - rr * a.s;
+          uint8_t* sa = smem + st * C::STAGE;
+          tma_load_4d_pair(sa, &tmx, fb, cc * BKC, ow0 * a.stride + ss - a.pad, oh0 * a.stride + rr - a.pad, n0);
+          tma_load_2d_pair(sa + C::A_BYTES, &tmw, fb, tap * cin_stored + cc * BKC, k0 + rank * (BN / 2));
+          if (++st == C::STAGES) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(256, BN, 0, 0);
+      const uint64_t adesc0 = umma_smem_desc(smem_u32(smem), 16, 8 * C::SW, C::LAYOUT);
+      int st = 0, lt = 0;
+      uint32_t ph = 0;
+      for (int t = pair; t < total; t += pairs, ++lt) {
+        const int acc = lt & 1;
+        if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t dacc = tmem + static_cast<uint32_t>(acc * BN);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[st], ph);
+          tc_fence_after();
+          const uint64_t a0 = adesc0 + static_cast<uint32_t>((st * C::STAGE) >> 4);
+          const uint64_t b0 = a0 + static_cast<uint32_t>(C::A_BYTES >> 4);
+#pragma unroll
+          for (int kk = 0; kk < BKC / 16; ++kk)
+            umma_bf16_pair(dacc, a0 + 2 * kk, b0 + 2 * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
+          umma_commit_pair(&empty[st]);
+          if (++st == C::STAGES) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+        umma_commit_pair(&tfull[acc]);
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    int lt = 0;
+    for (int t = pair; t < total; t += pairs, ++lt) {
+      const int acc = lt & 1;
+      mbar_wait(&tfull[acc], (lt >> 1) & 1);
+      tc_fence_after();
+      const int mp = t / a.n_tiles;
+      const int k0 = (t - mp * a.n_tiles) * BN;
+      const int m_tile = 2 * mp + rank;
+      const int tq = m_tile % a.tiles_q;
+      const int t2 = m_tile / a.tiles_q;
+      const TileRows rows{&a, (t2 / a.tiles_p) * a.bn, (t2 % a.tiles_p) * a.bh, tq * a.bw};
+      const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * BN);
+      fprop_epilogue<BN>(a, trow, quarter * 32 + lane, k0, rows);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(dsmem_addr(smem_u32(&tempty[acc]), 0));
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, C::TMEM_COLS);
+  }
+}
+
+template <int BN, int BKC>
+cudaError_t launch_fprop_pair(const FpropPlan& p, cudaStream_t stream) {
+  using C = PairCfg<BN, BKC>;
+  if (stream == reinterpret_cast<cudaStream_t>(-1)) {
+    return cudaFuncSetAttribute(conv_fprop_pair_kernel<BN, BKC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                C::SMEM);
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = p.grid;
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, conv_fprop_pair_kernel<BN, BKC>, p.tmx, p.tmw, p.args);
+}
+
 // ------------------------------------------------------------------ halo fprop (3x3, stride 1, pad 1)
 // For wide images (W = 32) the per-tap boxes re-read every input pixel 9 times through L2.
 // Here the GEMM rows index a zero-padded image: output position p = h*(W+2) + w' (w' in
@@ -287,7 +669,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 // smem tile read from row offset (p0 % (W+2)) + r*(W+2) + s: all 9 taps come from a single
 // load, so activation traffic drops ~5x for a ~6% row overhead (32x32: 9 tiles of 128 rows
 // cover the 1088 padded positions of an image).  Filters stay resident in shared memory.
-template <int BN, int BKC>
+//
+// The MMA issuer is instruction-latency bound unless every descriptor offset is a compile-time
+// constant (measured: 74 cycles/MMA with runtime row/tap strides vs the 48-cycle SS-operand
+// rate at N = 64), so the padded width WP is a template parameter and the resident filter is
+// laid out [channel chunk][tap]: per tile only the stage base and j0 = p0 % WP are runtime.
+template <int BN, int BKC, int WP>
 struct HaloCfg {
   static constexpr int SW = BKC * 2;
   static constexpr int LAYOUT = layout_for_sw(SW);
@@ -295,36 +682,38 @@ struct HaloCfg {
   static constexpr int B_RES_MAX = 96 * 1024;
   static constexpr int ACC_COLS = BN < 32 ? 32 : BN;
   static constexpr int TMEM_COLS = tmem_cols_for(2 * ACC_COLS);
-  static constexpr int SMEM = kFpropBudget + 1024 + 256;
+  static constexpr int ROWS = 3 + (129 + WP - 1) / WP;  // padded rows one 128-row tile touches
+  static constexpr int BOX_BYTES = ROWS * WP * SW;
+  static constexpr int STAGE = round_up(BOX_BYTES, 1024);
+  static constexpr int STAGES = ((kFpropBudget - B_RES_MAX) / STAGE) > 8 ? 8 : ((kFpropBudget - B_RES_MAX) / STAGE);
+  static constexpr int SMEM = STAGES * STAGE + B_RES_MAX + 1024 + 256;
+  static_assert(STAGES >= 2, "halo stage does not fit");
 };
 
-template <int BN, int BKC>
+template <int BN, int BKC, int WP>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_fprop_halo_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
                            const FpropArgs a) {
-  using C = HaloCfg<BN, BKC>;
+  using C = HaloCfg<BN, BKC, WP>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  const int stages = a.halo_stages;
-  const int stage_bytes = a.halo_stage_bytes;
-  uint8_t* bres = smem + stages * stage_bytes;
+  uint8_t* bres = smem + C::STAGES * C::STAGE;
   uint64_t* full = reinterpret_cast<uint64_t*>(bres + C::B_RES_MAX);
-  uint64_t* empty = full + 8;
-  uint64_t* tfull = empty + 8;
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* bfull = tempty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
 
   const int warp = warp_id();
   const int lane = lane_id();
-  const int wp = a.q + 2;
-  const int taps = a.r * a.s;
   const int total = a.m_tiles;  // single N tile
+  const int chunks = a.c_chunks;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmx);
     tma_prefetch(&tmw);
-    for (int i = 0; i < stages; ++i) {
+    for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
@@ -343,108 +732,80 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      const int cin_stored = a.c_chunks * BKC;
-      const int num_kb = taps * a.c_chunks;
-      mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(num_kb * C::B_BYTES));
-      for (int kb = 0; kb < num_kb; ++kb) {
-        const int tap = kb / a.c_chunks;
-        const int cc = kb - tap * a.c_chunks;
-        tma_load_2d(bres + kb * C::B_BYTES, &tmw, bfull, tap * cin_stored + cc * BKC, 0);
-      }
-      const uint32_t box_bytes = static_cast<uint32_t>(a.halo_rows * wp * C::SW);
-      int it = 0;
+      const int cin_stored = chunks * BKC;
+      mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(9 * chunks * C::B_BYTES));
+      for (int cc = 0; cc < chunks; ++cc)
+        for (int tap = 0; tap < 9; ++tap)
+          tma_load_2d(bres + (cc * 9 + tap) * C::B_BYTES, &tmw, bfull, tap * cin_stored + cc * BKC, 0);
+      int it = 0, st = 0;
+      uint32_t ph = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         const int img = t / a.tiles_img;
         const int p0 = (t - img * a.tiles_img) * 128;
-        for (int cc = 0; cc < a.c_chunks; ++cc, ++it) {
-          const int st = it % stages;
-          if (it >= stages) mbar_wait(&empty[st], ((it / stages) - 1) & 1);
-          mbar_arrive_expect_tx(&full[st], box_bytes);
-          tma_load_4d(smem + st * stage_bytes, &tmx, &full[st], cc * BKC, -1, p0 / wp - 1, img);
+        for (int cc = 0; cc < chunks; ++cc, ++it) {
+          if (it >= C::STAGES) mbar_wait(&empty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&full[st], C::BOX_BYTES);
+          tma_load_4d(smem + st * C::STAGE, &tmx, &full[st], cc * BKC, -1, p0 / WP - 1, img);
+          if (++st == C::STAGES) {
+            st = 0;
+            ph ^= 1;
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc_bf16(128, BN, 0, 0);
+      // Descriptors advance by adding (byte offset >> 4) to the start-address field (smem
+      // addresses < 256 KB never carry out of the 14-bit field).
+      const uint64_t adesc0 = umma_smem_desc(smem_u32(smem), 16, 8 * C::SW, C::LAYOUT);
+      const uint64_t bdesc0 = umma_smem_desc(smem_u32(bres), 16, 8 * C::SW, C::LAYOUT);
       mbar_wait(bfull, 0);
-      int it = 0, lt = 0;
-      long long c_start = clock64(), c_tempty = 0, c_full = 0, c_issue = 0;
+      int lt = 0, st = 0;
+      uint32_t ph = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
         const int acc = lt & 1;
-        long long c0 = clock64();
         if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
-        c_tempty += clock64() - c0;
         tc_fence_after();
         const uint32_t dacc = tmem + static_cast<uint32_t>(acc * C::ACC_COLS);
-        const int img = t / a.tiles_img;
-        const int p0 = (t - img * a.tiles_img) * 128;
-        const int j0 = p0 % wp;
-        // Descriptors are advanced by adding (byte offset >> 4) to the start-address field
-        // (smem addresses < 256 KB never carry out of the 14-bit field): no per-MMA rebuild.
-        const uint32_t row_step = static_cast<uint32_t>(wp * C::SW) >> 4;     // +1 filter row (r)
-        const uint32_t tap_step = static_cast<uint32_t>(a.c_chunks * C::B_BYTES) >> 4;
-        for (int cc = 0; cc < a.c_chunks; ++cc, ++it) {
-          const int st = it % stages;
-          long long c1 = clock64();
-          mbar_wait(&full[st], (it / stages) & 1);
-          long long c2 = clock64();
-          c_full += c2 - c1;
+        const int j0 = (t % a.tiles_img) * 128 % WP;
+        for (int cc = 0; cc < chunks; ++cc) {
+          mbar_wait(&full[st], ph);
           tc_fence_after();
-          const uint64_t a0 =
-              umma_smem_desc(smem_u32(smem + st * stage_bytes) + static_cast<uint32_t>(j0 * C::SW), 16, 8 * C::SW,
-                             C::LAYOUT);
-          const uint64_t b0 = umma_smem_desc(smem_u32(bres + cc * C::B_BYTES), 16, 8 * C::SW, C::LAYOUT);
+          const uint64_t a0 = adesc0 + static_cast<uint32_t>((st * C::STAGE + j0 * C::SW) >> 4);
+          const uint64_t b0 = bdesc0 + static_cast<uint32_t>((cc * 9 * C::B_BYTES) >> 4);
 #pragma unroll
-          for (int rr = 0; rr < 3; ++rr) {
+          for (int tap = 0; tap < 9; ++tap) {
 #pragma unroll
-            for (int ss = 0; ss < 3; ++ss) {
-#pragma unroll
-              for (int kk = 0; kk < BKC / 16; ++kk) {
-                const uint64_t ad = a0 + rr * row_step + static_cast<uint32_t>((ss * C::SW + kk * 32) >> 4);
-                const uint64_t bd = b0 + (rr * 3 + ss) * tap_step + static_cast<uint32_t>((kk * 32) >> 4);
-                const uint32_t accum = (cc != 0 || rr != 0 || ss != 0 || kk != 0) ? 1u : 0u;
-                if (a.debug != 2) umma_bf16(dacc, ad, bd, idesc, accum);
-              }
+            for (int kk = 0; kk < BKC / 16; ++kk) {
+              const uint32_t aoff = static_cast<uint32_t>((((tap / 3) * WP + tap % 3) * C::SW + kk * 32) >> 4);
+              const uint32_t boff = static_cast<uint32_t>((tap * C::B_BYTES + kk * 32) >> 4);
+              umma_bf16(dacc, a0 + aoff, b0 + boff, idesc, (cc | tap | kk) != 0 ? 1u : 0u);
             }
           }
           umma_commit(&empty[st]);
-          c_issue += clock64() - c2;
+          if (++st == C::STAGES) {
+            st = 0;
+            ph ^= 1;
+          }
         }
         umma_commit(&tfull[acc]);
-      }
-      if (a.debug == 4) {
-        long long* d = a.dbg_buf + blockIdx.x * 8;
-        d[0] = clock64() - c_start;
-        d[1] = c_tempty;
-        d[2] = c_full;
-        d[3] = c_issue;
-        d[6] = lt;
       }
     }
   } else {
     const int quarter = warp & 3;
     int lt = 0;
-    long long e_wait = 0, e_work = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
       const int acc = lt & 1;
-      long long c0 = clock64();
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
-      long long c1 = clock64();
-      e_wait += c1 - c0;
       tc_fence_after();
       const int img = t / a.tiles_img;
-      const HaloRows rows{&a, img, (t - img * a.tiles_img) * 128, wp};
+      const HaloRows rows{&a, img, (t - img * a.tiles_img) * 128, WP};
       const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * C::ACC_COLS);
       fprop_epilogue<BN>(a, trow, quarter * 32 + lane, 0, rows);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
-      e_work += clock64() - c1;
-    }
-    if (a.debug == 4 && quarter == 0 && lane == 0) {
-      a.dbg_buf[blockIdx.x * 8 + 4] = e_wait;
-      a.dbg_buf[blockIdx.x * 8 + 5] = e_work;
     }
   }
   tc_fence_before();
@@ -455,14 +816,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int BN, int BKC>
+template <int BN, int BKC, int WP>
 cudaError_t launch_fprop_halo(const FpropPlan& p, cudaStream_t stream) {
-  using C = HaloCfg<BN, BKC>;
+  using C = HaloCfg<BN, BKC, WP>;
   if (stream == reinterpret_cast<cudaStream_t>(-1)) {
-    return cudaFuncSetAttribute(conv_fprop_halo_kernel<BN, BKC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    return cudaFuncSetAttribute(conv_fprop_halo_kernel<BN, BKC, WP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 C::SMEM);
   }
-  conv_fprop_halo_kernel<BN, BKC><<<p.grid, kThreads, C::SMEM, stream>>>(p.tmx, p.tmw, p.args);
+  conv_fprop_halo_kernel<BN, BKC, WP><<<p.grid, kThreads, C::SMEM, stream>>>(p.tmx, p.tmw, p.args);
   return cudaGetLastError();
 }
 
@@ -717,13 +1078,15 @@ FpropLauncher pick_fprop(int bn) {
   }
 }
 
+constexpr int kHaloWP = 34;  // halo kernel instantiated for 32-wide images (W + 2 padded columns)
+
 template <int BKC>
 FpropLauncher pick_halo(int bn) {
   switch (bn) {
-    case 16: return launch_fprop_halo<16, BKC>;
-    case 32: return launch_fprop_halo<32, BKC>;
-    case 64: return launch_fprop_halo<64, BKC>;
-    case 128: return launch_fprop_halo<128, BKC>;
+    case 16: return launch_fprop_halo<16, BKC, kHaloWP>;
+    case 32: return launch_fprop_halo<32, BKC, kHaloWP>;
+    case 64: return launch_fprop_halo<64, BKC, kHaloWP>;
+    case 128: return launch_fprop_halo<128, BKC, kHaloWP>;
     default: return nullptr;
   }
 }
@@ -769,6 +1132,88 @@ WgradLauncher pick_wgrad(int bn, int swa, int swb) {
 
 int wgrad_bn(int c) { return c >= 128 ? 128 : c; }
 
+template <int BKC>
+FpropLauncher pick_splitk(int bn) {
+  switch (bn) {
+    case 128: return launch_fprop_splitk<128, BKC>;
+    case 256: return launch_fprop_splitk<256, BKC>;
+    default: return nullptr;
+  }
+}
+
+bool fprop_bres(const pbdk_conv_desc& d, int bn, int bkc) {
+  return d.k == bn && d.r * d.s * (d.c / bkc) * bn * bkc * 2 <= 96 * 1024;
+}
+
+// Tile width and split count from a throughput model measured on B200:
+// 128 x N x 16 MMA = 46/48/64/128 cycles for N = 32/64/128/256, and each SM ingests at most
+// ~100 B/clk from L2 with ~192 KB of TMA loads in flight (latency ~1 us under load;
+// scripts/micro/tma_rate.cu, l2_ingress.cu), so a K block costs
+// max(MMA cycles, bytes loaded / kIngress).  Persistent (S = 1) kernels pay ceil(tiles / SMs) tiles per
+// CTA; split-K (S in 2..8, one wave, K blocks divided S ways) pays a DSMEM reduction.
+struct FpropChoice {
+  int bn;
+  int splits;
+  bool pair;  // 2-CTA (cta_group::2) tiles of 256 x bn
+};
+
+constexpr double kIngress = 100.0;  // L2 -> smem bytes per SM clock with ~192 KB of loads in flight
+
+FpropChoice choose_fprop(const pbdk_conv_desc& d, const ConvGeom& g, int bkc) {
+  const int num_kb = d.r * d.s * (d.c / bkc);
+  const int sms = num_sms();
+  static const int forced = [] {
+    const char* e = std::getenv("PBDK_FPROP_SPLITS");  // 1: never split (A/B runs)
+    return e != nullptr ? std::atoi(e) : 0;
+  }();
+  // 2-CTA tiles measured no faster than one-CTA tiles on the step's shapes (the K loop is
+  // not load-bound once enough bytes are in flight); opt-in for experiments.
+  static const int no_pair = [] {
+    const char* e = std::getenv("PBDK_PAIR");
+    return e == nullptr || e[0] == '0';
+  }();
+  FpropChoice best{0, 1, false};
+  double best_cost = 1e300;
+  for (int bn : {256, 128, 64, 32, 16}) {
+    if (d.k % bn != 0) continue;
+    const bool bres = fprop_bres(d, bn, bkc);
+    const double mma = (bkc / 16) * (bn <= 32 ? 46.0 : bn == 64 ? 48.0 : bn == 128 ? 64.0 : 128.0);
+    const double bytes = 128.0 * bkc * 2 + (bres ? 0.0 : static_cast<double>(bn) * bkc * 2);
+    const double kb_cost = std::max(mma, bytes / kIngress);
+    const int tiles = g.m_tiles * (d.k / bn);
+    for (int sp : {1, 2, 4, 8}) {
+      if (sp > 1) {
+        if (bkc != 64 || (bn != 128 && bn != 256) || tiles * sp > sms || num_kb < 4 * sp) continue;
+      }
+      if (forced == 1 && sp > 1) continue;
+      double cost;
+      if (sp == 1) {
+        const int per_cta = (tiles + std::min(tiles, sms) - 1) / std::min(tiles, sms);
+        cost = per_cta * num_kb * kb_cost + 4.0 * bn;
+      } else {
+        cost = ((num_kb + sp - 1) / sp) * kb_cost + 8.0 * bn + 6500.0;  // measured reduction + sync cost
+      }
+      if (cost < best_cost) {
+        best_cost = cost;
+        best = {bn, sp, false};
+      }
+    }
+    // 2-CTA: per SM a K block loads 16 KB of A and half the filter tile
+    if (!no_pair && bkc == 64 && (bn == 128 || bn == 256) && !bres && g.m_tiles % 2 == 0) {
+      const double pbytes = 128.0 * bkc * 2 + static_cast<double>(bn / 2) * bkc * 2;
+      const double pkb = std::max(mma, pbytes / kIngress);
+      const int ptiles = tiles / 2;
+      const int pairs = std::min(ptiles, sms / 2);
+      const double cost = ((ptiles + pairs - 1) / pairs) * num_kb * pkb + 4.0 * bn + 500.0;
+      if (cost < best_cost) {
+        best_cost = cost;
+        best = {bn, 1, true};
+      }
+    }
+  }
+  return best;
+}
+
 }  // namespace
 
 int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, const float* bias, const void* aux,
@@ -780,17 +1225,13 @@ int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, c
     return PBDK_EINVAL;
   if ((epi == PBDK_EPI_BIAS_RES_RELU || epi == PBDK_EPI_RELU_MASK) && aux == nullptr) return PBDK_EINVAL;
   const int bkc = chan_block(d.c);
-  int bn = 16;
-  for (int cand : {256, 128, 64, 32, 16}) {
-    if (d.k % cand == 0) {
-      bn = cand;
-      break;
-    }
-  }
-  const int num_kb = d.r * d.s * (d.c / bkc);
-  const bool bres = (d.k == bn) && num_kb * bn * bkc * 2 <= 96 * 1024;
-  const bool halo = halo_enabled() && bres && bn <= 128 && d.r == 3 && d.s == 3 && d.stride == 1 && d.pad == 1 &&
-                    d.q >= 32 && d.q + 2 <= 256;
+  const FpropChoice ch = choose_fprop(d, g, bkc);
+  const int bn = ch.bn;
+  const int splits = ch.splits;
+  const bool pair = ch.pair;
+  const bool bres = !pair && fprop_bres(d, bn, bkc);
+  const bool halo = splits == 1 && !pair && halo_enabled() && bres && bn <= 128 && d.r == 3 && d.s == 3 && d.stride == 1 && d.pad == 1 &&
+                    d.q + 2 == kHaloWP && d.w == d.q;
   FpropLauncher l = nullptr;
   switch (bkc) {
     case 16: l = bres ? pick_fprop<16, true>(bn) : pick_fprop<16, false>(bn); break;
@@ -798,6 +1239,8 @@ int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, c
     case 64: l = bres ? pick_fprop<64, true>(bn) : pick_fprop<64, false>(bn); break;
     default: break;
   }
+  if (splits > 1) l = bkc == 64 ? pick_splitk<64>(bn) : nullptr;
+  if (pair) l = bkc != 64 ? nullptr : bn == 256 ? launch_fprop_pair<256, 64> : bn == 128 ? launch_fprop_pair<128, 64> : nullptr;
   if (halo) {
     switch (bkc) {
       case 16: l = pick_halo<16>(bn); break;
@@ -809,18 +1252,15 @@ int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, c
   if (l == nullptr) return PBDK_EINVAL;
   FpropArgs& a0 = plan->args;
   if (halo) {
-    const int wp = d.q + 2;
-    a0.halo_rows = 3 + (129 + wp - 1) / wp;
-    a0.halo_stage_bytes = round_up(a0.halo_rows * wp * bkc * 2, 1024);
-    a0.halo_stages = std::min(8, (kFpropBudget - 96 * 1024) / a0.halo_stage_bytes);
+    const int wp = kHaloWP;
+    const int halo_rows = 3 + (129 + wp - 1) / wp;
     a0.tiles_img = (d.p * wp + 127) / 128;
-    if (a0.halo_stages < 2) return PBDK_EINVAL;
     const uint64_t dims[4] = {static_cast<uint64_t>(d.c), static_cast<uint64_t>(d.w), static_cast<uint64_t>(d.h),
                               static_cast<uint64_t>(d.n)};
     const uint64_t strides[3] = {static_cast<uint64_t>(d.c) * 2, static_cast<uint64_t>(d.w) * d.c * 2,
                                  static_cast<uint64_t>(d.h) * d.w * d.c * 2};
     const uint32_t box[4] = {static_cast<uint32_t>(bkc), static_cast<uint32_t>(wp),
-                             static_cast<uint32_t>(a0.halo_rows), 1};
+                             static_cast<uint32_t>(halo_rows), 1};
     const uint32_t es[4] = {1, 1, 1, 1};
     if (!encode_tmap_bf16(&plan->tmx, x, 4, dims, strides, box, es, bkc * 2)) return PBDK_ECUDA;
   } else if (!act_map(&plan->tmx, x, d.n, d.h, d.w, d.c, bkc, g.bw, g.bh, g.bn, d.stride)) {
@@ -830,7 +1270,7 @@ int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, c
     const uint64_t ktot = static_cast<uint64_t>(d.r) * d.s * d.c;
     const uint64_t dims[2] = {ktot, static_cast<uint64_t>(d.k)};
     const uint64_t strides[1] = {ktot * 2};
-    const uint32_t box[2] = {static_cast<uint32_t>(bkc), static_cast<uint32_t>(bn)};
+    const uint32_t box[2] = {static_cast<uint32_t>(bkc), static_cast<uint32_t>(pair ? bn / 2 : bn)};
     const uint32_t es[2] = {1, 1};
     if (!encode_tmap_bf16(&plan->tmw, w, 2, dims, strides, box, es, bkc * 2)) return PBDK_ECUDA;
   }
@@ -853,7 +1293,7 @@ int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, c
   {
     const char* dbg = std::getenv("PBDK_CONV_DEBUG");
     a.debug = dbg != nullptr ? std::atoi(dbg) : 0;
-    a.dbg_buf = a.debug == 4 ? static_cast<long long*>(const_cast<void*>(aux)) : nullptr;
+    a.dbg_buf = (a.debug >= 4 && aux != nullptr) ? static_cast<long long*>(const_cast<void*>(aux)) : nullptr;
   }
   a.y = static_cast<__nv_bfloat16*>(y);
   a.bias = bias;
@@ -861,7 +1301,13 @@ int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, c
   a.n_tiles = d.k / bn;
   a.m_tiles = halo ? d.n * a.tiles_img : g.m_tiles;
   const int tiles = a.n_tiles * a.m_tiles;
-  plan->grid = dim3(static_cast<unsigned>(std::min(tiles, num_sms())), 1, 1);
+  if (pair) {
+    plan->grid = dim3(static_cast<unsigned>(2 * std::min(tiles / 2, num_sms() / 2)), 1, 1);
+  } else if (splits > 1) {
+    plan->grid = dim3(static_cast<unsigned>(splits), static_cast<unsigned>(tiles), 1);
+  } else {
+    plan->grid = dim3(static_cast<unsigned>(std::min(tiles, num_sms())), 1, 1);
+  }
   plan->bn_tile = bn;
   plan->bkc = bkc;
   plan->smem_bytes = 0;

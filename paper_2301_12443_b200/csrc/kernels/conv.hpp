@@ -31,7 +31,7 @@ struct FpropArgs {
   int bw, bh, bn, tiles_q, tiles_p;
   int c_chunks;
   int n_tiles, m_tiles;
-  int tiles_img, halo_rows, halo_stage_bytes, halo_stages;  // halo variant only
+  int tiles_img;  // halo variant only
   int epi;
   int debug;  // 0 normal; 1 skip epilogue stores; 2 skip MMAs; 3 skip epilogue; 4 cycle counters
   long long* dbg_buf;  // debug 4: per CTA {total, wait_tempty, wait_full, issue, epi_wait, epi_work}

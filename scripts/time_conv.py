@@ -13,9 +13,14 @@ s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 f = lambda: L.pbdk_conv_fprop(ctypes.byref(d), x.data_ptr(), w.data_ptr(), y.data_ptr(), None, None, 0, s)
 for _ in range(5): assert f() == 0
 torch.cuda.synchronize()
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g):
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for _ in range(50): assert f() == 0
+g.replay(); torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
-for _ in range(50): f()
+g.replay()
 e1.record(); torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 50
 print(f"{ms*1e3:.1f} us {2.0*n*p*p*k*r*r*c/ms/1e9:.0f} TFLOP/s")

@@ -28,7 +28,9 @@ def desc(L, n, h, c, k, r, stride):
 
 CASES = [(2, 32, 64, 64, 3, 1), (2, 32, 16, 64, 3, 1), (2, 32, 16, 32, 3, 1), (2, 32, 32, 64, 3, 1),
          (3, 32, 64, 128, 3, 2), (3, 32, 64, 128, 1, 2), (4, 16, 128, 128, 3, 1), (4, 8, 256, 512, 3, 2),
-         (5, 4, 512, 512, 3, 1), (2, 16, 128, 256, 3, 2), (3, 16, 32, 64, 3, 2), (9, 4, 64, 32, 3, 1)]
+         (5, 4, 512, 512, 3, 1), (2, 16, 128, 256, 3, 2), (3, 16, 32, 64, 3, 2), (9, 4, 64, 32, 3, 1),
+         # few output tiles -> split-K clusters (DSMEM reduction)
+         (16, 4, 512, 512, 3, 1), (32, 8, 256, 256, 3, 2), (8, 4, 512, 256, 3, 1), (4, 8, 256, 128, 3, 1)]
 
 
 def stream():
@@ -81,6 +83,24 @@ def test_conv_wgrad(L, case):
                                       stride=st, padding=r // 2).permute(0, 2, 3, 1)
     torch.cuda.synchronize()
     assert (dw - ref).abs().max().item() <= 1e-3 * ref.abs().max().item() + 1e-4
+
+
+@pytest.mark.parametrize("case", [(16, 4, 512, 512, 3, 1), (32, 8, 256, 256, 3, 2), (64, 16, 128, 128, 3, 1)])
+def test_conv_fprop_deterministic(L, case):
+    """Split-K partials are reduced in a fixed order: two runs are bit-identical."""
+    n, h, c, k, r, st = case
+    d = desc(L, n, h, c, k, r, st)
+    torch.manual_seed(7)
+    x = (torch.rand(n, h, h, c, device="cuda") * 2 - 1).bfloat16()
+    w = ((torch.rand(k, r, r, c, device="cuda") * 2 - 1) / (r * r * c) ** 0.5).bfloat16()
+    outs = []
+    for _ in range(2):
+        y = torch.empty(n, d.p, d.q, k, device="cuda", dtype=torch.bfloat16)
+        assert L.lib().pbdk_conv_fprop(ctypes.byref(d), x.data_ptr(), w.data_ptr(), y.data_ptr(), None, None, 0,
+                                       stream()) == 0
+        outs.append(y)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
 
 
 def test_weight_flip(L):

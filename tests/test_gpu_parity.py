@@ -181,7 +181,10 @@ def test_deterministic_across_runs(ex):
 
 
 def test_full_size_teacher_sample_independence(ex):
-    """b=256 (BASELINE configs[1] batch): the first 4 samples' teacher output equals the b=4 run."""
+    """b=256 (BASELINE configs[1] batch): the first 4 samples' teacher output equals the b=4 run.
+
+    Tile shapes are chosen per batch size and small batches use split-K (a different fp32
+    summation order), so the outputs agree to bf16 rounding noise, not bit for bit."""
     big = ex.Partition(0, 3, 256, 256)
     big.init_params()
     big.teacher_forward()
@@ -190,7 +193,9 @@ def test_full_size_teacher_sample_independence(ex):
     small.set_shard(4, 0)
     small.teacher_forward()
     torch.cuda.synchronize()
-    assert torch.equal(big.teacher_out()[:4], small.teacher_out()[:4])
+    a, b = big.teacher_out()[:4].float(), small.teacher_out()[:4].float()
+    # rounding differences propagate through the 20-conv chain: bf16-noise level, not bitwise
+    assert (a - b).norm() <= 4e-3 * a.norm(), ((a - b).norm() / a.norm()).item()
     big.student_step()
     torch.cuda.synchronize()
     losses = big.losses()
