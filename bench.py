@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--batch", type=int, default=PER_GPU_BATCH, help="global batch per GPU")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--relay", choices=["peer", "nccl"], default="peer",
+                    help="N>1 teacher-activation relay: K11 peer stores over NVLink (default) or NCCL send/recv")
     ap.add_argument("--pipeline", action="store_true",
                     help="use the multi-GPU runtime (profile -> best_schedule -> PipeBD) even at N=1")
     return ap.parse_args()

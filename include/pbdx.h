@@ -49,6 +49,8 @@ typedef struct pbdx_desc {
 #define PBDX_BUF_LOSSES 5       /* double[num_blocks]: per-block partial loss of the last step */
 #define PBDX_BUF_STEP 6         /* int64 step counter (advanced by apply_update) */
 #define PBDX_BUF_TEACHER_PARAMS 7 /* bf16 teacher conv weights of block_lo..hi (flat, program order) */
+#define PBDX_BUF_MAILBOX 8      /* uint64 flags written by relay peers: [0,16) ready, one per sender slot;
+                                   [16,32) consumed, one per receiver slot (own allocation, IPC-exportable) */
 
 int pbdx_create(const pbdx_desc* d, void** handle);
 void pbdx_destroy(void* handle);
@@ -99,6 +101,33 @@ int pbdx_block_times(void* handle, float* teacher_ms, float* student_ms);
  * out[9] = {w1, w2, wsc, g1, b1, g2, b2, gsc, bsc}; returns the block's element count
  * (negative on error).  Block 0 stores its 3 input channels padded to 16. */
 long pbdx_student_layout(int block, long* offsets);
+
+/* ------------------------------------------------------------------ K11 peer relay (TR)
+ * The reference models the hand-over of t_hi as ready = teacher_end + max(C(b_up), C(b_down))
+ * (simulate.cpp:203-214).  Here the SENDER's SMs store its rows directly into the receiver's
+ * PBDX_BUF_INPUT through peer memory (NVLink; a CUDA IPC mapping across processes) on a side
+ * stream right after T.forward, then publish a sequence number into the receiver's mailbox.
+ * The receiver's teacher_forward first waits for every sender's flag; its student_step ends by
+ * publishing "consumed" into each sender's mailbox, which gates the next overwrite (one slot).
+ * All of it is device-side, so a rank's whole step (and its CUDA graph) needs no host handshake.
+ *
+ * Receiver: remote_consumed_flags[i] = &mailbox_of_sender_i[16 + (my slot in sender i's list)];
+ *           sender i writes my mailbox[i].
+ * Sender:   msgs[j] = rows [src_row, src_row+rows) of my PBDX_BUF_TEACHER_OUT -> dst (peer pointer into
+ *           receiver j's input, already offset), remote_flag = &mailbox_of_receiver_j[my slot there];
+ *           receiver j writes my mailbox[16 + j]. */
+typedef struct pbdx_relay_msg {
+  long long src_row, rows;
+  void* dst;
+  void* remote_flag;
+} pbdx_relay_msg;
+int pbdx_relay_set_recv(void* handle, int nsenders, void* const* remote_consumed_flags);
+int pbdx_relay_set_send(void* handle, int nmsgs, const pbdx_relay_msg* msgs);
+/* CUDA IPC of an executor buffer (the allocation base: PBDX_BUF_INPUT / PBDX_BUF_MAILBOX) for ranks in
+ * other processes; handle = 64 bytes (cudaIpcMemHandle_t). */
+int pbdx_ipc_export(void* dev_ptr, void* handle);
+int pbdx_ipc_open(const void* handle, void** dev_ptr);
+int pbdx_ipc_close(void* dev_ptr);
 
 /* Kernel launches issued per step by this executor (for the bench's gpu_launches claim). */
 int pbdx_launches_per_step(void* handle);

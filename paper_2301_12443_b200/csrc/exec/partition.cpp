@@ -25,6 +25,7 @@
 #include "conv.hpp"
 #include "pbdk.h"
 #include "pbdx.h"
+#include "relay.hpp"
 
 namespace pbd::exec {
 
@@ -236,7 +237,81 @@ class Partition {
     check(pbdk::pack_image(stage_, input_, n, st), "pack image");
   }
 
+  // ---- K11 peer relay (relay.cu): the receiver's input buffer is written by its senders
+  void relay_set_recv(int n, void* const* remote_consumed) {
+    if (n < 0 || n > pbdk::kRelayMaxPeers) throw BadArg("relay: too many senders");
+    if (n > 0 && d_.block_lo == 0) throw BadArg("relay: partition 0 loads data, it receives nothing");
+    recv_consumed_.assign(remote_consumed, remote_consumed + n);
+    graph_valid_ = phases_valid_ = false;
+  }
+
+  void relay_set_send(int n, const pbdx_relay_msg* msgs) {
+    if (n < 0 || n > pbdk::kRelayMaxPeers) throw BadArg("relay: too many receivers");
+    const size_t row = tout_bytes_ / static_cast<size_t>(d_.n_max);
+    send_.clear();
+    for (int i = 0; i < n; ++i) {
+      const pbdx_relay_msg& m = msgs[i];
+      if (m.src_row < 0 || m.rows < 0 || m.src_row + m.rows > n_ || m.dst == nullptr || m.remote_flag == nullptr)
+        throw BadArg("relay: bad message");
+      if ((row * m.rows) % 16 != 0 || reinterpret_cast<uintptr_t>(m.dst) % 16 != 0) throw BadArg("relay: alignment");
+      send_.push_back(m);
+    }
+    if (!send_.empty() && relay_stream_ == nullptr) {
+      cuda(cudaStreamCreateWithFlags(&relay_stream_, cudaStreamNonBlocking), "stream");
+      cuda(cudaEventCreateWithFlags(&relay_fork_, cudaEventDisableTiming), "event");
+      cuda(cudaEventCreateWithFlags(&relay_done_, cudaEventDisableTiming), "event");
+    }
+    graph_valid_ = phases_valid_ = false;
+  }
+
+  void relay_wait_input(cudaStream_t st) {
+    if (recv_consumed_.empty()) return;
+    pbdk::RelayWaitArgs a{};
+    for (size_t i = 0; i < recv_consumed_.size(); ++i) a.flags[i] = mailbox_ + i;
+    a.seq = relay_seq_ + 0;  // receive sequence
+    a.bias = 1;
+    a.count = static_cast<int>(recv_consumed_.size());
+    check(pbdk::relay_wait(a, st), "relay wait input");
+  }
+
+  void relay_send_output(cudaStream_t st) {
+    if (send_.empty()) return;
+    cuda(cudaEventRecord(relay_fork_, st), "event");
+    cuda(cudaStreamWaitEvent(relay_stream_, relay_fork_, 0), "wait");
+    pbdk::RelayWaitArgs w{};
+    pbdk::RelayCopyArgs c{};
+    const size_t row = tout_bytes_ / static_cast<size_t>(d_.n_max);
+    const char* out = reinterpret_cast<const char*>(tblocks_.back().out);
+    for (size_t i = 0; i < send_.size(); ++i) {
+      w.flags[i] = mailbox_ + pbdk::kRelayMaxPeers + i;
+      c.src[i] = out + row * static_cast<size_t>(send_[i].src_row);
+      c.dst[i] = send_[i].dst;
+      c.vec16[i] = static_cast<long long>(row * static_cast<size_t>(send_[i].rows) / 16);
+      c.ready[i] = static_cast<unsigned long long*>(send_[i].remote_flag);
+    }
+    w.count = c.count = static_cast<int>(send_.size());
+    w.seq = c.seq = relay_seq_ + 1;  // send sequence
+    w.bias = 0;
+    c.ticket = relay_ticket_;
+    check(pbdk::relay_wait(w, relay_stream_), "relay wait consumed");
+    check(pbdk::relay_copy(c, 64, relay_stream_), "relay copy");
+    cuda(cudaEventRecord(relay_done_, relay_stream_), "event");
+  }
+
+  // after the last reader of the input (teacher block lo, student block lo) and the send
+  void relay_finish(cudaStream_t st) {
+    if (!send_.empty()) cuda(cudaStreamWaitEvent(st, relay_done_, 0), "join relay");
+    if (recv_consumed_.empty()) return;
+    pbdk::RelayReleaseArgs a{};
+    for (size_t i = 0; i < recv_consumed_.size(); ++i)
+      a.flags[i] = static_cast<unsigned long long*>(recv_consumed_[i]);
+    a.seq = relay_seq_ + 0;
+    a.count = static_cast<int>(recv_consumed_.size());
+    check(pbdk::relay_release(a, st), "relay release");
+  }
+
   void teacher_forward(cudaStream_t st) {
+    relay_wait_input(st);
     if (d_.block_lo == 0 && !external_)
       check(pbdk::philox_image(input_, n_, first_, step_, d_.global_batch, d_.seed_data, st), "philox");
     for (size_t i = 0; i < tblocks_.size(); ++i) {
@@ -245,6 +320,7 @@ class Partition {
       if (timing_) cuda(cudaEventRecord(ev_t_[2 * i + 1], st), "event");
       cuda(cudaEventRecord(tdone_[i], st), "event");
     }
+    relay_send_output(st);
   }
 
   // Student block k runs on its own stream.  Fused step(): it starts once teacher block k is
@@ -285,6 +361,7 @@ class Partition {
       cuda(cudaEventRecord(s.done, st), "event");
     }
     for (SBlock& s : sblocks_) cuda(cudaStreamWaitEvent(caller, s.done, 0), "join");
+    relay_finish(caller);
   }
 
   // bf16 shadows + flipped dgrad weights from the fp32 master weights (after a state migration)
@@ -412,6 +489,7 @@ class Partition {
       case PBDX_BUF_LOSSES: *ptr = losses_; *bytes = nblocks() * sizeof(double); break;
       case PBDX_BUF_STEP: *ptr = step_; *bytes = sizeof(long long); break;
       case PBDX_BUF_TEACHER_PARAMS: *ptr = tparams_; *bytes = tparam_bytes_; break;
+      case PBDX_BUF_MAILBOX: *ptr = mailbox_; *bytes = 2 * pbdk::kRelayMaxPeers * sizeof(unsigned long long); break;
       default: throw BadArg("unknown buffer");
     }
   }
@@ -430,6 +508,8 @@ class Partition {
       n += (s.p_w2.splits > 1 ? 2 : 1) + (s.p_wsc.splits > 1 ? 2 : 1) + (s.p_w1.splits > 1 ? 2 : 1);
     }
     n += 1 + static_cast<int>(sblocks_.size());  // sgd + flips
+    if (!recv_consumed_.empty()) n += 2;         // relay wait + release
+    if (!send_.empty()) n += 2;                  // relay wait + copy
     return n;
   }
 
@@ -444,6 +524,9 @@ class Partition {
     for (auto g : phase_exec_)
       if (g != nullptr) cudaGraphExecDestroy(g);
     if (fork_ != nullptr) cudaEventDestroy(fork_);
+    if (relay_stream_ != nullptr) cudaStreamDestroy(relay_stream_);
+    if (relay_fork_ != nullptr) cudaEventDestroy(relay_fork_);
+    if (relay_done_ != nullptr) cudaEventDestroy(relay_done_);
     for (auto e : ev_t_) cudaEventDestroy(e);
     for (auto e : ev_s_) cudaEventDestroy(e);
   }
@@ -582,6 +665,9 @@ class Partition {
     shadow_ = arena_.get<bf16>(total_ * sizeof(bf16));
     losses_ = arena_.get<double>(kBlocks * sizeof(double));
     step_ = arena_.get<long long>(sizeof(long long));
+    mailbox_ = arena_.get<unsigned long long>(2 * pbdk::kRelayMaxPeers * sizeof(unsigned long long));
+    relay_seq_ = arena_.get<unsigned long long>(2 * sizeof(unsigned long long));
+    relay_ticket_ = arena_.get<unsigned int>(sizeof(unsigned int));
 
     // ---- per-block scratch sized for n_max, streams and events
     for (SBlock& s : sblocks_) {
@@ -663,6 +749,15 @@ class Partition {
   long long* step_ = nullptr;
   std::vector<cudaEvent_t> tdone_;
   std::vector<cudaEvent_t> ev_t_, ev_s_;
+  // K11 relay state: mailbox_ = flags written by peers ([0,16) ready per sender, [16,32) consumed
+  // per receiver); relay_seq_ = {receive seq, send seq} (device-side, so graph replays advance them)
+  unsigned long long* mailbox_ = nullptr;
+  unsigned long long* relay_seq_ = nullptr;
+  unsigned int* relay_ticket_ = nullptr;
+  std::vector<void*> recv_consumed_;
+  std::vector<pbdx_relay_msg> send_;
+  cudaStream_t relay_stream_ = nullptr;
+  cudaEvent_t relay_fork_ = nullptr, relay_done_ = nullptr;
 };
 
 }  // namespace pbd::exec
@@ -727,6 +822,28 @@ int pbdx_refresh_shadows(void* h, void* st) { return guard([&] { P(h)->refresh_s
 int pbdx_set_timing(void* h, int enabled) { return guard([&] { P(h)->set_timing(enabled != 0); }); }
 int pbdx_block_times(void* h, float* t, float* s) { return guard([&] { P(h)->block_times(t, s); }); }
 int pbdx_launches_per_step(void* h) { return P(h)->launches_per_step(); }
+int pbdx_relay_set_recv(void* h, int nsenders, void* const* remote_consumed_flags) {
+  if (nsenders > 0 && remote_consumed_flags == nullptr) return PBDK_EINVAL;
+  return guard([&] { P(h)->relay_set_recv(nsenders, remote_consumed_flags); });
+}
+int pbdx_relay_set_send(void* h, int nmsgs, const pbdx_relay_msg* msgs) {
+  if (nmsgs > 0 && msgs == nullptr) return PBDK_EINVAL;
+  return guard([&] { P(h)->relay_set_send(nmsgs, msgs); });
+}
+int pbdx_ipc_export(void* dev_ptr, void* handle) {
+  if (dev_ptr == nullptr || handle == nullptr) return PBDK_EINVAL;
+  cudaIpcMemHandle_t hd;
+  if (cudaIpcGetMemHandle(&hd, dev_ptr) != cudaSuccess) return PBDK_ECUDA;
+  std::memcpy(handle, &hd, sizeof(hd));
+  return PBDK_OK;
+}
+int pbdx_ipc_open(const void* handle, void** dev_ptr) {
+  if (dev_ptr == nullptr || handle == nullptr) return PBDK_EINVAL;
+  cudaIpcMemHandle_t hd;
+  std::memcpy(&hd, handle, sizeof(hd));
+  return cudaIpcOpenMemHandle(dev_ptr, hd, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess ? PBDK_OK : PBDK_ECUDA;
+}
+int pbdx_ipc_close(void* dev_ptr) { return cudaIpcCloseMemHandle(dev_ptr) == cudaSuccess ? PBDK_OK : PBDK_ECUDA; }
 
 long pbdx_student_layout(int block, long* out) {
   if (block < 0 || block >= pbd::exec::kBlocks || out == nullptr) return -1;

@@ -17,7 +17,9 @@ import torch
 
 from . import _lib
 
-BUF_INPUT, BUF_TEACHER_OUT, BUF_GRADS, BUF_PARAMS, BUF_MOMENTUM, BUF_LOSSES, BUF_STEP, BUF_TEACHER_PARAMS = range(8)
+(BUF_INPUT, BUF_TEACHER_OUT, BUF_GRADS, BUF_PARAMS, BUF_MOMENTUM, BUF_LOSSES, BUF_STEP, BUF_TEACHER_PARAMS,
+ BUF_MAILBOX) = range(9)
+RELAY_MAX_PEERS = 16  # relay.hpp kRelayMaxPeers: mailbox = [ready x16 | consumed x16] uint64
 BLOCKS = 4
 T_CH = (3, 64, 128, 256, 512)
 T_HW = (32, 32, 16, 8, 4)
@@ -28,6 +30,12 @@ class PbdxDesc(ctypes.Structure):
     _fields_ = [("block_lo", ctypes.c_int), ("block_hi", ctypes.c_int), ("n_max", ctypes.c_int),
                 ("global_batch", ctypes.c_int), ("seed_data", ctypes.c_uint32), ("seed_teacher", ctypes.c_uint32),
                 ("seed_student", ctypes.c_uint32), ("lr", ctypes.c_float), ("momentum", ctypes.c_float)]
+
+
+class RelayMsg(ctypes.Structure):
+    """pbdx_relay_msg (include/pbdx.h)."""
+    _fields_ = [("src_row", ctypes.c_longlong), ("rows", ctypes.c_longlong), ("dst", ctypes.c_void_p),
+                ("remote_flag", ctypes.c_void_p)]
 
 
 def _bind(L):
@@ -54,6 +62,11 @@ def _bind(L):
     L.pbdx_student_layout.restype = ctypes.c_long
     L.pbdx_launches_per_step.argtypes = [V]
     L.pbdx_refresh_shadows.argtypes = [V, V]
+    L.pbdx_relay_set_recv.argtypes = [V, I, P(V)]
+    L.pbdx_relay_set_send.argtypes = [V, I, P(RelayMsg)]
+    L.pbdx_ipc_export.argtypes = [V, ctypes.c_char_p]
+    L.pbdx_ipc_open.argtypes = [ctypes.c_char_p, P(V)]
+    L.pbdx_ipc_close.argtypes = [V]
     L._pbdx_bound = True
     return L
 
@@ -181,6 +194,30 @@ class Partition:
         flat = {"params": self.params, "grads": self.grads, "momentum": self.momentum}[which]()
         return {name: flat[base + o: base + o + n] for name, (o, n) in lay.items()}
 
+    # -- K11 peer relay (include/pbdx.h): device pointers of this rank's relay endpoints
+    def row_bytes_in(self) -> int:
+        k = self.block_lo
+        return T_HW[k] * T_HW[k] * stored_channels(T_CH[k]) * 2
+
+    def row_bytes_out(self) -> int:
+        k = self.block_hi + 1
+        return T_HW[k] * T_HW[k] * T_CH[k] * 2
+
+    def mailbox_ptr(self) -> int:
+        return self.buffer_ptr(BUF_MAILBOX)[0]
+
+    def input_ptr(self) -> int:
+        return self.buffer_ptr(BUF_INPUT)[0]
+
+    def relay_set_recv(self, remote_consumed_flags: List[int]):
+        arr = (ctypes.c_void_p * max(1, len(remote_consumed_flags)))(*remote_consumed_flags)
+        _check(lib().pbdx_relay_set_recv(self.handle, len(remote_consumed_flags), arr), "relay_set_recv")
+
+    def relay_set_send(self, msgs: List[Tuple[int, int, int, int]]):
+        """msgs: (src_row, rows, dst device pointer, remote ready-flag pointer)."""
+        arr = (RelayMsg * max(1, len(msgs)))(*[RelayMsg(a, b, c, d) for a, b, c, d in msgs])
+        _check(lib().pbdx_relay_set_send(self.handle, len(msgs), arr), "relay_set_send")
+
     # -- phases of Algorithm 1
     def init_params(self, stream=None):
         _check(lib().pbdx_init_params(self.handle, self._stream(stream)), "init_params")
@@ -268,3 +305,20 @@ class Partition:
 
     def set_step_index(self, step: int):
         self.step_counter().fill_(int(step))
+
+
+# ---------------------------------------------------------------- CUDA IPC of relay endpoints
+def ipc_export(ptr: int) -> bytes:
+    buf = ctypes.create_string_buffer(64)
+    _check(lib().pbdx_ipc_export(ctypes.c_void_p(ptr), buf), "ipc_export")
+    return buf.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    p = ctypes.c_void_p()
+    _check(lib().pbdx_ipc_open(ctypes.c_char_p(handle), ctypes.byref(p)), "ipc_open")
+    return p.value
+
+
+def ipc_close(ptr: int):
+    _check(lib().pbdx_ipc_close(ctypes.c_void_p(ptr)), "ipc_close")

@@ -83,6 +83,36 @@ def relay_plan(schedule: dict, global_batch: int, boundary: int) -> List[Tuple[i
     return msgs
 
 
+def peer_wiring(schedule: dict, global_batch: int, rank: int, endpoints: Dict[int, dict]):
+    """K11 peer relay wiring of `rank` (include/pbdx.h): endpoints[r] = {"input", "mailbox", "row"} are
+    rank r's input buffer, relay mailbox (device pointers valid in THIS process) and relay row bytes.
+    Returns (remote consumed-flag pointers, one per sender; send messages (src_row, rows, dst, flag)).
+    Slot rule: a receiver's ready slot for a sender = the sender's index in its sender list; a sender's
+    consumed slot for a receiver = the receiver's index in its receiver list (both ascending ranks)."""
+    place = placements(schedule, global_batch)
+    me = place[rank]
+    nparts = len(schedule["partitions"])
+
+    def senders_of(r):
+        return [m for m in relay_plan(schedule, global_batch, place[r].partition) if m[1] == r]
+
+    def receivers_of(r):
+        return [m for m in relay_plan(schedule, global_batch, place[r].partition + 1) if m[0] == r]
+
+    recv = []
+    if me.partition > 0:
+        for src, _, _, _, _ in senders_of(rank):
+            slot = [m[1] for m in receivers_of(src)].index(rank)
+            recv.append(endpoints[src]["mailbox"] + 8 * (16 + slot))
+    send = []
+    if me.partition + 1 < nparts:
+        for _, dst, src_off, dst_off, rows in receivers_of(rank):
+            slot = [m[0] for m in senders_of(dst)].index(rank)
+            send.append((src_off, rows, endpoints[dst]["input"] + dst_off * endpoints[dst]["row"],
+                         endpoints[dst]["mailbox"] + 8 * slot))
+    return recv, send
+
+
 class PipeBD:
     """This rank's share of a Pipe-BD schedule.
 
@@ -91,7 +121,14 @@ class PipeBD:
     """
 
     def __init__(self, schedule: dict, global_batch: int, make_stage: Callable, dpu: bool = True,
-                 groups: Optional[Dict[int, object]] = None):
+                 groups: Optional[Dict[int, object]] = None, relay: str = "nccl"):
+        """relay: "nccl" (batch_isend_irecv of the overlapping row slices) or "peer" (K11: the
+        sender's SMs store straight into the receiver's input through NVLink/IPC peer memory,
+        device-side flags, no host handshake; stages must be executor.Partition on CUDA)."""
+        if relay not in ("nccl", "peer"):
+            raise ValueError(f"unknown relay {relay!r}")
+        self.relay = relay
+        self._ipc_mapped: List[int] = []
         self.schedule = schedule
         self.b = global_batch
         self.dpu = dpu
@@ -116,10 +153,41 @@ class PipeBD:
         self.send_msgs = [m for m in relay_plan(schedule, global_batch, me.partition + 1) if m[0] == self.rank] \
             if me.partition + 1 < self.nparts else []
         self._pending_sends: List = []
+        if relay == "peer":
+            self._wire_peer()
+
+    def _wire_peer(self):
+        """Exchange the relay endpoints (CUDA IPC handles) and configure this rank's stage."""
+        import os
+        from . import executor
+        for p in self._ipc_mapped:
+            executor.ipc_close(p)
+        self._ipc_mapped = []
+        st = self.stage
+        mine = {"pid": os.getpid(), "input": st.input_ptr(), "mailbox": st.mailbox_ptr(), "row": st.row_bytes_in(),
+                "h_input": executor.ipc_export(st.input_ptr()), "h_mailbox": executor.ipc_export(st.mailbox_ptr())}
+        allp = [None] * self.world
+        dist.all_gather_object(allp, mine)
+        endpoints = {}
+        for r, e in enumerate(allp):
+            if e["pid"] == mine["pid"]:
+                endpoints[r] = {"input": e["input"], "mailbox": e["mailbox"], "row": e["row"]}
+            else:
+                peers = {m[1] for m in self.send_msgs} | {m[0] for m in self.recv_msgs}
+                if r not in peers:
+                    continue
+                ip, mb = executor.ipc_open(e["h_input"]), executor.ipc_open(e["h_mailbox"])
+                self._ipc_mapped += [ip, mb]
+                endpoints[r] = {"input": ip, "mailbox": mb, "row": e["row"]}
+        recv, send = peer_wiring(self.schedule, self.b, self.rank, endpoints)
+        st.relay_set_recv(recv)
+        st.relay_set_send(send)
+        torch.cuda.synchronize(st.device)
+        dist.barrier()
 
     # -- relay
     def _recv_input(self):
-        if not self.recv_msgs:
+        if not self.recv_msgs or self.relay == "peer":
             return
         buf = self.stage.input_act()
         ops = [dist.P2POp(dist.irecv, buf[dst_off:dst_off + rows], src) for src, _, _, dst_off, rows in self.recv_msgs]
@@ -127,7 +195,7 @@ class PipeBD:
             w.wait()
 
     def _send_output(self):
-        if not self.send_msgs:
+        if not self.send_msgs or self.relay == "peer":
             return
         out = self.stage.teacher_out()
         ops = [dist.P2POp(dist.isend, out[src_off:src_off + rows], dst) for _, dst, src_off, _, rows in self.send_msgs]
@@ -143,7 +211,8 @@ class PipeBD:
         """Replay each phase as a CUDA graph (stages that support capture_phases)."""
         if hasattr(self.stage, "capture_phases"):
             # a rank that relays nothing downstream keeps the teacher->student overlap in one graph
-            self.stage.capture_phases(fuse_teacher_student=not self.send_msgs)
+            # (the peer relay is issued inside the teacher phase on a side stream, so it never splits it)
+            self.stage.capture_phases(fuse_teacher_student=not self.send_msgs or self.relay == "peer")
             self._graphs = True
 
     def _phase(self, i, fn):
@@ -249,6 +318,8 @@ class PipeBD:
         self.send_msgs = [m for m in relay_plan(new_schedule, self.b, nme.partition + 1) if m[0] == self.rank] \
             if nme.partition + 1 < self.nparts else []
         self._pending_sends = []
+        if self.relay == "peer":
+            self._wire_peer()
         if getattr(self, "_graphs", False):
             self.use_graphs()
 
@@ -374,7 +445,7 @@ def bench_pipeline(args, rank: int, world: int, local_rank: int) -> dict:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t[0]), float(t[1])
 
-    pipe = PipeBD(sched, gb, make_stage)
+    pipe = PipeBD(sched, gb, make_stage, relay=getattr(args, "relay", "peer"))
     if not getattr(args, "no_graph", False):
         pipe.use_graphs()
     for _ in range(max(3, args.warmup)):
@@ -414,6 +485,7 @@ def bench_pipeline(args, rank: int, world: int, local_rank: int) -> dict:
             "config": {"workload": "cifar-resnet18-teacher/slim-student 4 blocks (configs[1])", "global_batch": gb,
                        "parallelism": "ahd " + ";".join(f"{p['blocks']}x{len(p['devices'])}"
                                                         for p in sched["partitions"]),
+                       "relay": pipe.relay,
                        "l2": "no flush: per-step working set > 126 MB L2"},
             "e2e": {"value": gb / e2e_ms * 1e3, "unit": "samples/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 8 * len(pipe.stage.blocks), "ms_per_step": e2e_ms},

@@ -162,3 +162,34 @@ def test_reconfiguration_migrates_state_exactly():
             assert v == pytest.approx(want[k], rel=1e-12, abs=1e-15), (rank, k)
         for k, p in params.items():
             np.testing.assert_allclose(p, tr.sp[k], rtol=1e-6, atol=1e-9)
+
+
+def test_peer_wiring_slots_are_consistent():
+    """K11 wiring (runtime.peer_wiring): every sender writes exactly the flag slot its receiver waits
+    on, every receiver releases exactly the slot its sender waits on, and the peer stores cover each
+    receiver's input rows once."""
+    for b in (5, 8, 255):
+        for parts in ([(0, 0, [0]), (1, 2, [1, 2]), (3, 3, [3])], [(0, 1, [0, 1, 2]), (2, 3, [3, 4])],
+                      [(0, 0, [0, 1]), (1, 1, [2]), (2, 3, [3, 4, 5])]):
+            s = sched(parts, b)
+            place = runtime.placements(s, b)
+            eps = {r: {"input": 10 ** 9 * (r + 1), "mailbox": 10 ** 12 * (r + 1), "row": 1000} for r in place}
+            wiring = {r: runtime.peer_wiring(s, b, r, eps) for r in place}
+            for r, (recv, send) in wiring.items():
+                pl = place[r]
+                senders = [m[0] for m in runtime.relay_plan(s, b, pl.partition) if m[1] == r] if pl.partition else []
+                # receiver r waits on mailbox[i] for sender i; sender i must write exactly that address
+                for i, src in enumerate(senders):
+                    flags = [f for _, _, dst, f in wiring[src][1] if eps[r]["input"] <= dst < eps[r]["input"] + 10 ** 9]
+                    assert flags == [eps[r]["mailbox"] + 8 * i]
+                    # r releases into sender's consumed slot = r's index among src's receivers
+                    recvs = [m[1] for m in runtime.relay_plan(s, b, place[src].partition + 1) if m[0] == src]
+                    assert recv[i] == eps[src]["mailbox"] + 8 * (16 + recvs.index(r))
+                if senders:
+                    rows = np.zeros(pl.count, int)
+                    for src in senders:
+                        for _, nrows, dst, _ in wiring[src][1]:
+                            off = dst - eps[r]["input"]
+                            if 0 <= off < 10 ** 9:
+                                rows[off // 1000: off // 1000 + nrows] += 1
+                    assert (rows == 1).all()
