@@ -1,0 +1,125 @@
+"""Generate tests/golden/mb_torch_fp64.npz — pins the MBConv C oracle (oracle/mb_oracle.c) against an
+independent implementation: the MobileNetV2 teacher / ProxylessNAS student blockwise-distillation
+step written with torch ops + autograd (PyTorch is the paper's framework), in
+float64 so the fixture is a clean reference for the oracle's fp32 mode.  Inputs (data, teacher and
+student weights, the sampled path) come from the oracle's Philox generators; everything computed
+here is torch's (F.conv2d with groups for depthwise, F.batch_norm in training mode, hardtanh as
+ReLU6, autograd).  Run from the repo root:  python tests/golden/make_golden_mb.py
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.nn.functional as F
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+from oracle import mb  # noqa: E402
+
+torch.set_num_threads(8)
+OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "mb_torch_fp64.npz")
+B, S = 3, 64
+SUB = 53
+DRAW = 5  # path sampling index
+DT = torch.float64
+
+
+def nchw(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(DT).permute(0, 3, 1, 2)
+
+
+def nhwc(x):
+    return x.permute(0, 2, 3, 1).contiguous()
+
+
+def relu6(x):
+    return F.hardtanh(x, 0.0, 6.0)
+
+
+def teacher_fwd(b, tp, x):
+    p = torch.from_numpy(tp).to(DT)
+    off = [0]
+
+    def take(n):
+        t = p[off[0]:off[0] + n]
+        off[0] += n
+        return t
+
+    if b == 0:
+        w = take(32 * 9 * 16).reshape(32, 3, 3, 16)[..., :3].permute(0, 3, 1, 2)
+        x = relu6(F.conv2d(x, w, take(32), stride=2, padding=1))
+    for l in range(mb.NL[b]):
+        t, k, cin, cout, s = mb.teacher_layer(b, l)
+        E = cin if t == 1 else mb.round_ch(cin * t)
+        h = x
+        if t != 1:
+            w = take(E * cin).reshape(E, cin, 1, 1)
+            h = relu6(F.conv2d(h, w, take(E)))
+        wd = take(E * k * k).reshape(E, 1, k, k)
+        h = relu6(F.conv2d(h, wd, take(E), stride=s, padding=k // 2, groups=E))
+        wp = take(cout * E).reshape(cout, E, 1, 1)
+        y = F.conv2d(h, wp, take(cout))
+        x = y + x if (s == 1 and cin == cout) else y
+    return x
+
+
+def student(b, sp, path, x, t, norm):
+    """loss, {(layer, tensor): grad} of the active path."""
+    params = {}
+    for l in range(mb.layers(b)):
+        c = int(path[l])
+        off, _ = mb.candidate_span(b, l, c)
+        for name, (o, n) in mb.candidate_layout(b, l, c).items():
+            params[(l, name)] = torch.tensor(sp[off + o: off + o + n], dtype=DT, requires_grad=True)
+
+    def bn(y, l, g, be):
+        return F.batch_norm(y, None, None, params[(l, g)], params[(l, be)], training=True, eps=1e-5)
+
+    h = x
+    for l in range(mb.layers(b)):
+        g = mb.student_layer(b, l, int(path[l]))
+        if g["kind"] == "stem":
+            w = params[(l, "w")].reshape(32, 3, 3, 16)[..., :3].permute(0, 3, 1, 2)
+            h = relu6(bn(F.conv2d(h, w, stride=2, padding=1), l, "g2", "b2"))
+            continue
+        E, k, cin, cout = g["E"], g["k"], g["cin"], g["cout"]
+        a = h
+        if g["e"] != 1:
+            a = relu6(bn(F.conv2d(h, params[(l, "we")].reshape(E, cin, 1, 1)), l, "g1", "b1"))
+        a = relu6(bn(F.conv2d(a, params[(l, "wd")].reshape(E, 1, k, k), stride=g["stride"], padding=k // 2,
+                              groups=E), l, "g2", "b2"))
+        z = bn(F.conv2d(a, params[(l, "wp")].reshape(cout, E, 1, 1)), l, "g3", "b3")
+        h = z + h if g["res"] else z
+    loss = ((h - t) ** 2).sum() / norm
+    loss.backward()
+    return float(loss), {key: v.grad.numpy() for key, v in params.items()}
+
+
+def main():
+    out = {}
+    x = mb.image(B, 0, S, bf16=False)
+    acts = [x]
+    for b in range(mb.BLOCKS):
+        tp = mb.teacher_params(b, bf16=False)
+        y = nhwc(teacher_fwd(b, tp, nchw(acts[-1]))).numpy()
+        acts.append(y)
+        out[f"t{b}"] = y.reshape(-1)[::SUB]
+        out[f"t{b}_norm"] = np.linalg.norm(y)
+    for b in range(mb.BLOCKS):
+        sp = mb.student_params(b)
+        path = mb.sample_path(b, DRAW)
+        c, hh = mb.channels(b + 1), mb.hw(b + 1, S)
+        norm = float(B) * c * hh * hh
+        loss, grads = student(b, sp, path, nchw(acts[b]), nchw(acts[b + 1]), norm)
+        out[f"s{b}_path"] = path
+        out[f"s{b}_loss"] = loss
+        for (l, name), gv in grads.items():
+            out[f"s{b}_l{l}_{name}_norm"] = np.linalg.norm(gv)
+            out[f"s{b}_l{l}_{name}"] = gv.reshape(-1)[::SUB] if gv.size > 64 else gv
+    np.savez_compressed(OUT, **out)
+    print("wrote", OUT, len(out), "arrays")
+
+
+if __name__ == "__main__":
+    main()
