@@ -41,6 +41,10 @@ extern "C" {
 #define PBDK_EPI_BIAS_RELU 2      /* y = relu(acc + bias[k])                   */
 #define PBDK_EPI_BIAS_RES_RELU 3  /* y = relu(acc + bias[k] + aux[m][k])       */
 #define PBDK_EPI_RELU_MASK 4      /* y = aux[m][k] > 0 ? acc : 0   (relu bwd)  */
+#define PBDK_EPI_BIAS_RELU6 5     /* y = min(max(acc + bias[k], 0), 6)          */
+#define PBDK_EPI_BIAS_RES 6       /* y = acc + bias[k] + aux[m][k]              */
+#define PBDK_EPI_RELU6_MASK 7     /* y = 0 < aux[m][k] < 6 ? acc : 0 (relu6 bwd) */
+#define PBDK_EPI_ADD 8            /* y = acc + aux[m][k]                        */
 
 typedef struct pbdk_conv_desc {
   int n, h, w, c;  /* input NHWC, c = stored channels (multiple of 16) */

@@ -32,12 +32,18 @@
 extern "C" {
 #endif
 
+/* workloads */
+#define PBDX_MODEL_RESNET_CIFAR 0    /* configs[0..1]: ResNet-18-CIFAR teacher -> slim residual student, 4 blocks */
+#define PBDX_MODEL_MBV2_PROXYLESS 1  /* configs[2]: MobileNetV2 teacher -> ProxylessNAS supernet student, 6 blocks */
+
 typedef struct pbdx_desc {
-  int block_lo, block_hi; /* inclusive range of the 4-block CIFAR ResNet chain  */
+  int block_lo, block_hi; /* inclusive block range of the model's chain        */
   int n_max;              /* largest shard this executor will run               */
   int global_batch;       /* b: MSE normalisation + synthetic sample indexing   */
   uint32_t seed_data, seed_teacher, seed_student;
   float lr, momentum;
+  int model;              /* PBDX_MODEL_*                                        */
+  int image;              /* input side S (CIFAR: 32; MBV2: e.g. 224)           */
 } pbdx_desc;
 
 /* buffers for pbdx_buffer */
@@ -96,6 +102,12 @@ int pbdx_refresh_shadows(void* handle, void* stream);
 /* Per-block CUDA-event timing of the last step (ms): teacher[k], student[k] for k in the range. */
 int pbdx_set_timing(void* handle, int enabled);
 int pbdx_block_times(void* handle, float* teacher_ms, float* student_ms);
+
+/* Search space (PBDX_MODEL_MBV2_PROXYLESS): active candidate of every student layer of `block`
+ * (path[l] in [0, candidates); fixed layers 0).  Only the active path runs forward/backward and is
+ * updated (inactive candidates keep weights and momentum: torch semantics for params without
+ * .grad).  Invalidates captured graphs.  Layout of the supernet parameters: DESIGN.md §10. */
+int pbdx_set_path(void* handle, int block, const int* path, int n);
 
 /* Flat student-parameter layout of one block (element offsets, padded storage):
  * out[9] = {w1, w2, wsc, g1, b1, g2, b2, gsc, bsc}; returns the block's element count

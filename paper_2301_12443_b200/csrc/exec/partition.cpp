@@ -24,8 +24,8 @@
 #include "bd_kernels.hpp"
 #include "conv.hpp"
 #include "pbdk.h"
+#include "partition_base.hpp"
 #include "pbdx.h"
-#include "relay.hpp"
 
 namespace pbd::exec {
 
@@ -37,42 +37,7 @@ constexpr int T_HW[5] = {32, 32, 16, 8, 4};
 
 int stored(int c) { return c == 3 ? 16 : c; }
 
-struct CudaFail : std::runtime_error {
-  explicit CudaFail(const std::string& m) : std::runtime_error(m) {}
-};
-struct BadArg : std::runtime_error {
-  explicit BadArg(const std::string& m) : std::runtime_error(m) {}
-};
-
-void check(int rc, const char* what) {
-  if (rc == PBDK_EINVAL) throw BadArg(what);
-  if (rc != PBDK_OK) throw CudaFail(std::string(what) + ": " + cudaGetErrorString(cudaGetLastError()));
-}
-void cuda(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) throw CudaFail(std::string(what) + ": " + cudaGetErrorString(e));
-}
-
 float kaiming(int fan_in, float gain) { return std::sqrt(6.0f / static_cast<float>(fan_in)) * gain; }
-
-class Arena {
- public:
-  ~Arena() {
-    for (void* p : ptrs_) cudaFree(p);
-  }
-  template <class T = void>
-  T* get(size_t bytes) {
-    void* p = nullptr;
-    bytes = (bytes + 255) / 256 * 256;
-    if (bytes == 0) bytes = 256;
-    cuda(cudaMalloc(&p, bytes), "cudaMalloc");
-    cuda(cudaMemset(p, 0, bytes), "cudaMemset");
-    ptrs_.push_back(p);
-    return static_cast<T*>(p);
-  }
-
- private:
-  std::vector<void*> ptrs_;
-};
 
 using bf16 = __nv_bfloat16;
 
@@ -162,21 +127,20 @@ struct SBlock {
   cudaEvent_t done = nullptr;
 };
 
-}  // namespace
-
-class Partition {
+class ResNetPartition final : public PartitionBase {
  public:
-  explicit Partition(const pbdx_desc& d) : d_(d) {
+  explicit ResNetPartition(const pbdx_desc& d) : PartitionBase(d) {
     if (d.block_lo < 0 || d.block_hi >= kBlocks || d.block_lo > d.block_hi) throw BadArg("bad block range");
-    if (d.n_max < 1 || d.global_batch < 1) throw BadArg("bad batch");
-    n_ = d.n_max;
     allocate();
     build_plans();
   }
 
-  int nblocks() const { return d_.block_hi - d_.block_lo + 1; }
+  int nblocks() const override { return d_.block_hi - d_.block_lo + 1; }
+  const void* relay_source() const override { return tblocks_.back().out; }
+  size_t relay_row_bytes() const override { return tout_bytes_ / static_cast<size_t>(d_.n_max); }
+  void rebuild_for_shard() override { build_plans(); }
 
-  void init_params(cudaStream_t st) {
+  void init_params(cudaStream_t st) override {
     for (TBlock& tb : tblocks_)
       for (TConv& c : tb.convs) {
         check(pbdk::init_uniform(c.w, 1, c.cout, c.r, c.r, c.cs, c.cin, d_.seed_teacher, c.tensor,
@@ -211,24 +175,7 @@ class Partition {
     cuda(cudaMemsetAsync(step_, 0, sizeof(long long), st), "memset");
   }
 
-  void set_shard(int n, int first) {
-    if (n < 1 || n > d_.n_max || first < 0 || first + n > d_.global_batch) throw BadArg("bad shard");
-    first_ = first;
-    if (n != n_) {
-      n_ = n;
-      build_plans();
-      graph_valid_ = false;
-      phases_valid_ = false;
-    }
-  }
-
-  void set_external_input(bool ext) {
-    external_ = ext;
-    graph_valid_ = false;
-    phases_valid_ = false;
-  }
-
-  void upload_images(const float* host, int n, cudaStream_t st) {
+  void upload_images(const float* host, int n, cudaStream_t st) override {
     if (d_.block_lo != 0) throw BadArg("only partition 0 loads data");
     if (n != n_) throw BadArg("upload size != shard size");
     cuda(cudaMemcpyAsync(stage_, host, static_cast<size_t>(n) * 32 * 32 * 3 * sizeof(float), cudaMemcpyHostToDevice,
@@ -237,81 +184,7 @@ class Partition {
     check(pbdk::pack_image(stage_, input_, n, st), "pack image");
   }
 
-  // ---- K11 peer relay (relay.cu): the receiver's input buffer is written by its senders
-  void relay_set_recv(int n, void* const* remote_consumed) {
-    if (n < 0 || n > pbdk::kRelayMaxPeers) throw BadArg("relay: too many senders");
-    if (n > 0 && d_.block_lo == 0) throw BadArg("relay: partition 0 loads data, it receives nothing");
-    recv_consumed_.assign(remote_consumed, remote_consumed + n);
-    graph_valid_ = phases_valid_ = false;
-  }
-
-  void relay_set_send(int n, const pbdx_relay_msg* msgs) {
-    if (n < 0 || n > pbdk::kRelayMaxPeers) throw BadArg("relay: too many receivers");
-    const size_t row = tout_bytes_ / static_cast<size_t>(d_.n_max);
-    send_.clear();
-    for (int i = 0; i < n; ++i) {
-      const pbdx_relay_msg& m = msgs[i];
-      if (m.src_row < 0 || m.rows < 0 || m.src_row + m.rows > n_ || m.dst == nullptr || m.remote_flag == nullptr)
-        throw BadArg("relay: bad message");
-      if ((row * m.rows) % 16 != 0 || reinterpret_cast<uintptr_t>(m.dst) % 16 != 0) throw BadArg("relay: alignment");
-      send_.push_back(m);
-    }
-    if (!send_.empty() && relay_stream_ == nullptr) {
-      cuda(cudaStreamCreateWithFlags(&relay_stream_, cudaStreamNonBlocking), "stream");
-      cuda(cudaEventCreateWithFlags(&relay_fork_, cudaEventDisableTiming), "event");
-      cuda(cudaEventCreateWithFlags(&relay_done_, cudaEventDisableTiming), "event");
-    }
-    graph_valid_ = phases_valid_ = false;
-  }
-
-  void relay_wait_input(cudaStream_t st) {
-    if (recv_consumed_.empty()) return;
-    pbdk::RelayWaitArgs a{};
-    for (size_t i = 0; i < recv_consumed_.size(); ++i) a.flags[i] = mailbox_ + i;
-    a.seq = relay_seq_ + 0;  // receive sequence
-    a.bias = 1;
-    a.count = static_cast<int>(recv_consumed_.size());
-    check(pbdk::relay_wait(a, st), "relay wait input");
-  }
-
-  void relay_send_output(cudaStream_t st) {
-    if (send_.empty()) return;
-    cuda(cudaEventRecord(relay_fork_, st), "event");
-    cuda(cudaStreamWaitEvent(relay_stream_, relay_fork_, 0), "wait");
-    pbdk::RelayWaitArgs w{};
-    pbdk::RelayCopyArgs c{};
-    const size_t row = tout_bytes_ / static_cast<size_t>(d_.n_max);
-    const char* out = reinterpret_cast<const char*>(tblocks_.back().out);
-    for (size_t i = 0; i < send_.size(); ++i) {
-      w.flags[i] = mailbox_ + pbdk::kRelayMaxPeers + i;
-      c.src[i] = out + row * static_cast<size_t>(send_[i].src_row);
-      c.dst[i] = send_[i].dst;
-      c.vec16[i] = static_cast<long long>(row * static_cast<size_t>(send_[i].rows) / 16);
-      c.ready[i] = static_cast<unsigned long long*>(send_[i].remote_flag);
-    }
-    w.count = c.count = static_cast<int>(send_.size());
-    w.seq = c.seq = relay_seq_ + 1;  // send sequence
-    w.bias = 0;
-    c.ticket = relay_ticket_;
-    check(pbdk::relay_wait(w, relay_stream_), "relay wait consumed");
-    check(pbdk::relay_copy(c, 64, relay_stream_), "relay copy");
-    cuda(cudaEventRecord(relay_done_, relay_stream_), "event");
-  }
-
-  // after the last reader of the input (teacher block lo, student block lo) and the send
-  void relay_finish(cudaStream_t st) {
-    if (!send_.empty()) cuda(cudaStreamWaitEvent(st, relay_done_, 0), "join relay");
-    if (recv_consumed_.empty()) return;
-    pbdk::RelayReleaseArgs a{};
-    for (size_t i = 0; i < recv_consumed_.size(); ++i)
-      a.flags[i] = static_cast<unsigned long long*>(recv_consumed_[i]);
-    a.seq = relay_seq_ + 0;
-    a.count = static_cast<int>(recv_consumed_.size());
-    check(pbdk::relay_release(a, st), "relay release");
-  }
-
-  void teacher_forward(cudaStream_t st) {
-    relay_wait_input(st);
+  void teacher_body(cudaStream_t st) override {
     if (d_.block_lo == 0 && !external_)
       check(pbdk::philox_image(input_, n_, first_, step_, d_.global_batch, d_.seed_data, st), "philox");
     for (size_t i = 0; i < tblocks_.size(); ++i) {
@@ -320,16 +193,13 @@ class Partition {
       if (timing_) cuda(cudaEventRecord(ev_t_[2 * i + 1], st), "event");
       cuda(cudaEventRecord(tdone_[i], st), "event");
     }
-    relay_send_output(st);
   }
 
   // Student block k runs on its own stream.  Fused step(): it starts once teacher block k is
   // done (event recorded by teacher_forward).  Standalone phase (multi-GPU driver, phase
   // graphs): the student streams fork from the caller's stream at entry.  The caller's
   // stream joins all of them before returning.
-  void student_step(cudaStream_t caller) { student_step_impl(caller, true); }
-
-  void student_step_impl(cudaStream_t caller, bool fork) {
+  void student_body(cudaStream_t caller, bool fork) override {
     if (fork) cuda(cudaEventRecord(fork_, caller), "event");
     for (size_t i = 0; i < sblocks_.size(); ++i) {
       SBlock& s = sblocks_[i];
@@ -361,105 +231,20 @@ class Partition {
       cuda(cudaEventRecord(s.done, st), "event");
     }
     for (SBlock& s : sblocks_) cuda(cudaStreamWaitEvent(caller, s.done, 0), "join");
-    relay_finish(caller);
   }
 
   // bf16 shadows + flipped dgrad weights from the fp32 master weights (after a state migration)
-  void refresh_shadows(cudaStream_t st) {
+  void refresh_shadows(cudaStream_t st) override {
     check(pbdk::sgd_momentum(params_, mom_, grads_, shadow_, total_, 0.0f, 1.0f, nullptr, st), "shadow");
     refresh_flips(st);
   }
 
-  void apply_update(cudaStream_t st) {
+  void update_body(cudaStream_t st) override {
     check(pbdk::sgd_momentum(params_, mom_, grads_, shadow_, total_, d_.lr, d_.momentum, step_, st), "sgd");
     refresh_flips(st);
   }
 
-  void step(cudaStream_t st) {
-    teacher_forward(st);
-    student_step_impl(st, false);
-    apply_update(st);
-  }
-
-  // Three graphs (teacher_forward / student_step / apply_update) for the multi-GPU driver, which
-  // interleaves NCCL relay and allreduce between them.
-  // fuse_ts: phase 0 = teacher_forward + student_step with the per-block teacher->student
-  // overlap of step(), phase 1 empty (ranks that send no relay: nothing to put in between).
-  void capture_phases(cudaStream_t caller, bool fuse_ts) {
-    if (cap_stream_ == nullptr) cuda(cudaStreamCreateWithFlags(&cap_stream_, cudaStreamNonBlocking), "stream");
-    cuda(cudaStreamSynchronize(caller), "sync");
-    const bool was_timing = timing_;
-    timing_ = false;
-    for (int ph = 0; ph < 3; ++ph) {
-      if (phase_exec_[ph] != nullptr) {
-        cudaGraphExecDestroy(phase_exec_[ph]);
-        phase_exec_[ph] = nullptr;
-      }
-      cudaGraph_t g = nullptr;
-      cuda(cudaStreamBeginCapture(cap_stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
-      try {
-        if (ph == 0) {
-          teacher_forward(cap_stream_);
-          if (fuse_ts) student_step_impl(cap_stream_, false);
-        }
-        if (ph == 1 && !fuse_ts) student_step_impl(cap_stream_, true);
-        if (ph == 2) apply_update(cap_stream_);
-      } catch (...) {
-        cudaStreamEndCapture(cap_stream_, &g);
-        if (g) cudaGraphDestroy(g);
-        timing_ = was_timing;
-        throw;
-      }
-      cuda(cudaStreamEndCapture(cap_stream_, &g), "end capture");
-      size_t nodes = 0;
-      cuda(cudaGraphGetNodes(g, nullptr, &nodes), "graph nodes");
-      if (nodes > 0) cuda(cudaGraphInstantiate(&phase_exec_[ph], g, 0), "instantiate");
-      cudaGraphDestroy(g);
-    }
-    timing_ = was_timing;
-    phases_valid_ = true;
-  }
-
-  void replay_phase(int ph, cudaStream_t st) {
-    if (ph < 0 || ph > 2 || !phases_valid_) throw BadArg("no captured phase graph");
-    if (phase_exec_[ph] != nullptr) cuda(cudaGraphLaunch(phase_exec_[ph], st), "graph launch");
-  }
-
-  // Captures on a private non-blocking stream (the legacy default stream cannot be
-  // captured); the instantiated graph is replayed on the caller's stream.
-  void capture(cudaStream_t caller) {
-    if (graph_exec_ != nullptr) {
-      cudaGraphExecDestroy(graph_exec_);
-      graph_exec_ = nullptr;
-    }
-    if (cap_stream_ == nullptr) cuda(cudaStreamCreateWithFlags(&cap_stream_, cudaStreamNonBlocking), "stream");
-    cuda(cudaStreamSynchronize(caller), "sync");
-    cudaStream_t st = cap_stream_;
-    cudaGraph_t g = nullptr;
-    cuda(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
-    const bool was_timing = timing_;
-    timing_ = false;
-    try {
-      step(st);
-    } catch (...) {
-      cudaStreamEndCapture(st, &g);
-      if (g) cudaGraphDestroy(g);
-      timing_ = was_timing;
-      throw;
-    }
-    timing_ = was_timing;
-    cuda(cudaStreamEndCapture(st, &g), "end capture");
-    cuda(cudaGraphInstantiate(&graph_exec_, g, 0), "instantiate");
-    cudaGraphDestroy(g);
-    graph_valid_ = true;
-  }
-
-  void replay(cudaStream_t st) {
-    if (!graph_valid_ || graph_exec_ == nullptr) throw BadArg("no captured graph for the current shard");
-    cuda(cudaGraphLaunch(graph_exec_, st), "graph launch");
-  }
-
-  void set_timing(bool on) {
+  void set_timing(bool on) override {
     timing_ = on;
     if (on && ev_t_.empty()) {
       ev_t_.resize(2 * tblocks_.size());
@@ -469,7 +254,7 @@ class Partition {
     }
   }
 
-  void block_times(float* tms, float* sms) {
+  void block_times(float* tms, float* sms) override {
     if (ev_t_.empty()) throw BadArg("timing not enabled");
     for (size_t i = 0; i < tblocks_.size(); ++i) {
       cuda(cudaEventSynchronize(ev_t_[2 * i + 1]), "event sync");
@@ -479,7 +264,7 @@ class Partition {
     }
   }
 
-  void buffer(int which, void** ptr, size_t* bytes) {
+  void buffer(int which, void** ptr, size_t* bytes) override {
     switch (which) {
       case PBDX_BUF_INPUT: *ptr = input_; *bytes = input_bytes_; break;
       case PBDX_BUF_TEACHER_OUT: *ptr = tblocks_.back().out; *bytes = tout_bytes_; break;
@@ -494,13 +279,13 @@ class Partition {
     }
   }
 
-  void teacher_act(int k, void** ptr, size_t* bytes) {
+  void teacher_act(int k, void** ptr, size_t* bytes) override {
     if (k < d_.block_lo || k > d_.block_hi) throw BadArg("block outside partition");
     *ptr = tblocks_[static_cast<size_t>(k - d_.block_lo)].out;
     *bytes = act_bytes(T_HW[k + 1], T_CH[k + 1]);
   }
 
-  int launches_per_step() const {
+  int body_launches_per_step() const override {
     int n = (d_.block_lo == 0 && !external_) ? 1 : 0;
     for (const TBlock& tb : tblocks_) n += static_cast<int>(tb.convs.size());
     for (const SBlock& s : sblocks_) {
@@ -508,25 +293,16 @@ class Partition {
       n += (s.p_w2.splits > 1 ? 2 : 1) + (s.p_wsc.splits > 1 ? 2 : 1) + (s.p_w1.splits > 1 ? 2 : 1);
     }
     n += 1 + static_cast<int>(sblocks_.size());  // sgd + flips
-    if (!recv_consumed_.empty()) n += 2;         // relay wait + release
-    if (!send_.empty()) n += 2;                  // relay wait + copy
     return n;
   }
 
-  ~Partition() {
-    if (graph_exec_ != nullptr) cudaGraphExecDestroy(graph_exec_);
-    if (cap_stream_ != nullptr) cudaStreamDestroy(cap_stream_);
+  ~ResNetPartition() override {
     for (SBlock& s : sblocks_) {
       if (s.stream != nullptr) cudaStreamDestroy(s.stream);
       if (s.done != nullptr) cudaEventDestroy(s.done);
     }
     for (auto e : tdone_) cudaEventDestroy(e);
-    for (auto g : phase_exec_)
-      if (g != nullptr) cudaGraphExecDestroy(g);
     if (fork_ != nullptr) cudaEventDestroy(fork_);
-    if (relay_stream_ != nullptr) cudaStreamDestroy(relay_stream_);
-    if (relay_fork_ != nullptr) cudaEventDestroy(relay_fork_);
-    if (relay_done_ != nullptr) cudaEventDestroy(relay_done_);
     for (auto e : ev_t_) cudaEventDestroy(e);
     for (auto e : ev_s_) cudaEventDestroy(e);
   }
@@ -665,9 +441,7 @@ class Partition {
     shadow_ = arena_.get<bf16>(total_ * sizeof(bf16));
     losses_ = arena_.get<double>(kBlocks * sizeof(double));
     step_ = arena_.get<long long>(sizeof(long long));
-    mailbox_ = arena_.get<unsigned long long>(2 * pbdk::kRelayMaxPeers * sizeof(unsigned long long));
-    relay_seq_ = arena_.get<unsigned long long>(2 * sizeof(unsigned long long));
-    relay_ticket_ = arena_.get<unsigned int>(sizeof(unsigned int));
+    allocate_relay();
 
     // ---- per-block scratch sized for n_max, streams and events
     for (SBlock& s : sblocks_) {
@@ -722,18 +496,7 @@ class Partition {
     }
   }
 
-  pbdx_desc d_;
-  int n_ = 0;
-  int first_ = 0;
-  bool external_ = false;
-  bool timing_ = false;
-  bool graph_valid_ = false;
-  cudaGraphExec_t graph_exec_ = nullptr;
-  cudaGraphExec_t phase_exec_[3] = {nullptr, nullptr, nullptr};
-  bool phases_valid_ = false;
   cudaEvent_t fork_ = nullptr;
-  cudaStream_t cap_stream_ = nullptr;
-  Arena arena_;
   bf16* input_ = nullptr;
   size_t input_bytes_ = 0;
   float* stage_ = nullptr;
@@ -749,108 +512,19 @@ class Partition {
   long long* step_ = nullptr;
   std::vector<cudaEvent_t> tdone_;
   std::vector<cudaEvent_t> ev_t_, ev_s_;
-  // K11 relay state: mailbox_ = flags written by peers ([0,16) ready per sender, [16,32) consumed
-  // per receiver); relay_seq_ = {receive seq, send seq} (device-side, so graph replays advance them)
-  unsigned long long* mailbox_ = nullptr;
-  unsigned long long* relay_seq_ = nullptr;
-  unsigned int* relay_ticket_ = nullptr;
-  std::vector<void*> recv_consumed_;
-  std::vector<pbdx_relay_msg> send_;
-  cudaStream_t relay_stream_ = nullptr;
-  cudaEvent_t relay_fork_ = nullptr, relay_done_ = nullptr;
 };
-
-}  // namespace pbd::exec
-
-// ------------------------------------------------------------------ C ABI
-namespace {
-
-using pbd::exec::Partition;
-
-template <class F>
-int guard(F&& f) {
-  try {
-    f();
-    return PBDK_OK;
-  } catch (const pbd::exec::BadArg&) {
-    return PBDK_EINVAL;
-  } catch (const std::bad_alloc&) {
-    return PBDK_ECUDA;
-  } catch (const std::exception&) {
-    return PBDK_ECUDA;
-  }
-}
-
-Partition* P(void* h) { return static_cast<Partition*>(h); }
-cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 
 }  // namespace
 
-extern "C" {
+PartitionBase* make_resnet_partition(const pbdx_desc& d) { return new ResNetPartition(d); }
 
-int pbdx_create(const pbdx_desc* d, void** handle) {
-  if (d == nullptr || handle == nullptr) return PBDK_EINVAL;
-  return guard([&] { *handle = new Partition(*d); });
-}
+}  // namespace pbd::exec
 
-void pbdx_destroy(void* handle) { delete P(handle); }
-
-int pbdx_init_params(void* h, void* st) { return guard([&] { P(h)->init_params(S(st)); }); }
-int pbdx_set_shard(void* h, int n, int first) { return guard([&] { P(h)->set_shard(n, first); }); }
-int pbdx_set_input_mode(void* h, int external) { return guard([&] { P(h)->set_external_input(external != 0); }); }
-int pbdx_upload_images(void* h, const float* host, int n, void* st) {
-  return guard([&] { P(h)->upload_images(host, n, S(st)); });
-}
-int pbdx_teacher_forward(void* h, void* st) { return guard([&] { P(h)->teacher_forward(S(st)); }); }
-int pbdx_student_step(void* h, void* st) { return guard([&] { P(h)->student_step(S(st)); }); }
-int pbdx_apply_update(void* h, void* st) { return guard([&] { P(h)->apply_update(S(st)); }); }
-int pbdx_step(void* h, void* st) { return guard([&] { P(h)->step(S(st)); }); }
-int pbdx_capture(void* h, void* st) { return guard([&] { P(h)->capture(S(st)); }); }
-int pbdx_replay(void* h, void* st) { return guard([&] { P(h)->replay(S(st)); }); }
-int pbdx_capture_phases(void* h, int fuse_ts, void* st) {
-  return guard([&] { P(h)->capture_phases(S(st), fuse_ts != 0); });
-}
-int pbdx_replay_phase(void* h, int phase, void* st) { return guard([&] { P(h)->replay_phase(phase, S(st)); }); }
-int pbdx_buffer(void* h, int which, void** ptr, size_t* bytes) {
-  return guard([&] { P(h)->buffer(which, ptr, bytes); });
-}
-int pbdx_num_blocks(void* h) { return P(h)->nblocks(); }
-int pbdx_teacher_act(void* h, int block, void** ptr, size_t* bytes) {
-  return guard([&] { P(h)->teacher_act(block, ptr, bytes); });
-}
-int pbdx_refresh_shadows(void* h, void* st) { return guard([&] { P(h)->refresh_shadows(S(st)); }); }
-int pbdx_set_timing(void* h, int enabled) { return guard([&] { P(h)->set_timing(enabled != 0); }); }
-int pbdx_block_times(void* h, float* t, float* s) { return guard([&] { P(h)->block_times(t, s); }); }
-int pbdx_launches_per_step(void* h) { return P(h)->launches_per_step(); }
-int pbdx_relay_set_recv(void* h, int nsenders, void* const* remote_consumed_flags) {
-  if (nsenders > 0 && remote_consumed_flags == nullptr) return PBDK_EINVAL;
-  return guard([&] { P(h)->relay_set_recv(nsenders, remote_consumed_flags); });
-}
-int pbdx_relay_set_send(void* h, int nmsgs, const pbdx_relay_msg* msgs) {
-  if (nmsgs > 0 && msgs == nullptr) return PBDK_EINVAL;
-  return guard([&] { P(h)->relay_set_send(nmsgs, msgs); });
-}
-int pbdx_ipc_export(void* dev_ptr, void* handle) {
-  if (dev_ptr == nullptr || handle == nullptr) return PBDK_EINVAL;
-  cudaIpcMemHandle_t hd;
-  if (cudaIpcGetMemHandle(&hd, dev_ptr) != cudaSuccess) return PBDK_ECUDA;
-  std::memcpy(handle, &hd, sizeof(hd));
-  return PBDK_OK;
-}
-int pbdx_ipc_open(const void* handle, void** dev_ptr) {
-  if (dev_ptr == nullptr || handle == nullptr) return PBDK_EINVAL;
-  cudaIpcMemHandle_t hd;
-  std::memcpy(&hd, handle, sizeof(hd));
-  return cudaIpcOpenMemHandle(dev_ptr, hd, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess ? PBDK_OK : PBDK_ECUDA;
-}
-int pbdx_ipc_close(void* dev_ptr) { return cudaIpcCloseMemHandle(dev_ptr) == cudaSuccess ? PBDK_OK : PBDK_ECUDA; }
-
-long pbdx_student_layout(int block, long* out) {
+// ------------------------------------------------------------------ C ABI (ResNet layout query)
+extern "C" long pbdx_student_layout(int block, long* out) {
   if (block < 0 || block >= pbd::exec::kBlocks || out == nullptr) return -1;
   const auto l = pbd::exec::student_layout(block);
   const size_t v[9] = {l.w1, l.w2, l.wsc, l.g1, l.b1, l.g2, l.b2, l.gsc, l.bsc};
   for (int i = 0; i < 9; ++i) out[i] = static_cast<long>(v[i]);
   return static_cast<long>(l.total);
 }
-
-}  // extern "C"

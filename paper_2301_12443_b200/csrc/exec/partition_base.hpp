@@ -1,0 +1,330 @@
+// Model-independent half of the per-GPU partition executor (include/pbdx.h): the phases of
+// Algorithm 1 around the model's own teacher / student / update bodies,
+// the K11 peer relay hooks (relay.cu), CUDA-graph capture of a whole step or of its phases,
+// and the device arena.  Models: ResNetPartition (CIFAR ResNet-18 -> slim residual student,
+// partition.cpp) and MbPartition (MobileNetV2 -> ProxylessNAS supernet, mb_partition.cpp).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "pbdk.h"
+#include "pbdx.h"
+#include "relay.hpp"
+
+namespace pbd::exec {
+
+struct CudaFail : std::runtime_error {
+  explicit CudaFail(const std::string& m) : std::runtime_error(m) {}
+};
+struct BadArg : std::runtime_error {
+  explicit BadArg(const std::string& m) : std::runtime_error(m) {}
+};
+
+inline void check(int rc, const char* what) {
+  if (rc == PBDK_EINVAL) throw BadArg(what);
+  if (rc != PBDK_OK) throw CudaFail(std::string(what) + ": " + cudaGetErrorString(cudaGetLastError()));
+}
+inline void cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaFail(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+class Arena {
+ public:
+  ~Arena() {
+    for (void* p : ptrs_) cudaFree(p);
+  }
+  template <class T = void>
+  T* get(size_t bytes) {
+    void* p = nullptr;
+    bytes = (bytes + 255) / 256 * 256;
+    if (bytes == 0) bytes = 256;
+    cuda(cudaMalloc(&p, bytes), "cudaMalloc");
+    cuda(cudaMemset(p, 0, bytes), "cudaMemset");
+    ptrs_.push_back(p);
+    bytes_ += bytes;
+    return static_cast<T*>(p);
+  }
+  size_t bytes() const { return bytes_; }
+
+ private:
+  std::vector<void*> ptrs_;
+  size_t bytes_ = 0;
+};
+
+class PartitionBase {
+ public:
+  explicit PartitionBase(const pbdx_desc& d) : d_(d), n_(d.n_max) {
+    if (d.n_max < 1 || d.global_batch < 1) throw BadArg("bad batch");
+  }
+  virtual ~PartitionBase() {
+    if (graph_exec_ != nullptr) cudaGraphExecDestroy(graph_exec_);
+    for (auto g : phase_exec_)
+      if (g != nullptr) cudaGraphExecDestroy(g);
+    if (cap_stream_ != nullptr) cudaStreamDestroy(cap_stream_);
+    if (relay_stream_ != nullptr) cudaStreamDestroy(relay_stream_);
+    if (relay_fork_ != nullptr) cudaEventDestroy(relay_fork_);
+    if (relay_done_ != nullptr) cudaEventDestroy(relay_done_);
+  }
+
+  // ---- model hooks
+  virtual int nblocks() const = 0;
+  virtual void init_params(cudaStream_t st) = 0;
+  virtual void rebuild_for_shard() = 0;  // n_ changed
+  virtual void upload_images(const float* host, int n, cudaStream_t st) = 0;
+  virtual void teacher_body(cudaStream_t st) = 0;
+  // student blocks; fork: start from the caller's stream (standalone phase) instead of the
+  // per-block teacher events.  Must join every side stream back into `caller`.
+  virtual void student_body(cudaStream_t caller, bool fork) = 0;
+  virtual void update_body(cudaStream_t st) = 0;
+  virtual void refresh_shadows(cudaStream_t st) = 0;
+  virtual void buffer(int which, void** ptr, size_t* bytes) = 0;
+  virtual void teacher_act(int k, void** ptr, size_t* bytes) = 0;
+  virtual void set_timing(bool on) = 0;
+  virtual void block_times(float* tms, float* sms) = 0;
+  virtual int body_launches_per_step() const = 0;
+  virtual void set_path(int /*block*/, const int* /*path*/, int /*n*/) { throw BadArg("model has no search space"); }
+  // relayed activation (teacher output of block_hi) and its bytes per sample
+  virtual const void* relay_source() const = 0;
+  virtual size_t relay_row_bytes() const = 0;
+
+  // ---- Algorithm 1 phases
+  void set_shard(int n, int first) {
+    if (n < 1 || n > d_.n_max || first < 0 || first + n > d_.global_batch) throw BadArg("bad shard");
+    first_ = first;
+    if (n != n_) {
+      n_ = n;
+      rebuild_for_shard();
+      invalidate_graphs();
+    }
+  }
+
+  void set_external_input(bool ext) {
+    external_ = ext;
+    invalidate_graphs();
+  }
+
+  void teacher_forward(cudaStream_t st) {
+    relay_wait_input(st);
+    teacher_body(st);
+    relay_send_output(st);
+  }
+  void student_step(cudaStream_t caller) { student_step_impl(caller, true); }
+  void student_step_impl(cudaStream_t caller, bool fork) {
+    student_body(caller, fork);
+    relay_finish(caller);
+  }
+  void apply_update(cudaStream_t st) { update_body(st); }
+  void step(cudaStream_t st) {
+    teacher_forward(st);
+    student_step_impl(st, false);
+    apply_update(st);
+  }
+
+  int launches_per_step() const {
+    int n = body_launches_per_step();
+    if (!recv_consumed_.empty()) n += 2;  // relay wait + release
+    if (!send_.empty()) n += 2;           // relay wait + copy
+    return n;
+  }
+
+  // ---- CUDA graphs
+  // Three graphs (teacher_forward / student_step / apply_update) for the multi-GPU driver, which
+  // interleaves NCCL collectives between them.  fuse_ts: phase 0 = teacher_forward + student_step
+  // with the per-block teacher->student overlap of step(), phase 1 empty.
+  void capture_phases(cudaStream_t caller, bool fuse_ts) {
+    ensure_cap_stream();
+    cuda(cudaStreamSynchronize(caller), "sync");
+    const bool was_timing = timing_;
+    timing_ = false;
+    for (int ph = 0; ph < 3; ++ph) {
+      if (phase_exec_[ph] != nullptr) {
+        cudaGraphExecDestroy(phase_exec_[ph]);
+        phase_exec_[ph] = nullptr;
+      }
+      cudaGraph_t g = nullptr;
+      cuda(cudaStreamBeginCapture(cap_stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
+      try {
+        if (ph == 0) {
+          teacher_forward(cap_stream_);
+          if (fuse_ts) student_step_impl(cap_stream_, false);
+        }
+        if (ph == 1 && !fuse_ts) student_step_impl(cap_stream_, true);
+        if (ph == 2) apply_update(cap_stream_);
+      } catch (...) {
+        cudaStreamEndCapture(cap_stream_, &g);
+        if (g) cudaGraphDestroy(g);
+        timing_ = was_timing;
+        throw;
+      }
+      cuda(cudaStreamEndCapture(cap_stream_, &g), "end capture");
+      size_t nodes = 0;
+      cuda(cudaGraphGetNodes(g, nullptr, &nodes), "graph nodes");
+      if (nodes > 0) cuda(cudaGraphInstantiate(&phase_exec_[ph], g, 0), "instantiate");
+      cudaGraphDestroy(g);
+    }
+    timing_ = was_timing;
+    phases_valid_ = true;
+  }
+
+  void replay_phase(int ph, cudaStream_t st) {
+    if (ph < 0 || ph > 2 || !phases_valid_) throw BadArg("no captured phase graph");
+    if (phase_exec_[ph] != nullptr) cuda(cudaGraphLaunch(phase_exec_[ph], st), "graph launch");
+  }
+
+  // Captures on a private non-blocking stream (the legacy default stream cannot be captured);
+  // the instantiated graph is replayed on the caller's stream.
+  void capture(cudaStream_t caller) {
+    if (graph_exec_ != nullptr) {
+      cudaGraphExecDestroy(graph_exec_);
+      graph_exec_ = nullptr;
+    }
+    ensure_cap_stream();
+    cuda(cudaStreamSynchronize(caller), "sync");
+    cudaGraph_t g = nullptr;
+    cuda(cudaStreamBeginCapture(cap_stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
+    const bool was_timing = timing_;
+    timing_ = false;
+    try {
+      step(cap_stream_);
+    } catch (...) {
+      cudaStreamEndCapture(cap_stream_, &g);
+      if (g) cudaGraphDestroy(g);
+      timing_ = was_timing;
+      throw;
+    }
+    timing_ = was_timing;
+    cuda(cudaStreamEndCapture(cap_stream_, &g), "end capture");
+    cuda(cudaGraphInstantiate(&graph_exec_, g, 0), "instantiate");
+    cudaGraphDestroy(g);
+    graph_valid_ = true;
+  }
+
+  void replay(cudaStream_t st) {
+    if (!graph_valid_ || graph_exec_ == nullptr) throw BadArg("no captured graph for the current shard");
+    cuda(cudaGraphLaunch(graph_exec_, st), "graph launch");
+  }
+
+  // ---- K11 peer relay (relay.cu): the receiver's input buffer is written by its senders
+  void relay_set_recv(int n, void* const* remote_consumed) {
+    if (n < 0 || n > pbdk::kRelayMaxPeers) throw BadArg("relay: too many senders");
+    if (n > 0 && d_.block_lo == 0) throw BadArg("relay: partition 0 loads data, it receives nothing");
+    recv_consumed_.assign(remote_consumed, remote_consumed + n);
+    invalidate_graphs();
+  }
+
+  void relay_set_send(int n, const pbdx_relay_msg* msgs) {
+    if (n < 0 || n > pbdk::kRelayMaxPeers) throw BadArg("relay: too many receivers");
+    const size_t row = relay_row_bytes();
+    send_.clear();
+    for (int i = 0; i < n; ++i) {
+      const pbdx_relay_msg& m = msgs[i];
+      if (m.src_row < 0 || m.rows < 0 || m.src_row + m.rows > n_ || m.dst == nullptr || m.remote_flag == nullptr)
+        throw BadArg("relay: bad message");
+      if ((row * m.rows) % 16 != 0 || reinterpret_cast<uintptr_t>(m.dst) % 16 != 0) throw BadArg("relay: alignment");
+      send_.push_back(m);
+    }
+    if (!send_.empty() && relay_stream_ == nullptr) {
+      cuda(cudaStreamCreateWithFlags(&relay_stream_, cudaStreamNonBlocking), "stream");
+      cuda(cudaEventCreateWithFlags(&relay_fork_, cudaEventDisableTiming), "event");
+      cuda(cudaEventCreateWithFlags(&relay_done_, cudaEventDisableTiming), "event");
+    }
+    invalidate_graphs();
+  }
+
+  const pbdx_desc& desc() const { return d_; }
+
+ protected:
+  void invalidate_graphs() { graph_valid_ = phases_valid_ = false; }
+
+  void ensure_cap_stream() {
+    if (cap_stream_ == nullptr) cuda(cudaStreamCreateWithFlags(&cap_stream_, cudaStreamNonBlocking), "stream");
+  }
+
+  // relay flag storage (call from the model's allocate())
+  void allocate_relay() {
+    mailbox_ = arena_.get<unsigned long long>(2 * pbdk::kRelayMaxPeers * sizeof(unsigned long long));
+    relay_seq_ = arena_.get<unsigned long long>(2 * sizeof(unsigned long long));
+    relay_ticket_ = arena_.get<unsigned int>(sizeof(unsigned int));
+  }
+
+  void relay_wait_input(cudaStream_t st) {
+    if (recv_consumed_.empty()) return;
+    pbdk::RelayWaitArgs a{};
+    for (size_t i = 0; i < recv_consumed_.size(); ++i) a.flags[i] = mailbox_ + i;
+    a.seq = relay_seq_ + 0;  // receive sequence
+    a.bias = 1;
+    a.count = static_cast<int>(recv_consumed_.size());
+    check(pbdk::relay_wait(a, st), "relay wait input");
+  }
+
+  void relay_send_output(cudaStream_t st) {
+    if (send_.empty()) return;
+    cuda(cudaEventRecord(relay_fork_, st), "event");
+    cuda(cudaStreamWaitEvent(relay_stream_, relay_fork_, 0), "wait");
+    pbdk::RelayWaitArgs w{};
+    pbdk::RelayCopyArgs c{};
+    const size_t row = relay_row_bytes();
+    const char* out = static_cast<const char*>(relay_source());
+    for (size_t i = 0; i < send_.size(); ++i) {
+      w.flags[i] = mailbox_ + pbdk::kRelayMaxPeers + i;
+      c.src[i] = out + row * static_cast<size_t>(send_[i].src_row);
+      c.dst[i] = send_[i].dst;
+      c.vec16[i] = static_cast<long long>(row * static_cast<size_t>(send_[i].rows) / 16);
+      c.ready[i] = static_cast<unsigned long long*>(send_[i].remote_flag);
+    }
+    w.count = c.count = static_cast<int>(send_.size());
+    w.seq = c.seq = relay_seq_ + 1;  // send sequence
+    w.bias = 0;
+    c.ticket = relay_ticket_;
+    check(pbdk::relay_wait(w, relay_stream_), "relay wait consumed");
+    check(pbdk::relay_copy(c, 64, relay_stream_), "relay copy");
+    cuda(cudaEventRecord(relay_done_, relay_stream_), "event");
+  }
+
+  // after the last reader of the input (teacher block lo, student block lo) and the send
+  void relay_finish(cudaStream_t st) {
+    if (!send_.empty()) cuda(cudaStreamWaitEvent(st, relay_done_, 0), "join relay");
+    if (recv_consumed_.empty()) return;
+    pbdk::RelayReleaseArgs a{};
+    for (size_t i = 0; i < recv_consumed_.size(); ++i)
+      a.flags[i] = static_cast<unsigned long long*>(recv_consumed_[i]);
+    a.seq = relay_seq_ + 0;
+    a.count = static_cast<int>(recv_consumed_.size());
+    check(pbdk::relay_release(a, st), "relay release");
+  }
+
+  pbdx_desc d_;
+  int n_ = 0;
+  int first_ = 0;
+  bool external_ = false;
+  bool timing_ = false;
+  Arena arena_;
+  // K11 relay state: mailbox_ = flags written by peers ([0,16) ready per sender, [16,32) consumed
+  // per receiver); relay_seq_ = {receive seq, send seq} (device-side, so graph replays advance them)
+  unsigned long long* mailbox_ = nullptr;
+  unsigned long long* relay_seq_ = nullptr;
+  unsigned int* relay_ticket_ = nullptr;
+
+ private:
+  bool graph_valid_ = false;
+  bool phases_valid_ = false;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  cudaGraphExec_t phase_exec_[3] = {nullptr, nullptr, nullptr};
+  cudaStream_t cap_stream_ = nullptr;
+  std::vector<void*> recv_consumed_;
+  std::vector<pbdx_relay_msg> send_;
+  cudaStream_t relay_stream_ = nullptr;
+  cudaEvent_t relay_fork_ = nullptr, relay_done_ = nullptr;
+};
+
+// model factories
+PartitionBase* make_resnet_partition(const pbdx_desc& d);
+PartitionBase* make_mb_partition(const pbdx_desc& d);
+
+}  // namespace pbd::exec

@@ -72,18 +72,19 @@ __device__ __forceinline__ float sym_unit(uint32_t u) {
 // ------------------------------------------------------------------ data / init
 
 // x[n][32][32][16] bf16; channels 0..2 from Philox, 3..15 zero.
-__global__ void philox_image_kernel(__nv_bfloat16* __restrict__ x, int n, long long first, const long long* counter,
-                                    int global_batch, uint32_t seed) {
+__global__ void philox_image_kernel(__nv_bfloat16* __restrict__ x, int n, int npix, long long first,
+                                    const long long* counter, int global_batch, uint32_t seed) {
   const long long base = first + (counter != nullptr ? (*counter) * global_batch : 0);
-  const int total = n * 1024;
-  for (int pix = blockIdx.x * blockDim.x + threadIdx.x; pix < total; pix += gridDim.x * blockDim.x) {
-    const int i = pix / 1024;
-    const int hw = pix - i * 1024;
+  const long long total = static_cast<long long>(n) * npix;
+  for (long long pix = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; pix < total;
+       pix += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = pix / npix;
+    const long long hw = pix - i * npix;
     float v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const unsigned long long idx =
-          static_cast<unsigned long long>(base + i) * 3072ull + static_cast<unsigned long long>(hw * 3 + c);
+          static_cast<unsigned long long>(base + i) * (3ull * npix) + static_cast<unsigned long long>(hw * 3 + c);
       uint32_t o;
       philox10(static_cast<uint32_t>(idx), static_cast<uint32_t>(idx >> 32), 0u, 0u, seed, 0xDA7A0000u, o);
       v[c] = sym_unit(o);
@@ -95,9 +96,9 @@ __global__ void philox_image_kernel(__nv_bfloat16* __restrict__ x, int n, long l
   }
 }
 
-__global__ void pack_image_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ x, int n) {
-  const int total = n * 1024;
-  for (int pix = blockIdx.x * blockDim.x + threadIdx.x; pix < total; pix += gridDim.x * blockDim.x) {
+__global__ void pack_image_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ x, long long total) {
+  for (long long pix = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; pix < total;
+       pix += static_cast<long long>(gridDim.x) * blockDim.x) {
     float v[8] = {src[pix * 3], src[pix * 3 + 1], src[pix * 3 + 2], 0, 0, 0, 0, 0};
     const float z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     uint4* dst = reinterpret_cast<uint4*>(x + static_cast<size_t>(pix) * 16);
@@ -587,14 +588,17 @@ size_t reduce_workspace_floats(int m, int c, int nv) {
   return static_cast<size_t>(chunks) * std::max(nv, 4) * c + chunks;
 }
 
-int philox_image(void* x, int n, long long first, const long long* counter, int gb, uint32_t seed, cudaStream_t st) {
-  philox_image_kernel<<<grid_for(n * 1024LL), kThreads, 0, st>>>(static_cast<__nv_bfloat16*>(x), n, first, counter,
-                                                                  gb, seed);
+int philox_image(void* x, int n, long long first, const long long* counter, int gb, uint32_t seed, cudaStream_t st,
+                 int side) {
+  const int npix = side * side;
+  philox_image_kernel<<<grid_for(static_cast<long long>(n) * npix), kThreads, 0, st>>>(
+      static_cast<__nv_bfloat16*>(x), n, npix, first, counter, gb, seed);
   return ok(cudaGetLastError());
 }
 
-int pack_image(const float* src, void* x, int n, cudaStream_t st) {
-  pack_image_kernel<<<grid_for(n * 1024LL), kThreads, 0, st>>>(src, static_cast<__nv_bfloat16*>(x), n);
+int pack_image(const float* src, void* x, int n, cudaStream_t st, int side) {
+  const long long total = static_cast<long long>(n) * side * side;
+  pack_image_kernel<<<grid_for(total), kThreads, 0, st>>>(src, static_cast<__nv_bfloat16*>(x), total);
   return ok(cudaGetLastError());
 }
 

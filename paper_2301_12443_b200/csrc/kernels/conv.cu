@@ -56,6 +56,32 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
 
+// Epilogue semantics (pbdk.h PBDK_EPI_*): y = act(aux_op(acc + bias, aux)), fp32, one bf16 rounding.
+struct EpiFlags {
+  bool bias, aux, add, mask0, mask6, relu, relu6;
+};
+__host__ __device__ constexpr EpiFlags epi_flags(int e) {
+  return EpiFlags{e == PBDK_EPI_BIAS || e == PBDK_EPI_BIAS_RELU || e == PBDK_EPI_BIAS_RES_RELU ||
+                      e == PBDK_EPI_BIAS_RELU6 || e == PBDK_EPI_BIAS_RES,
+                  e == PBDK_EPI_BIAS_RES_RELU || e == PBDK_EPI_RELU_MASK || e == PBDK_EPI_BIAS_RES ||
+                      e == PBDK_EPI_RELU6_MASK || e == PBDK_EPI_ADD,
+                  e == PBDK_EPI_BIAS_RES_RELU || e == PBDK_EPI_BIAS_RES || e == PBDK_EPI_ADD,
+                  e == PBDK_EPI_RELU_MASK,
+                  e == PBDK_EPI_RELU6_MASK,
+                  e == PBDK_EPI_BIAS_RELU || e == PBDK_EPI_BIAS_RES_RELU,
+                  e == PBDK_EPI_BIAS_RELU6};
+}
+__device__ __forceinline__ float epi_aux(const EpiFlags& f, float v, float r) {
+  if (f.add) return v + r;
+  if (f.mask0) return r > 0.f ? v : 0.f;
+  return (r > 0.f && r < 6.f) ? v : 0.f;  // mask6: ReLU6 backward from the stored activation
+}
+__device__ __forceinline__ float epi_act(const EpiFlags& f, float v) {
+  if (f.relu) return fmaxf(v, 0.f);
+  if (f.relu6) return fminf(fmaxf(v, 0.f), 6.f);
+  return v;
+}
+
 // Epilogue: thread = accumulator row (TMEM lane).  tcgen05.ld 16 columns at a time, fused
 // bias / residual / ReLU / ReLU-mask in fp32, one bf16 rounding, 2 x 16 B stores straight
 // from registers.  No shared-memory staging on purpose: for N <= 128 the tensor core is
@@ -67,8 +93,8 @@ __device__ __forceinline__ void fprop_epilogue(const FpropArgs& a, uint32_t trow
   bool valid;
   size_t m;
   rowmap(row, valid, m);
-  const bool has_bias = a.epi == PBDK_EPI_BIAS || a.epi == PBDK_EPI_BIAS_RELU || a.epi == PBDK_EPI_BIAS_RES_RELU;
-  const bool relu = a.epi == PBDK_EPI_BIAS_RELU || a.epi == PBDK_EPI_BIAS_RES_RELU;
+  const EpiFlags f = epi_flags(a.epi);
+  const bool has_bias = f.bias;
   if (a.debug == 3 || a.debug == 9) return;
 #pragma unroll 1
   for (int c0 = 0; c0 < BN; c0 += 16) {
@@ -87,29 +113,19 @@ __device__ __forceinline__ void fprop_epilogue(const FpropArgs& a, uint32_t trow
         v[4 * j + 3] += b.w;
       }
     }
-    if (a.epi == PBDK_EPI_BIAS_RES_RELU || a.epi == PBDK_EPI_RELU_MASK) {
+    if (f.aux) {
       const uint4* r4 = reinterpret_cast<const uint4*>(a.aux + m * a.k + col);
       const uint4 ra = __ldg(r4);
       const uint4 rb = __ldg(r4 + 1);
       const uint32_t rw[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
-      if (a.epi == PBDK_EPI_BIAS_RES_RELU) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          v[2 * j] += bf16_lo(rw[j]);
-          v[2 * j + 1] += bf16_hi(rw[j]);
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          v[2 * j] = bf16_lo(rw[j]) > 0.f ? v[2 * j] : 0.f;
-          v[2 * j + 1] = bf16_hi(rw[j]) > 0.f ? v[2 * j + 1] : 0.f;
-        }
+      for (int j = 0; j < 8; ++j) {
+        v[2 * j] = epi_aux(f, v[2 * j], bf16_lo(rw[j]));
+        v[2 * j + 1] = epi_aux(f, v[2 * j + 1], bf16_hi(rw[j]));
       }
     }
-    if (relu) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j], 0.f);
-    }
+    for (int j = 0; j < 16; ++j) v[j] = epi_act(f, v[j]);
     uint4 o0, o1;
     o0.x = pack_bf16x2(v[0], v[1]);
     o0.y = pack_bf16x2(v[2], v[3]);
@@ -296,27 +312,22 @@ struct SplitCfg {
 
 __device__ __forceinline__ void epi_store4(const FpropArgs& a, size_t m, int col, float4 v) {
   float x[4] = {v.x, v.y, v.z, v.w};
-  const int epi = a.epi;
-  if (epi == PBDK_EPI_BIAS || epi == PBDK_EPI_BIAS_RELU || epi == PBDK_EPI_BIAS_RES_RELU) {
+  const EpiFlags f = epi_flags(a.epi);
+  if (f.bias) {
     const float4 b = __ldg(reinterpret_cast<const float4*>(a.bias + col));
     x[0] += b.x;
     x[1] += b.y;
     x[2] += b.z;
     x[3] += b.w;
   }
-  if (epi == PBDK_EPI_BIAS_RES_RELU || epi == PBDK_EPI_RELU_MASK) {
+  if (f.aux) {
     const uint2 r = __ldg(reinterpret_cast<const uint2*>(a.aux + m * a.k + col));
     const float rv[4] = {bf16_lo(r.x), bf16_hi(r.x), bf16_lo(r.y), bf16_hi(r.y)};
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (epi == PBDK_EPI_BIAS_RES_RELU) x[j] += rv[j];
-      else x[j] = rv[j] > 0.f ? x[j] : 0.f;
-    }
+    for (int j = 0; j < 4; ++j) x[j] = epi_aux(f, x[j], rv[j]);
   }
-  if (epi == PBDK_EPI_BIAS_RELU || epi == PBDK_EPI_BIAS_RES_RELU) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) x[j] = fmaxf(x[j], 0.f);
-  }
+  for (int j = 0; j < 4; ++j) x[j] = epi_act(f, x[j]);
   uint2 o;
   o.x = pack_bf16x2(x[0], x[1]);
   o.y = pack_bf16x2(x[2], x[3]);
@@ -1130,7 +1141,7 @@ WgradLauncher pick_wgrad(int bn, int swa, int swb) {
   }
 }
 
-int wgrad_bn(int c) { return c >= 128 ? 128 : c; }
+int wgrad_bn(int c) { return c % 128 == 0 ? 128 : c >= 64 ? 64 : c; }  // c in {16, 32} or a multiple of 64
 
 template <int BKC>
 FpropLauncher pick_splitk(int bn) {
@@ -1220,10 +1231,9 @@ int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, c
                int epi, FpropPlan* plan) {
   ConvGeom g;
   if (!make_geom(d, &g) || !chan_ok(d.c) || d.k % 16 != 0 || d.k < 16) return PBDK_EINVAL;
-  if (epi < PBDK_EPI_STORE || epi > PBDK_EPI_RELU_MASK) return PBDK_EINVAL;
-  if ((epi == PBDK_EPI_BIAS || epi == PBDK_EPI_BIAS_RELU || epi == PBDK_EPI_BIAS_RES_RELU) && bias == nullptr)
-    return PBDK_EINVAL;
-  if ((epi == PBDK_EPI_BIAS_RES_RELU || epi == PBDK_EPI_RELU_MASK) && aux == nullptr) return PBDK_EINVAL;
+  if (epi < PBDK_EPI_STORE || epi > PBDK_EPI_ADD) return PBDK_EINVAL;
+  if (epi_flags(epi).bias && bias == nullptr) return PBDK_EINVAL;
+  if (epi_flags(epi).aux && aux == nullptr) return PBDK_EINVAL;
   const int bkc = chan_block(d.c);
   const FpropChoice ch = choose_fprop(d, g, bkc);
   const int bn = ch.bn;

@@ -1,0 +1,586 @@
+// CUDA-core kernels of the MobileNetV2 -> ProxylessNAS workload (sm_100a), DESIGN.md §10:
+//   depthwise k x k conv (k = 3/5/7, stride 1/2): forward (+bias+ReLU6 for the teacher),
+//     data gradient with the ReLU6 mask of the stored activation, weight gradient (two-level,
+//     fixed-order reduction);
+//   stem 3x3/s2 conv on the 16-channel padded image: forward and weight gradient;
+//   BN apply as a per-channel affine map with {none, ReLU6} and an optional residual add;
+//   MSE distillation loss + its gradient on z = BN(y) [+ residual] (no activation).
+// The 1x1 expand / project convolutions run on the tcgen05 implicit-GEMM engine (conv.cu).
+// Layout: NHWC bf16, every thread owns 8 consecutive channels (one 16-byte vector).
+// Depthwise weights are stored flipped and tap-major, wt[r'][s'][c] = w[c][K-1-r'][K-1-s']
+// (pbdk_weight_flip with c = 1), so one array serves the forward and the data gradient.
+// Accumulation order (fmaf over taps, r then s ascending) is the contract with the oracle
+// (oracle/mb_oracle.c), which makes these kernels bit-exact against it on identical inputs.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "mb_kernels.hpp"
+#include "pbdk.h"
+
+namespace pbdk {
+
+namespace {
+
+constexpr int kT = 256;
+
+__device__ __forceinline__ void ld8(const __nv_bfloat16* p, float (&f)[8]) {
+  const uint4 v = *reinterpret_cast<const uint4*>(p);
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+  }
+}
+
+__device__ __forceinline__ uint32_t pk2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__device__ __forceinline__ void st8(__nv_bfloat16* p, const float (&f)[8]) {
+  *reinterpret_cast<uint4*>(p) = make_uint4(pk2(f[0], f[1]), pk2(f[2], f[3]), pk2(f[4], f[5]), pk2(f[6], f[7]));
+}
+
+__device__ __forceinline__ float relu6f(float z) { return fminf(fmaxf(z, 0.0f), 6.0f); }
+
+int grid_for(long long work) {
+  const long long b = (work + kT - 1) / kT;
+  return static_cast<int>(std::max<long long>(1, std::min<long long>(b, 148LL * 16)));
+}
+
+inline int ok(cudaError_t e) { return e == cudaSuccess ? PBDK_OK : PBDK_ECUDA; }
+
+// ------------------------------------------------------------------ depthwise forward
+template <int K, int ST>
+__global__ void __launch_bounds__(kT) dw_fwd_kernel(const __nv_bfloat16* __restrict__ x,
+                                                    const __nv_bfloat16* __restrict__ wt,
+                                                    const float* __restrict__ bias, __nv_bfloat16* __restrict__ y,
+                                                    int N, int H, int W, int C, int P, int Q, int relu6) {
+  constexpr int PAD = K / 2;
+  const int G = C / 8;
+  const long long total = static_cast<long long>(N) * P * Q * G;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int g = static_cast<int>(i % G);
+    const long long pix = i / G;
+    const int q = static_cast<int>(pix % Q);
+    const int p = static_cast<int>((pix / Q) % P);
+    const int n = static_cast<int>(pix / (static_cast<long long>(P) * Q));
+    const int c0 = g * 8;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      const int h = p * ST + r - PAD;
+      if (h < 0 || h >= H) continue;
+#pragma unroll
+      for (int s = 0; s < K; ++s) {
+        const int w = q * ST + s - PAD;
+        if (w < 0 || w >= W) continue;
+        float xv[8], wv[8];
+        ld8(x + ((static_cast<size_t>(n) * H + h) * W + w) * C + c0, xv);
+        ld8(wt + (static_cast<size_t>(K - 1 - r) * K + (K - 1 - s)) * C + c0, wv);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = fmaf(xv[j], wv[j], acc[j]);
+      }
+    }
+    if (bias != nullptr) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = acc[j] + bias[c0 + j];
+    }
+    if (relu6) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = relu6f(acc[j]);
+    }
+    st8(y + pix * C + c0, acc);
+  }
+}
+
+// ------------------------------------------------------------------ depthwise data gradient
+// dx[n,h,w,c] = fmaf chain over (r, s) ascending of dy[n,(h+PAD-r)/ST,(w+PAD-s)/ST,c] w[c][r][s],
+// then the ReLU6 mask of the stored activation `act` (0 < a < 6) when given.
+template <int K, int ST>
+__global__ void __launch_bounds__(kT) dw_dgrad_kernel(const __nv_bfloat16* __restrict__ dy,
+                                                      const __nv_bfloat16* __restrict__ wt,
+                                                      const __nv_bfloat16* __restrict__ act,
+                                                      __nv_bfloat16* __restrict__ dx, int N, int H, int W, int C, int P,
+                                                      int Q) {
+  constexpr int PAD = K / 2;
+  const int G = C / 8;
+  const long long total = static_cast<long long>(N) * H * W * G;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int g = static_cast<int>(i % G);
+    const long long pix = i / G;
+    const int w = static_cast<int>(pix % W);
+    const int h = static_cast<int>((pix / W) % H);
+    const int n = static_cast<int>(pix / (static_cast<long long>(H) * W));
+    const int c0 = g * 8;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      const int pn = h + PAD - r;
+      if (pn < 0 || pn % ST != 0 || pn / ST >= P) continue;
+#pragma unroll
+      for (int s = 0; s < K; ++s) {
+        const int qn = w + PAD - s;
+        if (qn < 0 || qn % ST != 0 || qn / ST >= Q) continue;
+        float gv[8], wv[8];
+        ld8(dy + ((static_cast<size_t>(n) * P + pn / ST) * Q + qn / ST) * C + c0, gv);
+        ld8(wt + (static_cast<size_t>(K - 1 - r) * K + (K - 1 - s)) * C + c0, wv);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = fmaf(gv[j], wv[j], acc[j]);
+      }
+    }
+    if (act != nullptr) {
+      float av[8];
+      ld8(act + pix * C + c0, av);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = (av[j] > 0.0f && av[j] < 6.0f) ? acc[j] : 0.0f;
+    }
+    st8(dx + pix * C + c0, acc);
+  }
+}
+
+// ------------------------------------------------------------------ depthwise weight gradient
+// Pass 1, grid (chunks, channel windows, K): CTA = lanes_c channel groups x lanes_p pixel lanes,
+// filter row r = blockIdx.z; every thread accumulates K x 8 fp32 sums over its pixels, then the
+// CTA adds the pixel lanes in lane order -> partial[chunk][c][r][s].
+template <int K, int ST>
+__global__ void __launch_bounds__(kT) dw_wgrad_partial_kernel(const __nv_bfloat16* __restrict__ a,
+                                                              const __nv_bfloat16* __restrict__ dy,
+                                                              float* __restrict__ partial, int N, int H, int W, int C,
+                                                              int P, int Q, int lanes_c, long long pix_per_chunk) {
+  constexpr int PAD = K / 2;
+  __shared__ float red[kT * 8];
+  const int G = C / 8;
+  const int cl = threadIdx.x % lanes_c;
+  const int pl = threadIdx.x / lanes_c;
+  const int lanes_p = kT / lanes_c;
+  const int g = blockIdx.y * lanes_c + cl;
+  const int r = blockIdx.z;
+  const long long M = static_cast<long long>(N) * P * Q;
+  const long long p0 = blockIdx.x * pix_per_chunk;
+  const long long p1 = min(M, p0 + pix_per_chunk);
+  float acc[K][8];
+#pragma unroll
+  for (int s = 0; s < K; ++s)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[s][j] = 0.0f;
+  if (g < G && pl < lanes_p) {
+    const int c0 = g * 8;
+    for (long long pix = p0 + pl; pix < p1; pix += lanes_p) {
+      const int q = static_cast<int>(pix % Q);
+      const int p = static_cast<int>((pix / Q) % P);
+      const int n = static_cast<int>(pix / (static_cast<long long>(P) * Q));
+      const int h = p * ST + r - PAD;
+      if (h < 0 || h >= H) continue;
+      float gv[8];
+      ld8(dy + pix * C + c0, gv);
+#pragma unroll
+      for (int s = 0; s < K; ++s) {
+        const int w = q * ST + s - PAD;
+        if (w < 0 || w >= W) continue;
+        float av[8];
+        ld8(a + ((static_cast<size_t>(n) * H + h) * W + w) * C + c0, av);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[s][j] = fmaf(gv[j], av[j], acc[s][j]);
+      }
+    }
+  }
+  const size_t cKK = static_cast<size_t>(C) * K * K;
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) red[(pl * lanes_c + cl) * 8 + j] = acc[s][j];
+    __syncthreads();
+    for (int o = threadIdx.x; o < lanes_c * 8; o += kT) {
+      const int l = o / 8, j = o % 8;
+      const int gg = blockIdx.y * lanes_c + l;
+      if (gg < G) {
+        float t = 0.0f;
+        for (int pp = 0; pp < lanes_p; ++pp) t += red[(pp * lanes_c + l) * 8 + j];
+        partial[blockIdx.x * cKK + (static_cast<size_t>(gg * 8 + j) * K + r) * K + s] = t;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Pass 2: dw[o] = sum over chunks (chunk order, fp64) of partial[chunk][o].
+__global__ void chunk_sum_kernel(const float* __restrict__ partial, int chunks, size_t n, float* __restrict__ out) {
+  for (size_t o = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; o < n;
+       o += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < chunks; ++c) s += partial[c * n + o];
+    out[o] = static_cast<float>(s);
+  }
+}
+
+// ------------------------------------------------------------------ stem 3x3 / stride 2 (3 -> 32)
+// x: [N][S][S][16] bf16 (channels 3..15 zero), w: [32][3][3][16] bf16 (the product layout);
+// y[n,p,q,k] = fmaf chain over (r, s, c < 3).  Thread = (output pixel, 8 output channels).
+__global__ void __launch_bounds__(kT) stem_fwd_kernel(const __nv_bfloat16* __restrict__ x,
+                                                      const __nv_bfloat16* __restrict__ w,
+                                                      const float* __restrict__ bias, __nv_bfloat16* __restrict__ y,
+                                                      int N, int S, int relu6) {
+  __shared__ float ws[27][32];  // [r*9 + s*3 + c][k]
+  for (int i = threadIdx.x; i < 27 * 32; i += blockDim.x) {
+    const int k = i % 32, t = i / 32;
+    ws[t][k] = __bfloat162float(w[(k * 9 + t / 3) * 16 + t % 3]);
+  }
+  __syncthreads();
+  const int P = S / 2;
+  const long long total = static_cast<long long>(N) * P * P * 4;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int g = static_cast<int>(i % 4);
+    const long long pix = i / 4;
+    const int q = static_cast<int>(pix % P);
+    const int p = static_cast<int>((pix / P) % P);
+    const int n = static_cast<int>(pix / (static_cast<long long>(P) * P));
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int h = 2 * p + r - 1;
+      if (h < 0 || h >= S) continue;
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        const int ww = 2 * q + s - 1;
+        if (ww < 0 || ww >= S) continue;
+        const uint2 v = *reinterpret_cast<const uint2*>(x + ((static_cast<size_t>(n) * S + h) * S + ww) * 16);
+        const float xc[3] = {__uint_as_float(v.x << 16), __uint_as_float(v.x & 0xFFFF0000u),
+                             __uint_as_float(v.y << 16)};
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[j] = fmaf(xc[c], ws[r * 9 + s * 3 + c][g * 8 + j], acc[j]);
+      }
+    }
+    if (bias != nullptr) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = acc[j] + bias[g * 8 + j];
+    }
+    if (relu6) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = relu6f(acc[j]);
+    }
+    st8(y + pix * 32 + g * 8, acc);
+  }
+}
+
+// dw[k][r][s][c] (c < 3; pad channels stay 0) = sum_pix dy[pix][k] x[...][c].  Pass 1: warp lane =
+// output channel k, 8 warps split the chunk's pixels, 27 fp32 sums per lane; warps added in order.
+__global__ void __launch_bounds__(kT) stem_wgrad_partial_kernel(const __nv_bfloat16* __restrict__ x,
+                                                                const __nv_bfloat16* __restrict__ dy,
+                                                                float* __restrict__ partial, int N, int S,
+                                                                long long pix_per_chunk) {
+  __shared__ float red[8][27][32];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int P = S / 2;
+  const long long M = static_cast<long long>(N) * P * P;
+  const long long p0 = blockIdx.x * pix_per_chunk;
+  const long long p1 = min(M, p0 + pix_per_chunk);
+  float acc[27];
+#pragma unroll
+  for (int t = 0; t < 27; ++t) acc[t] = 0.0f;
+  for (long long pix = p0 + wp; pix < p1; pix += 8) {
+    const int q = static_cast<int>(pix % P);
+    const int p = static_cast<int>((pix / P) % P);
+    const int n = static_cast<int>(pix / (static_cast<long long>(P) * P));
+    const float g = __bfloat162float(dy[pix * 32 + lane]);
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int h = 2 * p + r - 1;
+      if (h < 0 || h >= S) continue;
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        const int ww = 2 * q + s - 1;
+        if (ww < 0 || ww >= S) continue;
+        const uint2 v = *reinterpret_cast<const uint2*>(x + ((static_cast<size_t>(n) * S + h) * S + ww) * 16);
+        acc[r * 9 + s * 3 + 0] = fmaf(g, __uint_as_float(v.x << 16), acc[r * 9 + s * 3 + 0]);
+        acc[r * 9 + s * 3 + 1] = fmaf(g, __uint_as_float(v.x & 0xFFFF0000u), acc[r * 9 + s * 3 + 1]);
+        acc[r * 9 + s * 3 + 2] = fmaf(g, __uint_as_float(v.y << 16), acc[r * 9 + s * 3 + 2]);
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 27; ++t) red[wp][t][lane] = acc[t];
+  __syncthreads();
+  for (int o = threadIdx.x; o < 27 * 32; o += kT) {
+    const int t = o / 32, k = o % 32;
+    float s = 0.0f;
+    for (int i = 0; i < 8; ++i) s += red[i][t][k];
+    // partial layout = the weight layout [32][3][3][16] (pad channels written as 0 by pass 2)
+    partial[blockIdx.x * (32 * 9 * 16) + (k * 9 + t / 3) * 16 + t % 3] = s;
+  }
+  for (int o = threadIdx.x; o < 32 * 9 * 13; o += kT) {
+    const int k = o / (9 * 13), rem = o % (9 * 13);
+    partial[blockIdx.x * (32 * 9 * 16) + (k * 9 + rem / 13) * 16 + 3 + rem % 13] = 0.0f;
+  }
+}
+
+// ------------------------------------------------------------------ BN apply (affine) + act [+ residual]
+template <int ACT, bool RES>
+__global__ void __launch_bounds__(kT) bn_apply_act_kernel(const __nv_bfloat16* __restrict__ y,
+                                                          const float* __restrict__ mean_rstd,
+                                                          const float* __restrict__ gamma,
+                                                          const float* __restrict__ beta,
+                                                          const __nv_bfloat16* __restrict__ res,
+                                                          __nv_bfloat16* __restrict__ out, long long m, int C) {
+  const int G = C / 8;
+  const long long total = m * G;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int c0 = static_cast<int>(i % G) * 8;
+    const size_t off = static_cast<size_t>(i / G) * C + c0;
+    float f[8], rv[8];
+    ld8(y + off, f);
+    if (RES) ld8(res + off, rv);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = c0 + j;
+      const float A = gamma[c] * mean_rstd[C + c];
+      const float B = fmaf(-A, mean_rstd[c], beta[c]);
+      float z = fmaf(A, f[j], B);
+      if (ACT == 6) z = relu6f(z);
+      if (RES) z = z + rv[j];
+      f[j] = z;
+    }
+    st8(out + off, f);
+  }
+}
+
+// ------------------------------------------------------------------ MSE loss on z = BN(y) [+ res]
+// g = bf16((z - t) * gscale); per-CTA loss partial (fp64 per thread, fixed-order CTA tree),
+// then one CTA sums the partials in chunk order.
+__global__ void __launch_bounds__(kT) mse_affine_partial_kernel(const __nv_bfloat16* __restrict__ y,
+                                                                const float* __restrict__ mean_rstd,
+                                                                const float* __restrict__ gamma,
+                                                                const float* __restrict__ beta,
+                                                                const __nv_bfloat16* __restrict__ res,
+                                                                const __nv_bfloat16* __restrict__ t, long long m,
+                                                                int C, float gscale, __nv_bfloat16* __restrict__ g,
+                                                                double* __restrict__ loss_partial) {
+  __shared__ double sm[kT / 32];
+  const int G = C / 8;
+  const long long total = m * G;
+  double ls = 0.0;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int c0 = static_cast<int>(i % G) * 8;
+    const size_t off = static_cast<size_t>(i / G) * C + c0;
+    float f[8], tv[8], rv[8];
+    ld8(y + off, f);
+    ld8(t + off, tv);
+    if (res != nullptr) ld8(res + off, rv);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = c0 + j;
+      const float A = gamma[c] * mean_rstd[C + c];
+      const float B = fmaf(-A, mean_rstd[c], beta[c]);
+      float z = fmaf(A, f[j], B);
+      if (res != nullptr) z = z + rv[j];
+      const float d = z - tv[j];
+      ls += static_cast<double>(d) * d;
+      f[j] = d * gscale;
+    }
+    st8(g + off, f);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = ls;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kT / 32; ++w) s += sm[w];
+    loss_partial[blockIdx.x] = s;
+  }
+}
+
+__global__ void loss_sum_kernel(const double* __restrict__ part, int n, double norm, double* __restrict__ loss) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += part[i];
+    *loss = s / norm;
+  }
+}
+
+template <int K>
+cudaError_t launch_dw_fwd(int st, const DwArgs& d, const void* x, const void* wt, const float* bias, void* y,
+                          int relu6, cudaStream_t s) {
+  const int g = grid_for(static_cast<long long>(d.n) * d.p * d.q * (d.c / 8));
+  if (st == 1)
+    dw_fwd_kernel<K, 1><<<g, kT, 0, s>>>(static_cast<const __nv_bfloat16*>(x),
+                                         static_cast<const __nv_bfloat16*>(wt), bias,
+                                         static_cast<__nv_bfloat16*>(y), d.n, d.h, d.w, d.c, d.p, d.q, relu6);
+  else
+    dw_fwd_kernel<K, 2><<<g, kT, 0, s>>>(static_cast<const __nv_bfloat16*>(x),
+                                         static_cast<const __nv_bfloat16*>(wt), bias,
+                                         static_cast<__nv_bfloat16*>(y), d.n, d.h, d.w, d.c, d.p, d.q, relu6);
+  return cudaGetLastError();
+}
+
+template <int K>
+cudaError_t launch_dw_dgrad(int st, const DwArgs& d, const void* dy, const void* wt, const void* act, void* dx,
+                            cudaStream_t s) {
+  const int g = grid_for(static_cast<long long>(d.n) * d.h * d.w * (d.c / 8));
+  auto* a = static_cast<const __nv_bfloat16*>(act);
+  if (st == 1)
+    dw_dgrad_kernel<K, 1><<<g, kT, 0, s>>>(static_cast<const __nv_bfloat16*>(dy),
+                                           static_cast<const __nv_bfloat16*>(wt), a,
+                                           static_cast<__nv_bfloat16*>(dx), d.n, d.h, d.w, d.c, d.p, d.q);
+  else
+    dw_dgrad_kernel<K, 2><<<g, kT, 0, s>>>(static_cast<const __nv_bfloat16*>(dy),
+                                           static_cast<const __nv_bfloat16*>(wt), a,
+                                           static_cast<__nv_bfloat16*>(dx), d.n, d.h, d.w, d.c, d.p, d.q);
+  return cudaGetLastError();
+}
+
+struct WgradTiling {
+  int lanes_c, cwin, chunks;
+  long long per_chunk;
+};
+
+WgradTiling dw_wgrad_tiling(const DwArgs& d) {
+  WgradTiling t;
+  const int G = d.c / 8;
+  t.lanes_c = std::min(G, 32);
+  t.cwin = (G + t.lanes_c - 1) / t.lanes_c;
+  const long long M = static_cast<long long>(d.n) * d.p * d.q;
+  const int target = 148 * 4;
+  t.chunks = static_cast<int>(std::max<long long>(1, std::min<long long>(M / 64 + 1, target / (t.cwin * d.k) + 1)));
+  t.per_chunk = (M + t.chunks - 1) / t.chunks;
+  t.chunks = static_cast<int>((M + t.per_chunk - 1) / t.per_chunk);
+  return t;
+}
+
+template <int K>
+cudaError_t launch_dw_wgrad(int st, const DwArgs& d, const void* a, const void* dy, float* partial, float* dw,
+                            cudaStream_t s) {
+  const WgradTiling t = dw_wgrad_tiling(d);
+  const dim3 grid(t.chunks, t.cwin, K);
+  if (st == 1)
+    dw_wgrad_partial_kernel<K, 1><<<grid, kT, 0, s>>>(static_cast<const __nv_bfloat16*>(a),
+                                                      static_cast<const __nv_bfloat16*>(dy), partial, d.n, d.h, d.w,
+                                                      d.c, d.p, d.q, t.lanes_c, t.per_chunk);
+  else
+    dw_wgrad_partial_kernel<K, 2><<<grid, kT, 0, s>>>(static_cast<const __nv_bfloat16*>(a),
+                                                      static_cast<const __nv_bfloat16*>(dy), partial, d.n, d.h, d.w,
+                                                      d.c, d.p, d.q, t.lanes_c, t.per_chunk);
+  const size_t n = static_cast<size_t>(d.c) * K * K;
+  chunk_sum_kernel<<<grid_for(static_cast<long long>(n)), kT, 0, s>>>(partial, t.chunks, n, dw);
+  return cudaGetLastError();
+}
+
+bool dw_ok(const DwArgs& d) {
+  if (d.n < 1 || d.h < 1 || d.w < 1 || d.c % 8 != 0 || d.c < 8) return false;
+  if (d.k != 3 && d.k != 5 && d.k != 7) return false;
+  if (d.stride != 1 && d.stride != 2) return false;
+  const int pad = d.k / 2;
+  return d.p == (d.h + 2 * pad - d.k) / d.stride + 1 && d.q == (d.w + 2 * pad - d.k) / d.stride + 1;
+}
+
+long long stem_chunk_pixels(int n, int S) {
+  const long long M = static_cast<long long>(n) * (S / 2) * (S / 2);
+  const long long chunks = std::max<long long>(1, std::min<long long>(148 * 2, M / 256 + 1));
+  return (M + chunks - 1) / chunks;
+}
+
+}  // namespace
+
+size_t dw_wgrad_workspace_floats(const DwArgs& d) {
+  if (!dw_ok(d)) return 0;
+  return static_cast<size_t>(dw_wgrad_tiling(d).chunks) * d.c * d.k * d.k;
+}
+
+int dw_fwd(const DwArgs& d, const void* x, const void* wt, const float* bias, void* y, int relu6, cudaStream_t s) {
+  if (!dw_ok(d)) return PBDK_EINVAL;
+  switch (d.k) {
+    case 3: return ok(launch_dw_fwd<3>(d.stride, d, x, wt, bias, y, relu6, s));
+    case 5: return ok(launch_dw_fwd<5>(d.stride, d, x, wt, bias, y, relu6, s));
+    default: return ok(launch_dw_fwd<7>(d.stride, d, x, wt, bias, y, relu6, s));
+  }
+}
+
+int dw_dgrad(const DwArgs& d, const void* dy, const void* wt, const void* act, void* dx, cudaStream_t s) {
+  if (!dw_ok(d)) return PBDK_EINVAL;
+  switch (d.k) {
+    case 3: return ok(launch_dw_dgrad<3>(d.stride, d, dy, wt, act, dx, s));
+    case 5: return ok(launch_dw_dgrad<5>(d.stride, d, dy, wt, act, dx, s));
+    default: return ok(launch_dw_dgrad<7>(d.stride, d, dy, wt, act, dx, s));
+  }
+}
+
+int dw_wgrad(const DwArgs& d, const void* a, const void* dy, float* ws, size_t ws_floats, float* dw, cudaStream_t s) {
+  if (!dw_ok(d) || ws == nullptr || ws_floats < dw_wgrad_workspace_floats(d)) return PBDK_EINVAL;
+  switch (d.k) {
+    case 3: return ok(launch_dw_wgrad<3>(d.stride, d, a, dy, ws, dw, s));
+    case 5: return ok(launch_dw_wgrad<5>(d.stride, d, a, dy, ws, dw, s));
+    default: return ok(launch_dw_wgrad<7>(d.stride, d, a, dy, ws, dw, s));
+  }
+}
+
+int stem_fwd(const void* x, const void* w, const float* bias, void* y, int n, int S, int relu6, cudaStream_t s) {
+  if (n < 1 || S < 2 || S % 2 != 0) return PBDK_EINVAL;
+  stem_fwd_kernel<<<grid_for(static_cast<long long>(n) * (S / 2) * (S / 2) * 4), kT, 0, s>>>(
+      static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(w), bias,
+      static_cast<__nv_bfloat16*>(y), n, S, relu6);
+  return ok(cudaGetLastError());
+}
+
+size_t stem_wgrad_workspace_floats(int n, int S) {
+  const long long M = static_cast<long long>(n) * (S / 2) * (S / 2);
+  const long long per = stem_chunk_pixels(n, S);
+  return static_cast<size_t>((M + per - 1) / per) * 32 * 9 * 16;
+}
+
+int stem_wgrad(const void* x, const void* dy, int n, int S, float* ws, size_t ws_floats, float* dw, cudaStream_t s) {
+  if (n < 1 || S < 2 || S % 2 != 0 || ws == nullptr || ws_floats < stem_wgrad_workspace_floats(n, S))
+    return PBDK_EINVAL;
+  const long long M = static_cast<long long>(n) * (S / 2) * (S / 2);
+  const long long per = stem_chunk_pixels(n, S);
+  const int chunks = static_cast<int>((M + per - 1) / per);
+  stem_wgrad_partial_kernel<<<chunks, kT, 0, s>>>(static_cast<const __nv_bfloat16*>(x),
+                                                  static_cast<const __nv_bfloat16*>(dy), ws, n, S, per);
+  chunk_sum_kernel<<<grid_for(32 * 9 * 16), kT, 0, s>>>(ws, chunks, 32 * 9 * 16, dw);
+  return ok(cudaGetLastError());
+}
+
+int bn_apply_act(const void* y, const float* mean_rstd, const float* gamma, const float* beta, const void* res,
+                 void* out, long long m, int c, int relu6, cudaStream_t s) {
+  if (c % 8 != 0 || m < 1) return PBDK_EINVAL;
+  const int g = grid_for(m * (c / 8));
+  auto* yy = static_cast<const __nv_bfloat16*>(y);
+  auto* rr = static_cast<const __nv_bfloat16*>(res);
+  auto* oo = static_cast<__nv_bfloat16*>(out);
+  if (relu6 && res == nullptr)
+    bn_apply_act_kernel<6, false><<<g, kT, 0, s>>>(yy, mean_rstd, gamma, beta, rr, oo, m, c);
+  else if (!relu6 && res == nullptr)
+    bn_apply_act_kernel<0, false><<<g, kT, 0, s>>>(yy, mean_rstd, gamma, beta, rr, oo, m, c);
+  else if (!relu6)
+    bn_apply_act_kernel<0, true><<<g, kT, 0, s>>>(yy, mean_rstd, gamma, beta, rr, oo, m, c);
+  else
+    return PBDK_EINVAL;
+  return ok(cudaGetLastError());
+}
+
+size_t mse_affine_workspace_doubles(long long m, int c) { return static_cast<size_t>(grid_for(m * (c / 8))); }
+
+int mse_affine(const void* y, const float* mean_rstd, const float* gamma, const float* beta, const void* res,
+               const void* t, long long m, int c, float gscale, double norm, void* g, double* ws, double* loss,
+               cudaStream_t s) {
+  if (c % 8 != 0 || m < 1) return PBDK_EINVAL;
+  const int grid = grid_for(m * (c / 8));
+  mse_affine_partial_kernel<<<grid, kT, 0, s>>>(static_cast<const __nv_bfloat16*>(y), mean_rstd, gamma, beta,
+                                                static_cast<const __nv_bfloat16*>(res),
+                                                static_cast<const __nv_bfloat16*>(t), m, c, gscale,
+                                                static_cast<__nv_bfloat16*>(g), ws);
+  loss_sum_kernel<<<1, 32, 0, s>>>(ws, grid, norm, loss);
+  return ok(cudaGetLastError());
+}
+
+}  // namespace pbdk

@@ -26,10 +26,15 @@ T_HW = (32, 32, 16, 8, 4)
 STUDENT_TENSORS = ("w1", "w2", "wsc", "g1", "b1", "g2", "b2", "gsc", "bsc")
 
 
+MODEL_RESNET_CIFAR, MODEL_MBV2_PROXYLESS = 0, 1
+MODELS = {"resnet": MODEL_RESNET_CIFAR, "mbv2": MODEL_MBV2_PROXYLESS}
+
+
 class PbdxDesc(ctypes.Structure):
     _fields_ = [("block_lo", ctypes.c_int), ("block_hi", ctypes.c_int), ("n_max", ctypes.c_int),
                 ("global_batch", ctypes.c_int), ("seed_data", ctypes.c_uint32), ("seed_teacher", ctypes.c_uint32),
-                ("seed_student", ctypes.c_uint32), ("lr", ctypes.c_float), ("momentum", ctypes.c_float)]
+                ("seed_student", ctypes.c_uint32), ("lr", ctypes.c_float), ("momentum", ctypes.c_float),
+                ("model", ctypes.c_int), ("image", ctypes.c_int)]
 
 
 class RelayMsg(ctypes.Structure):
@@ -67,6 +72,13 @@ def _bind(L):
     L.pbdx_ipc_export.argtypes = [V, ctypes.c_char_p]
     L.pbdx_ipc_open.argtypes = [ctypes.c_char_p, P(V)]
     L.pbdx_ipc_close.argtypes = [V]
+    L.pbdx_set_path.argtypes = [V, I, P(I), I]
+    L.pbdx_mb_layers.argtypes = [I]
+    L.pbdx_mb_candidates.argtypes = [I, I]
+    L.pbdx_mb_candidate_offset.argtypes = [I, I, I, P(ctypes.c_long)]
+    L.pbdx_mb_candidate_offset.restype = ctypes.c_long
+    L.pbdx_mb_block_params.argtypes = [I]
+    L.pbdx_mb_block_params.restype = ctypes.c_long
     L._pbdx_bound = True
     return L
 
@@ -108,15 +120,48 @@ def stored_channels(c: int) -> int:
     return 16 if c == 3 else c
 
 
+# ---------------------------------------------------------------- MobileNetV2 -> ProxylessNAS geometry
+MB_CH = (3, 32, 32, 64, 128, 192, 320)
+MB_DIV = (1, 4, 8, 16, 16, 32, 32)
+MB_BLOCKS = 6
+
+
+def mb_layers(block: int) -> int:
+    return int(lib().pbdx_mb_layers(block))
+
+
+def mb_candidates(block: int, layer: int) -> int:
+    return int(lib().pbdx_mb_candidates(block, layer))
+
+
+def mb_candidate_span(block: int, layer: int, cand: int) -> Tuple[int, int]:
+    """(offset inside the block's flat supernet parameters, count) of one candidate."""
+    n = ctypes.c_long()
+    off = lib().pbdx_mb_candidate_offset(block, layer, cand, ctypes.byref(n))
+    if off < 0:
+        raise ValueError("bad (block, layer, candidate)")
+    return int(off), int(n.value)
+
+
+def mb_block_params(block: int) -> int:
+    return int(lib().pbdx_mb_block_params(block))
+
+
 class Partition:
+    """One device's share of a Pipe-BD schedule.  model: "resnet" (CIFAR ResNet-18 -> slim residual
+    student, 4 blocks, 32x32) or "mbv2" (MobileNetV2 -> ProxylessNAS supernet, 6 blocks, image x image)."""
+
     def __init__(self, block_lo: int, block_hi: int, n_max: int, global_batch: int, seed_data: int = 1234,
                  seed_teacher: int = 1, seed_student: int = 2, lr: float = 0.1, momentum: float = 0.9,
-                 device: Optional[torch.device] = None):
+                 device: Optional[torch.device] = None, model: str = "resnet", image: Optional[int] = None):
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.block_lo, self.block_hi, self.n_max, self.global_batch = block_lo, block_hi, n_max, global_batch
+        self.model = model
+        self.image = image if image is not None else (32 if model == "resnet" else 224)
         self.n = n_max
         self.first = 0
-        d = PbdxDesc(block_lo, block_hi, n_max, global_batch, seed_data, seed_teacher, seed_student, lr, momentum)
+        d = PbdxDesc(block_lo, block_hi, n_max, global_batch, seed_data, seed_teacher, seed_student, lr, momentum,
+                     MODELS[model], self.image)
         h = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             _check(lib().pbdx_create(ctypes.byref(d), ctypes.byref(h)), "pbdx_create")
@@ -125,7 +170,10 @@ class Partition:
         self.layouts = {}
         off = 0
         for k in self.blocks:
-            lay, total = student_layout(k)
+            if model == "resnet":
+                lay, total = student_layout(k)
+            else:
+                lay, total = {}, mb_block_params(k)
             self.layouts[k] = (off, lay, total)
             off += total
 
@@ -160,19 +208,24 @@ class Partition:
 
     # -- views the driver moves with NCCL
     def input_act(self) -> torch.Tensor:
-        k = self.block_lo
-        return self.tensor(BUF_INPUT, (self.n_max, T_HW[k], T_HW[k], stored_channels(T_CH[k])), torch.bfloat16)
+        return self.tensor(BUF_INPUT, (self.n_max,) + self.act_hwc(self.block_lo), torch.bfloat16)
 
     def teacher_out(self) -> torch.Tensor:
-        k = self.block_hi + 1
-        return self.tensor(BUF_TEACHER_OUT, (self.n_max, T_HW[k], T_HW[k], T_CH[k]), torch.bfloat16)
+        return self.tensor(BUF_TEACHER_OUT, (self.n_max,) + self.act_hwc(self.block_hi + 1), torch.bfloat16)
 
     def teacher_act(self, k: int) -> torch.Tensor:
         """Teacher output t_k of a block inside the partition (bf16 NHWC, n_max rows)."""
         p, n = ctypes.c_void_p(), ctypes.c_size_t()
         _check(lib().pbdx_teacher_act(self.handle, k, ctypes.byref(p), ctypes.byref(n)), "pbdx_teacher_act")
-        shape = (self.n_max, T_HW[k + 1], T_HW[k + 1], T_CH[k + 1])
+        shape = (self.n_max,) + self.act_hwc(k + 1)
         return torch.as_tensor(_CudaArray(p.value, shape, "<i2"), device=self.device).view(torch.bfloat16)
+
+    def set_path(self, block: int, path):
+        """Active candidate per student layer of `block` (mbv2 supernet)."""
+        arr = (ctypes.c_int * len(path))(*[int(c) for c in path])
+        _check(lib().pbdx_set_path(self.handle, block, arr, len(path)), "set_path")
+        self.paths = getattr(self, "paths", {})
+        self.paths[block] = [int(c) for c in path]
 
     def grads(self) -> torch.Tensor:
         return self.tensor(BUF_GRADS)
@@ -194,14 +247,21 @@ class Partition:
         flat = {"params": self.params, "grads": self.grads, "momentum": self.momentum}[which]()
         return {name: flat[base + o: base + o + n] for name, (o, n) in lay.items()}
 
+    # -- geometry of block boundaries (boundary 0 = the stored 16-channel image)
+    def act_hwc(self, boundary: int) -> Tuple[int, int, int]:
+        if self.model == "resnet":
+            return T_HW[boundary], T_HW[boundary], stored_channels(T_CH[boundary])
+        hw = self.image // MB_DIV[boundary]
+        return hw, hw, 16 if boundary == 0 else MB_CH[boundary]
+
     # -- K11 peer relay (include/pbdx.h): device pointers of this rank's relay endpoints
     def row_bytes_in(self) -> int:
-        k = self.block_lo
-        return T_HW[k] * T_HW[k] * stored_channels(T_CH[k]) * 2
+        h, w, c = self.act_hwc(self.block_lo)
+        return h * w * c * 2
 
     def row_bytes_out(self) -> int:
-        k = self.block_hi + 1
-        return T_HW[k] * T_HW[k] * T_CH[k] * 2
+        h, w, c = self.act_hwc(self.block_hi + 1)
+        return h * w * c * 2
 
     def mailbox_ptr(self) -> int:
         return self.buffer_ptr(BUF_MAILBOX)[0]
@@ -230,6 +290,7 @@ class Partition:
         _check(lib().pbdx_set_input_mode(self.handle, int(external)), "set_input_mode")
 
     def upload_images(self, host: torch.Tensor, stream=None):
+        """host: fp32 NHWC [n, S, S, 3] (pinned for an async copy)."""
         assert host.dtype == torch.float32 and not host.is_cuda and host.is_contiguous()
         _check(lib().pbdx_upload_images(self.handle, ctypes.c_void_p(host.data_ptr()), host.shape[0],
                                         self._stream(stream)), "upload_images")
@@ -285,7 +346,7 @@ class Partition:
 
     def block_state_like(self, k: int) -> List[torch.Tensor]:
         """Receive buffers for any block's state (owned by this partition or not)."""
-        _, total = student_layout(k)
+        total = student_layout(k)[1] if self.model == "resnet" else mb_block_params(k)
         return [torch.empty(total, dtype=torch.float32, device=self.device) for _ in range(2)]
 
     def set_block_state(self, k: int, weights: torch.Tensor, momentum: torch.Tensor):

@@ -94,3 +94,16 @@ def test_device_entry_points_validate_without_gpu():
     assert L.pbdk_conv_fprop(ctypes.byref(bad), None, None, None, None, None, 0, None) == 1
     assert L.pbdk_conv_wgrad_workspace_bytes(ctypes.byref(bad)) == 0
     assert L.pbdk_weight_flip(None, None, 1, 1, 1, 1, None) == 1
+
+
+def test_mb_supernet_layout_matches_oracle():
+    """Host-only layout queries of the MBConv executor (pbdx_mb_*) == the oracle's layout."""
+    from oracle import mb
+    from paper_2301_12443_b200 import executor as ex
+    for b in range(6):
+        assert ex.mb_layers(b) == mb.layers(b)
+        assert ex.mb_block_params(b) == mb.student_param_count(b)
+        for l in range(mb.layers(b)):
+            assert ex.mb_candidates(b, l) == mb.candidates(b, l)
+            for c in range(mb.candidates(b, l)):
+                assert ex.mb_candidate_span(b, l, c) == mb.candidate_span(b, l, c)
