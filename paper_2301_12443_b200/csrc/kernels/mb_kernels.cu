@@ -55,47 +55,71 @@ int grid_for(long long work) {
 inline int ok(cudaError_t e) { return e == cudaSuccess ? PBDK_OK : PBDK_ECUDA; }
 
 // ------------------------------------------------------------------ depthwise forward
+// Work item = (output row n,p ; strip of QT output columns ; 8-channel group).  For every filter
+// row r the thread walks the strip's input window once (each input vector loaded once per r) and
+// scatters it into the QT accumulators; per output the fmaf order is (r, s) ascending, exactly the
+// oracle's.  Consecutive threads take consecutive channel groups (coalesced 16-byte loads).
+constexpr int kQT = 4;
+
 template <int K, int ST>
 __global__ void __launch_bounds__(kT) dw_fwd_kernel(const __nv_bfloat16* __restrict__ x,
                                                     const __nv_bfloat16* __restrict__ wt,
                                                     const float* __restrict__ bias, __nv_bfloat16* __restrict__ y,
                                                     int N, int H, int W, int C, int P, int Q, int relu6) {
   constexpr int PAD = K / 2;
+  constexpr int WIN = (kQT - 1) * ST + K;
   const int G = C / 8;
-  const long long total = static_cast<long long>(N) * P * Q * G;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int g = static_cast<int>(i % G);
-    const long long pix = i / G;
-    const int q = static_cast<int>(pix % Q);
-    const int p = static_cast<int>((pix / Q) % P);
-    const int n = static_cast<int>(pix / (static_cast<long long>(P) * Q));
+  const int QS = (Q + kQT - 1) / kQT;
+  const int total = N * P * QS * G;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int g = i % G;
+    const int t = i / G;
+    const int q0 = (t % QS) * kQT;
+    const int row = t / QS;  // n * P + p
+    const int p = row % P;
+    const int n = row / P;
     const int c0 = g * 8;
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    float acc[kQT][8];
+#pragma unroll
+    for (int u = 0; u < kQT; ++u)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[u][j] = 0.0f;
 #pragma unroll
     for (int r = 0; r < K; ++r) {
       const int h = p * ST + r - PAD;
       if (h < 0 || h >= H) continue;
+      float wr[K][8];  // filter row r of this channel group (w[c][r][s] = wt[K-1-r][K-1-s][c])
 #pragma unroll
-      for (int s = 0; s < K; ++s) {
-        const int w = q * ST + s - PAD;
+      for (int sidx = 0; sidx < K; ++sidx)
+        ld8(wt + static_cast<size_t>((K - 1 - r) * K + (K - 1 - sidx)) * C + c0, wr[sidx]);
+      const __nv_bfloat16* xrow = x + (static_cast<size_t>(n) * H + h) * W * C + c0;
+#pragma unroll
+      for (int j = 0; j < WIN; ++j) {
+        const int w = q0 * ST - PAD + j;
         if (w < 0 || w >= W) continue;
-        float xv[8], wv[8];
-        ld8(x + ((static_cast<size_t>(n) * H + h) * W + w) * C + c0, xv);
-        ld8(wt + (static_cast<size_t>(K - 1 - r) * K + (K - 1 - s)) * C + c0, wv);
+        float xv[8];
+        ld8(xrow + static_cast<size_t>(w) * C, xv);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = fmaf(xv[j], wv[j], acc[j]);
+        for (int u = 0; u < kQT; ++u) {
+          const int sidx = j - u * ST;
+          if (sidx < 0 || sidx >= K) continue;
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) acc[u][jj] = fmaf(xv[jj], wr[sidx][jj], acc[u][jj]);
+        }
       }
     }
-    if (bias != nullptr) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[j] = acc[j] + bias[c0 + j];
-    }
-    if (relu6) {
+    for (int u = 0; u < kQT; ++u) {
+      if (q0 + u >= Q) break;
+      float o[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[j] = relu6f(acc[j]);
+      for (int jj = 0; jj < 8; ++jj) {
+        float v = acc[u][jj];
+        if (bias != nullptr) v = v + bias[c0 + jj];
+        o[jj] = relu6 ? relu6f(v) : v;
+      }
+      st8(y + ((static_cast<size_t>(row) * Q) + q0 + u) * C + c0, o);
     }
-    st8(y + pix * C + c0, acc);
   }
 }
 
@@ -110,38 +134,39 @@ __global__ void __launch_bounds__(kT) dw_dgrad_kernel(const __nv_bfloat16* __res
                                                       int Q) {
   constexpr int PAD = K / 2;
   const int G = C / 8;
-  const long long total = static_cast<long long>(N) * H * W * G;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int g = static_cast<int>(i % G);
-    const long long pix = i / G;
-    const int w = static_cast<int>(pix % W);
-    const int h = static_cast<int>((pix / W) % H);
-    const int n = static_cast<int>(pix / (static_cast<long long>(H) * W));
+  const int total = N * H * W * G;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int g = i % G;
+    const int pix = i / G;
+    const int w = pix % W;
+    const int h = (pix / W) % H;
+    const int n = pix / (H * W);
     const int c0 = g * 8;
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
     for (int r = 0; r < K; ++r) {
       const int pn = h + PAD - r;
       if (pn < 0 || pn % ST != 0 || pn / ST >= P) continue;
+      const __nv_bfloat16* grow = dy + (static_cast<size_t>(n) * P + pn / ST) * Q * C + c0;
+      const __nv_bfloat16* wrow = wt + static_cast<size_t>(K - 1 - r) * K * C + c0;
 #pragma unroll
       for (int s = 0; s < K; ++s) {
         const int qn = w + PAD - s;
         if (qn < 0 || qn % ST != 0 || qn / ST >= Q) continue;
         float gv[8], wv[8];
-        ld8(dy + ((static_cast<size_t>(n) * P + pn / ST) * Q + qn / ST) * C + c0, gv);
-        ld8(wt + (static_cast<size_t>(K - 1 - r) * K + (K - 1 - s)) * C + c0, wv);
+        ld8(grow + static_cast<size_t>(qn / ST) * C, gv);
+        ld8(wrow + static_cast<size_t>(K - 1 - s) * C, wv);
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[j] = fmaf(gv[j], wv[j], acc[j]);
       }
     }
     if (act != nullptr) {
       float av[8];
-      ld8(act + pix * C + c0, av);
+      ld8(act + static_cast<size_t>(pix) * C + c0, av);
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[j] = (av[j] > 0.0f && av[j] < 6.0f) ? acc[j] : 0.0f;
     }
-    st8(dx + pix * C + c0, acc);
+    st8(dx + static_cast<size_t>(pix) * C + c0, acc);
   }
 }
 
@@ -153,7 +178,7 @@ template <int K, int ST>
 __global__ void __launch_bounds__(kT) dw_wgrad_partial_kernel(const __nv_bfloat16* __restrict__ a,
                                                               const __nv_bfloat16* __restrict__ dy,
                                                               float* __restrict__ partial, int N, int H, int W, int C,
-                                                              int P, int Q, int lanes_c, long long pix_per_chunk) {
+                                                              int P, int Q, int lanes_c, int rows_per_chunk) {
   constexpr int PAD = K / 2;
   __shared__ float red[kT * 8];
   const int G = C / 8;
@@ -162,9 +187,9 @@ __global__ void __launch_bounds__(kT) dw_wgrad_partial_kernel(const __nv_bfloat1
   const int lanes_p = kT / lanes_c;
   const int g = blockIdx.y * lanes_c + cl;
   const int r = blockIdx.z;
-  const long long M = static_cast<long long>(N) * P * Q;
-  const long long p0 = blockIdx.x * pix_per_chunk;
-  const long long p1 = min(M, p0 + pix_per_chunk);
+  const int rows = N * P;
+  const int r0 = blockIdx.x * rows_per_chunk;
+  const int r1 = min(rows, r0 + rows_per_chunk);
   float acc[K][8];
 #pragma unroll
   for (int s = 0; s < K; ++s)
@@ -172,20 +197,25 @@ __global__ void __launch_bounds__(kT) dw_wgrad_partial_kernel(const __nv_bfloat1
     for (int j = 0; j < 8; ++j) acc[s][j] = 0.0f;
   if (g < G && pl < lanes_p) {
     const int c0 = g * 8;
-    for (long long pix = p0 + pl; pix < p1; pix += lanes_p) {
-      const int q = static_cast<int>(pix % Q);
-      const int p = static_cast<int>((pix / Q) % P);
-      const int n = static_cast<int>(pix / (static_cast<long long>(P) * Q));
+    // pixel lanes stride over the chunk's (row, q) pairs in row-major order (32-bit indices)
+    const int npix = (r1 - r0) * Q;
+#pragma unroll 2
+    for (int idx = pl; idx < npix; idx += lanes_p) {
+      const int row = r0 + idx / Q;
+      const int q = idx - (row - r0) * Q;
+      const int p = row % P;
+      const int n = row / P;
       const int h = p * ST + r - PAD;
       if (h < 0 || h >= H) continue;
+      const __nv_bfloat16* arow = a + (static_cast<size_t>(n) * H + h) * W * C + c0;
       float gv[8];
-      ld8(dy + pix * C + c0, gv);
+      ld8(dy + (static_cast<size_t>(row) * Q + q) * C + c0, gv);
 #pragma unroll
       for (int s = 0; s < K; ++s) {
         const int w = q * ST + s - PAD;
         if (w < 0 || w >= W) continue;
         float av[8];
-        ld8(a + ((static_cast<size_t>(n) * H + h) * W + w) * C + c0, av);
+        ld8(arow + static_cast<size_t>(w) * C, av);
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[s][j] = fmaf(gv[j], av[j], acc[s][j]);
       }
@@ -234,14 +264,13 @@ __global__ void __launch_bounds__(kT) stem_fwd_kernel(const __nv_bfloat16* __res
   }
   __syncthreads();
   const int P = S / 2;
-  const long long total = static_cast<long long>(N) * P * P * 4;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int g = static_cast<int>(i % 4);
-    const long long pix = i / 4;
-    const int q = static_cast<int>(pix % P);
-    const int p = static_cast<int>((pix / P) % P);
-    const int n = static_cast<int>(pix / (static_cast<long long>(P) * P));
+  const int total = N * P * P * 4;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int g = i & 3;
+    const int pix = i >> 2;
+    const int q = pix % P;
+    const int p = (pix / P) % P;
+    const int n = pix / (P * P);
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
@@ -268,7 +297,7 @@ __global__ void __launch_bounds__(kT) stem_fwd_kernel(const __nv_bfloat16* __res
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[j] = relu6f(acc[j]);
     }
-    st8(y + pix * 32 + g * 8, acc);
+    st8(y + static_cast<size_t>(pix) * 32 + g * 8, acc);
   }
 }
 
@@ -277,33 +306,36 @@ __global__ void __launch_bounds__(kT) stem_fwd_kernel(const __nv_bfloat16* __res
 __global__ void __launch_bounds__(kT) stem_wgrad_partial_kernel(const __nv_bfloat16* __restrict__ x,
                                                                 const __nv_bfloat16* __restrict__ dy,
                                                                 float* __restrict__ partial, int N, int S,
-                                                                long long pix_per_chunk) {
+                                                                int rows_per_chunk) {
   __shared__ float red[8][27][32];
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const int P = S / 2;
-  const long long M = static_cast<long long>(N) * P * P;
-  const long long p0 = blockIdx.x * pix_per_chunk;
-  const long long p1 = min(M, p0 + pix_per_chunk);
+  const int r0 = blockIdx.x * rows_per_chunk;
+  const int r1 = min(N * P, r0 + rows_per_chunk);
   float acc[27];
 #pragma unroll
   for (int t = 0; t < 27; ++t) acc[t] = 0.0f;
-  for (long long pix = p0 + wp; pix < p1; pix += 8) {
-    const int q = static_cast<int>(pix % P);
-    const int p = static_cast<int>((pix / P) % P);
-    const int n = static_cast<int>(pix / (static_cast<long long>(P) * P));
-    const float g = __bfloat162float(dy[pix * 32 + lane]);
+  for (int row = r0 + wp; row < r1; row += 8) {  // output row (n, p)
+    const int p = row % P;
+    const int n = row / P;
+    const __nv_bfloat16* grow = dy + static_cast<size_t>(row) * P * 32 + lane;
+#pragma unroll 4
+    for (int q = 0; q < P; ++q) {
+      const float g = __bfloat162float(grow[static_cast<size_t>(q) * 32]);
 #pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      const int h = 2 * p + r - 1;
-      if (h < 0 || h >= S) continue;
+      for (int r = 0; r < 3; ++r) {
+        const int h = 2 * p + r - 1;
+        if (h < 0 || h >= S) continue;
+        const __nv_bfloat16* xr = x + (static_cast<size_t>(n) * S + h) * S * 16;
 #pragma unroll
-      for (int s = 0; s < 3; ++s) {
-        const int ww = 2 * q + s - 1;
-        if (ww < 0 || ww >= S) continue;
-        const uint2 v = *reinterpret_cast<const uint2*>(x + ((static_cast<size_t>(n) * S + h) * S + ww) * 16);
-        acc[r * 9 + s * 3 + 0] = fmaf(g, __uint_as_float(v.x << 16), acc[r * 9 + s * 3 + 0]);
-        acc[r * 9 + s * 3 + 1] = fmaf(g, __uint_as_float(v.x & 0xFFFF0000u), acc[r * 9 + s * 3 + 1]);
-        acc[r * 9 + s * 3 + 2] = fmaf(g, __uint_as_float(v.y << 16), acc[r * 9 + s * 3 + 2]);
+        for (int s = 0; s < 3; ++s) {
+          const int ww = 2 * q + s - 1;
+          if (ww < 0 || ww >= S) continue;
+          const uint2 v = *reinterpret_cast<const uint2*>(xr + static_cast<size_t>(ww) * 16);
+          acc[r * 9 + s * 3 + 0] = fmaf(g, __uint_as_float(v.x << 16), acc[r * 9 + s * 3 + 0]);
+          acc[r * 9 + s * 3 + 1] = fmaf(g, __uint_as_float(v.x & 0xFFFF0000u), acc[r * 9 + s * 3 + 1]);
+          acc[r * 9 + s * 3 + 2] = fmaf(g, __uint_as_float(v.y << 16), acc[r * 9 + s * 3 + 2]);
+        }
       }
     }
   }
@@ -314,7 +346,7 @@ __global__ void __launch_bounds__(kT) stem_wgrad_partial_kernel(const __nv_bfloa
     const int t = o / 32, k = o % 32;
     float s = 0.0f;
     for (int i = 0; i < 8; ++i) s += red[i][t][k];
-    // partial layout = the weight layout [32][3][3][16] (pad channels written as 0 by pass 2)
+    // partial layout = the weight layout [32][3][3][16] (pad channels written as 0 here)
     partial[blockIdx.x * (32 * 9 * 16) + (k * 9 + t / 3) * 16 + t % 3] = s;
   }
   for (int o = threadIdx.x; o < 32 * 9 * 13; o += kT) {
@@ -324,28 +356,35 @@ __global__ void __launch_bounds__(kT) stem_wgrad_partial_kernel(const __nv_bfloa
 }
 
 // ------------------------------------------------------------------ BN apply (affine) + act [+ residual]
+// Thread = one 8-channel group for rows slot, slot + rpp, ... (cg = C/8 groups, rpp = 256/cg rows
+// per CTA pass), so A, B live in registers for the whole kernel.
 template <int ACT, bool RES>
 __global__ void __launch_bounds__(kT) bn_apply_act_kernel(const __nv_bfloat16* __restrict__ y,
                                                           const float* __restrict__ mean_rstd,
                                                           const float* __restrict__ gamma,
                                                           const float* __restrict__ beta,
                                                           const __nv_bfloat16* __restrict__ res,
-                                                          __nv_bfloat16* __restrict__ out, long long m, int C) {
-  const int G = C / 8;
-  const long long total = m * G;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int c0 = static_cast<int>(i % G) * 8;
-    const size_t off = static_cast<size_t>(i / G) * C + c0;
+                                                          __nv_bfloat16* __restrict__ out, int m, int C) {
+  const int cg = C / 8;
+  const int rpp = kT / cg;
+  const int g = threadIdx.x % cg;
+  const int slot = threadIdx.x / cg;
+  if (slot >= rpp) return;
+  const int c0 = g * 8;
+  float A[8], B[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    A[j] = gamma[c0 + j] * mean_rstd[C + c0 + j];
+    B[j] = fmaf(-A[j], mean_rstd[c0 + j], beta[c0 + j]);
+  }
+  for (int r = blockIdx.x * rpp + slot; r < m; r += gridDim.x * rpp) {
+    const size_t off = static_cast<size_t>(r) * C + c0;
     float f[8], rv[8];
     ld8(y + off, f);
     if (RES) ld8(res + off, rv);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const int c = c0 + j;
-      const float A = gamma[c] * mean_rstd[C + c];
-      const float B = fmaf(-A, mean_rstd[c], beta[c]);
-      float z = fmaf(A, f[j], B);
+      float z = fmaf(A[j], f[j], B[j]);
       if (ACT == 6) z = relu6f(z);
       if (RES) z = z + rv[j];
       f[j] = z;
@@ -401,18 +440,26 @@ __global__ void __launch_bounds__(kT) mse_affine_partial_kernel(const __nv_bfloa
   }
 }
 
+// one CTA: strided per-thread sums, xor-shuffle tree per warp, warps added in order (deterministic)
 __global__ void loss_sum_kernel(const double* __restrict__ part, int n, double norm, double* __restrict__ loss) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < n; ++i) s += part[i];
-    *loss = s / norm;
+  __shared__ double sm[kT / 32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kT / 32; ++w) t += sm[w];
+    *loss = t / norm;
   }
 }
 
 template <int K>
 cudaError_t launch_dw_fwd(int st, const DwArgs& d, const void* x, const void* wt, const float* bias, void* y,
                           int relu6, cudaStream_t s) {
-  const int g = grid_for(static_cast<long long>(d.n) * d.p * d.q * (d.c / 8));
+  const int g = grid_for(static_cast<long long>(d.n) * d.p * ((d.q + kQT - 1) / kQT) * (d.c / 8));
   if (st == 1)
     dw_fwd_kernel<K, 1><<<g, kT, 0, s>>>(static_cast<const __nv_bfloat16*>(x),
                                          static_cast<const __nv_bfloat16*>(wt), bias,
@@ -441,8 +488,7 @@ cudaError_t launch_dw_dgrad(int st, const DwArgs& d, const void* dy, const void*
 }
 
 struct WgradTiling {
-  int lanes_c, cwin, chunks;
-  long long per_chunk;
+  int lanes_c, cwin, chunks, per_chunk;  // per_chunk = output rows (n, p) per chunk
 };
 
 WgradTiling dw_wgrad_tiling(const DwArgs& d) {
@@ -450,11 +496,11 @@ WgradTiling dw_wgrad_tiling(const DwArgs& d) {
   const int G = d.c / 8;
   t.lanes_c = std::min(G, 32);
   t.cwin = (G + t.lanes_c - 1) / t.lanes_c;
-  const long long M = static_cast<long long>(d.n) * d.p * d.q;
-  const int target = 148 * 4;
-  t.chunks = static_cast<int>(std::max<long long>(1, std::min<long long>(M / 64 + 1, target / (t.cwin * d.k) + 1)));
-  t.per_chunk = (M + t.chunks - 1) / t.chunks;
-  t.chunks = static_cast<int>((M + t.per_chunk - 1) / t.per_chunk);
+  const int rows = d.n * d.p;
+  const int target = 148 * 8;
+  t.chunks = std::max(1, std::min(rows, target / (t.cwin * d.k) + 1));
+  t.per_chunk = (rows + t.chunks - 1) / t.chunks;
+  t.chunks = (rows + t.per_chunk - 1) / t.per_chunk;
   return t;
 }
 
@@ -481,13 +527,14 @@ bool dw_ok(const DwArgs& d) {
   if (d.k != 3 && d.k != 5 && d.k != 7) return false;
   if (d.stride != 1 && d.stride != 2) return false;
   const int pad = d.k / 2;
+  if (static_cast<long long>(d.n) * d.h * d.w * d.c >= (1LL << 31)) return false;  // 32-bit work indices
   return d.p == (d.h + 2 * pad - d.k) / d.stride + 1 && d.q == (d.w + 2 * pad - d.k) / d.stride + 1;
 }
 
-long long stem_chunk_pixels(int n, int S) {
-  const long long M = static_cast<long long>(n) * (S / 2) * (S / 2);
-  const long long chunks = std::max<long long>(1, std::min<long long>(148 * 2, M / 256 + 1));
-  return (M + chunks - 1) / chunks;
+int stem_chunk_rows(int n, int S) {  // output rows (n, p) per chunk: ~2 waves of CTAs
+  const int rows = n * (S / 2);
+  const int chunks = std::max(1, std::min(148 * 8, rows / 8 + 1));
+  return (rows + chunks - 1) / chunks;
 }
 
 }  // namespace
@@ -525,7 +572,7 @@ int dw_wgrad(const DwArgs& d, const void* a, const void* dy, float* ws, size_t w
 }
 
 int stem_fwd(const void* x, const void* w, const float* bias, void* y, int n, int S, int relu6, cudaStream_t s) {
-  if (n < 1 || S < 2 || S % 2 != 0) return PBDK_EINVAL;
+  if (n < 1 || S < 2 || S % 2 != 0 || static_cast<long long>(n) * S * S >= (1LL << 29)) return PBDK_EINVAL;
   stem_fwd_kernel<<<grid_for(static_cast<long long>(n) * (S / 2) * (S / 2) * 4), kT, 0, s>>>(
       static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(w), bias,
       static_cast<__nv_bfloat16*>(y), n, S, relu6);
@@ -533,17 +580,17 @@ int stem_fwd(const void* x, const void* w, const float* bias, void* y, int n, in
 }
 
 size_t stem_wgrad_workspace_floats(int n, int S) {
-  const long long M = static_cast<long long>(n) * (S / 2) * (S / 2);
-  const long long per = stem_chunk_pixels(n, S);
-  return static_cast<size_t>((M + per - 1) / per) * 32 * 9 * 16;
+  const int rows = n * (S / 2);
+  const int per = stem_chunk_rows(n, S);
+  return static_cast<size_t>((rows + per - 1) / per) * 32 * 9 * 16;
 }
 
 int stem_wgrad(const void* x, const void* dy, int n, int S, float* ws, size_t ws_floats, float* dw, cudaStream_t s) {
   if (n < 1 || S < 2 || S % 2 != 0 || ws == nullptr || ws_floats < stem_wgrad_workspace_floats(n, S))
     return PBDK_EINVAL;
-  const long long M = static_cast<long long>(n) * (S / 2) * (S / 2);
-  const long long per = stem_chunk_pixels(n, S);
-  const int chunks = static_cast<int>((M + per - 1) / per);
+  const int rows = n * (S / 2);
+  const int per = stem_chunk_rows(n, S);
+  const int chunks = (rows + per - 1) / per;
   stem_wgrad_partial_kernel<<<chunks, kT, 0, s>>>(static_cast<const __nv_bfloat16*>(x),
                                                   static_cast<const __nv_bfloat16*>(dy), ws, n, S, per);
   chunk_sum_kernel<<<grid_for(32 * 9 * 16), kT, 0, s>>>(ws, chunks, 32 * 9 * 16, dw);
@@ -552,17 +599,18 @@ int stem_wgrad(const void* x, const void* dy, int n, int S, float* ws, size_t ws
 
 int bn_apply_act(const void* y, const float* mean_rstd, const float* gamma, const float* beta, const void* res,
                  void* out, long long m, int c, int relu6, cudaStream_t s) {
-  if (c % 8 != 0 || m < 1) return PBDK_EINVAL;
-  const int g = grid_for(m * (c / 8));
+  if (c % 8 != 0 || c / 8 > kT || m < 1 || m >= (1LL << 31)) return PBDK_EINVAL;
+  const int rpp = kT / (c / 8);
+  const int g = static_cast<int>(std::max<long long>(1, std::min<long long>((m + rpp - 1) / rpp, 148LL * 8)));
   auto* yy = static_cast<const __nv_bfloat16*>(y);
   auto* rr = static_cast<const __nv_bfloat16*>(res);
   auto* oo = static_cast<__nv_bfloat16*>(out);
   if (relu6 && res == nullptr)
-    bn_apply_act_kernel<6, false><<<g, kT, 0, s>>>(yy, mean_rstd, gamma, beta, rr, oo, m, c);
+    bn_apply_act_kernel<6, false><<<g, kT, 0, s>>>(yy, mean_rstd, gamma, beta, rr, oo, static_cast<int>(m), c);
   else if (!relu6 && res == nullptr)
-    bn_apply_act_kernel<0, false><<<g, kT, 0, s>>>(yy, mean_rstd, gamma, beta, rr, oo, m, c);
+    bn_apply_act_kernel<0, false><<<g, kT, 0, s>>>(yy, mean_rstd, gamma, beta, rr, oo, static_cast<int>(m), c);
   else if (!relu6)
-    bn_apply_act_kernel<0, true><<<g, kT, 0, s>>>(yy, mean_rstd, gamma, beta, rr, oo, m, c);
+    bn_apply_act_kernel<0, true><<<g, kT, 0, s>>>(yy, mean_rstd, gamma, beta, rr, oo, static_cast<int>(m), c);
   else
     return PBDK_EINVAL;
   return ok(cudaGetLastError());
@@ -579,7 +627,7 @@ int mse_affine(const void* y, const float* mean_rstd, const float* gamma, const 
                                                 static_cast<const __nv_bfloat16*>(res),
                                                 static_cast<const __nv_bfloat16*>(t), m, c, gscale,
                                                 static_cast<__nv_bfloat16*>(g), ws);
-  loss_sum_kernel<<<1, 32, 0, s>>>(ws, grid, norm, loss);
+  loss_sum_kernel<<<1, kT, 0, s>>>(ws, grid, norm, loss);
   return ok(cudaGetLastError());
 }
 
