@@ -340,17 +340,25 @@ def _dev_of(stage):
 # ---------------------------------------------------------------- device profiler + AHD on B200
 
 def profile_blocks(global_batch: int, world: int, keys: Optional[List[int]] = None, reps: int = 5,
-                   device: Optional[torch.device] = None) -> dict:
+                   device: Optional[torch.device] = None, model: str = "resnet", image: Optional[int] = None,
+                   paths: Optional[Dict[int, List[int]]] = None) -> dict:
     """Measure T_k(b), S_k(b) of every block on this GPU with CUDA events ("runs steps
-    of each block with feasible batch sizes") and emit a profile document (profile.hpp:30-86)."""
-    from . import executor, models
+    of each block with feasible batch sizes") and emit a profile document (profile.hpp:30-86).
+    model "mbv2": the active single path `paths[k]` of the supernet is what is timed."""
+    from . import executor, models, mb_models
     keys = keys or sorted({max(1, global_batch // d) for d in (16, 8, 4, 2, 1)})
+    nblocks = models.BLOCKS if model == "resnet" else mb_models.NL.__len__()
+    if model == "mbv2":
+        image = image or 224
+        paths = paths or mb_models.paths_for(0)
     blocks = []
-    for k in range(models.BLOCKS):
+    for k in range(nblocks):
         tms, sms = {}, {}
         for n in keys:
-            p = executor.Partition(k, k, n, max(n, global_batch), device=device)
+            p = executor.Partition(k, k, n, max(n, global_batch), device=device, model=model, image=image)
             p.init_params()
+            if model == "mbv2":
+                p.set_path(k, paths[k])
             p.set_timing(True)
             t_samples, s_samples = [], []
             for r in range(reps + 2):
@@ -368,12 +376,17 @@ def profile_blocks(global_batch: int, world: int, keys: Optional[List[int]] = No
             run_t = max(run_t, tms[n])
             run_s = max(run_s, sms[n])
             tms[n], sms[n] = run_t, run_s
-        g = models.student_geom(k)
-        act = models.T_HW[k + 1] ** 2 * models.T_CH[k + 1] * 2
-        tparams = sum(c[1] * c[2] * c[2] * (16 if c[0] == 3 else c[0]) * 2 for c, _ in models.teacher_convs(k))
+        if model == "resnet":
+            act = models.T_HW[k + 1] ** 2 * models.T_CH[k + 1] * 2
+            tparams = sum(c[1] * c[2] * c[2] * (16 if c[0] == 3 else c[0]) * 2 for c, _ in models.teacher_convs(k))
+            pbytes = models.student_param_count(k) * 4
+        else:
+            act = mb_models.act_bytes_per_sample(k + 1, image)
+            tparams = mb_models.teacher_param_bytes(k)
+            pbytes = mb_models.path_param_bytes(k, paths[k])
         blocks.append({"id": k, "teacher_ms": {str(n): tms[n] for n in keys},
                        "student_ms": {str(n): sms[n] for n in keys}, "act_bytes_per_sample": float(act),
-                       "param_bytes": float(models.student_param_count(k) * 4), "teacher_param_bytes": float(tparams)})
+                       "param_bytes": float(pbytes), "teacher_param_bytes": float(tparams)})
     return {"blocks": blocks, "global_batch": global_batch,
             "hardware": {"num_devices": world, "link_bytes_per_ms": 7.7e8, "allreduce_bytes_per_ms": 7.25e8,
                          "mem_bytes_per_device": 1.8e11, "data_load_ms_per_batch": 0.0,
@@ -410,19 +423,26 @@ def bench_pipeline(args, rank: int, world: int, local_rank: int) -> dict:
         os.environ.setdefault("WORLD_SIZE", str(world))
         dist.init_process_group("nccl", device_id=dev)
     gb = args.batch * world
+    model = "mbv2" if getattr(args, "workload", "cifar") == "mbv2" else "resnet"
+    image = getattr(args, "image", 224) if model == "mbv2" else None
+    from . import mb_models
+    paths = mb_models.paths_for(0) if model == "mbv2" else None
     # profile on rank 0's GPU, schedule on rank 0, broadcast the documents
     obj = [None, None]
     if rank == 0:
-        prof = profile_blocks(gb, world, device=dev)
+        prof = profile_blocks(gb, world, device=dev, model=model, image=image, paths=paths)
         sched, meta = core.best_schedule(prof)
         obj = [sched, {"profile": prof, "meta": meta}]
     dist.broadcast_object_list(obj, src=0)
     sched, info = obj
 
     def make_stage(lo, hi, n, first):
-        p = executor.Partition(lo, hi, n, gb, device=dev)
+        p = executor.Partition(lo, hi, n, gb, device=dev, model=model, image=image)
         p.init_params()
         p.set_shard(n, first)
+        for k in range(lo, hi + 1):
+            if paths is not None:
+                p.set_path(k, paths[k])
         return p
 
     def timed(pipe, steps, e2e_hook=None):
@@ -459,7 +479,8 @@ def bench_pipeline(args, rank: int, world: int, local_rank: int) -> dict:
     host = None
     if me.partition == 0:
         pipe.stage.set_external_input(True)
-        host = torch.empty(me.count, 32, 32, 3, dtype=torch.float32).pin_memory().uniform_(-1, 1)
+        side = image or 32
+        host = torch.empty(me.count, side, side, 3, dtype=torch.float32).pin_memory().uniform_(-1, 1)
         if getattr(pipe, "_graphs", False):
             pipe.use_graphs()  # re-capture without the on-device data generation
     loss_host = torch.empty(len(pipe.stage.blocks), dtype=torch.float64).pin_memory()
@@ -475,14 +496,16 @@ def bench_pipeline(args, rank: int, world: int, local_rank: int) -> dict:
     all_losses = [None] * world
     dist.all_gather_object(all_losses, losses)
     pred = core.predicted_step_time(info["profile"], sched)
-    h2d = (me.count * 32 * 32 * 3 * 4) if host is not None else 0
+    h2d = (me.count * (image or 32) ** 2 * 3 * 4) if host is not None else 0
     dist.barrier()
     dist.destroy_process_group()
     return {"metric": "blockwise-distill samples/sec", "value": gb / ms * 1e3, "unit": "samples/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (Philox4x32-10 on device)",
-            "config": {"workload": "cifar-resnet18-teacher/slim-student 4 blocks (configs[1])", "global_batch": gb,
+            "config": {"workload": ("cifar-resnet18-teacher/slim-student 4 blocks (configs[1])" if model == "resnet"
+                                    else f"mbv2-teacher/proxyless-supernet 6 blocks {image}x{image} (configs[2])"),
+                       "global_batch": gb,
                        "parallelism": "ahd " + ";".join(f"{p['blocks']}x{len(p['devices'])}"
                                                         for p in sched["partitions"]),
                        "relay": pipe.relay,

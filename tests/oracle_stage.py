@@ -85,3 +85,59 @@ class OracleStage:
 
     def set_step_index(self, step):
         self.step_idx = int(step)
+
+
+class MbOracleStage(OracleStage):
+    """The MobileNetV2 -> ProxylessNAS workload (oracle/mb_oracle.c) behind the same interface:
+    image side S, a fixed single path per block."""
+
+    def __init__(self, lo, hi, n, first, global_batch, S, paths):
+        from oracle import mb
+        self.mb = mb
+        self.lo, self.hi, self.n, self.first, self.b, self.S = lo, hi, n, first, global_batch, S
+        self.paths = paths
+        self.blocks = list(range(lo, hi + 1))
+        self.tp = {k: mb.teacher_params(k) for k in self.blocks}
+        self.sp = {k: mb.student_params(k) for k in self.blocks}
+        self.mom = {k: np.zeros_like(self.sp[k]) for k in self.blocks}
+        self.sizes = [self.sp[k].size for k in self.blocks]
+        self.in_buf = torch.zeros(mb.act_shape(lo, n, S) if lo > 0 else (n, S, S, 3))
+        self.out_buf = torch.zeros(mb.act_shape(hi + 1, n, S))
+        self.grad_buf = torch.zeros(sum(self.sizes))
+        self.step_idx = 0
+        self._losses = [0.0] * len(self.blocks)
+        self.acts = None
+
+    def teacher_forward(self):
+        mb = self.mb
+        if self.lo == 0:
+            x = mb.image(self.n, self.step_idx * self.b + self.first, self.S)
+        else:
+            x = self.in_buf.numpy().copy()
+        acts = [x]
+        for k in self.blocks:
+            acts.append(mb.teacher_fwd(k, self.tp[k], acts[-1], self.S))
+        self.acts = acts
+        self.out_buf.copy_(torch.from_numpy(acts[-1]))
+
+    def student_step(self):
+        mb = self.mb
+        parts = []
+        for i, k in enumerate(self.blocks):
+            norm = float(self.b) * mb.channels(k + 1) * mb.hw(k + 1, self.S) ** 2
+            g, loss = mb.student_fwd_bwd(k, self.sp[k], self.paths[k], self.acts[i], self.acts[i + 1], self.S, norm)
+            self._losses[i] = loss
+            parts.append(g)
+        self.grad_buf.copy_(torch.from_numpy(np.concatenate(parts)))
+
+    def apply_update(self):
+        off = 0
+        g = self.grad_buf.numpy()
+        for k, sz in zip(self.blocks, self.sizes):
+            self.mb.sgd_path(k, self.paths[k], self.sp[k], self.mom[k], g[off:off + sz].copy())
+            off += sz
+        self.step_idx += 1
+
+    def block_state_like(self, k):
+        n = self.mb.student_param_count(k)
+        return [torch.empty(n), torch.empty(n)]

@@ -174,3 +174,32 @@ def test_path_switch_recaptures(ex):
     p.replay()
     torch.cuda.synchronize()
     assert all(np.isfinite(p.losses()))
+
+
+def test_reconfiguration_on_measured_drift(ex):
+    """configs[4]: switching late blocks to heavier candidates at an epoch boundary drifts the
+    device-measured block times; reconfigure() re-plans and the new plan is best_schedule() of the
+    observed profile (bit-exact, as the reference's reconfigure is defined, schedule.cpp:347-359)."""
+    from paper_2301_12443_b200 import core, mb_models, runtime
+    gb, image, N = 64, 64, 8
+    paths0 = {k: [0] * mb.layers(k) for k in range(6)}  # lightest candidates (k3, e3)
+    prof = runtime.profile_blocks(gb, N, keys=[8, 16, 32, 64], reps=3, model="mbv2", image=image, paths=paths0)
+    sched0, _ = core.best_schedule(prof)
+    paths1 = {k: list(v) for k, v in paths0.items()}
+    for k in (4, 5):
+        paths1[k] = [0 if (k == 0 and l < 2) else 5 for l in range(mb.layers(k))]
+    heavy = runtime.profile_blocks(gb, N, keys=[8, 16, 32, 64], reps=3, model="mbv2", image=image, paths=paths1)
+    # the monitor observes every block at its current per-device batch
+    measured = {}
+    for part in sched0["partitions"]:
+        lo, hi = part["blocks"]
+        bj = part["per_device_batch"]
+        for k in range(lo, hi + 1):
+            measured[k] = (bj, core.exec_time(heavy, k, "teacher", bj), core.exec_time(heavy, k, "student", bj))
+    observed = runtime.observed_profile(prof, measured)
+    assert core.profile_drift(prof, observed) > 0.1
+    new = core.reconfigure(prof, sched0, observed, 0.1)
+    assert new is not None
+    best, _ = core.best_schedule(observed)
+    assert new["partitions"] == best["partitions"]
+    assert core.predicted_step_time(observed, new)["step_ms"] <= core.predicted_step_time(observed, sched0)["step_ms"]

@@ -193,3 +193,52 @@ def test_peer_wiring_slots_are_consistent():
                             if 0 <= off < 10 ** 9:
                                 rows[off // 1000: off // 1000 + nrows] += 1
                     assert (rows == 1).all()
+
+
+def _mb_worker(rank, world, port, schedule, b, S, steps, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    torch.set_num_threads(2)
+    os.environ["OMP_NUM_THREADS"] = "2"
+    from oracle import mb
+    from tests.oracle_stage import MbOracleStage
+    paths = {k: mb.sample_path(k, 2) for k in range(6)}
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        pipe = runtime.PipeBD(schedule, b, lambda lo, hi, n, first: MbOracleStage(lo, hi, n, first, b, S, paths))
+        for _ in range(steps):
+            pipe.step()
+        pipe.end_epoch()
+        q.put((rank, pipe.block_losses(), {k: pipe.stage.sp[k] for k in pipe.stage.blocks}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_mbv2_hybrid_distributed_equals_single_process():
+    """configs[2] workload through the multi-rank runtime: [0-1]x1 -> [2-4]x2 -> [5]x1 (1->2 and 2->1
+    resharding, a DP group over the supernet's path-sparse gradients) == one process, same shards."""
+    from oracle import mb
+    b, S, steps, world = 3, 32, 2, 4
+    parts = [(0, 1, [0]), (2, 4, [1, 2]), (5, 5, [3])]
+    s = sched(parts, b)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_mb_worker, args=(r, world, port, s, b, S, steps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    paths = {k: mb.sample_path(k, 2) for k in range(6)}
+    groups = {k: len(devs) for lo, hi, devs in parts for k in range(lo, hi + 1)}
+    tr = mb.Trainer(b, S)
+    for st in range(steps):
+        want = tr.step(st, paths, groups)
+    for rank, losses, params in out:
+        for k, v in losses.items():
+            assert v == pytest.approx(want[k], rel=1e-12, abs=1e-15), (rank, k)
+        for k, p in params.items():
+            np.testing.assert_allclose(p, tr.sp[k], rtol=1e-6, atol=1e-9)
