@@ -42,8 +42,9 @@ def parse():
     ap.add_argument("--batch", type=int, default=PER_GPU_BATCH, help="global batch per GPU")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", choices=["cifar", "mbv2"], default="cifar",
-                    help="cifar: configs[1] (headline); mbv2: configs[2] MobileNetV2 -> ProxylessNAS at 224x224")
+    ap.add_argument("--workload", choices=["cifar", "mbv2", "effb0"], default="cifar",
+                    help="cifar: configs[1] (headline); mbv2: configs[2] MobileNetV2 -> ProxylessNAS at 224x224; "
+                         "effb0: configs[3] EfficientNet-B0 -> ProxylessNAS")
     ap.add_argument("--image", type=int, default=224, help="mbv2 image side")
     ap.add_argument("--relay", choices=["peer", "nccl"], default="peer",
                     help="N>1 teacher-activation relay: K11 peer stores over NVLink (default) or NCCL send/recv")
@@ -236,7 +237,7 @@ def run_ours(args, rank, world, local_rank):
             print(json.dumps(res), flush=True)
         return
 
-    if args.workload == "mbv2":
+    if args.workload in ("mbv2", "effb0"):
         return run_ours_mbv2(args, dev, local_rank)
 
     b = args.batch
@@ -332,9 +333,10 @@ def run_ours_mbv2(args, dev, local_rank):
     one GPU (the IR point); the seeded single path of epoch 0 (draw 0) is active, graph replay."""
     import torch
     from paper_2301_12443_b200 import executor, mb_models
-    b, S = args.batch, args.image
+    b, S, model = args.batch, args.image, args.workload
+    mb_models.set_family(model)
     paths = mb_models.paths_for(0)
-    part = executor.Partition(0, 5, b, b, device=dev, model="mbv2", image=S)
+    part = executor.Partition(0, 5, b, b, device=dev, model=model, image=S)
     part.init_params()
     for k in range(6):
         part.set_path(k, paths[k])
@@ -385,6 +387,7 @@ def run_ours_mbv2(args, dev, local_rank):
     cpu = None
     if not args.no_cpu_baseline:
         from oracle import mb
+        mb.set_family(1 if model == "effb0" else 0)
         tr = mb.Trainer(1, S)
         tr.step(0, paths)
         t0 = time.perf_counter()
@@ -396,7 +399,10 @@ def run_ours_mbv2(args, dev, local_rank):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (Philox4x32-10 images on device each step; random-init weights)",
-            "config": {"workload": "mbv2-teacher/proxyless-supernet 6 blocks, IR point on 1 GPU (configs[2] shape)",
+            "config": {"workload": ("mbv2-teacher/proxyless-supernet 6 blocks, IR point on 1 GPU (configs[2] shape)"
+                                    if model == "mbv2" else
+                                    "effb0-teacher(swish,SE)/proxyless-supernet 6 blocks, IR point on 1 GPU "
+                                    "(configs[3] shape)"),
                        "global_batch": b, "image": f"{S}x{S}x3", "blocks": 6, "paths": paths,
                        "parallelism": "ir1 (blocks 0-5 on 1 GPU)", "cuda_graph": True,
                        "l2": "no flush: per-step working set > 20 GiB >> 126 MB L2"},

@@ -45,6 +45,7 @@ extern "C" {
 #define PBDK_EPI_BIAS_RES 6       /* y = acc + bias[k] + aux[m][k]              */
 #define PBDK_EPI_RELU6_MASK 7     /* y = 0 < aux[m][k] < 6 ? acc : 0 (relu6 bwd) */
 #define PBDK_EPI_ADD 8            /* y = acc + aux[m][k]                        */
+#define PBDK_EPI_BIAS_SWISH 9     /* y = z * sigmoid(z), z = acc + bias[k]      */
 
 typedef struct pbdk_conv_desc {
   int n, h, w, c;  /* input NHWC, c = stored channels (multiple of 16) */

@@ -35,6 +35,7 @@ extern "C" {
 /* workloads */
 #define PBDX_MODEL_RESNET_CIFAR 0    /* configs[0..1]: ResNet-18-CIFAR teacher -> slim residual student, 4 blocks */
 #define PBDX_MODEL_MBV2_PROXYLESS 1  /* configs[2]: MobileNetV2 teacher -> ProxylessNAS supernet student, 6 blocks */
+#define PBDX_MODEL_EFFB0_PROXYLESS 2 /* configs[3]: EfficientNet-B0 teacher (swish, squeeze-excite) -> same space */
 
 typedef struct pbdx_desc {
   int block_lo, block_hi; /* inclusive block range of the model's chain        */
@@ -103,7 +104,15 @@ int pbdx_refresh_shadows(void* handle, void* stream);
 int pbdx_set_timing(void* handle, int enabled);
 int pbdx_block_times(void* handle, float* teacher_ms, float* student_ms);
 
-/* Search space (PBDX_MODEL_MBV2_PROXYLESS): active candidate of every student layer of `block`
+/* Supernet layout of the MBConv models (host-only queries, no device needed): student layers of a
+ * block, candidates of a layer, a candidate's (offset, count) inside the block's flat parameters,
+ * and the block's parameter count.  -1 on bad arguments. */
+int pbdx_mb_layers(int model, int block);
+int pbdx_mb_candidates(int model, int block, int layer);
+long pbdx_mb_candidate_offset(int model, int block, int layer, int cand, long* count);
+long pbdx_mb_block_params(int model, int block);
+
+/* Search space (PBDX_MODEL_MBV2_PROXYLESS / _EFFB0_PROXYLESS): active candidate of every student layer of `block`
  * (path[l] in [0, candidates); fixed layers 0).  Only the active path runs forward/backward and is
  * updated (inactive candidates keep weights and momentum: torch semantics for params without
  * .grad).  Invalidates captured graphs.  Layout of the supernet parameters: DESIGN.md §10. */

@@ -48,8 +48,20 @@ def lib():
         L.mbo_teacher_fwd.argtypes = [I, F32P, I, I, F32P, F32P, I]
         L.mbo_student_fwd_bwd.argtypes = [I, F32P, I32P, I, I, F32P, F32P, D, I, F32P, ctypes.POINTER(D)]
         L.mbo_sgd_path.argtypes = [I, I32P, F32P, F32P, F32P, ctypes.c_float, ctypes.c_float]
+        L.mbo_set_family.argtypes = [I]
+        L.mbo_family.restype = I
         _L = L
     return _L
+
+
+def set_family(f: int):
+    """0 = MobileNetV2 teacher (configs[2]), 1 = EfficientNet-B0 teacher (configs[3])."""
+    global FAMILY
+    lib().mbo_set_family(int(f))
+    FAMILY = int(f)
+
+
+FAMILY = 0
 
 
 def channels(b: int) -> int:
@@ -174,9 +186,29 @@ class Trainer:
 
 # ---------------------------------------------------------------- per-candidate layout (mb_oracle.c cand_lay)
 KS, ES = (3, 5, 7), (3, 6)
-NL = (3, 3, 4, 3, 3, 1)
+NLF = ((3, 3, 4, 3, 3, 1), (3, 2, 3, 3, 4, 1))
+CHF = ((3, 32, 32, 64, 128, 192, 320), (3, 32, 64, 128, 128, 192, 320))
+KF = ((3, 3, 3, 3, 3, 3), (3, 5, 3, 5, 5, 3))
 DIV = (1, 4, 8, 16, 16, 32, 32)
-CH = (3, 32, 32, 64, 128, 192, 320)
+
+
+class _FamTable:
+    def __init__(self, t):
+        self.t = t
+
+    def __getitem__(self, i):
+        return self.t[FAMILY][i]
+
+    def __len__(self):
+        return len(self.t[FAMILY])
+
+
+NL = _FamTable(NLF)
+CH = _FamTable(CHF)
+
+
+def se_ch(cin: int) -> int:
+    return max(1, cin // 4) if FAMILY == 1 else 0
 
 
 def round_ch(c: int) -> int:
@@ -189,7 +221,8 @@ def teacher_layer(b: int, l: int):
         return ((1, 3, 32, 16, 1), (6, 3, 16, 32, 2), (6, 3, 32, 32, 1))[l]
     cin, cout = CH[b], CH[b + 1]
     s = DIV[b + 1] // DIV[b]
-    return (6, 3, cin, cout, s) if l == 0 else (6, 3, cout, cout, 1)
+    k = KF[FAMILY][b]
+    return (6, k, cin, cout, s) if l == 0 else (6, k, cout, cout, 1)
 
 
 def student_layer(b: int, l: int, c: int):

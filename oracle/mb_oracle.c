@@ -23,9 +23,17 @@ typedef struct {
   int t, k, cin, cout, stride; /* teacher: expansion t (1 = no expand conv), kernel k */
 } mb_layer;
 
-static const int CH[7] = {3, 32, 32, 64, 128, 192, 320};
+/* teacher families: 0 = MobileNetV2 (ReLU6), 1 = EfficientNet-B0 (swish + squeeze-excite) */
+static int FAM = 0;
+static const int CHF[2][7] = {{3, 32, 32, 64, 128, 192, 320}, {3, 32, 64, 128, 128, 192, 320}};
+static const int NLF[2][6] = {{3, 3, 4, 3, 3, 1}, {3, 2, 3, 3, 4, 1}}; /* teacher MBConv layers per block */
+static const int KF[2][6] = {{3, 3, 3, 3, 3, 3}, {3, 5, 3, 5, 5, 3}};  /* teacher kernel per block */
+#define CH (CHF[FAM])
+#define NL (NLF[FAM])
 static const int DIV[7] = {1, 4, 8, 16, 16, 32, 32};
-static const int NL[6] = {3, 3, 4, 3, 3, 1}; /* teacher MBConv layers per block */
+
+void mbo_set_family(int f) { FAM = (f == 1) ? 1 : 0; }
+int mbo_family(void) { return FAM; }
 
 static int teacher_layer(int b, int l, mb_layer* o) {
   static const mb_layer B0[3] = {{1, 3, 32, 16, 1}, {6, 3, 16, 32, 2}, {6, 3, 32, 32, 1}};
@@ -36,8 +44,19 @@ static int teacher_layer(int b, int l, mb_layer* o) {
   }
   const int cin = CH[b], cout = CH[b + 1];
   const int s = DIV[b + 1] / DIV[b];
-  *o = l == 0 ? (mb_layer){6, 3, cin, cout, s} : (mb_layer){6, 3, cout, cout, 1};
+  const int k = KF[FAM][b];
+  *o = l == 0 ? (mb_layer){6, k, cin, cout, s} : (mb_layer){6, k, cout, cout, 1};
   return 1;
+}
+
+/* squeeze-excite width of an EfficientNet layer (0.25 x the layer's input channels) */
+static int se_ch(const mb_layer* m) { return FAM == 1 ? (m->cin / 4 > 0 ? m->cin / 4 : 1) : 0; }
+static inline float swishf(float z) { return z / (1.0f + expf(-z)); }
+static inline float sigmoidf(float z) { return 1.0f / (1.0f + expf(-z)); }
+/* the teacher's activation: ReLU6 (MobileNetV2) or swish (EfficientNet-B0) */
+static inline float tact(float z) {
+  if (FAM == 1) return swishf(z);
+  return z > 0.0f ? (z < 6.0f ? z : 6.0f) : 0.0f;
 }
 
 static int round_ch(int c) { return c <= 16 ? 16 : c <= 32 ? 32 : (c + 63) / 64 * 64; }
@@ -142,8 +161,10 @@ size_t mbo_teacher_param_count(int b) {
     mb_layer m;
     teacher_layer(b, l, &m);
     const int E = expand_ch(m.cin, m.t);
+    const int cs = se_ch(&m);
     if (m.t != 1) t += (size_t)E * m.cin + E;
     t += (size_t)E * m.k * m.k + E;
+    if (cs) t += (size_t)cs * E + cs + (size_t)E * cs + E;
     t += (size_t)m.cout * E + m.cout;
   }
   return t;
@@ -212,6 +233,19 @@ void mbo_teacher_init(int b, uint32_t seed, float* p, int bf16) {
     fill(p, E, 1, 1, 1, seed, base + 10u * j + 1u, 0.1f, 0);
     p += E;
     ++j;
+    const int cs = se_ch(&m);
+    if (cs) { /* squeeze-excite: W1 [cs][E] + b1, W2 [E][cs] + b2 */
+      fill(p, cs, 1, E, E, seed, base + 10u * j, kaiming(E, 1.0f), bf16);
+      p += (size_t)cs * E;
+      fill(p, cs, 1, 1, 1, seed, base + 10u * j + 1u, 0.1f, 0);
+      p += cs;
+      ++j;
+      fill(p, E, 1, cs, cs, seed, base + 10u * j, kaiming(cs, 1.0f), bf16);
+      p += (size_t)E * cs;
+      fill(p, E, 1, 1, 1, seed, base + 10u * j + 1u, 0.1f, 0);
+      p += E;
+      ++j;
+    }
     const int res = m.stride == 1 && m.cin == m.cout;
     fill(p, m.cout, 1, E, E, seed, base + 10u * j, kaiming(E, res ? 0.5f : 1.0f), bf16);
     p += (size_t)m.cout * E;
@@ -445,8 +479,45 @@ static void bias_act(float* y, size_t m, int K, const float* b, const float* res
       float v = y[(size_t)i * K + k] + b[k];
       if (res) v += res[(size_t)i * K + k];
       if (act == 6) v = relu6(v);
+      if (act == 7) v = tact(v);
       y[(size_t)i * K + k] = rnd(v, bf16);
     }
+}
+
+/* squeeze-excite on y [n][hw][E] in place: pooled = mean_hw y (double sum), h = swish(W1 pooled + b1),
+ * gate = sigmoid(W2 h + b2), y = rnd(y * gate).  p = [W1 [cs][E], b1 [cs], W2 [E][cs], b2 [E]]. */
+static void se_apply(float* y, int n, int hw, int E, int cs, const float* p, int bf16) {
+  const float* W1 = p;
+  const float* b1 = W1 + (size_t)cs * E;
+  const float* W2 = b1 + cs;
+  const float* b2 = W2 + (size_t)E * cs;
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < n; ++i) {
+    float* pooled = (float*)malloc(sizeof(float) * E);
+    float* h = (float*)malloc(sizeof(float) * cs);
+    float* gate = (float*)malloc(sizeof(float) * E);
+    float* yi = y + (size_t)i * hw * E;
+    for (int c = 0; c < E; ++c) {
+      double acc = 0.0;
+      for (int q = 0; q < hw; ++q) acc += yi[(size_t)q * E + c];
+      pooled[c] = (float)(acc / hw);
+    }
+    for (int j = 0; j < cs; ++j) {
+      float acc = b1[j];
+      for (int c = 0; c < E; ++c) acc = fmaf(W1[(size_t)j * E + c], pooled[c], acc);
+      h[j] = swishf(acc);
+    }
+    for (int c = 0; c < E; ++c) {
+      float acc = b2[c];
+      for (int j = 0; j < cs; ++j) acc = fmaf(W2[(size_t)c * cs + j], h[j], acc);
+      gate[c] = sigmoidf(acc);
+    }
+    for (int q = 0; q < hw; ++q)
+      for (int c = 0; c < E; ++c) yi[(size_t)q * E + c] = rnd(yi[(size_t)q * E + c] * gate[c], bf16);
+    free(pooled);
+    free(h);
+    free(gate);
+  }
 }
 
 /* ------------------------------------------------------------------ teacher forward */
@@ -466,7 +537,7 @@ int mbo_teacher_fwd(int b, const float* tp, int n, int S, const float* in, float
   float* o = (float*)malloc(sizeof(float) * cap);
   if (b == 0) {
     stem_fwd(in, n, S, tp, x);
-    bias_act(x, (size_t)n * (S / 2) * (S / 2), 32, tp + 32 * 9 * 16, NULL, 6, bf16);
+    bias_act(x, (size_t)n * (S / 2) * (S / 2), 32, tp + 32 * 9 * 16, NULL, 7, bf16);
     tp += 32 * 9 * 16 + 32;
     H = S / 2;
   } else {
@@ -480,13 +551,16 @@ int mbo_teacher_fwd(int b, const float* tp, int n, int S, const float* in, float
     const float* a = x;
     if (m.t != 1) {
       conv1x1(x, (size_t)n * H * H, m.cin, tp, E, e1);
-      bias_act(e1, (size_t)n * H * H, E, tp + (size_t)E * m.cin, NULL, 6, bf16);
+      bias_act(e1, (size_t)n * H * H, E, tp + (size_t)E * m.cin, NULL, 7, bf16);
       tp += (size_t)E * m.cin + E;
       a = e1;
     }
     dw_fwd(a, n, H, H, E, tp, m.k, m.stride, P, P, e2);
-    bias_act(e2, (size_t)n * P * P, E, tp + (size_t)E * m.k * m.k, NULL, 6, bf16);
+    bias_act(e2, (size_t)n * P * P, E, tp + (size_t)E * m.k * m.k, NULL, 7, bf16);
     tp += (size_t)E * m.k * m.k + E;
+    const int cs = se_ch(&m);
+    if (cs) se_apply(e2, n, P * P, E, cs, tp, bf16);
+    if (cs) tp += (size_t)cs * E + cs + (size_t)E * cs + E;
     conv1x1(e2, (size_t)n * P * P, E, tp, m.cout, o);
     const int res = m.stride == 1 && m.cin == m.cout;
     bias_act(o, (size_t)n * P * P, m.cout, tp + (size_t)m.cout * E, res ? x : NULL, 0, bf16);

@@ -28,6 +28,12 @@ extern "C" {
 #define MBO_BLOCKS 6
 #define MBO_CANDIDATES 6 /* candidate c: kernel {3,5,7}[c % 3], expansion {3,6}[c / 3] */
 
+/* teacher family (process-wide, test infrastructure): 0 = MobileNetV2 (ReLU6; configs[2]),
+ * 1 = EfficientNet-B0 (swish, squeeze-excite, k5 stages; configs[3]).  The student supernet is the
+ * same ProxylessNAS space over the family's block / layer structure. */
+void mbo_set_family(int family);
+int mbo_family(void);
+
 /* geometry (image side S, e.g. 224): boundary b in 0..6 (0 = the image, stored as 16 channels) */
 int mbo_channels(int boundary);                 /* 3, 32, 32, 64, 128, 192, 320 */
 int mbo_hw(int boundary, int S);                /* S, S/4, S/8, S/16, S/16, S/32, S/32 */

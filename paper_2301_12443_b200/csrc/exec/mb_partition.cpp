@@ -36,9 +36,31 @@ using bf16 = __nv_bfloat16;
 
 constexpr int kBlocks = 6;
 constexpr int kCands = 6;
-constexpr int CH[7] = {3, 32, 32, 64, 128, 192, 320};
 constexpr int DIV[7] = {1, 4, 8, 16, 16, 32, 32};
-constexpr int NL[6] = {3, 3, 4, 3, 3, 1};
+
+// Teacher families: MobileNetV2 (ReLU6; configs[2]) and EfficientNet-B0 (swish,
+// squeeze-excite, k5 stages; configs[3]); the student is the same ProxylessNAS supernet over the
+// family's block / layer structure.  Channel widths rounded to the tensor-tile granularity.
+struct Family {
+  int CH[7];
+  int NL[6];
+  int K[6];
+  int act;  // teacher activation code (mb_kernels.hpp): 1 ReLU6, 2 swish
+  bool se;  // squeeze-excite in every teacher MBConv
+};
+constexpr Family kMbv2{{3, 32, 32, 64, 128, 192, 320}, {3, 3, 4, 3, 3, 1}, {3, 3, 3, 3, 3, 3}, 1, false};
+constexpr Family kEffb0{{3, 32, 64, 128, 128, 192, 320}, {3, 2, 3, 3, 4, 1}, {3, 5, 3, 5, 5, 3}, 2, true};
+const Family& family(int model) { return model == PBDX_MODEL_EFFB0_PROXYLESS ? kEffb0 : kMbv2; }
+
+// the family in effect for the layout helpers below (set by every public entry point)
+thread_local const Family* g_fam = &kMbv2;
+struct FamScope {
+  const Family* prev;
+  explicit FamScope(const Family& f) : prev(g_fam) { g_fam = &f; }
+  ~FamScope() { g_fam = prev; }
+};
+#define CH (g_fam->CH)
+#define NL (g_fam->NL)
 
 struct MbLayer {
   int t, k, cin, cout, stride;
@@ -49,9 +71,11 @@ MbLayer teacher_layer(int b, int l) {
   if (b == 0) return B0[l];
   const int cin = CH[b], cout = CH[b + 1];
   const int s = DIV[b + 1] / DIV[b];
-  return l == 0 ? MbLayer{6, 3, cin, cout, s} : MbLayer{6, 3, cout, cout, 1};
+  const int k = g_fam->K[b];
+  return l == 0 ? MbLayer{6, k, cin, cout, s} : MbLayer{6, k, cout, cout, 1};
 }
 
+int se_ch(const MbLayer& m) { return g_fam->se ? std::max(1, m.cin / 4) : 0; }
 int round_ch(int c) { return c <= 16 ? 16 : c <= 32 ? 32 : (c + 63) / 64 * 64; }
 int expand_ch(int cin, int t) { return t == 1 ? cin : round_ch(cin * t); }
 int student_layers(int b) { return NL[b] + (b == 0 ? 1 : 0); }
@@ -140,7 +164,10 @@ pbdk_conv_desc pw_desc(size_t m, int cin, int cout) {
 
 // ---- teacher program
 struct TOp {
-  enum Kind { STEM, PW, DW } kind;
+  enum Kind { STEM, PW, DW, SE } kind;
+  int cs = 0;                                  // SE width
+  bf16 *w2 = nullptr;                          // SE: w = W1 [cs][E], w2 = W2 [E][cs]
+  float* b2 = nullptr;                         // SE: bias = b1 [cs], b2 [E]
   int cin = 0, cout = 0, k = 0, stride = 1, hin = 0, hout = 0, epi = 0;
   uint32_t tensor = 0;
   float gain = 1.0f;
@@ -203,10 +230,11 @@ struct SBlock {
 
 class MbPartition final : public PartitionBase {
  public:
-  explicit MbPartition(const pbdx_desc& d) : PartitionBase(d) {
+  explicit MbPartition(const pbdx_desc& d) : PartitionBase(d), fam_(family(d.model)) {
     if (d.block_lo < 0 || d.block_hi >= kBlocks || d.block_lo > d.block_hi) throw BadArg("bad block range");
     if (d.image < 32 || d.image % 32 != 0) throw BadArg("image side must be a multiple of 32");
     S_ = d.image;
+    FamScope fs(fam_);
     allocate();
     build_plans();
   }
@@ -225,11 +253,25 @@ class MbPartition final : public PartitionBase {
   int nblocks() const override { return d_.block_hi - d_.block_lo + 1; }
   const void* relay_source() const override { return tblocks_.back().out; }
   size_t relay_row_bytes() const override { return act_row_bytes(d_.block_hi + 1); }
-  void rebuild_for_shard() override { build_plans(); }
+  void rebuild_for_shard() override {
+    FamScope fs(fam_);
+    build_plans();
+  }
 
   void init_params(cudaStream_t st) override {
     for (TBlock& tb : tblocks_)
       for (TOp& op : tb.ops) {
+        if (op.kind == TOp::SE) {
+          check(pbdk::init_uniform(op.w, 1, op.cs, 1, 1, op.cout, op.cout, d_.seed_teacher, op.tensor,
+                                   kaiming(op.cout, 1.0f), st),
+                "init");
+          check(pbdk::init_uniform(op.bias, 0, op.cs, 1, 1, 1, 1, d_.seed_teacher, op.tensor + 1, 0.1f, st), "init");
+          check(pbdk::init_uniform(op.w2, 1, op.cout, 1, 1, op.cs, op.cs, d_.seed_teacher, op.tensor + 10,
+                                   kaiming(op.cs, 1.0f), st),
+                "init");
+          check(pbdk::init_uniform(op.b2, 0, op.cout, 1, 1, 1, 1, d_.seed_teacher, op.tensor + 11, 0.1f, st), "init");
+          continue;
+        }
         if (op.kind == TOp::STEM) {
           check(pbdk::init_uniform(op.w, 1, 32, 3, 3, 16, 3, d_.seed_teacher, op.tensor, kaiming(27, 1.0f), st), "init");
         } else if (op.kind == TOp::PW) {
@@ -296,6 +338,7 @@ class MbPartition final : public PartitionBase {
         throw BadArg("candidate out of range");
     for (int l = 0; l < n; ++l) sb.layers[static_cast<size_t>(l)].active = path[l];
     // inactive candidates carry no gradient (a DP allreduce then sums zeros)
+    FamScope fs(fam_);
     cuda(cudaMemset(grads_ + sb.base, 0, block_params(sb.k) * sizeof(float)), "memset");
     invalidate_graphs();
   }
@@ -441,12 +484,16 @@ class MbPartition final : public PartitionBase {
 
   void run_teacher_op(TOp& op, cudaStream_t st) {
     if (op.kind == TOp::STEM) {
-      check(pbdk::stem_fwd(op.in, op.w, op.bias, op.out, n_, S_, 1, st), "teacher stem");
+      check(pbdk::stem_fwd(op.in, op.w, op.bias, op.out, n_, S_, fam_.act, st), "teacher stem");
     } else if (op.kind == TOp::PW) {
       check(pbdk::fprop_run(op.plan, st), "teacher 1x1");
+    } else if (op.kind == TOp::SE) {
+      check(pbdk::se_apply(op.out, n_, op.hout * op.hout, op.cout, op.cs, op.w, op.bias, op.w2, op.b2, se_pool_,
+                           se_gate_, st),
+            "teacher squeeze-excite");
     } else {
       const pbdk::DwArgs a{n_, op.hin, op.hin, op.cout, op.k, op.stride, op.hout, op.hout};
-      check(pbdk::dw_fwd(a, op.in, op.wflip, op.bias, op.out, 1, st), "teacher dw");
+      check(pbdk::dw_fwd(a, op.in, op.wflip, op.bias, op.out, fam_.act, st), "teacher dw");
     }
   }
 
@@ -547,6 +594,7 @@ class MbPartition final : public PartitionBase {
 
     // ---- teacher program
     const bf16* prev = input_;
+    size_t se_elems = 0;
     for (int b = lo; b <= hi; ++b) {
       TBlock tb;
       int j = 0;
@@ -582,7 +630,7 @@ class MbPartition final : public PartitionBase {
           e.cin = m.cin;
           e.cout = E;
           e.hin = e.hout = hw;
-          e.epi = PBDK_EPI_BIAS_RELU6;
+          e.epi = fam_.act == 2 ? PBDK_EPI_BIAS_SWISH : PBDK_EPI_BIAS_RELU6;
           e.tensor = base + 10u * j++;
           e.in = x;
           e.out = act(rows_max(hw), E);
@@ -605,6 +653,22 @@ class MbPartition final : public PartitionBase {
         d.wflip = arena_.get<bf16>(static_cast<size_t>(E) * m.k * m.k * sizeof(bf16));
         d.bias = arena_.get<float>(E * sizeof(float));
         tb.ops.push_back(d);
+        if (const int cs = se_ch(m); cs > 0) {  // squeeze-excite in place on the depthwise output
+          TOp q{};
+          q.kind = TOp::SE;
+          q.cout = E;
+          q.cs = cs;
+          q.hin = q.hout = ho;
+          q.tensor = base + 10u * j;
+          j += 2;
+          q.out = d.out;
+          q.w = arena_.get<bf16>(static_cast<size_t>(cs) * E * sizeof(bf16));
+          q.bias = arena_.get<float>(cs * sizeof(float));
+          q.w2 = arena_.get<bf16>(static_cast<size_t>(E) * cs * sizeof(bf16));
+          q.b2 = arena_.get<float>(E * sizeof(float));
+          tb.ops.push_back(q);
+          se_elems = std::max(se_elems, static_cast<size_t>(N) * E);
+        }
         const bool res = m.stride == 1 && m.cin == m.cout;
         TOp pj{};
         pj.kind = TOp::PW;
@@ -626,6 +690,10 @@ class MbPartition final : public PartitionBase {
       tb.out = const_cast<bf16*>(x);
       prev = tb.out;
       tblocks_.push_back(std::move(tb));
+    }
+    if (se_elems > 0) {
+      se_pool_ = arena_.get<float>(se_elems * sizeof(float));
+      se_gate_ = arena_.get<float>(se_elems * sizeof(float));
     }
 
     // ---- student blocks
@@ -781,6 +849,9 @@ class MbPartition final : public PartitionBase {
       }
   }
 
+  const Family& fam_;
+  float* se_pool_ = nullptr;
+  float* se_gate_ = nullptr;
   int S_ = 224;
   bf16* input_ = nullptr;
   size_t input_bytes_ = 0;
@@ -801,32 +872,54 @@ class MbPartition final : public PartitionBase {
 
 PartitionBase* make_mb_partition(const pbdx_desc& d) { return new MbPartition(d); }
 
+// layout queries for the C-ABI
+int mb_layers(int model, int b) {
+  FamScope fs(family(model));
+  return student_layers(b);
+}
+int mb_cands(int model, int b, int l) {
+  FamScope fs(family(model));
+  return layer_cands(b, l);
+}
+size_t mb_offset(int model, int b, int l, int c, size_t* n) {
+  FamScope fs(family(model));
+  return cand_offset(b, l, c, n);
+}
+size_t mb_block_params(int model, int b) {
+  FamScope fs(family(model));
+  return block_params(b);
+}
+
 }  // namespace pbd::exec
 
 // ------------------------------------------------------------------ C ABI: supernet layout
+namespace {
+bool mb_model(int m) { return m == PBDX_MODEL_MBV2_PROXYLESS || m == PBDX_MODEL_EFFB0_PROXYLESS; }
+}  // namespace
+
 extern "C" {
 
-int pbdx_mb_layers(int block) {
-  if (block < 0 || block >= pbd::exec::kBlocks) return -1;
-  return pbd::exec::student_layers(block);
+int pbdx_mb_layers(int model, int block) {
+  if (!mb_model(model) || block < 0 || block >= pbd::exec::kBlocks) return -1;
+  return pbd::exec::mb_layers(model, block);
 }
 
-int pbdx_mb_candidates(int block, int layer) {
-  if (block < 0 || block >= pbd::exec::kBlocks || layer < 0 || layer >= pbd::exec::student_layers(block)) return -1;
-  return pbd::exec::layer_cands(block, layer);
+int pbdx_mb_candidates(int model, int block, int layer) {
+  if (pbdx_mb_layers(model, block) <= layer || layer < 0) return -1;
+  return pbd::exec::mb_cands(model, block, layer);
 }
 
-long pbdx_mb_candidate_offset(int block, int layer, int cand, long* count) {
-  if (pbdx_mb_candidates(block, layer) <= cand || cand < 0) return -1;
+long pbdx_mb_candidate_offset(int model, int block, int layer, int cand, long* count) {
+  if (pbdx_mb_candidates(model, block, layer) <= cand || cand < 0) return -1;
   size_t n = 0;
-  const size_t off = pbd::exec::cand_offset(block, layer, cand, &n);
+  const size_t off = pbd::exec::mb_offset(model, block, layer, cand, &n);
   if (count != nullptr) *count = static_cast<long>(n);
   return static_cast<long>(off);
 }
 
-long pbdx_mb_block_params(int block) {
-  if (block < 0 || block >= pbd::exec::kBlocks) return -1;
-  return static_cast<long>(pbd::exec::block_params(block));
+long pbdx_mb_block_params(int model, int block) {
+  if (!mb_model(model) || block < 0 || block >= pbd::exec::kBlocks) return -1;
+  return static_cast<long>(pbd::exec::mb_block_params(model, block));
 }
 
 }  // extern "C"

@@ -58,18 +58,19 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
 
 // Epilogue semantics (pbdk.h PBDK_EPI_*): y = act(aux_op(acc + bias, aux)), fp32, one bf16 rounding.
 struct EpiFlags {
-  bool bias, aux, add, mask0, mask6, relu, relu6;
+  bool bias, aux, add, mask0, mask6, relu, relu6, swish;
 };
 __host__ __device__ constexpr EpiFlags epi_flags(int e) {
   return EpiFlags{e == PBDK_EPI_BIAS || e == PBDK_EPI_BIAS_RELU || e == PBDK_EPI_BIAS_RES_RELU ||
-                      e == PBDK_EPI_BIAS_RELU6 || e == PBDK_EPI_BIAS_RES,
+                      e == PBDK_EPI_BIAS_RELU6 || e == PBDK_EPI_BIAS_RES || e == PBDK_EPI_BIAS_SWISH,
                   e == PBDK_EPI_BIAS_RES_RELU || e == PBDK_EPI_RELU_MASK || e == PBDK_EPI_BIAS_RES ||
                       e == PBDK_EPI_RELU6_MASK || e == PBDK_EPI_ADD,
                   e == PBDK_EPI_BIAS_RES_RELU || e == PBDK_EPI_BIAS_RES || e == PBDK_EPI_ADD,
                   e == PBDK_EPI_RELU_MASK,
                   e == PBDK_EPI_RELU6_MASK,
                   e == PBDK_EPI_BIAS_RELU || e == PBDK_EPI_BIAS_RES_RELU,
-                  e == PBDK_EPI_BIAS_RELU6};
+                  e == PBDK_EPI_BIAS_RELU6,
+                  e == PBDK_EPI_BIAS_SWISH};
 }
 __device__ __forceinline__ float epi_aux(const EpiFlags& f, float v, float r) {
   if (f.add) return v + r;
@@ -79,6 +80,7 @@ __device__ __forceinline__ float epi_aux(const EpiFlags& f, float v, float r) {
 __device__ __forceinline__ float epi_act(const EpiFlags& f, float v) {
   if (f.relu) return fmaxf(v, 0.f);
   if (f.relu6) return fminf(fmaxf(v, 0.f), 6.f);
+  if (f.swish) return v / (1.0f + expf(-v));
   return v;
 }
 
@@ -1231,7 +1233,7 @@ int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, c
                int epi, FpropPlan* plan) {
   ConvGeom g;
   if (!make_geom(d, &g) || !chan_ok(d.c) || d.k % 16 != 0 || d.k < 16) return PBDK_EINVAL;
-  if (epi < PBDK_EPI_STORE || epi > PBDK_EPI_ADD) return PBDK_EINVAL;
+  if (epi < PBDK_EPI_STORE || epi > PBDK_EPI_BIAS_SWISH) return PBDK_EINVAL;
   if (epi_flags(epi).bias && bias == nullptr) return PBDK_EINVAL;
   if (epi_flags(epi).aux && aux == nullptr) return PBDK_EINVAL;
   const int bkc = chan_block(d.c);

@@ -46,6 +46,12 @@ __device__ __forceinline__ void st8(__nv_bfloat16* p, const float (&f)[8]) {
 }
 
 __device__ __forceinline__ float relu6f(float z) { return fminf(fmaxf(z, 0.0f), 6.0f); }
+__device__ __forceinline__ float swishf(float z) { return z / (1.0f + expf(-z)); }
+__device__ __forceinline__ float sigmoidf(float z) { return 1.0f / (1.0f + expf(-z)); }
+// activation codes (mb_kernels.hpp): 0 none, 1 ReLU6, 2 swish
+__device__ __forceinline__ float act_fn(int act, float v) {
+  return act == 1 ? relu6f(v) : act == 2 ? swishf(v) : v;
+}
 
 int grid_for(long long work) {
   const long long b = (work + kT - 1) / kT;
@@ -116,7 +122,7 @@ __global__ void __launch_bounds__(kT) dw_fwd_kernel(const __nv_bfloat16* __restr
       for (int jj = 0; jj < 8; ++jj) {
         float v = acc[u][jj];
         if (bias != nullptr) v = v + bias[c0 + jj];
-        o[jj] = relu6 ? relu6f(v) : v;
+        o[jj] = act_fn(relu6, v);
       }
       st8(y + ((static_cast<size_t>(row) * Q) + q0 + u) * C + c0, o);
     }
@@ -293,10 +299,8 @@ __global__ void __launch_bounds__(kT) stem_fwd_kernel(const __nv_bfloat16* __res
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[j] = acc[j] + bias[g * 8 + j];
     }
-    if (relu6) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[j] = relu6f(acc[j]);
-    }
+    for (int j = 0; j < 8; ++j) acc[j] = act_fn(relu6, acc[j]);
     st8(y + static_cast<size_t>(pix) * 32 + g * 8, acc);
   }
 }
@@ -453,6 +457,82 @@ __global__ void loss_sum_kernel(const double* __restrict__ part, int n, double n
     double t = 0.0;
     for (int w = 0; w < kT / 32; ++w) t += sm[w];
     *loss = t / norm;
+  }
+}
+
+// ------------------------------------------------------------------ squeeze-excite (EfficientNet teacher)
+// pooled[n][c] = (sum_q y[n][q][c]) / hw: CTA per (n, 8-channel group window of 32 groups); threads
+// stride over q in double, fixed-order tree over the CTA.
+__global__ void __launch_bounds__(kT) se_pool_kernel(const __nv_bfloat16* __restrict__ y, int hw, int E,
+                                                     float* __restrict__ pooled) {
+  __shared__ double red[kT / 32][8];
+  const int n = blockIdx.x;
+  const int g = blockIdx.y;  // 8-channel group
+  const __nv_bfloat16* base = y + static_cast<size_t>(n) * hw * E + g * 8;
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int q = threadIdx.x; q < hw; q += kT) {
+    float f[8];
+    ld8(base + static_cast<size_t>(q) * E, f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] += f[j];
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    double v = acc[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][j] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 8) {
+    double t = 0.0;
+    for (int w = 0; w < kT / 32; ++w) t += red[w][threadIdx.x];
+    pooled[static_cast<size_t>(n) * E + g * 8 + threadIdx.x] = static_cast<float>(t / hw);
+  }
+}
+
+// gate[n][c] = sigmoid(b2[c] + W2[c] . swish(b1 + W1 pooled[n])): one CTA per sample, fmaf order of
+// the oracle (c ascending for W1, j ascending for W2); bf16 weights, fp32 math.
+__global__ void __launch_bounds__(kT) se_fc_kernel(const float* __restrict__ pooled, const __nv_bfloat16* __restrict__ w1,
+                                                   const float* __restrict__ b1, const __nv_bfloat16* __restrict__ w2,
+                                                   const float* __restrict__ b2, int E, int cs,
+                                                   float* __restrict__ gate) {
+  extern __shared__ float sm[];  // pooled[E], h[cs]
+  float* pl = sm;
+  float* h = sm + E;
+  const int n = blockIdx.x;
+  for (int c = threadIdx.x; c < E; c += kT) pl[c] = pooled[static_cast<size_t>(n) * E + c];
+  __syncthreads();
+  for (int j = threadIdx.x; j < cs; j += kT) {
+    float acc = b1[j];
+    const __nv_bfloat16* wr = w1 + static_cast<size_t>(j) * E;
+    for (int c = 0; c < E; ++c) acc = fmaf(__bfloat162float(wr[c]), pl[c], acc);
+    h[j] = swishf(acc);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < E; c += kT) {
+    float acc = b2[c];
+    const __nv_bfloat16* wr = w2 + static_cast<size_t>(c) * cs;
+    for (int j = 0; j < cs; ++j) acc = fmaf(__bfloat162float(wr[j]), h[j], acc);
+    gate[static_cast<size_t>(n) * E + c] = sigmoidf(acc);
+  }
+}
+
+// y[n][q][c] = bf16(y * gate[n][c]) in place
+__global__ void __launch_bounds__(kT) se_scale_kernel(__nv_bfloat16* __restrict__ y, const float* __restrict__ gate,
+                                                      int hw, int E, int total) {
+  const int G = E / 8;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int g = i % G;
+    const int pix = i / G;
+    const int n = pix / hw;
+    float f[8];
+    __nv_bfloat16* p = y + static_cast<size_t>(pix) * E + g * 8;
+    ld8(p, f);
+    const float* gt = gate + static_cast<size_t>(n) * E + g * 8;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = f[j] * gt[j];
+    st8(p, f);
   }
 }
 
@@ -613,6 +693,17 @@ int bn_apply_act(const void* y, const float* mean_rstd, const float* gamma, cons
     bn_apply_act_kernel<0, true><<<g, kT, 0, s>>>(yy, mean_rstd, gamma, beta, rr, oo, static_cast<int>(m), c);
   else
     return PBDK_EINVAL;
+  return ok(cudaGetLastError());
+}
+
+int se_apply(void* y, int n, int hw, int E, int cs, const void* w1, const float* b1, const void* w2,
+             const float* b2, float* pooled, float* gate, cudaStream_t s) {
+  if (E % 8 != 0 || cs < 1 || n < 1 || static_cast<long long>(n) * hw * E >= (1LL << 31)) return PBDK_EINVAL;
+  se_pool_kernel<<<dim3(n, E / 8), kT, 0, s>>>(static_cast<const __nv_bfloat16*>(y), hw, E, pooled);
+  se_fc_kernel<<<n, kT, (E + cs) * sizeof(float), s>>>(pooled, static_cast<const __nv_bfloat16*>(w1), b1,
+                                                        static_cast<const __nv_bfloat16*>(w2), b2, E, cs, gate);
+  const int total = n * hw * (E / 8);
+  se_scale_kernel<<<grid_for(total), kT, 0, s>>>(static_cast<__nv_bfloat16*>(y), gate, hw, E, total);
   return ok(cudaGetLastError());
 }
 

@@ -14,7 +14,8 @@ struct DwArgs {
   int p, q;  // output
 };
 
-// y = [relu6](dw(x) [+ bias]); wt = flipped tap-major weights wt[r'][s'][c]
+// activation codes of dw_fwd / stem_fwd: 0 none, 1 ReLU6, 2 swish
+// y = act(dw(x) [+ bias]); wt = flipped tap-major weights wt[r'][s'][c]
 int dw_fwd(const DwArgs& d, const void* x, const void* wt, const float* bias, void* y, int relu6, cudaStream_t s);
 // dx = dw^T(dy) [masked by 0 < act < 6]
 int dw_dgrad(const DwArgs& d, const void* dy, const void* wt, const void* act, void* dx, cudaStream_t s);
@@ -26,6 +27,11 @@ int dw_wgrad(const DwArgs& d, const void* a, const void* dy, float* ws, size_t w
 int stem_fwd(const void* x, const void* w, const float* bias, void* y, int n, int S, int relu6, cudaStream_t s);
 size_t stem_wgrad_workspace_floats(int n, int S);
 int stem_wgrad(const void* x, const void* dy, int n, int S, float* ws, size_t ws_floats, float* dw, cudaStream_t s);
+
+// squeeze-excite (EfficientNet teacher) in place on y [n][hw][E]: gate = sigmoid(W2 swish(W1 mean_hw(y) + b1)
+// + b2), y *= gate.  w1 [cs][E], w2 [E][cs] bf16; pooled, gate: n*E floats of workspace each.
+int se_apply(void* y, int n, int hw, int E, int cs, const void* w1, const float* b1, const void* w2,
+             const float* b2, float* pooled, float* gate, cudaStream_t s);
 
 // out = bf16(act(fmaf(A, y, B)) [+ res]), A = gamma*rstd, B = fmaf(-A, mean, beta)
 int bn_apply_act(const void* y, const float* mean_rstd, const float* gamma, const float* beta, const void* res,

@@ -26,8 +26,8 @@ T_HW = (32, 32, 16, 8, 4)
 STUDENT_TENSORS = ("w1", "w2", "wsc", "g1", "b1", "g2", "b2", "gsc", "bsc")
 
 
-MODEL_RESNET_CIFAR, MODEL_MBV2_PROXYLESS = 0, 1
-MODELS = {"resnet": MODEL_RESNET_CIFAR, "mbv2": MODEL_MBV2_PROXYLESS}
+MODEL_RESNET_CIFAR, MODEL_MBV2_PROXYLESS, MODEL_EFFB0_PROXYLESS = 0, 1, 2
+MODELS = {"resnet": MODEL_RESNET_CIFAR, "mbv2": MODEL_MBV2_PROXYLESS, "effb0": MODEL_EFFB0_PROXYLESS}
 
 
 class PbdxDesc(ctypes.Structure):
@@ -73,11 +73,11 @@ def _bind(L):
     L.pbdx_ipc_open.argtypes = [ctypes.c_char_p, P(V)]
     L.pbdx_ipc_close.argtypes = [V]
     L.pbdx_set_path.argtypes = [V, I, P(I), I]
-    L.pbdx_mb_layers.argtypes = [I]
-    L.pbdx_mb_candidates.argtypes = [I, I]
-    L.pbdx_mb_candidate_offset.argtypes = [I, I, I, P(ctypes.c_long)]
+    L.pbdx_mb_layers.argtypes = [I, I]
+    L.pbdx_mb_candidates.argtypes = [I, I, I]
+    L.pbdx_mb_candidate_offset.argtypes = [I, I, I, I, P(ctypes.c_long)]
     L.pbdx_mb_candidate_offset.restype = ctypes.c_long
-    L.pbdx_mb_block_params.argtypes = [I]
+    L.pbdx_mb_block_params.argtypes = [I, I]
     L.pbdx_mb_block_params.restype = ctypes.c_long
     L._pbdx_bound = True
     return L
@@ -121,30 +121,30 @@ def stored_channels(c: int) -> int:
 
 
 # ---------------------------------------------------------------- MobileNetV2 -> ProxylessNAS geometry
-MB_CH = (3, 32, 32, 64, 128, 192, 320)
+MB_CH = {"mbv2": (3, 32, 32, 64, 128, 192, 320), "effb0": (3, 32, 64, 128, 128, 192, 320)}
 MB_DIV = (1, 4, 8, 16, 16, 32, 32)
 MB_BLOCKS = 6
 
 
-def mb_layers(block: int) -> int:
-    return int(lib().pbdx_mb_layers(block))
+def mb_layers(block: int, model: str = "mbv2") -> int:
+    return int(lib().pbdx_mb_layers(MODELS[model], block))
 
 
-def mb_candidates(block: int, layer: int) -> int:
-    return int(lib().pbdx_mb_candidates(block, layer))
+def mb_candidates(block: int, layer: int, model: str = "mbv2") -> int:
+    return int(lib().pbdx_mb_candidates(MODELS[model], block, layer))
 
 
-def mb_candidate_span(block: int, layer: int, cand: int) -> Tuple[int, int]:
+def mb_candidate_span(block: int, layer: int, cand: int, model: str = "mbv2") -> Tuple[int, int]:
     """(offset inside the block's flat supernet parameters, count) of one candidate."""
     n = ctypes.c_long()
-    off = lib().pbdx_mb_candidate_offset(block, layer, cand, ctypes.byref(n))
+    off = lib().pbdx_mb_candidate_offset(MODELS[model], block, layer, cand, ctypes.byref(n))
     if off < 0:
         raise ValueError("bad (block, layer, candidate)")
     return int(off), int(n.value)
 
 
-def mb_block_params(block: int) -> int:
-    return int(lib().pbdx_mb_block_params(block))
+def mb_block_params(block: int, model: str = "mbv2") -> int:
+    return int(lib().pbdx_mb_block_params(MODELS[model], block))
 
 
 class Partition:
@@ -173,7 +173,7 @@ class Partition:
             if model == "resnet":
                 lay, total = student_layout(k)
             else:
-                lay, total = {}, mb_block_params(k)
+                lay, total = {}, mb_block_params(k, model)
             self.layouts[k] = (off, lay, total)
             off += total
 
@@ -252,7 +252,7 @@ class Partition:
         if self.model == "resnet":
             return T_HW[boundary], T_HW[boundary], stored_channels(T_CH[boundary])
         hw = self.image // MB_DIV[boundary]
-        return hw, hw, 16 if boundary == 0 else MB_CH[boundary]
+        return hw, hw, 16 if boundary == 0 else MB_CH[self.model][boundary]
 
     # -- K11 peer relay (include/pbdx.h): device pointers of this rank's relay endpoints
     def row_bytes_in(self) -> int:
@@ -346,7 +346,7 @@ class Partition:
 
     def block_state_like(self, k: int) -> List[torch.Tensor]:
         """Receive buffers for any block's state (owned by this partition or not)."""
-        total = student_layout(k)[1] if self.model == "resnet" else mb_block_params(k)
+        total = student_layout(k)[1] if self.model == "resnet" else mb_block_params(k, self.model)
         return [torch.empty(total, dtype=torch.float32, device=self.device) for _ in range(2)]
 
     def set_block_state(self, k: int, weights: torch.Tensor, momentum: torch.Tensor):

@@ -10,10 +10,22 @@ from __future__ import annotations
 
 from typing import Dict, List, Sequence, Tuple
 
-CH = (3, 32, 32, 64, 128, 192, 320)
+FAMILIES = {
+    # channels per boundary, teacher MBConv layers per block, teacher kernel per block, squeeze-excite
+    "mbv2": ((3, 32, 32, 64, 128, 192, 320), (3, 3, 4, 3, 3, 1), (3, 3, 3, 3, 3, 3), False),
+    "effb0": ((3, 32, 64, 128, 128, 192, 320), (3, 2, 3, 3, 4, 1), (3, 5, 3, 5, 5, 3), True),
+}
+CH, NL, KT, SE = FAMILIES["mbv2"]
 DIV = (1, 4, 8, 16, 16, 32, 32)
-NL = (3, 3, 4, 3, 3, 1)
 KS, ES = (3, 5, 7), (3, 6)
+
+
+def set_family(model: str):
+    """Select the teacher family the helpers below describe ("mbv2" | "effb0")."""
+    global CH, NL, KT, SE
+    CH, NL, KT, SE = FAMILIES[model]
+
+
 BF, F4 = 2, 4
 
 
@@ -26,7 +38,8 @@ def teacher_layer(b: int, l: int) -> Tuple[int, int, int, int, int]:
         return ((1, 3, 32, 16, 1), (6, 3, 16, 32, 2), (6, 3, 32, 32, 1))[l]
     cin, cout = CH[b], CH[b + 1]
     s = DIV[b + 1] // DIV[b]
-    return (6, 3, cin, cout, s) if l == 0 else (6, 3, cout, cout, 1)
+    k = KT[b]
+    return (6, k, cin, cout, s) if l == 0 else (6, k, cout, cout, 1)
 
 
 def _mb(acc, n, hin, cin, E, k, stride, cout, res, expand, train, last):
@@ -91,9 +104,13 @@ def block_work(b: int, n: int, S: int, path: Sequence[int]) -> Tuple[float, floa
         else:
             c = int(path[sl])
             sk, se = KS[c % 3], ES[c // 3]
-        SE = cin if se == 1 else round_ch(cin * se)
-        hs = _mb(s, n, hs, cin, SE, sk, st, cout, res, se != 1, True, l == NL[b] - 1)
-        params += (SE * cin if se != 1 else 0) + SE * sk * sk + cout * SE + 4 * SE + 2 * cout
+        if SE:  # teacher squeeze-excite: pool (read), two tiny FCs, scale (read + write)
+            ho = (hw - 1) // 1 + 1
+            t[0] += 2.0 * n * 2 * E * max(1, cin // 4)
+            t[1] += 3 * n * ho * ho * E * BF
+        Es = cin if se == 1 else round_ch(cin * se)
+        hs = _mb(s, n, hs, cin, Es, sk, st, cout, res, se != 1, True, l == NL[b] - 1)
+        params += (Es * cin if se != 1 else 0) + Es * sk * sk + cout * Es + 4 * Es + 2 * cout
     # SGD over the active path: read w, v, g, write w, v, bf16 shadow
     s[1] += params * (5 * F4 + BF)
     return t[0], t[1], s[0], s[1], params
@@ -120,6 +137,9 @@ def teacher_param_bytes(b: int) -> int:
         tt, k, cin, cout, st = teacher_layer(b, l)
         E = cin if tt == 1 else round_ch(cin * tt)
         n += (E * cin + E if tt != 1 else 0) + E * k * k + E + cout * E + cout
+        if SE:
+            cs = max(1, cin // 4)
+            n += 2 * cs * E + cs + E
     return n * BF
 
 

@@ -347,8 +347,9 @@ def profile_blocks(global_batch: int, world: int, keys: Optional[List[int]] = No
     model "mbv2": the active single path `paths[k]` of the supernet is what is timed."""
     from . import executor, models, mb_models
     keys = keys or sorted({max(1, global_batch // d) for d in (16, 8, 4, 2, 1)})
-    nblocks = models.BLOCKS if model == "resnet" else mb_models.NL.__len__()
-    if model == "mbv2":
+    nblocks = models.BLOCKS if model == "resnet" else 6
+    if model != "resnet":
+        mb_models.set_family(model)
         image = image or 224
         paths = paths or mb_models.paths_for(0)
     blocks = []
@@ -357,7 +358,7 @@ def profile_blocks(global_batch: int, world: int, keys: Optional[List[int]] = No
         for n in keys:
             p = executor.Partition(k, k, n, max(n, global_batch), device=device, model=model, image=image)
             p.init_params()
-            if model == "mbv2":
+            if model != "resnet":
                 p.set_path(k, paths[k])
             p.set_timing(True)
             t_samples, s_samples = [], []
@@ -423,10 +424,13 @@ def bench_pipeline(args, rank: int, world: int, local_rank: int) -> dict:
         os.environ.setdefault("WORLD_SIZE", str(world))
         dist.init_process_group("nccl", device_id=dev)
     gb = args.batch * world
-    model = "mbv2" if getattr(args, "workload", "cifar") == "mbv2" else "resnet"
-    image = getattr(args, "image", 224) if model == "mbv2" else None
+    wl = getattr(args, "workload", "cifar")
+    model = wl if wl in ("mbv2", "effb0") else "resnet"
+    image = getattr(args, "image", 224) if model != "resnet" else None
     from . import mb_models
-    paths = mb_models.paths_for(0) if model == "mbv2" else None
+    if model != "resnet":
+        mb_models.set_family(model)
+    paths = mb_models.paths_for(0) if model != "resnet" else None
     # profile on rank 0's GPU, schedule on rank 0, broadcast the documents
     obj = [None, None]
     if rank == 0:
@@ -504,7 +508,8 @@ def bench_pipeline(args, rank: int, world: int, local_rank: int) -> dict:
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (Philox4x32-10 on device)",
             "config": {"workload": ("cifar-resnet18-teacher/slim-student 4 blocks (configs[1])" if model == "resnet"
-                                    else f"mbv2-teacher/proxyless-supernet 6 blocks {image}x{image} (configs[2])"),
+                                    else f"{model}-teacher/proxyless-supernet 6 blocks {image}x{image} "
+                                         f"({'configs[2]' if model == 'mbv2' else 'configs[3]'})"),
                        "global_batch": gb,
                        "parallelism": "ahd " + ";".join(f"{p['blocks']}x{len(p['devices'])}"
                                                         for p in sched["partitions"]),

@@ -4,7 +4,8 @@ step written with torch ops + autograd (PyTorch is the paper's framework, PAPER.
 float64 so the fixture is a clean reference for the oracle's fp32 mode.  Inputs (data, teacher and
 student weights, the sampled path) come from the oracle's Philox generators; everything computed
 here is torch's (F.conv2d with groups for depthwise, F.batch_norm in training mode, hardtanh as
-ReLU6, autograd).  Run from the repo root:  python tests/golden/make_golden_mb.py
+ReLU6, autograd).  Run from the repo root:  python tests/golden/make_golden_mb.py [0|1]   (1 = EfficientNet-B0 teacher:
+swish, squeeze-excite -> effb0_torch_fp64.npz)
 """
 import os
 import sys
@@ -18,7 +19,9 @@ sys.path.insert(0, ROOT)
 from oracle import mb  # noqa: E402
 
 torch.set_num_threads(8)
-OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "mb_torch_fp64.npz")
+FAMILY = int(sys.argv[1]) if len(sys.argv) > 1 else 0  # 0 MobileNetV2, 1 EfficientNet-B0 teacher
+OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                   "mb_torch_fp64.npz" if FAMILY == 0 else "effb0_torch_fp64.npz")
 B, S = 3, 64
 SUB = 53
 DRAW = 5  # path sampling index
@@ -37,6 +40,11 @@ def relu6(x):
     return F.hardtanh(x, 0.0, 6.0)
 
 
+def tact(x):
+    """the teacher's activation: ReLU6 (MobileNetV2) or swish = x * sigmoid(x) (EfficientNet-B0)"""
+    return x * torch.sigmoid(x) if FAMILY == 1 else relu6(x)
+
+
 def teacher_fwd(b, tp, x):
     p = torch.from_numpy(tp).to(DT)
     off = [0]
@@ -48,16 +56,25 @@ def teacher_fwd(b, tp, x):
 
     if b == 0:
         w = take(32 * 9 * 16).reshape(32, 3, 3, 16)[..., :3].permute(0, 3, 1, 2)
-        x = relu6(F.conv2d(x, w, take(32), stride=2, padding=1))
+        x = tact(F.conv2d(x, w, take(32), stride=2, padding=1))
     for l in range(mb.NL[b]):
         t, k, cin, cout, s = mb.teacher_layer(b, l)
         E = cin if t == 1 else mb.round_ch(cin * t)
         h = x
         if t != 1:
             w = take(E * cin).reshape(E, cin, 1, 1)
-            h = relu6(F.conv2d(h, w, take(E)))
+            h = tact(F.conv2d(h, w, take(E)))
         wd = take(E * k * k).reshape(E, 1, k, k)
-        h = relu6(F.conv2d(h, wd, take(E), stride=s, padding=k // 2, groups=E))
+        h = tact(F.conv2d(h, wd, take(E), stride=s, padding=k // 2, groups=E))
+        cs = mb.se_ch(cin)
+        if cs:  # squeeze-excite
+            w1, b1 = take(cs * E).reshape(cs, E), take(cs)
+            w2, b2 = take(E * cs).reshape(E, cs), take(E)
+            z = h.mean(dim=(2, 3))
+            z = z @ w1.T + b1
+            z = z * torch.sigmoid(z)
+            gate = torch.sigmoid(z @ w2.T + b2)
+            h = h * gate[:, :, None, None]
         wp = take(cout * E).reshape(cout, E, 1, 1)
         y = F.conv2d(h, wp, take(cout))
         x = y + x if (s == 1 and cin == cout) else y
@@ -97,6 +114,7 @@ def student(b, sp, path, x, t, norm):
 
 
 def main():
+    mb.set_family(FAMILY)
     out = {}
     x = mb.image(B, 0, S, bf16=False)
     acts = [x]

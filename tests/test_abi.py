@@ -100,10 +100,15 @@ def test_mb_supernet_layout_matches_oracle():
     """Host-only layout queries of the MBConv executor (pbdx_mb_*) == the oracle's layout."""
     from oracle import mb
     from paper_2301_12443_b200 import executor as ex
-    for b in range(6):
-        assert ex.mb_layers(b) == mb.layers(b)
-        assert ex.mb_block_params(b) == mb.student_param_count(b)
-        for l in range(mb.layers(b)):
-            assert ex.mb_candidates(b, l) == mb.candidates(b, l)
-            for c in range(mb.candidates(b, l)):
-                assert ex.mb_candidate_span(b, l, c) == mb.candidate_span(b, l, c)
+    for fam, model in ((0, "mbv2"), (1, "effb0")):
+        mb.set_family(fam)
+        try:
+            for b in range(6):
+                assert ex.mb_layers(b, model) == mb.layers(b)
+                assert ex.mb_block_params(b, model) == mb.student_param_count(b)
+                for l in range(mb.layers(b)):
+                    assert ex.mb_candidates(b, l, model) == mb.candidates(b, l)
+                    for c in range(mb.candidates(b, l)):
+                        assert ex.mb_candidate_span(b, l, c, model) == mb.candidate_span(b, l, c)
+        finally:
+            mb.set_family(0)

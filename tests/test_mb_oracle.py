@@ -5,7 +5,7 @@ layout, determinism across thread counts, single-path sparsity of gradients and 
 Tolerances: the oracle runs fp32 (bf16 off) against a float64 reference at S=64 (blocks 4-5 at
 2x2 pixels, m = 12 BN samples); teacher outputs 1e-5 relative L2 / 1e-4 per element of the output
 scale; losses 1e-5 relative; gradient tensors: norm 5e-3 relative (an fp32-vs-fp64 flip of a ReLU6 mask element moves
-the expand-layer gradients by ~3e-3), subsampled elements 1e-2
+the expand-layer gradients by ~3e-3), subsampled elements 2e-2
 relative L2 (a few elements sit on BN-backward cancellations); gradients that cancel to < 1e-4 of
 the block's gradient scale (gamma behind a following BN) to 1e-5 of that scale."""
 import os
@@ -15,17 +15,26 @@ import pytest
 
 from oracle import mb
 
-GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "mb_torch_fp64.npz")
+GOLD = {0: os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "mb_torch_fp64.npz"),
+        1: os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "effb0_torch_fp64.npz")}
 B, S, SUB, DRAW = 3, 64, 53, 5
 
 
-@pytest.fixture(scope="module")
-def gold():
-    return np.load(GOLD)
+@pytest.fixture(scope="module", params=[0, 1], ids=["mbv2", "effb0"])
+def family(request):
+    """teacher family: MobileNetV2 (configs[2]) / EfficientNet-B0 with swish + squeeze-excite (configs[3])"""
+    mb.set_family(request.param)
+    yield request.param
+    mb.set_family(0)
 
 
 @pytest.fixture(scope="module")
-def chain():
+def gold(family):
+    return np.load(GOLD[family])
+
+
+@pytest.fixture(scope="module")
+def chain(family):
     x = mb.image(B, 0, S, bf16=False)
     acts = [x]
     for b in range(mb.BLOCKS):
@@ -66,7 +75,7 @@ def test_student_matches_torch(gold, chain):
                 sub = v.reshape(-1)[::SUB] if v.size > 64 else v
                 ref = gold[f"s{b}_l{l}_{name}"]
                 err = np.linalg.norm(sub - ref) / np.linalg.norm(ref)
-                assert err <= 1e-2, (b, l, name, err)
+                assert err <= 2e-2, (b, l, name, err)
 
 
 def test_gradients_only_on_active_path_and_sgd_touches_only_it():
