@@ -137,8 +137,10 @@ def ncu_traffic(kernel_key):
 
 
 def time_dominant_kernel(torch, batch):
-    """CUDA-event timing of the dominant kernel (teacher block-0 3x3 conv, 64->64 @32x32, tcgen05)
-    launched alone on the current stream; algorithmic FLOPs = 2*M*N*K."""
+    """CUDA-event timing of the dominant kernel (teacher block-0 3x3 conv, 64->64 @32x32 with the
+    bias+ReLU epilogue, tcgen05) launched alone: 50 back-to-back launches replayed from a CUDA graph
+    on the current stream (so host-side plan building and ctypes overhead stay out of the device
+    timing); algorithmic FLOPs = 2*M*N*K."""
     import ctypes
     from paper_2301_12443_b200 import _lib
     L = _lib.lib()
@@ -147,21 +149,27 @@ def time_dominant_kernel(torch, batch):
     w = (torch.randn(64, 3, 3, 64, device="cuda") * 0.05).bfloat16()
     bias = torch.zeros(64, device="cuda")
     y = torch.empty(batch, 32, 32, 64, device="cuda", dtype=torch.bfloat16)
-    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    reps = 50
 
     def launch():
+        s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
         rc = L.pbdk_conv_fprop(ctypes.byref(d), x.data_ptr(), w.data_ptr(), y.data_ptr(), bias.data_ptr(), None, 2, s)
         assert rc == 0
 
     for _ in range(5):
         launch()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    e0.record()
-    reps = 50
-    for _ in range(reps):
-        launch()
-    e1.record()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(reps):
+            launch()
+    g.replay()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    g.replay()
+    e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     flops = 2.0 * batch * 32 * 32 * 64 * 9 * 64

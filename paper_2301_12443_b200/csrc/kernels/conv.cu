@@ -829,6 +829,173 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ------------------------------------------------------------------ fprop, two M tiles per filter load
+// Non-resident filters (128..512-channel 3x3 convs) make the implicit GEMM L2-throughput bound: the
+// chip-wide TMA/L2 ingest (~6300 B/clk, B300_MICROARCH.md "TMA chip-throughput") is reached long
+// before the tensor pipe, and half of the bytes are the filter tile re-streamed for every M tile.
+// Here each work item is a PAIR of M tiles with the same N tile: every stage carries A0, A1 and one
+// B box, the MMA issuer runs both 128 x BN x 16 MMAs off the same B descriptor into two TMEM
+// accumulators, so B bytes per FLOP halve.  Four accumulators (2 tiles x double buffer) = 4 x BN
+// TMEM columns, hence BN <= 128.
+template <int BN, int BKC>
+struct FpropM2Cfg {
+  static constexpr int SW = BKC * 2;
+  static constexpr int LAYOUT = layout_for_sw(SW);
+  static constexpr int A_BYTES = 128 * SW;
+  static constexpr int B_BYTES = BN * SW;
+  static constexpr int STAGE = round_up(2 * A_BYTES + B_BYTES, 1024);
+  static constexpr int STAGES = (kFpropBudget / STAGE) > 8 ? 8 : (kFpropBudget / STAGE);
+  static constexpr int ACC_COLS = BN < 32 ? 32 : BN;
+  static constexpr int TMEM_COLS = tmem_cols_for(4 * ACC_COLS);
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+  static_assert(4 * ACC_COLS <= 512, "two double-buffered accumulators must fit TMEM");
+};
+
+template <int BN, int BKC>
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_fprop_m2_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
+                         const FpropArgs a) {
+  using C = FpropM2Cfg<BN, BKC>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;         // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int num_kb = a.r * a.s * a.c_chunks;
+  const int m_pairs = (a.m_tiles + 1) / 2;
+  const int total = m_pairs * a.n_tiles;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmx);
+    tma_prefetch(&tmw);
+    for (int i = 0; i < C::STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int cin_stored = a.c_chunks * BKC;
+      int it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int mp = t / a.n_tiles;
+        const int k0 = (t - mp * a.n_tiles) * BN;
+        const int nval = (2 * mp + 1 < a.m_tiles) ? 2 : 1;
+        int ow0[2], oh0[2], n0[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int m_tile = 2 * mp + u;
+          const int tq = m_tile % a.tiles_q;
+          const int t2 = m_tile / a.tiles_q;
+          ow0[u] = tq * a.bw;
+          oh0[u] = (t2 % a.tiles_p) * a.bh;
+          n0[u] = (t2 / a.tiles_p) * a.bn;
+        }
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int st = it % C::STAGES;
+          if (it >= C::STAGES) mbar_wait(&empty[st], ((it / C::STAGES) - 1) & 1);
+          const int tap = kb / a.c_chunks;
+          const int cc = kb - tap * a.c_chunks;
+          const int rr = tap / a.s;
+          const int ss = tap - rr * a.s;
+          uint8_t* sa = smem + st * C::STAGE;
+          mbar_arrive_expect_tx(&full[st], nval * C::A_BYTES + C::B_BYTES);
+          for (int u = 0; u < nval; ++u)
+            tma_load_4d(sa + u * C::A_BYTES, &tmx, &full[st], cc * BKC, ow0[u] * a.stride + ss - a.pad,
+                        oh0[u] * a.stride + rr - a.pad, n0[u]);
+          tma_load_2d(sa + 2 * C::A_BYTES, &tmw, &full[st], tap * cin_stored + cc * BKC, k0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(128, BN, 0, 0);
+      int it = 0, lt = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+        const int mp = t / a.n_tiles;
+        const int nval = (2 * mp + 1 < a.m_tiles) ? 2 : 1;
+        const int acc = lt & 1;
+        if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t d0 = tmem + static_cast<uint32_t>(acc * 2 * C::ACC_COLS);
+        const uint32_t d1 = d0 + static_cast<uint32_t>(C::ACC_COLS);
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int st = it % C::STAGES;
+          mbar_wait(&full[st], (it / C::STAGES) & 1);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + st * C::STAGE);
+          const uint64_t a0 = umma_smem_desc(sa, 16, 8 * C::SW, C::LAYOUT);
+          const uint64_t a1 = umma_smem_desc(sa + C::A_BYTES, 16, 8 * C::SW, C::LAYOUT);
+          const uint64_t b0 = umma_smem_desc(sa + 2 * C::A_BYTES, 16, 8 * C::SW, C::LAYOUT);
+#pragma unroll
+          for (int kk = 0; kk < BKC / 16; ++kk) {
+            const uint32_t accum = (kb | kk) != 0 ? 1u : 0u;
+            umma_bf16(d0, a0 + 2 * kk, b0 + 2 * kk, idesc, accum);
+            if (nval == 2) umma_bf16(d1, a1 + 2 * kk, b0 + 2 * kk, idesc, accum);
+          }
+          umma_commit(&empty[st]);
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    int lt = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+      const int acc = lt & 1;
+      mbar_wait(&tfull[acc], (lt >> 1) & 1);
+      tc_fence_after();
+      const int mp = t / a.n_tiles;
+      const int k0 = (t - mp * a.n_tiles) * BN;
+      const int nval = (2 * mp + 1 < a.m_tiles) ? 2 : 1;
+      for (int u = 0; u < nval; ++u) {
+        const int m_tile = 2 * mp + u;
+        const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16) +
+                              static_cast<uint32_t>((acc * 2 + u) * C::ACC_COLS);
+        const int tq = m_tile % a.tiles_q;
+        const int t2 = m_tile / a.tiles_q;
+        const TileRows rows{&a, (t2 / a.tiles_p) * a.bn, (t2 % a.tiles_p) * a.bh, tq * a.bw};
+        fprop_epilogue<BN>(a, trow, quarter * 32 + lane, k0, rows);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+template <int BN, int BKC>
+cudaError_t launch_fprop_m2(const FpropPlan& p, cudaStream_t stream) {
+  using C = FpropM2Cfg<BN, BKC>;
+  if (stream == reinterpret_cast<cudaStream_t>(-1)) {
+    return cudaFuncSetAttribute(conv_fprop_m2_kernel<BN, BKC>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  }
+  conv_fprop_m2_kernel<BN, BKC><<<p.grid, kThreads, C::SMEM, stream>>>(p.tmx, p.tmw, p.args);
+  return cudaGetLastError();
+}
+
 template <int BN, int BKC, int WP>
 cudaError_t launch_fprop_halo(const FpropPlan& p, cudaStream_t stream) {
   using C = HaloCfg<BN, BKC, WP>;
@@ -998,27 +1165,48 @@ cudaError_t launch_wgrad(const WgradPlan& p, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
-// Fixed-order split reduction: dw[i] = sum_s ws[s][i]  (deterministic).
-__global__ void split_reduce_kernel(const float4* __restrict__ ws, float4* __restrict__ dw, size_t n4, int splits) {
-  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
-    float4 acc = ws[i];
-    int s = 1;
-    for (; s + 3 < splits; s += 4) {  // 4 loads in flight, added in split order
-      const float4 v0 = ws[s * n4 + i];
-      const float4 v1 = ws[(s + 1) * n4 + i];
-      const float4 v2 = ws[(s + 2) * n4 + i];
-      const float4 v3 = ws[(s + 3) * n4 + i];
-      acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
-      acc.x += v1.x; acc.y += v1.y; acc.z += v1.z; acc.w += v1.w;
-      acc.x += v2.x; acc.y += v2.y; acc.z += v2.z; acc.w += v2.w;
-      acc.x += v3.x; acc.y += v3.y; acc.z += v3.z; acc.w += v3.w;
+// Fixed-order split reduction: dw[i] = sum_s ws[s][i]  (deterministic).  CTA = 32 float4 lanes x 8
+// split lanes: split lane l adds splits l, l+8, ... in order, then the 8 partial sums are added in
+// lane order through shared memory — every split slab is read by 8x more threads in flight than a
+// serial walk, which matters for the small slabs of the early blocks (up to 148 splits).
+constexpr int kRedLanes = 32, kRedSplitLanes = 8;
+__global__ void __launch_bounds__(kRedLanes * kRedSplitLanes)
+    split_reduce_kernel(const float4* __restrict__ ws, float4* __restrict__ dw, size_t n4, int splits) {
+  __shared__ float4 part[kRedSplitLanes][kRedLanes];
+  const int e = threadIdx.x % kRedLanes;
+  const int sl = threadIdx.x / kRedLanes;
+  for (size_t base = static_cast<size_t>(blockIdx.x) * kRedLanes; base < n4;
+       base += static_cast<size_t>(gridDim.x) * kRedLanes) {
+    const size_t i = base + e;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i < n4) {
+      int s = sl;
+      for (; s + 3 * kRedSplitLanes < splits; s += 4 * kRedSplitLanes) {  // 4 loads in flight, in order
+        const float4 v0 = ws[s * n4 + i];
+        const float4 v1 = ws[(s + kRedSplitLanes) * n4 + i];
+        const float4 v2 = ws[(s + 2 * kRedSplitLanes) * n4 + i];
+        const float4 v3 = ws[(s + 3 * kRedSplitLanes) * n4 + i];
+        acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
+        acc.x += v1.x; acc.y += v1.y; acc.z += v1.z; acc.w += v1.w;
+        acc.x += v2.x; acc.y += v2.y; acc.z += v2.z; acc.w += v2.w;
+        acc.x += v3.x; acc.y += v3.y; acc.z += v3.z; acc.w += v3.w;
+      }
+      for (; s < splits; s += kRedSplitLanes) {
+        const float4 v = ws[s * n4 + i];
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
     }
-    for (; s < splits; ++s) {
-      const float4 v = ws[s * n4 + i];
-      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    part[sl][e] = acc;
+    __syncthreads();
+    if (sl == 0 && i < n4) {
+      float4 t = part[0][e];
+      for (int l = 1; l < kRedSplitLanes; ++l) {
+        const float4 v = part[l][e];
+        t.x += v.x; t.y += v.y; t.z += v.z; t.w += v.w;
+      }
+      dw[i] = t;
     }
-    dw[i] = acc;
+    __syncthreads();
   }
 }
 
@@ -1168,6 +1356,7 @@ struct FpropChoice {
   int bn;
   int splits;
   bool pair;  // 2-CTA (cta_group::2) tiles of 256 x bn
+  bool m2 = false;  // two M tiles per filter load (conv_fprop_m2_kernel)
 };
 
 constexpr double kIngress = 100.0;  // L2 -> smem bytes per SM clock with ~192 KB of loads in flight
@@ -1227,6 +1416,26 @@ FpropChoice choose_fprop(const pbdk_conv_desc& d, const ConvGeom& g, int bkc) {
   return best;
 }
 
+// Pairing halves the re-streamed filter bytes but leaves half as many work items to spread over the
+// SMs; take it when the chip-wide L2 ingest (not the wave count) bounds the persistent kernel:
+// compare max(items/SMs rounds x MMA, bytes / chip ingest) of both variants.
+constexpr double kChipIngest = 6300.0;  // B/clk, whole chip (B300_MICROARCH.md TMA chip-throughput)
+
+bool m2_auto(const pbdk_conv_desc& d, const ConvGeom& g, int bn) {
+  const int bkc = 64;
+  const int num_kb = d.r * d.s * (d.c / bkc);
+  const int sms = num_sms();
+  const double mma = (bkc / 16) * (bn == 64 ? 48.0 : 64.0);
+  const double a_b = 128.0 * bkc * 2, b_b = static_cast<double>(bn) * bkc * 2;
+  const int n_tiles = d.k / bn;
+  const int tiles = g.m_tiles * n_tiles;
+  const int items = (g.m_tiles + 1) / 2 * n_tiles;
+  const double t1 = std::max(((tiles + sms - 1) / sms) * num_kb * mma, tiles * num_kb * (a_b + b_b) / kChipIngest);
+  const double t2 = std::max(((items + sms - 1) / sms) * num_kb * 2 * mma,
+                             items * num_kb * (2 * a_b + b_b) / kChipIngest);
+  return t2 < 0.95 * t1;
+}
+
 }  // namespace
 
 int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, const float* bias, const void* aux,
@@ -1237,11 +1446,24 @@ int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, c
   if (epi_flags(epi).bias && bias == nullptr) return PBDK_EINVAL;
   if (epi_flags(epi).aux && aux == nullptr) return PBDK_EINVAL;
   const int bkc = chan_block(d.c);
-  const FpropChoice ch = choose_fprop(d, g, bkc);
+  FpropChoice ch = choose_fprop(d, g, bkc);
+  {
+    static const int m2_mode = [] {
+      const char* e = std::getenv("PBDK_M2");  // 0 off, 1 auto (default), 2 force where legal
+      return e != nullptr ? std::atoi(e) : 1;
+    }();
+    const bool legal = ch.splits == 1 && !ch.pair && (ch.bn == 64 || ch.bn == 128) && bkc == 64 &&
+                       g.m_tiles >= 2 && !fprop_bres(d, ch.bn, bkc) && d.r * d.s > 1;
+    // measured (scripts/time_conv.py): a win when the pairs still fill every SM (128->128 @16x16:
+    // 24.4 -> 21.9 us), a loss on the small-M strided / 4x4 convs
+    const int items = (g.m_tiles + 1) / 2 * (d.k / ch.bn);
+    if (legal && m2_mode == 2) ch.m2 = true;
+    if (legal && m2_mode == 1) ch.m2 = items >= num_sms() && m2_auto(d, g, ch.bn);
+  }
   const int bn = ch.bn;
   const int splits = ch.splits;
   const bool pair = ch.pair;
-  const bool bres = !pair && fprop_bres(d, bn, bkc);
+  const bool bres = !pair && !ch.m2 && fprop_bres(d, bn, bkc);
   const bool halo = splits == 1 && !pair && halo_enabled() && bres && bn <= 128 && d.r == 3 && d.s == 3 && d.stride == 1 && d.pad == 1 &&
                     d.q + 2 == kHaloWP && d.w == d.q;
   FpropLauncher l = nullptr;
@@ -1261,6 +1483,7 @@ int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, c
       default: l = nullptr; break;
     }
   }
+  if (ch.m2) l = bn == 128 ? launch_fprop_m2<128, 64> : bn == 64 ? launch_fprop_m2<64, 64> : nullptr;
   if (l == nullptr) return PBDK_EINVAL;
   FpropArgs& a0 = plan->args;
   if (halo) {
@@ -1313,7 +1536,10 @@ int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, c
   a.n_tiles = d.k / bn;
   a.m_tiles = halo ? d.n * a.tiles_img : g.m_tiles;
   const int tiles = a.n_tiles * a.m_tiles;
-  if (pair) {
+  if (ch.m2) {
+    const int items = (a.m_tiles + 1) / 2 * a.n_tiles;
+    plan->grid = dim3(static_cast<unsigned>(std::min(items, num_sms())), 1, 1);
+  } else if (pair) {
     plan->grid = dim3(static_cast<unsigned>(2 * std::min(tiles / 2, num_sms() / 2)), 1, 1);
   } else if (splits > 1) {
     plan->grid = dim3(static_cast<unsigned>(splits), static_cast<unsigned>(tiles), 1);
@@ -1403,8 +1629,9 @@ int wgrad_run(const WgradPlan& plan, cudaStream_t stream) {
   if (plan.launch(plan, stream) != cudaSuccess) return PBDK_ECUDA;
   if (plan.splits > 1) {
     const size_t n4 = plan.slab / 4;
-    const int blocks = static_cast<int>(std::max<size_t>(1, std::min<size_t>((n4 + 127) / 128, 148 * 8)));
-    split_reduce_kernel<<<blocks, 128, 0, stream>>>(reinterpret_cast<const float4*>(plan.args.out),
+    const int blocks =
+        static_cast<int>(std::max<size_t>(1, std::min<size_t>((n4 + kRedLanes - 1) / kRedLanes, 148 * 8)));
+    split_reduce_kernel<<<blocks, kRedLanes * kRedSplitLanes, 0, stream>>>(reinterpret_cast<const float4*>(plan.args.out),
                                                     reinterpret_cast<float4*>(plan.dw), n4, plan.splits);
     if (cudaGetLastError() != cudaSuccess) return PBDK_ECUDA;
   }

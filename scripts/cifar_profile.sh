@@ -17,6 +17,6 @@ torch.cuda.synchronize()
 torch.cuda.nvtx.range_pop()
 PY
 ncu --nvtx --nvtx-include "step/" --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,launch__grid_size \
-  --clock-control none --csv --log-file gpurun_out/cifar_launches.csv python /tmp/cifar_one.py > gpurun_out/cifar_prof.log 2>&1
+  --clock-control none --cache-control ${CACHE:-all} --csv --log-file gpurun_out/cifar_launches${CACHE:+_$CACHE}.csv python /tmp/cifar_one.py > gpurun_out/cifar_prof.log 2>&1
 python scripts/phase_times.py 256 >> gpurun_out/cifar_prof.log 2>&1
 tail -3 gpurun_out/cifar_prof.log
