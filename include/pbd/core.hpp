@@ -287,5 +287,9 @@ SimReport simulate_baseline(const CostModel& model, const BaselinePlan& plan, co
 double steady_state_step_time(const SimReport& report);
 double validate_prediction(const SimReport& report, const ConfigCost& cost);
 std::string save_report(const SimReport& report);
+// Parse a save_report() document (simulated or measured) back into a SimReport.
+SimReport load_report(const std::string& text);
+// Per-device Gantt chart (SVG) of a report (the role of report.cpp:93-165 gantt_svg).
+std::string gantt(const SimReport& report, const std::string& title = "");
 
 }  // namespace pbd

@@ -14,6 +14,9 @@
  *   pbd_profile_drift        <- pbd::profile_drift       schedule.hpp:137
  *   pbd_exec_time            <- pbd::CostModel::exec_time cost_model.hpp:41
  *   pbd_synth_profile        <- pbd::synth_profile       profile.hpp:136 / pbd_cli.cpp profile-gen
+ *   pbd_report_steady_state  <- pbd::steady_state_step_time simulate.hpp:120 (on any report document)
+ *   pbd_validate_prediction  <- pbd::validate_prediction simulate.hpp:123 (measured report vs the plan)
+ *   pbd_gantt_svg            <- pbd::gantt_svg           report.hpp:44 (per-device Gantt chart)
  *
  * Return codes mirror the CLI exit codes (pbd_cli.cpp:29-32):
  *   0 ok, 1 ValidationError, 2 InfeasibleError, 3 IoError, 4 other.
@@ -60,6 +63,14 @@ int pbd_shard_range(int global_batch, int group_size, int rank, int* first_out, 
 
 /* mean wall ms of `reps` best_schedule searches (bench: host-side search cost) */
 int pbd_time_best_schedule(const char* profile_json, int reps, double* ms_out, char** err_out);
+
+/* Reports from real runs: steady-state step of a report document (simulated, or
+ * measured by runtime.measured_report), |steady - predicted| / predicted for a schedule on a profile,
+ * and an SVG Gantt chart of the report. */
+int pbd_report_steady_state(const char* report_json, double* out, char** err_out);
+int pbd_validate_prediction(const char* report_json, const char* profile_json, const char* schedule_json,
+                            double* out, char** err_out);
+int pbd_gantt_svg(const char* report_json, const char* title, char** svg_out, char** err_out);
 
 #ifdef __cplusplus
 }

@@ -103,6 +103,12 @@ int pbdx_refresh_shadows(void* handle, void* stream);
 /* Per-block CUDA-event timing of the last step (ms): teacher[k], student[k] for k in the range. */
 int pbdx_set_timing(void* handle, int enabled);
 int pbdx_block_times(void* handle, float* teacher_ms, float* student_ms);
+/* Measured timelines (the reference's SimReport, simulate.hpp:27-86, built from real runs): record a
+ * reference event on `stream`, then after a timed step read every block's teacher / student
+ * [start, end] relative to it (ms, per block in the range). */
+int pbdx_trace_mark(void* handle, void* stream);
+int pbdx_block_trace(void* handle, float* teacher_start, float* teacher_end, float* student_start,
+                     float* student_end);
 
 /* Supernet layout of the MBConv models (host-only queries, no device needed): student layers of a
  * block, candidates of a layer, a candidate's (offset, count) inside the block's flat parameters,

@@ -135,3 +135,36 @@ def time_best_schedule(profile: Doc, reps: int = 20) -> float:
     rc = _lib.lib().pbd_time_best_schedule(_text(profile), reps, ctypes.byref(ms), ctypes.byref(err))
     _check(rc, err)
     return ms.value
+
+
+# ---------------------------------------------------------------- reports of real runs
+def report_steady_state(report: Doc) -> float:
+    """steady_state_step_time (simulate.cpp:388-424) of any report document, simulated or measured."""
+    d, err = ctypes.c_double(), ctypes.c_void_p()
+    L = _lib.lib()
+    L.pbd_report_steady_state.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_void_p)]
+    rc = L.pbd_report_steady_state(_text(report), ctypes.byref(d), ctypes.byref(err))
+    _check(rc, err)
+    return d.value
+
+
+def validate_prediction(report: Doc, profile: Doc, schedule: Doc) -> float:
+    """|steady(report) - predicted step_ms| / predicted (simulate.cpp:426-429): how far a measured run is
+    from the plan the partitioner made on `profile`."""
+    d, err = ctypes.c_double(), ctypes.c_void_p()
+    L = _lib.lib()
+    L.pbd_validate_prediction.argtypes = [ctypes.c_char_p] * 3 + [ctypes.POINTER(ctypes.c_double),
+                                                                   ctypes.POINTER(ctypes.c_void_p)]
+    rc = L.pbd_validate_prediction(_text(report), _text(profile), _text(schedule), ctypes.byref(d), ctypes.byref(err))
+    _check(rc, err)
+    return d.value
+
+
+def gantt_svg(report: Doc, title: str = "") -> str:
+    out, err = ctypes.c_void_p(), ctypes.c_void_p()
+    L = _lib.lib()
+    L.pbd_gantt_svg.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p),
+                                ctypes.POINTER(ctypes.c_void_p)]
+    rc = L.pbd_gantt_svg(_text(report), title.encode(), ctypes.byref(out), ctypes.byref(err))
+    _check(rc, err)
+    return _lib.take_string(out)

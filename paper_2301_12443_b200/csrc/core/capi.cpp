@@ -194,4 +194,23 @@ int pbd_time_best_schedule(const char* profile_json, int reps, double* ms_out, c
   });
 }
 
+int pbd_report_steady_state(const char* report_json, double* out, char** err_out) {
+  return shielded(err_out, [&] { *out = pbd::steady_state_step_time(pbd::load_report(report_json)); });
+}
+
+int pbd_validate_prediction(const char* report_json, const char* profile_json, const char* schedule_json,
+                            double* out, char** err_out) {
+  return shielded(err_out, [&] {
+    const pbd::CostModel m(pbd::load_profile(profile_json));
+    const auto sched = pbd::load_schedule(schedule_json);
+    *out = pbd::validate_prediction(pbd::load_report(report_json), pbd::predicted_step_time(m, sched.first));
+  });
+}
+
+int pbd_gantt_svg(const char* report_json, const char* title, char** svg_out, char** err_out) {
+  return shielded(err_out, [&] {
+    *svg_out = heap_copy(pbd::gantt(pbd::load_report(report_json), title != nullptr ? title : ""));
+  });
+}
+
 }  // extern "C"

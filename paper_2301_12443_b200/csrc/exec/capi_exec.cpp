@@ -74,6 +74,10 @@ int pbdx_teacher_act(void* h, int block, void** ptr, size_t* bytes) {
 int pbdx_refresh_shadows(void* h, void* st) { return guard([&] { P(h)->refresh_shadows(S(st)); }); }
 int pbdx_set_timing(void* h, int enabled) { return guard([&] { P(h)->set_timing(enabled != 0); }); }
 int pbdx_block_times(void* h, float* t, float* s) { return guard([&] { P(h)->block_times(t, s); }); }
+int pbdx_trace_mark(void* h, void* st) { return guard([&] { P(h)->trace_mark(S(st)); }); }
+int pbdx_block_trace(void* h, float* t0, float* t1, float* s0, float* s1) {
+  return guard([&] { P(h)->block_trace(t0, t1, s0, s1); });
+}
 int pbdx_launches_per_step(void* h) { return P(h)->launches_per_step(); }
 int pbdx_relay_set_recv(void* h, int nsenders, void* const* remote_consumed_flags) {
   if (nsenders > 0 && remote_consumed_flags == nullptr) return PBDK_EINVAL;

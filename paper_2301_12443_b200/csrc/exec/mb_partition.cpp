@@ -246,8 +246,6 @@ class MbPartition final : public PartitionBase {
     }
     for (auto e : tdone_) cudaEventDestroy(e);
     if (fork_ != nullptr) cudaEventDestroy(fork_);
-    for (auto e : ev_t_) cudaEventDestroy(e);
-    for (auto e : ev_s_) cudaEventDestroy(e);
   }
 
   int nblocks() const override { return d_.block_hi - d_.block_lo + 1; }
@@ -395,26 +393,6 @@ class MbPartition final : public PartitionBase {
     for (SBlock& sb : sblocks_)
       for (SLayer& L : sb.layers)
         for (SCand& C : L.cands) refresh_derived(L, C, st);
-  }
-
-  void set_timing(bool on) override {
-    timing_ = on;
-    if (on && ev_t_.empty()) {
-      ev_t_.resize(2 * tblocks_.size());
-      ev_s_.resize(2 * sblocks_.size());
-      for (auto& e : ev_t_) cuda(cudaEventCreate(&e), "event create");
-      for (auto& e : ev_s_) cuda(cudaEventCreate(&e), "event create");
-    }
-  }
-
-  void block_times(float* tms, float* sms) override {
-    if (ev_t_.empty()) throw BadArg("timing not enabled");
-    for (size_t i = 0; i < tblocks_.size(); ++i) {
-      cuda(cudaEventSynchronize(ev_t_[2 * i + 1]), "event sync");
-      cuda(cudaEventElapsedTime(&tms[i], ev_t_[2 * i], ev_t_[2 * i + 1]), "elapsed");
-      cuda(cudaEventSynchronize(ev_s_[2 * i + 1]), "event sync");
-      cuda(cudaEventElapsedTime(&sms[i], ev_s_[2 * i], ev_s_[2 * i + 1]), "elapsed");
-    }
   }
 
   void buffer(int which, void** ptr, size_t* bytes) override {
@@ -864,7 +842,6 @@ class MbPartition final : public PartitionBase {
   double* losses_ = nullptr;
   long long* step_ = nullptr;
   std::vector<cudaEvent_t> tdone_;
-  std::vector<cudaEvent_t> ev_t_, ev_s_;
   cudaEvent_t fork_ = nullptr;
 };
 

@@ -70,6 +70,9 @@ class PartitionBase {
     if (relay_stream_ != nullptr) cudaStreamDestroy(relay_stream_);
     if (relay_fork_ != nullptr) cudaEventDestroy(relay_fork_);
     if (relay_done_ != nullptr) cudaEventDestroy(relay_done_);
+    for (auto e : ev_t_) cudaEventDestroy(e);
+    for (auto e : ev_s_) cudaEventDestroy(e);
+    if (trace_ref_ != nullptr) cudaEventDestroy(trace_ref_);
   }
 
   // ---- model hooks
@@ -85,8 +88,42 @@ class PartitionBase {
   virtual void refresh_shadows(cudaStream_t st) = 0;
   virtual void buffer(int which, void** ptr, size_t* bytes) = 0;
   virtual void teacher_act(int k, void** ptr, size_t* bytes) = 0;
-  virtual void set_timing(bool on) = 0;
-  virtual void block_times(float* tms, float* sms) = 0;
+  // Per-block CUDA-event timing (teacher block on the caller's stream, student block on its own).
+  void set_timing(bool on) {
+    timing_ = on;
+    if (on && ev_t_.empty()) {
+      ev_t_.resize(2 * static_cast<size_t>(nblocks()));
+      ev_s_.resize(2 * static_cast<size_t>(nblocks()));
+      for (auto& e : ev_t_) cuda(cudaEventCreate(&e), "event create");
+      for (auto& e : ev_s_) cuda(cudaEventCreate(&e), "event create");
+    }
+  }
+  void block_times(float* tms, float* sms) {
+    if (ev_t_.empty()) throw BadArg("timing not enabled");
+    for (int i = 0; i < nblocks(); ++i) {
+      cuda(cudaEventSynchronize(ev_t_[2 * i + 1]), "event sync");
+      cuda(cudaEventElapsedTime(&tms[i], ev_t_[2 * i], ev_t_[2 * i + 1]), "elapsed");
+      cuda(cudaEventSynchronize(ev_s_[2 * i + 1]), "event sync");
+      cuda(cudaEventElapsedTime(&sms[i], ev_s_[2 * i], ev_s_[2 * i + 1]), "elapsed");
+    }
+  }
+  // Measured timelines (SimReport of real runs, §8f): a reference event on the caller's stream, and
+  // every block's [start, end] of the last step relative to it (ms).
+  void trace_mark(cudaStream_t st) {
+    if (trace_ref_ == nullptr) cuda(cudaEventCreate(&trace_ref_), "event create");
+    cuda(cudaEventRecord(trace_ref_, st), "event");
+  }
+  void block_trace(float* t0, float* t1, float* s0, float* s1) {
+    if (ev_t_.empty() || trace_ref_ == nullptr) throw BadArg("timing / trace mark not enabled");
+    for (int i = 0; i < nblocks(); ++i) {
+      cuda(cudaEventSynchronize(ev_s_[2 * i + 1]), "event sync");
+      cuda(cudaEventSynchronize(ev_t_[2 * i + 1]), "event sync");
+      cuda(cudaEventElapsedTime(&t0[i], trace_ref_, ev_t_[2 * i]), "elapsed");
+      cuda(cudaEventElapsedTime(&t1[i], trace_ref_, ev_t_[2 * i + 1]), "elapsed");
+      cuda(cudaEventElapsedTime(&s0[i], trace_ref_, ev_s_[2 * i]), "elapsed");
+      cuda(cudaEventElapsedTime(&s1[i], trace_ref_, ev_s_[2 * i + 1]), "elapsed");
+    }
+  }
   virtual int body_launches_per_step() const = 0;
   virtual void set_path(int /*block*/, const int* /*path*/, int /*n*/) { throw BadArg("model has no search space"); }
   // relayed activation (teacher output of block_hi) and its bytes per sample
@@ -310,6 +347,8 @@ class PartitionBase {
   unsigned long long* mailbox_ = nullptr;
   unsigned long long* relay_seq_ = nullptr;
   unsigned int* relay_ticket_ = nullptr;
+  std::vector<cudaEvent_t> ev_t_, ev_s_;  // per block: {start, end} pairs
+  cudaEvent_t trace_ref_ = nullptr;
 
  private:
   bool graph_valid_ = false;

@@ -73,6 +73,8 @@ def _bind(L):
     L.pbdx_ipc_open.argtypes = [ctypes.c_char_p, P(V)]
     L.pbdx_ipc_close.argtypes = [V]
     L.pbdx_set_path.argtypes = [V, I, P(I), I]
+    L.pbdx_trace_mark.argtypes = [V, V]
+    L.pbdx_block_trace.argtypes = [V] + [P(ctypes.c_float)] * 4
     L.pbdx_mb_layers.argtypes = [I, I]
     L.pbdx_mb_candidates.argtypes = [I, I, I]
     L.pbdx_mb_candidate_offset.argtypes = [I, I, I, I, P(ctypes.c_long)]
@@ -331,6 +333,18 @@ class Partition:
         t, s = (ctypes.c_float * nb)(), (ctypes.c_float * nb)()
         _check(lib().pbdx_block_times(self.handle, t, s), "block_times")
         return list(t), list(s)
+
+    def trace_mark(self, stream=None):
+        """Reference event for block_trace (measured timelines)."""
+        _check(lib().pbdx_trace_mark(self.handle, self._stream(stream)), "trace_mark")
+
+    def block_trace(self):
+        """(teacher start, teacher end, student start, student end) per block of the last timed step,
+        ms relative to the last trace_mark."""
+        nb = len(self.blocks)
+        arrs = [(ctypes.c_float * nb)() for _ in range(4)]
+        _check(lib().pbdx_block_trace(self.handle, *arrs), "block_trace")
+        return tuple(list(a) for a in arrs)
 
     def launches_per_step(self) -> int:
         return int(lib().pbdx_launches_per_step(self.handle))

@@ -221,18 +221,27 @@ class PipeBD:
         else:
             fn()
 
-    def step(self):
+    def step(self, trace: Optional[Callable[[str], None]] = None):
+        """One step of Algorithm 1 on this rank.  trace(name) is called at the phase boundaries
+        ("start", "teacher", "student", "share", "barrier", "update") for measured timelines."""
+        tr = trace or (lambda name: None)
+        tr("start")
         self._recv_input()
         self._finish_sends()  # the previous step's send must drain before t_hi is overwritten
         self._phase(0, self.stage.teacher_forward)
+        tr("teacher")
         self._send_output()
         self._phase(1, self.stage.student_step)
+        tr("student")
         g = self.groups.get(self.me.partition)
         if g is not None:
             dist.all_reduce(self.stage.grads(), op=dist.ReduceOp.SUM, group=g)
+        tr("share")
         if not self.dpu:
             dist.barrier()
+        tr("barrier")
         self._phase(2, self.stage.apply_update)
+        tr("update")
 
     def end_epoch(self):
         """Full synchronisation at the epoch boundary (simulate.cpp:263)."""
@@ -331,6 +340,110 @@ class PipeBD:
         if g is not None:
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=g)
         return {k: float(v) for k, v in zip(range(self.me.block_lo, self.me.block_hi + 1), t.tolist())}
+
+
+def measured_report(pipe: "PipeBD", steps: int) -> Optional[dict]:
+    """Measured timelines of `steps` eager steps in the reference's report format (save_report,
+    simulate.cpp:431-465; categories simulate.hpp:32-42), one lane per rank on a common timebase
+    (each rank's zero is a CUDA event recorded right after a barrier).  Per step: data_load
+    (partition 0) or recv_wait (relay), teacher_fwd / student_fwd_bwd per block from the executor's
+    CUDA events (student blocks run on their own streams; the part overlapping the teacher lane is
+    flagged `overlapped` and kept out of the category totals, as the reference does for overlapped
+    sends), grad_share (NCCL allreduce), barrier_wait, weight_update.  Returns the document on rank 0
+    (None elsewhere); feed it to core.report_steady_state / core.validate_prediction / core.gantt_svg."""
+    stage = pipe.stage
+    dev = stage.device
+    stream = torch.cuda.current_stream(dev)
+    stage.set_timing(True)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    zero = torch.cuda.Event(enable_timing=True)
+    zero.record(stream)
+    lane = []
+    lo = pipe.me.block_lo
+    for s in range(steps):
+        marks = {}
+
+        def tr(name, marks=marks):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            marks[name] = e
+            if name == "start":
+                stage.trace_mark(stream)
+
+        pipe.step(trace=tr)
+        torch.cuda.synchronize(dev)
+        base = zero.elapsed_time(marks["start"])
+        t = {k: zero.elapsed_time(e) for k, e in marks.items()}
+        t0, t1, s0, s1 = stage.block_trace()
+        first_teacher = base + t0[0]
+        lane.append(("data_load" if lo == 0 else "recv_wait", None, t["start"], first_teacher, s, False))
+        for i, k in enumerate(stage.blocks):
+            lane.append(("teacher_fwd", k, base + t0[i], base + t1[i], s, False))
+        teacher_end = base + t1[-1]
+        for i, k in enumerate(stage.blocks):
+            a, b = base + s0[i], base + s1[i]
+            if a < teacher_end:  # concurrent with the teacher lane: its own stream
+                lane.append(("student_fwd_bwd", k, a, b, s, True))
+            else:
+                lane.append(("student_fwd_bwd", k, a, b, s, False))
+        lane.append(("grad_share", None, t["student"], t["share"], s, False))
+        lane.append(("barrier_wait", None, t["share"], t["barrier"], s, False))
+        lane.append(("weight_update", None, t["barrier"], t["update"], s, False))
+    stage.set_timing(False)
+    # serialise the lane: non-overlapped events tile it (student tails past the teacher extend it),
+    # gaps become idle
+    events = []
+    busy_end = 0.0
+    seq = sorted([e for e in lane if not e[5] and e[3] > e[2]], key=lambda e: (e[2], e[3]))
+    for cat, blk, a, b, st, _ in seq:
+        a = max(a, busy_end)
+        if b <= a:
+            continue
+        if a > busy_end + 1e-6:
+            events.append({"category": "idle", "block": None, "start_ms": busy_end, "end_ms": a, "step": st,
+                           "epoch": 0, "overlapped": False})
+        events.append({"category": cat, "block": blk, "start_ms": a, "end_ms": b, "step": st, "epoch": 0,
+                       "overlapped": False})
+        busy_end = b
+    for cat, blk, a, b, st, ov in lane:
+        if ov:
+            events.append({"category": cat, "block": blk, "start_ms": a, "end_ms": b, "step": st, "epoch": 0,
+                           "overlapped": True})
+    events.sort(key=lambda e: (e["start_ms"], e["overlapped"]))
+    gathered = [None] * pipe.world
+    dist.all_gather_object(gathered, events)
+    if pipe.rank != 0:
+        return None
+    makespan = max((e["end_ms"] for ev in gathered for e in ev), default=0.0)
+    totals = {c: 0.0 for c in ("data_load", "teacher_fwd", "student_fwd_bwd", "send", "recv_wait", "grad_share",
+                               "weight_update", "barrier_wait", "idle")}
+    overlapped = 0.0
+    for ev in gathered:
+        for e in ev:
+            d = e["end_ms"] - e["start_ms"]
+            if e["overlapped"]:
+                overlapped += d
+            else:
+                totals[e["category"]] += d
+    # pad every lane with idle to the makespan (the reference's timelines are idle-filled)
+    for ev in gathered:
+        end = max((e["end_ms"] for e in ev if not e["overlapped"]), default=0.0)
+        if makespan > end + 1e-6:
+            ev.append({"category": "idle", "block": None, "start_ms": end, "end_ms": makespan, "step": steps - 1,
+                       "epoch": 0, "overlapped": False})
+            totals["idle"] += makespan - end
+    n = len(gathered)
+    bubble = (totals["idle"] + totals["recv_wait"] + totals["barrier_wait"]) / (makespan * n) if makespan else 0.0
+    rep = {"num_devices": n, "makespan_ms": makespan, "steady_state_step_ms": 0.0, "bubble_ratio": bubble,
+           "category_totals_ms": totals, "overlapped_send_ms": 0.0, "overlapped_compute_ms": overlapped,
+           "peak_mem_bytes": [0.0] * n,
+           "sim": {"steps_per_epoch": steps, "epochs": 1, "dpu": pipe.dpu, "overlap_send": True, "overlap_load": True,
+                   "epoch_sync_ms": 0.0, "weight_update_ms": 0.0},
+           "timelines": gathered, "measured": True}
+    if steps >= 4:
+        rep["steady_state_step_ms"] = core.report_steady_state(rep)
+    return rep
 
 
 def _dev_of(stage):

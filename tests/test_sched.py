@@ -288,3 +288,27 @@ def test_synth_profile_matches_reference():
         got = core.synth_profile(**spec)
         want = ref.synth_profile(**spec)
         assert json.dumps(got, sort_keys=True) == json.dumps(want, sort_keys=True)
+
+
+def test_report_roundtrip_steady_state_validation_and_gantt():
+    """§8f: reports of real runs — any save_report document (simulated here; measured ones come from
+    runtime.measured_report) parses back, yields the reference's steady-state step and prediction
+    error, and renders a per-device Gantt chart."""
+    from paper_2301_12443_b200 import core
+    prof = core.synth_profile(shape="front-heavy", blocks=6, front_weight=3.0, curvature=0.4, num_devices=4)
+    sched, _ = core.best_schedule(prof)
+    rep = core.simulate(prof, sched, {"steps_per_epoch": 8, "epochs": 1})
+    assert core.report_steady_state(rep) == rep["steady_state_step_ms"]
+    assert core.validate_prediction(rep, prof, sched) < 1e-12
+    # a "measured" run 10% slower than planned
+    slow = json.loads(json.dumps(rep))
+    for line in slow["timelines"]:
+        for e in line:
+            e["start_ms"] *= 1.1
+            e["end_ms"] *= 1.1
+    slow["makespan_ms"] *= 1.1
+    assert core.validate_prediction(slow, prof, sched) == pytest.approx(0.1, rel=1e-9)
+    svg = core.gantt_svg(rep, "plan")
+    assert svg.startswith("<svg") and svg.count("<rect") > 4 * 8 and "GPU 3" in svg
+    with pytest.raises(core.ValidationError):
+        core.report_steady_state({**rep, "sim": {**rep["sim"], "steps_per_epoch": 2}})
