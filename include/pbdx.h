@@ -103,6 +103,11 @@ int pbdx_refresh_shadows(void* handle, void* stream);
 /* Per-block CUDA-event timing of the last step (ms): teacher[k], student[k] for k in the range. */
 int pbdx_set_timing(void* handle, int enabled);
 int pbdx_block_times(void* handle, float* teacher_ms, float* student_ms);
+/* Student blocks that train (bit i = block block_lo + i; default all).  The paper's DP baseline
+ * trains blocks one after another, each step recomputing the teacher prefix:
+ * partition [0, k] with mask 1 << k.  Untrained blocks run only their teacher part. */
+int pbdx_set_train_mask(void* handle, unsigned int mask);
+
 /* Measured timelines (the reference's SimReport, simulate.hpp:27-86, built from real runs): record a
  * reference event on `stream`, then after a timed step read every block's teacher / student
  * [start, end] relative to it (ms, per block in the range). */

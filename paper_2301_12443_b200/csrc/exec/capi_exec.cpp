@@ -74,6 +74,7 @@ int pbdx_teacher_act(void* h, int block, void** ptr, size_t* bytes) {
 int pbdx_refresh_shadows(void* h, void* st) { return guard([&] { P(h)->refresh_shadows(S(st)); }); }
 int pbdx_set_timing(void* h, int enabled) { return guard([&] { P(h)->set_timing(enabled != 0); }); }
 int pbdx_block_times(void* h, float* t, float* s) { return guard([&] { P(h)->block_times(t, s); }); }
+int pbdx_set_train_mask(void* h, unsigned int mask) { return guard([&] { P(h)->set_train_mask(mask); }); }
 int pbdx_trace_mark(void* h, void* st) { return guard([&] { P(h)->trace_mark(S(st)); }); }
 int pbdx_block_trace(void* h, float* t0, float* t1, float* s0, float* s1) {
   return guard([&] { P(h)->block_trace(t0, t1, s0, s1); });

@@ -368,7 +368,7 @@ class MbPartition final : public PartitionBase {
       cudaStream_t st = sb.stream;
       cuda(cudaStreamWaitEvent(st, fork ? fork_ : tdone_[i], 0), "wait teacher");
       if (timing_) cuda(cudaEventRecord(ev_s_[2 * i], st), "event");
-      student_block(sb, i, st);
+      if (trains(static_cast<int>(i))) student_block(sb, i, st);
       if (timing_) cuda(cudaEventRecord(ev_s_[2 * i + 1], st), "event");
       cuda(cudaEventRecord(sb.done, st), "event");
     }
@@ -377,7 +377,9 @@ class MbPartition final : public PartitionBase {
 
   void update_body(cudaStream_t st) override {
     long long* counter = step_;
-    for (SBlock& sb : sblocks_)
+    for (size_t i = 0; i < sblocks_.size(); ++i) {
+      if (!trains(static_cast<int>(i))) continue;
+      SBlock& sb = sblocks_[i];
       for (SLayer& L : sb.layers) {
         SCand& C = L.cands[static_cast<size_t>(L.active)];
         check(pbdk::sgd_momentum(params_ + C.off, mom_ + C.off, grads_ + C.off, shadow_ + C.off, C.L.total, d_.lr,
@@ -386,6 +388,7 @@ class MbPartition final : public PartitionBase {
         counter = nullptr;  // advance the step counter once
         refresh_derived(L, C, st);
       }
+    }
   }
 
   void refresh_shadows(cudaStream_t st) override {
@@ -419,8 +422,9 @@ class MbPartition final : public PartitionBase {
   int body_launches_per_step() const override {
     int n = (d_.block_lo == 0 && !external_) ? 1 : 0;
     for (const TBlock& tb : tblocks_) n += static_cast<int>(tb.ops.size());
-    for (const SBlock& sb : sblocks_)
-      for (const SLayer& L : sb.layers) {
+    for (size_t bi = 0; bi < sblocks_.size(); ++bi) {
+      if (!trains(static_cast<int>(bi))) continue;
+      for (const SLayer& L : sblocks_[bi].layers) {
         const SCand& C = L.cands[static_cast<size_t>(L.active)];
         if (L.stem) {
           n += (1 + 2 + 1) + (3 + 2) + 1;  // conv, stats, apply | bn bwd, wgrad | sgd
@@ -432,6 +436,7 @@ class MbPartition final : public PartitionBase {
         n += e ? (1 + 3 + (C.w_exp.splits > 1 ? 2 : 1) + (L.need_dx ? 1 : 0)) : (L.need_dx ? 1 : 0);
         n += 1 + (e ? 2 : 1) + 1;                                                      // sgd, transposes, flip
       }
+    }
     return n;
   }
 

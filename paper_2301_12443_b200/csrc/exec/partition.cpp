@@ -206,6 +206,11 @@ class ResNetPartition final : public PartitionBase {
       cudaStream_t st = s.stream;
       cuda(cudaStreamWaitEvent(st, fork ? fork_ : tdone_[i], 0), "wait teacher");
       if (timing_) cuda(cudaEventRecord(ev_s_[2 * i], st), "event");
+      if (!trains(static_cast<int>(i))) {  // DP-baseline mode: this block only feeds the teacher prefix
+        if (timing_) cuda(cudaEventRecord(ev_s_[2 * i + 1], st), "event");
+        cuda(cudaEventRecord(s.done, st), "event");
+        continue;
+      }
       const float* p = params_ + s.base;
       float* g = grads_ + s.base;
       const int m = n_ * s.hout * s.hout;
@@ -240,8 +245,21 @@ class ResNetPartition final : public PartitionBase {
   }
 
   void update_body(cudaStream_t st) override {
-    check(pbdk::sgd_momentum(params_, mom_, grads_, shadow_, total_, d_.lr, d_.momentum, step_, st), "sgd");
-    refresh_flips(st);
+    if (all_train()) {
+      check(pbdk::sgd_momentum(params_, mom_, grads_, shadow_, total_, d_.lr, d_.momentum, step_, st), "sgd");
+      refresh_flips(st);
+      return;
+    }
+    long long* counter = step_;
+    for (size_t i = 0; i < sblocks_.size(); ++i) {
+      if (!trains(static_cast<int>(i))) continue;
+      const SBlock& s = sblocks_[i];
+      check(pbdk::sgd_momentum(params_ + s.base, mom_ + s.base, grads_ + s.base, shadow_ + s.base, s.lay.total,
+                               d_.lr, d_.momentum, counter, st),
+            "sgd");
+      counter = nullptr;
+      check(pbdk_weight_flip(shadow_ + s.base + s.lay.w2, s.w2flip, s.cout, 3, 3, s.mid, st), "flip");
+    }
   }
 
   void buffer(int which, void** ptr, size_t* bytes) override {
@@ -268,11 +286,15 @@ class ResNetPartition final : public PartitionBase {
   int body_launches_per_step() const override {
     int n = (d_.block_lo == 0 && !external_) ? 1 : 0;
     for (const TBlock& tb : tblocks_) n += static_cast<int>(tb.convs.size());
-    for (const SBlock& s : sblocks_) {
+    int trained = 0;
+    for (size_t i = 0; i < sblocks_.size(); ++i) {
+      if (!trains(static_cast<int>(i))) continue;
+      const SBlock& s = sblocks_[i];
+      ++trained;
       n += 3 + 3 + 2 + 3 + 1 + 3;  // convs, bn1 stats(2)+apply, bn2+bnsc stats(2), mse(3), dgrad, bn_bwd(3)
       n += (s.p_w2.splits > 1 ? 2 : 1) + (s.p_wsc.splits > 1 ? 2 : 1) + (s.p_w1.splits > 1 ? 2 : 1);
     }
-    n += 1 + static_cast<int>(sblocks_.size());  // sgd + flips
+    n += all_train() ? 1 + static_cast<int>(sblocks_.size()) : 2 * trained;  // sgd + flips
     return n;
   }
 

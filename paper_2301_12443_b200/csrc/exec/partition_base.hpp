@@ -276,6 +276,16 @@ class PartitionBase {
 
   const pbdx_desc& desc() const { return d_; }
 
+  // Which student blocks of the range train (bit i = block block_lo + i).  All by default; the DP
+  // baseline of the paper (blocks trained one after another, every step
+  // recomputing the teacher prefix) runs partition [0, k] with only block k training.
+  void set_train_mask(uint32_t mask) {
+    const uint32_t full = nblocks() >= 32 ? 0xFFFFFFFFu : ((1u << nblocks()) - 1u);
+    if ((mask & full) == 0) throw BadArg("train mask selects no block");
+    train_mask_ = mask & full;
+    invalidate_graphs();
+  }
+
  protected:
   void invalidate_graphs() { graph_valid_ = phases_valid_ = false; }
 
@@ -336,7 +346,11 @@ class PartitionBase {
     check(pbdk::relay_release(a, st), "relay release");
   }
 
+  bool trains(int i) const { return (train_mask_ >> i) & 1u; }
+  bool all_train() const { return train_mask_ == 0xFFFFFFFFu || train_mask_ == ((1u << nblocks()) - 1u); }
+
   pbdx_desc d_;
+  uint32_t train_mask_ = 0xFFFFFFFFu;
   int n_ = 0;
   int first_ = 0;
   bool external_ = false;

@@ -89,57 +89,85 @@ __device__ __forceinline__ float epi_act(const EpiFlags& f, float v) {
 // from registers.  No shared-memory staging on purpose: for N <= 128 the tensor core is
 // bound by its shared-memory read port (SS operands), so the epilogue must not compete
 // for it.  RowMap(r) -> (valid, output pixel index) of tile row r.
-template <int BN, class RowMap>
+// `wait` blocks until the tile's accumulator is complete (tfull barrier); the first column group's
+// aux / bias vectors are requested BEFORE it, so their latency hides behind the tile's last MMAs.
+struct NoWait {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+template <int BN, class RowMap, class Wait = NoWait>
 __device__ __forceinline__ void fprop_epilogue(const FpropArgs& a, uint32_t trow, int row, int k0,
-                                               const RowMap& rowmap) {
+                                               const RowMap& rowmap, const Wait& wait = Wait()) {
   bool valid;
   size_t m;
   rowmap(row, valid, m);
   const EpiFlags f = epi_flags(a.epi);
   const bool has_bias = f.bias;
-  if (a.debug == 3 || a.debug == 9) return;
+  if (a.debug == 3 || a.debug == 9) {
+    wait();
+    return;
+  }
+  // Columns in groups of up to 64: the group's aux (residual / mask) vectors are requested up front,
+  // so one global-load latency is paid per 64 columns instead of one per 16 (the epilogue of a
+  // N = 64 tile was latency-bound on them and fell behind the MMAs: 64->64 conv + residual
+  // 50 -> see DESIGN.md §6).
+  constexpr int GC = BN < 64 ? BN : 64;
+  const bool live = valid && a.debug != 1;
 #pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 16) {
-    float v[16];
-    tmem_ld16(trow + c0, v);
-    if (!valid || a.debug == 1) continue;
-    const int col = k0 + c0;
-    if (has_bias) {
-      const float4* b4 = reinterpret_cast<const float4*>(a.bias + col);
+  for (int g0 = 0; g0 < BN; g0 += GC) {
+    uint4 ra[GC / 8];
+    float4 rb[GC / 4];
+    if (f.aux && live) {
+      const uint4* r4 = reinterpret_cast<const uint4*>(a.aux + m * a.k + k0 + g0);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float4 b = __ldg(b4 + j);
-        v[4 * j + 0] += b.x;
-        v[4 * j + 1] += b.y;
-        v[4 * j + 2] += b.z;
-        v[4 * j + 3] += b.w;
-      }
+      for (int i = 0; i < GC / 8; ++i) ra[i] = __ldg(r4 + i);
     }
-    if (f.aux) {
-      const uint4* r4 = reinterpret_cast<const uint4*>(a.aux + m * a.k + col);
-      const uint4 ra = __ldg(r4);
-      const uint4 rb = __ldg(r4 + 1);
-      const uint32_t rw[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+    if (has_bias && live) {  // warp-uniform addresses: one broadcast wavefront per load
+      const float4* b4 = reinterpret_cast<const float4*>(a.bias + k0 + g0);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        v[2 * j] = epi_aux(f, v[2 * j], bf16_lo(rw[j]));
-        v[2 * j + 1] = epi_aux(f, v[2 * j + 1], bf16_hi(rw[j]));
-      }
+      for (int i = 0; i < GC / 4; ++i) rb[i] = __ldg(b4 + i);
     }
+    if (g0 == 0) wait();
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = epi_act(f, v[j]);
-    uint4 o0, o1;
-    o0.x = pack_bf16x2(v[0], v[1]);
-    o0.y = pack_bf16x2(v[2], v[3]);
-    o0.z = pack_bf16x2(v[4], v[5]);
-    o0.w = pack_bf16x2(v[6], v[7]);
-    o1.x = pack_bf16x2(v[8], v[9]);
-    o1.y = pack_bf16x2(v[10], v[11]);
-    o1.z = pack_bf16x2(v[12], v[13]);
-    o1.w = pack_bf16x2(v[14], v[15]);
-    uint4* dst = reinterpret_cast<uint4*>(a.y + m * a.k + col);
-    dst[0] = o0;
-    dst[1] = o1;
+    for (int c = 0; c < GC; c += 16) {
+      float v[16];
+      tmem_ld16(trow + g0 + c, v);
+      if (!live) continue;
+      const int col = k0 + g0 + c;
+      if (has_bias) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float4 b = rb[c / 4 + j];
+          v[4 * j + 0] += b.x;
+          v[4 * j + 1] += b.y;
+          v[4 * j + 2] += b.z;
+          v[4 * j + 3] += b.w;
+        }
+      }
+      if (f.aux) {
+        const uint4 r0 = ra[c / 8], r1 = ra[c / 8 + 1];
+        const uint32_t rw[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          v[2 * j] = epi_aux(f, v[2 * j], bf16_lo(rw[j]));
+          v[2 * j + 1] = epi_aux(f, v[2 * j + 1], bf16_hi(rw[j]));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = epi_act(f, v[j]);
+      uint4 o0, o1;
+      o0.x = pack_bf16x2(v[0], v[1]);
+      o0.y = pack_bf16x2(v[2], v[3]);
+      o0.z = pack_bf16x2(v[4], v[5]);
+      o0.w = pack_bf16x2(v[6], v[7]);
+      o1.x = pack_bf16x2(v[8], v[9]);
+      o1.y = pack_bf16x2(v[10], v[11]);
+      o1.z = pack_bf16x2(v[12], v[13]);
+      o1.w = pack_bf16x2(v[14], v[15]);
+      uint4* dst = reinterpret_cast<uint4*>(a.y + m * a.k + col);
+      dst[0] = o0;
+      dst[1] = o1;
+    }
   }
 }
 
@@ -275,15 +303,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     int lt = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
       const int acc = lt & 1;
-      mbar_wait(&tfull[acc], (lt >> 1) & 1);
-      tc_fence_after();
       const int m_tile = t / a.n_tiles;
       const int k0 = (t - m_tile * a.n_tiles) * BN;
       const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * C::ACC_COLS);
       const int tq = m_tile % a.tiles_q;
       const int t2 = m_tile / a.tiles_q;
       const TileRows rows{&a, (t2 / a.tiles_p) * a.bn, (t2 % a.tiles_p) * a.bh, tq * a.bw};
-      fprop_epilogue<BN>(a, trow, quarter * 32 + lane, k0, rows);
+      fprop_epilogue<BN>(a, trow, quarter * 32 + lane, k0, rows, [&] {
+        mbar_wait(&tfull[acc], (lt >> 1) & 1);
+        tc_fence_after();
+      });
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -629,8 +658,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     int lt = 0;
     for (int t = pair; t < total; t += pairs, ++lt) {
       const int acc = lt & 1;
-      mbar_wait(&tfull[acc], (lt >> 1) & 1);
-      tc_fence_after();
       const int mp = t / a.n_tiles;
       const int k0 = (t - mp * a.n_tiles) * BN;
       const int m_tile = 2 * mp + rank;
@@ -638,6 +665,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int t2 = m_tile / a.tiles_q;
       const TileRows rows{&a, (t2 / a.tiles_p) * a.bn, (t2 % a.tiles_p) * a.bh, tq * a.bw};
       const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * BN);
+      mbar_wait(&tfull[acc], (lt >> 1) & 1);
+      tc_fence_after();
       fprop_epilogue<BN>(a, trow, quarter * 32 + lane, k0, rows);
       tc_fence_before();
       __syncwarp();
@@ -810,12 +839,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     int lt = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
       const int acc = lt & 1;
-      mbar_wait(&tfull[acc], (lt >> 1) & 1);
-      tc_fence_after();
       const int img = t / a.tiles_img;
       const HaloRows rows{&a, img, (t - img * a.tiles_img) * 128, WP};
       const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * C::ACC_COLS);
-      fprop_epilogue<BN>(a, trow, quarter * 32 + lane, 0, rows);
+      fprop_epilogue<BN>(a, trow, quarter * 32 + lane, 0, rows, [&] {
+        mbar_wait(&tfull[acc], (lt >> 1) & 1);
+        tc_fence_after();
+      });
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -959,8 +989,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     int lt = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
       const int acc = lt & 1;
-      mbar_wait(&tfull[acc], (lt >> 1) & 1);
-      tc_fence_after();
       const int mp = t / a.n_tiles;
       const int k0 = (t - mp * a.n_tiles) * BN;
       const int nval = (2 * mp + 1 < a.m_tiles) ? 2 : 1;
@@ -971,7 +999,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int tq = m_tile % a.tiles_q;
         const int t2 = m_tile / a.tiles_q;
         const TileRows rows{&a, (t2 / a.tiles_p) * a.bn, (t2 % a.tiles_p) * a.bh, tq * a.bw};
-        fprop_epilogue<BN>(a, trow, quarter * 32 + lane, k0, rows);
+        if (u == 0) {
+          fprop_epilogue<BN>(a, trow, quarter * 32 + lane, k0, rows, [&] {
+            mbar_wait(&tfull[acc], (lt >> 1) & 1);
+            tc_fence_after();
+          });
+        } else {
+          fprop_epilogue<BN>(a, trow, quarter * 32 + lane, k0, rows);
+        }
       }
       tc_fence_before();
       __syncwarp();

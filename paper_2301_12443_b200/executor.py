@@ -74,6 +74,7 @@ def _bind(L):
     L.pbdx_ipc_close.argtypes = [V]
     L.pbdx_set_path.argtypes = [V, I, P(I), I]
     L.pbdx_trace_mark.argtypes = [V, V]
+    L.pbdx_set_train_mask.argtypes = [V, ctypes.c_uint]
     L.pbdx_block_trace.argtypes = [V] + [P(ctypes.c_float)] * 4
     L.pbdx_mb_layers.argtypes = [I, I]
     L.pbdx_mb_candidates.argtypes = [I, I, I]
@@ -333,6 +334,10 @@ class Partition:
         t, s = (ctypes.c_float * nb)(), (ctypes.c_float * nb)()
         _check(lib().pbdx_block_times(self.handle, t, s), "block_times")
         return list(t), list(s)
+
+    def set_train_mask(self, mask: int):
+        """Bit i = student block block_lo + i trains (DP-baseline mode trains one block of [0, k])."""
+        _check(lib().pbdx_set_train_mask(self.handle, int(mask)), "set_train_mask")
 
     def trace_mark(self, stream=None):
         """Reference event for block_trace (measured timelines)."""

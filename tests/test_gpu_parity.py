@@ -242,3 +242,25 @@ def test_state_migration_resumes_bitwise(ex):
     assert a.losses() == fresh.losses()
     assert torch.equal(a.params(), fresh.params())
     assert torch.equal(a.momentum(), fresh.momentum())
+
+
+def test_dp_baseline_train_mask(ex):
+    """DP-baseline mode (pbdx_set_train_mask): partition [0, 1] training only block 1 reproduces block 1
+    of the full run bit for bit, and leaves block 0's weights and momentum untouched."""
+    b = 8
+    full = ex.Partition(0, 1, b, b)
+    full.init_params()
+    only = ex.Partition(0, 1, b, b)
+    only.init_params()
+    only.set_train_mask(0b10)
+    w0 = only.block_state(0)[0].clone()
+    for _ in range(2):
+        full.step()
+        only.step()
+    torch.cuda.synchronize()
+    assert only.losses()[1] == full.losses()[1]
+    assert torch.equal(only.block_state(1)[0], full.block_state(1)[0])
+    assert torch.equal(only.block_state(0)[0], w0)
+    assert not only.block_state(0)[1].any()
+    with pytest.raises(ValueError):
+        only.set_train_mask(0)
