@@ -53,9 +53,12 @@ def launch_list(path):
     h = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     hdr, data = rows[h], rows[h + 1:]
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    mi = hdr.index("Metric Name") if "Metric Name" in hdr else None
     agg, cnt, tot = collections.defaultdict(float), collections.Counter(), 0.0
     for r in data:
-        t = float(r[vi].replace(",", "")) * (1e-3 if r[ui] in ("ns", "nsecond") else 1.0)
+        if mi is not None and r[mi] != "gpu__time_duration.sum":
+            continue
+        t = float(r[vi].replace(",", "")) * (1e-3 if r[ui] in ("ns", "nsecond") else 1e3 if r[ui] == "ms" else 1.0)
         name = r[ki].split("(")[0].replace("void ", "").replace("pbdk::", "").replace("(anonymous namespace)::", "")
         name = name.replace("<unnamed>::", "")
         agg[name] += t
