@@ -233,12 +233,13 @@ def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
     from paper_2301_12443_b200 import executor, models
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    ngpu = max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local_rank % ngpu)  # % ngpu: ranks may share a GPU (PBD_DIST_BACKEND=gloo runs)
+    dev = torch.device("cuda", local_rank % ngpu)
     if world > 1 or args.pipeline:
         from paper_2301_12443_b200 import runtime
         with ClockSampler(local_rank) as clocks:
-            res = runtime.bench_pipeline(args, rank, world, local_rank)
+            res = runtime.bench_pipeline(args, rank, world, local_rank % ngpu)
         if rank == 0:
             res["clocks"] = clocks.summary()
             res["cpu_baseline"] = None

@@ -535,7 +535,13 @@ def bench_pipeline(args, rank: int, world: int, local_rank: int) -> dict:
         os.environ.setdefault("MASTER_PORT", "29517")
         os.environ.setdefault("RANK", str(rank))
         os.environ.setdefault("WORLD_SIZE", str(world))
-        dist.init_process_group("nccl", device_id=dev)
+        # NCCL (one process per GPU).  PBD_DIST_BACKEND=gloo lets several ranks share one GPU (the CI /
+        # single-GPU exercise of this exact path: the relay is the K11 peer relay either way)
+        backend = os.environ.get("PBD_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     gb = args.batch * world
     wl = getattr(args, "workload", "cifar")
     model = wl if wl in ("mbv2", "effb0") else "resnet"
@@ -632,4 +638,33 @@ def bench_pipeline(args, rank: int, world: int, local_rank: int) -> dict:
                     "d2h_bytes_per_step": 8 * len(pipe.stage.blocks), "ms_per_step": e2e_ms},
             "schedule": sched, "predicted_step_ms": pred["step_ms"], "profile": info["profile"],
             "block_losses": {k: v for d in all_losses for k, v in d.items()},
-            "gpu_launches": pipe.stage.launches_per_step() * args.steps}
+            "gpu_launches": pipe.stage.launches_per_step() * args.steps,
+            "roofline": _step_roofline(model, image, paths, gb, ms, world)}
+
+
+def _step_roofline(model, image, paths, gb, ms, world) -> dict:
+    """Whole-job step roofline of a multi-rank run: algorithmic work of the global step (models.py /
+    mb_models.py accounting) over the measured step time and the peaks of `world` GPUs."""
+    import json as _json
+    import os as _os
+    from . import mb_models, models
+    root = _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__)))
+    peaks = {"hbm_gbs": 6650.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+    path = _os.path.join(root, "MEASURED_PEAKS.json")
+    if _os.path.exists(path):
+        with open(path) as f:
+            d = _json.load(f)
+        peaks = {"hbm_gbs": d["hbm_gbs"], "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                 "source": "measured"}
+    if model == "resnet":
+        flops, nbytes = models.step_flops(gb), models.step_bytes(gb)
+    else:
+        flops, nbytes = mb_models.step_work(gb, image, paths)
+    t_tensor = flops / (peaks["bf16_tflops_sustained"] * 1e12 * world)
+    t_hbm = nbytes / (peaks["hbm_gbs"] * 1e9 * world)
+    bound = "tensor" if t_tensor >= t_hbm else "hbm"
+    achieved = flops / (ms * 1e-3) / 1e12 / world if bound == "tensor" else nbytes / (ms * 1e-3) / 1e9 / world
+    peak = peaks["bf16_tflops_sustained"] if bound == "tensor" else peaks["hbm_gbs"]
+    return {"bound": bound, "kernel": "whole step, per GPU (all ranks)", "achieved": achieved, "peak": peak,
+            "unit": "TFLOP/s" if bound == "tensor" else "GB/s", "frac": achieved / peak, "traffic": None,
+            "peak_source": peaks["source"] + " sustained"}
