@@ -779,7 +779,9 @@ class MbPartition final : public PartitionBase {
       sb.wws_bytes = wws;
       sb.wws = arena_.get<void>(wws);
       sb.lws = arena_.get<double>(std::max<size_t>(lws, 1) * sizeof(double));
-      cuda(cudaStreamCreateWithFlags(&sb.stream, cudaStreamNonBlocking), "stream");
+      cuda(cudaStreamCreateWithPriority(&sb.stream, cudaStreamNonBlocking,
+                                        b == hi ? priority_high() : priority_low()),
+           "stream");
       cuda(cudaEventCreateWithFlags(&sb.done, cudaEventDisableTiming), "event");
       sblocks_.push_back(std::move(sb));
     }

@@ -453,7 +453,9 @@ class ResNetPartition final : public PartitionBase {
       s.rws = arena_.get<float>(rws * sizeof(float));
       s.wws_bytes = wws;
       s.wws = arena_.get<void>(wws);
-      cuda(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "stream");
+      const bool last = s.k == d_.block_hi;
+      cuda(cudaStreamCreateWithPriority(&s.stream, cudaStreamNonBlocking, last ? priority_high() : priority_low()),
+           "stream");
       cuda(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming), "event");
     }
     tdone_.resize(tblocks_.size());

@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -202,7 +203,7 @@ class PartitionBase {
       cuda(cudaStreamEndCapture(cap_stream_, &g), "end capture");
       size_t nodes = 0;
       cuda(cudaGraphGetNodes(g, nullptr, &nodes), "graph nodes");
-      if (nodes > 0) cuda(cudaGraphInstantiate(&phase_exec_[ph], g, 0), "instantiate");
+      if (nodes > 0) cuda(cudaGraphInstantiate(&phase_exec_[ph], g, graph_flags()), "instantiate");
       cudaGraphDestroy(g);
     }
     timing_ = was_timing;
@@ -237,7 +238,7 @@ class PartitionBase {
     }
     timing_ = was_timing;
     cuda(cudaStreamEndCapture(cap_stream_, &g), "end capture");
-    cuda(cudaGraphInstantiate(&graph_exec_, g, 0), "instantiate");
+    cuda(cudaGraphInstantiate(&graph_exec_, g, graph_flags()), "instantiate");
     cudaGraphDestroy(g);
     graph_valid_ = true;
   }
@@ -289,8 +290,30 @@ class PartitionBase {
  protected:
   void invalidate_graphs() { graph_valid_ = phases_valid_ = false; }
 
+  // Scheduling priorities: the teacher chain (caller / capture stream) is the step's critical path
+  // (every student block waits for its teacher block; the last student block starts only after the
+  // whole chain), so its kernels get the highest priority, the last student block next, the
+  // earlier student blocks (which have the whole remaining chain to hide behind) the lowest.
+  // Graphs keep the captured per-node priorities (cudaGraphInstantiateFlagUseNodePriority).
+  static int priority_high() {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    return std::getenv("PBD_NO_PRIORITY") != nullptr ? 0 : hi;
+  }
+  static int priority_low() {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    return std::getenv("PBD_NO_PRIORITY") != nullptr ? 0 : lo;
+  }
+  static unsigned long long graph_flags() {
+    return std::getenv("PBD_NO_PRIORITY") != nullptr
+               ? 0ull
+               : static_cast<unsigned long long>(cudaGraphInstantiateFlagUseNodePriority);
+  }
+
   void ensure_cap_stream() {
-    if (cap_stream_ == nullptr) cuda(cudaStreamCreateWithFlags(&cap_stream_, cudaStreamNonBlocking), "stream");
+    if (cap_stream_ == nullptr)
+      cuda(cudaStreamCreateWithPriority(&cap_stream_, cudaStreamNonBlocking, priority_high()), "stream");
   }
 
   // relay flag storage (call from the model's allocate())
