@@ -323,22 +323,30 @@ __global__ void __launch_bounds__(kT) stem_wgrad_partial_kernel(const __nv_bfloa
     const int p = row % P;
     const int n = row / P;
     const __nv_bfloat16* grow = dy + static_cast<size_t>(row) * P * 32 + lane;
-#pragma unroll 4
+    // the three input rows of this output row, clamped; out-of-image taps contribute 0 * x (branch-free)
+    float hv[3];
+    const __nv_bfloat16* xr[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int h = 2 * p + r - 1;
+      hv[r] = (h >= 0 && h < S) ? 1.0f : 0.0f;
+      xr[r] = x + (static_cast<size_t>(n) * S + min(max(h, 0), S - 1)) * S * 16;
+    }
+#pragma unroll 2
     for (int q = 0; q < P; ++q) {
       const float g = __bfloat162float(grow[static_cast<size_t>(q) * 32]);
 #pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        const int h = 2 * p + r - 1;
-        if (h < 0 || h >= S) continue;
-        const __nv_bfloat16* xr = x + (static_cast<size_t>(n) * S + h) * S * 16;
+      for (int s = 0; s < 3; ++s) {
+        const int ww = 2 * q + s - 1;
+        const float wv = (ww >= 0 && ww < S) ? 1.0f : 0.0f;
+        const int wc = min(max(ww, 0), S - 1);
 #pragma unroll
-        for (int s = 0; s < 3; ++s) {
-          const int ww = 2 * q + s - 1;
-          if (ww < 0 || ww >= S) continue;
-          const uint2 v = *reinterpret_cast<const uint2*>(xr + static_cast<size_t>(ww) * 16);
-          acc[r * 9 + s * 3 + 0] = fmaf(g, __uint_as_float(v.x << 16), acc[r * 9 + s * 3 + 0]);
-          acc[r * 9 + s * 3 + 1] = fmaf(g, __uint_as_float(v.x & 0xFFFF0000u), acc[r * 9 + s * 3 + 1]);
-          acc[r * 9 + s * 3 + 2] = fmaf(g, __uint_as_float(v.y << 16), acc[r * 9 + s * 3 + 2]);
+        for (int r = 0; r < 3; ++r) {
+          const uint2 v = *reinterpret_cast<const uint2*>(xr[r] + static_cast<size_t>(wc) * 16);
+          const float gm = g * (hv[r] * wv);
+          acc[r * 9 + s * 3 + 0] = fmaf(gm, __uint_as_float(v.x << 16), acc[r * 9 + s * 3 + 0]);
+          acc[r * 9 + s * 3 + 1] = fmaf(gm, __uint_as_float(v.x & 0xFFFF0000u), acc[r * 9 + s * 3 + 1]);
+          acc[r * 9 + s * 3 + 2] = fmaf(gm, __uint_as_float(v.y << 16), acc[r * 9 + s * 3 + 2]);
         }
       }
     }
