@@ -103,7 +103,7 @@ __device__ __forceinline__ void fprop_epilogue(const FpropArgs& a, uint32_t trow
   rowmap(row, valid, m);
   const EpiFlags f = epi_flags(a.epi);
   const bool has_bias = f.bias;
-  if (a.debug == 3 || a.debug == 9) {
+  if (a.debug == 3 || a.debug == 9 || a.debug == 7) {
     wait();
     return;
   }
@@ -781,13 +781,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load_2d(bres + (cc * 9 + tap) * C::B_BYTES, &tmw, bfull, tap * cin_stored + cc * BKC, 0);
       int it = 0, st = 0;
       uint32_t ph = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int t = blockIdx.x; t < (a.debug == 8 ? 0 : total); t += gridDim.x) {
         const int img = t / a.tiles_img;
         const int p0 = (t - img * a.tiles_img) * 128;
         for (int cc = 0; cc < chunks; ++cc, ++it) {
           if (it >= C::STAGES) mbar_wait(&empty[st], ph ^ 1);
-          mbar_arrive_expect_tx(&full[st], C::BOX_BYTES);
-          tma_load_4d(smem + st * C::STAGE, &tmx, &full[st], cc * BKC, -1, p0 / WP - 1, img);
+          if (a.debug >= 6) {  // timing only: no activation loads (MMA + epilogue pipeline alone)
+            mbar_arrive(&full[st]);
+          } else {
+            mbar_arrive_expect_tx(&full[st], C::BOX_BYTES);
+            tma_load_4d(smem + st * C::STAGE, &tmx, &full[st], cc * BKC, -1, p0 / WP - 1, img);
+          }
           if (++st == C::STAGES) {
             st = 0;
             ph ^= 1;
@@ -807,12 +811,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t ph = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
         const int acc = lt & 1;
-        if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
+        if (lt >= 2 && a.debug != 8) mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
         tc_fence_after();
         const uint32_t dacc = tmem + static_cast<uint32_t>(acc * C::ACC_COLS);
         const int j0 = (t % a.tiles_img) * 128 % WP;
         for (int cc = 0; cc < chunks; ++cc) {
-          mbar_wait(&full[st], ph);
+          if (a.debug != 8) mbar_wait(&full[st], ph);
           tc_fence_after();
           const uint64_t a0 = adesc0 + static_cast<uint32_t>((st * C::STAGE + j0 * C::SW) >> 4);
           const uint64_t b0 = bdesc0 + static_cast<uint32_t>((cc * 9 * C::B_BYTES) >> 4);
@@ -822,7 +826,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int kk = 0; kk < BKC / 16; ++kk) {
               const uint32_t aoff = static_cast<uint32_t>((((tap / 3) * WP + tap % 3) * C::SW + kk * 32) >> 4);
               const uint32_t boff = static_cast<uint32_t>((tap * C::B_BYTES + kk * 32) >> 4);
-              umma_bf16(dacc, a0 + aoff, b0 + boff, idesc, (cc | tap | kk) != 0 ? 1u : 0u);
+              if (a.debug != 2) umma_bf16(dacc, a0 + aoff, b0 + boff, idesc, (cc | tap | kk) != 0 ? 1u : 0u);
             }
           }
           umma_commit(&empty[st]);
@@ -837,7 +841,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     const int quarter = warp & 3;
     int lt = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+    for (int t = blockIdx.x; t < (a.debug == 8 ? 0 : total); t += gridDim.x, ++lt) {
       const int acc = lt & 1;
       const int img = t / a.tiles_img;
       const HaloRows rows{&a, img, (t - img * a.tiles_img) * 128, WP};

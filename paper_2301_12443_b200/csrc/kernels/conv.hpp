@@ -33,7 +33,9 @@ struct FpropArgs {
   int n_tiles, m_tiles;
   int tiles_img;  // halo variant only
   int epi;
-  int debug;  // 0 normal; 1 skip epilogue stores; 2 skip MMAs; 3 skip epilogue; 4 cycle counters
+  int debug;  // timing experiments (PBDK_CONV_DEBUG): 0 normal; 1 skip epilogue stores; 2 skip MMAs;
+              // 3 skip epilogue; 4 cycle counters; halo kernel: 6 no activation loads, 7 = 6 + 3,
+              // 8 MMA warp alone (no producer / epilogue, no barrier waits)
   long long* dbg_buf;  // debug 4: per CTA {total, wait_tempty, wait_full, issue, epi_wait, epi_work}
   __nv_bfloat16* y;
   const float* bias;
