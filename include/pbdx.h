@@ -56,8 +56,9 @@ typedef struct pbdx_desc {
 #define PBDX_BUF_LOSSES 5       /* double[num_blocks]: per-block partial loss of the last step */
 #define PBDX_BUF_STEP 6         /* int64 step counter (advanced by apply_update) */
 #define PBDX_BUF_TEACHER_PARAMS 7 /* bf16 teacher conv weights of block_lo..hi (flat, program order) */
-#define PBDX_BUF_MAILBOX 8      /* uint64 flags written by relay peers: [0,16) ready, one per sender slot;
-                                   [16,32) consumed, one per receiver slot (own allocation, IPC-exportable) */
+#define PBDX_BUF_MAILBOX 8      /* 64 uint64 flags written by peers (own allocation, IPC-exportable):
+                                   [0,16) relay ready (per sender slot), [16,32) relay consumed (per
+                                   receiver slot), [32,48) DP ready, [48,64) DP consumed (per member) */
 
 int pbdx_create(const pbdx_desc* d, void** handle);
 void pbdx_destroy(void* handle);
@@ -155,6 +156,14 @@ typedef struct pbdx_relay_msg {
 } pbdx_relay_msg;
 int pbdx_relay_set_recv(void* handle, int nsenders, void* const* remote_consumed_flags);
 int pbdx_relay_set_send(void* handle, int nmsgs, const pbdx_relay_msg* msgs);
+/* DP group over peer memory (share_gradient; AHD partitions with |G| > 1): instead of an
+ * NCCL allreduce, every member announces its gradients after S_i.backward (device-side flag into each
+ * peer's mailbox), waits for all members, and the update kernel reads the group's gradient slabs straight
+ * from the peers' PBDX_BUF_GRADS (NVLink loads), adds them in member order and applies SGD-momentum —
+ * bit-identical weights on every member, no host round trip, and the whole step stays one CUDA graph.
+ * peer_grads[j] / peer_mailbox[j]: member j's buffers as seen from this process (j == me ignored). */
+int pbdx_dp_set_group(void* handle, int size, int me, void* const* peer_grads, void* const* peer_mailbox);
+
 /* CUDA IPC of an executor buffer (the allocation base: PBDX_BUF_INPUT / PBDX_BUF_MAILBOX) for ranks in
  * other processes; handle = 64 bytes (cudaIpcMemHandle_t). */
 int pbdx_ipc_export(void* dev_ptr, void* handle);

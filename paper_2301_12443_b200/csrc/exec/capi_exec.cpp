@@ -74,6 +74,10 @@ int pbdx_teacher_act(void* h, int block, void** ptr, size_t* bytes) {
 int pbdx_refresh_shadows(void* h, void* st) { return guard([&] { P(h)->refresh_shadows(S(st)); }); }
 int pbdx_set_timing(void* h, int enabled) { return guard([&] { P(h)->set_timing(enabled != 0); }); }
 int pbdx_block_times(void* h, float* t, float* s) { return guard([&] { P(h)->block_times(t, s); }); }
+int pbdx_dp_set_group(void* h, int size, int me, void* const* peer_grads, void* const* peer_mailbox) {
+  if (size > 1 && (peer_grads == nullptr || peer_mailbox == nullptr)) return PBDK_EINVAL;
+  return guard([&] { P(h)->dp_set_group(size, me, peer_grads, peer_mailbox); });
+}
 int pbdx_set_train_mask(void* h, unsigned int mask) { return guard([&] { P(h)->set_train_mask(mask); }); }
 int pbdx_trace_mark(void* h, void* st) { return guard([&] { P(h)->trace_mark(S(st)); }); }
 int pbdx_block_trace(void* h, float* t0, float* t1, float* s0, float* s1) {

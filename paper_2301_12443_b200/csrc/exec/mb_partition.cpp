@@ -382,9 +382,16 @@ class MbPartition final : public PartitionBase {
       SBlock& sb = sblocks_[i];
       for (SLayer& L : sb.layers) {
         SCand& C = L.cands[static_cast<size_t>(L.active)];
-        check(pbdk::sgd_momentum(params_ + C.off, mom_ + C.off, grads_ + C.off, shadow_ + C.off, C.L.total, d_.lr,
-                                 d_.momentum, counter, st),
-              "sgd");
+        if (dp_active()) {
+          const auto src = dp_sources(grads_, C.off);
+          check(pbdk::sgd_momentum_sum(params_ + C.off, mom_ + C.off, src.data(), static_cast<int>(src.size()),
+                                       shadow_ + C.off, C.L.total, d_.lr, d_.momentum, counter, st),
+                "sgd (dp)");
+        } else {
+          check(pbdk::sgd_momentum(params_ + C.off, mom_ + C.off, grads_ + C.off, shadow_ + C.off, C.L.total, d_.lr,
+                                   d_.momentum, counter, st),
+                "sgd");
+        }
         counter = nullptr;  // advance the step counter once
         refresh_derived(L, C, st);
       }
@@ -408,7 +415,7 @@ class MbPartition final : public PartitionBase {
       case PBDX_BUF_LOSSES: *ptr = losses_; *bytes = nblocks() * sizeof(double); break;
       case PBDX_BUF_STEP: *ptr = step_; *bytes = sizeof(long long); break;
       case PBDX_BUF_TEACHER_PARAMS: *ptr = nullptr; *bytes = 0; break;
-      case PBDX_BUF_MAILBOX: *ptr = mailbox_; *bytes = 2 * pbdk::kRelayMaxPeers * sizeof(unsigned long long); break;
+      case PBDX_BUF_MAILBOX: *ptr = mailbox_; *bytes = kMailboxSlots * sizeof(unsigned long long); break;
       default: throw BadArg("unknown buffer");
     }
   }

@@ -245,6 +245,14 @@ class ResNetPartition final : public PartitionBase {
   }
 
   void update_body(cudaStream_t st) override {
+    if (dp_active()) {  // share_gradient + update fused: sum the group's gradient slabs from peer memory
+      const auto src = dp_sources(grads_, 0);
+      check(pbdk::sgd_momentum_sum(params_, mom_, src.data(), static_cast<int>(src.size()), shadow_, total_, d_.lr,
+                                   d_.momentum, step_, st),
+            "sgd (dp)");
+      refresh_flips(st);
+      return;
+    }
     if (all_train()) {
       check(pbdk::sgd_momentum(params_, mom_, grads_, shadow_, total_, d_.lr, d_.momentum, step_, st), "sgd");
       refresh_flips(st);
@@ -272,7 +280,7 @@ class ResNetPartition final : public PartitionBase {
       case PBDX_BUF_LOSSES: *ptr = losses_; *bytes = nblocks() * sizeof(double); break;
       case PBDX_BUF_STEP: *ptr = step_; *bytes = sizeof(long long); break;
       case PBDX_BUF_TEACHER_PARAMS: *ptr = tparams_; *bytes = tparam_bytes_; break;
-      case PBDX_BUF_MAILBOX: *ptr = mailbox_; *bytes = 2 * pbdk::kRelayMaxPeers * sizeof(unsigned long long); break;
+      case PBDX_BUF_MAILBOX: *ptr = mailbox_; *bytes = kMailboxSlots * sizeof(unsigned long long); break;
       default: throw BadArg("unknown buffer");
     }
   }

@@ -148,6 +148,7 @@ class PartitionBase {
   }
 
   void teacher_forward(cudaStream_t st) {
+    dp_wait_consumed(st);  // the previous step's DP peers finished reading my gradients
     relay_wait_input(st);
     teacher_body(st);
     relay_send_output(st);
@@ -156,8 +157,12 @@ class PartitionBase {
   void student_step_impl(cudaStream_t caller, bool fork) {
     student_body(caller, fork);
     relay_finish(caller);
+    dp_exchange(caller);  // share_gradient: announce mine, wait for every member's
   }
-  void apply_update(cudaStream_t st) { update_body(st); }
+  void apply_update(cudaStream_t st) {
+    update_body(st);
+    dp_release(st);
+  }
   void step(cudaStream_t st) {
     teacher_forward(st);
     student_step_impl(st, false);
@@ -168,6 +173,7 @@ class PartitionBase {
     int n = body_launches_per_step();
     if (!recv_consumed_.empty()) n += 2;  // relay wait + release
     if (!send_.empty()) n += 2;           // relay wait + copy
+    if (dp_active()) n += 4;              // dp wait consumed, ready, wait ready, consumed
     return n;
   }
 
@@ -277,6 +283,26 @@ class PartitionBase {
 
   const pbdx_desc& desc() const { return d_; }
 
+  // ---- DP group over peer memory (share_gradient fused into the update, bd_kernels.cu sgd_sum_kernel)
+  // peer_grads[j] / peer_mailbox[j]: member j's PBDX_BUF_GRADS and PBDX_BUF_MAILBOX (device pointers
+  // valid here; j == me is ignored).  Slots: member j writes my mailbox[32 + j] (ready) and
+  // mailbox[48 + j] (consumed).
+  void dp_set_group(int size, int me, void* const* peer_grads, void* const* peer_mailbox) {
+    if (size < 1 || size > pbdk::kDpMaxGroup || me < 0 || me >= size) throw BadArg("dp group: bad size / index");
+    dp_size_ = size;
+    dp_me_ = me;
+    dp_grads_.assign(static_cast<size_t>(size), nullptr);
+    dp_mail_.assign(static_cast<size_t>(size), nullptr);
+    for (int j = 0; j < size; ++j) {
+      if (j == me) continue;
+      if (peer_grads[j] == nullptr || peer_mailbox[j] == nullptr) throw BadArg("dp group: null peer pointer");
+      dp_grads_[static_cast<size_t>(j)] = static_cast<const float*>(peer_grads[j]);
+      dp_mail_[static_cast<size_t>(j)] = static_cast<unsigned long long*>(peer_mailbox[j]);
+    }
+    invalidate_graphs();
+  }
+  bool dp_active() const { return dp_size_ > 1; }
+
   // Which student blocks of the range train (bit i = block block_lo + i).  All by default; the DP
   // baseline of the paper (blocks trained one after another, every step
   // recomputing the teacher prefix) runs partition [0, k] with only block k training.
@@ -316,12 +342,69 @@ class PartitionBase {
       cuda(cudaStreamCreateWithPriority(&cap_stream_, cudaStreamNonBlocking, priority_high()), "stream");
   }
 
-  // relay flag storage (call from the model's allocate())
+  // relay / DP flag storage (call from the model's allocate())
   void allocate_relay() {
-    mailbox_ = arena_.get<unsigned long long>(2 * pbdk::kRelayMaxPeers * sizeof(unsigned long long));
-    relay_seq_ = arena_.get<unsigned long long>(2 * sizeof(unsigned long long));
+    mailbox_ = arena_.get<unsigned long long>(kMailboxSlots * sizeof(unsigned long long));
+    relay_seq_ = arena_.get<unsigned long long>(3 * sizeof(unsigned long long));
     relay_ticket_ = arena_.get<unsigned int>(sizeof(unsigned int));
   }
+
+  // gradient sources of a DP-group update: member order, `mine` at my index, peers' slabs at the same
+  // element offset
+  std::vector<const float*> dp_sources(const float* mine, size_t offset) const {
+    std::vector<const float*> v(static_cast<size_t>(dp_size_));
+    for (int j = 0; j < dp_size_; ++j) v[static_cast<size_t>(j)] = (j == dp_me_ ? mine : dp_grads_[static_cast<size_t>(j)]) + offset;
+    return v;
+  }
+
+  void dp_exchange(cudaStream_t st) {
+    if (!dp_active()) return;
+    pbdk::RelayReleaseArgs r{};  // ready(seq+1) into every peer's mailbox[32 + me]
+    pbdk::RelayWaitArgs w{};     // then every peer's ready in my mailbox[32 + j]
+    int n = 0;
+    for (int j = 0; j < dp_size_; ++j) {
+      if (j == dp_me_) continue;
+      r.flags[n] = dp_mail_[static_cast<size_t>(j)] + 32 + dp_me_;
+      w.flags[n] = mailbox_ + 32 + j;
+      ++n;
+    }
+    r.count = w.count = n;
+    r.seq = relay_seq_ + 2;
+    w.seq = relay_seq_ + 2;
+    r.advance = 1;
+    w.bias = 0;
+    check(pbdk::relay_release(r, st), "dp ready");
+    check(pbdk::relay_wait(w, st), "dp wait ready");
+  }
+
+  void dp_release(cudaStream_t st) {  // I have read every peer's gradients of this step
+    if (!dp_active()) return;
+    pbdk::RelayReleaseArgs r{};
+    int n = 0;
+    for (int j = 0; j < dp_size_; ++j)
+      if (j != dp_me_) r.flags[n++] = dp_mail_[static_cast<size_t>(j)] + 48 + dp_me_;
+    r.count = n;
+    r.seq = relay_seq_ + 2;
+    r.advance = 0;
+    check(pbdk::relay_release(r, st), "dp consumed");
+  }
+
+  void dp_wait_consumed(cudaStream_t st) {  // before this step's wgrads overwrite my gradients
+    if (!dp_active()) return;
+    pbdk::RelayWaitArgs w{};
+    int n = 0;
+    for (int j = 0; j < dp_size_; ++j)
+      if (j != dp_me_) w.flags[n++] = mailbox_ + 48 + j;
+    w.count = n;
+    w.seq = relay_seq_ + 2;
+    w.bias = 0;
+    check(pbdk::relay_wait(w, st), "dp wait consumed");
+  }
+
+  static constexpr int kMailboxSlots = 64;  // [0,16) relay ready, [16,32) relay consumed, [32,48) dp ready, [48,64) dp consumed
+  int dp_size_ = 1, dp_me_ = 0;
+  std::vector<const float*> dp_grads_;
+  std::vector<unsigned long long*> dp_mail_;
 
   void relay_wait_input(cudaStream_t st) {
     if (recv_consumed_.empty()) return;

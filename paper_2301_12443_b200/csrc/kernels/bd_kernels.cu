@@ -573,6 +573,44 @@ __global__ void sgd_kernel(float4* __restrict__ w, float4* __restrict__ v, const
   if (counter != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *counter += 1;
 }
 
+// share_gradient + update_weight fused for a DP group: g = sum of the G members'
+// gradient slabs read straight from their device memory (NVLink peer loads; CUDA IPC mappings across
+// processes), added in member order on every member — so all members compute bit-identical weights
+// without an NCCL allreduce — then the momentum SGD of sgd_kernel.
+struct GradSources {
+  const float4* g[8];
+  int count;
+};
+
+__global__ void sgd_sum_kernel(float4* __restrict__ w, float4* __restrict__ v, const GradSources src,
+                               uint2* __restrict__ shadow, size_t n4, float lr, float mu, long long* counter) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    float4 gg = src.g[0][i];
+    for (int r = 1; r < src.count; ++r) {
+      const float4 o = src.g[r][i];
+      gg.x = gg.x + o.x;
+      gg.y = gg.y + o.y;
+      gg.z = gg.z + o.z;
+      gg.w = gg.w + o.w;
+    }
+    float4 vv = v[i];
+    float4 ww = w[i];
+    vv.x = fmaf(mu, vv.x, gg.x);
+    vv.y = fmaf(mu, vv.y, gg.y);
+    vv.z = fmaf(mu, vv.z, gg.z);
+    vv.w = fmaf(mu, vv.w, gg.w);
+    ww.x = fmaf(-lr, vv.x, ww.x);
+    ww.y = fmaf(-lr, vv.y, ww.y);
+    ww.z = fmaf(-lr, vv.z, ww.z);
+    ww.w = fmaf(-lr, vv.w, ww.w);
+    v[i] = vv;
+    w[i] = ww;
+    if (shadow != nullptr) shadow[i] = make_uint2(pack2(ww.x, ww.y), pack2(ww.z, ww.w));
+  }
+  if (counter != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *counter += 1;
+}
+
 int grid_for(long long work, int per_block = kThreads) {
   const long long b = (work + per_block - 1) / per_block;
   return static_cast<int>(std::max<long long>(1, std::min<long long>(b, 148LL * 16)));
@@ -685,6 +723,18 @@ int sgd_momentum(float* w, float* v, const float* g, void* shadow, size_t n, flo
   sgd_kernel<<<grid_for(static_cast<long long>(n / 4)), kThreads, 0, st>>>(
       reinterpret_cast<float4*>(w), reinterpret_cast<float4*>(v), reinterpret_cast<const float4*>(g),
       static_cast<uint2*>(shadow), n / 4, lr, mu, counter);
+  return ok(cudaGetLastError());
+}
+
+int sgd_momentum_sum(float* w, float* v, const float* const* g, int count, void* shadow, size_t n, float lr, float mu,
+                     long long* counter, cudaStream_t st) {
+  if (n % 4 != 0 || count < 1 || count > 8) return PBDK_EINVAL;
+  GradSources src{};
+  for (int r = 0; r < count; ++r) src.g[r] = reinterpret_cast<const float4*>(g[r]);
+  src.count = count;
+  sgd_sum_kernel<<<grid_for(static_cast<long long>(n / 4)), kThreads, 0, st>>>(
+      reinterpret_cast<float4*>(w), reinterpret_cast<float4*>(v), src, static_cast<uint2*>(shadow), n / 4, lr, mu,
+      counter);
   return ok(cudaGetLastError());
 }
 

@@ -50,5 +50,8 @@ int bn_bwd(const void* g, const void* y, const float* mean_rstd, const float* ga
            float* red, float* dgamma, float* dbeta, void* dy, cudaStream_t st);
 int sgd_momentum(float* w, float* v, const float* g, void* shadow, size_t n, float lr, float mu, long long* counter,
                  cudaStream_t st);
+// the same update on g = g[0] + g[1] + ... (member order), the DP group's gradient slabs in peer memory
+int sgd_momentum_sum(float* w, float* v, const float* const* g, int count, void* shadow, size_t n, float lr, float mu,
+                     long long* counter, cudaStream_t st);
 
 }  // namespace pbdk

@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(256) relay_copy_kernel(RelayCopyArgs a) {
 __global__ void relay_release_kernel(RelayReleaseArgs a) {
   if (threadIdx.x != 0) return;
   __threadfence_system();
-  const unsigned long long seq = *a.seq + 1;
+  const unsigned long long seq = *a.seq + (a.advance ? 1 : 0);
   *a.seq = seq;
   for (int i = 0; i < a.count; ++i) st_release_sys(a.flags[i], seq);
 }

@@ -26,15 +26,19 @@ struct RelayCopyArgs {
   int count;
 };
 
-// *seq += 1; flags[i] = *seq
+// advance: *seq += 1; then flags[i] = *seq (peer stores, system scope)
 struct RelayReleaseArgs {
   unsigned long long* flags[kRelayMaxPeers];
   unsigned long long* seq;
   int count;
+  int advance = 1;
 };
 
 int relay_wait(const RelayWaitArgs& a, cudaStream_t st);
 int relay_copy(const RelayCopyArgs& a, int ctas, cudaStream_t st);
 int relay_release(const RelayReleaseArgs& a, cudaStream_t st);
+
+// ---- DP-group gradient sharing over peer memory (fused with the SGD update, bd_kernels.cu)
+constexpr int kDpMaxGroup = 8;
 
 }  // namespace pbdk

@@ -75,6 +75,7 @@ def _bind(L):
     L.pbdx_set_path.argtypes = [V, I, P(I), I]
     L.pbdx_trace_mark.argtypes = [V, V]
     L.pbdx_set_train_mask.argtypes = [V, ctypes.c_uint]
+    L.pbdx_dp_set_group.argtypes = [V, I, I, P(V), P(V)]
     L.pbdx_block_trace.argtypes = [V] + [P(ctypes.c_float)] * 4
     L.pbdx_mb_layers.argtypes = [I, I]
     L.pbdx_mb_candidates.argtypes = [I, I, I]
@@ -334,6 +335,16 @@ class Partition:
         t, s = (ctypes.c_float * nb)(), (ctypes.c_float * nb)()
         _check(lib().pbdx_block_times(self.handle, t, s), "block_times")
         return list(t), list(s)
+
+    def dp_set_group(self, me: int, peer_grads: List[int], peer_mailboxes: List[int]):
+        """DP group over peer memory (include/pbdx.h pbdx_dp_set_group): member pointers in member order."""
+        n = len(peer_grads)
+        g = (ctypes.c_void_p * n)(*[p or 0 for p in peer_grads])
+        m = (ctypes.c_void_p * n)(*[p or 0 for p in peer_mailboxes])
+        _check(lib().pbdx_dp_set_group(self.handle, n, me, g, m), "dp_set_group")
+
+    def grads_ptr(self) -> int:
+        return self.buffer_ptr(BUF_GRADS)[0]
 
     def set_train_mask(self, mask: int):
         """Bit i = student block block_lo + i trains (DP-baseline mode trains one block of [0, k])."""

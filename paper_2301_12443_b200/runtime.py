@@ -121,13 +121,15 @@ class PipeBD:
     """
 
     def __init__(self, schedule: dict, global_batch: int, make_stage: Callable, dpu: bool = True,
-                 groups: Optional[Dict[int, object]] = None, relay: str = "nccl"):
+                 groups: Optional[Dict[int, object]] = None, relay: str = "nccl", grad_share: Optional[str] = None):
         """relay: "nccl" (batch_isend_irecv of the overlapping row slices) or "peer" (K11: the
         sender's SMs store straight into the receiver's input through NVLink/IPC peer memory,
         device-side flags, no host handshake; stages must be executor.Partition on CUDA)."""
         if relay not in ("nccl", "peer"):
             raise ValueError(f"unknown relay {relay!r}")
         self.relay = relay
+        # with the peer relay the DP groups also share gradients over peer memory (no NCCL allreduce)
+        self.grad_share = grad_share if grad_share is not None else ("peer" if relay == "peer" else "nccl")
         self._ipc_mapped: List[int] = []
         self.schedule = schedule
         self.b = global_batch
@@ -165,23 +167,29 @@ class PipeBD:
         self._ipc_mapped = []
         st = self.stage
         mine = {"pid": os.getpid(), "input": st.input_ptr(), "mailbox": st.mailbox_ptr(), "row": st.row_bytes_in(),
-                "h_input": executor.ipc_export(st.input_ptr()), "h_mailbox": executor.ipc_export(st.mailbox_ptr())}
+                "grads": st.grads_ptr(),
+                "h_input": executor.ipc_export(st.input_ptr()), "h_mailbox": executor.ipc_export(st.mailbox_ptr()),
+                "h_grads": executor.ipc_export(st.grads_ptr())}
         allp = [None] * self.world
         dist.all_gather_object(allp, mine)
         endpoints = {}
+        group = list(self.me.group)
+        peers = {m[1] for m in self.send_msgs} | {m[0] for m in self.recv_msgs} | set(group)
         for r, e in enumerate(allp):
             if e["pid"] == mine["pid"]:
-                endpoints[r] = {"input": e["input"], "mailbox": e["mailbox"], "row": e["row"]}
-            else:
-                peers = {m[1] for m in self.send_msgs} | {m[0] for m in self.recv_msgs}
-                if r not in peers:
-                    continue
-                ip, mb = executor.ipc_open(e["h_input"]), executor.ipc_open(e["h_mailbox"])
-                self._ipc_mapped += [ip, mb]
-                endpoints[r] = {"input": ip, "mailbox": mb, "row": e["row"]}
+                endpoints[r] = {"input": e["input"], "mailbox": e["mailbox"], "row": e["row"], "grads": e["grads"]}
+            elif r in peers:
+                ip, mb, gr = (executor.ipc_open(e["h_input"]), executor.ipc_open(e["h_mailbox"]),
+                              executor.ipc_open(e["h_grads"]))
+                self._ipc_mapped += [ip, mb, gr]
+                endpoints[r] = {"input": ip, "mailbox": mb, "row": e["row"], "grads": gr}
         recv, send = peer_wiring(self.schedule, self.b, self.rank, endpoints)
         st.relay_set_recv(recv)
         st.relay_set_send(send)
+        # share_gradient over peer memory inside the DP group (fused into the update kernel)
+        if len(group) > 1 and self.grad_share == "peer":
+            st.dp_set_group(group.index(self.rank), [endpoints[r]["grads"] for r in group],
+                            [endpoints[r]["mailbox"] for r in group])
         torch.cuda.synchronize(st.device)
         dist.barrier()
 
@@ -234,7 +242,7 @@ class PipeBD:
         self._phase(1, self.stage.student_step)
         tr("student")
         g = self.groups.get(self.me.partition)
-        if g is not None:
+        if g is not None and self.grad_share == "nccl":
             dist.all_reduce(self.stage.grads(), op=dist.ReduceOp.SUM, group=g)
         tr("share")
         if not self.dpu:

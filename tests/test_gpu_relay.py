@@ -54,19 +54,33 @@ def run_inprocess(ex, schedule, b, steps, mode):
         p.set_shard(pl.count, pl.first)
         stages[r] = p
     streams = {r: torch.cuda.Stream() for r in stages}
-    if mode in ("peer", "peer-eager"):
+    if mode in ("peer", "peer-eager", "peer-dp"):
         eps = {r: {"input": p.input_ptr(), "mailbox": p.mailbox_ptr(), "row": p.row_bytes_in()}
                for r, p in stages.items()}
         for r, p in stages.items():
             recv, send = runtime.peer_wiring(schedule, b, r, eps)
             p.relay_set_recv(recv)
             p.relay_set_send(send)
-        if mode == "peer":
+        if mode == "peer-dp":  # gradients shared over peer memory, fused into the update
+            for part in schedule["partitions"]:
+                devs = part["devices"]
+                if len(devs) > 1:
+                    for r in devs:
+                        stages[r].dp_set_group(devs.index(r), [stages[q].grads_ptr() for q in devs],
+                                               [stages[q].mailbox_ptr() for q in devs])
+        if mode in ("peer", "peer-dp"):
             for r, p in stages.items():
                 p.capture_phases(fuse_teacher_student=True, stream=streams[r])
     torch.cuda.synchronize()
     nparts = len(schedule["partitions"])
     for _ in range(steps):
+        if mode == "peer-dp":  # the whole step of every rank is device-side: one graph each
+            for r, p in stages.items():
+                p.replay_phase(0, streams[r])
+            for r, p in stages.items():
+                p.replay_phase(2, streams[r])
+            torch.cuda.synchronize()
+            continue
         if mode == "peer":
             for r, p in stages.items():  # every rank's whole forward/backward, device-side relay
                 p.replay_phase(0, streams[r])
@@ -137,6 +151,23 @@ def test_resharded_hybrid_peer_relay_bitwise(ex):
         assert torch.equal(got[r][3], want[r][3]), r
 
 
+@pytest.mark.parametrize("parts,b", [([(0, 3, [0, 1])], 8), ([(0, 0, [0]), (1, 2, [1, 2]), (3, 3, [3])], 10),
+                                     ([(0, 1, [0, 1, 2]), (2, 3, [3, 4])], 7)])
+def test_dp_gradients_over_peer_memory_bitwise(ex, parts, b):
+    """share_gradient fused into the update (pbdx_dp_set_group): members read each other's gradient slabs
+    from peer memory and sum in member order — identical to the host-side sum, every member identical."""
+    s = sched(parts, b)
+    got = run_inprocess(ex, s, b, 3, "peer-dp")
+    want = run_inprocess(ex, s, b, 3, "copy")
+    for r in got:
+        assert torch.equal(got[r][0], want[r][0]), r
+        assert torch.equal(got[r][1], want[r][1]), r
+        assert got[r][2] == want[r][2], r
+    for _, _, devs in parts:
+        for r in devs[1:]:
+            assert torch.equal(got[r][0], got[devs[0]][0])  # DP members hold identical weights
+
+
 def test_peer_relay_many_steps_no_drift(ex):
     """Sequence flags keep advancing across many graph replays (the slot protocol never stalls)."""
     b = 4
@@ -179,6 +210,28 @@ def _ipc_worker(rank, world, port, schedule, b, steps, q):
         dist.barrier()
     finally:
         dist.destroy_process_group()
+
+
+def test_dp_group_across_processes_ipc(ex):
+    """[0-3]x2 in two processes: gradients shared through CUDA IPC mappings of each other's buffers."""
+    b, steps = 8, 3
+    s = sched([(0, 3, [0, 1])], b)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, s, b, steps, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r, params, losses = q.get(timeout=300)
+        res[r] = (params, losses)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    want = run_inprocess(ex, s, b, steps, "copy")
+    for r in (0, 1):
+        assert np.array_equal(res[r][0], want[r][0].numpy())
 
 
 def test_peer_relay_across_processes_ipc(ex):
