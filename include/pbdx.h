@@ -70,10 +70,15 @@ int pbdx_init_params(void* handle, void* stream);
 int pbdx_set_shard(void* handle, int n, int first);
 
 /* 0: block 0 input generated on device by Philox (synthetic data);
- * 1: block 0 input comes from pbdx_upload_images (host data, e2e path). */
+ * 1: block 0 input comes from pbdx_upload_images (host data, e2e path);
+ * 2: block 0 input staged by pbdx_stage_images into two slots (overlapped host input). */
 int pbdx_set_input_mode(void* handle, int external);
 /* host fp32 NHWC [n][32][32][3] (pinned for async) -> device padded bf16 input */
 int pbdx_upload_images(void* handle, const float* host, int n, void* stream);
+/* input mode 2 (double-buffered host input): copy the images of a step into staging slot 0/1 on any
+ * stream (a copy stream, overlapping the previous step); the step itself packs slot (step counter & 1),
+ * so one captured graph serves every step.  CIFAR model. */
+int pbdx_stage_images(void* handle, const float* host, int n, int slot, void* stream);
 
 int pbdx_teacher_forward(void* handle, void* stream);
 int pbdx_student_step(void* handle, void* stream);

@@ -50,7 +50,10 @@ void pbdx_destroy(void* handle) { delete P(handle); }
 
 int pbdx_init_params(void* h, void* st) { return guard([&] { P(h)->init_params(S(st)); }); }
 int pbdx_set_shard(void* h, int n, int first) { return guard([&] { P(h)->set_shard(n, first); }); }
-int pbdx_set_input_mode(void* h, int external) { return guard([&] { P(h)->set_external_input(external != 0); }); }
+int pbdx_set_input_mode(void* h, int external) { return guard([&] { P(h)->set_external_input(external); }); }
+int pbdx_stage_images(void* h, const float* host, int n, int slot, void* st) {
+  return guard([&] { P(h)->stage_images(host, n, slot, S(st)); });
+}
 int pbdx_upload_images(void* h, const float* host, int n, void* st) {
   return guard([&] { P(h)->upload_images(host, n, S(st)); });
 }

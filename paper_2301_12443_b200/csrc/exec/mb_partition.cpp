@@ -351,6 +351,7 @@ class MbPartition final : public PartitionBase {
   }
 
   void teacher_body(cudaStream_t st) override {
+    if (external_ == 2) throw BadArg("staged input (mode 2) is implemented for the CIFAR model");
     if (d_.block_lo == 0 && !external_)
       check(pbdk::philox_image(input_, n_, first_, step_, d_.global_batch, d_.seed_data, st, S_), "philox");
     for (size_t i = 0; i < tblocks_.size(); ++i) {

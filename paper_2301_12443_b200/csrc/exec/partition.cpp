@@ -184,7 +184,18 @@ class ResNetPartition final : public PartitionBase {
     check(pbdk::pack_image(stage_, input_, n, st), "pack image");
   }
 
+  void stage_images(const float* host, int n, int slot, cudaStream_t st) override {
+    if (d_.block_lo == 0 && n == n_ && (slot == 0 || slot == 1)) {
+      const size_t bytes = static_cast<size_t>(n) * 32 * 32 * 3 * sizeof(float);
+      cuda(cudaMemcpyAsync(slot == 0 ? stage_ : stage2_, host, bytes, cudaMemcpyHostToDevice, st), "H2D stage");
+      return;
+    }
+    throw BadArg("stage_images: partition 0 only, n == shard size, slot 0/1");
+  }
+
   void teacher_body(cudaStream_t st) override {
+    if (d_.block_lo == 0 && external_ == 2)
+      check(pbdk::pack_image_parity(stage_, stage2_, step_, input_, n_, st), "pack staged image");
     if (d_.block_lo == 0 && !external_)
       check(pbdk::philox_image(input_, n_, first_, step_, d_.global_batch, d_.seed_data, st), "philox");
     for (size_t i = 0; i < tblocks_.size(); ++i) {
@@ -292,7 +303,7 @@ class ResNetPartition final : public PartitionBase {
   }
 
   int body_launches_per_step() const override {
-    int n = (d_.block_lo == 0 && !external_) ? 1 : 0;
+    int n = (d_.block_lo == 0 && external_ != 1) ? 1 : 0;  // philox or staged pack
     for (const TBlock& tb : tblocks_) n += static_cast<int>(tb.convs.size());
     int trained = 0;
     for (size_t i = 0; i < sblocks_.size(); ++i) {
@@ -327,7 +338,10 @@ class ResNetPartition final : public PartitionBase {
     const int lo = d_.block_lo, hi = d_.block_hi;
     input_bytes_ = act_bytes(T_HW[lo], stored(T_CH[lo]));
     input_ = arena_.get<bf16>(input_bytes_);
-    if (lo == 0) stage_ = arena_.get<float>(static_cast<size_t>(d_.n_max) * 32 * 32 * 3 * sizeof(float));
+    if (lo == 0) {
+      stage_ = arena_.get<float>(static_cast<size_t>(d_.n_max) * 32 * 32 * 3 * sizeof(float));
+      stage2_ = arena_.get<float>(static_cast<size_t>(d_.n_max) * 32 * 32 * 3 * sizeof(float));
+    }
 
     // ---- teacher program
     size_t tw = 0;
@@ -510,6 +524,7 @@ class ResNetPartition final : public PartitionBase {
   bf16* input_ = nullptr;
   size_t input_bytes_ = 0;
   float* stage_ = nullptr;
+  float* stage2_ = nullptr;  // second staging slot (input mode 2)
   size_t tout_bytes_ = 0;
   bf16* tparams_ = nullptr;
   size_t tparam_bytes_ = 0;

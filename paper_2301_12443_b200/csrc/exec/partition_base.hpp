@@ -81,6 +81,8 @@ class PartitionBase {
   virtual void init_params(cudaStream_t st) = 0;
   virtual void rebuild_for_shard() = 0;  // n_ changed
   virtual void upload_images(const float* host, int n, cudaStream_t st) = 0;
+  // input mode 2: host images copied into staging slot 0/1 (any stream); the step packs slot (step & 1)
+  virtual void stage_images(const float*, int, int, cudaStream_t) { throw BadArg("model has no staged input"); }
   virtual void teacher_body(cudaStream_t st) = 0;
   // student blocks; fork: start from the caller's stream (standalone phase) instead of the
   // per-block teacher events.  Must join every side stream back into `caller`.
@@ -142,8 +144,9 @@ class PartitionBase {
     }
   }
 
-  void set_external_input(bool ext) {
-    external_ = ext;
+  void set_external_input(int mode) {
+    if (mode < 0 || mode > 2) throw BadArg("input mode 0/1/2");
+    external_ = mode;
     invalidate_graphs();
   }
 
@@ -459,7 +462,7 @@ class PartitionBase {
   uint32_t train_mask_ = 0xFFFFFFFFu;
   int n_ = 0;
   int first_ = 0;
-  bool external_ = false;
+  int external_ = 0;  // 0 synthetic (Philox), 1 upload_images, 2 staged double buffer
   bool timing_ = false;
   Arena arena_;
   // K11 relay state: mailbox_ = flags written by peers ([0,16) ready per sender, [16,32) consumed

@@ -107,6 +107,22 @@ __global__ void pack_image_kernel(const float* __restrict__ src, __nv_bfloat16* 
   }
 }
 
+// double-buffered host input: the graph packs staging slot (*counter & 1) — the host copies the next
+// step's images into the other slot while this step runs
+__global__ void pack_image_parity_kernel(const float* __restrict__ s0, const float* __restrict__ s1,
+                                         const long long* __restrict__ counter, __nv_bfloat16* __restrict__ x,
+                                         long long total) {
+  const float* __restrict__ src = (*counter & 1) ? s1 : s0;
+  for (long long pix = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; pix < total;
+       pix += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float v[8] = {src[pix * 3], src[pix * 3 + 1], src[pix * 3 + 2], 0, 0, 0, 0, 0};
+    const float z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint4* dst = reinterpret_cast<uint4*>(x + static_cast<size_t>(pix) * 16);
+    dst[0] = pack8(v);
+    dst[1] = pack8(z);
+  }
+}
+
 // dst[k][r][s][c_stored] = c < c_true ? U(-1,1)[counter=((k*r+..)*c_true+c, tensor)] * bound : 0
 __global__ void init_uniform_kernel(void* dst, int bf16_out, int k, int r, int s, int cs, int ct, uint32_t seed,
                                     uint32_t tensor, float bound) {
@@ -637,6 +653,14 @@ int philox_image(void* x, int n, long long first, const long long* counter, int 
 int pack_image(const float* src, void* x, int n, cudaStream_t st, int side) {
   const long long total = static_cast<long long>(n) * side * side;
   pack_image_kernel<<<grid_for(total), kThreads, 0, st>>>(src, static_cast<__nv_bfloat16*>(x), total);
+  return ok(cudaGetLastError());
+}
+
+int pack_image_parity(const float* s0, const float* s1, const long long* counter, void* x, int n, cudaStream_t st,
+                      int side) {
+  const long long total = static_cast<long long>(n) * side * side;
+  pack_image_parity_kernel<<<grid_for(total), kThreads, 0, st>>>(s0, s1, counter, static_cast<__nv_bfloat16*>(x),
+                                                                 total);
   return ok(cudaGetLastError());
 }
 

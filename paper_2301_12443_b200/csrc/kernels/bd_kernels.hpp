@@ -37,6 +37,8 @@ size_t reduce_workspace_floats(int m, int c, int nv);
 int philox_image(void* x, int n, long long first, const long long* counter, int gb, uint32_t seed, cudaStream_t st,
                  int side = 32);
 int pack_image(const float* src, void* x, int n, cudaStream_t st, int side = 32);
+int pack_image_parity(const float* s0, const float* s1, const long long* counter, void* x, int n, cudaStream_t st,
+                      int side = 32);
 int init_uniform(void* dst, int bf16_out, int k, int r, int s, int cs, int ct, uint32_t seed, uint32_t tensor,
                  float bound, cudaStream_t st);
 int fill(float* dst, size_t n, float v, cudaStream_t st);

@@ -58,6 +58,7 @@ def _bind(L):
     L.pbdx_set_shard.argtypes = [V, I, I]
     L.pbdx_set_input_mode.argtypes = [V, I]
     L.pbdx_upload_images.argtypes = [V, V, I, V]
+    L.pbdx_stage_images.argtypes = [V, V, I, I, V]
     L.pbdx_buffer.argtypes = [V, I, P(V), P(ctypes.c_size_t)]
     L.pbdx_num_blocks.argtypes = [V]
     L.pbdx_teacher_act.argtypes = [V, I, P(V), P(ctypes.c_size_t)]
@@ -290,8 +291,16 @@ class Partition:
         _check(lib().pbdx_set_shard(self.handle, n, first), "set_shard")
         self.n, self.first = n, first
 
-    def set_external_input(self, external: bool):
+    def set_external_input(self, external):
+        """False/0 synthetic (Philox on device), True/1 upload_images, 2 staged double buffer (stage_images)."""
         _check(lib().pbdx_set_input_mode(self.handle, int(external)), "set_input_mode")
+
+    def stage_images(self, host: torch.Tensor, slot: int, stream=None):
+        """Input mode 2: copy a step's host images (pinned fp32 NHWC) into staging slot 0/1 on `stream`;
+        the step packs slot (step counter & 1)."""
+        assert host.dtype == torch.float32 and not host.is_cuda and host.is_contiguous()
+        _check(lib().pbdx_stage_images(self.handle, ctypes.c_void_p(host.data_ptr()), host.shape[0], int(slot),
+                                       self._stream(stream)), "stage_images")
 
     def upload_images(self, host: torch.Tensor, stream=None):
         """host: fp32 NHWC [n, S, S, 3] (pinned for an async copy)."""

@@ -264,3 +264,25 @@ def test_dp_baseline_train_mask(ex):
     assert not only.block_state(0)[1].any()
     with pytest.raises(ValueError):
         only.set_train_mask(0)
+
+
+def test_staged_double_buffered_input_equals_upload(ex):
+    """Input mode 2 (pbdx_stage_images + parity pack inside the graph) == mode 1 (upload per step)."""
+    b = 8
+    hosts = [torch.empty(b, 32, 32, 3).uniform_(-1, 1).pin_memory() for _ in range(3)]
+    a = ex.Partition(0, 3, b, b)
+    a.init_params()
+    a.set_external_input(1)
+    for h in hosts:
+        a.upload_images(h)
+        a.step()
+    s = ex.Partition(0, 3, b, b)
+    s.init_params()
+    s.set_external_input(2)
+    s.capture()
+    for i, h in enumerate(hosts):
+        s.stage_images(h, i & 1)  # step counter starts at 0: step i packs slot i & 1
+        s.replay()
+    torch.cuda.synchronize()
+    assert a.losses() == s.losses()
+    assert torch.equal(a.params(), s.params())
