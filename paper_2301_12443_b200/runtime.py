@@ -604,24 +604,47 @@ def bench_pipeline(args, rank: int, world: int, local_rank: int) -> dict:
     ms, _ = timed(pipe, args.steps)
     losses = pipe.block_losses()
 
-    # e2e: partition-0 ranks upload their images from pinned host memory every step; the last
-    # partition reads its losses back to the host every step.
+    # e2e: partition-0 ranks copy every step's images from pinned host memory (CIFAR: staged double
+    # buffer on a copy stream, overlapped with the previous step; MBConv: upload per step); the last
+    # partition reads every step's losses back (on the host one step later).
     me = pipe.me
     host = None
+    stream = torch.cuda.current_stream(dev)
+    staged = model == "resnet"
     if me.partition == 0:
-        pipe.stage.set_external_input(True)
+        pipe.stage.set_external_input(2 if staged else 1)
         side = image or 32
         host = torch.empty(me.count, side, side, 3, dtype=torch.float32).pin_memory().uniform_(-1, 1)
         if getattr(pipe, "_graphs", False):
             pipe.use_graphs()  # re-capture without the on-device data generation
-    loss_host = torch.empty(len(pipe.stage.blocks), dtype=torch.float64).pin_memory()
+    loss_host = [torch.empty(len(pipe.stage.blocks), dtype=torch.float64).pin_memory() for _ in range(2)]
+    copy_stream = torch.cuda.Stream(dev)
+    ev_copy = [torch.cuda.Event() for _ in range(2)]
+    ev_done = [torch.cuda.Event() for _ in range(2)]
+    state = {"s": 0, "p0": int(pipe.stage.step_counter().item()) & 1 if staged and host is not None else 0}
 
     def hook(p, when):
+        s_ = state["s"]
+        cur, nxt = (state["p0"] + s_) & 1, (state["p0"] + s_ + 1) & 1
         if when == "pre" and host is not None:
-            p.stage.upload_images(host)
-        elif when == "post" and me.partition == pipe.nparts - 1:
-            loss_host.copy_(p.stage.losses_tensor(), non_blocking=True)
-            torch.cuda.current_stream(dev).synchronize()
+            if not staged:
+                p.stage.upload_images(host)
+                return
+            if s_ == 0:
+                p.stage.stage_images(host, cur, stream)
+                ev_copy[cur].record(stream)
+            if s_ >= 1:
+                copy_stream.wait_event(ev_done[nxt])
+            p.stage.stage_images(host, nxt, copy_stream)  # the next step's images, overlapped
+            ev_copy[nxt].record(copy_stream)
+            stream.wait_event(ev_copy[cur])
+        elif when == "post":
+            ev_done[cur].record(stream)
+            if me.partition == pipe.nparts - 1:
+                loss_host[cur].copy_(p.stage.losses_tensor(), non_blocking=True)
+                if s_ >= 1:
+                    ev_done[nxt].synchronize()  # the previous step's losses are on the host
+            state["s"] = s_ + 1
 
     _, e2e_ms = timed(pipe, args.steps, hook)
     all_losses = [None] * world
