@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--image", type=int, default=224, help="mbv2 image side")
     ap.add_argument("--relay", choices=["peer", "nccl"], default="peer",
                     help="N>1 teacher-activation relay: K11 peer stores over NVLink (default) or NCCL send/recv")
+    ap.add_argument("--no-ahd", action="store_true",
+                    help="N>1: search only contiguous one-group-per-partition schedules (pure pipeline)")
     ap.add_argument("--pipeline", action="store_true",
                     help="use the multi-GPU runtime (profile -> best_schedule -> PipeBD) even at N=1")
     return ap.parse_args()

@@ -562,7 +562,8 @@ def bench_pipeline(args, rank: int, world: int, local_rank: int) -> dict:
     obj = [None, None]
     if rank == 0:
         prof = profile_blocks(gb, world, device=dev, model=model, image=image, paths=paths)
-        sched, meta = core.best_schedule(prof)
+        # --no-ahd: contiguous_only (TR / pure pipeline, schedule.cpp:172-185; configs[1] at B = N = 4)
+        sched, meta = core.best_schedule(prof, contiguous_only=getattr(args, "no_ahd", False))
         obj = [sched, {"profile": prof, "meta": meta}]
     dist.broadcast_object_list(obj, src=0)
     sched, info = obj
