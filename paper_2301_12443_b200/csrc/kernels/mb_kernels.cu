@@ -185,6 +185,9 @@ __global__ void __launch_bounds__(kT) dw_wgrad_partial_kernel(const __nv_bfloat1
                                                               const __nv_bfloat16* __restrict__ dy,
                                                               float* __restrict__ partial, int N, int H, int W, int C,
                                                               int P, int Q, int lanes_c, int rows_per_chunk) {
+  // Thread = (channel group, row lane): walks whole output rows (n, p) of its chunk, q ascending, with the
+  // K input vectors of filter row r the current q touches held in a register window that slides by ST
+  // per q — one dy load and ST activation loads per pixel instead of 1 + K.
   constexpr int PAD = K / 2;
   __shared__ float red[kT * 8];
   const int G = C / 8;
@@ -203,27 +206,46 @@ __global__ void __launch_bounds__(kT) dw_wgrad_partial_kernel(const __nv_bfloat1
     for (int j = 0; j < 8; ++j) acc[s][j] = 0.0f;
   if (g < G && pl < lanes_p) {
     const int c0 = g * 8;
-    // pixel lanes stride over the chunk's (row, q) pairs in row-major order (32-bit indices)
-    const int npix = (r1 - r0) * Q;
-#pragma unroll 2
-    for (int idx = pl; idx < npix; idx += lanes_p) {
-      const int row = r0 + idx / Q;
-      const int q = idx - (row - r0) * Q;
+    for (int row = r0 + pl; row < r1; row += lanes_p) {
       const int p = row % P;
       const int n = row / P;
       const int h = p * ST + r - PAD;
       if (h < 0 || h >= H) continue;
       const __nv_bfloat16* arow = a + (static_cast<size_t>(n) * H + h) * W * C + c0;
-      float gv[8];
-      ld8(dy + (static_cast<size_t>(row) * Q + q) * C + c0, gv);
+      const __nv_bfloat16* grow = dy + static_cast<size_t>(row) * Q * C + c0;
+      float win[K][8];  // win[s] = a[h][q*ST + s - PAD] (zero outside the image)
 #pragma unroll
       for (int s = 0; s < K; ++s) {
-        const int w = q * ST + s - PAD;
-        if (w < 0 || w >= W) continue;
-        float av[8];
-        ld8(arow + static_cast<size_t>(w) * C, av);
+        const int w = s - PAD;
+        if (w >= 0 && w < W) {
+          ld8(arow + static_cast<size_t>(w) * C, win[s]);
+        } else {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[s][j] = fmaf(gv[j], av[j], acc[s][j]);
+          for (int j = 0; j < 8; ++j) win[s][j] = 0.0f;
+        }
+      }
+      for (int q = 0; q < Q; ++q) {
+        float gv[8];
+        ld8(grow + static_cast<size_t>(q) * C, gv);
+#pragma unroll
+        for (int s = 0; s < K; ++s)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[s][j] = fmaf(gv[j], win[s][j], acc[s][j]);
+        // slide by ST: the next q needs a[(q+1)*ST + s - PAD]
+#pragma unroll
+        for (int s = 0; s < K - ST; ++s)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) win[s][j] = win[s + ST][j];
+#pragma unroll
+        for (int t = 0; t < ST; ++t) {
+          const int w = (q + 1) * ST + (K - ST + t) - PAD;
+          if (w >= 0 && w < W) {
+            ld8(arow + static_cast<size_t>(w) * C, win[K - ST + t]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) win[K - ST + t][j] = 0.0f;
+          }
+        }
       }
     }
   }
@@ -585,8 +607,10 @@ WgradTiling dw_wgrad_tiling(const DwArgs& d) {
   t.lanes_c = std::min(G, 32);
   t.cwin = (G + t.lanes_c - 1) / t.lanes_c;
   const int rows = d.n * d.p;
-  const int target = 148 * 8;
-  t.chunks = std::max(1, std::min(rows, target / (t.cwin * d.k) + 1));
+  const int lanes_p = 256 / t.lanes_c;
+  const int target = 148 * 4;
+  // every row lane of a chunk walks >= 2 whole output rows
+  t.chunks = std::max(1, std::min(rows / (2 * lanes_p) + 1, target / (t.cwin * d.k) + 1));
   t.per_chunk = (rows + t.chunks - 1) / t.chunks;
   t.chunks = (rows + t.per_chunk - 1) / t.per_chunk;
   return t;
