@@ -350,8 +350,16 @@ class MbPartition final : public PartitionBase {
     check(pbdk::pack_image(stage_, input_, n, st, S_), "pack image");
   }
 
+  void stage_images(const float* host, int n, int slot, cudaStream_t st) override {
+    if (d_.block_lo != 0 || n != n_ || (slot != 0 && slot != 1))
+      throw BadArg("stage_images: partition 0 only, n == shard size, slot 0/1");
+    const size_t bytes = static_cast<size_t>(n) * S_ * S_ * 3 * sizeof(float);
+    cuda(cudaMemcpyAsync(slot == 0 ? stage_ : stage2_, host, bytes, cudaMemcpyHostToDevice, st), "H2D stage");
+  }
+
   void teacher_body(cudaStream_t st) override {
-    if (external_ == 2) throw BadArg("staged input (mode 2) is implemented for the CIFAR model");
+    if (d_.block_lo == 0 && external_ == 2)
+      check(pbdk::pack_image_parity(stage_, stage2_, step_, input_, n_, st, S_), "pack staged image");
     if (d_.block_lo == 0 && !external_)
       check(pbdk::philox_image(input_, n_, first_, step_, d_.global_batch, d_.seed_data, st, S_), "philox");
     for (size_t i = 0; i < tblocks_.size(); ++i) {
@@ -428,7 +436,7 @@ class MbPartition final : public PartitionBase {
   }
 
   int body_launches_per_step() const override {
-    int n = (d_.block_lo == 0 && !external_) ? 1 : 0;
+    int n = (d_.block_lo == 0 && external_ != 1) ? 1 : 0;
     for (const TBlock& tb : tblocks_) n += static_cast<int>(tb.ops.size());
     for (size_t bi = 0; bi < sblocks_.size(); ++bi) {
       if (!trains(static_cast<int>(bi))) continue;
@@ -581,7 +589,10 @@ class MbPartition final : public PartitionBase {
     // input of block lo: the padded image or a relayed activation
     input_bytes_ = act_bytes(lo);
     input_ = arena_.get<bf16>(input_bytes_);
-    if (lo == 0) stage_ = arena_.get<float>(static_cast<size_t>(N) * S_ * S_ * 3 * sizeof(float));
+    if (lo == 0) {
+      stage_ = arena_.get<float>(static_cast<size_t>(N) * S_ * S_ * 3 * sizeof(float));
+      stage2_ = arena_.get<float>(static_cast<size_t>(N) * S_ * S_ * 3 * sizeof(float));
+    }
 
     // ---- teacher program
     const bf16* prev = input_;
@@ -849,6 +860,7 @@ class MbPartition final : public PartitionBase {
   bf16* input_ = nullptr;
   size_t input_bytes_ = 0;
   float* stage_ = nullptr;
+  float* stage2_ = nullptr;
   std::vector<TBlock> tblocks_;
   std::vector<SBlock> sblocks_;
   size_t total_ = 0;

@@ -611,7 +611,7 @@ def bench_pipeline(args, rank: int, world: int, local_rank: int) -> dict:
     me = pipe.me
     host = None
     stream = torch.cuda.current_stream(dev)
-    staged = model == "resnet"
+    staged = True  # both models pack staged slots inside the step (input mode 2)
     if me.partition == 0:
         pipe.stage.set_external_input(2 if staged else 1)
         side = image or 32

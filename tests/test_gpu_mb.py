@@ -213,3 +213,23 @@ def test_reconfiguration_on_measured_drift(ex):
     best, _ = core.best_schedule(observed)
     assert new["partitions"] == best["partitions"]
     assert core.predicted_step_time(observed, new)["step_ms"] <= core.predicted_step_time(observed, sched0)["step_ms"]
+
+
+def test_staged_input_equals_upload(ex):
+    """Input mode 2 on the MBConv executor (stage slots packed by step parity) == per-step upload."""
+    b = 2
+    hosts = [torch.empty(b, S, S, 3).uniform_(-1, 1).pin_memory() for _ in range(3)]
+    a = make(ex, 0, 1, b)
+    a.set_external_input(1)
+    for h in hosts:
+        a.upload_images(h)
+        a.step()
+    s = make(ex, 0, 1, b)
+    s.set_external_input(2)
+    s.capture()
+    for i, h in enumerate(hosts):
+        s.stage_images(h, i & 1)
+        s.replay()
+    torch.cuda.synchronize()
+    assert a.losses() == s.losses()
+    assert torch.equal(a.params(), s.params())
