@@ -7,8 +7,10 @@ profile-gen, report — are the C++ binary lib/pbd, csrc/tools/pbd_cli.cpp).
       profile document (profile.hpp:30-86; the paper's profiling step)
   [torchrun ...] python -m paper_2301_12443_b200.cli run --schedule schedule.json [--model ...]
          [--global-batch B] [--steps K] [--trace report.json] [--gantt timeline.svg]
-      run a schedule with one process per GPU (K11 peer relay, NCCL allreduce) and optionally write the
-      measured-timeline report + Gantt chart
+         [--resume DIR] [--save DIR]
+      run a schedule with one process per GPU (K11 peer relay, gradients over peer memory) and
+      optionally write the measured-timeline report + Gantt chart; --resume / --save restore / write
+      a per-block checkpoint (runtime.PipeBD.save_checkpoint, schedule-independent)
 
 Exit codes follow the reference CLI (pbd_cli.cpp:29-32): 0 ok, 1 validation, 2 infeasible, 3 I/O.
 """
@@ -70,9 +72,15 @@ def _run(a) -> int:
             return p
 
         pipe = runtime.PipeBD(sched, a.global_batch, make, relay="peer")
+        if a.resume:
+            meta = pipe.load_checkpoint(a.resume)
+            if rank == 0:
+                print(f"resumed at step {meta['step']} from {a.resume}", file=sys.stderr)
         for _ in range(a.steps):
             pipe.step()
         losses = pipe.block_losses()
+        if a.save:
+            pipe.save_checkpoint(a.save)
         rep = runtime.measured_report(pipe, max(4, a.trace_steps)) if (a.trace or a.gantt) else None
         gathered = [None] * world
         dist.all_gather_object(gathered, losses)
@@ -111,6 +119,8 @@ def main(argv=None) -> int:
     r.add_argument("--trace")
     r.add_argument("--trace-steps", type=int, default=8)
     r.add_argument("--gantt")
+    r.add_argument("--resume")
+    r.add_argument("--save")
     a = ap.parse_args(argv)
     try:
         return _profile(a) if a.cmd == "profile" else _run(a)

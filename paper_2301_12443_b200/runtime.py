@@ -340,6 +340,76 @@ class PipeBD:
         if getattr(self, "_graphs", False):
             self.use_graphs()
 
+    # -- checkpoint / resume (the reference persists only profile/schedule/report JSON)
+    def save_checkpoint(self, path: str):
+        """Write every student block's fp32 weights + momentum and the data stream's step index
+        under directory `path` (collective: call on every rank at a step boundary).
+
+        One file per block, written by the first member of the block's DP group (members hold
+        identical state after the group's gradient share), so a checkpoint is independent of the
+        schedule that wrote it: load_checkpoint() under any other schedule / world size resumes
+        bit-identically.  Layout: meta.json + block_KK.bin = weights then momentum, little-endian
+        fp32 in the executor's padded student layout (executor.Partition.block_state)."""
+        import os
+        self._finish_sends()
+        os.makedirs(path, exist_ok=True)
+        dist.barrier()
+        if self.me.index == 0:
+            for k in range(self.me.block_lo, self.me.block_hi + 1):
+                w, v = (t.detach().to("cpu", torch.float32).contiguous() for t in self.stage.block_state(k))
+                tmp = os.path.join(path, f".block_{k:02d}.bin.{self.rank}")
+                with open(tmp, "wb") as f:
+                    f.write(w.numpy().tobytes())
+                    f.write(v.numpy().tobytes())
+                os.replace(tmp, os.path.join(path, f"block_{k:02d}.bin"))
+        sizes = {k: int(self.stage.block_state(k)[0].numel()) for k in range(self.me.block_lo, self.me.block_hi + 1)}
+        gathered = [None] * self.world
+        dist.all_gather_object(gathered, (sizes, int(self.stage.step_index())))
+        if self.rank == 0:
+            steps = {s for _, s in gathered}
+            if len(steps) != 1:
+                raise RuntimeError(f"ranks disagree on the step index: {sorted(steps)}")
+            meta = {"format": "pbd-b200-checkpoint/1", "global_batch": self.b, "step": steps.pop(),
+                    "block_numel": {str(k): n for d, _ in gathered for k, n in sorted(d.items())},
+                    "schedule": self.schedule}
+            tmp = os.path.join(path, ".meta.json.tmp")
+            with open(tmp, "w") as f:
+                json.dump(meta, f, indent=1, sort_keys=True)
+            os.replace(tmp, os.path.join(path, "meta.json"))
+        dist.barrier()
+
+    def load_checkpoint(self, path: str) -> dict:
+        """Restore this rank's blocks and the step index from a save_checkpoint() directory (written
+        under any schedule).  Raises ValueError on a global-batch or block-size mismatch, OSError on
+        missing files.  Returns the checkpoint's meta document."""
+        import os
+        import numpy as np
+        with open(os.path.join(path, "meta.json")) as f:
+            meta = json.load(f)
+        if meta.get("format") != "pbd-b200-checkpoint/1":
+            raise ValueError(f"not a pbd-b200 checkpoint: {meta.get('format')!r}")
+        if meta["global_batch"] != self.b:
+            raise ValueError(f"checkpoint global batch {meta['global_batch']} != {self.b} (the data stream "
+                             "index is per global batch)")
+        self._finish_sends()
+        for k in range(self.me.block_lo, self.me.block_hi + 1):
+            n = int(self.stage.block_state(k)[0].numel())
+            if meta["block_numel"].get(str(k)) != n:
+                raise ValueError(f"block {k}: checkpoint holds {meta['block_numel'].get(str(k))} parameters, "
+                                 f"this model {n}")
+            raw = np.fromfile(os.path.join(path, f"block_{k:02d}.bin"), dtype="<f4")
+            if raw.size != 2 * n:
+                raise ValueError(f"block {k}: truncated state file ({raw.size} of {2 * n} floats)")
+            dev = _dev_of(self.stage)
+            w = torch.from_numpy(raw[:n].copy()).to(dev)
+            v = torch.from_numpy(raw[n:].copy()).to(dev)
+            self.stage.set_block_state(k, w, v)
+        self.stage.set_step_index(int(meta["step"]))
+        if _dev_of(self.stage).type == "cuda":
+            torch.cuda.synchronize(_dev_of(self.stage))
+        dist.barrier()
+        return meta
+
     def block_losses(self) -> Dict[int, float]:
         """Per-block loss of the last step summed over each DP group (the global-batch MSE)."""
         local = self.stage.losses()

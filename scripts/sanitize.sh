@@ -1,0 +1,24 @@
+#!/bin/bash
+# compute-sanitizer (memcheck / racecheck / synccheck) over small steps of every executor path
+mkdir -p gpurun_out
+cat > /tmp/san_step.py <<'PY'
+import os, sys
+sys.path.insert(0, os.getcwd())
+import torch
+from paper_2301_12443_b200 import executor as ex
+p = ex.Partition(0, 3, 4, 4); p.init_params()
+for _ in range(2): p.step()
+p.capture(); p.replay()
+m = ex.Partition(0, 5, 2, 2, model="mbv2", image=64); m.init_params()
+for k in range(6): m.set_path(k, [0] * ex.mb_layers(k))
+for _ in range(2): m.step()
+e = ex.Partition(0, 5, 2, 2, model="effb0", image=64); e.init_params()
+for k in range(6): e.set_path(k, [5 if c > 1 else 0 for c in range(ex.mb_layers(k, "effb0"))] if k else [0, 0, 5, 5])
+e.step()
+torch.cuda.synchronize()
+print("ok", p.losses(), m.losses(), e.losses())
+PY
+for tool in memcheck racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python /tmp/san_step.py > gpurun_out/sanitize_$tool.log 2>&1
+  echo "$tool rc=$? $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY|Errors' gpurun_out/sanitize_$tool.log | tail -1)"
+done

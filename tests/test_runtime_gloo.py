@@ -242,3 +242,81 @@ def test_mbv2_hybrid_distributed_equals_single_process():
             assert v == pytest.approx(want[k], rel=1e-12, abs=1e-15), (rank, k)
         for k, p in params.items():
             np.testing.assert_allclose(p, tr.sp[k], rtol=1e-6, atol=1e-9)
+
+
+def _ckpt_worker(rank, world, port, schedule, b, steps, path, mode, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    torch.set_num_threads(2)
+    from tests.oracle_stage import OracleStage
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        pipe = runtime.PipeBD(schedule, b, lambda lo, hi, n, first: OracleStage(lo, hi, n, first, b))
+        if mode == "resume":
+            try:
+                meta = pipe.load_checkpoint(path)
+            except ValueError as e:
+                q.put((rank, "error", str(e)))
+                return
+            assert meta["step"] == steps
+        for _ in range(steps):
+            pipe.step()
+        pipe.end_epoch()
+        if mode == "save":
+            pipe.save_checkpoint(path)
+        q.put((rank, pipe.block_losses(), {k: pipe.stage.sp[k].copy() for k in pipe.stage.blocks}))
+    finally:
+        dist.destroy_process_group()
+
+
+def _spawn(target, world, *args):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=target, args=(r, world, port) + args + (q,)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return out
+
+
+def test_checkpoint_resume_under_another_schedule(tmp_path):
+    """save_checkpoint on 3 ranks ([0]x2 -> [1-3]x1), resume on 2 ranks ([0-1] -> [2-3]): the resumed
+    run equals one uninterrupted single-process run with A's then B's DP shards."""
+    from oracle import bd
+    b, steps = 5, 2
+    parts_a = [(0, 0, [0, 1]), (1, 3, [2])]
+    parts_b = [(0, 1, [0]), (2, 3, [1])]
+    ck = str(tmp_path / "ckpt")
+    _spawn(_ckpt_worker, 3, sched(parts_a, b), b, steps, ck, "save")
+    assert sorted(os.listdir(ck)) == ["block_00.bin", "block_01.bin", "block_02.bin", "block_03.bin", "meta.json"]
+    out = _spawn(_ckpt_worker, 2, sched(parts_b, b), b, steps, ck, "resume")
+
+    def groups(parts):
+        return {k: len(devs) for lo, hi, devs in parts for k in range(lo, hi + 1)}
+
+    tr = bd.Trainer(b, bf16_mode=1)
+    for st in range(steps):
+        tr.step(st, groups(parts_a))
+    for st in range(steps, 2 * steps):
+        want = tr.step(st, groups(parts_b))
+    for rank, losses, params in out:
+        for k, v in losses.items():
+            assert v == pytest.approx(want[k], rel=1e-12, abs=1e-15), (rank, k)
+        for k, p in params.items():
+            np.testing.assert_allclose(p, tr.sp[k], rtol=1e-6, atol=1e-9)
+
+
+def test_checkpoint_rejects_mismatch(tmp_path):
+    import json
+    ck = str(tmp_path / "ckpt")
+    b = 5
+    _spawn(_ckpt_worker, 1, sched([(0, 3, [0])], b), b, 1, ck, "save")
+    meta = json.load(open(os.path.join(ck, "meta.json")))
+    assert meta["step"] == 1 and meta["global_batch"] == b and set(meta["block_numel"]) == {"0", "1", "2", "3"}
+    (rank, tag, msg), = _spawn(_ckpt_worker, 1, sched([(0, 3, [0])], 7), 7, 1, ck, "resume")
+    assert tag == "error" and "global batch" in msg
