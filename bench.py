@@ -180,16 +180,19 @@ def time_dominant_kernel(torch, batch):
 
 
 # ---------------------------------------------------------------- CPU legs
-def cpu_oracle_rate(samples_per_step=32, steps=6):
-    """The oracle (C restatement, OpenMP) on the host cores: samples/s over `steps` bounded steps."""
+def cpu_oracle_rate(samples_per_step=32, budget_s=10.0, max_steps=64):
+    """The oracle (C restatement, OpenMP) on the host cores: samples/s over as many whole steps as fit
+    in about `budget_s` seconds of CPU work (bounded sample of the same workload)."""
     from oracle import bd
     tr = bd.Trainer(samples_per_step, bf16_mode=1)
     tr.step(0)  # warm (allocation, page faults)
     t0 = time.perf_counter()
-    for s in range(steps):
-        tr.step(1 + s)
+    steps = 0
+    while steps < max_steps and (steps < 2 or time.perf_counter() - t0 < budget_s):
+        tr.step(1 + steps)
+        steps += 1
     dt = time.perf_counter() - t0
-    return samples_per_step * steps / dt, bd.lib().bdo_threads(), dt
+    return samples_per_step * steps / dt, bd.lib().bdo_threads(), dt, steps
 
 
 def run_reference(args, rank, world):
@@ -370,9 +373,9 @@ def run_ours(args, rank, world, local_rank):
 
     cpu = None
     if not args.no_cpu_baseline:
-        rate, cores, dt = cpu_oracle_rate()
+        rate, cores, dt, nsteps = cpu_oracle_rate()
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"32 samples x 6 steps of the same workload (oracle/bd_oracle.c, {dt:.1f} s)"}
+               "sample": f"32 samples x {nsteps} steps of the same workload (oracle/bd_oracle.c, {dt:.1f} s)"}
 
     working_set = models.step_working_set_bytes(b)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,

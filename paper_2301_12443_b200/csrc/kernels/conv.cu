@@ -1193,6 +1193,158 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// Multi-tap wgrad for narrow inputs (c = CB in {16, 32}, k <= 128): ONE CTA computes every tap of
+// the filter for its pixel range.  Per 128-pixel stage it loads the dy box once (A, MN-major) and
+// the TAPS shifted x boxes side by side as the N atoms of B, so one MMA covers up to 256/CB taps:
+// D[k][tap*CB + c] = dW[k][tap][c] is exactly the row-major filter-gradient layout.  Versus the
+// per-tap kernel (one CTA per tap) this reads dy once instead of TAPS times and replaces TAPS
+// narrow MMAs (each re-reading the whole 128-row A from shared memory) with one or two wide ones.
+// A's rows beyond k (M = 128) are never loaded: their atoms alias the B region (read, discarded).
+template <int CB, int SWA, int AAT, int TAPS>
+struct WgradMtCfg {
+  static constexpr int KT = 128;
+  static constexpr int SWB = 2 * CB;
+  static constexpr int A_ATOM = KT * SWA;
+  static constexpr int B_ATOM = KT * SWB;
+  static constexpr int G0 = TAPS < 256 / CB ? TAPS : 256 / CB;  // taps in MMA group 0
+  static constexpr int G1 = TAPS - G0;
+  static constexpr int N0 = G0 * CB, N1 = G1 * CB;
+  static constexpr int STAGE = round_up(AAT * A_ATOM + TAPS * B_ATOM, 1024);
+  static constexpr int STAGES = (kSmemBudget / STAGE) > 6 ? 6 : (kSmemBudget / STAGE);
+  static constexpr int TMEM_COLS = tmem_cols_for(N0 + N1);
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+  static_assert(N1 <= 256 && N0 + N1 <= 512, "taps x channels must fit two MMAs / TMEM");
+  static_assert(STAGE >= 128 * KT * 2, "aliased A atoms must stay inside the stage");
+};
+
+template <int CB, int SWA, int AAT, int TAPS>
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_wgrad_mt_kernel(const __grid_constant__ CUtensorMap tmdy, const __grid_constant__ CUtensorMap tmx,
+                         const WgradArgs a) {
+  using C = WgradMtCfg<CB, SWA, AAT, TAPS>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int split = blockIdx.x;
+  const int mt0 = split * a.tiles_per_split;
+  const int mt1 = min(a.m_tiles, mt0 + a.tiles_per_split);
+  const int num_kb = max(0, mt1 - mt0);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmdy);
+    tma_prefetch(&tmx);
+    for (int i = 0; i < C::STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(tfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      constexpr uint32_t bytes = static_cast<uint32_t>(AAT * C::A_ATOM + TAPS * C::B_ATOM);
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int st = kb % C::STAGES;
+        if (kb >= C::STAGES) mbar_wait(&empty[st], ((kb / C::STAGES) - 1) & 1);
+        const int mt = mt0 + kb;
+        const int tq = mt % a.tiles_q;
+        const int t2 = mt / a.tiles_q;
+        const int tp = t2 % a.tiles_p;
+        const int tn = t2 / a.tiles_p;
+        const int ow0 = tq * a.bw, oh0 = tp * a.bh, n0 = tn * a.bn;
+        uint8_t* sa = smem + st * C::STAGE;
+        uint8_t* sb = sa + AAT * C::A_ATOM;
+        mbar_arrive_expect_tx(&full[st], bytes);
+#pragma unroll
+        for (int i = 0; i < AAT; ++i) tma_load_4d(sa + i * C::A_ATOM, &tmdy, &full[st], i * (SWA / 2), ow0, oh0, n0);
+#pragma unroll
+        for (int t = 0; t < TAPS; ++t) {
+          const int rr = t / a.s, ss = t - (t / a.s) * a.s;
+          tma_load_4d(sb + t * C::B_ATOM, &tmx, &full[st], 0, ow0 * a.stride + ss - a.pad, oh0 * a.stride + rr - a.pad,
+                      n0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc0 = umma_idesc_bf16(128, C::N0, 1, 1);
+      constexpr uint32_t idesc1 = umma_idesc_bf16(128, C::N1 > 0 ? C::N1 : 16, 1, 1);
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int st = kb % C::STAGES;
+        mbar_wait(&full[st], (kb / C::STAGES) & 1);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + st * C::STAGE);
+        const uint32_t sb = sa + AAT * C::A_ATOM;
+#pragma unroll
+        for (int kk = 0; kk < C::KT / 16; ++kk) {
+          const uint32_t acc = (kb | kk) != 0 ? 1u : 0u;
+          const uint64_t ad = umma_smem_desc(sa + kk * 16 * SWA, C::A_ATOM, 8 * SWA, layout_for_sw(SWA));
+          const uint64_t b0 = umma_smem_desc(sb + kk * 16 * C::SWB, C::B_ATOM, 8 * C::SWB, layout_for_sw(C::SWB));
+          umma_bf16(tmem, ad, b0, idesc0, acc);
+          if constexpr (C::N1 > 0) {
+            const uint64_t b1 = umma_smem_desc(sb + C::G0 * C::B_ATOM + kk * 16 * C::SWB, C::B_ATOM, 8 * C::SWB,
+                                               layout_for_sw(C::SWB));
+            umma_bf16(tmem + C::N0, ad, b1, idesc1, acc);
+          }
+        }
+        umma_commit(&empty[st]);
+      }
+      if (num_kb > 0) umma_commit(tfull);
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int co = quarter * 32 + lane;
+    constexpr int NC = TAPS * CB;
+    float* dst_row = a.out + static_cast<size_t>(split) * a.k * NC + static_cast<size_t>(co) * NC;
+    if (num_kb > 0) {
+      mbar_wait(tfull, 0);
+      tc_fence_after();
+      const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+#pragma unroll 1
+      for (int c0 = 0; c0 < NC; c0 += 16) {
+        float v[16];
+        tmem_ld16(trow + c0, v);
+        if (co < a.k) {
+          float4* d4 = reinterpret_cast<float4*>(dst_row + c0);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        }
+      }
+    } else if (co < a.k) {
+      for (int c0 = 0; c0 < NC; c0 += 4) *reinterpret_cast<float4*>(dst_row + c0) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+template <int CB, int SWA, int AAT, int TAPS>
+cudaError_t launch_wgrad_mt(const WgradPlan& p, cudaStream_t stream) {
+  using C = WgradMtCfg<CB, SWA, AAT, TAPS>;
+  if (stream == reinterpret_cast<cudaStream_t>(-1)) {
+    return cudaFuncSetAttribute(conv_wgrad_mt_kernel<CB, SWA, AAT, TAPS>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  }
+  conv_wgrad_mt_kernel<CB, SWA, AAT, TAPS><<<p.grid, kThreads, C::SMEM, stream>>>(p.tmdy, p.tmx, p.args);
+  return cudaGetLastError();
+}
+
 template <int BN, int SWA, int SWB>
 cudaError_t launch_wgrad(const WgradPlan& p, cudaStream_t stream) {
   using C = WgradCfg<BN, SWA, SWB>;
@@ -1371,6 +1523,28 @@ WgradLauncher pick_wgrad(int bn, int swa, int swb) {
 }
 
 int wgrad_bn(int c) { return c % 128 == 0 ? 128 : c >= 64 ? 64 : c; }  // c in {16, 32} or a multiple of 64
+
+// multi-tap wgrad (conv_wgrad_mt_kernel): 3x3 filters, c in {16, 32}, k <= 128, >= 2 pipeline stages
+template <int CB>
+WgradLauncher pick_wgrad_mt_c(int swa, int aat) {
+  if (swa == 32 && aat == 1) return launch_wgrad_mt<CB, 32, 1, 9>;
+  if (swa == 64 && aat == 1) return launch_wgrad_mt<CB, 64, 1, 9>;
+  if (swa == 128 && aat == 1) return launch_wgrad_mt<CB, 128, 1, 9>;
+  if constexpr (CB == 16)
+    if (swa == 128 && aat == 2) return launch_wgrad_mt<CB, 128, 2, 9>;
+  return nullptr;
+}
+
+WgradLauncher pick_wgrad_mt(const pbdk_conv_desc& d) {
+  static const bool off = [] {
+    const char* e = std::getenv("PBDK_WGRAD_MT");
+    return e != nullptr && e[0] == '0';
+  }();
+  if (off || d.r * d.s != 9 || d.k > 128 || (d.c != 16 && d.c != 32)) return nullptr;
+  const int swa = chan_block(d.k) * 2;
+  const int aat = (std::min(128, d.k) + swa / 2 - 1) / (swa / 2);
+  return d.c == 16 ? pick_wgrad_mt_c<16>(swa, aat) : pick_wgrad_mt_c<32>(swa, aat);
+}
 
 template <int BKC>
 FpropLauncher pick_splitk(int bn) {
@@ -1598,7 +1772,15 @@ int fprop_run(const FpropPlan& plan, cudaStream_t stream) {
   return plan.launch(plan, stream) == cudaSuccess ? PBDK_OK : PBDK_ECUDA;
 }
 
+// the multi-tap kernel wants >= 4 pixel tiles per CTA in one wave (else the per-tap grid, whose
+// CTAs split the taps, fills the GPU with far fewer partial slabs)
+bool use_wgrad_mt(const ConvGeom& g) { return pick_wgrad_mt(g.d) != nullptr && g.m_tiles >= 4 * num_sms(); }
+
 int wgrad_splits(const ConvGeom& g) {
+  if (use_wgrad_mt(g)) {  // one CTA per split covers every tap: one wave of splits
+    const int tps = (g.m_tiles + num_sms() - 1) / num_sms();
+    return (g.m_tiles + tps - 1) / tps;
+  }
   const int co_tiles = (g.d.k + 127) / 128;
   const int ci_tiles = g.d.c / wgrad_bn(g.d.c);
   const int tiles = co_tiles * ci_tiles * g.d.r * g.d.s;
@@ -1624,8 +1806,9 @@ int wgrad_plan(const pbdk_conv_desc& d, const void* x, const void* dy, float* dw
   if (!make_geom(d, &g) || !chan_ok(d.c) || !chan_ok(d.k)) return PBDK_EINVAL;
   const int swa = chan_block(d.k) * 2;
   const int swb = chan_block(d.c) * 2;
-  const int bn = wgrad_bn(d.c);
-  WgradLauncher l = pick_wgrad(bn, swa, swb);
+  const WgradLauncher mt = use_wgrad_mt(g) ? pick_wgrad_mt(d) : nullptr;
+  const int bn = mt != nullptr ? d.c : wgrad_bn(d.c);
+  WgradLauncher l = mt != nullptr ? mt : pick_wgrad(bn, swa, swb);
   if (l == nullptr) return PBDK_EINVAL;
   const int splits = wgrad_splits(g);
   const size_t slab = static_cast<size_t>(d.k) * d.r * d.s * d.c;
@@ -1653,7 +1836,9 @@ int wgrad_plan(const pbdk_conv_desc& d, const void* x, const void* dy, float* dw
   a.tiles_per_split = (g.m_tiles + splits - 1) / splits;
   a.a_atoms = (std::min(128, d.k) + swa / 2 - 1) / (swa / 2);
   a.out = splits > 1 ? static_cast<float*>(ws) : dw;
-  plan->grid = dim3(static_cast<unsigned>(a.co_tiles * a.ci_tiles * d.r * d.s), static_cast<unsigned>(splits), 1);
+  plan->grid = mt != nullptr ? dim3(static_cast<unsigned>(splits), 1, 1)
+                              : dim3(static_cast<unsigned>(a.co_tiles * a.ci_tiles * d.r * d.s),
+                                     static_cast<unsigned>(splits), 1);
   plan->splits = splits;
   plan->bn_tile = bn;
   plan->dw = dw;

@@ -66,7 +66,13 @@ def test_conv_fprop_epilogues(L, case, epi):
     assert err <= 2e-2 * ref.abs().max().item() + 1e-3
 
 
-@pytest.mark.parametrize("case", CASES)
+WGRAD_EXTRA = [  # narrow inputs -> the multi-tap kernel (every tap in one CTA), k = 16 .. 128
+    (4, 32, 16, 16, 3, 1), (4, 32, 32, 32, 3, 1), (2, 32, 16, 128, 3, 1), (2, 32, 32, 128, 3, 1),
+    (96, 32, 16, 32, 3, 1), (96, 32, 32, 64, 3, 1), (96, 32, 16, 16, 3, 1), (96, 32, 32, 32, 3, 1),
+    (96, 32, 16, 128, 3, 1), (384, 16, 32, 64, 3, 1), (64, 32, 16, 32, 3, 1)]
+
+
+@pytest.mark.parametrize("case", CASES + WGRAD_EXTRA)
 def test_conv_wgrad(L, case):
     n, h, c, k, r, st = case
     d = desc(L, n, h, c, k, r, st)
@@ -116,3 +122,23 @@ def test_unsupported_shapes_fail_loudly(L):
     x = torch.zeros(2, 30, 30, 64, device="cuda", dtype=torch.bfloat16)
     assert L.lib().pbdk_conv_fprop(ctypes.byref(d), x.data_ptr(), x.data_ptr(), x.data_ptr(), None, None, 0,
                                    stream()) == 1
+
+
+@pytest.mark.parametrize("case", [(96, 32, 16, 32, 3, 1), (96, 32, 32, 64, 3, 1), (32, 16, 128, 128, 3, 1)])
+def test_conv_wgrad_deterministic(L, case):
+    """Split partials are summed in split order: two runs are bit-identical."""
+    n, h, c, k, r, st = case
+    d = desc(L, n, h, c, k, r, st)
+    torch.manual_seed(11)
+    x = (torch.rand(n, h, h, c, device="cuda") * 2 - 1).bfloat16()
+    dy = (torch.rand(n, d.p, d.q, k, device="cuda") * 2 - 1).bfloat16()
+    wsb = L.lib().pbdk_conv_wgrad_workspace_bytes(ctypes.byref(d))
+    ws = torch.empty(max(wsb, 16), device="cuda", dtype=torch.uint8)
+    outs = []
+    for _ in range(2):
+        dw = torch.empty(k, r, r, c, device="cuda")
+        assert L.lib().pbdk_conv_wgrad(ctypes.byref(d), x.data_ptr(), dy.data_ptr(), dw.data_ptr(), ws.data_ptr(),
+                                       wsb, stream()) == 0
+        outs.append(dw)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
