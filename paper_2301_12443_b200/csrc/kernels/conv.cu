@@ -1203,7 +1203,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int CB, int SWA, int AAT, int TAPS>
 struct WgradMtCfg {
   static constexpr int KT = 128;
-  static constexpr int SWB = 2 * CB;
+  static constexpr int SWB = 2 * CB;  // CB <= 64: one swizzle atom of B per tap
   static constexpr int A_ATOM = KT * SWA;
   static constexpr int B_ATOM = KT * SWB;
   static constexpr int G0 = TAPS < 256 / CB ? TAPS : 256 / CB;  // taps in MMA group 0
@@ -1232,6 +1232,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = warp_id();
   const int lane = lane_id();
   const int split = blockIdx.x;
+  // blockIdx.y = (tap group, co tile, ci tile), ci fastest
+  int grp = blockIdx.y;
+  const int ci0 = (grp % a.ci_tiles) * CB;
+  grp /= a.ci_tiles;
+  const int co0 = (grp % a.co_tiles) * 128;
+  const int tap0 = (grp / a.co_tiles) * TAPS;
   const int mt0 = split * a.tiles_per_split;
   const int mt1 = min(a.m_tiles, mt0 + a.tiles_per_split);
   const int num_kb = max(0, mt1 - mt0);
@@ -1268,12 +1274,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* sb = sa + AAT * C::A_ATOM;
         mbar_arrive_expect_tx(&full[st], bytes);
 #pragma unroll
-        for (int i = 0; i < AAT; ++i) tma_load_4d(sa + i * C::A_ATOM, &tmdy, &full[st], i * (SWA / 2), ow0, oh0, n0);
+        for (int i = 0; i < AAT; ++i)
+          tma_load_4d(sa + i * C::A_ATOM, &tmdy, &full[st], co0 + i * (SWA / 2), ow0, oh0, n0);
 #pragma unroll
         for (int t = 0; t < TAPS; ++t) {
-          const int rr = t / a.s, ss = t - (t / a.s) * a.s;
-          tma_load_4d(sb + t * C::B_ATOM, &tmx, &full[st], 0, ow0 * a.stride + ss - a.pad, oh0 * a.stride + rr - a.pad,
-                      n0);
+          const int rr = (tap0 + t) / a.s, ss = (tap0 + t) - rr * a.s;
+          tma_load_4d(sb + t * C::B_ATOM, &tmx, &full[st], ci0, ow0 * a.stride + ss - a.pad,
+                      oh0 * a.stride + rr - a.pad, n0);
         }
       }
     }
@@ -1305,25 +1312,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     const int quarter = warp & 3;
-    const int co = quarter * 32 + lane;
-    constexpr int NC = TAPS * CB;
-    float* dst_row = a.out + static_cast<size_t>(split) * a.k * NC + static_cast<size_t>(co) * NC;
+    const int co = co0 + quarter * 32 + lane;
+    const int taps = a.r * a.s;
+    // D column t*CB + c = dW[co][tap0 + t][ci0 + c]
+    float* dst_row = a.out + static_cast<size_t>(split) * a.k * taps * a.c + (static_cast<size_t>(co) * taps + tap0) * a.c + ci0;
     if (num_kb > 0) {
       mbar_wait(tfull, 0);
       tc_fence_after();
       const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
 #pragma unroll 1
-      for (int c0 = 0; c0 < NC; c0 += 16) {
+      for (int c0 = 0; c0 < TAPS * CB; c0 += 16) {
         float v[16];
         tmem_ld16(trow + c0, v);
         if (co < a.k) {
-          float4* d4 = reinterpret_cast<float4*>(dst_row + c0);
+          float4* d4 = reinterpret_cast<float4*>(dst_row + (c0 / CB) * a.c + c0 % CB);
 #pragma unroll
           for (int j = 0; j < 4; ++j) d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
         }
       }
     } else if (co < a.k) {
-      for (int c0 = 0; c0 < NC; c0 += 4) *reinterpret_cast<float4*>(dst_row + c0) = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int c0 = 0; c0 < TAPS * CB; c0 += 4)
+        *reinterpret_cast<float4*>(dst_row + (c0 / CB) * a.c + c0 % CB) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
   tc_fence_before();
@@ -1524,7 +1533,8 @@ WgradLauncher pick_wgrad(int bn, int swa, int swb) {
 
 int wgrad_bn(int c) { return c % 128 == 0 ? 128 : c >= 64 ? 64 : c; }  // c in {16, 32} or a multiple of 64
 
-// multi-tap wgrad (conv_wgrad_mt_kernel): 3x3 filters, c in {16, 32}, k <= 128, >= 2 pipeline stages
+// multi-tap wgrad (conv_wgrad_mt_kernel) for 3x3 filters: c in {16, 32} with all 9 taps per CTA (k <= 128),
+// or c = 64 with one filter row (3 taps, N = 192) per CTA (any k: 128-row co tiles)
 template <int CB>
 WgradLauncher pick_wgrad_mt_c(int swa, int aat) {
   if (swa == 32 && aat == 1) return launch_wgrad_mt<CB, 32, 1, 9>;
@@ -1535,14 +1545,21 @@ WgradLauncher pick_wgrad_mt_c(int swa, int aat) {
   return nullptr;
 }
 
+int wgrad_mt_taps(const pbdk_conv_desc& d) { return d.c >= 64 ? 3 : 9; }
+
 WgradLauncher pick_wgrad_mt(const pbdk_conv_desc& d) {
-  static const bool off = [] {
-    const char* e = std::getenv("PBDK_WGRAD_MT");
-    return e != nullptr && e[0] == '0';
+  static const int mode = [] {
+    const char* e = std::getenv("PBDK_WGRAD_MT");  // 0 off, 1 narrow inputs only, 2 (default) + 64-ch tiles
+    return e != nullptr ? std::atoi(e) : 2;
   }();
-  if (off || d.r * d.s != 9 || d.k > 128 || (d.c != 16 && d.c != 32)) return nullptr;
+  if (mode == 0 || d.r * d.s != 9) return nullptr;
   const int swa = chan_block(d.k) * 2;
   const int aat = (std::min(128, d.k) + swa / 2 - 1) / (swa / 2);
+  if (d.c >= 64) {  // measured (scripts/time_wgrad.py): a win at c = 64 (s2 19.4 -> 14.6 us), a loss at c >= 128
+    if (mode < 2 || swa != 128 || d.c != 64) return nullptr;
+    return aat == 1 ? launch_wgrad_mt<64, 128, 1, 3> : launch_wgrad_mt<64, 128, 2, 3>;
+  }
+  if (d.k > 128 || (d.c != 16 && d.c != 32)) return nullptr;
   return d.c == 16 ? pick_wgrad_mt_c<16>(swa, aat) : pick_wgrad_mt_c<32>(swa, aat);
 }
 
@@ -1774,11 +1791,21 @@ int fprop_run(const FpropPlan& plan, cudaStream_t stream) {
 
 // the multi-tap kernel wants >= 4 pixel tiles per CTA in one wave (else the per-tap grid, whose
 // CTAs split the taps, fills the GPU with far fewer partial slabs)
-bool use_wgrad_mt(const ConvGeom& g) { return pick_wgrad_mt(g.d) != nullptr && g.m_tiles >= 4 * num_sms(); }
+int wgrad_mt_groups(const pbdk_conv_desc& d) {
+  return d.c >= 64 ? ((d.k + 127) / 128) * (d.c / 64) * (9 / wgrad_mt_taps(d)) : 1;
+}
+
+bool use_wgrad_mt(const ConvGeom& g) {
+  if (pick_wgrad_mt(g.d) == nullptr) return false;
+  const int groups = wgrad_mt_groups(g.d);
+  return g.m_tiles * groups >= 4 * num_sms();  // >= 4 pixel tiles per CTA in one wave
+}
 
 int wgrad_splits(const ConvGeom& g) {
-  if (use_wgrad_mt(g)) {  // one CTA per split covers every tap: one wave of splits
-    const int tps = (g.m_tiles + num_sms() - 1) / num_sms();
+  if (use_wgrad_mt(g)) {  // one wave: groups x splits ~ #SMs
+    const int groups = wgrad_mt_groups(g.d);
+    const int want = std::max(1, num_sms() / groups);
+    const int tps = (g.m_tiles + want - 1) / want;
     return (g.m_tiles + tps - 1) / tps;
   }
   const int co_tiles = (g.d.k + 127) / 128;
@@ -1807,7 +1834,7 @@ int wgrad_plan(const pbdk_conv_desc& d, const void* x, const void* dy, float* dw
   const int swa = chan_block(d.k) * 2;
   const int swb = chan_block(d.c) * 2;
   const WgradLauncher mt = use_wgrad_mt(g) ? pick_wgrad_mt(d) : nullptr;
-  const int bn = mt != nullptr ? d.c : wgrad_bn(d.c);
+  const int bn = mt != nullptr ? std::min(d.c, 64) : wgrad_bn(d.c);
   WgradLauncher l = mt != nullptr ? mt : pick_wgrad(bn, swa, swb);
   if (l == nullptr) return PBDK_EINVAL;
   const int splits = wgrad_splits(g);
@@ -1836,7 +1863,7 @@ int wgrad_plan(const pbdk_conv_desc& d, const void* x, const void* dy, float* dw
   a.tiles_per_split = (g.m_tiles + splits - 1) / splits;
   a.a_atoms = (std::min(128, d.k) + swa / 2 - 1) / (swa / 2);
   a.out = splits > 1 ? static_cast<float*>(ws) : dw;
-  plan->grid = mt != nullptr ? dim3(static_cast<unsigned>(splits), 1, 1)
+  plan->grid = mt != nullptr ? dim3(static_cast<unsigned>(splits), static_cast<unsigned>(wgrad_mt_groups(d)), 1)
                               : dim3(static_cast<unsigned>(a.co_tiles * a.ci_tiles * d.r * d.s),
                                      static_cast<unsigned>(splits), 1);
   plan->splits = splits;

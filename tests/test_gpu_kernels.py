@@ -69,7 +69,9 @@ def test_conv_fprop_epilogues(L, case, epi):
 WGRAD_EXTRA = [  # narrow inputs -> the multi-tap kernel (every tap in one CTA), k = 16 .. 128
     (4, 32, 16, 16, 3, 1), (4, 32, 32, 32, 3, 1), (2, 32, 16, 128, 3, 1), (2, 32, 32, 128, 3, 1),
     (96, 32, 16, 32, 3, 1), (96, 32, 32, 64, 3, 1), (96, 32, 16, 16, 3, 1), (96, 32, 32, 32, 3, 1),
-    (96, 32, 16, 128, 3, 1), (384, 16, 32, 64, 3, 1), (64, 32, 16, 32, 3, 1)]
+    (96, 32, 16, 128, 3, 1), (384, 16, 32, 64, 3, 1), (64, 32, 16, 32, 3, 1),
+    # c = 64: one filter row per CTA (co tiles, stride 2); wider inputs stay on the per-tap kernel
+    (128, 16, 64, 64, 3, 1), (128, 32, 64, 128, 3, 2), (64, 16, 64, 256, 3, 1), (32, 16, 128, 256, 3, 1)]
 
 
 @pytest.mark.parametrize("case", CASES + WGRAD_EXTRA)
@@ -124,7 +126,8 @@ def test_unsupported_shapes_fail_loudly(L):
                                    stream()) == 1
 
 
-@pytest.mark.parametrize("case", [(96, 32, 16, 32, 3, 1), (96, 32, 32, 64, 3, 1), (32, 16, 128, 128, 3, 1)])
+@pytest.mark.parametrize("case", [(96, 32, 16, 32, 3, 1), (96, 32, 32, 64, 3, 1), (32, 16, 128, 128, 3, 1),
+                                  (128, 16, 64, 64, 3, 1)])
 def test_conv_wgrad_deterministic(L, case):
     """Split partials are summed in split order: two runs are bit-identical."""
     n, h, c, k, r, st = case
