@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -122,9 +123,14 @@ struct SBlock {
   // other student blocks; the late blocks alone do not fill 148 SMs).
   float* rws = nullptr;
   void* wws = nullptr;
+  void* wws2 = nullptr;  // workspace of the side stream's wgrads
   size_t wws_bytes = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t done = nullptr;
+  // backward fork: wgrad(conv2) + wgrad(shortcut) on `side` run beside dgrad(conv2) -> BN1 backward ->
+  // wgrad(conv1), which is the block's critical chain
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
 };
 
 class ResNetPartition final : public PartitionBase {
@@ -236,13 +242,23 @@ class ResNetPartition final : public PartitionBase {
                       m, s.cout, static_cast<float>(2.0 / norm), norm, s.rws, s.red, g + s.lay.g2, g + s.lay.b2,
                       g + s.lay.gsc, g + s.lay.bsc, losses_ + i, s.dy2, s.dys};
       check(pbdk::mse_bn_loss(a, st), "mse");
-      check(pbdk::wgrad_run(s.p_w2, st), "wgrad2");
-      check(pbdk::wgrad_run(s.p_wsc, st), "wgrad sc");
+      cudaStream_t ws = st;
+      if (s.side != nullptr) {
+        cuda(cudaEventRecord(s.fork, st), "event");
+        cuda(cudaStreamWaitEvent(s.side, s.fork, 0), "fork");
+        ws = s.side;
+      }
+      check(pbdk::wgrad_run(s.p_w2, ws), "wgrad2");
+      check(pbdk::wgrad_run(s.p_wsc, ws), "wgrad sc");
       check(pbdk::fprop_run(s.p_dgrad, st), "dgrad2");
       check(pbdk::bn_bwd(s.g1, s.y1, s.st1, p + s.lay.g1, m, s.mid, s.rws, s.red1, g + s.lay.g1, g + s.lay.b1, s.dy1,
                          st),
             "bn1 bwd");
       check(pbdk::wgrad_run(s.p_w1, st), "wgrad1");
+      if (s.side != nullptr) {
+        cuda(cudaEventRecord(s.join, s.side), "event");
+        cuda(cudaStreamWaitEvent(st, s.join, 0), "join");
+      }
       if (timing_) cuda(cudaEventRecord(ev_s_[2 * i + 1], st), "event");
       cuda(cudaEventRecord(s.done, st), "event");
     }
@@ -317,10 +333,21 @@ class ResNetPartition final : public PartitionBase {
     return n;
   }
 
+  static bool student_fork() {
+    static const bool on = [] {
+      const char* e = std::getenv("PBD_STUDENT_FORK");
+      return e == nullptr || e[0] != '0';
+    }();
+    return on;
+  }
+
   ~ResNetPartition() override {
     for (SBlock& s : sblocks_) {
       if (s.stream != nullptr) cudaStreamDestroy(s.stream);
       if (s.done != nullptr) cudaEventDestroy(s.done);
+      if (s.side != nullptr) cudaStreamDestroy(s.side);
+      if (s.fork != nullptr) cudaEventDestroy(s.fork);
+      if (s.join != nullptr) cudaEventDestroy(s.join);
     }
     for (auto e : tdone_) cudaEventDestroy(e);
     if (fork_ != nullptr) cudaEventDestroy(fork_);
@@ -479,6 +506,13 @@ class ResNetPartition final : public PartitionBase {
       cuda(cudaStreamCreateWithPriority(&s.stream, cudaStreamNonBlocking, last ? priority_high() : priority_low()),
            "stream");
       cuda(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming), "event");
+      if (student_fork()) {
+        s.wws2 = arena_.get<void>(wws);
+        cuda(cudaStreamCreateWithPriority(&s.side, cudaStreamNonBlocking, last ? priority_high() : priority_low()),
+             "stream");
+        cuda(cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming), "event");
+        cuda(cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming), "event");
+      }
     }
     tdone_.resize(tblocks_.size());
     for (auto& e : tdone_) cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -514,8 +548,9 @@ class ResNetPartition final : public PartitionBase {
             "conv2 plan");
       const pbdk_conv_desc dg{n_, s.hout, s.hout, s.cout, s.mid, 3, 3, 1, 1, s.hout, s.hout};
       check(pbdk::fprop_plan(dg, s.dy2, s.w2flip, s.g1, nullptr, s.a1, PBDK_EPI_RELU_MASK, &s.p_dgrad), "dgrad plan");
-      check(pbdk::wgrad_plan(conv2_desc(s, n_), s.a1, s.dy2, g + s.lay.w2, s.wws, s.wws_bytes, &s.p_w2), "wgrad2 plan");
-      check(pbdk::wgrad_plan(sc_desc(s, n_), s.in, s.dys, g + s.lay.wsc, s.wws, s.wws_bytes, &s.p_wsc), "wgradsc plan");
+      void* ws2 = s.wws2 != nullptr ? s.wws2 : s.wws;
+      check(pbdk::wgrad_plan(conv2_desc(s, n_), s.a1, s.dy2, g + s.lay.w2, ws2, s.wws_bytes, &s.p_w2), "wgrad2 plan");
+      check(pbdk::wgrad_plan(sc_desc(s, n_), s.in, s.dys, g + s.lay.wsc, ws2, s.wws_bytes, &s.p_wsc), "wgradsc plan");
       check(pbdk::wgrad_plan(conv1_desc(s, n_), s.in, s.dy1, g + s.lay.w1, s.wws, s.wws_bytes, &s.p_w1), "wgrad1 plan");
     }
   }
