@@ -164,9 +164,7 @@ __device__ __forceinline__ void fprop_epilogue(const FpropArgs& a, uint32_t trow
       o1.y = pack_bf16x2(v[10], v[11]);
       o1.z = pack_bf16x2(v[12], v[13]);
       o1.w = pack_bf16x2(v[14], v[15]);
-      uint4* dst = reinterpret_cast<uint4*>(a.y + m * a.k + col);
-      dst[0] = o0;
-      dst[1] = o1;
+      st_global_256(a.y + m * a.k + col, o0, o1);
     }
   }
 }
@@ -196,8 +194,12 @@ struct HaloRows {  // halo tiles: 128 consecutive positions of a (W+2)-wide padd
   }
 };
 
-template <int BN, int BKC, bool BRES>
-__global__ void __launch_bounds__(kThreads, 1)
+// EPW epilogue warps per TMEM lane quarter (each takes BN/EPW columns): 2 for convs whose short K
+// leaves the tile's epilogue, not its MMAs, on the critical path.
+constexpr int epi_threads(int epw) { return 64 + 128 * epw; }
+
+template <int BN, int BKC, bool BRES, int EPW = 1>
+__global__ void __launch_bounds__(epi_threads(EPW), 1)
     conv_fprop_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
                       const FpropArgs a) {
   using C = FpropCfg<BN, BKC, BRES>;
@@ -225,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], 4 * EPW);
     }
     mbar_init(bfull, 1);
     fence_barrier_init();
@@ -298,8 +300,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // epilogue: warps 2..5, TMEM lane quarter = warp % 4
+    // epilogue: warps 2.., TMEM lane quarter = warp % 4, column slice (warp - 2) / 4
     const int quarter = warp & 3;
+    constexpr int CW = BN / EPW;
+    const int c_lo = ((warp - 2) >> 2) * CW;
     int lt = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
       const int acc = lt & 1;
@@ -309,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int tq = m_tile % a.tiles_q;
       const int t2 = m_tile / a.tiles_q;
       const TileRows rows{&a, (t2 / a.tiles_p) * a.bn, (t2 % a.tiles_p) * a.bh, tq * a.bw};
-      fprop_epilogue<BN>(a, trow, quarter * 32 + lane, k0, rows, [&] {
+      fprop_epilogue<CW>(a, trow + c_lo, quarter * 32 + lane, k0 + c_lo, rows, [&] {
         mbar_wait(&tfull[acc], (lt >> 1) & 1);
         tc_fence_after();
       });
@@ -732,8 +736,8 @@ struct HaloCfg {
   static_assert(STAGES >= 2, "halo stage does not fit");
 };
 
-template <int BN, int BKC, int WP>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int BN, int BKC, int WP, int EPW = 1>
+__global__ void __launch_bounds__(epi_threads(EPW), 1)
     conv_fprop_halo_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
                            const FpropArgs a) {
   using C = HaloCfg<BN, BKC, WP>;
@@ -761,7 +765,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], 4 * EPW);
     }
     mbar_init(bfull, 1);
     fence_barrier_init();
@@ -840,13 +844,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     const int quarter = warp & 3;
+    constexpr int CW = BN / EPW;
+    const int c_lo = ((warp - 2) >> 2) * CW;
     int lt = 0;
     for (int t = blockIdx.x; t < (a.debug == 8 ? 0 : total); t += gridDim.x, ++lt) {
       const int acc = lt & 1;
       const int img = t / a.tiles_img;
       const HaloRows rows{&a, img, (t - img * a.tiles_img) * 128, WP};
       const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * C::ACC_COLS);
-      fprop_epilogue<BN>(a, trow, quarter * 32 + lane, 0, rows, [&] {
+      fprop_epilogue<CW>(a, trow + c_lo, quarter * 32 + lane, c_lo, rows, [&] {
         mbar_wait(&tfull[acc], (lt >> 1) & 1);
         tc_fence_after();
       });
@@ -1035,25 +1041,25 @@ cudaError_t launch_fprop_m2(const FpropPlan& p, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
-template <int BN, int BKC, int WP>
+template <int BN, int BKC, int WP, int EPW = 1>
 cudaError_t launch_fprop_halo(const FpropPlan& p, cudaStream_t stream) {
   using C = HaloCfg<BN, BKC, WP>;
   if (stream == reinterpret_cast<cudaStream_t>(-1)) {
-    return cudaFuncSetAttribute(conv_fprop_halo_kernel<BN, BKC, WP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    return cudaFuncSetAttribute(conv_fprop_halo_kernel<BN, BKC, WP, EPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 C::SMEM);
   }
-  conv_fprop_halo_kernel<BN, BKC, WP><<<p.grid, kThreads, C::SMEM, stream>>>(p.tmx, p.tmw, p.args);
+  conv_fprop_halo_kernel<BN, BKC, WP, EPW><<<p.grid, epi_threads(EPW), C::SMEM, stream>>>(p.tmx, p.tmw, p.args);
   return cudaGetLastError();
 }
 
-template <int BN, int BKC, bool BRES>
+template <int BN, int BKC, bool BRES, int EPW = 1>
 cudaError_t launch_fprop(const FpropPlan& p, cudaStream_t stream) {
   using C = FpropCfg<BN, BKC, BRES>;
   if (stream == reinterpret_cast<cudaStream_t>(-1)) {  // prepare: set the smem attribute outside any capture
-    return cudaFuncSetAttribute(conv_fprop_kernel<BN, BKC, BRES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    return cudaFuncSetAttribute(conv_fprop_kernel<BN, BKC, BRES, EPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 C::SMEM);
   }
-  conv_fprop_kernel<BN, BKC, BRES><<<p.grid, kThreads, C::SMEM, stream>>>(p.tmx, p.tmw, p.args);
+  conv_fprop_kernel<BN, BKC, BRES, EPW><<<p.grid, epi_threads(EPW), C::SMEM, stream>>>(p.tmx, p.tmw, p.args);
   return cudaGetLastError();
 }
 
@@ -1468,7 +1474,15 @@ bool act_map(CUtensorMap* m, const void* base, int n, int h, int w, int c, int c
 using FpropLauncher = cudaError_t (*)(const FpropPlan&, cudaStream_t);
 
 template <int BKC, bool BRES>
-FpropLauncher pick_fprop(int bn) {
+FpropLauncher pick_fprop(int bn, int epw = 1) {
+  if (epw == 2) {
+    switch (bn) {
+      case 32: return launch_fprop<32, BKC, BRES, 2>;
+      case 64: return launch_fprop<64, BKC, BRES, 2>;
+      case 128: return launch_fprop<128, BKC, BRES, 2>;
+      default: break;
+    }
+  }
   switch (bn) {
     case 16: return launch_fprop<16, BKC, BRES>;
     case 32: return launch_fprop<32, BKC, BRES>;
@@ -1482,7 +1496,14 @@ FpropLauncher pick_fprop(int bn) {
 constexpr int kHaloWP = 34;  // halo kernel instantiated for 32-wide images (W + 2 padded columns)
 
 template <int BKC>
-FpropLauncher pick_halo(int bn) {
+FpropLauncher pick_halo(int bn, int epw = 1) {
+  if (epw == 2) {
+    switch (bn) {
+      case 32: return launch_fprop_halo<32, BKC, kHaloWP, 2>;
+      case 64: return launch_fprop_halo<64, BKC, kHaloWP, 2>;
+      default: break;
+    }
+  }
   switch (bn) {
     case 16: return launch_fprop_halo<16, BKC, kHaloWP>;
     case 32: return launch_fprop_halo<32, BKC, kHaloWP>;
@@ -1696,20 +1717,28 @@ int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, c
   const bool bres = !pair && !ch.m2 && fprop_bres(d, bn, bkc);
   const bool halo = splits == 1 && !pair && halo_enabled() && bres && bn <= 128 && d.r == 3 && d.s == 3 && d.stride == 1 && d.pad == 1 &&
                     d.q + 2 == kHaloWP && d.w == d.q;
+  // short-K convs (3x3 over <= 32 channels, 1x1 over <= 64): the epilogue bounds the tile, so two
+  // epilogue warps per TMEM lane quarter (PBDK_EPW=1/2 forces)
+  static const int epw_env = [] {
+    const char* e = std::getenv("PBDK_EPW");
+    return e != nullptr ? std::atoi(e) : 0;
+  }();
+  const bool short_k = (d.r * d.s == 9 && d.c <= 32) || (d.r * d.s == 1 && d.c <= 64);
+  const int epw = bn >= 32 && bn <= 128 && (epw_env == 2 || (epw_env == 0 && short_k)) ? 2 : 1;
   FpropLauncher l = nullptr;
   switch (bkc) {
-    case 16: l = bres ? pick_fprop<16, true>(bn) : pick_fprop<16, false>(bn); break;
-    case 32: l = bres ? pick_fprop<32, true>(bn) : pick_fprop<32, false>(bn); break;
-    case 64: l = bres ? pick_fprop<64, true>(bn) : pick_fprop<64, false>(bn); break;
+    case 16: l = bres ? pick_fprop<16, true>(bn, epw) : pick_fprop<16, false>(bn, epw); break;
+    case 32: l = bres ? pick_fprop<32, true>(bn, epw) : pick_fprop<32, false>(bn, epw); break;
+    case 64: l = bres ? pick_fprop<64, true>(bn, epw) : pick_fprop<64, false>(bn, epw); break;
     default: break;
   }
   if (splits > 1) l = bkc == 64 ? pick_splitk<64>(bn) : nullptr;
   if (pair) l = bkc != 64 ? nullptr : bn == 256 ? launch_fprop_pair<256, 64> : bn == 128 ? launch_fprop_pair<128, 64> : nullptr;
   if (halo) {
     switch (bkc) {
-      case 16: l = pick_halo<16>(bn); break;
-      case 32: l = pick_halo<32>(bn); break;
-      case 64: l = pick_halo<64>(bn); break;
+      case 16: l = pick_halo<16>(bn, epw); break;
+      case 32: l = pick_halo<32>(bn, epw); break;
+      case 64: l = pick_halo<64>(bn, epw); break;
       default: l = nullptr; break;
     }
   }
