@@ -45,6 +45,22 @@ __device__ __forceinline__ void st8(__nv_bfloat16* p, const float (&f)[8]) {
   *reinterpret_cast<uint4*>(p) = make_uint4(pk2(f[0], f[1]), pk2(f[2], f[3]), pk2(f[4], f[5]), pk2(f[6], f[7]));
 }
 
+// acc[j] = fmaf(x[j], w[j], acc[j]) for j < 8 as four packed FFMA2 (fma.rn.f32x2: per-lane IEEE fma,
+// bit-identical to the scalar chain, half the fma-pipe issue slots)
+__device__ __forceinline__ void fma8(float (&acc)[8], const float (&x)[8], const float (&w)[8]) {
+#pragma unroll
+  for (int j = 0; j < 8; j += 2) {
+    unsigned long long a = (static_cast<unsigned long long>(__float_as_uint(acc[j + 1])) << 32) | __float_as_uint(acc[j]);
+    const unsigned long long xx =
+        (static_cast<unsigned long long>(__float_as_uint(x[j + 1])) << 32) | __float_as_uint(x[j]);
+    const unsigned long long ww =
+        (static_cast<unsigned long long>(__float_as_uint(w[j + 1])) << 32) | __float_as_uint(w[j]);
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a) : "l"(xx), "l"(ww));
+    acc[j] = __uint_as_float(static_cast<uint32_t>(a));
+    acc[j + 1] = __uint_as_float(static_cast<uint32_t>(a >> 32));
+  }
+}
+
 __device__ __forceinline__ float relu6f(float z) { return fminf(fmaxf(z, 0.0f), 6.0f); }
 __device__ __forceinline__ float swishf(float z) { return z / (1.0f + expf(-z)); }
 __device__ __forceinline__ float sigmoidf(float z) { return 1.0f / (1.0f + expf(-z)); }
@@ -109,8 +125,7 @@ __global__ void __launch_bounds__(kT) dw_fwd_kernel(const __nv_bfloat16* __restr
         for (int u = 0; u < kQT; ++u) {
           const int sidx = j - u * ST;
           if (sidx < 0 || sidx >= K) continue;
-#pragma unroll
-          for (int jj = 0; jj < 8; ++jj) acc[u][jj] = fmaf(xv[jj], wr[sidx][jj], acc[u][jj]);
+          fma8(acc[u], xv, wr[sidx]);
         }
       }
     }
@@ -162,8 +177,7 @@ __global__ void __launch_bounds__(kT) dw_dgrad_kernel(const __nv_bfloat16* __res
         float gv[8], wv[8];
         ld8(grow + static_cast<size_t>(qn / ST) * C, gv);
         ld8(wrow + static_cast<size_t>(K - 1 - s) * C, wv);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = fmaf(gv[j], wv[j], acc[j]);
+        fma8(acc, gv, wv);
       }
     }
     if (act != nullptr) {
