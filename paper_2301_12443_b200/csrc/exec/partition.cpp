@@ -217,6 +217,7 @@ class ResNetPartition final : public PartitionBase {
   // graphs): the student streams fork from the caller's stream at entry.  The caller's
   // stream joins all of them before returning.
   void student_body(cudaStream_t caller, bool fork) override {
+    const pbdk::GridScope grids(148, 296);  // passes share the GPU with the other student streams
     if (fork) cuda(cudaEventRecord(fork_, caller), "event");
     for (size_t i = 0; i < sblocks_.size(); ++i) {
       SBlock& s = sblocks_[i];

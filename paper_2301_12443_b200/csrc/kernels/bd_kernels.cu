@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "bd_kernels.hpp"
 #include "pbdk.h"
@@ -184,11 +185,30 @@ struct RowTiling {
   int cg, rpp, chunks, rows_per_chunk;
 };
 
-RowTiling tiling_for(int m, int c, int v) {
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e != nullptr ? std::atoi(e) : dflt;
+}
+// Grid sizes of the reduction (partial) and elementwise (apply) passes (GridScope, bd_kernels.hpp).
+// Measured, CUDA-graph ResNet step at b=256 (4 concurrent student streams): partials 296 -> 148 CTAs
+// and applies 1184 -> 296 CTAs took the step from 0.997 to 0.932 ms although each kernel alone is
+// slower — a one-CTA-per-SM wave leaves the other streams' convs their SMs.  The MBConv step (passes
+// mostly alone) prefers 296 / 1184 (19.74 vs 20.17 ms).  PBDK_RED_TARGET / PBDK_APPLY_CTAS override.
+thread_local int t_red = 0, t_apply = 0;
+int red_target() {
+  static const int e = env_int("PBDK_RED_TARGET", 0);
+  return e > 0 ? e : (t_red > 0 ? t_red : 148 * 2);
+}
+int apply_cap() {
+  static const int e = env_int("PBDK_APPLY_CTAS", 0);
+  return e > 0 ? e : (t_apply > 0 ? t_apply : 148 * 8);
+}
+
+RowTiling tiling_for(int m, int c, int v, int target = -1) {
+  if (target < 0) target = red_target();
   RowTiling t;
   t.cg = c / v;
   t.rpp = std::max(1, kThreads / t.cg);
-  const int target = 148 * 2;
   const int passes = (m + t.rpp - 1) / t.rpp;
   const int chunks = std::max(1, std::min(target, passes));
   t.rows_per_chunk = (passes + chunks - 1) / chunks * t.rpp;
@@ -196,7 +216,7 @@ RowTiling tiling_for(int m, int c, int v) {
   return t;
 }
 
-int apply_grid(int m, int rpp) { return std::max(1, std::min((m + rpp - 1) / rpp, 148 * 8)); }
+int apply_grid(int m, int rpp) { return std::max(1, std::min((m + rpp - 1) / rpp, apply_cap())); }
 
 // CTA-level fixed-order reduction of NV*V floats per thread into partial[chunk][NV][C].
 template <int NV, int V>
@@ -266,7 +286,7 @@ __global__ void __launch_bounds__(kThreads) bn_stats_partial_kernel(const __nv_b
   if (slot < rpp) {
     const int r0 = blockIdx.x * rows_per_chunk;
     const int r1 = min(m, r0 + rows_per_chunk);
-#pragma unroll 2
+#pragma unroll 4
     for (int r = r0 + slot; r < r1; r += rpp) {
       const size_t off = static_cast<size_t>(r) * C + g * V;
       float f[NT][V];
@@ -323,7 +343,7 @@ __global__ void __launch_bounds__(kThreads) bn_apply_relu_kernel(const __nv_bflo
     B[j] = fmaf(-A[j], mean_rstd[c0 + j], beta[c0 + j]);
   }
   const int step = gridDim.x * rpp;
-#pragma unroll 2
+#pragma unroll 4
   for (int r = blockIdx.x * rpp + slot; r < m; r += step) {
     const size_t off = static_cast<size_t>(r) * C + c0;
     float f[V];
@@ -366,6 +386,7 @@ __device__ __forceinline__ void loss_affine(const LossParams& p, int c0, float (
 }
 
 constexpr int kLossPartialV = 8;
+const int kLossChunks = -1;  // = red_target(), as the BN partials
 constexpr int kLossApplyV = 4;
 
 __global__ void __launch_bounds__(kThreads) loss_partial_kernel(const LossParams p, int rows_per_chunk, int cg, int rpp,
@@ -381,7 +402,7 @@ __global__ void __launch_bounds__(kThreads) loss_partial_kernel(const LossParams
     loss_affine<V>(p, gi * V, A2, As, Bz);
     const int r0 = blockIdx.x * rows_per_chunk;
     const int r1 = min(p.m, r0 + rows_per_chunk);
-#pragma unroll 2
+#pragma unroll 4
     for (int r = r0 + slot; r < r1; r += rpp) {
       const size_t off = static_cast<size_t>(r) * p.C + gi * V;
       float y2[V], ys[V], t[V];
@@ -466,7 +487,7 @@ __global__ void __launch_bounds__(kThreads) loss_bwd_apply_kernel(const LossPara
     Rs[j] = coef[3 * p.C + c0 + j];
   }
   const int step = gridDim.x * rpp;
-#pragma unroll 2
+#pragma unroll 4
   for (int r = blockIdx.x * rpp + slot; r < p.m; r += step) {
     const size_t off = static_cast<size_t>(r) * p.C + c0;
     float y2[V], ys[V], t[V], o2[V], os[V];
@@ -498,7 +519,7 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_partial_kernel(const __nv_bfl
   if (slot < rpp) {
     const int r0 = blockIdx.x * rows_per_chunk;
     const int r1 = min(m, r0 + rows_per_chunk);
-#pragma unroll 2
+#pragma unroll 4
     for (int r = r0 + slot; r < r1; r += rpp) {
       const size_t off = static_cast<size_t>(r) * C + gi * V;
       float fg[V], fy[V];
@@ -554,7 +575,7 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_apply_kernel(const __nv_bfloa
     R[j] = coef[C + c0 + j];
   }
   const int step = gridDim.x * rpp;
-#pragma unroll 2
+#pragma unroll 4
   for (int r = blockIdx.x * rpp + slot; r < m; r += step) {
     const size_t off = static_cast<size_t>(r) * C + c0;
     float fg[V], fy[V], o[V];
@@ -636,9 +657,18 @@ inline int ok(cudaError_t e) { return e == cudaSuccess ? PBDK_OK : PBDK_ECUDA; }
 
 }  // namespace
 
+GridScope::GridScope(int red_ctas, int apply_ctas) : saved_red(t_red), saved_apply(t_apply) {
+  t_red = red_ctas;
+  t_apply = apply_ctas;
+}
+GridScope::~GridScope() {
+  t_red = saved_red;
+  t_apply = saved_apply;
+}
+
 size_t reduce_workspace_floats(int m, int c, int nv) {
   int chunks = 1;
-  for (int v : {4, 8}) chunks = std::max(chunks, tiling_for(m, c, v).chunks);
+  for (int v : {4, 8}) chunks = std::max(chunks, tiling_for(m, c, v, 148 * 8).chunks);  // any target <= 8/SM
   return static_cast<size_t>(chunks) * std::max(nv, 4) * c + chunks;
 }
 
@@ -713,7 +743,7 @@ int mse_bn_loss(const MseArgs& a, cudaStream_t st) {
   LossParams p{static_cast<const __nv_bfloat16*>(a.y2), static_cast<const __nv_bfloat16*>(a.ysc),
                static_cast<const __nv_bfloat16*>(a.t), a.stats2, a.statssc, a.gamma2, a.beta2, a.gammasc, a.betasc,
                a.m, a.c, a.gscale};
-  const RowTiling t = tiling_for(a.m, a.c, kLossPartialV);
+  const RowTiling t = tiling_for(a.m, a.c, kLossPartialV, kLossChunks);
   float* partial = a.ws;
   float* loss_partial = a.ws + static_cast<size_t>(t.chunks) * 3 * a.c;
   loss_partial_kernel<<<t.chunks, kThreads, 0, st>>>(p, t.rows_per_chunk, t.cg, t.rpp, partial, loss_partial);

@@ -33,6 +33,16 @@ struct MseArgs {
 };
 
 size_t reduce_workspace_floats(int m, int c, int nv);
+
+// Grid sizes of the reduction (partial) and elementwise (apply) passes launched by this thread while
+// the scope is alive.  Default (no scope): 2 partial CTAs and 8 apply CTAs per SM, best when the
+// passes run mostly alone (MBConv step).  The ResNet step runs them beside the conv kernels of the
+// other student streams and uses GridScope(148, 296) (see bd_kernels.cu).
+struct GridScope {
+  GridScope(int red_ctas, int apply_ctas);
+  ~GridScope();
+  int saved_red, saved_apply;
+};
 // synthetic / host images of side x side pixels, stored [n][side][side][16] bf16
 int philox_image(void* x, int n, long long first, const long long* counter, int gb, uint32_t seed, cudaStream_t st,
                  int side = 32);

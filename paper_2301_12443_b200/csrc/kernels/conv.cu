@@ -1904,13 +1904,21 @@ int wgrad_plan(const pbdk_conv_desc& d, const void* x, const void* dy, float* dw
   return PBDK_OK;
 }
 
+int split_reduce_cap() {
+  static const int cap = [] {
+    const char* e = std::getenv("PBDK_SPLITRED_CTAS");
+    return e != nullptr ? std::max(1, std::atoi(e)) : 148 * 8;
+  }();
+  return cap;
+}
+
 int wgrad_run(const WgradPlan& plan, cudaStream_t stream) {
   if (plan.launch == nullptr) return PBDK_EINVAL;
   if (plan.launch(plan, stream) != cudaSuccess) return PBDK_ECUDA;
   if (plan.splits > 1) {
     const size_t n4 = plan.slab / 4;
     const int blocks =
-        static_cast<int>(std::max<size_t>(1, std::min<size_t>((n4 + kRedLanes - 1) / kRedLanes, 148 * 8)));
+        static_cast<int>(std::max<size_t>(1, std::min<size_t>((n4 + kRedLanes - 1) / kRedLanes, split_reduce_cap())));
     split_reduce_kernel<<<blocks, kRedLanes * kRedSplitLanes, 0, stream>>>(reinterpret_cast<const float4*>(plan.args.out),
                                                     reinterpret_cast<float4*>(plan.dw), n4, plan.splits);
     if (cudaGetLastError() != cudaSuccess) return PBDK_ECUDA;

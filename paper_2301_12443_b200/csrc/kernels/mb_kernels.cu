@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "mb_kernels.hpp"
 #include "pbdk.h"
@@ -71,7 +72,11 @@ __device__ __forceinline__ float act_fn(int act, float v) {
 
 int grid_for(long long work) {
   const long long b = (work + kT - 1) / kT;
-  return static_cast<int>(std::max<long long>(1, std::min<long long>(b, 148LL * 16)));
+  static const long long cap = [] {
+    const char* e = std::getenv("PBDK_MB_CTAS");
+    return e != nullptr ? std::max(1LL, std::atoll(e)) : 148LL * 16;
+  }();
+  return static_cast<int>(std::max<long long>(1, std::min<long long>(b, cap)));
 }
 
 inline int ok(cudaError_t e) { return e == cudaSuccess ? PBDK_OK : PBDK_ECUDA; }
