@@ -217,7 +217,11 @@ class ResNetPartition final : public PartitionBase {
   // graphs): the student streams fork from the caller's stream at entry.  The caller's
   // stream joins all of them before returning.
   void student_body(cudaStream_t caller, bool fork) override {
-    const pbdk::GridScope grids(148, 296);  // passes share the GPU with the other student streams
+    // The BN / loss passes leave SMs to the other student streams' convs: one partial CTA per SM (for
+    // every block count — the chunking fixes the summation order, so a block's results must not
+    // depend on how many blocks the partition holds) and, with >= 3 concurrent streams, two apply
+    // CTAs per SM.
+    const pbdk::GridScope grids(148, sblocks_.size() >= 3 ? 296 : 0);
     if (fork) cuda(cudaEventRecord(fork_, caller), "event");
     for (size_t i = 0; i < sblocks_.size(); ++i) {
       SBlock& s = sblocks_[i];
@@ -530,12 +534,27 @@ class ResNetPartition final : public PartitionBase {
     return pbdk_conv_desc{n, s.hout, s.hout, s.mid, s.cout, 3, 3, 1, 1, s.hout, s.hout};
   }
 
+  static int env_ctas(const char* name) {
+    const char* e = std::getenv(name);
+    return e != nullptr ? std::atoi(e) : 0;
+  }
+
   void build_plans() {
-    for (TBlock& tb : tblocks_)
-      for (TConv& c : tb.convs) {
-        const pbdk_conv_desc cd{n_, c.hin, c.hin, c.cs, c.cout, c.r, c.r, c.stride, c.pad, c.hout, c.hout};
-        check(pbdk::fprop_plan(cd, c.in, c.w, c.out, c.bias, c.aux, c.epi, &c.plan), "teacher plan");
-      }
+    {
+      const pbdk::ConvGridScope scope(env_ctas("PBDK_TCONV_CTAS"));
+      for (TBlock& tb : tblocks_)
+        for (TConv& c : tb.convs) {
+          const pbdk_conv_desc cd{n_, c.hin, c.hin, c.cs, c.cout, c.r, c.r, c.stride, c.pad, c.hout, c.hout};
+          check(pbdk::fprop_plan(cd, c.in, c.w, c.out, c.bias, c.aux, c.epi, &c.plan), "teacher plan");
+        }
+    }
+    // With >= 3 student blocks their streams run concurrently: each student conv spreads over at most
+    // 64 SMs so the streams share the GPU spatially instead of queueing behind each other's full-GPU
+    // persistent grids (measured, 4 blocks at b=256: 0.934 -> 0.907 ms per step; capping the teacher
+    // convs, which run mostly alone, costs time).  PBDK_SCONV_CTAS overrides (0 = all SMs).
+    const int sconv = std::getenv("PBDK_SCONV_CTAS") != nullptr ? env_ctas("PBDK_SCONV_CTAS")
+                                                                : (sblocks_.size() >= 3 ? 64 : 0);
+    const pbdk::ConvGridScope scope(sconv);
     for (SBlock& s : sblocks_) {
       const bf16* sh = shadow_ + s.base;
       float* g = grads_ + s.base;

@@ -1521,6 +1521,10 @@ bool halo_enabled() {
   return on;
 }
 
+thread_local int t_grid_sms = 0;  // ConvGridScope
+// SMs a plan may spread over (persistent grids, one-wave split counts)
+int grid_sms();
+
 int num_sms() {
   static int n = [] {
     int dev = 0, v = 148;
@@ -1529,6 +1533,8 @@ int num_sms() {
   }();
   return n;
 }
+
+int grid_sms() { return t_grid_sms > 0 ? std::min(t_grid_sms, num_sms()) : num_sms(); }
 
 
 
@@ -1689,6 +1695,9 @@ bool m2_auto(const pbdk_conv_desc& d, const ConvGeom& g, int bn) {
 
 }  // namespace
 
+ConvGridScope::ConvGridScope(int sms) : saved(t_grid_sms) { t_grid_sms = sms; }
+ConvGridScope::~ConvGridScope() { t_grid_sms = saved; }
+
 int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, const float* bias, const void* aux,
                int epi, FpropPlan* plan) {
   ConvGeom g;
@@ -1797,13 +1806,13 @@ int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, c
   const int tiles = a.n_tiles * a.m_tiles;
   if (ch.m2) {
     const int items = (a.m_tiles + 1) / 2 * a.n_tiles;
-    plan->grid = dim3(static_cast<unsigned>(std::min(items, num_sms())), 1, 1);
+    plan->grid = dim3(static_cast<unsigned>(std::min(items, grid_sms())), 1, 1);
   } else if (pair) {
-    plan->grid = dim3(static_cast<unsigned>(2 * std::min(tiles / 2, num_sms() / 2)), 1, 1);
+    plan->grid = dim3(static_cast<unsigned>(2 * std::min(tiles / 2, grid_sms() / 2)), 1, 1);
   } else if (splits > 1) {
     plan->grid = dim3(static_cast<unsigned>(splits), static_cast<unsigned>(tiles), 1);
   } else {
-    plan->grid = dim3(static_cast<unsigned>(std::min(tiles, num_sms())), 1, 1);
+    plan->grid = dim3(static_cast<unsigned>(std::min(tiles, grid_sms())), 1, 1);
   }
   plan->bn_tile = bn;
   plan->bkc = bkc;
@@ -1827,13 +1836,26 @@ int wgrad_mt_groups(const pbdk_conv_desc& d) {
 bool use_wgrad_mt(const ConvGeom& g) {
   if (pick_wgrad_mt(g.d) == nullptr) return false;
   const int groups = wgrad_mt_groups(g.d);
-  return g.m_tiles * groups >= 4 * num_sms();  // >= 4 pixel tiles per CTA in one wave
+  return g.m_tiles * groups >= 4 * 148;  // >= 4 pixel tiles per CTA in one wave
+}
+
+// CTAs of one wgrad split grid.  A constant, not a function of the partition that plans it: the split
+// count fixes the summation order, so a block's gradients must not depend on its placement.  The
+// wgrads run beside the other student streams; measured on the 4-block step at b=256: a 148-CTA wave
+// 0.928 ms, 96 / 64 / 48 CTAs 0.907 / 0.908 / 0.902 ms (fewer splits also shrink the reduction).
+// PBDK_WGRAD_WAVE overrides.
+int wgrad_wave() {
+  static const int w = [] {
+    const char* e = std::getenv("PBDK_WGRAD_WAVE");
+    return e != nullptr ? std::max(1, std::atoi(e)) : 64;
+  }();
+  return w;
 }
 
 int wgrad_splits(const ConvGeom& g) {
   if (use_wgrad_mt(g)) {  // one wave: groups x splits ~ #SMs
     const int groups = wgrad_mt_groups(g.d);
-    const int want = std::max(1, num_sms() / groups);
+    const int want = std::max(1, wgrad_wave() / groups);
     const int tps = (g.m_tiles + want - 1) / want;
     return (g.m_tiles + tps - 1) / tps;
   }
@@ -1842,7 +1864,7 @@ int wgrad_splits(const ConvGeom& g) {
   const int tiles = co_tiles * ci_tiles * g.d.r * g.d.s;
   // one wave of CTAs: the student streams run concurrently, so the wgrads need not fill the
   // GPU alone, and every split costs a partial slab in the fixed-order reduction.
-  const int target = 148;
+  const int target = wgrad_wave();
   int splits = std::max(1, target / tiles);
   splits = std::min(splits, std::max(1, g.m_tiles / 8));  // >= 8 pixel tiles per split
   return splits;

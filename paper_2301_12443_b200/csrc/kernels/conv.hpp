@@ -68,6 +68,15 @@ struct WgradArgs {
   float* out;   // dw (splits == 1) or workspace
 };
 
+// While alive, fprop plans built by this thread spread their persistent grid over at most `sms` SMs
+// (0 = all).  Results do not depend on it (tiles are independent); wgrad split counts, which fix a
+// summation order, ignore it.
+struct ConvGridScope {
+  explicit ConvGridScope(int sms);
+  ~ConvGridScope();
+  int saved;
+};
+
 struct WgradPlan {
   CUtensorMap tmdy;
   CUtensorMap tmx;
