@@ -538,15 +538,27 @@ class ResNetPartition final : public PartitionBase {
     const char* e = std::getenv(name);
     return e != nullptr ? std::atoi(e) : 0;
   }
+  // PBDK_TCONV_CTAS_LIST / PBDK_SCONV_CTAS_LIST = "a,b,c,d": per-block grid caps (experiments)
+  static int env_list(const char* name, size_t i, int dflt) {
+    const char* e = std::getenv(name);
+    if (e == nullptr) return dflt;
+    std::string v(e);
+    size_t pos = 0;
+    for (size_t k = 0; k < i; ++k) {
+      pos = v.find(',', pos);
+      if (pos == std::string::npos) return dflt;
+      ++pos;
+    }
+    return std::atoi(v.c_str() + pos);
+  }
 
   void build_plans() {
-    {
-      const pbdk::ConvGridScope scope(env_ctas("PBDK_TCONV_CTAS"));
-      for (TBlock& tb : tblocks_)
-        for (TConv& c : tb.convs) {
-          const pbdk_conv_desc cd{n_, c.hin, c.hin, c.cs, c.cout, c.r, c.r, c.stride, c.pad, c.hout, c.hout};
-          check(pbdk::fprop_plan(cd, c.in, c.w, c.out, c.bias, c.aux, c.epi, &c.plan), "teacher plan");
-        }
+    for (size_t i = 0; i < tblocks_.size(); ++i) {
+      const pbdk::ConvGridScope scope(env_list("PBDK_TCONV_CTAS_LIST", i, env_ctas("PBDK_TCONV_CTAS")));
+      for (TConv& c : tblocks_[i].convs) {
+        const pbdk_conv_desc cd{n_, c.hin, c.hin, c.cs, c.cout, c.r, c.r, c.stride, c.pad, c.hout, c.hout};
+        check(pbdk::fprop_plan(cd, c.in, c.w, c.out, c.bias, c.aux, c.epi, &c.plan), "teacher plan");
+      }
     }
     // With >= 3 student blocks their streams run concurrently: each student conv spreads over at most
     // 64 SMs so the streams share the GPU spatially instead of queueing behind each other's full-GPU
@@ -554,8 +566,9 @@ class ResNetPartition final : public PartitionBase {
     // convs, which run mostly alone, costs time).  PBDK_SCONV_CTAS overrides (0 = all SMs).
     const int sconv = std::getenv("PBDK_SCONV_CTAS") != nullptr ? env_ctas("PBDK_SCONV_CTAS")
                                                                 : (sblocks_.size() >= 3 ? 64 : 0);
-    const pbdk::ConvGridScope scope(sconv);
-    for (SBlock& s : sblocks_) {
+    for (size_t i = 0; i < sblocks_.size(); ++i) {
+      SBlock& s = sblocks_[i];
+      const pbdk::ConvGridScope scope(env_list("PBDK_SCONV_CTAS_LIST", i, sconv));
       const bf16* sh = shadow_ + s.base;
       float* g = grads_ + s.base;
       check(pbdk::fprop_plan(conv1_desc(s, n_), s.in, sh + s.lay.w1, s.y1, nullptr, nullptr, PBDK_EPI_STORE,
