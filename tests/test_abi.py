@@ -112,3 +112,23 @@ def test_mb_supernet_layout_matches_oracle():
                         assert ex.mb_candidate_span(b, l, c, model) == mb.candidate_span(b, l, c)
         finally:
             mb.set_family(0)
+
+
+def test_wgrad_workspace_monotone_in_batch():
+    """Partitions size the split-K workspace for n_max and plan their DP shard n <= n_max: the
+    workspace a plan needs must never grow when the batch shrinks (host-only planning, no GPU)."""
+    from paper_2301_12443_b200 import _lib
+    L = _lib.lib()
+    shapes = [(32, 16, 32, 3, 1), (32, 32, 64, 3, 1), (32, 16, 64, 1, 1), (32, 64, 64, 3, 2), (16, 64, 128, 3, 1),
+              (16, 64, 128, 1, 2), (16, 128, 128, 3, 2), (8, 128, 256, 3, 1), (8, 256, 256, 3, 2),
+              (4, 256, 512, 3, 1)]
+    for h, c, k, r, st in shapes:
+        prev = None
+        for n in (256, 192, 128, 86, 64, 43, 32, 16, 8, 4, 1):
+            pad = r // 2
+            p = (h + 2 * pad - r) // st + 1
+            d = _lib.ConvDesc(n, h, h, c, k, r, r, st, pad, p, p)
+            ws = L.pbdk_conv_wgrad_workspace_bytes(ctypes.byref(d))
+            if prev is not None:
+                assert ws <= prev, (h, c, k, r, st, n, ws, prev)
+            prev = ws
