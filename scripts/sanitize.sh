@@ -16,7 +16,21 @@ e = ex.Partition(0, 5, 2, 2, model="effb0", image=64); e.init_params()
 for k in range(6): e.set_path(k, [5 if c > 1 else 0 for c in range(ex.mb_layers(k, "effb0"))] if k else [0, 0, 5, 5])
 e.step()
 torch.cuda.synchronize()
-print("ok", p.losses(), m.losses(), e.losses())
+# b = 96: block 0's student wgrads take the multi-tap kernel (m_tiles x groups >= 4 x 148)
+q = ex.Partition(0, 3, 96, 96); q.init_params(); q.step()
+import ctypes
+from paper_2301_12443_b200 import _lib
+L = _lib.lib()
+for (n, h, c, k, r, st) in [(96, 32, 16, 32, 3, 1), (96, 32, 32, 64, 3, 1), (128, 32, 64, 128, 3, 2)]:
+    pp = (h + 2 * (r // 2) - r) // st + 1
+    d = _lib.ConvDesc(n, h, h, c, k, r, r, st, r // 2, pp, pp)
+    x = torch.randn(n, h, h, c, device="cuda").bfloat16(); dy = torch.randn(n, pp, pp, k, device="cuda").bfloat16()
+    dw = torch.empty(k, r, r, c, device="cuda")
+    wsb = L.pbdk_conv_wgrad_workspace_bytes(ctypes.byref(d)); ws = torch.empty(max(wsb, 16), device="cuda", dtype=torch.uint8)
+    assert L.pbdk_conv_wgrad(ctypes.byref(d), x.data_ptr(), dy.data_ptr(), dw.data_ptr(), ws.data_ptr(), wsb,
+                             ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)) == 0
+torch.cuda.synchronize()
+print("ok", p.losses(), m.losses(), e.losses(), q.losses())
 PY
 for tool in memcheck racecheck synccheck; do
   timeout 900 compute-sanitizer --tool $tool --print-limit 20 python /tmp/san_step.py > gpurun_out/sanitize_$tool.log 2>&1
