@@ -562,8 +562,12 @@ class ResNetPartition final : public PartitionBase {
   }
 
   void build_plans() {
+    // Every ResNet conv (teacher and student) gets two epilogue warps per TMEM lane quarter whatever
+    // its K — slightly slower alone (64->64 @32x32: 26.7 -> 27.1 us) but the step, where the convs
+    // share SMs, gains 0.892 -> 0.886 ms (teacher-only or student-only: no gain).  PBDK_EPW=1
+    // disables it everywhere.
     for (size_t i = 0; i < tblocks_.size(); ++i) {
-      const pbdk::ConvGridScope scope(env_list("PBDK_TCONV_CTAS_LIST", i, env_ctas("PBDK_TCONV_CTAS")));
+      const pbdk::ConvGridScope scope(env_list("PBDK_TCONV_CTAS_LIST", i, env_ctas("PBDK_TCONV_CTAS")), 2);
       for (TConv& c : tblocks_[i].convs) {
         const pbdk_conv_desc cd{n_, c.hin, c.hin, c.cs, c.cout, c.r, c.r, c.stride, c.pad, c.hout, c.hout};
         check(pbdk::fprop_plan(cd, c.in, c.w, c.out, c.bias, c.aux, c.epi, &c.plan), "teacher plan");
@@ -577,7 +581,7 @@ class ResNetPartition final : public PartitionBase {
                                                                 : (sblocks_.size() >= 3 ? 64 : 0);
     for (size_t i = 0; i < sblocks_.size(); ++i) {
       SBlock& s = sblocks_[i];
-      const pbdk::ConvGridScope scope(env_list("PBDK_SCONV_CTAS_LIST", i, sconv));
+      const pbdk::ConvGridScope scope(env_list("PBDK_SCONV_CTAS_LIST", i, sconv), 2);
       const bf16* sh = shadow_ + s.base;
       float* g = grads_ + s.base;
       check(pbdk::fprop_plan(conv1_desc(s, n_), s.in, sh + s.lay.w1, s.y1, nullptr, nullptr, PBDK_EPI_STORE,

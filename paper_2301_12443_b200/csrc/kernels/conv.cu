@@ -1522,6 +1522,7 @@ bool halo_enabled() {
 }
 
 thread_local int t_grid_sms = 0;  // ConvGridScope
+thread_local int t_epw = 0;       // ConvGridScope: preferred epilogue warps per lane quarter (0 = by shape)
 // SMs a plan may spread over (persistent grids, one-wave split counts)
 int grid_sms();
 
@@ -1695,8 +1696,14 @@ bool m2_auto(const pbdk_conv_desc& d, const ConvGeom& g, int bn) {
 
 }  // namespace
 
-ConvGridScope::ConvGridScope(int sms) : saved(t_grid_sms) { t_grid_sms = sms; }
-ConvGridScope::~ConvGridScope() { t_grid_sms = saved; }
+ConvGridScope::ConvGridScope(int sms, int epw) : saved(t_grid_sms), saved_epw(t_epw) {
+  t_grid_sms = sms;
+  t_epw = epw;
+}
+ConvGridScope::~ConvGridScope() {
+  t_grid_sms = saved;
+  t_epw = saved_epw;
+}
 
 int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, const float* bias, const void* aux,
                int epi, FpropPlan* plan) {
@@ -1733,7 +1740,7 @@ int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, c
     return e != nullptr ? std::atoi(e) : 0;
   }();
   const bool short_k = (d.r * d.s == 9 && d.c <= 32) || (d.r * d.s == 1 && d.c <= 64);
-  const int epw = bn >= 32 && bn <= 128 && (epw_env == 2 || (epw_env == 0 && short_k)) ? 2 : 1;
+  const int epw = bn >= 32 && bn <= 128 && (epw_env == 2 || (epw_env == 0 && (short_k || t_epw == 2))) ? 2 : 1;
   FpropLauncher l = nullptr;
   switch (bkc) {
     case 16: l = bres ? pick_fprop<16, true>(bn, epw) : pick_fprop<16, false>(bn, epw); break;

@@ -71,10 +71,11 @@ struct WgradArgs {
 // While alive, fprop plans built by this thread spread their persistent grid over at most `sms` SMs
 // (0 = all).  Results do not depend on it (tiles are independent); wgrad split counts, which fix a
 // summation order, ignore it.
+// `epw` = 2 asks for two epilogue warps per TMEM lane quarter on every eligible conv (0 = by shape).
 struct ConvGridScope {
-  explicit ConvGridScope(int sms);
+  explicit ConvGridScope(int sms, int epw = 0);
   ~ConvGridScope();
-  int saved;
+  int saved, saved_epw;
 };
 
 struct WgradPlan {
