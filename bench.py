@@ -185,7 +185,7 @@ def time_dominant_kernel(torch, batch):
 
 
 # ---------------------------------------------------------------- CPU legs
-def cpu_oracle_rate(samples_per_step=32, budget_s=10.0, max_steps=64):
+def cpu_oracle_rate(samples_per_step=256, budget_s=15.0, max_steps=16):
     """The oracle (C restatement, OpenMP) on the host cores: samples/s over as many whole steps as fit
     in about `budget_s` seconds of CPU work (bounded sample of the same workload)."""
     from oracle import bd
@@ -201,39 +201,48 @@ def cpu_oracle_rate(samples_per_step=32, budget_s=10.0, max_steps=64):
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the CPU implementation of the path (the oracle port: the reference itself has
-    no executable distillation step) on the host cores, same metric and config."""
+    """--impl reference: the CPU implementation of the path on the host cores, same metric, config and
+    global batch as our arm.  The reference itself has no executable distillation step, so
+    this is the oracle port (oracle/bd_oracle.c, OpenMP over every host core): each step is one whole
+    global batch (256 samples per GPU, all 4 blocks, teacher fwd + student fwd/bwd + SGD).  The run is
+    bounded: after one warm-up step, steps are timed until `--steps` are done or ~150 s of CPU time
+    elapsed (min 2), and the line says how many ran.  Only oracle/ libraries are loaded here (no repo
+    product .so); the reference's own partitioner (oracle/_ref, compiled unmodified) is timed beside it."""
     if rank != 0:
         return
     from oracle import bd
-    sample = 8
-    tr = bd.Trainer(sample, bf16_mode=1)
-    for w in range(args.warmup):
+    gb = args.batch * max(1, args.gpus)
+    tr = bd.Trainer(gb, bf16_mode=1)
+    warm = min(args.warmup, 1)
+    for w in range(warm):
         tr.step(w)
+    budget_s = float(os.environ.get("PBD_REF_BUDGET_S", "150"))
     t0 = time.perf_counter()
-    for s in range(args.steps):
-        tr.step(args.warmup + s)
+    done = 0
+    while done < args.steps and (done < 2 or time.perf_counter() - t0 < budget_s):
+        tr.step(warm + done)
+        done += 1
     dt = time.perf_counter() - t0
-    rate = sample * args.steps / dt
+    rate = gb * done / dt
     threads = bd.lib().bdo_threads()
+    sample = f"{done} whole steps of the {gb}-sample global batch (all 4 blocks, fwd+bwd+SGD), {dt:.1f} s"
     line = {"metric": METRIC, "value": rate, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+            "steps": done, "warmup": warm, "ms_per_step": dt / done * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16-emulated fp32",
             "data": "synthetic (Philox4x32-10, DESIGN.md §3)",
             "config": {"workload": "cifar-resnet18-teacher/slim-student 4 blocks (configs[1])",
-                       "global_batch": args.batch * args.gpus, "sample_per_step": sample, "parallelism": "cpu"},
-            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"{sample} samples x {args.steps} steps, all 4 blocks, fwd+bwd+SGD"},
+                       "global_batch": gb, "image": "32x32x3", "blocks": 4, "parallelism": "cpu",
+                       "steps_requested": args.steps, "warmup_requested": args.warmup,
+                       "same_config": True},
+            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     try:
         from oracle import ref
         if ref.available():
-            from paper_2301_12443_b200 import core
-            prof = core.synth_profile(shape="front-heavy", blocks=10, front_weight=4.0, curvature=0.4,
-                                      num_devices=8)
+            prof = ref.synth_profile(shape="front-heavy", blocks=10, front_weight=4.0, curvature=0.4,
+                                     num_devices=8)
             line["partitioner"] = {"reference_best_schedule_ms": ref.time_best_schedule(prof, threads=1, reps=20),
-                                   "ours_best_schedule_ms": core.time_best_schedule(prof, reps=20),
-                                   "case": "B=10 N=8 (11440 configs)"}
+                                   "case": "B=10 N=8 (11440 configs), reference core compiled unmodified"}
     except Exception as e:  # pragma: no cover - informational only
         line["partitioner"] = {"error": str(e)}
     print(json.dumps(line), flush=True)
@@ -380,7 +389,7 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_cpu_baseline:
         rate, cores, dt, nsteps = cpu_oracle_rate()
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"32 samples x {nsteps} steps of the same workload (oracle/bd_oracle.c, {dt:.1f} s)"}
+               "sample": f"{nsteps} whole steps of the same 256-sample batch (oracle/bd_oracle.c, {dt:.1f} s)"}
 
     working_set = models.step_working_set_bytes(b)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,

@@ -296,7 +296,10 @@ class PipeBD:
         step_index = self.stage.step_index()
         B = len({k for p in self.schedule["partitions"] for k in range(p["blocks"][0], p["blocks"][1] + 1)})
         # current state of the blocks this rank owns (identical across its DP group after sync)
-        state = {k: self.stage.block_state(k) for k in range(self.me.block_lo, self.me.block_hi + 1)}
+        # Owned copies: block_state() returns zero-copy views of the executor's device arena, which
+        # is freed when the old stage is dropped below (make_stage) — the views must not outlive it.
+        state = {k: [t.clone() for t in self.stage.block_state(k)]
+                 for k in range(self.me.block_lo, self.me.block_hi + 1)}
         nme = new_place[self.rank]
         incoming = {}
         ops = []
@@ -326,6 +329,7 @@ class PipeBD:
         for j, p in enumerate(new_schedule["partitions"]):
             devs = list(p["devices"])
             self.groups[j] = dist.new_group(devs) if len(devs) > 1 else None
+        self.stage = None  # release the old executor (its arena) before allocating the new one
         self.stage = make_stage(nme.block_lo, nme.block_hi, nme.count, nme.first)
         for k, (w, v) in incoming.items():
             self.stage.set_block_state(k, w, v)

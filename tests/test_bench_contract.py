@@ -22,3 +22,6 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] in ("port", "reference") and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["config"]["workload"].startswith("cifar")
+    # like-for-like with our arm: one whole 256-sample global batch per timed step
+    assert d["config"]["same_config"] is True and d["config"]["global_batch"] == 256
+    assert "ours_best_schedule_ms" not in d.get("partitioner", {})  # the arm loads no product library

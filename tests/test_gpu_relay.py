@@ -303,3 +303,50 @@ def test_checkpoint_resume_bitwise_across_schedules(ex, tmp_path):
     ref = _single(ex, b, 2 * steps)
     assert np.array_equal(res[0][0], ref.params().cpu().numpy())
     assert res[0][1] == ref.losses()
+
+
+def _migrate_worker(rank, world, port, sched_a, sched_b, b, steps, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    from paper_2301_12443_b200 import executor
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        def make(lo, hi, n, first):
+            p = executor.Partition(lo, hi, n, b)
+            p.init_params()
+            p.set_shard(n, first)
+            return p
+        pipe = runtime.PipeBD(sched_a, b, make, relay="peer")
+        for _ in range(steps):
+            pipe.step()
+        pipe.end_epoch()
+        torch.cuda.synchronize()
+        # rebuild the stage: the old executor's arena is freed while its state is handed over
+        pipe.migrate(sched_b, make)
+        for _ in range(steps):
+            pipe.step()
+        torch.cuda.synchronize()
+        q.put((rank, pipe.stage.params().cpu().numpy(), pipe.stage.momentum().cpu().numpy(), pipe.stage.losses()))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_migrate_with_device_executor_bitwise(ex):
+    """runtime.PipeBD.migrate on real executors (the handed-over state must not be views of the
+    old executor's freed arena): 3 steps, migrate (stage rebuilt), 3 more steps == 6 uninterrupted steps."""
+    b, steps = 8, 3
+    s = sched([(0, 3, [0])], b)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    proc = ctx.Process(target=_migrate_worker, args=(0, 1, port, s, s, b, steps, q))
+    proc.start()
+    _, params, mom, losses = q.get(timeout=300)
+    proc.join(timeout=120)
+    assert proc.exitcode == 0
+    ref = _single(ex, b, 2 * steps)
+    assert np.array_equal(params, ref.params().cpu().numpy())
+    assert np.array_equal(mom, ref.momentum().cpu().numpy())
+    assert losses == ref.losses()
