@@ -5,12 +5,15 @@
  * fields, function names, argument meanings and exception types as
  * proj/core/include/pbd/{errors,profile,cost_model,schedule,simulate}.hpp, so
  * reference callers (pbd_cli.cpp, the reference tests) compile against it
- * unchanged through the forwarding headers next to this file.  The
- * implementation is new (csrc/core/ sources): the AHD search precomputes every
- * (block range, group size) partition cost once and scans compositions over
- * that table instead of materialising ScheduleConfig objects, while keeping
- * the reference's floating-point evaluation order so the chosen partition and
- * its predicted times are bit-identical.
+ * unchanged through the forwarding headers next to this file (plus pbd/report.hpp for the
+ * reporting API).  Provenance of the implementation (csrc/core/): the AHD search is new — it
+ * precomputes every (block range, group size) partition cost once and scans compositions over
+ * that table instead of materialising ScheduleConfig objects, keeping the reference's
+ * floating-point evaluation order so the chosen partition and its predicted times are
+ * bit-identical.  The profile validation / JSON I/O / synth_profile (bpdg.cpp), the cost model
+ * (costs.cpp) and the simulator (pipeline_sim.cpp) are close restatements of the reference's
+ * profile.cpp, cost_model.cpp and simulate.cpp (Apache-2.0, The pbd Authors), because their
+ * error strings and operand order are the bit-exact contract.
  *
  * Additions beyond the reference API are marked [B200].
  */

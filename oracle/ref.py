@@ -40,6 +40,7 @@ def lib():
         L.ref_profile_drift.argtypes = [ctypes.c_char_p, ctypes.c_char_p, P(ctypes.c_double), P(V)]
         L.ref_load_save_profile.argtypes = [ctypes.c_char_p, P(V), P(V)]
         L.ref_synth_profile.argtypes = [ctypes.c_char_p, P(V), P(V)]
+        L.ref_report_render.argtypes = [ctypes.c_char_p, ctypes.c_char_p, P(V), P(V)]
         _L = L
     return _L
 
@@ -134,3 +135,11 @@ def synth_profile(**spec):
     out, err = V(), V()
     _chk(lib().ref_synth_profile(json.dumps(spec).encode(), ctypes.byref(out), ctypes.byref(err)), err)
     return json.loads(_take(out))
+
+
+def report_render(profile, sim=None):
+    """speedup/breakdown tables (text, csv, json) + two gantt_svg renderings, "\n@@\n"-separated."""
+    out, err = V(), V()
+    _chk(lib().ref_report_render(_t(profile), json.dumps(sim or {}).encode(), ctypes.byref(out), ctypes.byref(err)),
+         err)
+    return _take(out)

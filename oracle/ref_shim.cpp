@@ -14,6 +14,7 @@
 #include "json.hpp"
 #include "pbd/cost_model.hpp"
 #include "pbd/profile.hpp"
+#include "pbd/report.hpp"
 #include "pbd/schedule.hpp"
 #include "pbd/simulate.hpp"
 
@@ -191,6 +192,33 @@ int ref_synth_profile(const char* spec_json, char** out, char** err) {
     if (j.contains("num_devices")) s.hardware.num_devices = j.at("num_devices").get<int>();
     if (j.contains("global_batch")) s.global_batch = j.at("global_batch").get<int>();
     *out = dup(pbd::save_profile(pbd::synth_profile(s)));
+  });
+}
+
+// The reference's report API on one profile: Comparison {dp (baseline), ir, tr+dpu+ahd}, its
+// speedup / breakdown tables in text, CSV and JSON, and gantt_svg of the AHD run with default and
+// non-default options, concatenated with "\n@@\n" separators (tests/test_report.py renders the
+// same with libpbd.so and compares the bytes).
+int ref_report_render(const char* profile, const char* sim, char** out, char** err) {
+  return guarded(err, [&] {
+    const pbd::CostModel m(pbd::load_profile(profile));
+    const pbd::SimConfig sc = sim_from_json(sim);
+    const pbd::SimReport ahd = pbd::simulate(m, pbd::best_schedule(m).first, sc);
+    pbd::Comparison c({{"dp", pbd::simulate_baseline(m, pbd::dp_schedule(m), sc)},
+                       {"ir", pbd::simulate(m, pbd::ir_schedule(m), sc)},
+                       {"tr+dpu+ahd", ahd}},
+                      "dp");
+    pbd::GanttOptions o;
+    o.title = "pipeline";
+    o.legend = false;
+    o.show_overlapped_sends = false;
+    o.plot_width_px = 700.0;
+    o.lane_height_px = 20.0;
+    const std::string sep = "\n@@\n";
+    *out = dup(pbd::speedup_table(c).to_text() + sep + pbd::speedup_table(c).to_csv() + sep +
+               pbd::speedup_table(c).to_json() + sep + pbd::breakdown_table(c).to_text() + sep +
+               pbd::breakdown_table(c).to_csv() + sep + pbd::breakdown_table(c).to_json() + sep +
+               pbd::gantt_svg(ahd) + sep + pbd::gantt_svg(ahd, o));
   });
 }
 

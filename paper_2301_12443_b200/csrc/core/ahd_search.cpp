@@ -1,3 +1,6 @@
+// Attribution: validate_schedule / predicted_step_time / the DP-LS plan generators restate
+// proj/core/src/schedule.cpp, Copyright 2026 The pbd Authors, Apache License 2.0; the
+// best_schedule table search is new.
 // Automatic hybrid distribution (AHD) search and schedule documents.
 // Reference semantics: proj/core/src/schedule.cpp.
 //   canonical enumeration order      schedule.cpp:37-69, 115-134

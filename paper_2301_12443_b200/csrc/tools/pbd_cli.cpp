@@ -16,6 +16,7 @@
 //
 // The GPU-side commands (measure a profile on the device, run a schedule) live in
 // `python -m paper_2301_12443_b200.cli` because they drive torch.distributed.
+#include <charconv>
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
@@ -29,6 +30,7 @@
 #include <vector>
 
 #include "pbd/core.hpp"
+#include "pbd/report.hpp"
 
 namespace {
 
@@ -121,6 +123,15 @@ pbd::SimConfig sim_config(const Args& a, bool dpu_default) {
   return c;
 }
 
+// shortest round-trip form, integral values with ".0" (the JSON documents' number format)
+std::string shortest(double v) {
+  char b[64];
+  const auto r = std::to_chars(b, b + sizeof(b), v);
+  std::string t(b, r.ptr);
+  if (t.find_first_of(".eEn") == std::string::npos) t += ".0";
+  return t;
+}
+
 std::string fixed(double v, int digits = 6) {
   char b[64];
   std::snprintf(b, sizeof(b), "%.*f", digits, v);
@@ -202,49 +213,29 @@ int cmd_compare(const Args& a) {
   };
   std::vector<std::pair<std::string, pbd::SimReport>> rows;
   for (const auto& l : labels) rows.emplace_back(l, run(l));
-  // speedup = baseline makespan / makespan (the reference's speedup(), report.cpp:244-254)
-  const double ref = rows.front().second.makespan_ms;
-  for (const auto& [l, r] : rows)
-    if (r.makespan_ms <= 0.0) throw pbd::ValidationError("zero makespan for label \"" + l + "\"");
-  std::vector<std::string> cats;
-  for (pbd::EventCategory c : pbd::kAllCategories) cats.emplace_back(pbd::to_string(c));
+  // the reference's report API (pbd/report.hpp, pbd_cli.cpp:238-252 of the reference)
+  const pbd::Comparison cmp(std::move(rows), base.front());
+  const pbd::Table speed = pbd::speedup_table(cmp), split = pbd::breakdown_table(cmp);
   const std::string fmt = a.get("format", "text");
   std::ostringstream o;
-  if (fmt == "json") {
-    o << "{\n  \"baseline\": \"" << rows.front().first << "\",\n  \"speedup\": {";
-    for (size_t i = 0; i < rows.size(); ++i)
-      o << (i ? ", " : "") << "\"" << rows[i].first << "\": " << ref / rows[i].second.makespan_ms;
-    o << "},\n  \"breakdown\": {";
-    for (size_t i = 0; i < rows.size(); ++i) {
-      o << (i ? ", " : "") << "\"" << rows[i].first << "\": {";
-      bool first = true;
-      for (const auto& c : cats) {
-        const auto it = rows[i].second.category_totals_ms.find(c);
-        const double v = it == rows[i].second.category_totals_ms.end() ? 0.0 : it->second;
-        o << (first ? "" : ", ") << "\"" << c << "\": " << v / rows[i].second.num_devices;
-        first = false;
-      }
-      o << "}";
+  if (fmt == "json") {  // {"baseline", "breakdown": rows of breakdown_table, "speedup": label -> ratio}
+    std::string rows_json = split.to_json();
+    rows_json.pop_back();
+    for (size_t p = rows_json.find('\n'); p != std::string::npos; p = rows_json.find('\n', p + 3))
+      rows_json.replace(p, 1, "\n  ");
+    o << "{\n  \"baseline\": \"" << cmp.baseline_label << "\",\n  \"breakdown\": " << rows_json
+      << ",\n  \"speedup\": {";
+    bool first = true;
+    for (const auto& [l, v] : pbd::speedup(cmp)) {
+      o << (first ? "\n" : ",\n") << "    \"" << l << "\": " << shortest(v);
+      first = false;
     }
-    o << "}\n}\n";
+    o << "\n  }\n}\n";
+  } else if (fmt == "csv") {
+    o << speed.to_csv() << "\n" << split.to_csv();
   } else {
-    const char sep = fmt == "csv" ? ',' : ' ';
-    if (fmt != "csv") o << "== speedup vs " << rows.front().first << " ==\n";
-    o << "label" << sep << "makespan_ms" << sep << "steady_step_ms" << sep << "bubble_ratio" << sep << "speedup\n";
-    for (const auto& [l, r] : rows)
-      o << l << sep << fixed(r.makespan_ms, 3) << sep << fixed(r.steady_state_step_ms, 3) << sep
-        << fixed(r.bubble_ratio, 3) << sep << fixed(ref / r.makespan_ms, 3) << "x\n";
-    o << (fmt == "csv" ? "\n" : "\n== breakdown (per-device ms) ==\n") << "label";
-    for (const auto& c : cats) o << sep << c;
-    o << "\n";
-    for (const auto& [l, r] : rows) {
-      o << l;
-      for (const auto& c : cats) {
-        const auto it = r.category_totals_ms.find(c);
-        o << sep << fixed((it == r.category_totals_ms.end() ? 0.0 : it->second) / r.num_devices, 4);
-      }
-      o << "\n";
-    }
+    o << "== speedup vs " << cmp.baseline_label << " ==\n"
+      << speed.to_text() << "\n== breakdown (per-device ms) ==\n" << split.to_text();
   }
   write_doc(o.str(), a.get("out"));
   return kOk;

@@ -52,7 +52,7 @@ def test_simulate_report_gantt_and_compare(profile, tmp_path):
     r = run("compare", str(profile), "--against", "dp,ls,ir", "--ablation", "tr,tr+dpu,tr+dpu+ahd", "--format", "json")
     assert r.returncode == 0, r.stderr
     cmp = json.loads(r.stdout)
-    assert cmp["baseline"] == "dp" and cmp["speedup"]["dp"] == 1.0 and set(cmp["breakdown"]) == {
+    assert cmp["baseline"] == "dp" and cmp["speedup"]["dp"] == 1.0 and {row["label"] for row in cmp["breakdown"]} == {
         "dp", "ls", "ir", "tr", "tr+dpu", "tr+dpu+ahd"}
     assert run("compare", str(profile), "--against", "dp,xx").returncode == 1
 
