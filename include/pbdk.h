@@ -74,6 +74,25 @@ int pbdk_conv_wgrad(const pbdk_conv_desc* d, const void* x, const void* dy, floa
 int pbdk_weight_flip(const void* w, void* wt, int k, int r, int s, int c, void* stream);
 
 
+/* ------------------------------------------------------------------ fp32 convolutions (3xTF32, configs[0]) */
+/* Split-fp32 storage: an operand tensor [rows][2c] holds hi = tf32(x) (round to nearest) in channels
+ * [0, c) and lo = x - hi (exact) in [c, 2c); hi + lo == x.  The tensor cores compute every product as
+ * a_hi*b_hi + a_hi*b_lo + a_lo*b_hi (tcgen05 kind::tf32, fp32 accumulation).  d->c / d->k are the
+ * channels per half (multiples of 16; 16 or a multiple of 32 for inputs).
+ * x: split [n][h][w][2c]; w: split [k][r][s][2c]; y: split [m][2k] (y_split = 1) or plain [m][k];
+ * aux (residual for PBDK_EPI_BIAS_RES_RELU, mask source for PBDK_EPI_RELU_MASK): split [m][2k].
+ * Epilogues: STORE, BIAS, BIAS_RELU, BIAS_RES_RELU, RELU_MASK. */
+int pbdk_conv3x_fprop(const pbdk_conv_desc* d, const float* x, const float* w, float* y, int y_split,
+                      const float* bias, const float* aux, int epilogue, void* stream);
+/* dw[k,r,s,c] (plain fp32) from split x [n][h][w][2c] and split dy [n][p][q][2k] (k multiple of 32) */
+size_t pbdk_conv3x_wgrad_workspace_bytes(const pbdk_conv_desc* d);
+int pbdk_conv3x_wgrad(const pbdk_conv_desc* d, const float* x, const float* dy, float* dw, void* workspace,
+                      size_t workspace_bytes, void* stream);
+/* plain [rows][c] -> split [rows][2c] */
+int pbdk_split_tf32(const float* src, float* dst, size_t rows, int c, void* stream);
+/* master w [k][r][s][c] -> split flipped wt [c][r][s][2k] (dgrad weights) */
+int pbdk_weight_flip_split(const float* w, float* wt, int k, int r, int s, int c, void* stream);
+
 /* ------------------------------------------------------------------ K12: synthetic input (load_data) */
 /* x[n][32][32][16] bf16 (3 Philox channels + 13 zero pad channels) for global samples
  * first_sample + (*step_counter)*global_batch + i  (step_counter may be NULL). */

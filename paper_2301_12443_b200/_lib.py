@@ -65,7 +65,16 @@ def lib() -> ctypes.CDLL:
     L.pbdk_conv_wgrad.argtypes = [ctypes.POINTER(ConvDesc), c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
                                   c_void_p]
     L.pbdk_weight_flip.argtypes = [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p]
-    for name in ("pbdk_conv_fprop", "pbdk_conv_wgrad", "pbdk_weight_flip"):
+    L.pbdk_conv3x_fprop.argtypes = [ctypes.POINTER(ConvDesc), c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p,
+                                    c_int, c_void_p]
+    L.pbdk_conv3x_wgrad_workspace_bytes.argtypes = [ctypes.POINTER(ConvDesc)]
+    L.pbdk_conv3x_wgrad_workspace_bytes.restype = c_size_t
+    L.pbdk_conv3x_wgrad.argtypes = [ctypes.POINTER(ConvDesc), c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
+                                    c_void_p]
+    L.pbdk_split_tf32.argtypes = [c_void_p, c_void_p, c_size_t, c_int, c_void_p]
+    L.pbdk_weight_flip_split.argtypes = [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p]
+    for name in ("pbdk_conv_fprop", "pbdk_conv_wgrad", "pbdk_weight_flip", "pbdk_conv3x_fprop", "pbdk_conv3x_wgrad",
+                 "pbdk_split_tf32", "pbdk_weight_flip_split"):
         getattr(L, name).restype = c_int
     _lib = L
     return L

@@ -19,6 +19,7 @@
 
 #include "bd_kernels.hpp"
 #include "pbdk.h"
+#include "sm100.cuh"
 
 namespace pbdk {
 
@@ -181,6 +182,74 @@ struct Vec<4> {
   }
 };
 
+// Row I/O policies of the [M][C] kernels: bf16 rows (the bf16 workloads), plain fp32 rows and split
+// fp32 rows (the fp32 workload; conv_tf32.hpp: row r = [hi(C) | lo(C)] at r*2C, value = hi + lo,
+// stored as hi = tf32(x), lo = x - hi).
+struct IoBf16 {
+  using T = __nv_bfloat16;
+  template <int V>
+  __device__ static void load(const T* p, size_t r, int C, int c0, float (&f)[V]) {
+    Vec<V>::load(p + r * C + c0, f);
+  }
+  template <int V>
+  __device__ static void store(T* p, size_t r, int C, int c0, const float (&f)[V]) {
+    Vec<V>::store(p + r * C + c0, f);
+  }
+};
+struct IoF32 {
+  using T = float;
+  template <int V>
+  __device__ static void load(const T* p, size_t r, int C, int c0, float (&f)[V]) {
+    const float4* q = reinterpret_cast<const float4*>(p + r * C + c0);
+#pragma unroll
+    for (int i = 0; i < V / 4; ++i) {
+      const float4 v = q[i];
+      f[4 * i] = v.x;
+      f[4 * i + 1] = v.y;
+      f[4 * i + 2] = v.z;
+      f[4 * i + 3] = v.w;
+    }
+  }
+  template <int V>
+  __device__ static void store(T* p, size_t r, int C, int c0, const float (&f)[V]) {
+    float4* q = reinterpret_cast<float4*>(p + r * C + c0);
+#pragma unroll
+    for (int i = 0; i < V / 4; ++i) q[i] = make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]);
+  }
+};
+struct IoSplit {
+  using T = float;
+  template <int V>
+  __device__ static void load(const T* p, size_t r, int C, int c0, float (&f)[V]) {
+    const float4* h = reinterpret_cast<const float4*>(p + r * 2 * C + c0);
+    const float4* l = reinterpret_cast<const float4*>(p + r * 2 * C + C + c0);
+#pragma unroll
+    for (int i = 0; i < V / 4; ++i) {
+      const float4 a = h[i], b = l[i];
+      f[4 * i] = a.x + b.x;
+      f[4 * i + 1] = a.y + b.y;
+      f[4 * i + 2] = a.z + b.z;
+      f[4 * i + 3] = a.w + b.w;
+    }
+  }
+  template <int V>
+  __device__ static void store(T* p, size_t r, int C, int c0, const float (&f)[V]) {
+    float4* h = reinterpret_cast<float4*>(p + r * 2 * C + c0);
+    float4* l = reinterpret_cast<float4*>(p + r * 2 * C + C + c0);
+#pragma unroll
+    for (int i = 0; i < V / 4; ++i) {
+      float hi[4], lo[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        hi[j] = tf32_hi(f[4 * i + j]);
+        lo[j] = f[4 * i + j] - hi[j];
+      }
+      h[i] = make_float4(hi[0], hi[1], hi[2], hi[3]);
+      l[i] = make_float4(lo[0], lo[1], lo[2], lo[3]);
+    }
+  }
+};
+
 struct RowTiling {
   int cg, rpp, chunks, rows_per_chunk;
 };
@@ -275,9 +344,9 @@ __device__ __forceinline__ double cta_sum(const float* __restrict__ v, int n) {
 }
 
 // -- BN statistics: per-channel (sum y, sum y^2) of one or two tensors of the same shape
-template <int V, int NT>
-__global__ void __launch_bounds__(kThreads) bn_stats_partial_kernel(const __nv_bfloat16* __restrict__ y0,
-                                                                    const __nv_bfloat16* __restrict__ y1, int m,
+template <int V, int NT, class IO = IoBf16>
+__global__ void __launch_bounds__(kThreads) bn_stats_partial_kernel(const typename IO::T* __restrict__ y0,
+                                                                    const typename IO::T* __restrict__ y1, int m,
                                                                     int C, int rows_per_chunk, int cg, int rpp,
                                                                     float* __restrict__ partial) {
   const int g = threadIdx.x % cg;
@@ -288,10 +357,9 @@ __global__ void __launch_bounds__(kThreads) bn_stats_partial_kernel(const __nv_b
     const int r1 = min(m, r0 + rows_per_chunk);
 #pragma unroll 4
     for (int r = r0 + slot; r < r1; r += rpp) {
-      const size_t off = static_cast<size_t>(r) * C + g * V;
       float f[NT][V];
-      Vec<V>::load(y0 + off, f[0]);
-      if (NT == 2) Vec<V>::load(y1 + off, f[NT - 1]);
+      IO::template load<V>(y0, r, C, g * V, f[0]);
+      if (NT == 2) IO::template load<V>(y1, r, C, g * V, f[NT - 1]);
 #pragma unroll
       for (int t = 0; t < NT; ++t)
 #pragma unroll
@@ -325,12 +393,12 @@ __global__ void bn_stats_finalize_kernel(const float* __restrict__ partial, int 
 
 // -- BN apply + ReLU as a per-channel affine map: a = bf16(relu(fmaf(A, y, B))),
 //    A = gamma*rstd, B = fmaf(-A, mean, beta)
-template <int V>
-__global__ void __launch_bounds__(kThreads) bn_apply_relu_kernel(const __nv_bfloat16* __restrict__ y,
+template <int V, class IN = IoBf16, class OUT = IoBf16>
+__global__ void __launch_bounds__(kThreads) bn_apply_relu_kernel(const typename IN::T* __restrict__ y,
                                                                  const float* __restrict__ mean_rstd,
                                                                  const float* __restrict__ gamma,
                                                                  const float* __restrict__ beta,
-                                                                 __nv_bfloat16* __restrict__ a, int m, int C, int cg,
+                                                                 typename OUT::T* __restrict__ a, int m, int C, int cg,
                                                                  int rpp) {
   const int g = threadIdx.x % cg;
   const int slot = threadIdx.x / cg;
@@ -345,24 +413,23 @@ __global__ void __launch_bounds__(kThreads) bn_apply_relu_kernel(const __nv_bflo
   const int step = gridDim.x * rpp;
 #pragma unroll 4
   for (int r = blockIdx.x * rpp + slot; r < m; r += step) {
-    const size_t off = static_cast<size_t>(r) * C + c0;
     float f[V];
-    Vec<V>::load(y + off, f);
+    IN::template load<V>(y, r, C, c0, f);
 #pragma unroll
     for (int j = 0; j < V; ++j) {
       const float z = fmaf(A[j], f[j], B[j]);
       f[j] = z > 0.0f ? z : 0.0f;
     }
-    Vec<V>::store(a + off, f);
+    OUT::template store<V>(a, r, C, c0, f);
   }
 }
 
 // -- fused distillation loss.  z = A2*y2 + As*ysc + Bz (both BNs as affine maps), s = relu(z),
 //    L += (s-t)^2, g = [z>0] (s-t)*gscale; partial sums of g, g*y2, g*ysc.
 struct LossParams {
-  const __nv_bfloat16* y2;
-  const __nv_bfloat16* ys;
-  const __nv_bfloat16* t;
+  const void* y2;  // IN rows
+  const void* ys;  // IN rows
+  const void* t;   // TG rows
   const float* st2;  // mean[C], rstd[C]
   const float* sts;
   const float* g2;
@@ -389,6 +456,7 @@ constexpr int kLossPartialV = 8;
 const int kLossChunks = -1;  // = red_target(), as the BN partials
 constexpr int kLossApplyV = 4;
 
+template <class IN = IoBf16, class TG = IoBf16>
 __global__ void __launch_bounds__(kThreads) loss_partial_kernel(const LossParams p, int rows_per_chunk, int cg, int rpp,
                                                                 float* __restrict__ partial,
                                                                 float* __restrict__ loss_partial) {
@@ -404,11 +472,10 @@ __global__ void __launch_bounds__(kThreads) loss_partial_kernel(const LossParams
     const int r1 = min(p.m, r0 + rows_per_chunk);
 #pragma unroll 4
     for (int r = r0 + slot; r < r1; r += rpp) {
-      const size_t off = static_cast<size_t>(r) * p.C + gi * V;
       float y2[V], ys[V], t[V];
-      Vec<V>::load(p.y2 + off, y2);
-      Vec<V>::load(p.ys + off, ys);
-      Vec<V>::load(p.t + off, t);
+      IN::template load<V>(static_cast<const typename IN::T*>(p.y2), r, p.C, gi * V, y2);
+      IN::template load<V>(static_cast<const typename IN::T*>(p.ys), r, p.C, gi * V, ys);
+      TG::template load<V>(static_cast<const typename TG::T*>(p.t), r, p.C, gi * V, t);
 #pragma unroll
       for (int j = 0; j < V; ++j) {
         const float z = fmaf(A2[j], y2[j], fmaf(As[j], ys[j], Bz[j]));
@@ -469,9 +536,10 @@ __global__ void loss_finalize_kernel(const LossParams p, const float* __restrict
   }
 }
 
+template <class IN = IoBf16, class TG = IoBf16, class OUT = IoBf16>
 __global__ void __launch_bounds__(kThreads) loss_bwd_apply_kernel(const LossParams p, const float* __restrict__ coef,
-                                                                  int cg, int rpp, __nv_bfloat16* __restrict__ dy2,
-                                                                  __nv_bfloat16* __restrict__ dys) {
+                                                                  int cg, int rpp, typename OUT::T* __restrict__ dy2,
+                                                                  typename OUT::T* __restrict__ dys) {
   constexpr int V = kLossApplyV;
   const int gi = threadIdx.x % cg;
   const int slot = threadIdx.x / cg;
@@ -489,11 +557,10 @@ __global__ void __launch_bounds__(kThreads) loss_bwd_apply_kernel(const LossPara
   const int step = gridDim.x * rpp;
 #pragma unroll 4
   for (int r = blockIdx.x * rpp + slot; r < p.m; r += step) {
-    const size_t off = static_cast<size_t>(r) * p.C + c0;
     float y2[V], ys[V], t[V], o2[V], os[V];
-    Vec<V>::load(p.y2 + off, y2);
-    Vec<V>::load(p.ys + off, ys);
-    Vec<V>::load(p.t + off, t);
+    IN::template load<V>(static_cast<const typename IN::T*>(p.y2), r, p.C, c0, y2);
+    IN::template load<V>(static_cast<const typename IN::T*>(p.ys), r, p.C, c0, ys);
+    TG::template load<V>(static_cast<const typename TG::T*>(p.t), r, p.C, c0, t);
 #pragma unroll
     for (int j = 0; j < V; ++j) {
       const float z = fmaf(A2[j], y2[j], fmaf(As[j], ys[j], Bz[j]));
@@ -502,15 +569,15 @@ __global__ void __launch_bounds__(kThreads) loss_bwd_apply_kernel(const LossPara
       o2[j] = fmaf(A2[j], g, fmaf(Q2[j], y2[j], R2[j]));
       os[j] = fmaf(As[j], g, fmaf(Qs[j], ys[j], Rs[j]));
     }
-    Vec<V>::store(dy2 + off, o2);
-    Vec<V>::store(dys + off, os);
+    OUT::template store<V>(dy2, r, p.C, c0, o2);
+    OUT::template store<V>(dys, r, p.C, c0, os);
   }
 }
 
 // -- BN backward (first BN of the unit): partial sums of g and g*y, finalize, apply
-template <int V>
-__global__ void __launch_bounds__(kThreads) bn_bwd_partial_kernel(const __nv_bfloat16* __restrict__ gin,
-                                                                  const __nv_bfloat16* __restrict__ y, int m, int C,
+template <int V, class IN = IoBf16>
+__global__ void __launch_bounds__(kThreads) bn_bwd_partial_kernel(const typename IN::T* __restrict__ gin,
+                                                                  const typename IN::T* __restrict__ y, int m, int C,
                                                                   int rows_per_chunk, int cg, int rpp,
                                                                   float* __restrict__ partial) {
   const int gi = threadIdx.x % cg;
@@ -521,10 +588,9 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_partial_kernel(const __nv_bfl
     const int r1 = min(m, r0 + rows_per_chunk);
 #pragma unroll 4
     for (int r = r0 + slot; r < r1; r += rpp) {
-      const size_t off = static_cast<size_t>(r) * C + gi * V;
       float fg[V], fy[V];
-      Vec<V>::load(gin + off, fg);
-      Vec<V>::load(y + off, fy);
+      IN::template load<V>(gin, r, C, gi * V, fg);
+      IN::template load<V>(y, r, C, gi * V, fy);
 #pragma unroll
       for (int j = 0; j < V; ++j) {
         acc[0][j] += fg[j];
@@ -556,13 +622,13 @@ __global__ void bn_bwd_finalize_kernel(const float* __restrict__ partial, int ch
   }
 }
 
-template <int V>
-__global__ void __launch_bounds__(kThreads) bn_bwd_apply_kernel(const __nv_bfloat16* __restrict__ gin,
-                                                                const __nv_bfloat16* __restrict__ y,
+template <int V, class IN = IoBf16, class OUT = IoBf16>
+__global__ void __launch_bounds__(kThreads) bn_bwd_apply_kernel(const typename IN::T* __restrict__ gin,
+                                                                const typename IN::T* __restrict__ y,
                                                                 const float* __restrict__ st,
                                                                 const float* __restrict__ gamma,
                                                                 const float* __restrict__ coef, int m, int C, int cg,
-                                                                int rpp, __nv_bfloat16* __restrict__ dy) {
+                                                                int rpp, typename OUT::T* __restrict__ dy) {
   const int gi = threadIdx.x % cg;
   const int slot = threadIdx.x / cg;
   if (slot >= rpp) return;
@@ -577,13 +643,12 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_apply_kernel(const __nv_bfloa
   const int step = gridDim.x * rpp;
 #pragma unroll 4
   for (int r = blockIdx.x * rpp + slot; r < m; r += step) {
-    const size_t off = static_cast<size_t>(r) * C + c0;
     float fg[V], fy[V], o[V];
-    Vec<V>::load(gin + off, fg);
-    Vec<V>::load(y + off, fy);
+    IN::template load<V>(gin, r, C, c0, fg);
+    IN::template load<V>(y, r, C, c0, fy);
 #pragma unroll
     for (int j = 0; j < V; ++j) o[j] = fmaf(A[j], fg[j], fmaf(Q[j], fy[j], R[j]));
-    Vec<V>::store(dy + off, o);
+    OUT::template store<V>(dy, r, C, c0, o);
   }
 }
 

@@ -21,9 +21,10 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 }  // namespace
 
-bool encode_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
-                      const uint64_t* gstride_bytes, const uint32_t* box, const uint32_t* estride,
-                      int swizzle_bytes) {
+namespace {
+
+bool encode_tmap(CUtensorMapDataType type, CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
+                 const uint64_t* gstride_bytes, const uint32_t* box, const uint32_t* estride, int swizzle_bytes) {
   auto fn = encode_fn();
   if (fn == nullptr) return false;
   CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_NONE;
@@ -31,6 +32,7 @@ bool encode_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64
     case 32: sw = CU_TENSOR_MAP_SWIZZLE_32B; break;
     case 64: sw = CU_TENSOR_MAP_SWIZZLE_64B; break;
     case 128: sw = CU_TENSOR_MAP_SWIZZLE_128B; break;
+    case kSwizzle128Atom32: sw = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B; break;
     default: sw = CU_TENSOR_MAP_SWIZZLE_NONE; break;
   }
   cuuint64_t d[5];
@@ -43,10 +45,26 @@ bool encode_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64
     e[i] = estride[i];
   }
   for (int i = 0; i + 1 < rank; ++i) s[i] = gstride_bytes[i];
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, static_cast<cuuint32_t>(rank), const_cast<void*>(base), d, s,
+  CUresult r = fn(map, type, static_cast<cuuint32_t>(rank), const_cast<void*>(base), d, s,
                   b, e, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool encode_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
+                      const uint64_t* gstride_bytes, const uint32_t* box, const uint32_t* estride,
+                      int swizzle_bytes) {
+  return encode_tmap(CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, map, base, rank, dims, gstride_bytes, box, estride,
+                     swizzle_bytes);
+}
+
+bool encode_tmap_f32(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
+                     const uint64_t* gstride_bytes, const uint32_t* box, const uint32_t* estride,
+                     int swizzle_bytes) {
+  return encode_tmap(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, map, base, rank, dims, gstride_bytes, box, estride,
+                     swizzle_bytes);
 }
 
 }  // namespace pbdk
