@@ -36,6 +36,8 @@ extern "C" {
 #define PBDX_MODEL_RESNET_CIFAR 0    /* configs[0..1]: ResNet-18-CIFAR teacher -> slim residual student, 4 blocks */
 #define PBDX_MODEL_MBV2_PROXYLESS 1  /* configs[2]: MobileNetV2 teacher -> ProxylessNAS supernet student, 6 blocks */
 #define PBDX_MODEL_EFFB0_PROXYLESS 2 /* configs[3]: EfficientNet-B0 teacher (swish, squeeze-excite) -> same space */
+#define PBDX_MODEL_RESNET_CIFAR_FP32 3 /* configs[0]: the CIFAR workload in fp32 (3xTF32 tensor-core convolutions;
+                                          activations stored split fp32, see pbdk_conv3x_fprop) */
 
 typedef struct pbdx_desc {
   int block_lo, block_hi; /* inclusive block range of the model's chain        */
@@ -139,6 +141,8 @@ int pbdx_set_path(void* handle, int block, const int* path, int n);
  * out[9] = {w1, w2, wsc, g1, b1, g2, b2, gsc, bsc}; returns the block's element count
  * (negative on error).  Block 0 stores its 3 input channels padded to 16. */
 long pbdx_student_layout(int block, long* offsets);
+/* The same for PBDX_MODEL_RESNET_CIFAR_FP32 (block 0 stores its 3 input channels padded to 32). */
+long pbdx_student_layout_fp32(int block, long* offsets);
 
 /* ------------------------------------------------------------------ K11 peer relay (TR)
  * The reference models the hand-over of t_hi as ready = teacher_end + max(C(b_up), C(b_down))

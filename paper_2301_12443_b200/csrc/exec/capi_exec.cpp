@@ -39,6 +39,7 @@ int pbdx_create(const pbdx_desc* d, void** handle) {
   return guard([&] {
     switch (d->model) {
       case PBDX_MODEL_RESNET_CIFAR: *handle = pbd::exec::make_resnet_partition(*d); break;
+      case PBDX_MODEL_RESNET_CIFAR_FP32: *handle = pbd::exec::make_resnet_f32_partition(*d); break;
       case PBDX_MODEL_MBV2_PROXYLESS:
       case PBDX_MODEL_EFFB0_PROXYLESS: *handle = pbd::exec::make_mb_partition(*d); break;
       default: throw pbd::exec::BadArg("unknown model");

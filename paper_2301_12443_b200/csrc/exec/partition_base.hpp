@@ -487,6 +487,7 @@ class PartitionBase {
 
 // model factories
 PartitionBase* make_resnet_partition(const pbdx_desc& d);
+PartitionBase* make_resnet_f32_partition(const pbdx_desc& d);
 PartitionBase* make_mb_partition(const pbdx_desc& d);
 
 }  // namespace pbd::exec

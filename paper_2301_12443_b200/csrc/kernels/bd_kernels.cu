@@ -125,6 +125,43 @@ __global__ void pack_image_parity_kernel(const float* __restrict__ s0, const flo
   }
 }
 
+// fp32 workload image (conv_tf32.hpp split layout): x[pix][64] = [hi(32) | lo(32)], channels 0..2
+// real, from Philox (mode 0), staging slot s0 (mode 1) or slot (*counter & 1) (mode 2).
+constexpr int kF32ImageC = 32;
+__global__ void image_split_kernel(float* __restrict__ x, int n, int npix, long long first,
+                                   const long long* counter, int global_batch, uint32_t seed,
+                                   const float* __restrict__ s0, const float* __restrict__ s1, int mode) {
+  const long long base = first + (mode == 0 && counter != nullptr ? (*counter) * global_batch : 0);
+  const float* __restrict__ src = mode == 2 && (*counter & 1) ? s1 : s0;
+  const long long total = static_cast<long long>(n) * npix;
+  for (long long pix = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; pix < total;
+       pix += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float v[3];
+    if (mode == 0) {
+      const long long i = pix / npix;
+      const long long hw = pix - i * npix;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const unsigned long long idx =
+            static_cast<unsigned long long>(base + i) * (3ull * npix) + static_cast<unsigned long long>(hw * 3 + c);
+        uint32_t o;
+        philox10(static_cast<uint32_t>(idx), static_cast<uint32_t>(idx >> 32), 0u, 0u, seed, 0xDA7A0000u, o);
+        v[c] = sym_unit(o);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) v[c] = src[pix * 3 + c];
+    }
+    float4* dst = reinterpret_cast<float4*>(x + static_cast<size_t>(pix) * 2 * kF32ImageC);
+    const float h0 = tf32_hi(v[0]), h1 = tf32_hi(v[1]), h2 = tf32_hi(v[2]);
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    dst[0] = make_float4(h0, h1, h2, 0.f);
+    for (int q = 1; q < kF32ImageC / 4; ++q) dst[q] = z;
+    dst[kF32ImageC / 4] = make_float4(v[0] - h0, v[1] - h1, v[2] - h2, 0.f);
+    for (int q = kF32ImageC / 4 + 1; q < kF32ImageC / 2; ++q) dst[q] = z;
+  }
+}
+
 // dst[k][r][s][c_stored] = c < c_true ? U(-1,1)[counter=((k*r+..)*c_true+c, tensor)] * bound : 0
 __global__ void init_uniform_kernel(void* dst, int bf16_out, int k, int r, int s, int cs, int ct, uint32_t seed,
                                     uint32_t tensor, float bound) {
@@ -140,10 +177,15 @@ __global__ void init_uniform_kernel(void* dst, int bf16_out, int k, int r, int s
       philox10(static_cast<uint32_t>(j), tensor, 0u, 0u, seed, 0xB200B200u, o);
       v = sym_unit(o) * bound;
     }
-    if (bf16_out)
+    if (bf16_out == 1) {
       static_cast<__nv_bfloat16*>(dst)[i] = __float2bfloat16_rn(v);
-    else
+    } else if (bf16_out == 2) {  // split fp32 [k][r][s][hi cs | lo cs]
+      const float h = tf32_hi(v);
+      static_cast<float*>(dst)[krs * 2 * cs + c] = h;
+      static_cast<float*>(dst)[krs * 2 * cs + cs + c] = v - h;
+    } else {
       static_cast<float*>(dst)[i] = v;
+    }
   }
 }
 
@@ -738,22 +780,37 @@ size_t reduce_workspace_floats(int m, int c, int nv) {
 }
 
 int philox_image(void* x, int n, long long first, const long long* counter, int gb, uint32_t seed, cudaStream_t st,
-                 int side) {
+                 int side, int prec) {
   const int npix = side * side;
+  if (prec == 1) {
+    image_split_kernel<<<grid_for(static_cast<long long>(n) * npix), kThreads, 0, st>>>(
+        static_cast<float*>(x), n, npix, first, counter, gb, seed, nullptr, nullptr, 0);
+    return ok(cudaGetLastError());
+  }
   philox_image_kernel<<<grid_for(static_cast<long long>(n) * npix), kThreads, 0, st>>>(
       static_cast<__nv_bfloat16*>(x), n, npix, first, counter, gb, seed);
   return ok(cudaGetLastError());
 }
 
-int pack_image(const float* src, void* x, int n, cudaStream_t st, int side) {
+int pack_image(const float* src, void* x, int n, cudaStream_t st, int side, int prec) {
   const long long total = static_cast<long long>(n) * side * side;
+  if (prec == 1) {
+    image_split_kernel<<<grid_for(total), kThreads, 0, st>>>(static_cast<float*>(x), n, side * side, 0, nullptr, 0, 0,
+                                                             src, nullptr, 1);
+    return ok(cudaGetLastError());
+  }
   pack_image_kernel<<<grid_for(total), kThreads, 0, st>>>(src, static_cast<__nv_bfloat16*>(x), total);
   return ok(cudaGetLastError());
 }
 
 int pack_image_parity(const float* s0, const float* s1, const long long* counter, void* x, int n, cudaStream_t st,
-                      int side) {
+                      int side, int prec) {
   const long long total = static_cast<long long>(n) * side * side;
+  if (prec == 1) {
+    image_split_kernel<<<grid_for(total), kThreads, 0, st>>>(static_cast<float*>(x), n, side * side, 0, counter, 0, 0,
+                                                             s0, s1, 2);
+    return ok(cudaGetLastError());
+  }
   pack_image_parity_kernel<<<grid_for(total), kThreads, 0, st>>>(s0, s1, counter, static_cast<__nv_bfloat16*>(x),
                                                                  total);
   return ok(cudaGetLastError());
@@ -772,31 +829,45 @@ int fill(float* dst, size_t n, float v, cudaStream_t st) {
   return ok(cudaGetLastError());
 }
 
-int bn_stats(const void* y, int m, int c, float* ws, float* mean_rstd, cudaStream_t st) {
+int bn_stats(const void* y, int m, int c, float* ws, float* mean_rstd, cudaStream_t st, int prec) {
   if (c % 8 != 0 || c / 8 > kThreads) return PBDK_EINVAL;
   const RowTiling t = tiling_for(m, c, 8);
-  bn_stats_partial_kernel<8, 1><<<t.chunks, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(y), nullptr, m, c,
-                                                               t.rows_per_chunk, t.cg, t.rpp, ws);
+  if (prec == 1)
+    bn_stats_partial_kernel<8, 1, IoF32><<<t.chunks, kThreads, 0, st>>>(static_cast<const float*>(y), nullptr, m, c,
+                                                                        t.rows_per_chunk, t.cg, t.rpp, ws);
+  else
+    bn_stats_partial_kernel<8, 1><<<t.chunks, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(y), nullptr, m, c,
+                                                                 t.rows_per_chunk, t.cg, t.rpp, ws);
   bn_stats_finalize_kernel<1><<<(c + kFinWarps - 1) / kFinWarps, kFinWarps * 32, 0, st>>>(ws, t.chunks, c, m,
                                                                                           mean_rstd, nullptr);
   return ok(cudaGetLastError());
 }
 
-int bn_stats2(const void* y0, const void* y1, int m, int c, float* ws, float* mr0, float* mr1, cudaStream_t st) {
+int bn_stats2(const void* y0, const void* y1, int m, int c, float* ws, float* mr0, float* mr1, cudaStream_t st,
+              int prec) {
   if (c % 8 != 0 || c / 8 > kThreads) return PBDK_EINVAL;
   const RowTiling t = tiling_for(m, c, 8);
-  bn_stats_partial_kernel<8, 2><<<t.chunks, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(y0),
-                                                               static_cast<const __nv_bfloat16*>(y1), m, c,
-                                                               t.rows_per_chunk, t.cg, t.rpp, ws);
+  if (prec == 1)
+    bn_stats_partial_kernel<8, 2, IoF32><<<t.chunks, kThreads, 0, st>>>(
+        static_cast<const float*>(y0), static_cast<const float*>(y1), m, c, t.rows_per_chunk, t.cg, t.rpp, ws);
+  else
+    bn_stats_partial_kernel<8, 2><<<t.chunks, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(y0),
+                                                                 static_cast<const __nv_bfloat16*>(y1), m, c,
+                                                                 t.rows_per_chunk, t.cg, t.rpp, ws);
   bn_stats_finalize_kernel<2><<<(2 * c + kFinWarps - 1) / kFinWarps, kFinWarps * 32, 0, st>>>(ws, t.chunks, c, m, mr0,
                                                                                               mr1);
   return ok(cudaGetLastError());
 }
 
 int bn_apply_relu(const void* y, const float* mean_rstd, const float* gamma, const float* beta, void* a, int m, int c,
-                  cudaStream_t st) {
+                  cudaStream_t st, int prec) {
   if (c % 8 != 0 || c / 8 > kThreads) return PBDK_EINVAL;
   const RowTiling t = tiling_for(m, c, 8);
+  if (prec == 1) {  // fp32 in, split fp32 out (the next convolution's operand)
+    bn_apply_relu_kernel<8, IoF32, IoSplit><<<apply_grid(m, t.rpp), kThreads, 0, st>>>(
+        static_cast<const float*>(y), mean_rstd, gamma, beta, static_cast<float*>(a), m, c, t.cg, t.rpp);
+    return ok(cudaGetLastError());
+  }
   bn_apply_relu_kernel<8><<<apply_grid(m, t.rpp), kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(y), mean_rstd,
                                                                      gamma, beta, static_cast<__nv_bfloat16*>(a), m, c,
                                                                      t.cg, t.rpp);
@@ -805,31 +876,49 @@ int bn_apply_relu(const void* y, const float* mean_rstd, const float* gamma, con
 
 int mse_bn_loss(const MseArgs& a, cudaStream_t st) {
   if (a.c % 8 != 0 || a.c / kLossApplyV > kThreads) return PBDK_EINVAL;
-  LossParams p{static_cast<const __nv_bfloat16*>(a.y2), static_cast<const __nv_bfloat16*>(a.ysc),
-               static_cast<const __nv_bfloat16*>(a.t), a.stats2, a.statssc, a.gamma2, a.beta2, a.gammasc, a.betasc,
+  LossParams p{a.y2, a.ysc, a.t, a.stats2, a.statssc, a.gamma2, a.beta2, a.gammasc, a.betasc,
                a.m, a.c, a.gscale};
   const RowTiling t = tiling_for(a.m, a.c, kLossPartialV, kLossChunks);
   float* partial = a.ws;
   float* loss_partial = a.ws + static_cast<size_t>(t.chunks) * 3 * a.c;
-  loss_partial_kernel<<<t.chunks, kThreads, 0, st>>>(p, t.rows_per_chunk, t.cg, t.rpp, partial, loss_partial);
+  if (a.prec == 1)  // y2 / ysc plain fp32, target split fp32
+    loss_partial_kernel<IoF32, IoSplit><<<t.chunks, kThreads, 0, st>>>(p, t.rows_per_chunk, t.cg, t.rpp, partial,
+                                                                       loss_partial);
+  else
+    loss_partial_kernel<<<t.chunks, kThreads, 0, st>>>(p, t.rows_per_chunk, t.cg, t.rpp, partial, loss_partial);
   loss_finalize_kernel<<<(a.c + kFinWarps - 1) / kFinWarps + 1, kFinWarps * 32, 0, st>>>(
       p, partial, loss_partial, t.chunks, a.norm, a.red, a.dgamma2, a.dbeta2, a.dgammasc, a.dbetasc, a.loss);
   const RowTiling ta = tiling_for(a.m, a.c, kLossApplyV);
-  loss_bwd_apply_kernel<<<apply_grid(a.m, ta.rpp), kThreads, 0, st>>>(p, a.red, ta.cg, ta.rpp,
-                                                                      static_cast<__nv_bfloat16*>(a.dy2),
-                                                                      static_cast<__nv_bfloat16*>(a.dysc));
+  if (a.prec == 1)  // dy2 / dysc split fp32 (dgrad / wgrad operands)
+    loss_bwd_apply_kernel<IoF32, IoSplit, IoSplit><<<apply_grid(a.m, ta.rpp), kThreads, 0, st>>>(
+        p, a.red, ta.cg, ta.rpp, static_cast<float*>(a.dy2), static_cast<float*>(a.dysc));
+  else
+    loss_bwd_apply_kernel<<<apply_grid(a.m, ta.rpp), kThreads, 0, st>>>(p, a.red, ta.cg, ta.rpp,
+                                                                        static_cast<__nv_bfloat16*>(a.dy2),
+                                                                        static_cast<__nv_bfloat16*>(a.dysc));
   return ok(cudaGetLastError());
 }
 
 int bn_bwd(const void* g, const void* y, const float* mean_rstd, const float* gamma, int m, int c, float* ws,
-           float* red, float* dgamma, float* dbeta, void* dy, cudaStream_t st) {
+           float* red, float* dgamma, float* dbeta, void* dy, cudaStream_t st, int prec) {
   if (c % 8 != 0 || c / 8 > kThreads) return PBDK_EINVAL;
   const RowTiling t = tiling_for(m, c, 8);
-  bn_bwd_partial_kernel<8><<<t.chunks, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(g),
-                                                          static_cast<const __nv_bfloat16*>(y), m, c,
-                                                          t.rows_per_chunk, t.cg, t.rpp, ws);
+  if (prec == 1)
+    bn_bwd_partial_kernel<8, IoF32><<<t.chunks, kThreads, 0, st>>>(static_cast<const float*>(g),
+                                                                   static_cast<const float*>(y), m, c,
+                                                                   t.rows_per_chunk, t.cg, t.rpp, ws);
+  else
+    bn_bwd_partial_kernel<8><<<t.chunks, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(g),
+                                                            static_cast<const __nv_bfloat16*>(y), m, c,
+                                                            t.rows_per_chunk, t.cg, t.rpp, ws);
   bn_bwd_finalize_kernel<<<(c + kFinWarps - 1) / kFinWarps, kFinWarps * 32, 0, st>>>(ws, t.chunks, c, m, mean_rstd,
                                                                                     gamma, red, dgamma, dbeta);
+  if (prec == 1) {  // dy split fp32 (the wgrad operand)
+    bn_bwd_apply_kernel<8, IoF32, IoSplit><<<apply_grid(m, t.rpp), kThreads, 0, st>>>(
+        static_cast<const float*>(g), static_cast<const float*>(y), mean_rstd, gamma, red, m, c, t.cg, t.rpp,
+        static_cast<float*>(dy));
+    return ok(cudaGetLastError());
+  }
   bn_bwd_apply_kernel<8><<<apply_grid(m, t.rpp), kThreads, 0, st>>>(
       static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(y), mean_rstd, gamma, red, m, c, t.cg,
       t.rpp, static_cast<__nv_bfloat16*>(dy));

@@ -30,6 +30,7 @@ struct MseArgs {
   double* loss;
   void* dy2;
   void* dysc;
+  int prec = 0;  // 0: bf16 rows; 1: y2/ysc fp32, t / dy2 / dysc split fp32 (the fp32 workload)
 };
 
 size_t reduce_workspace_floats(int m, int c, int nv);
@@ -44,22 +45,26 @@ struct GridScope {
   int saved_red, saved_apply;
 };
 // synthetic / host images of side x side pixels, stored [n][side][side][16] bf16
+// prec 1: split fp32 [n][side][side][2*32] (conv_tf32.hpp) instead
 int philox_image(void* x, int n, long long first, const long long* counter, int gb, uint32_t seed, cudaStream_t st,
-                 int side = 32);
-int pack_image(const float* src, void* x, int n, cudaStream_t st, int side = 32);
+                 int side = 32, int prec = 0);
+int pack_image(const float* src, void* x, int n, cudaStream_t st, int side = 32, int prec = 0);
 int pack_image_parity(const float* s0, const float* s1, const long long* counter, void* x, int n, cudaStream_t st,
-                      int side = 32);
+                      int side = 32, int prec = 0);
+// bf16_out: 0 fp32, 1 bf16, 2 split fp32 [k][r][s][2cs]
 int init_uniform(void* dst, int bf16_out, int k, int r, int s, int cs, int ct, uint32_t seed, uint32_t tensor,
                  float bound, cudaStream_t st);
 int fill(float* dst, size_t n, float v, cudaStream_t st);
-int bn_stats(const void* y, int m, int c, float* ws, float* mean_rstd, cudaStream_t st);
+// prec 1 (fp32 workload): fp32 inputs; outputs that feed convolutions are split fp32
+int bn_stats(const void* y, int m, int c, float* ws, float* mean_rstd, cudaStream_t st, int prec = 0);
 // statistics of two same-shape tensors in one pass (the student's y2 and shortcut y)
-int bn_stats2(const void* y0, const void* y1, int m, int c, float* ws, float* mr0, float* mr1, cudaStream_t st);
+int bn_stats2(const void* y0, const void* y1, int m, int c, float* ws, float* mr0, float* mr1, cudaStream_t st,
+              int prec = 0);
 int bn_apply_relu(const void* y, const float* mean_rstd, const float* gamma, const float* beta, void* a, int m, int c,
-                  cudaStream_t st);
+                  cudaStream_t st, int prec = 0);
 int mse_bn_loss(const MseArgs& a, cudaStream_t st);
 int bn_bwd(const void* g, const void* y, const float* mean_rstd, const float* gamma, int m, int c, float* ws,
-           float* red, float* dgamma, float* dbeta, void* dy, cudaStream_t st);
+           float* red, float* dgamma, float* dbeta, void* dy, cudaStream_t st, int prec = 0);
 int sgd_momentum(float* w, float* v, const float* g, void* shadow, size_t n, float lr, float mu, long long* counter,
                  cudaStream_t st);
 // the same update on g = g[0] + g[1] + ... (member order), the DP group's gradient slabs in peer memory

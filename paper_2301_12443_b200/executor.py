@@ -26,8 +26,10 @@ T_HW = (32, 32, 16, 8, 4)
 STUDENT_TENSORS = ("w1", "w2", "wsc", "g1", "b1", "g2", "b2", "gsc", "bsc")
 
 
-MODEL_RESNET_CIFAR, MODEL_MBV2_PROXYLESS, MODEL_EFFB0_PROXYLESS = 0, 1, 2
-MODELS = {"resnet": MODEL_RESNET_CIFAR, "mbv2": MODEL_MBV2_PROXYLESS, "effb0": MODEL_EFFB0_PROXYLESS}
+MODEL_RESNET_CIFAR, MODEL_MBV2_PROXYLESS, MODEL_EFFB0_PROXYLESS, MODEL_RESNET_CIFAR_FP32 = 0, 1, 2, 3
+MODELS = {"resnet": MODEL_RESNET_CIFAR, "mbv2": MODEL_MBV2_PROXYLESS, "effb0": MODEL_EFFB0_PROXYLESS,
+          "resnet_fp32": MODEL_RESNET_CIFAR_FP32}
+RESNETS = ("resnet", "resnet_fp32")
 
 
 class PbdxDesc(ctypes.Structure):
@@ -66,6 +68,8 @@ def _bind(L):
     L.pbdx_block_times.argtypes = [V, P(ctypes.c_float), P(ctypes.c_float)]
     L.pbdx_student_layout.argtypes = [I, P(ctypes.c_long)]
     L.pbdx_student_layout.restype = ctypes.c_long
+    L.pbdx_student_layout_fp32.argtypes = [I, P(ctypes.c_long)]
+    L.pbdx_student_layout_fp32.restype = ctypes.c_long
     L.pbdx_launches_per_step.argtypes = [V]
     L.pbdx_refresh_shadows.argtypes = [V, V]
     L.pbdx_relay_set_recv.argtypes = [V, I, P(V)]
@@ -111,17 +115,21 @@ class _CudaArray:
                                          "version": 3, "strides": None}
 
 
-def student_layout(block: int) -> Tuple[Dict[str, Tuple[int, int]], int]:
+def student_layout(block: int, model: str = "resnet") -> Tuple[Dict[str, Tuple[int, int]], int]:
     """{tensor: (offset, count)} of a block's flat (padded) student parameters."""
     offs = (ctypes.c_long * 9)()
-    total = lib().pbdx_student_layout(block, offs)
+    total = (lib().pbdx_student_layout_fp32 if model == "resnet_fp32" else lib().pbdx_student_layout)(block, offs)
     if total < 0:
         raise ValueError("bad block")
     bounds = list(offs) + [total]
     return {name: (bounds[i], bounds[i + 1] - bounds[i]) for i, name in enumerate(STUDENT_TENSORS)}, total
 
 
-def stored_channels(c: int) -> int:
+def stored_channels(c: int, model: str = "resnet") -> int:
+    """Stored channels of a ResNet activation (bf16: the image padded to 16; fp32: padded to 32 and
+    kept split, [hi | lo], so the buffer holds twice this many fp32 values per pixel)."""
+    if model == "resnet_fp32":
+        return 32 if c == 3 else c
     return 16 if c == 3 else c
 
 
@@ -154,7 +162,8 @@ def mb_block_params(block: int, model: str = "mbv2") -> int:
 
 class Partition:
     """One device's share of a Pipe-BD schedule.  model: "resnet" (CIFAR ResNet-18 -> slim residual
-    student, 4 blocks, 32x32) or "mbv2" (MobileNetV2 -> ProxylessNAS supernet, 6 blocks, image x image)."""
+    student, 4 blocks, 32x32, bf16), "resnet_fp32" (the same in fp32: 3xTF32 tensor-core convolutions,
+    configs[0]) or "mbv2" / "effb0" (MobileNetV2 / EfficientNet-B0 -> ProxylessNAS supernet, 6 blocks)."""
 
     def __init__(self, block_lo: int, block_hi: int, n_max: int, global_batch: int, seed_data: int = 1234,
                  seed_teacher: int = 1, seed_student: int = 2, lr: float = 0.1, momentum: float = 0.9,
@@ -162,7 +171,8 @@ class Partition:
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.block_lo, self.block_hi, self.n_max, self.global_batch = block_lo, block_hi, n_max, global_batch
         self.model = model
-        self.image = image if image is not None else (32 if model == "resnet" else 224)
+        self.image = image if image is not None else (32 if model in RESNETS else 224)
+        self.act_dtype = torch.float32 if model == "resnet_fp32" else torch.bfloat16
         self.n = n_max
         self.first = 0
         d = PbdxDesc(block_lo, block_hi, n_max, global_batch, seed_data, seed_teacher, seed_student, lr, momentum,
@@ -175,8 +185,8 @@ class Partition:
         self.layouts = {}
         off = 0
         for k in self.blocks:
-            if model == "resnet":
-                lay, total = student_layout(k)
+            if model in RESNETS:
+                lay, total = student_layout(k, model)
             else:
                 lay, total = {}, mb_block_params(k, model)
             self.layouts[k] = (off, lay, total)
@@ -213,17 +223,27 @@ class Partition:
 
     # -- views the driver moves with NCCL
     def input_act(self) -> torch.Tensor:
-        return self.tensor(BUF_INPUT, (self.n_max,) + self.act_hwc(self.block_lo), torch.bfloat16)
+        return self.tensor(BUF_INPUT, (self.n_max,) + self.act_hwc(self.block_lo), self.act_dtype)
 
     def teacher_out(self) -> torch.Tensor:
-        return self.tensor(BUF_TEACHER_OUT, (self.n_max,) + self.act_hwc(self.block_hi + 1), torch.bfloat16)
+        return self.tensor(BUF_TEACHER_OUT, (self.n_max,) + self.act_hwc(self.block_hi + 1), self.act_dtype)
 
     def teacher_act(self, k: int) -> torch.Tensor:
-        """Teacher output t_k of a block inside the partition (bf16 NHWC, n_max rows)."""
+        """Teacher output t_k of a block inside the partition (NHWC, n_max rows; bf16, or split fp32
+        [..., hi | lo] for resnet_fp32 — see value())."""
         p, n = ctypes.c_void_p(), ctypes.c_size_t()
         _check(lib().pbdx_teacher_act(self.handle, k, ctypes.byref(p), ctypes.byref(n)), "pbdx_teacher_act")
         shape = (self.n_max,) + self.act_hwc(k + 1)
+        if self.act_dtype == torch.float32:
+            return torch.as_tensor(_CudaArray(p.value, shape, "<f4"), device=self.device)
         return torch.as_tensor(_CudaArray(p.value, shape, "<i2"), device=self.device).view(torch.bfloat16)
+
+    def value(self, act: torch.Tensor) -> torch.Tensor:
+        """fp32 values of an activation view: bf16 widened, split fp32 [..., hi | lo] summed (exact)."""
+        if self.act_dtype == torch.float32:
+            c = act.shape[-1] // 2
+            return act[..., :c] + act[..., c:]
+        return act.float()
 
     def set_path(self, block: int, path):
         """Active candidate per student layer of `block` (mbv2 supernet)."""
@@ -254,19 +274,20 @@ class Partition:
 
     # -- geometry of block boundaries (boundary 0 = the stored 16-channel image)
     def act_hwc(self, boundary: int) -> Tuple[int, int, int]:
-        if self.model == "resnet":
-            return T_HW[boundary], T_HW[boundary], stored_channels(T_CH[boundary])
+        if self.model in RESNETS:
+            split = 2 if self.model == "resnet_fp32" else 1
+            return T_HW[boundary], T_HW[boundary], split * stored_channels(T_CH[boundary], self.model)
         hw = self.image // MB_DIV[boundary]
         return hw, hw, 16 if boundary == 0 else MB_CH[self.model][boundary]
 
     # -- K11 peer relay (include/pbdx.h): device pointers of this rank's relay endpoints
     def row_bytes_in(self) -> int:
         h, w, c = self.act_hwc(self.block_lo)
-        return h * w * c * 2
+        return h * w * c * self.act_dtype.itemsize
 
     def row_bytes_out(self) -> int:
         h, w, c = self.act_hwc(self.block_hi + 1)
-        return h * w * c * 2
+        return h * w * c * self.act_dtype.itemsize
 
     def mailbox_ptr(self) -> int:
         return self.buffer_ptr(BUF_MAILBOX)[0]
@@ -385,7 +406,7 @@ class Partition:
 
     def block_state_like(self, k: int) -> List[torch.Tensor]:
         """Receive buffers for any block's state (owned by this partition or not)."""
-        total = student_layout(k)[1] if self.model == "resnet" else mb_block_params(k, self.model)
+        total = student_layout(k, self.model)[1] if self.model in RESNETS else mb_block_params(k, self.model)
         return [torch.empty(total, dtype=torch.float32, device=self.device) for _ in range(2)]
 
     def set_block_state(self, k: int, weights: torch.Tensor, momentum: torch.Tensor):

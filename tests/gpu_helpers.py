@@ -5,14 +5,14 @@ import torch
 from oracle import bd
 
 
-def to_oracle_layout(k, flat_block: np.ndarray) -> np.ndarray:
-    """Product block params (padded input channels for block 0) -> oracle flat layout."""
-    from paper_2301_12443_b200.executor import student_layout
-    lay, _ = student_layout(k)
+def to_oracle_layout(k, flat_block: np.ndarray, model: str = "resnet") -> np.ndarray:
+    """Product block params (padded input channels for block 0: 16 bf16 / 32 fp32) -> oracle flat layout."""
+    from paper_2301_12443_b200.executor import student_layout, stored_channels
+    lay, _ = student_layout(k, model)
     g = bd.geom(k)
     cin, cout = g["cin"], g["cout"]
     mid = cout // 2
-    cs = 16 if cin == 3 else cin
+    cs = stored_channels(cin, model)
     parts = []
     for name in ("w1", "w2", "wsc", "g1", "b1", "g2", "b2", "gsc", "bsc"):
         o, n = lay[name]
@@ -28,7 +28,7 @@ def to_oracle_layout(k, flat_block: np.ndarray) -> np.ndarray:
 def partition_params(part, k) -> np.ndarray:
     base, _, total = part.layouts[k]
     flat = part.params()[base:base + total].cpu().numpy()
-    return to_oracle_layout(k, flat)
+    return to_oracle_layout(k, flat, part.model)
 
 
 def bf16_to_np(t: torch.Tensor) -> np.ndarray:
