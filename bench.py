@@ -30,6 +30,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "blockwise-distill samples/sec"
+TF32_PEAK_TFLOPS = 1100.0  # nominal dense tf32 (B200_PROFILING.md); not in MEASURED_PEAKS.json
 UNIT = "samples/s"
 PER_GPU_BATCH = 256
 
@@ -42,12 +43,13 @@ def parse():
                          "timed region, 300 for the MBConv workloads, 20 for --impl reference)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--batch", type=int, default=PER_GPU_BATCH, help="global batch per GPU")
+    ap.add_argument("--batch", type=int, default=None, help="global batch per GPU (default 256; cifar_fp32: 64)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", choices=["cifar", "mbv2", "effb0"], default="cifar",
-                    help="cifar: configs[1] (headline); mbv2: configs[2] MobileNetV2 -> ProxylessNAS at 224x224; "
-                         "effb0: configs[3] EfficientNet-B0 -> ProxylessNAS")
+    ap.add_argument("--workload", choices=["cifar", "cifar_fp32", "mbv2", "effb0"], default="cifar",
+                    help="cifar: configs[1] (headline, bf16); cifar_fp32: configs[0] (the same chain in fp32, batch "
+                         "64, 3xTF32 tensor-core convolutions); mbv2: configs[2] MobileNetV2 -> ProxylessNAS at "
+                         "224x224; effb0: configs[3] EfficientNet-B0 -> ProxylessNAS")
     ap.add_argument("--image", type=int, default=224, help="mbv2 image side")
     ap.add_argument("--relay", choices=["peer", "nccl"], default="peer",
                     help="N>1 teacher-activation relay: K11 peer stores over NVLink (default) or NCCL send/recv")
@@ -56,8 +58,10 @@ def parse():
     ap.add_argument("--pipeline", action="store_true",
                     help="use the multi-GPU runtime (profile -> best_schedule -> PipeBD) even at N=1")
     args = ap.parse_args()
+    if args.batch is None:
+        args.batch = 64 if args.workload == "cifar_fp32" else PER_GPU_BATCH
     if args.steps is None:
-        args.steps = 20 if args.impl == "reference" else (1000 if args.workload == "cifar" else 300)
+        args.steps = 20 if args.impl == "reference" else (1000 if args.workload.startswith("cifar") else 300)
     return args
 
 
@@ -128,12 +132,6 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
 
 
-def step_work(batch):
-    """Algorithmic FLOPs and bytes of one step (models.py accounting)."""
-    from paper_2301_12443_b200 import models
-    return models.step_flops(batch), models.step_bytes(batch)
-
-
 def ncu_traffic(kernel_key):
     """DRAM bytes per launch for the dominant kernel from the committed ncu capture (or None)."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -184,12 +182,52 @@ def time_dominant_kernel(torch, batch):
     return "conv_fprop_bn64_bkc64", flops, ms
 
 
+def time_dominant_kernel_fp32(torch, batch):
+    """configs[0]: the same dominant conv (teacher block-0 3x3, 64->64 @32x32, bias+ReLU) in fp32 as
+    3xTF32 on the tensor cores (split operands, split output), 50 launches from a CUDA graph.
+    Algorithmic FLOPs = 2*M*N*K; the tensor cores execute 3x that (three tf32 MMAs per product)."""
+    import ctypes
+    from paper_2301_12443_b200 import _lib
+    L = _lib.lib()
+    d = _lib.ConvDesc(batch, 32, 32, 64, 64, 3, 3, 1, 1, 32, 32)
+    x = torch.randn(batch, 32, 32, 128, device="cuda")
+    w = torch.randn(64, 3, 3, 128, device="cuda") * 0.05
+    bias = torch.zeros(64, device="cuda")
+    y = torch.empty(batch, 32, 32, 128, device="cuda")
+    reps = 50
+
+    def launch():
+        s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        rc = L.pbdk_conv3x_fprop(ctypes.byref(d), x.data_ptr(), w.data_ptr(), y.data_ptr(), 1, bias.data_ptr(), None,
+                                 2, s)
+        assert rc == 0
+
+    for _ in range(5):
+        launch()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(reps):
+            launch()
+    g.replay()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    g.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    flops = 2.0 * batch * 32 * 32 * 64 * 9 * 64
+    return "conv3x_fprop_bn64_ck32", flops, ms
+
+
 # ---------------------------------------------------------------- CPU legs
-def cpu_oracle_rate(samples_per_step=256, budget_s=15.0, max_steps=16):
+def cpu_oracle_rate(samples_per_step=256, budget_s=15.0, max_steps=16, bf16_mode=1):
     """The oracle (C restatement, OpenMP) on the host cores: samples/s over as many whole steps as fit
     in about `budget_s` seconds of CPU work (bounded sample of the same workload)."""
     from oracle import bd
-    tr = bd.Trainer(samples_per_step, bf16_mode=1)
+    tr = bd.Trainer(samples_per_step, bf16_mode=bf16_mode)
     tr.step(0)  # warm (allocation, page faults)
     t0 = time.perf_counter()
     steps = 0
@@ -212,7 +250,8 @@ def run_reference(args, rank, world):
         return
     from oracle import bd
     gb = args.batch * max(1, args.gpus)
-    tr = bd.Trainer(gb, bf16_mode=1)
+    fp32 = args.workload == "cifar_fp32"
+    tr = bd.Trainer(gb, bf16_mode=0 if fp32 else 1)
     warm = min(args.warmup, 1)
     for w in range(warm):
         tr.step(w)
@@ -228,9 +267,11 @@ def run_reference(args, rank, world):
     sample = f"{done} whole steps of the {gb}-sample global batch (all 4 blocks, fwd+bwd+SGD), {dt:.1f} s"
     line = {"metric": METRIC, "value": rate, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": done, "warmup": warm, "ms_per_step": dt / done * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16-emulated fp32",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "fp32" if fp32 else "bf16-emulated fp32",
             "data": "synthetic (Philox4x32-10, DESIGN.md §3)",
-            "config": {"workload": "cifar-resnet18-teacher/slim-student 4 blocks (configs[1])",
+            "config": {"workload": "cifar-resnet18-teacher/slim-student 4 blocks (%s)" % (
+                           "configs[0], fp32" if fp32 else "configs[1]"),
                        "global_batch": gb, "image": "32x32x3", "blocks": 4, "parallelism": "cpu",
                        "steps_requested": args.steps, "warmup_requested": args.warmup,
                        "same_config": True},
@@ -270,7 +311,9 @@ def run_ours(args, rank, world, local_rank):
         return run_ours_mbv2(args, dev, local_rank)
 
     b = args.batch
-    part = executor.Partition(0, 3, b, b, device=dev)
+    fp32 = args.workload == "cifar_fp32"
+    model = "resnet_fp32" if fp32 else "resnet"
+    part = executor.Partition(0, 3, b, b, device=dev, model=model)
     part.init_params()
     stream = torch.cuda.current_stream(dev)
     use_graph = not args.no_graph
@@ -298,7 +341,7 @@ def run_ours(args, rank, world, local_rank):
     # ---- e2e through the public API with host buffers: every step H2D of its images from pinned memory
     # (on a copy stream, into the staging slot the previous step is not reading — overlapped with the
     # previous step's compute), the step, and a D2H read of its losses (read on the host one step later)
-    e2e_part = executor.Partition(0, 3, b, b, device=dev)
+    e2e_part = executor.Partition(0, 3, b, b, device=dev, model=model)
     e2e_part.init_params()
     e2e_part.set_external_input(2)
     host = torch.empty(b, 32, 32, 3, dtype=torch.float32).pin_memory()
@@ -348,23 +391,33 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- roofline of the dominant kernel + step-level accounting
     peaks = measured_peaks()
-    key, kflops, kms = time_dominant_kernel(torch, b)
+    key, kflops, kms = (time_dominant_kernel_fp32 if fp32 else time_dominant_kernel)(torch, b)
     achieved = kflops / (kms * 1e-3) / 1e12
     traffic = ncu_traffic(key)
-    roof = {"bound": "tensor", "kernel": key, "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-            "frac": achieved / peaks["bf16_tflops"], "traffic": traffic, "launch_us": kms * 1e3,
-            "peak_source": peaks["source"] + " burst (kernel timed alone)"}
-    sflops, sbytes = step_work(b)
-    t_roof = max(sflops / (peaks["bf16_tflops_sustained"] * 1e12), sbytes / (peaks["hbm_gbs"] * 1e9))
+    if fp32:  # no measured tf32 figure: the nominal dense tf32 peak (B200_PROFILING.md), 3 MMAs per product
+        roof = {"bound": "tensor", "kernel": key, "achieved": 3 * achieved, "peak": TF32_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": 3 * achieved / TF32_PEAK_TFLOPS, "traffic": traffic,
+                "launch_us": kms * 1e3, "algorithmic_tflops": achieved,
+                "peak_source": "nominal dense tf32 (B200_PROFILING.md; MEASURED_PEAKS.json has no tf32 figure); "
+                               "achieved counts the 3 tf32 MMAs per product of the 3xTF32 split"}
+    else:
+        roof = {"bound": "tensor", "kernel": key, "achieved": achieved, "peak": peaks["bf16_tflops"],
+                "unit": "TFLOP/s", "frac": achieved / peaks["bf16_tflops"], "traffic": traffic,
+                "launch_us": kms * 1e3, "peak_source": peaks["source"] + " burst (kernel timed alone)"}
+    from paper_2301_12443_b200 import models as _m
+    sflops, sbytes = _m.step_flops(b), _m.step_bytes(b, act_bytes=4 if fp32 else 2)
+    peak_t = (TF32_PEAK_TFLOPS / 3.0) if fp32 else peaks["bf16_tflops_sustained"]
+    t_roof = max(sflops / (peak_t * 1e12), sbytes / (peaks["hbm_gbs"] * 1e9))
     step_roof = {"step_flops": sflops, "step_bytes": sbytes, "t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms,
                  "achieved_tflops": sflops / (ms * 1e-3) / 1e12,
-                 "note": "sum of algorithmic work / measured step; peak = sustained bf16, measured HBM"}
+                 "note": "algorithmic work (each tensor written + read once, weights once) / measured step; peak = " +
+                         ("nominal tf32 / 3 (3xTF32)" if fp32 else "sustained bf16") + ", measured HBM"}
 
     # ---- the paper's DP baseline measured on the same GPU:
     # blocks trained one after another, every step recomputing the teacher prefix T_0..T_k
     dp_ms = []
     for k in range(4):
-        dp = executor.Partition(0, k, b, b, device=dev)
+        dp = executor.Partition(0, k, b, b, device=dev, model=model)
         dp.init_params()
         dp.set_train_mask(1 << k)
         dp.capture()
@@ -387,15 +440,17 @@ def run_ours(args, rank, world, local_rank):
 
     cpu = None
     if not args.no_cpu_baseline:
-        rate, cores, dt, nsteps = cpu_oracle_rate()
+        rate, cores, dt, nsteps = cpu_oracle_rate(b, bf16_mode=0 if fp32 else 1)
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"{nsteps} whole steps of the same 256-sample batch (oracle/bd_oracle.c, {dt:.1f} s)"}
+               "sample": f"{nsteps} whole steps of the same {b}-sample batch (oracle/bd_oracle.c, {dt:.1f} s)"}
 
-    working_set = models.step_working_set_bytes(b)
+    working_set = models.step_working_set_bytes(b) * (3 if fp32 else 1)  # fp32: ~2x bytes, split operands 2x again
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "fp32" if fp32 else "bf16",
             "data": "synthetic (Philox4x32-10 inputs generated on device each step; random-init weights)",
-            "config": {"workload": "cifar-resnet18-teacher/slim-student 4 blocks, IR point on 1 GPU (configs[1])",
+            "config": {"workload": "cifar-resnet18-teacher/slim-student 4 blocks, IR point on 1 GPU (%s)" % (
+                           "configs[0]: fp32, 3xTF32 tensor-core convolutions" if fp32 else "configs[1]"),
                        "global_batch": b, "image": "32x32x3", "blocks": 4, "parallelism": "ir1 (blocks 0-3 on 1 GPU)",
                        "cuda_graph": use_graph,
                        "l2": f"no flush: per-step working set {working_set / 2**30:.2f} GiB > 126 MB L2"},

@@ -78,9 +78,35 @@ def _act(n, hw, c):
     return n * hw * hw * c * BF16
 
 
-def step_bytes(n: int, blocks=range(BLOCKS)) -> float:
-    """Minimal HBM traffic of the implemented kernel decomposition: every kernel reads its
-    operands once and writes its results once (weights once per step)."""
+def step_bytes(n: int, blocks=range(BLOCKS), act_bytes: int = BF16) -> float:
+    """ALGORITHMIC HBM bytes of one step (the roofline denominator): every logical tensor
+    of the step written once and read once — the 3-channel input image, each teacher conv output, the
+    student's y1, a1, y2, ysc (forward) and dy2, dysc, g1, dy1 (backward) — every weight read once, the
+    student gradients written once, and the momentum SGD's minimal traffic (w, v read+write, g read,
+    bf16 shadow write).  Independent of how the kernels are split: re-reads, recomputation and padded
+    channels of the implementation are NOT counted (step_bytes_decomposition counts those)."""
+    def act(hw, c):
+        return n * hw * hw * c * act_bytes
+
+    total = 0.0
+    for k in blocks:
+        if k == 0:
+            total += 2 * act(32, 3)  # the image: written (load_data), read
+        for (cin, cout, r, st, hin, hout), _ in teacher_convs(k):
+            total += 2 * act(hout, cout) + cout * r * r * cin * act_bytes  # output w+r, weights r
+        g = student_geom(k)
+        m, o = act(g["hout"], g["mid"]), act(g["hout"], g["cout"])
+        total += 2 * (2 * m + 2 * o)  # forward: y1, a1, y2, ysc written + read
+        total += 2 * (2 * o + 2 * m)  # backward: dy2, dysc, g1, dy1 written + read
+        p = student_param_count(k)
+        total += p * act_bytes + p * F32 + p * (4 * F32 + F32 + BF16)  # weights r, grads w, SGD
+    return total
+
+
+def step_bytes_decomposition(n: int, blocks=range(BLOCKS)) -> float:
+    """HBM traffic of the implemented (round-1) kernel decomposition: every kernel reads its operands
+    once and writes its results once (weights once per step) — counts the BN statistics passes, the
+    loss reduce + recompute and the 16-channel padded image, so it is larger than step_bytes()."""
     total = 0.0
     for k in blocks:
         if k == 0:
