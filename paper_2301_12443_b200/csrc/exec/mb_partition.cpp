@@ -22,6 +22,7 @@
 #include <cstring>
 #include <vector>
 
+#include "knobs.hpp"
 #include "bd_kernels.hpp"
 #include "conv.hpp"
 #include "mb_kernels.hpp"
@@ -372,8 +373,8 @@ class MbPartition final : public PartitionBase {
   }
 
   void student_body(cudaStream_t caller, bool fork) override {
-    static const int red = [] { const char* e = std::getenv("PBDK_MB_RED"); return e ? std::atoi(e) : 0; }();
-    static const int app = [] { const char* e = std::getenv("PBDK_MB_APPLY"); return e ? std::atoi(e) : 0; }();
+    static const int red = [] { const char* e = pbd::knob_env("PBDK_MB_RED"); return e ? std::atoi(e) : 0; }();
+    static const int app = [] { const char* e = pbd::knob_env("PBDK_MB_APPLY"); return e ? std::atoi(e) : 0; }();
     const pbdk::GridScope grids(red, app);
     if (fork) cuda(cudaEventRecord(fork_, caller), "event");
     for (size_t i = 0; i < sblocks_.size(); ++i) {
@@ -827,7 +828,7 @@ class MbPartition final : public PartitionBase {
           check(pbdk::fprop_plan(pw_desc(act_rows_hw(op.hin), op.cin, op.cout), op.in, op.w, op.out, op.bias, op.aux,
                                  op.epi, &op.plan),
                 "teacher 1x1 plan");
-    const char* sc = std::getenv("PBDK_MB_SCONV");  // student conv grid cap (experiments; 0 = all SMs)
+    const char* sc = pbd::knob_env("PBDK_MB_SCONV");  // student conv grid cap (experiments; 0 = all SMs)
     const pbdk::ConvGridScope scope(sc != nullptr ? std::atoi(sc) : 0);
     for (SBlock& sb : sblocks_)
       for (SLayer& L : sb.layers) {

@@ -22,6 +22,7 @@
 #include <string>
 #include <vector>
 
+#include "knobs.hpp"
 #include "bd_kernels.hpp"
 #include "conv.hpp"
 #include "pbdk.h"
@@ -340,7 +341,7 @@ class ResNetPartition final : public PartitionBase {
 
   static bool student_fork() {
     static const bool on = [] {
-      const char* e = std::getenv("PBD_STUDENT_FORK");
+      const char* e = pbd::knob_env("PBD_STUDENT_FORK");
       return e == nullptr || e[0] != '0';
     }();
     return on;
@@ -512,7 +513,7 @@ class ResNetPartition final : public PartitionBase {
       // student chains in the middle, the side streams (wgrads off the critical chain) lowest.
       // Measured 0.907 -> 0.895 ms vs two levels (PBD_PRIO_MODE=0: side streams share their block's).
       static const int prio_mode = [] {
-        const char* e = std::getenv("PBD_PRIO_MODE");
+        const char* e = pbd::knob_env("PBD_PRIO_MODE");
         return e != nullptr ? std::atoi(e) : 2;
       }();
       const int hi = priority_high(), lo = priority_low();
@@ -544,12 +545,12 @@ class ResNetPartition final : public PartitionBase {
   }
 
   static int env_ctas(const char* name) {
-    const char* e = std::getenv(name);
+    const char* e = pbd::knob_env(name);
     return e != nullptr ? std::atoi(e) : 0;
   }
   // PBDK_TCONV_CTAS_LIST / PBDK_SCONV_CTAS_LIST = "a,b,c,d": per-block grid caps (experiments)
   static int env_list(const char* name, size_t i, int dflt) {
-    const char* e = std::getenv(name);
+    const char* e = pbd::knob_env(name);
     if (e == nullptr) return dflt;
     std::string v(e);
     size_t pos = 0;
@@ -577,7 +578,7 @@ class ResNetPartition final : public PartitionBase {
     // 64 SMs so the streams share the GPU spatially instead of queueing behind each other's full-GPU
     // persistent grids (measured, 4 blocks at b=256: 0.934 -> 0.907 ms per step; capping the teacher
     // convs, which run mostly alone, costs time).  PBDK_SCONV_CTAS overrides (0 = all SMs).
-    const int sconv = std::getenv("PBDK_SCONV_CTAS") != nullptr ? env_ctas("PBDK_SCONV_CTAS")
+    const int sconv = pbd::knob_env("PBDK_SCONV_CTAS") != nullptr ? env_ctas("PBDK_SCONV_CTAS")
                                                                 : (sblocks_.size() >= 3 ? 64 : 0);
     for (size_t i = 0; i < sblocks_.size(); ++i) {
       SBlock& s = sblocks_[i];

@@ -14,6 +14,7 @@
 #include <string>
 #include <vector>
 
+#include "knobs.hpp"
 #include "pbdk.h"
 #include "pbdx.h"
 #include "relay.hpp"
@@ -327,15 +328,15 @@ class PartitionBase {
   static int priority_high() {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    return std::getenv("PBD_NO_PRIORITY") != nullptr ? 0 : hi;
+    return pbd::knob_env("PBD_NO_PRIORITY") != nullptr ? 0 : hi;
   }
   static int priority_low() {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    return std::getenv("PBD_NO_PRIORITY") != nullptr ? 0 : lo;
+    return pbd::knob_env("PBD_NO_PRIORITY") != nullptr ? 0 : lo;
   }
   static unsigned long long graph_flags() {
-    return std::getenv("PBD_NO_PRIORITY") != nullptr
+    return pbd::knob_env("PBD_NO_PRIORITY") != nullptr
                ? 0ull
                : static_cast<unsigned long long>(cudaGraphInstantiateFlagUseNodePriority);
   }

@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include "knobs.hpp"
 #include "bd_kernels.hpp"
 #include "pbdk.h"
 #include "sm100.cuh"
@@ -297,7 +298,7 @@ struct RowTiling {
 };
 
 int env_int(const char* name, int dflt) {
-  const char* e = std::getenv(name);
+  const char* e = pbd::knob_env(name);
   return e != nullptr ? std::atoi(e) : dflt;
 }
 // Grid sizes of the reduction (partial) and elementwise (apply) passes (GridScope, bd_kernels.hpp).

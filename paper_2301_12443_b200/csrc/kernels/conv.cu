@@ -11,12 +11,17 @@
 //
 // Warp roles (192 threads): warp 0 TMA producer, warp 1 MMA issuer (one thread),
 // warps 2-5 epilogue (TMEM lane quarter = warp % 4); warp 2 owns TMEM alloc.
+#include "knobs.hpp"
 #include "conv.hpp"
 #include "sm100.cuh"
 #include "tmap.hpp"
 
 #include <algorithm>
 #include <cstdlib>
+
+// timing-experiment modes of FpropArgs::debug: compiled out of the product build (knobs.hpp)
+#define DBG_IS(args, v) (pbd::kExperiments && (args).debug == (v))
+#define DBG_GE(args, v) (pbd::kExperiments && (args).debug >= (v))
 
 namespace pbdk {
 
@@ -103,7 +108,7 @@ __device__ __forceinline__ void fprop_epilogue(const FpropArgs& a, uint32_t trow
   rowmap(row, valid, m);
   const EpiFlags f = epi_flags(a.epi);
   const bool has_bias = f.bias;
-  if (a.debug == 3 || a.debug == 9 || a.debug == 7) {
+  if (DBG_IS(a, 3) || DBG_IS(a, 9) || DBG_IS(a, 7)) {
     wait();
     return;
   }
@@ -112,7 +117,7 @@ __device__ __forceinline__ void fprop_epilogue(const FpropArgs& a, uint32_t trow
   // N = 64 tile was latency-bound on them and fell behind the MMAs: 64->64 conv + residual
   // 50 -> see DESIGN.md §6).
   constexpr int GC = BN < 64 ? BN : 64;
-  const bool live = valid && a.debug != 1;
+  const bool live = valid && !DBG_IS(a, 1);
 #pragma unroll 1
   for (int g0 = 0; g0 < BN; g0 += GC) {
     uint4 ra[GC / 8];
@@ -292,7 +297,7 @@ __global__ void __launch_bounds__(epi_threads(EPW), 1)
           const uint64_t b0 = umma_smem_desc(sb, 16, 8 * C::SW, C::LAYOUT);
 #pragma unroll
           for (int kk = 0; kk < BKC / 16; ++kk) {
-            if (a.debug != 2) umma_bf16(dacc, a0 + 2 * kk, b0 + 2 * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
+            if (!DBG_IS(a, 2)) umma_bf16(dacc, a0 + 2 * kk, b0 + 2 * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
           }
           umma_commit(&empty[st]);
         }
@@ -408,6 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(tfull, 1);
     fence_barrier_init();
   }
+  __syncwarp();  // warp 0 reconverges after the lane-0 barrier init (aligned barrier below)
   if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
@@ -509,7 +515,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
-  cluster_sync();  // every CTA's partial stays alive until all reads are done
+  __syncwarp();    // the lane-strided column loop may leave a warp diverged: reconverge before the
+  cluster_sync();  // .aligned cluster barrier; every CTA's partial stays alive until all reads are done
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, C::TMEM_COLS);
@@ -785,12 +792,12 @@ __global__ void __launch_bounds__(epi_threads(EPW), 1)
           tma_load_2d(bres + (cc * 9 + tap) * C::B_BYTES, &tmw, bfull, tap * cin_stored + cc * BKC, 0);
       int it = 0, st = 0;
       uint32_t ph = 0;
-      for (int t = blockIdx.x; t < (a.debug == 8 ? 0 : total); t += gridDim.x) {
+      for (int t = blockIdx.x; t < (DBG_IS(a, 8) ? 0 : total); t += gridDim.x) {
         const int img = t / a.tiles_img;
         const int p0 = (t - img * a.tiles_img) * 128;
         for (int cc = 0; cc < chunks; ++cc, ++it) {
           if (it >= C::STAGES) mbar_wait(&empty[st], ph ^ 1);
-          if (a.debug >= 6) {  // timing only: no activation loads (MMA + epilogue pipeline alone)
+          if (DBG_GE(a, 6)) {  // timing only: no activation loads (MMA + epilogue pipeline alone)
             mbar_arrive(&full[st]);
           } else {
             mbar_arrive_expect_tx(&full[st], C::BOX_BYTES);
@@ -815,12 +822,12 @@ __global__ void __launch_bounds__(epi_threads(EPW), 1)
       uint32_t ph = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
         const int acc = lt & 1;
-        if (lt >= 2 && a.debug != 8) mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
+        if (lt >= 2 && !DBG_IS(a, 8)) mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
         tc_fence_after();
         const uint32_t dacc = tmem + static_cast<uint32_t>(acc * C::ACC_COLS);
         const int j0 = (t % a.tiles_img) * 128 % WP;
         for (int cc = 0; cc < chunks; ++cc) {
-          if (a.debug != 8) mbar_wait(&full[st], ph);
+          if (!DBG_IS(a, 8)) mbar_wait(&full[st], ph);
           tc_fence_after();
           const uint64_t a0 = adesc0 + static_cast<uint32_t>((st * C::STAGE + j0 * C::SW) >> 4);
           const uint64_t b0 = bdesc0 + static_cast<uint32_t>((cc * 9 * C::B_BYTES) >> 4);
@@ -830,7 +837,7 @@ __global__ void __launch_bounds__(epi_threads(EPW), 1)
             for (int kk = 0; kk < BKC / 16; ++kk) {
               const uint32_t aoff = static_cast<uint32_t>((((tap / 3) * WP + tap % 3) * C::SW + kk * 32) >> 4);
               const uint32_t boff = static_cast<uint32_t>((tap * C::B_BYTES + kk * 32) >> 4);
-              if (a.debug != 2) umma_bf16(dacc, a0 + aoff, b0 + boff, idesc, (cc | tap | kk) != 0 ? 1u : 0u);
+              if (!DBG_IS(a, 2)) umma_bf16(dacc, a0 + aoff, b0 + boff, idesc, (cc | tap | kk) != 0 ? 1u : 0u);
             }
           }
           umma_commit(&empty[st]);
@@ -847,7 +854,7 @@ __global__ void __launch_bounds__(epi_threads(EPW), 1)
     constexpr int CW = BN / EPW;
     const int c_lo = ((warp - 2) >> 2) * CW;
     int lt = 0;
-    for (int t = blockIdx.x; t < (a.debug == 8 ? 0 : total); t += gridDim.x, ++lt) {
+    for (int t = blockIdx.x; t < (DBG_IS(a, 8) ? 0 : total); t += gridDim.x, ++lt) {
       const int acc = lt & 1;
       const int img = t / a.tiles_img;
       const HaloRows rows{&a, img, (t - img * a.tiles_img) * 128, WP};
@@ -1515,7 +1522,7 @@ FpropLauncher pick_halo(int bn, int epw = 1) {
 
 bool halo_enabled() {
   static const bool on = [] {
-    const char* e = std::getenv("PBDK_NO_HALO");
+    const char* e = pbd::knob_env("PBDK_NO_HALO");
     return e == nullptr || e[0] == '0';
   }();
   return on;
@@ -1577,7 +1584,7 @@ int wgrad_mt_taps(const pbdk_conv_desc& d) { return d.c >= 64 ? 3 : 9; }
 
 WgradLauncher pick_wgrad_mt(const pbdk_conv_desc& d) {
   static const int mode = [] {
-    const char* e = std::getenv("PBDK_WGRAD_MT");  // 0 off, 1 narrow inputs only, 2 (default) + 64-ch tiles
+    const char* e = pbd::knob_env("PBDK_WGRAD_MT");  // 0 off, 1 narrow inputs only, 2 (default) + 64-ch tiles
     return e != nullptr ? std::atoi(e) : 2;
   }();
   if (mode == 0 || d.r * d.s != 9) return nullptr;
@@ -1623,13 +1630,13 @@ FpropChoice choose_fprop(const pbdk_conv_desc& d, const ConvGeom& g, int bkc) {
   const int num_kb = d.r * d.s * (d.c / bkc);
   const int sms = num_sms();
   static const int forced = [] {
-    const char* e = std::getenv("PBDK_FPROP_SPLITS");  // 1: never split (A/B runs)
+    const char* e = pbd::knob_env("PBDK_FPROP_SPLITS");  // 1: never split (A/B runs)
     return e != nullptr ? std::atoi(e) : 0;
   }();
   // 2-CTA tiles measured no faster than one-CTA tiles on the step's shapes (the K loop is
   // not load-bound once enough bytes are in flight); opt-in for experiments.
   static const int no_pair = [] {
-    const char* e = std::getenv("PBDK_PAIR");
+    const char* e = pbd::knob_env("PBDK_PAIR");
     return e == nullptr || e[0] == '0';
   }();
   FpropChoice best{0, 1, false};
@@ -1716,7 +1723,7 @@ int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, c
   FpropChoice ch = choose_fprop(d, g, bkc);
   {
     static const int m2_mode = [] {
-      const char* e = std::getenv("PBDK_M2");  // 0 off, 1 auto (default), 2 force where legal
+      const char* e = pbd::knob_env("PBDK_M2");  // 0 off, 1 auto (default), 2 force where legal
       return e != nullptr ? std::atoi(e) : 1;
     }();
     const bool legal = ch.splits == 1 && !ch.pair && (ch.bn == 64 || ch.bn == 128) && bkc == 64 &&
@@ -1736,7 +1743,7 @@ int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, c
   // short-K convs (3x3 over <= 32 channels, 1x1 over <= 64): the epilogue bounds the tile, so two
   // epilogue warps per TMEM lane quarter (PBDK_EPW=1/2 forces)
   static const int epw_env = [] {
-    const char* e = std::getenv("PBDK_EPW");
+    const char* e = pbd::knob_env("PBDK_EPW");
     return e != nullptr ? std::atoi(e) : 0;
   }();
   const bool short_k = (d.r * d.s == 9 && d.c <= 32) || (d.r * d.s == 1 && d.c <= 64);
@@ -1801,9 +1808,9 @@ int fprop_plan(const pbdk_conv_desc& d, const void* x, const void* w, void* y, c
   a.c_chunks = d.c / bkc;
   a.epi = epi;
   {
-    const char* dbg = std::getenv("PBDK_CONV_DEBUG");
+    const char* dbg = pbd::knob_env("PBDK_CONV_DEBUG");
     a.debug = dbg != nullptr ? std::atoi(dbg) : 0;
-    a.dbg_buf = (a.debug >= 4 && aux != nullptr) ? static_cast<long long*>(const_cast<void*>(aux)) : nullptr;
+    a.dbg_buf = (DBG_GE(a, 4) && aux != nullptr) ? static_cast<long long*>(const_cast<void*>(aux)) : nullptr;
   }
   a.y = static_cast<__nv_bfloat16*>(y);
   a.bias = bias;
@@ -1853,7 +1860,7 @@ bool use_wgrad_mt(const ConvGeom& g) {
 // PBDK_WGRAD_WAVE overrides.
 int wgrad_wave() {
   static const int w = [] {
-    const char* e = std::getenv("PBDK_WGRAD_WAVE");
+    const char* e = pbd::knob_env("PBDK_WGRAD_WAVE");
     return e != nullptr ? std::max(1, std::atoi(e)) : 64;
   }();
   return w;
@@ -1935,7 +1942,7 @@ int wgrad_plan(const pbdk_conv_desc& d, const void* x, const void* dy, float* dw
 
 int split_reduce_cap() {
   static const int cap = [] {
-    const char* e = std::getenv("PBDK_SPLITRED_CTAS");
+    const char* e = pbd::knob_env("PBDK_SPLITRED_CTAS");
     return e != nullptr ? std::max(1, std::atoi(e)) : 148 * 8;
   }();
   return cap;

@@ -18,6 +18,7 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include "knobs.hpp"
 #include "mb_kernels.hpp"
 #include "pbdk.h"
 
@@ -73,7 +74,7 @@ __device__ __forceinline__ float act_fn(int act, float v) {
 int grid_for(long long work) {
   const long long b = (work + kT - 1) / kT;
   static const long long cap = [] {
-    const char* e = std::getenv("PBDK_MB_CTAS");
+    const char* e = pbd::knob_env("PBDK_MB_CTAS");
     return e != nullptr ? std::max(1LL, std::atoll(e)) : 148LL * 16;
   }();
   return static_cast<int>(std::max<long long>(1, std::min<long long>(b, cap)));
