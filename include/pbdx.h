@@ -58,9 +58,10 @@ typedef struct pbdx_desc {
 #define PBDX_BUF_LOSSES 5       /* double[num_blocks]: per-block partial loss of the last step */
 #define PBDX_BUF_STEP 6         /* int64 step counter (advanced by apply_update) */
 #define PBDX_BUF_TEACHER_PARAMS 7 /* bf16 teacher conv weights of block_lo..hi (flat, program order) */
-#define PBDX_BUF_MAILBOX 8      /* 64 uint64 flags written by peers (own allocation, IPC-exportable):
+#define PBDX_BUF_MAILBOX 8      /* 80 uint64 flags written by peers (own allocation, IPC-exportable):
                                    [0,16) relay ready (per sender slot), [16,32) relay consumed (per
-                                   receiver slot), [32,48) DP ready, [48,64) DP consumed (per member) */
+                                   receiver slot), [32,48) DP ready, [48,64) DP consumed, [64,80) DP
+                                   slice updated (per member) */
 
 int pbdx_create(const pbdx_desc* d, void** handle);
 void pbdx_destroy(void* handle);
@@ -172,6 +173,18 @@ int pbdx_relay_set_send(void* handle, int nmsgs, const pbdx_relay_msg* msgs);
  * bit-identical weights on every member, no host round trip, and the whole step stays one CUDA graph.
  * peer_grads[j] / peer_mailbox[j]: member j's buffers as seen from this process (j == me ignored). */
 int pbdx_dp_set_group(void* handle, int size, int me, void* const* peer_grads, void* const* peer_mailbox);
+/* The exchange itself is a reduce-scatter + all-gather over peer memory: member `me` sums and updates
+ * slice `me` of every parameter region (its peers' gradient slices, member order), publishes a
+ * device-side "updated" flag (mailbox slots [64, 80)), then copies every other member's updated slice
+ * of the master weights — 2(G-1)/G * 4P bytes of NVLink reads per member, the ring-allreduce volume of
+ * cost_model.cpp:79-86.  peer_params[j]: member j's PBDX_BUF_PARAMS (the allocation also holds its
+ * momentum).  Required when size > 1. */
+int pbdx_dp_set_params(void* handle, int size, void* const* peer_params);
+/* Momentum is sharded by the exchange (only a slice's owner keeps it current): pull every other
+ * member's slices of weights and momentum before the host reads block state (checkpoint, migration). */
+int pbdx_dp_sync_state(void* handle, void* stream);
+/* Host-only: peer bytes read per member and step by the exchange for an n-float region (n % 4 == 0). */
+long long pbdx_dp_peer_bytes(long long n, int size, int me);
 
 /* CUDA IPC of an executor buffer (the allocation base: PBDX_BUF_INPUT / PBDX_BUF_MAILBOX) for ranks in
  * other processes; handle = 64 bytes (cudaIpcMemHandle_t). */

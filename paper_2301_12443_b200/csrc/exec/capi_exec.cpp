@@ -82,6 +82,26 @@ int pbdx_dp_set_group(void* h, int size, int me, void* const* peer_grads, void* 
   if (size > 1 && (peer_grads == nullptr || peer_mailbox == nullptr)) return PBDK_EINVAL;
   return guard([&] { P(h)->dp_set_group(size, me, peer_grads, peer_mailbox); });
 }
+int pbdx_dp_set_params(void* h, int size, void* const* peer_params) {
+  if (size > 1 && peer_params == nullptr) return PBDK_EINVAL;
+  return guard([&] { P(h)->dp_set_params(size, peer_params); });
+}
+int pbdx_dp_sync_state(void* h, void* st) { return guard([&] { P(h)->dp_sync_state(S(st)); }); }
+long long pbdx_dp_peer_bytes(long long n, int size, int me) {
+  if (n < 0 || n % 4 != 0 || size < 1 || me < 0 || me >= size) return -1;
+  long long bytes = 0;
+  for (int j = 0; j < size; ++j) {  // reduce-scatter: my slice from each peer; all-gather: each peer's slice
+    size_t lo = 0, hi = 0;
+    pbdk::dp_slice(static_cast<size_t>(n), size, j, &lo, &hi);
+    const long long mine_lo = static_cast<long long>(lo), mine_hi = static_cast<long long>(hi);
+    if (j == me) {
+      bytes += (size - 1) * (mine_hi - mine_lo) * 4;
+    } else {
+      bytes += (mine_hi - mine_lo) * 4;
+    }
+  }
+  return bytes;
+}
 int pbdx_set_train_mask(void* h, unsigned int mask) { return guard([&] { P(h)->set_train_mask(mask); }); }
 int pbdx_trace_mark(void* h, void* st) { return guard([&] { P(h)->trace_mark(S(st)); }); }
 int pbdx_block_trace(void* h, float* t0, float* t1, float* s0, float* s1) {

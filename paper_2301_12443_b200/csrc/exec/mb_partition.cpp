@@ -390,26 +390,43 @@ class MbPartition final : public PartitionBase {
   }
 
   void update_body(cudaStream_t st) override {
+    if (dp_active()) {  // reduce-scatter + all-gather of the active candidates (PartitionBase::dp_update)
+      std::vector<DpRegion> regions;
+      for (size_t i = 0; i < sblocks_.size(); ++i) {
+        if (!trains(static_cast<int>(i))) continue;
+        for (SLayer& L : sblocks_[i].layers) {
+          const SCand& C = L.cands[static_cast<size_t>(L.active)];
+          regions.push_back({C.off, C.L.total});
+        }
+      }
+      dp_update(regions, params_, mom_, grads_, shadow_, step_, st);
+      for (size_t i = 0; i < sblocks_.size(); ++i) {
+        if (!trains(static_cast<int>(i))) continue;
+        for (SLayer& L : sblocks_[i].layers) refresh_derived(L, L.cands[static_cast<size_t>(L.active)], st);
+      }
+      return;
+    }
     long long* counter = step_;
     for (size_t i = 0; i < sblocks_.size(); ++i) {
       if (!trains(static_cast<int>(i))) continue;
       SBlock& sb = sblocks_[i];
       for (SLayer& L : sb.layers) {
         SCand& C = L.cands[static_cast<size_t>(L.active)];
-        if (dp_active()) {
-          const auto src = dp_sources(grads_, C.off);
-          check(pbdk::sgd_momentum_sum(params_ + C.off, mom_ + C.off, src.data(), static_cast<int>(src.size()),
-                                       shadow_ + C.off, C.L.total, d_.lr, d_.momentum, counter, st),
-                "sgd (dp)");
-        } else {
-          check(pbdk::sgd_momentum(params_ + C.off, mom_ + C.off, grads_ + C.off, shadow_ + C.off, C.L.total, d_.lr,
-                                   d_.momentum, counter, st),
-                "sgd");
-        }
+        check(pbdk::sgd_momentum(params_ + C.off, mom_ + C.off, grads_ + C.off, shadow_ + C.off, C.L.total, d_.lr,
+                                 d_.momentum, counter, st),
+              "sgd");
         counter = nullptr;  // advance the step counter once
         refresh_derived(L, C, st);
       }
     }
+  }
+
+  std::vector<DpRegion> dp_all_regions() const override {  // every candidate: each keeps its own slicing
+    std::vector<DpRegion> r;
+    for (const SBlock& sb : sblocks_)
+      for (const SLayer& L : sb.layers)
+        for (const SCand& C : L.cands) r.push_back({C.off, C.L.total});
+    return r;
   }
 
   void refresh_shadows(cudaStream_t st) override {
@@ -809,8 +826,10 @@ class MbPartition final : public PartitionBase {
       cuda(cudaEventCreateWithFlags(&sb.done, cudaEventDisableTiming), "event");
       sblocks_.push_back(std::move(sb));
     }
-    params_ = arena_.get<float>(total_ * sizeof(float));
-    mom_ = arena_.get<float>(total_ * sizeof(float));
+    // master weights and momentum in ONE allocation (momentum at +total_): a DP peer reaches both
+    // through the one IPC mapping of PBDX_BUF_PARAMS (PartitionBase::dp_sync_state)
+    params_ = arena_.get<float>(2 * total_ * sizeof(float));
+    mom_ = params_ + total_;
     grads_ = arena_.get<float>(total_ * sizeof(float));
     shadow_ = arena_.get<bf16>(total_ * sizeof(bf16));
     losses_ = arena_.get<double>(kBlocks * sizeof(double));

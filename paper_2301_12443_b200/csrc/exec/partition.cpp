@@ -278,11 +278,8 @@ class ResNetPartition final : public PartitionBase {
   }
 
   void update_body(cudaStream_t st) override {
-    if (dp_active()) {  // share_gradient + update fused: sum the group's gradient slabs from peer memory
-      const auto src = dp_sources(grads_, 0);
-      check(pbdk::sgd_momentum_sum(params_, mom_, src.data(), static_cast<int>(src.size()), shadow_, total_, d_.lr,
-                                   d_.momentum, step_, st),
-            "sgd (dp)");
+    if (dp_active()) {  // share_gradient + update: reduce-scatter + all-gather over peer memory
+      dp_update({{0, total_}}, params_, mom_, grads_, shadow_, step_, st);
       refresh_flips(st);
       return;
     }
@@ -302,6 +299,8 @@ class ResNetPartition final : public PartitionBase {
       check(pbdk_weight_flip(shadow_ + s.base + s.lay.w2, s.w2flip, s.cout, 3, 3, s.mid, st), "flip");
     }
   }
+
+  std::vector<DpRegion> dp_all_regions() const override { return {{0, total_}}; }
 
   void buffer(int which, void** ptr, size_t* bytes) override {
     switch (which) {
@@ -490,8 +489,10 @@ class ResNetPartition final : public PartitionBase {
       s.red = arena_.get<float>(4 * s.cout * sizeof(float));
       sblocks_.push_back(s);
     }
-    params_ = arena_.get<float>(total_ * sizeof(float));
-    mom_ = arena_.get<float>(total_ * sizeof(float));
+    // master weights and momentum in ONE allocation (momentum at +total_): a DP peer reaches both
+    // through the one IPC mapping of PBDX_BUF_PARAMS (PartitionBase::dp_sync_state)
+    params_ = arena_.get<float>(2 * total_ * sizeof(float));
+    mom_ = params_ + total_;
     grads_ = arena_.get<float>(total_ * sizeof(float));
     shadow_ = arena_.get<bf16>(total_ * sizeof(bf16));
     losses_ = arena_.get<double>(kBlocks * sizeof(double));

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "knobs.hpp"
+#include "bd_kernels.hpp"
 #include "pbdk.h"
 #include "pbdx.h"
 #include "relay.hpp"
@@ -177,7 +178,7 @@ class PartitionBase {
     int n = body_launches_per_step();
     if (!recv_consumed_.empty()) n += 2;  // relay wait + release
     if (!send_.empty()) n += 2;           // relay wait + copy
-    if (dp_active()) n += 4;              // dp wait consumed, ready, wait ready, consumed
+    if (dp_active()) n += 6;              // dp wait consumed, ready, wait ready, updated, wait updated, consumed
     return n;
   }
 
@@ -307,6 +308,43 @@ class PartitionBase {
   }
   bool dp_active() const { return dp_size_ > 1; }
 
+  // members' master-weight buffers (PBDX_BUF_PARAMS) as seen from this process, member order
+  void dp_set_params(int size, void* const* peer_params) {
+    if (size != dp_size_) throw BadArg("dp params: size differs from the group");
+    dp_params_.assign(static_cast<size_t>(size), nullptr);
+    for (int j = 0; j < size; ++j) {
+      if (j == dp_me_) continue;
+      if (peer_params[j] == nullptr) throw BadArg("dp params: null peer pointer");
+      dp_params_[static_cast<size_t>(j)] = static_cast<const float*>(peer_params[j]);
+    }
+    invalidate_graphs();
+  }
+
+  // Complete the sharded momentum (and weights) of every parameter region from the slice owners'
+  // peer memory: before a checkpoint / migration reads block_state (only the owner's slice is current).
+  void dp_sync_state(cudaStream_t st) {
+    if (!dp_active()) return;
+    float *w = nullptr, *v = nullptr;
+    size_t bytes = 0;
+    buffer(PBDX_BUF_PARAMS, reinterpret_cast<void**>(&w), &bytes);
+    buffer(PBDX_BUF_MOMENTUM, reinterpret_cast<void**>(&v), &bytes);
+    require_dp_params();
+    // momentum lives in the params allocation at +total (every model allocates them together), so a
+    // peer's momentum is its params pointer + the same offset
+    const ptrdiff_t dv = v - w;
+    if (dv != static_cast<ptrdiff_t>(bytes / sizeof(float))) throw BadArg("dp sync: momentum not adjacent to params");
+    for (const DpRegion& r : dp_all_regions()) {
+      std::vector<const float*> pw(static_cast<size_t>(dp_size_)), pv(static_cast<size_t>(dp_size_));
+      for (int j = 0; j < dp_size_; ++j) {
+        const float* base = j == dp_me_ ? w : dp_params_[static_cast<size_t>(j)];
+        pw[static_cast<size_t>(j)] = base + r.off;
+        pv[static_cast<size_t>(j)] = base + dv + r.off;
+      }
+      check(pbdk::dp_gather(w + r.off, nullptr, pw.data(), dp_size_, dp_me_, r.n, st), "dp sync w");
+      check(pbdk::dp_gather(v + r.off, nullptr, pv.data(), dp_size_, dp_me_, r.n, st), "dp sync v");
+    }
+  }
+
   // Which student blocks of the range train (bit i = block block_lo + i).  All by default; the DP
   // baseline of the paper (blocks trained one after another, every step
   // recomputing the teacher prefix) runs partition [0, k] with only block k training.
@@ -405,9 +443,69 @@ class PartitionBase {
     check(pbdk::relay_wait(w, st), "dp wait consumed");
   }
 
-  static constexpr int kMailboxSlots = 64;  // [0,16) relay ready, [16,32) relay consumed, [32,48) dp ready, [48,64) dp consumed
+  // share_gradient + update_weight of a DP group as reduce-scatter + all-gather over peer memory
+  // (DESIGN.md §8).  Every parameter region [off, off+n) of the step is cut into G slices
+  // (pbdk::dp_slice); member `me`:
+  //   1. sums slice `me` of the group's gradient slabs in member order (peer loads) and applies the
+  //      momentum SGD to that slice of w / v (+ bf16 shadow);
+  //   2. publishes "updated" to every member and waits for theirs (device-side flags, mailbox 64+j);
+  //   3. copies every other member's updated slice of w from its peer memory (+ bf16 shadow).
+  // Per member and step that is (G-1)/G * P fp32 read in 1 and again in 3: 2(G-1)/G * 4P bytes over
+  // NVLink, exactly the ring-allreduce volume cost_model.cpp:79-86 prices; each slice is computed
+  // once (fixed member order), so every member holds bit-identical weights.  Momentum stays sharded:
+  // dp_sync_state() completes it when the host reads it.
+  struct DpRegion {
+    size_t off, n;
+  };
+  virtual std::vector<DpRegion> dp_all_regions() const = 0;
+
+  void dp_update(const std::vector<DpRegion>& regions, float* w, float* v, const float* g, void* shadow_bf16,
+                 long long* counter, cudaStream_t st) {
+    require_dp_params();
+    const int G = dp_size_, me = dp_me_;
+    for (const DpRegion& r : regions) {
+      size_t lo = 0, hi = 0;
+      pbdk::dp_slice(r.n, G, me, &lo, &hi);
+      const auto src = dp_sources(g, r.off + lo);
+      void* sh = shadow_bf16 != nullptr ? static_cast<void*>(static_cast<uint16_t*>(shadow_bf16) + r.off + lo) : nullptr;
+      check(pbdk::sgd_momentum_sum(w + r.off + lo, v + r.off + lo, src.data(), G, sh, hi - lo, d_.lr, d_.momentum,
+                                   counter, st),
+            "dp reduce-scatter sgd");
+      counter = nullptr;
+    }
+    pbdk::RelayReleaseArgs rel{};
+    pbdk::RelayWaitArgs wt{};
+    int n = 0;
+    for (int j = 0; j < G; ++j) {
+      if (j == me) continue;
+      rel.flags[n] = dp_mail_[static_cast<size_t>(j)] + 64 + me;
+      wt.flags[n] = mailbox_ + 64 + j;
+      ++n;
+    }
+    rel.count = wt.count = n;
+    rel.seq = relay_seq_ + 2;
+    wt.seq = relay_seq_ + 2;
+    rel.advance = 0;
+    wt.bias = 0;
+    check(pbdk::relay_release(rel, st), "dp updated");
+    check(pbdk::relay_wait(wt, st), "dp wait updated");
+    for (const DpRegion& r : regions) {
+      std::vector<const float*> pw(static_cast<size_t>(G));
+      for (int j = 0; j < G; ++j) pw[static_cast<size_t>(j)] = (j == me ? w : dp_params_[static_cast<size_t>(j)]) + r.off;
+      void* sh = shadow_bf16 != nullptr ? static_cast<void*>(static_cast<uint16_t*>(shadow_bf16) + r.off) : nullptr;
+      check(pbdk::dp_gather(w + r.off, sh, pw.data(), G, me, r.n, st), "dp all-gather");
+    }
+  }
+
+  void require_dp_params() const {
+    if (static_cast<int>(dp_params_.size()) != dp_size_) throw BadArg("dp group: peer params not set (pbdx_dp_set_params)");
+  }
+
+  // [0,16) relay ready, [16,32) relay consumed, [32,48) dp ready, [48,64) dp consumed, [64,80) dp updated
+  static constexpr int kMailboxSlots = 80;
   int dp_size_ = 1, dp_me_ = 0;
   std::vector<const float*> dp_grads_;
+  std::vector<const float*> dp_params_;
   std::vector<unsigned long long*> dp_mail_;
 
   void relay_wait_input(cudaStream_t st) {

@@ -221,11 +221,8 @@ class ResNetF32Partition final : public PartitionBase {
   }
 
   void update_body(cudaStream_t st) override {
-    if (dp_active()) {
-      const auto src = dp_sources(grads_, 0);
-      check(pbdk::sgd_momentum_sum(params_, mom_, src.data(), static_cast<int>(src.size()), nullptr, total_, d_.lr,
-                                   d_.momentum, step_, st),
-            "sgd (dp)");
+    if (dp_active()) {  // reduce-scatter + all-gather over peer memory (PartitionBase::dp_update)
+      dp_update({{0, total_}}, params_, mom_, grads_, nullptr, step_, st);
     } else if (all_train()) {
       check(pbdk::sgd_momentum(params_, mom_, grads_, nullptr, total_, d_.lr, d_.momentum, step_, st), "sgd");
     } else {
@@ -242,6 +239,8 @@ class ResNetF32Partition final : public PartitionBase {
     for (size_t i = 0; i < sblocks_.size(); ++i)
       if (trains(static_cast<int>(i))) refresh_block(sblocks_[i], st);
   }
+
+  std::vector<DpRegion> dp_all_regions() const override { return {{0, total_}}; }
 
   void buffer(int which, void** ptr, size_t* bytes) override {
     switch (which) {
@@ -418,8 +417,10 @@ class ResNetF32Partition final : public PartitionBase {
       cuda(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming), "event");
       sblocks_.push_back(s);
     }
-    params_ = arena_.get<float>(total_ * sizeof(float));
-    mom_ = arena_.get<float>(total_ * sizeof(float));
+    // master weights and momentum in ONE allocation (momentum at +total_): a DP peer reaches both
+    // through the one IPC mapping of PBDX_BUF_PARAMS (PartitionBase::dp_sync_state)
+    params_ = arena_.get<float>(2 * total_ * sizeof(float));
+    mom_ = params_ + total_;
     grads_ = arena_.get<float>(total_ * sizeof(float));
     losses_ = arena_.get<double>(kBlocks * sizeof(double));
     step_ = arena_.get<long long>(sizeof(long long));

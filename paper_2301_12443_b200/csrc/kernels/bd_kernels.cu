@@ -756,6 +756,22 @@ __global__ void sgd_sum_kernel(float4* __restrict__ w, float4* __restrict__ v, c
   if (counter != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *counter += 1;
 }
 
+// all-gather half of the DP exchange: float4 index i of a region belongs to member
+// owner(i) = ((i+1)*G - 1) / n4 (slices [j*n4/G, (j+1)*n4/G)); copy every other member's updated slice
+// of the master weights from its peer memory and refresh the bf16 shadow.
+__global__ void dp_gather_kernel(float4* __restrict__ w, uint2* __restrict__ shadow, const GradSources peers, int me,
+                                 size_t n4) {
+  const unsigned long long G = static_cast<unsigned long long>(peers.count);
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int owner = static_cast<int>(((i + 1) * G - 1) / n4);
+    if (owner == me) continue;
+    const float4 x = peers.g[owner][i];
+    w[i] = x;
+    if (shadow != nullptr) shadow[i] = make_uint2(pack2(x.x, x.y), pack2(x.z, x.w));
+  }
+}
+
 int grid_for(long long work, int per_block = kThreads) {
   const long long b = (work + per_block - 1) / per_block;
   return static_cast<int>(std::max<long long>(1, std::min<long long>(b, 148LL * 16)));
@@ -932,6 +948,16 @@ int sgd_momentum(float* w, float* v, const float* g, void* shadow, size_t n, flo
   sgd_kernel<<<grid_for(static_cast<long long>(n / 4)), kThreads, 0, st>>>(
       reinterpret_cast<float4*>(w), reinterpret_cast<float4*>(v), reinterpret_cast<const float4*>(g),
       static_cast<uint2*>(shadow), n / 4, lr, mu, counter);
+  return ok(cudaGetLastError());
+}
+
+int dp_gather(float* w, void* shadow, const float* const* peer_w, int count, int me, size_t n, cudaStream_t st) {
+  if (n % 4 != 0 || count < 1 || count > 8 || me < 0 || me >= count) return PBDK_EINVAL;
+  GradSources src{};
+  for (int r = 0; r < count; ++r) src.g[r] = reinterpret_cast<const float4*>(peer_w[r]);
+  src.count = count;
+  dp_gather_kernel<<<grid_for(static_cast<long long>(n / 4)), kThreads, 0, st>>>(
+      reinterpret_cast<float4*>(w), static_cast<uint2*>(shadow), src, me, n / 4);
   return ok(cudaGetLastError());
 }
 

@@ -70,5 +70,15 @@ int sgd_momentum(float* w, float* v, const float* g, void* shadow, size_t n, flo
 // the same update on g = g[0] + g[1] + ... (member order), the DP group's gradient slabs in peer memory
 int sgd_momentum_sum(float* w, float* v, const float* const* g, int count, void* shadow, size_t n, float lr, float mu,
                      long long* counter, cudaStream_t st);
+// DP all-gather: w[slice j] = peer_w[j][slice j] for every member j != me (slices: float4 index i belongs to
+// ((i+1)*G-1)/(n/4)), bf16 shadow refreshed when non-null.  peer_w[me] is ignored.
+int dp_gather(float* w, void* shadow, const float* const* peer_w, int count, int me, size_t n, cudaStream_t st);
+
+// element range [lo, hi) of member j's slice of an n-element region (n multiple of 4) in a G-member group
+inline void dp_slice(size_t n, int G, int j, size_t* lo, size_t* hi) {
+  const size_t n4 = n / 4;
+  *lo = 4 * (static_cast<size_t>(j) * n4 / static_cast<size_t>(G));
+  *hi = 4 * ((static_cast<size_t>(j) + 1) * n4 / static_cast<size_t>(G));
+}
 
 }  // namespace pbdk

@@ -81,6 +81,10 @@ def _bind(L):
     L.pbdx_trace_mark.argtypes = [V, V]
     L.pbdx_set_train_mask.argtypes = [V, ctypes.c_uint]
     L.pbdx_dp_set_group.argtypes = [V, I, I, P(V), P(V)]
+    L.pbdx_dp_set_params.argtypes = [V, I, P(V)]
+    L.pbdx_dp_sync_state.argtypes = [V, V]
+    L.pbdx_dp_peer_bytes.argtypes = [ctypes.c_longlong, I, I]
+    L.pbdx_dp_peer_bytes.restype = ctypes.c_longlong
     L.pbdx_block_trace.argtypes = [V] + [P(ctypes.c_float)] * 4
     L.pbdx_mb_layers.argtypes = [I, I]
     L.pbdx_mb_candidates.argtypes = [I, I, I]
@@ -259,6 +263,10 @@ class Partition:
         return self.tensor(BUF_PARAMS)
 
     def momentum(self) -> torch.Tensor:
+        """fp32 momentum.  In a DP group it is sharded by the exchange: completed from the peers first."""
+        if getattr(self, "_dp", False):
+            self.dp_sync_state()
+            torch.cuda.synchronize(self.device)
         return self.tensor(BUF_MOMENTUM)
 
     def losses_tensor(self) -> torch.Tensor:
@@ -366,12 +374,28 @@ class Partition:
         _check(lib().pbdx_block_times(self.handle, t, s), "block_times")
         return list(t), list(s)
 
-    def dp_set_group(self, me: int, peer_grads: List[int], peer_mailboxes: List[int]):
-        """DP group over peer memory (include/pbdx.h pbdx_dp_set_group): member pointers in member order."""
+    def dp_set_group(self, me: int, peer_grads: List[int], peer_mailboxes: List[int],
+                     peer_params: Optional[List[int]] = None):
+        """DP group over peer memory (include/pbdx.h pbdx_dp_set_group / pbdx_dp_set_params): member pointers
+        in member order.  The exchange is a reduce-scatter + all-gather, so groups of size > 1 also need
+        every member's master-weight buffer (peer_params)."""
         n = len(peer_grads)
         g = (ctypes.c_void_p * n)(*[p or 0 for p in peer_grads])
         m = (ctypes.c_void_p * n)(*[p or 0 for p in peer_mailboxes])
         _check(lib().pbdx_dp_set_group(self.handle, n, me, g, m), "dp_set_group")
+        if n > 1:
+            if peer_params is None:
+                raise ValueError("dp group of size > 1 needs peer_params")
+            pp = (ctypes.c_void_p * n)(*[p or 0 for p in peer_params])
+            _check(lib().pbdx_dp_set_params(self.handle, n, pp), "dp_set_params")
+        self._dp = n > 1
+
+    def params_ptr(self) -> int:
+        return self.buffer_ptr(BUF_PARAMS)[0]
+
+    def dp_sync_state(self, stream=None):
+        """Complete the DP-sharded momentum (and weights) from the slice owners (before reading state)."""
+        _check(lib().pbdx_dp_sync_state(self.handle, self._stream(stream)), "dp_sync_state")
 
     def grads_ptr(self) -> int:
         return self.buffer_ptr(BUF_GRADS)[0]
@@ -400,7 +424,8 @@ class Partition:
 
     # -- state migration (runtime.PipeBD.migrate)
     def block_state(self, k: int) -> List[torch.Tensor]:
-        """[weights, momentum] of student block k (fp32, padded layout) — views into device memory."""
+        """[weights, momentum] of student block k (fp32, padded layout) — views into device memory (momentum()
+        completes a DP-sharded momentum first)."""
         base, _, total = self.layouts[k]
         return [self.params()[base:base + total], self.momentum()[base:base + total]]
 

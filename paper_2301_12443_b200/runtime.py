@@ -167,9 +167,9 @@ class PipeBD:
         self._ipc_mapped = []
         st = self.stage
         mine = {"pid": os.getpid(), "input": st.input_ptr(), "mailbox": st.mailbox_ptr(), "row": st.row_bytes_in(),
-                "grads": st.grads_ptr(),
+                "grads": st.grads_ptr(), "params": st.params_ptr(),
                 "h_input": executor.ipc_export(st.input_ptr()), "h_mailbox": executor.ipc_export(st.mailbox_ptr()),
-                "h_grads": executor.ipc_export(st.grads_ptr())}
+                "h_grads": executor.ipc_export(st.grads_ptr()), "h_params": executor.ipc_export(st.params_ptr())}
         allp = [None] * self.world
         dist.all_gather_object(allp, mine)
         endpoints = {}
@@ -177,19 +177,21 @@ class PipeBD:
         peers = {m[1] for m in self.send_msgs} | {m[0] for m in self.recv_msgs} | set(group)
         for r, e in enumerate(allp):
             if e["pid"] == mine["pid"]:
-                endpoints[r] = {"input": e["input"], "mailbox": e["mailbox"], "row": e["row"], "grads": e["grads"]}
+                endpoints[r] = {"input": e["input"], "mailbox": e["mailbox"], "row": e["row"], "grads": e["grads"],
+                                "params": e["params"]}
             elif r in peers:
                 ip, mb, gr = (executor.ipc_open(e["h_input"]), executor.ipc_open(e["h_mailbox"]),
                               executor.ipc_open(e["h_grads"]))
-                self._ipc_mapped += [ip, mb, gr]
-                endpoints[r] = {"input": ip, "mailbox": mb, "row": e["row"], "grads": gr}
+                pa = executor.ipc_open(e["h_params"]) if r in group else None
+                self._ipc_mapped += [ip, mb, gr] + ([pa] if pa is not None else [])
+                endpoints[r] = {"input": ip, "mailbox": mb, "row": e["row"], "grads": gr, "params": pa}
         recv, send = peer_wiring(self.schedule, self.b, self.rank, endpoints)
         st.relay_set_recv(recv)
         st.relay_set_send(send)
         # share_gradient over peer memory inside the DP group (fused into the update kernel)
         if len(group) > 1 and self.grad_share == "peer":
             st.dp_set_group(group.index(self.rank), [endpoints[r]["grads"] for r in group],
-                            [endpoints[r]["mailbox"] for r in group])
+                            [endpoints[r]["mailbox"] for r in group], [endpoints[r]["params"] for r in group])
         torch.cuda.synchronize(st.device)
         dist.barrier()
 
@@ -583,10 +585,48 @@ def profile_blocks(global_batch: int, world: int, keys: Optional[List[int]] = No
         blocks.append({"id": k, "teacher_ms": {str(n): tms[n] for n in keys},
                        "student_ms": {str(n): sms[n] for n in keys}, "act_bytes_per_sample": float(act),
                        "param_bytes": float(pbytes), "teacher_param_bytes": float(tparams)})
-    return {"blocks": blocks, "global_batch": global_batch,
-            "hardware": {"num_devices": world, "link_bytes_per_ms": 7.7e8, "allreduce_bytes_per_ms": 7.25e8,
-                         "mem_bytes_per_device": 1.8e11, "data_load_ms_per_batch": 0.0,
-                         "min_utilization_floor": 1.0}}
+    return {"blocks": blocks, "global_batch": global_batch, "hardware": hardware_spec(world, device)}
+
+
+# NVLink 5 fallback bandwidths (bytes per ms) when fewer than two GPUs are visible: 900 GB/s per
+# direction nominal, derated to what peer copies typically sustain (~85 %); the DP exchange
+# (PartitionBase::dp_update) moves the ring-allreduce volume with peer loads at ~the same rate (~80 %).
+FALLBACK_LINK_BYTES_PER_MS = 7.7e8
+FALLBACK_ALLREDUCE_BYTES_PER_MS = 7.25e8
+
+
+def measure_peer_bandwidth(src: int = 0, dst: int = 1, nbytes: int = 256 << 20, reps: int = 5) -> Optional[float]:
+    """Peer copy bandwidth GPU src -> dst in bytes/ms (CUDA events around device-to-device copies over
+    NVLink), or None when fewer than two GPUs are visible / peer access is unavailable."""
+    if torch.cuda.device_count() < 2 or not torch.cuda.can_device_access_peer(src, dst):
+        return None
+    a = torch.empty(nbytes, dtype=torch.uint8, device=torch.device("cuda", src))
+    b = torch.empty(nbytes, dtype=torch.uint8, device=torch.device("cuda", dst))
+    with torch.cuda.device(dst):
+        b.copy_(a)  # warm (peer mapping)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            b.copy_(a, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+    return nbytes / ms
+
+
+def hardware_spec(world: int, device: Optional[torch.device] = None) -> dict:
+    """HardwareSpec (profile.hpp:66-77) of this node: link and exchange bandwidth from a peer-copy
+    microbenchmark when >= 2 GPUs are visible (both C_i and DPC_j move bytes GPU-to-GPU over NVLink:
+    the relay with SM peer stores, the DP exchange with peer loads of exactly the ring-allreduce
+    volume), the documented fallbacks otherwise; device memory from the device properties."""
+    bw = measure_peer_bandwidth()
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    mem = float(torch.cuda.get_device_properties(dev).total_memory) if torch.cuda.is_available() else 1.8e11
+    return {"num_devices": world,
+            "link_bytes_per_ms": bw if bw is not None else FALLBACK_LINK_BYTES_PER_MS,
+            "allreduce_bytes_per_ms": bw if bw is not None else FALLBACK_ALLREDUCE_BYTES_PER_MS,
+            "mem_bytes_per_device": mem, "data_load_ms_per_batch": 0.0, "min_utilization_floor": 1.0}
 
 
 def observed_profile(reference: dict, measured: Dict[int, Tuple[int, float, float]]) -> dict:

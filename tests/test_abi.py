@@ -132,3 +132,23 @@ def test_wgrad_workspace_monotone_in_batch():
             if prev is not None:
                 assert ws <= prev, (h, c, k, r, st, n, ws, prev)
             prev = ws
+
+
+def test_dp_exchange_peer_bytes_match_ring_volume():
+    """The DP exchange (reduce-scatter + all-gather over peer memory, PartitionBase::dp_update) reads
+    2(G-1)/G * 4P bytes per member and step — the ring-allreduce volume the AHD cost model prices
+    (cost_model.cpp:79-86: 2(g-1)/g * param_bytes / allreduce bandwidth), not the (G-1) * 4P of a
+    member reading every peer's whole slab (round 1's sgd_sum)."""
+    from paper_2301_12443_b200 import executor
+    L = executor.lib()
+    for n in (4, 400, 1000, 12296, 2_914_304):
+        for G in range(1, 9):
+            total_rs = 0
+            for me in range(G):
+                got = L.pbdx_dp_peer_bytes(n, G, me)
+                want = 2 * (G - 1) / G * 4 * n
+                assert abs(got - want) <= 2 * 16 * G, (n, G, me, got, want)
+                assert got < (G - 1) * 4 * n or G <= 2 or n < 16 * G
+                total_rs += got
+            assert total_rs == 2 * (G - 1) * 4 * n  # every slice read G-1 times in each half
+    assert L.pbdx_dp_peer_bytes(6, 2, 0) == -1  # n must be a multiple of 4

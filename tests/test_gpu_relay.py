@@ -67,7 +67,8 @@ def run_inprocess(ex, schedule, b, steps, mode):
                 if len(devs) > 1:
                     for r in devs:
                         stages[r].dp_set_group(devs.index(r), [stages[q].grads_ptr() for q in devs],
-                                               [stages[q].mailbox_ptr() for q in devs])
+                                               [stages[q].mailbox_ptr() for q in devs],
+                                               [stages[q].params_ptr() for q in devs])
         if mode in ("peer", "peer-dp"):
             for r, p in stages.items():
                 p.capture_phases(fuse_teacher_student=True, stream=streams[r])
@@ -154,8 +155,10 @@ def test_resharded_hybrid_peer_relay_bitwise(ex):
 @pytest.mark.parametrize("parts,b", [([(0, 3, [0, 1])], 8), ([(0, 0, [0]), (1, 2, [1, 2]), (3, 3, [3])], 10),
                                      ([(0, 1, [0, 1, 2]), (2, 3, [3, 4])], 7)])
 def test_dp_gradients_over_peer_memory_bitwise(ex, parts, b):
-    """share_gradient fused into the update (pbdx_dp_set_group): members read each other's gradient slabs
-    from peer memory and sum in member order — identical to the host-side sum, every member identical."""
+    """share_gradient + update over peer memory (pbdx_dp_set_group / pbdx_dp_set_params): each member sums
+    its slice of the group's gradient slabs in member order and updates it, then gathers the other slices
+    (reduce-scatter + all-gather) — identical to the host-side sum, every member identical (momentum
+    completed from the slice owners by dp_sync_state when read)."""
     s = sched(parts, b)
     got = run_inprocess(ex, s, b, 3, "peer-dp")
     want = run_inprocess(ex, s, b, 3, "copy")
