@@ -55,6 +55,8 @@ def parse():
                     help="N>1 teacher-activation relay: K11 peer stores over NVLink (default) or NCCL send/recv")
     ap.add_argument("--no-ahd", action="store_true",
                     help="N>1: search only contiguous one-group-per-partition schedules (pure pipeline)")
+    ap.add_argument("--no-baselines", action="store_true",
+                    help="N>1: skip the measured DP / LS baselines (runtime.run_baseline)")
     ap.add_argument("--pipeline", action="store_true",
                     help="use the multi-GPU runtime (profile -> best_schedule -> PipeBD) even at N=1")
     args = ap.parse_args()

@@ -38,6 +38,10 @@ int pbd_best_schedule(const char* profile_json, int contiguous_only, int threads
                       char** meta_out, char** err_out);
 
 /* cost_out: {"partition_ms": [...], "step_ms": x, "feasible": b, "reason": s} */
+/* Baseline plans of the paper's comparison (schedule.cpp:246-303): kind 0 = DP (every block in turn on all
+ * devices with the teacher prefix recomputed), 1 = LS (LPT block assignment, full batch per device).
+ * JSON {"kind", "per_device_batch", "phase_step_ms", "device_blocks", "device_step_ms", "step_ms"}. */
+int pbd_baseline_plan(const char* profile_json, int kind, char** plan_out, char** err_out);
 int pbd_predicted_step_time(const char* profile_json, const char* schedule_json, char** cost_out, char** err_out);
 
 /* sim_json: SimConfig fields (any subset); report_out: save_report() document */

@@ -52,6 +52,8 @@ def lib() -> ctypes.CDLL:
     L.pbd_synth_profile.argtypes = [c_char_p, ctypes.POINTER(c_void_p), ctypes.POINTER(c_void_p)]
     L.pbd_shard_range.argtypes = [c_int, c_int, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_int)]
     L.pbd_time_best_schedule.argtypes = [c_char_p, c_int, ctypes.POINTER(c_double), ctypes.POINTER(c_void_p)]
+    L.pbd_baseline_plan.argtypes = [c_char_p, c_int, ctypes.POINTER(c_void_p), ctypes.POINTER(c_void_p)]
+    L.pbd_baseline_plan.restype = c_int
     for name in ("pbd_best_schedule", "pbd_predicted_step_time", "pbd_simulate", "pbd_reconfigure",
                  "pbd_profile_drift", "pbd_exec_time", "pbd_load_save_profile", "pbd_synth_profile",
                  "pbd_shard_range", "pbd_time_best_schedule"):

@@ -67,6 +67,14 @@ def best_schedule_text(profile: Doc, contiguous_only: bool = False) -> str:
     return _lib.take_string(out)
 
 
+def baseline_plan(profile: Doc, kind: str) -> dict:
+    """dp_schedule / ls_schedule (schedule.cpp:246-303) of a profile: the paper's DP and LS baselines."""
+    out, err = ctypes.c_void_p(), ctypes.c_void_p()
+    rc = _lib.lib().pbd_baseline_plan(_text(profile), {"dp": 0, "ls": 1}[kind], ctypes.byref(out), ctypes.byref(err))
+    _check(rc, err)
+    return json.loads(_lib.take_string(out))
+
+
 def predicted_step_time(profile: Doc, schedule: Doc) -> dict:
     out, err = ctypes.c_void_p(), ctypes.c_void_p()
     rc = _lib.lib().pbd_predicted_step_time(_text(profile), _text(schedule), ctypes.byref(out), ctypes.byref(err))

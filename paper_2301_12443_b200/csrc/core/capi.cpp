@@ -90,6 +90,32 @@ int pbd_best_schedule(const char* profile_json, int contiguous_only, int threads
   });
 }
 
+int pbd_baseline_plan(const char* profile_json, int kind, char** plan_out, char** err_out) {
+  return shielded(err_out, [&] {
+    const pbd::CostModel m(pbd::load_profile(profile_json));
+    if (kind != 0 && kind != 1) throw pbd::ValidationError("baseline kind must be 0 (dp) or 1 (ls)");
+    const pbd::BaselinePlan p = kind == 0 ? pbd::dp_schedule(m) : pbd::ls_schedule(m);
+    Value j = Value::object();
+    j["kind"] = Value::string(kind == 0 ? "dp" : "ls");
+    j["per_device_batch"] = Value::integer(p.per_device_batch);
+    Value ph = Value::array();
+    for (double x : p.phase_step_ms) ph.push(Value::real(x));
+    j["phase_step_ms"] = std::move(ph);
+    Value db = Value::array();
+    for (const auto& blocks : p.device_blocks) {
+      Value b = Value::array();
+      for (int k : blocks) b.push(Value::integer(k));
+      db.push(std::move(b));
+    }
+    j["device_blocks"] = std::move(db);
+    Value ds = Value::array();
+    for (double x : p.device_step_ms) ds.push(Value::real(x));
+    j["device_step_ms"] = std::move(ds);
+    j["step_ms"] = Value::real(p.step_ms);
+    *plan_out = heap_copy(j.dump(-1));
+  });
+}
+
 int pbd_predicted_step_time(const char* profile_json, const char* schedule_json, char** cost_out, char** err_out) {
   return shielded(err_out, [&] {
     const pbd::CostModel m(pbd::load_profile(profile_json));

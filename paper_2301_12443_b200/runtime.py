@@ -643,6 +643,108 @@ def observed_profile(reference: dict, measured: Dict[int, Tuple[int, float, floa
     return obs
 
 
+# ---------------------------------------------------------------- the paper's baselines on devices
+
+class _StepTimer:
+    """Per-step device time of this rank (CUDA events on the stage's device; wall clock on CPU)."""
+
+    def __init__(self, device):
+        self.cuda = device.type == "cuda"
+        self.device = device
+
+    def __enter__(self):
+        if self.cuda:
+            torch.cuda.synchronize(self.device)
+            self.e0, self.e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            self.e0.record()
+        else:
+            import time as _t
+            self.t0 = _t.perf_counter()
+        return self
+
+    def __exit__(self, *exc):
+        if self.cuda:
+            self.e1.record()
+            torch.cuda.synchronize(self.device)
+            self.ms = self.e0.elapsed_time(self.e1)
+        else:
+            import time as _t
+            self.ms = (_t.perf_counter() - self.t0) * 1e3
+
+
+def _max_over_ranks(x: float, device) -> float:
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=device if device.type == "cuda" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t[0])
+
+
+def run_baseline(kind: str, plan: dict, global_batch: int, make_stage: Callable, steps: int, warmup: int = 1,
+                 rank: int = 0, world: int = 1) -> dict:
+    """Execute one of the paper's baselines for real (plans from core.baseline_plan,
+    schedule.cpp:246-303; their simulated timelines simulate.cpp:269-386):
+
+      dp: every block in turn, on all `world` ranks data-parallel: phase k runs the teacher prefix
+          T_0..T_k (recomputed, no relay) and student k on this rank's shard, all-reduces block k's
+          gradients (torch.distributed, the DDP allreduce of PAPER.md:395) and updates it;
+      ls: LPT block assignment (plan["device_blocks"]): this rank runs T_0..T_{last assigned} and its
+          assigned students on the full batch, no communication.
+
+    make_stage(lo, hi, n, first) -> a stage with set_train_mask / layouts / grads (executor.Partition or
+    the oracle stage of the CPU tests).  Returns per-phase step ms (max over ranks) and the time to
+    train every block for one step of data ("all_blocks_ms": the sum of the phases for dp, the slowest
+    rank for ls), plus the final stages' block weights for the caller's checks."""
+    out = {"kind": kind, "plan": plan, "states": {}}
+    if kind == "dp":
+        first, n = shard(global_batch, world, rank)
+        phase_ms = []
+        for k in range(len(plan["phase_step_ms"])):
+            st = make_stage(0, k, n, first)
+            st.set_train_mask(1 << k)
+            base, _, total = st.layouts[k]
+            dev = _dev_of(st)
+            times = []
+            for s in range(warmup + steps):
+                with _StepTimer(dev) as t:
+                    st.teacher_forward()
+                    st.student_step()
+                    if world > 1:
+                        g = st.grads()[base:base + total]
+                        dist.all_reduce(g)
+                    st.apply_update()
+                if s >= warmup:
+                    times.append(t.ms)
+            phase_ms.append(_max_over_ranks(sorted(times)[len(times) // 2], dev))
+            out["states"][k] = [x.detach().cpu().clone() for x in st.block_state(k)]
+            del st
+        out["phase_ms"] = phase_ms
+        out["all_blocks_ms"] = sum(phase_ms)
+        return out
+    if kind == "ls":
+        mine = plan["device_blocks"][rank] if rank < len(plan["device_blocks"]) else []
+        ms = 0.0
+        dev = torch.device("cpu")
+        if mine:
+            st = make_stage(0, max(mine), global_batch, 0)
+            st.set_train_mask(sum(1 << k for k in mine))
+            dev = _dev_of(st)
+            times = []
+            for s in range(warmup + steps):
+                with _StepTimer(dev) as t:
+                    st.teacher_forward()
+                    st.student_step()
+                    st.apply_update()
+                if s >= warmup:
+                    times.append(t.ms)
+            ms = sorted(times)[len(times) // 2]
+            out["states"] = {k: [x.detach().cpu().clone() for x in st.block_state(k)] for k in mine}
+        out["device_ms"] = ms
+        out["all_blocks_ms"] = _max_over_ranks(ms, dev)
+        return out
+    raise ValueError("baseline kind must be dp or ls")
+
+
 # ---------------------------------------------------------------- bench entry (torchrun, N > 1)
 
 def bench_pipeline(args, rank: int, world: int, local_rank: int) -> dict:
@@ -766,6 +868,33 @@ def bench_pipeline(args, rank: int, world: int, local_rank: int) -> dict:
     dist.all_gather_object(all_losses, losses)
     pred = core.predicted_step_time(info["profile"], sched)
     h2d = (me.count * (image or 32) ** 2 * 3 * 4) if host is not None else 0
+    relay_mode, launches, nblk = pipe.relay, pipe.stage.launches_per_step(), len(pipe.stage.blocks)
+    baselines = None
+    if not getattr(args, "no_baselines", False) and model == "resnet":
+        # the paper's DP and LS baselines on the same ranks, bounded step counts
+        del pipe
+        torch.cuda.synchronize(dev)
+
+        def plain_stage(lo, hi, n, first):
+            p = executor.Partition(lo, hi, n, gb, device=dev, model=model, image=image)
+            p.init_params()
+            p.set_shard(n, first)
+            return p
+
+        nb = min(args.steps, 20)
+        baselines = {}
+        for kind in ("dp", "ls"):
+            plan = core.baseline_plan(info["profile"], kind)
+            res = run_baseline(kind, plan, gb, plain_stage, steps=nb, warmup=3, rank=rank, world=world)
+            baselines[kind] = {"all_blocks_ms": res["all_blocks_ms"], "predicted_ms": plan["step_ms"],
+                               "pipebd_step_ms": ms, "speedup": res["all_blocks_ms"] / ms, "steps": nb}
+            if kind == "dp":
+                baselines[kind]["phase_ms"] = res["phase_ms"]
+            else:
+                baselines[kind]["device_blocks"] = plan["device_blocks"]
+        baselines["note"] = ("time to train every block for one step of data on the same ranks: DP (blocks in "
+                             "turn, teacher prefix recomputed, NCCL allreduce) / LS (LPT blocks per rank, full "
+                             "batch) vs Pipe-BD's step; dp_schedule / ls_schedule plans (schedule.cpp:246-303)")
     dist.barrier()
     dist.destroy_process_group()
     return {"metric": "blockwise-distill samples/sec", "value": gb / ms * 1e3, "unit": "samples/s",
@@ -778,13 +907,13 @@ def bench_pipeline(args, rank: int, world: int, local_rank: int) -> dict:
                        "global_batch": gb,
                        "parallelism": "ahd " + ";".join(f"{p['blocks']}x{len(p['devices'])}"
                                                         for p in sched["partitions"]),
-                       "relay": pipe.relay,
+                       "relay": relay_mode,
                        "l2": "no flush: per-step working set > 126 MB L2"},
             "e2e": {"value": gb / e2e_ms * 1e3, "unit": "samples/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": 8 * len(pipe.stage.blocks), "ms_per_step": e2e_ms},
+                    "d2h_bytes_per_step": 8 * nblk, "ms_per_step": e2e_ms},
             "schedule": sched, "predicted_step_ms": pred["step_ms"], "profile": info["profile"],
             "block_losses": {k: v for d in all_losses for k, v in d.items()},
-            "gpu_launches": pipe.stage.launches_per_step() * args.steps,
+            "gpu_launches": launches * args.steps, "baselines_measured": baselines,
             "roofline": _step_roofline(model, image, paths, gb, ms, world)}
 
 

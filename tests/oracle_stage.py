@@ -28,6 +28,16 @@ class OracleStage:
         self.step_idx = 0
         self._losses = [0.0] * len(self.blocks)
         self.acts = None
+        self.mask = (1 << len(self.blocks)) - 1
+        offs = np.cumsum([0] + self.sizes)
+        self.layouts = {k: (int(offs[i]), None, self.sizes[i]) for i, k in enumerate(self.blocks)}
+
+    def set_train_mask(self, mask):
+        """Bit i = student block lo + i trains (the executor's pbdx_set_train_mask)."""
+        self.mask = mask
+
+    def _trains(self, i):
+        return (self.mask >> i) & 1
 
     def input_act(self):
         return self.in_buf
@@ -52,6 +62,9 @@ class OracleStage:
     def student_step(self):
         parts = []
         for i, k in enumerate(self.blocks):
+            if not self._trains(i):
+                parts.append(np.zeros_like(self.sp[k]))
+                continue
             loss, g = bd.student_fwd_bwd(k, self.sp[k], self.acts[i], self.acts[i + 1], self.b, 1)
             self._losses[i] = loss
             parts.append(g)
@@ -60,8 +73,9 @@ class OracleStage:
     def apply_update(self):
         off = 0
         g = self.grad_buf.numpy()
-        for k, sz in zip(self.blocks, self.sizes):
-            bd.sgd(self.sp[k], self.mom[k], g[off:off + sz].copy())
+        for i, (k, sz) in enumerate(zip(self.blocks, self.sizes)):
+            if self._trains(i):
+                bd.sgd(self.sp[k], self.mom[k], g[off:off + sz].copy())
             off += sz
         self.step_idx += 1
 

@@ -320,3 +320,58 @@ def test_checkpoint_rejects_mismatch(tmp_path):
     assert meta["step"] == 1 and meta["global_batch"] == b and set(meta["block_numel"]) == {"0", "1", "2", "3"}
     (rank, tag, msg), = _spawn(_ckpt_worker, 1, sched([(0, 3, [0])], 7), 7, 1, ck, "resume")
     assert tag == "error" and "global batch" in msg
+
+
+def _baseline_worker(rank, world, port, kind, plan, b, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    torch.set_num_threads(2)
+    from tests.oracle_stage import OracleStage
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        res = runtime.run_baseline(kind, plan, b, lambda lo, hi, n, first: OracleStage(lo, hi, n, first, b),
+                                   steps=1, warmup=0, rank=rank, world=world)
+        q.put((rank, {k: v[0].numpy().copy() for k, v in res["states"].items()}, res["all_blocks_ms"]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_dp_baseline_on_ranks_equals_ddp_oracle():
+    """The paper's DP baseline executed on 2 ranks (runtime.run_baseline, plan = core.baseline_plan 'dp'):
+    each block in turn, teacher prefix recomputed, gradients all-reduced over the shards — one step of
+    block k equals the oracle's DDP step of block k on the same 2 shards (remainder rule, odd batch)."""
+    from oracle import bd
+    from paper_2301_12443_b200 import core
+    from tests.profiles import proportional_doc
+    b = 5
+    plan = core.baseline_plan(proportional_doc([1, 1, 1, 1], [1, 1, 1, 1], 2, b), "dp")
+    assert len(plan["phase_step_ms"]) == 4 and plan["per_device_batch"] == 3
+    out = _spawn(_baseline_worker, 2, "dp", plan, b)
+    tr = bd.Trainer(b, bf16_mode=1)
+    tr.step(0, {k: 2 for k in range(4)})
+    for rank, states, ms in out:
+        assert ms > 0
+        for k, w in states.items():
+            np.testing.assert_allclose(w, tr.sp[k], rtol=1e-6, atol=1e-9)
+
+
+def test_ls_baseline_on_ranks_equals_oracle():
+    """LS baseline on 2 ranks: the LPT assignment of core.baseline_plan 'ls' (schedule.cpp:261-303), each
+    rank trains its blocks on the full batch with its own teacher prefix, no communication."""
+    from oracle import bd
+    from paper_2301_12443_b200 import core
+    from tests.profiles import proportional_doc
+    b = 4
+    plan = core.baseline_plan(proportional_doc([1, 2, 3, 4], [1, 2, 3, 4], 2, b), "ls")
+    assert sorted(k for d in plan["device_blocks"] for k in d) == [0, 1, 2, 3]
+    out = _spawn(_baseline_worker, 2, "ls", plan, b)
+    tr = bd.Trainer(b, bf16_mode=1)
+    tr.step(0)
+    seen = set()
+    for rank, states, ms in out:
+        assert sorted(states) == sorted(plan["device_blocks"][rank])
+        for k, w in states.items():
+            np.testing.assert_allclose(w, tr.sp[k], rtol=1e-6, atol=1e-9)
+            seen.add(k)
+    assert seen == {0, 1, 2, 3}
