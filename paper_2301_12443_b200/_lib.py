@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libpbd.so")
+# PBD_LIB_VARIANT=exp loads the experiments build (make EXPERIMENTS=1 -> lib-exp/, A/B scripts only)
+LIB_PATH = os.path.join(_HERE, "lib-exp" if os.environ.get("PBD_LIB_VARIANT") == "exp" else "lib", "libpbd.so")
 
 c_int, c_long, c_double, c_size_t, c_void_p, c_char_p = (
     ctypes.c_int, ctypes.c_long, ctypes.c_double, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_char_p)

@@ -117,12 +117,12 @@ struct SBlock {
   const bf16* target = nullptr;
   bf16 *y1, *a1, *y2, *ys, *dy2, *dys, *g1, *dy1, *w2flip;
   float *st1, *st2, *sts, *red, *red1;
+  pbdk::FixScratch fx[4];  // self-finalizing reductions: BN1 stats, BN2+BNsc stats, loss, BN1 backward
   pbdk::FpropPlan p_conv1, p_sc, p_conv2, p_dgrad;
   pbdk::WgradPlan p_w2, p_wsc, p_w1;
   // per-block scratch + stream: student blocks only depend on teacher outputs, so each runs
   // on its own stream as soon as its teacher block is done (overlaps teacher k+1 and the
   // other student blocks; the late blocks alone do not fill 148 SMs).
-  float* rws = nullptr;
   void* wws = nullptr;
   void* wws2 = nullptr;  // workspace of the side stream's wgrads
   size_t wws_bytes = 0;
@@ -239,15 +239,15 @@ class ResNetPartition final : public PartitionBase {
       const int m = n_ * s.hout * s.hout;
       check(pbdk::fprop_run(s.p_conv1, st), "conv1");
       check(pbdk::fprop_run(s.p_sc, st), "shortcut");
-      check(pbdk::bn_stats(s.y1, m, s.mid, s.rws, s.st1, st), "bn1 stats");
+      check(pbdk::bn_stats_fix(s.y1, nullptr, m, s.mid, s.fx[0], s.st1, nullptr, st), "bn1 stats");
       check(pbdk::bn_apply_relu(s.y1, s.st1, p + s.lay.g1, p + s.lay.b1, s.a1, m, s.mid, st), "bn1 apply");
       check(pbdk::fprop_run(s.p_conv2, st), "conv2");
-      check(pbdk::bn_stats2(s.y2, s.ys, m, s.cout, s.rws, s.st2, s.sts, st), "bn2/bnsc stats");
+      check(pbdk::bn_stats_fix(s.y2, s.ys, m, s.cout, s.fx[1], s.st2, s.sts, st), "bn2/bnsc stats");
       const double norm = static_cast<double>(d_.global_batch) * s.cout * s.hout * s.hout;
       pbdk::MseArgs a{s.y2, s.ys, s.target, s.st2, s.sts, p + s.lay.g2, p + s.lay.b2, p + s.lay.gsc, p + s.lay.bsc,
-                      m, s.cout, static_cast<float>(2.0 / norm), norm, s.rws, s.red, g + s.lay.g2, g + s.lay.b2,
+                      m, s.cout, static_cast<float>(2.0 / norm), norm, nullptr, s.red, g + s.lay.g2, g + s.lay.b2,
                       g + s.lay.gsc, g + s.lay.bsc, losses_ + i, s.dy2, s.dys};
-      check(pbdk::mse_bn_loss(a, st), "mse");
+      check(pbdk::mse_bn_loss_fix(a, s.fx[2], st), "mse");
       cudaStream_t ws = st;
       if (s.side != nullptr) {
         cuda(cudaEventRecord(s.fork, st), "event");
@@ -257,8 +257,8 @@ class ResNetPartition final : public PartitionBase {
       check(pbdk::wgrad_run(s.p_w2, ws), "wgrad2");
       check(pbdk::wgrad_run(s.p_wsc, ws), "wgrad sc");
       check(pbdk::fprop_run(s.p_dgrad, st), "dgrad2");
-      check(pbdk::bn_bwd(s.g1, s.y1, s.st1, p + s.lay.g1, m, s.mid, s.rws, s.red1, g + s.lay.g1, g + s.lay.b1, s.dy1,
-                         st),
+      check(pbdk::bn_bwd_fix(s.g1, s.y1, s.st1, p + s.lay.g1, m, s.mid, s.fx[3], s.red1, g + s.lay.g1, g + s.lay.b1,
+                             s.dy1, st),
             "bn1 bwd");
       check(pbdk::wgrad_run(s.p_w1, st), "wgrad1");
       if (s.side != nullptr) {
@@ -331,7 +331,7 @@ class ResNetPartition final : public PartitionBase {
       if (!trains(static_cast<int>(i))) continue;
       const SBlock& s = sblocks_[i];
       ++trained;
-      n += 3 + 3 + 2 + 3 + 1 + 3;  // convs, bn1 stats(2)+apply, bn2+bnsc stats(2), mse(3), dgrad, bn_bwd(3)
+      n += 3 + 2 + 1 + 2 + 1 + 2;  // convs, bn1 stats+apply, bn2+bnsc stats, mse(2), dgrad, bn_bwd(2)
       n += (s.p_w2.splits > 1 ? 2 : 1) + (s.p_wsc.splits > 1 ? 2 : 1) + (s.p_w1.splits > 1 ? 2 : 1);
     }
     n += all_train() ? 1 + static_cast<int>(sblocks_.size()) : 2 * trained;  // sgd + flips
@@ -487,6 +487,14 @@ class ResNetPartition final : public PartitionBase {
       s.st2 = arena_.get<float>(2 * s.cout * sizeof(float));
       s.sts = arena_.get<float>(2 * s.cout * sizeof(float));
       s.red = arena_.get<float>(4 * s.cout * sizeof(float));
+      {  // zero-initialised once; each reduction's last CTA re-zeroes its scratch
+        const size_t words = pbdk::fix_acc_words(s.cout);
+        auto* acc = arena_.get<unsigned long long>(4 * words * sizeof(unsigned long long));
+        auto* tickets = arena_.get<unsigned int>(4 * sizeof(unsigned int));
+        cuda(cudaMemset(acc, 0, 4 * words * sizeof(unsigned long long)), "memset");
+        cuda(cudaMemset(tickets, 0, 4 * sizeof(unsigned int)), "memset");
+        for (int j = 0; j < 4; ++j) s.fx[j] = pbdk::FixScratch{acc + j * words, tickets + j};
+      }
       sblocks_.push_back(s);
     }
     // master weights and momentum in ONE allocation (momentum at +total_): a DP peer reaches both
@@ -501,12 +509,9 @@ class ResNetPartition final : public PartitionBase {
 
     // ---- per-block scratch sized for n_max, streams and events
     for (SBlock& s : sblocks_) {
-      const int m = d_.n_max * s.hout * s.hout;
-      size_t rws = std::max(pbdk::reduce_workspace_floats(m, s.cout, 3), pbdk::reduce_workspace_floats(m, s.mid, 3));
       size_t wws = 0;
       for (const pbdk_conv_desc& cd : {conv1_desc(s, d_.n_max), sc_desc(s, d_.n_max), conv2_desc(s, d_.n_max)})
         wws = std::max(wws, pbdk::wgrad_workspace_bytes(cd));
-      s.rws = arena_.get<float>(rws * sizeof(float));
       s.wws_bytes = wws;
       s.wws = arena_.get<void>(wws);
       const bool last = s.k == d_.block_hi;

@@ -21,6 +21,7 @@
 #include "bd_kernels.hpp"
 #include "pbdk.h"
 #include "sm100.cuh"
+#include "fixacc.cuh"
 
 namespace pbdk {
 
@@ -695,6 +696,221 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_apply_kernel(const typename I
   }
 }
 
+
+// ------------------------------------------------------------------ self-finalizing partial passes
+// The ResNet student step's reductions (BN statistics, loss sums, BN-backward sums) add each CTA's
+// fp32 chunk partial EXACTLY into fixed-point accumulators (fixacc.cuh); the last CTA to finish
+// (atomic ticket) turns the totals into the consumers' coefficients — the former finalize kernels'
+// arithmetic — then zeroes the accumulators and its ticket for the next step.  One launch instead of
+// two per reduction; integer adds commute, so the result does not depend on CTA completion order.
+
+// CTA-level fixed-order reduction of NV*V floats per thread (as cta_reduce_store); the CTA's
+// per-channel fp32 partial (v, c) is added exactly to the sum out[(v * C + c) * kFixWords ..].
+template <int NV, int V>
+__device__ void cta_reduce_fix(float (&acc)[NV][V], int cg, int rpp, int C, unsigned long long* __restrict__ out) {
+  __shared__ float sm[kThreads * NV * V];
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int j = 0; j < V; ++j) sm[(v * V + j) * kThreads + t] = acc[v][j];
+  __syncthreads();
+  for (int o = t; o < NV * cg * V; o += kThreads) {
+    const int v = o / (cg * V);
+    const int rem = o - v * cg * V;
+    const int g = rem / V;
+    const int j = rem - g * V;
+    float s = 0.0f;
+    for (int r = 0; r < rpp; ++r) s += sm[(v * V + j) * kThreads + r * cg + g];
+    fix_red(out + (static_cast<size_t>(v) * C + g * V + j) * kFixWords, s);
+  }
+}
+
+// true in the last CTA of the grid to pass (every thread's accumulator atomics are performed before
+// its CTA takes a ticket); that CTA then sees every other CTA's adds.  Resets the ticket.
+__device__ __forceinline__ bool last_cta(unsigned int* ticket) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int prev = atomicAdd(ticket, 1u);
+    last = prev == gridDim.x - 1;
+    if (last) *ticket = 0u;
+  }
+  __syncthreads();
+  if (last) __threadfence();
+  return last;
+}
+
+__device__ __forceinline__ double fix_take(unsigned long long* p) {  // read a finished sum and zero it
+  const unsigned long long v[kFixWords] = {__ldcg(p), __ldcg(p + 1), __ldcg(p + 2)};
+  p[0] = 0ull;
+  p[1] = 0ull;
+  p[2] = 0ull;
+  return fix_value(v);
+}
+
+// -- BN statistics of NT same-shape tensors -> mean / rstd (bn_stats_finalize_kernel's arithmetic)
+template <int V, int NT>
+__global__ void __launch_bounds__(kThreads) bn_stats_fix_kernel(const __nv_bfloat16* __restrict__ y0,
+                                                                const __nv_bfloat16* __restrict__ y1, int m, int C,
+                                                                int rows_per_chunk, int cg, int rpp,
+                                                                unsigned long long* __restrict__ acc,
+                                                                unsigned int* ticket, float* __restrict__ mr0,
+                                                                float* __restrict__ mr1) {
+  const int g = threadIdx.x % cg;
+  const int slot = threadIdx.x / cg;
+  float a[2 * NT][V] = {};
+  if (slot < rpp) {
+    const int r0 = blockIdx.x * rows_per_chunk;
+    const int r1 = min(m, r0 + rows_per_chunk);
+#pragma unroll 4
+    for (int r = r0 + slot; r < r1; r += rpp) {
+      float f[NT][V];
+      IoBf16::template load<V>(y0, r, C, g * V, f[0]);
+      if (NT == 2) IoBf16::template load<V>(y1, r, C, g * V, f[NT - 1]);
+#pragma unroll
+      for (int t = 0; t < NT; ++t)
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          a[2 * t][j] += f[t][j];
+          a[2 * t + 1][j] += f[t][j] * f[t][j];
+        }
+    }
+  }
+  cta_reduce_fix<2 * NT, V>(a, cg, rpp, C, acc);  // acc[(2t + {0: sum, 1: sumsq}) * C + c]
+  if (!last_cta(ticket)) return;
+  for (int o = threadIdx.x; o < NT * C; o += blockDim.x) {
+    const int t = o / C, c = o - t * C;
+    const double s1 = fix_take(acc + (static_cast<size_t>(2 * t) * C + c) * kFixWords);
+    const double s2 = fix_take(acc + (static_cast<size_t>(2 * t + 1) * C + c) * kFixWords);
+    const double mu = s1 / static_cast<double>(m);
+    const double var = s2 / static_cast<double>(m) - mu * mu;
+    float* mr = t == 0 ? mr0 : mr1;
+    mr[c] = static_cast<float>(mu);
+    mr[C + c] = 1.0f / sqrtf(static_cast<float>(var) + 1e-5f);
+  }
+}
+
+// -- loss partial sums (sum g, g*y2, g*ys per channel; sum (s-t)^2) -> coef / parameter gradients / loss
+struct LossOut {
+  double norm;
+  unsigned long long* acc;  // sums [3][C] + [1] (loss), kFixWords each
+  unsigned int* ticket;
+  float* coef;  // [4C]: Q2, R2, Qs, Rs
+  float *dg2, *db2, *dgs, *dbs;
+  double* loss;
+};
+
+__global__ void __launch_bounds__(kThreads) loss_partial_fix_kernel(const LossParams p, int rows_per_chunk, int cg,
+                                                                    int rpp, const LossOut o) {
+  constexpr int V = kLossPartialV;
+  const int gi = threadIdx.x % cg;
+  const int slot = threadIdx.x / cg;
+  float acc[3][V] = {};
+  float lsum = 0.0f;
+  if (slot < rpp) {
+    float A2[V], As[V], Bz[V];
+    loss_affine<V>(p, gi * V, A2, As, Bz);
+    const int r0 = blockIdx.x * rows_per_chunk;
+    const int r1 = min(p.m, r0 + rows_per_chunk);
+#pragma unroll 4
+    for (int r = r0 + slot; r < r1; r += rpp) {
+      float y2[V], ys[V], t[V];
+      IoBf16::template load<V>(static_cast<const __nv_bfloat16*>(p.y2), r, p.C, gi * V, y2);
+      IoBf16::template load<V>(static_cast<const __nv_bfloat16*>(p.ys), r, p.C, gi * V, ys);
+      IoBf16::template load<V>(static_cast<const __nv_bfloat16*>(p.t), r, p.C, gi * V, t);
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const float z = fmaf(A2[j], y2[j], fmaf(As[j], ys[j], Bz[j]));
+        const float d = (z > 0.0f ? z : 0.0f) - t[j];
+        const float g = z > 0.0f ? d * p.gscale : 0.0f;
+        lsum += d * d;
+        acc[0][j] += g;
+        acc[1][j] += g * y2[j];
+        acc[2][j] += g * ys[j];
+      }
+    }
+  }
+  __shared__ float lred[kThreads / 32];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, off);
+  if ((threadIdx.x & 31) == 0) lred[threadIdx.x >> 5] = lsum;
+  cta_reduce_fix<3, V>(acc, cg, rpp, p.C, o.acc);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.0f;
+    for (int i = 0; i < kThreads / 32; ++i) s += lred[i];
+    fix_red(o.acc + 3 * p.C * kFixWords, s);
+  }
+  if (!last_cta(o.ticket)) return;
+  const int C = p.C;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {  // loss_finalize_kernel's arithmetic
+    const double sg = fix_take(o.acc + kFixWords * c);
+    const double sgy2 = fix_take(o.acc + kFixWords * (C + c));
+    const double sgys = fix_take(o.acc + kFixWords * (2 * C + c));
+    const float m2 = p.st2[c], r2 = p.st2[C + c], ms = p.sts[c], rs = p.sts[C + c];
+    const float A2 = p.g2[c] * r2, As = p.gs[c] * rs;
+    const double sgx2 = static_cast<double>(r2) * (sgy2 - static_cast<double>(m2) * sg);
+    const double sgxs = static_cast<double>(rs) * (sgys - static_cast<double>(ms) * sg);
+    o.db2[c] = static_cast<float>(sg);
+    o.dbs[c] = static_cast<float>(sg);
+    o.dg2[c] = static_cast<float>(sgx2);
+    o.dgs[c] = static_cast<float>(sgxs);
+    const double c2 = static_cast<double>(A2) / p.m, cs = static_cast<double>(As) / p.m;
+    o.coef[c] = static_cast<float>(-c2 * sgx2 * r2);
+    o.coef[C + c] = static_cast<float>(-c2 * (sg - sgx2 * r2 * m2));
+    o.coef[2 * C + c] = static_cast<float>(-cs * sgxs * rs);
+    o.coef[3 * C + c] = static_cast<float>(-cs * (sg - sgxs * rs * ms));
+  }
+  if (threadIdx.x == 0) *o.loss = fix_take(o.acc + kFixWords * 3 * C) / o.norm;
+}
+
+// -- BN backward sums (sum g, sum g*y) -> coef [Q | R] and dgamma / dbeta (bn_bwd_finalize_kernel's arithmetic)
+template <int V>
+__global__ void __launch_bounds__(kThreads) bn_bwd_fix_partial_kernel(const __nv_bfloat16* __restrict__ gin,
+                                                                      const __nv_bfloat16* __restrict__ y, int m, int C,
+                                                                      int rows_per_chunk, int cg, int rpp,
+                                                                      unsigned long long* __restrict__ acc,
+                                                                      unsigned int* ticket, const float* __restrict__ st,
+                                                                      const float* __restrict__ gamma,
+                                                                      float* __restrict__ coef,
+                                                                      float* __restrict__ dgamma,
+                                                                      float* __restrict__ dbeta) {
+  const int gi = threadIdx.x % cg;
+  const int slot = threadIdx.x / cg;
+  float a[2][V] = {};
+  if (slot < rpp) {
+    const int r0 = blockIdx.x * rows_per_chunk;
+    const int r1 = min(m, r0 + rows_per_chunk);
+#pragma unroll 4
+    for (int r = r0 + slot; r < r1; r += rpp) {
+      float fg[V], fy[V];
+      IoBf16::template load<V>(gin, r, C, gi * V, fg);
+      IoBf16::template load<V>(y, r, C, gi * V, fy);
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        a[0][j] += fg[j];
+        a[1][j] += fg[j] * fy[j];
+      }
+    }
+  }
+  cta_reduce_fix<2, V>(a, cg, rpp, C, acc);
+  if (!last_cta(ticket)) return;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const double sg = fix_take(acc + kFixWords * c);
+    const double sgy = fix_take(acc + kFixWords * (C + c));
+    const float mu = st[c], rs = st[C + c];
+    const float A = gamma[c] * rs;
+    const double sgx = static_cast<double>(rs) * (sgy - static_cast<double>(mu) * sg);
+    dbeta[c] = static_cast<float>(sg);
+    dgamma[c] = static_cast<float>(sgx);
+    const double k = static_cast<double>(A) / m;
+    coef[c] = static_cast<float>(-k * sgx * rs);
+    coef[C + c] = static_cast<float>(-k * (sg - sgx * rs * mu));
+  }
+}
+
 // -- SGD with momentum + bf16 shadow:  v = fmaf(mu, v, g); w = fmaf(-lr, v, w); ws = bf16(w)
 __global__ void sgd_kernel(float4* __restrict__ w, float4* __restrict__ v, const float4* __restrict__ g,
                            uint2* __restrict__ shadow, size_t n4, float lr, float mu, long long* counter) {
@@ -936,6 +1152,51 @@ int bn_bwd(const void* g, const void* y, const float* mean_rstd, const float* ga
         static_cast<float*>(dy));
     return ok(cudaGetLastError());
   }
+  bn_bwd_apply_kernel<8><<<apply_grid(m, t.rpp), kThreads, 0, st>>>(
+      static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(y), mean_rstd, gamma, red, m, c, t.cg,
+      t.rpp, static_cast<__nv_bfloat16*>(dy));
+  return ok(cudaGetLastError());
+}
+
+// ---- self-finalizing reductions (bf16 rows)
+size_t fix_acc_words(int c) { return (static_cast<size_t>(4) * c + 1) * kFixWords; }  // max over the four reductions
+
+int bn_stats_fix(const void* y0, const void* y1, int m, int c, FixScratch fx, float* mr0, float* mr1,
+                 cudaStream_t st) {
+  if (c % 8 != 0 || c / 8 > kThreads) return PBDK_EINVAL;
+  const RowTiling t = tiling_for(m, c, 8);
+  if (y1 != nullptr)
+    bn_stats_fix_kernel<8, 2><<<t.chunks, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(y0),
+                                                             static_cast<const __nv_bfloat16*>(y1), m, c,
+                                                             t.rows_per_chunk, t.cg, t.rpp, fx.acc, fx.ticket, mr0, mr1);
+  else
+    bn_stats_fix_kernel<8, 1><<<t.chunks, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(y0), nullptr, m, c,
+                                                             t.rows_per_chunk, t.cg, t.rpp, fx.acc, fx.ticket, mr0,
+                                                             nullptr);
+  return ok(cudaGetLastError());
+}
+
+int mse_bn_loss_fix(const MseArgs& a, FixScratch fx, cudaStream_t st) {
+  if (a.c % 8 != 0 || a.c / kLossApplyV > kThreads || a.prec != 0) return PBDK_EINVAL;
+  LossParams p{a.y2, a.ysc, a.t, a.stats2, a.statssc, a.gamma2, a.beta2, a.gammasc, a.betasc, a.m, a.c, a.gscale};
+  const RowTiling t = tiling_for(a.m, a.c, kLossPartialV, kLossChunks);
+  const LossOut o{a.norm, fx.acc, fx.ticket, a.red, a.dgamma2, a.dbeta2, a.dgammasc, a.dbetasc, a.loss};
+  loss_partial_fix_kernel<<<t.chunks, kThreads, 0, st>>>(p, t.rows_per_chunk, t.cg, t.rpp, o);
+  const RowTiling ta = tiling_for(a.m, a.c, kLossApplyV);
+  loss_bwd_apply_kernel<<<apply_grid(a.m, ta.rpp), kThreads, 0, st>>>(p, a.red, ta.cg, ta.rpp,
+                                                                      static_cast<__nv_bfloat16*>(a.dy2),
+                                                                      static_cast<__nv_bfloat16*>(a.dysc));
+  return ok(cudaGetLastError());
+}
+
+int bn_bwd_fix(const void* g, const void* y, const float* mean_rstd, const float* gamma, int m, int c, FixScratch fx,
+               float* red, float* dgamma, float* dbeta, void* dy, cudaStream_t st) {
+  if (c % 8 != 0 || c / 8 > kThreads) return PBDK_EINVAL;
+  const RowTiling t = tiling_for(m, c, 8);
+  bn_bwd_fix_partial_kernel<8><<<t.chunks, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(g),
+                                                              static_cast<const __nv_bfloat16*>(y), m, c,
+                                                              t.rows_per_chunk, t.cg, t.rpp, fx.acc, fx.ticket,
+                                                              mean_rstd, gamma, red, dgamma, dbeta);
   bn_bwd_apply_kernel<8><<<apply_grid(m, t.rpp), kThreads, 0, st>>>(
       static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(y), mean_rstd, gamma, red, m, c, t.cg,
       t.rpp, static_cast<__nv_bfloat16*>(dy));

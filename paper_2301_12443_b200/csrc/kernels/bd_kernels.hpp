@@ -67,6 +67,22 @@ int bn_bwd(const void* g, const void* y, const float* mean_rstd, const float* ga
            float* red, float* dgamma, float* dbeta, void* dy, cudaStream_t st, int prec = 0);
 int sgd_momentum(float* w, float* v, const float* g, void* shadow, size_t n, float lr, float mu, long long* counter,
                  cudaStream_t st);
+
+// ---- self-finalizing variants of bn_stats / bn_stats2 / mse_bn_loss / bn_bwd (bf16 rows): one partial
+// launch per reduction instead of partial + finalize.  Each CTA adds its chunk partial exactly into
+// fixed-point accumulators (fixacc.cuh); the last CTA to finish writes the same outputs the finalize
+// kernels wrote (mean/rstd, coefficients, parameter gradients, loss) and re-zeroes its scratch.
+// FixScratch: fix_acc_words(c) zero-initialised words + one zeroed ticket, per concurrent reduction.
+struct FixScratch {
+  unsigned long long* acc;
+  unsigned int* ticket;
+};
+size_t fix_acc_words(int c);
+int bn_stats_fix(const void* y0, const void* y1, int m, int c, FixScratch fx, float* mr0, float* mr1,
+                 cudaStream_t st);
+int mse_bn_loss_fix(const MseArgs& a, FixScratch fx, cudaStream_t st);
+int bn_bwd_fix(const void* g, const void* y, const float* mean_rstd, const float* gamma, int m, int c, FixScratch fx,
+               float* red, float* dgamma, float* dbeta, void* dy, cudaStream_t st);
 // the same update on g = g[0] + g[1] + ... (member order), the DP group's gradient slabs in peer memory
 int sgd_momentum_sum(float* w, float* v, const float* const* g, int count, void* shadow, size_t n, float lr, float mu,
                      long long* counter, cudaStream_t st);
