@@ -240,7 +240,7 @@ class ResNetPartition final : public PartitionBase {
       check(pbdk::fprop_run(s.p_conv1, st), "conv1");
       check(pbdk::fprop_run(s.p_sc, st), "shortcut");
       check(pbdk::bn_stats_fix(s.y1, nullptr, m, s.mid, s.fx[0], s.st1, nullptr, st), "bn1 stats");
-      check(pbdk::bn_apply_relu(s.y1, s.st1, p + s.lay.g1, p + s.lay.b1, s.a1, m, s.mid, st), "bn1 apply");
+      check(pbdk::bn_apply_relu_fix(s.y1, s.st1, p + s.lay.g1, p + s.lay.b1, s.a1, m, s.mid, st), "bn1 apply");
       check(pbdk::fprop_run(s.p_conv2, st), "conv2");
       check(pbdk::bn_stats_fix(s.y2, s.ys, m, s.cout, s.fx[1], s.st2, s.sts, st), "bn2/bnsc stats");
       const double norm = static_cast<double>(d_.global_batch) * s.cout * s.hout * s.hout;

@@ -750,34 +750,102 @@ __device__ __forceinline__ double fix_take(unsigned long long* p) {  // read a f
   return fix_value(v);
 }
 
+// ------------------------------------------------------------------ TMA-staged row streams
+// The student passes read [M][C] bf16 row ranges that are contiguous in HBM.  A CTA streams its range
+// through a kPipeStages-deep shared-memory ring filled by 1D bulk copies (one per input tensor and
+// tile of `tr` rows), so ~kPipeStages x kPipeStageBytes per SM are in flight instead of the handful of
+// 16-byte loads per thread the register loops kept outstanding (those ran at 0.5-2 TB/s, latency-bound
+// at one CTA per SM).  Thread (g, slot) visits rows r0 + slot + k*rpp in increasing order — the order
+// of the register loops, so the fp32 partials are unchanged.
+constexpr int kPipeStages = 4;
+constexpr int kPipeStageBytes = 24 * 1024;  // all inputs of one stage
+
+int pipe_tile_rows(int nin, int c, int rpp) {
+  const int rows = kPipeStageBytes / (nin * c * 2);
+  return std::max(rpp, rows / rpp * rpp);
+}
+size_t pipe_smem(int nin, int c, int tr) { return static_cast<size_t>(kPipeStages) * nin * tr * c * 2; }
+
+template <int NIN>
+struct PipeIn {
+  const __nv_bfloat16* p[NIN];
+};
+
+// f(row, s) with s[k] = this thread's V-channel group of row `row` of input k in shared memory.
+template <int NIN, int V, class F>
+__device__ __forceinline__ void row_pipe(const PipeIn<NIN>& in, int C, int r0, int r1, int tr, int g, int slot,
+                                         int rpp, F&& f) {
+  extern __shared__ __align__(128) uint8_t pipe_smem_raw[];
+  __shared__ uint64_t full[kPipeStages];
+  const int tile_elems = tr * C;
+  const int ntiles = r1 > r0 ? (r1 - r0 + tr - 1) / tr : 0;
+  __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(pipe_smem_raw);
+  auto issue = [&](int t) {
+    const int st = t % kPipeStages;
+    const int rows = min(tr, r1 - (r0 + t * tr));
+    const uint32_t bytes = static_cast<uint32_t>(rows) * C * 2;
+    mbar_arrive_expect_tx(&full[st], NIN * bytes);
+#pragma unroll
+    for (int k = 0; k < NIN; ++k)
+      bulk_load(ring + (st * NIN + k) * tile_elems, in.p[k] + static_cast<size_t>(r0 + t * tr) * C, bytes, &full[st]);
+  };
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kPipeStages; ++i) mbar_init(&full[i], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int t = 0; t < min(ntiles, kPipeStages); ++t) issue(t);
+  for (int t = 0; t < ntiles; ++t) {
+    const int st = t % kPipeStages;
+    mbar_wait(&full[st], (t / kPipeStages) & 1);
+    const int rows = min(tr, r1 - (r0 + t * tr));
+    if (slot < rpp) {
+      const __nv_bfloat16* s[NIN];
+#pragma unroll
+      for (int k = 0; k < NIN; ++k) s[k] = ring + (st * NIN + k) * tile_elems + g * V;
+#pragma unroll 2
+      for (int rr = slot; rr < rows; rr += rpp) {
+        const __nv_bfloat16* sr[NIN];
+#pragma unroll
+        for (int k = 0; k < NIN; ++k) sr[k] = s[k] + rr * C;
+        f(r0 + t * tr + rr, sr);
+      }
+    }
+    __syncthreads();  // stage st fully read before it is refilled
+    if (threadIdx.x == 0 && t + kPipeStages < ntiles) issue(t + kPipeStages);
+  }
+}
+
+template <int V>
+__device__ __forceinline__ void ld_smem(const __nv_bfloat16* p, float (&f)[V]) {
+  Vec<V>::load(p, f);
+}
+
 // -- BN statistics of NT same-shape tensors -> mean / rstd (bn_stats_finalize_kernel's arithmetic)
 template <int V, int NT>
-__global__ void __launch_bounds__(kThreads) bn_stats_fix_kernel(const __nv_bfloat16* __restrict__ y0,
-                                                                const __nv_bfloat16* __restrict__ y1, int m, int C,
-                                                                int rows_per_chunk, int cg, int rpp,
+__global__ void __launch_bounds__(kThreads) bn_stats_fix_kernel(const PipeIn<NT> in, int m, int C,
+                                                                int rows_per_chunk, int cg, int rpp, int tr,
                                                                 unsigned long long* __restrict__ acc,
                                                                 unsigned int* ticket, float* __restrict__ mr0,
                                                                 float* __restrict__ mr1) {
   const int g = threadIdx.x % cg;
   const int slot = threadIdx.x / cg;
   float a[2 * NT][V] = {};
-  if (slot < rpp) {
-    const int r0 = blockIdx.x * rows_per_chunk;
-    const int r1 = min(m, r0 + rows_per_chunk);
-#pragma unroll 4
-    for (int r = r0 + slot; r < r1; r += rpp) {
-      float f[NT][V];
-      IoBf16::template load<V>(y0, r, C, g * V, f[0]);
-      if (NT == 2) IoBf16::template load<V>(y1, r, C, g * V, f[NT - 1]);
+  const int r0 = blockIdx.x * rows_per_chunk;
+  row_pipe<NT, V>(in, C, r0, min(m, r0 + rows_per_chunk), tr, g, slot, rpp,
+                  [&](int, const __nv_bfloat16* const* s) {
 #pragma unroll
-      for (int t = 0; t < NT; ++t)
+                    for (int t = 0; t < NT; ++t) {
+                      float f[V];
+                      ld_smem<V>(s[t], f);
 #pragma unroll
-        for (int j = 0; j < V; ++j) {
-          a[2 * t][j] += f[t][j];
-          a[2 * t + 1][j] += f[t][j] * f[t][j];
-        }
-    }
-  }
+                      for (int j = 0; j < V; ++j) {
+                        a[2 * t][j] += f[j];
+                        a[2 * t + 1][j] += f[j] * f[j];
+                      }
+                    }
+                  });
   cta_reduce_fix<2 * NT, V>(a, cg, rpp, C, acc);  // acc[(2t + {0: sum, 1: sumsq}) * C + c]
   if (!last_cta(ticket)) return;
   for (int o = threadIdx.x; o < NT * C; o += blockDim.x) {
@@ -792,6 +860,36 @@ __global__ void __launch_bounds__(kThreads) bn_stats_fix_kernel(const __nv_bfloa
   }
 }
 
+// -- BN apply + ReLU (bn_apply_relu_kernel's arithmetic), staged
+template <int V>
+__global__ void __launch_bounds__(kThreads) bn_apply_relu_pipe_kernel(const PipeIn<1> in,
+                                                                      const float* __restrict__ mean_rstd,
+                                                                      const float* __restrict__ gamma,
+                                                                      const float* __restrict__ beta,
+                                                                      __nv_bfloat16* __restrict__ out, int m, int C,
+                                                                      int rows_per_chunk, int cg, int rpp, int tr) {
+  const int g = threadIdx.x % cg;
+  const int slot = threadIdx.x / cg;
+  const int c0 = g * V;
+  float A[V], B[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    A[j] = gamma[c0 + j] * mean_rstd[C + c0 + j];
+    B[j] = fmaf(-A[j], mean_rstd[c0 + j], beta[c0 + j]);
+  }
+  const int r0 = blockIdx.x * rows_per_chunk;
+  row_pipe<1, V>(in, C, r0, min(m, r0 + rows_per_chunk), tr, g, slot, rpp, [&](int r, const __nv_bfloat16* const* s) {
+    float f[V];
+    ld_smem<V>(s[0], f);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const float z = fmaf(A[j], f[j], B[j]);
+      f[j] = z > 0.0f ? z : 0.0f;
+    }
+    Vec<V>::store(out + static_cast<size_t>(r) * C + c0, f);
+  });
+}
+
 // -- loss partial sums (sum g, g*y2, g*ys per channel; sum (s-t)^2) -> coef / parameter gradients / loss
 struct LossOut {
   double norm;
@@ -802,36 +900,34 @@ struct LossOut {
   double* loss;
 };
 
-__global__ void __launch_bounds__(kThreads) loss_partial_fix_kernel(const LossParams p, int rows_per_chunk, int cg,
-                                                                    int rpp, const LossOut o) {
+__global__ void __launch_bounds__(kThreads) loss_partial_fix_kernel(const LossParams p, const PipeIn<3> in,
+                                                                    int rows_per_chunk, int cg, int rpp, int tr,
+                                                                    const LossOut o) {
   constexpr int V = kLossPartialV;
   const int gi = threadIdx.x % cg;
   const int slot = threadIdx.x / cg;
   float acc[3][V] = {};
   float lsum = 0.0f;
-  if (slot < rpp) {
-    float A2[V], As[V], Bz[V];
-    loss_affine<V>(p, gi * V, A2, As, Bz);
-    const int r0 = blockIdx.x * rows_per_chunk;
-    const int r1 = min(p.m, r0 + rows_per_chunk);
-#pragma unroll 4
-    for (int r = r0 + slot; r < r1; r += rpp) {
-      float y2[V], ys[V], t[V];
-      IoBf16::template load<V>(static_cast<const __nv_bfloat16*>(p.y2), r, p.C, gi * V, y2);
-      IoBf16::template load<V>(static_cast<const __nv_bfloat16*>(p.ys), r, p.C, gi * V, ys);
-      IoBf16::template load<V>(static_cast<const __nv_bfloat16*>(p.t), r, p.C, gi * V, t);
+  float A2[V], As[V], Bz[V];
+  loss_affine<V>(p, gi * V, A2, As, Bz);
+  const int r0 = blockIdx.x * rows_per_chunk;
+  row_pipe<3, V>(in, p.C, r0, min(p.m, r0 + rows_per_chunk), tr, gi, slot, rpp,
+                 [&](int, const __nv_bfloat16* const* s) {
+                   float y2[V], ys[V], t[V];
+                   ld_smem<V>(s[0], y2);
+                   ld_smem<V>(s[1], ys);
+                   ld_smem<V>(s[2], t);
 #pragma unroll
-      for (int j = 0; j < V; ++j) {
-        const float z = fmaf(A2[j], y2[j], fmaf(As[j], ys[j], Bz[j]));
-        const float d = (z > 0.0f ? z : 0.0f) - t[j];
-        const float g = z > 0.0f ? d * p.gscale : 0.0f;
-        lsum += d * d;
-        acc[0][j] += g;
-        acc[1][j] += g * y2[j];
-        acc[2][j] += g * ys[j];
-      }
-    }
-  }
+                   for (int j = 0; j < V; ++j) {
+                     const float z = fmaf(A2[j], y2[j], fmaf(As[j], ys[j], Bz[j]));
+                     const float d = (z > 0.0f ? z : 0.0f) - t[j];
+                     const float g = z > 0.0f ? d * p.gscale : 0.0f;
+                     lsum += d * d;
+                     acc[0][j] += g;
+                     acc[1][j] += g * y2[j];
+                     acc[2][j] += g * ys[j];
+                   }
+                 });
   __shared__ float lred[kThreads / 32];
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, off);
@@ -850,14 +946,14 @@ __global__ void __launch_bounds__(kThreads) loss_partial_fix_kernel(const LossPa
     const double sgy2 = fix_take(o.acc + kFixWords * (C + c));
     const double sgys = fix_take(o.acc + kFixWords * (2 * C + c));
     const float m2 = p.st2[c], r2 = p.st2[C + c], ms = p.sts[c], rs = p.sts[C + c];
-    const float A2 = p.g2[c] * r2, As = p.gs[c] * rs;
+    const float A2c = p.g2[c] * r2, Asc = p.gs[c] * rs;
     const double sgx2 = static_cast<double>(r2) * (sgy2 - static_cast<double>(m2) * sg);
     const double sgxs = static_cast<double>(rs) * (sgys - static_cast<double>(ms) * sg);
     o.db2[c] = static_cast<float>(sg);
     o.dbs[c] = static_cast<float>(sg);
     o.dg2[c] = static_cast<float>(sgx2);
     o.dgs[c] = static_cast<float>(sgxs);
-    const double c2 = static_cast<double>(A2) / p.m, cs = static_cast<double>(As) / p.m;
+    const double c2 = static_cast<double>(A2c) / p.m, cs = static_cast<double>(Asc) / p.m;
     o.coef[c] = static_cast<float>(-c2 * sgx2 * r2);
     o.coef[C + c] = static_cast<float>(-c2 * (sg - sgx2 * r2 * m2));
     o.coef[2 * C + c] = static_cast<float>(-cs * sgxs * rs);
@@ -866,11 +962,49 @@ __global__ void __launch_bounds__(kThreads) loss_partial_fix_kernel(const LossPa
   if (threadIdx.x == 0) *o.loss = fix_take(o.acc + kFixWords * 3 * C) / o.norm;
 }
 
+// -- dy2 / dys (loss_bwd_apply_kernel's arithmetic), staged
+__global__ void __launch_bounds__(kThreads) loss_bwd_apply_pipe_kernel(const LossParams p, const PipeIn<3> in,
+                                                                       const float* __restrict__ coef,
+                                                                       int rows_per_chunk, int cg, int rpp, int tr,
+                                                                       __nv_bfloat16* __restrict__ dy2,
+                                                                       __nv_bfloat16* __restrict__ dys) {
+  constexpr int V = kLossApplyV;
+  const int gi = threadIdx.x % cg;
+  const int slot = threadIdx.x / cg;
+  const int c0 = gi * V;
+  float A2[V], As[V], Bz[V], Q2[V], R2[V], Qs[V], Rs[V];
+  loss_affine<V>(p, c0, A2, As, Bz);
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    Q2[j] = coef[c0 + j];
+    R2[j] = coef[p.C + c0 + j];
+    Qs[j] = coef[2 * p.C + c0 + j];
+    Rs[j] = coef[3 * p.C + c0 + j];
+  }
+  const int r0 = blockIdx.x * rows_per_chunk;
+  row_pipe<3, V>(in, p.C, r0, min(p.m, r0 + rows_per_chunk), tr, gi, slot, rpp,
+                 [&](int r, const __nv_bfloat16* const* s) {
+                   float y2[V], ys[V], t[V], o2[V], os[V];
+                   ld_smem<V>(s[0], y2);
+                   ld_smem<V>(s[1], ys);
+                   ld_smem<V>(s[2], t);
+#pragma unroll
+                   for (int j = 0; j < V; ++j) {
+                     const float z = fmaf(A2[j], y2[j], fmaf(As[j], ys[j], Bz[j]));
+                     const float d = (z > 0.0f ? z : 0.0f) - t[j];
+                     const float g = z > 0.0f ? d * p.gscale : 0.0f;
+                     o2[j] = fmaf(A2[j], g, fmaf(Q2[j], y2[j], R2[j]));
+                     os[j] = fmaf(As[j], g, fmaf(Qs[j], ys[j], Rs[j]));
+                   }
+                   Vec<V>::store(dy2 + static_cast<size_t>(r) * p.C + c0, o2);
+                   Vec<V>::store(dys + static_cast<size_t>(r) * p.C + c0, os);
+                 });
+}
+
 // -- BN backward sums (sum g, sum g*y) -> coef [Q | R] and dgamma / dbeta (bn_bwd_finalize_kernel's arithmetic)
 template <int V>
-__global__ void __launch_bounds__(kThreads) bn_bwd_fix_partial_kernel(const __nv_bfloat16* __restrict__ gin,
-                                                                      const __nv_bfloat16* __restrict__ y, int m, int C,
-                                                                      int rows_per_chunk, int cg, int rpp,
+__global__ void __launch_bounds__(kThreads) bn_bwd_fix_partial_kernel(const PipeIn<2> in, int m, int C,
+                                                                      int rows_per_chunk, int cg, int rpp, int tr,
                                                                       unsigned long long* __restrict__ acc,
                                                                       unsigned int* ticket, const float* __restrict__ st,
                                                                       const float* __restrict__ gamma,
@@ -880,21 +1014,17 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_fix_partial_kernel(const __nv
   const int gi = threadIdx.x % cg;
   const int slot = threadIdx.x / cg;
   float a[2][V] = {};
-  if (slot < rpp) {
-    const int r0 = blockIdx.x * rows_per_chunk;
-    const int r1 = min(m, r0 + rows_per_chunk);
-#pragma unroll 4
-    for (int r = r0 + slot; r < r1; r += rpp) {
-      float fg[V], fy[V];
-      IoBf16::template load<V>(gin, r, C, gi * V, fg);
-      IoBf16::template load<V>(y, r, C, gi * V, fy);
+  const int r0 = blockIdx.x * rows_per_chunk;
+  row_pipe<2, V>(in, C, r0, min(m, r0 + rows_per_chunk), tr, gi, slot, rpp, [&](int, const __nv_bfloat16* const* s) {
+    float fg[V], fy[V];
+    ld_smem<V>(s[0], fg);
+    ld_smem<V>(s[1], fy);
 #pragma unroll
-      for (int j = 0; j < V; ++j) {
-        a[0][j] += fg[j];
-        a[1][j] += fg[j] * fy[j];
-      }
+    for (int j = 0; j < V; ++j) {
+      a[0][j] += fg[j];
+      a[1][j] += fg[j] * fy[j];
     }
-  }
+  });
   cta_reduce_fix<2, V>(a, cg, rpp, C, acc);
   if (!last_cta(ticket)) return;
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
@@ -909,6 +1039,34 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_fix_partial_kernel(const __nv
     coef[c] = static_cast<float>(-k * sgx * rs);
     coef[C + c] = static_cast<float>(-k * (sg - sgx * rs * mu));
   }
+}
+
+// -- dy = A*g + Q*y + R (bn_bwd_apply_kernel's arithmetic), staged
+template <int V>
+__global__ void __launch_bounds__(kThreads) bn_bwd_apply_pipe_kernel(const PipeIn<2> in, const float* __restrict__ st,
+                                                                     const float* __restrict__ gamma,
+                                                                     const float* __restrict__ coef, int m, int C,
+                                                                     int rows_per_chunk, int cg, int rpp, int tr,
+                                                                     __nv_bfloat16* __restrict__ dy) {
+  const int gi = threadIdx.x % cg;
+  const int slot = threadIdx.x / cg;
+  const int c0 = gi * V;
+  float A[V], Q[V], R[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    A[j] = gamma[c0 + j] * st[C + c0 + j];
+    Q[j] = coef[c0 + j];
+    R[j] = coef[C + c0 + j];
+  }
+  const int r0 = blockIdx.x * rows_per_chunk;
+  row_pipe<2, V>(in, C, r0, min(m, r0 + rows_per_chunk), tr, gi, slot, rpp, [&](int r, const __nv_bfloat16* const* s) {
+    float fg[V], fy[V], o[V];
+    ld_smem<V>(s[0], fg);
+    ld_smem<V>(s[1], fy);
+#pragma unroll
+    for (int j = 0; j < V; ++j) o[j] = fmaf(A[j], fg[j], fmaf(Q[j], fy[j], R[j]));
+    Vec<V>::store(dy + static_cast<size_t>(r) * C + c0, o);
+  });
 }
 
 // -- SGD with momentum + bf16 shadow:  v = fmaf(mu, v, g); w = fmaf(-lr, v, w); ws = bf16(w)
@@ -1161,46 +1319,108 @@ int bn_bwd(const void* g, const void* y, const float* mean_rstd, const float* ga
 // ---- self-finalizing reductions (bf16 rows)
 size_t fix_acc_words(int c) { return (static_cast<size_t>(4) * c + 1) * kFixWords; }  // max over the four reductions
 
+// grid of an elementwise staged pass: contiguous row chunks over apply_cap() CTAs (two per SM in the
+// ResNet step's GridScope; each keeps up to 96 KB of loads in flight)
+int apply_pipe_div() {  // PBDK_APPLY_PIPE_DIV: staged applies use apply_cap() / div CTAs (A/B runs)
+  static const int d = env_int("PBDK_APPLY_PIPE_DIV", 2);
+  return std::max(1, d);
+}
+bool apply_pipe() {  // PBDK_APPLY_PIPE=0: the register-loop apply kernels (A/B runs)
+  static const bool on = env_int("PBDK_APPLY_PIPE", 1) != 0;
+  return on;
+}
+RowTiling apply_tiling(int m, int c, int v) { return tiling_for(m, c, v, std::max(1, apply_cap() / apply_pipe_div())); }
+
+template <class K, class... Args>
+cudaError_t launch_pipe(K kernel, int grid, size_t smem, cudaStream_t st, Args... args) {
+  constexpr size_t kMax = 2 * kPipeStages * kPipeStageBytes;  // tiles rounded up to rpp rows stay below
+  if (smem > kMax) return cudaErrorInvalidValue;
+  static bool attr_set = false;  // per instantiation: opt in to > 48 KB of dynamic shared memory once
+  if (!attr_set) {
+    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(kMax));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  kernel<<<grid, kThreads, smem, st>>>(args...);
+  return cudaGetLastError();
+}
+
 int bn_stats_fix(const void* y0, const void* y1, int m, int c, FixScratch fx, float* mr0, float* mr1,
                  cudaStream_t st) {
   if (c % 8 != 0 || c / 8 > kThreads) return PBDK_EINVAL;
   const RowTiling t = tiling_for(m, c, 8);
+  const int nin = y1 != nullptr ? 2 : 1;
+  const int tr = pipe_tile_rows(nin, c, t.rpp);
+  const size_t smem = pipe_smem(nin, c, tr);
   if (y1 != nullptr)
-    bn_stats_fix_kernel<8, 2><<<t.chunks, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(y0),
-                                                             static_cast<const __nv_bfloat16*>(y1), m, c,
-                                                             t.rows_per_chunk, t.cg, t.rpp, fx.acc, fx.ticket, mr0, mr1);
-  else
-    bn_stats_fix_kernel<8, 1><<<t.chunks, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(y0), nullptr, m, c,
-                                                             t.rows_per_chunk, t.cg, t.rpp, fx.acc, fx.ticket, mr0,
-                                                             nullptr);
-  return ok(cudaGetLastError());
+    return ok(launch_pipe(bn_stats_fix_kernel<8, 2>, t.chunks, smem, st,
+                          PipeIn<2>{{static_cast<const __nv_bfloat16*>(y0), static_cast<const __nv_bfloat16*>(y1)}}, m,
+                          c, t.rows_per_chunk, t.cg, t.rpp, tr, fx.acc, fx.ticket, mr0, mr1));
+  return ok(launch_pipe(bn_stats_fix_kernel<8, 1>, t.chunks, smem, st,
+                        PipeIn<1>{{static_cast<const __nv_bfloat16*>(y0)}}, m, c, t.rows_per_chunk, t.cg, t.rpp, tr,
+                        fx.acc, fx.ticket, mr0, static_cast<float*>(nullptr)));
+}
+
+int bn_apply_relu_fix(const void* y, const float* mean_rstd, const float* gamma, const float* beta, void* a, int m,
+                      int c, cudaStream_t st) {
+  if (c % 8 != 0 || c / 8 > kThreads) return PBDK_EINVAL;
+  if (!apply_pipe()) return bn_apply_relu(y, mean_rstd, gamma, beta, a, m, c, st);
+  const RowTiling t = apply_tiling(m, c, 8);
+  const int tr = pipe_tile_rows(1, c, t.rpp);
+  return ok(launch_pipe(bn_apply_relu_pipe_kernel<8>, t.chunks, pipe_smem(1, c, tr), st,
+                        PipeIn<1>{{static_cast<const __nv_bfloat16*>(y)}}, mean_rstd, gamma, beta,
+                        static_cast<__nv_bfloat16*>(a), m, c, t.rows_per_chunk, t.cg, t.rpp, tr));
 }
 
 int mse_bn_loss_fix(const MseArgs& a, FixScratch fx, cudaStream_t st) {
   if (a.c % 8 != 0 || a.c / kLossApplyV > kThreads || a.prec != 0) return PBDK_EINVAL;
   LossParams p{a.y2, a.ysc, a.t, a.stats2, a.statssc, a.gamma2, a.beta2, a.gammasc, a.betasc, a.m, a.c, a.gscale};
+  const PipeIn<3> in{{static_cast<const __nv_bfloat16*>(a.y2), static_cast<const __nv_bfloat16*>(a.ysc),
+                      static_cast<const __nv_bfloat16*>(a.t)}};
   const RowTiling t = tiling_for(a.m, a.c, kLossPartialV, kLossChunks);
+  const int tr = pipe_tile_rows(3, a.c, t.rpp);
   const LossOut o{a.norm, fx.acc, fx.ticket, a.red, a.dgamma2, a.dbeta2, a.dgammasc, a.dbetasc, a.loss};
-  loss_partial_fix_kernel<<<t.chunks, kThreads, 0, st>>>(p, t.rows_per_chunk, t.cg, t.rpp, o);
-  const RowTiling ta = tiling_for(a.m, a.c, kLossApplyV);
-  loss_bwd_apply_kernel<<<apply_grid(a.m, ta.rpp), kThreads, 0, st>>>(p, a.red, ta.cg, ta.rpp,
-                                                                      static_cast<__nv_bfloat16*>(a.dy2),
-                                                                      static_cast<__nv_bfloat16*>(a.dysc));
-  return ok(cudaGetLastError());
+  cudaError_t e = launch_pipe(loss_partial_fix_kernel, t.chunks, pipe_smem(3, a.c, tr), st, p, in, t.rows_per_chunk,
+                              t.cg, t.rpp, tr, o);
+  if (e != cudaSuccess) return PBDK_ECUDA;
+  if (!apply_pipe()) {
+    const RowTiling ta = tiling_for(a.m, a.c, kLossApplyV);
+    loss_bwd_apply_kernel<<<apply_grid(a.m, ta.rpp), kThreads, 0, st>>>(p, a.red, ta.cg, ta.rpp,
+                                                                        static_cast<__nv_bfloat16*>(a.dy2),
+                                                                        static_cast<__nv_bfloat16*>(a.dysc));
+    return ok(cudaGetLastError());
+  }
+  const RowTiling ta = apply_tiling(a.m, a.c, kLossApplyV);
+  const int tra = pipe_tile_rows(3, a.c, ta.rpp);
+  e = launch_pipe(loss_bwd_apply_pipe_kernel, ta.chunks, pipe_smem(3, a.c, tra), st, p, in,
+                  static_cast<const float*>(a.red), ta.rows_per_chunk, ta.cg, ta.rpp, tra,
+                  static_cast<__nv_bfloat16*>(a.dy2), static_cast<__nv_bfloat16*>(a.dysc));
+  return ok(e);
 }
 
 int bn_bwd_fix(const void* g, const void* y, const float* mean_rstd, const float* gamma, int m, int c, FixScratch fx,
                float* red, float* dgamma, float* dbeta, void* dy, cudaStream_t st) {
   if (c % 8 != 0 || c / 8 > kThreads) return PBDK_EINVAL;
+  const PipeIn<2> in{{static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(y)}};
   const RowTiling t = tiling_for(m, c, 8);
-  bn_bwd_fix_partial_kernel<8><<<t.chunks, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(g),
-                                                              static_cast<const __nv_bfloat16*>(y), m, c,
-                                                              t.rows_per_chunk, t.cg, t.rpp, fx.acc, fx.ticket,
-                                                              mean_rstd, gamma, red, dgamma, dbeta);
-  bn_bwd_apply_kernel<8><<<apply_grid(m, t.rpp), kThreads, 0, st>>>(
-      static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(y), mean_rstd, gamma, red, m, c, t.cg,
-      t.rpp, static_cast<__nv_bfloat16*>(dy));
-  return ok(cudaGetLastError());
+  const int tr = pipe_tile_rows(2, c, t.rpp);
+  cudaError_t e = launch_pipe(bn_bwd_fix_partial_kernel<8>, t.chunks, pipe_smem(2, c, tr), st, in, m, c,
+                              t.rows_per_chunk, t.cg, t.rpp, tr, fx.acc, fx.ticket, mean_rstd, gamma, red, dgamma,
+                              dbeta);
+  if (e != cudaSuccess) return PBDK_ECUDA;
+  if (!apply_pipe()) {
+    bn_bwd_apply_kernel<8><<<apply_grid(m, t.rpp), kThreads, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(y), mean_rstd, gamma, red, m, c, t.cg,
+        t.rpp, static_cast<__nv_bfloat16*>(dy));
+    return ok(cudaGetLastError());
+  }
+  const RowTiling ta = apply_tiling(m, c, 8);
+  const int tra = pipe_tile_rows(2, c, ta.rpp);
+  e = launch_pipe(bn_bwd_apply_pipe_kernel<8>, ta.chunks, pipe_smem(2, c, tra), st, in, mean_rstd, gamma,
+                  static_cast<const float*>(red), m, c, ta.rows_per_chunk, ta.cg, ta.rpp, tra,
+                  static_cast<__nv_bfloat16*>(dy));
+  return ok(e);
 }
 
 int sgd_momentum(float* w, float* v, const float* g, void* shadow, size_t n, float lr, float mu, long long* counter,

@@ -69,7 +69,8 @@ int sgd_momentum(float* w, float* v, const float* g, void* shadow, size_t n, flo
                  cudaStream_t st);
 
 // ---- self-finalizing variants of bn_stats / bn_stats2 / mse_bn_loss / bn_bwd (bf16 rows): one partial
-// launch per reduction instead of partial + finalize.  Each CTA adds its chunk partial exactly into
+// launch per reduction instead of partial + finalize; every pass streams its rows through a TMA-staged
+// shared-memory ring (bd_kernels.cu row_pipe).  Each CTA adds its chunk partial exactly into
 // fixed-point accumulators (fixacc.cuh); the last CTA to finish writes the same outputs the finalize
 // kernels wrote (mean/rstd, coefficients, parameter gradients, loss) and re-zeroes its scratch.
 // FixScratch: fix_acc_words(c) zero-initialised words + one zeroed ticket, per concurrent reduction.
@@ -80,6 +81,8 @@ struct FixScratch {
 size_t fix_acc_words(int c);
 int bn_stats_fix(const void* y0, const void* y1, int m, int c, FixScratch fx, float* mr0, float* mr1,
                  cudaStream_t st);
+int bn_apply_relu_fix(const void* y, const float* mean_rstd, const float* gamma, const float* beta, void* a, int m,
+                      int c, cudaStream_t st);  // the same arithmetic as bn_apply_relu, TMA-staged rows
 int mse_bn_loss_fix(const MseArgs& a, FixScratch fx, cudaStream_t st);
 int bn_bwd_fix(const void* g, const void* y, const float* mean_rstd, const float* gamma, int m, int c, FixScratch fx,
                float* red, float* dgamma, float* dbeta, void* dy, cudaStream_t st);
