@@ -551,10 +551,12 @@ def run_ours_mbv2(args, dev, local_rank):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (Philox4x32-10 images on device each step; random-init weights)",
-            "config": {"workload": ("mbv2-teacher/proxyless-supernet 6 blocks, IR point on 1 GPU (configs[2] shape)"
+            "config": {"workload": ("MobileNetV2-1.0 teacher (true widths 24/32/64/96/160/320, stored zero-padded "
+                                    "to tile multiples) / ProxylessNAS supernet, 6 blocks, IR point on 1 GPU "
+                                    "(configs[2])"
                                     if model == "mbv2" else
-                                    "effb0-teacher(swish,SE)/proxyless-supernet 6 blocks, IR point on 1 GPU "
-                                    "(configs[3] shape)"),
+                                    "EfficientNet-B0 teacher (swish, SE; true widths 24/40/80/112/192/320, stored "
+                                    "zero-padded) / ProxylessNAS supernet, 6 blocks, IR point on 1 GPU (configs[3])"),
                        "global_batch": b, "image": f"{S}x{S}x3", "blocks": 6, "paths": paths,
                        "parallelism": "ir1 (blocks 0-5 on 1 GPU)", "cuda_graph": True,
                        "l2": "no flush: per-step working set > 20 GiB >> 126 MB L2"},

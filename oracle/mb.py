@@ -29,7 +29,7 @@ def lib():
             subprocess.run(["make", "-C", HERE, "oracle"], check=True, capture_output=True)
         L = ctypes.CDLL(LIB)
         I, S, U, D = ctypes.c_int, ctypes.c_size_t, ctypes.c_uint32, ctypes.c_double
-        for f in ("mbo_channels", "mbo_student_layers"):
+        for f in ("mbo_channels", "mbo_true_channels", "mbo_student_layers"):
             getattr(L, f).argtypes = [I]
             getattr(L, f).restype = I
         L.mbo_hw.argtypes = [I, I]
@@ -65,7 +65,13 @@ FAMILY = 0
 
 
 def channels(b: int) -> int:
+    """stored channels at boundary b (tensor-tile granularity)"""
     return lib().mbo_channels(b)
+
+
+def true_channels(b: int) -> int:
+    """the architecture's channels at boundary b (the stored extra channels are identically zero)"""
+    return lib().mbo_true_channels(b)
 
 
 def hw(b: int, S: int) -> int:
@@ -164,7 +170,7 @@ class Trainer:
             acts.append(teacher_fwd(k, self.tp[k], acts[-1], self.S, self.bf16))
         losses = {}
         for k in self.blocks:
-            c, hh = channels(k + 1), hw(k + 1, self.S)
+            c, hh = true_channels(k + 1), hw(k + 1, self.S)
             norm = float(self.b) * c * hh * hh
             g_total = np.zeros_like(self.sp[k])
             loss = 0.0
@@ -188,6 +194,7 @@ class Trainer:
 KS, ES = (3, 5, 7), (3, 6)
 NLF = ((3, 3, 4, 3, 3, 1), (3, 2, 3, 3, 4, 1))
 CHF = ((3, 32, 32, 64, 128, 192, 320), (3, 32, 64, 128, 128, 192, 320))
+CTF = ((3, 24, 32, 64, 96, 160, 320), (3, 24, 40, 80, 112, 192, 320))  # true widths
 KF = ((3, 3, 3, 3, 3, 3), (3, 5, 3, 5, 5, 3))
 DIV = (1, 4, 8, 16, 16, 32, 32)
 
@@ -205,6 +212,7 @@ class _FamTable:
 
 NL = _FamTable(NLF)
 CH = _FamTable(CHF)
+CT = _FamTable(CTF)
 
 
 def se_ch(cin: int) -> int:
@@ -216,26 +224,34 @@ def round_ch(c: int) -> int:
 
 
 def teacher_layer(b: int, l: int):
-    """(t, k, cin, cout, stride) of teacher MBConv layer l of block b."""
+    """(t, k, cin, cout, stride) of teacher MBConv layer l of block b (stored widths)."""
+    return teacher_layer_t(b, l)[:5]
+
+
+def teacher_layer_t(b: int, l: int):
+    """(t, k, cin, cout, stride, cin_true, cout_true)."""
     if b == 0:
-        return ((1, 3, 32, 16, 1), (6, 3, 16, 32, 2), (6, 3, 32, 32, 1))[l]
+        return ((1, 3, 32, 16, 1, 32, 16), (6, 3, 16, 32, 2, 16, 24), (6, 3, 32, 32, 1, 24, 24))[l]
     cin, cout = CH[b], CH[b + 1]
     s = DIV[b + 1] // DIV[b]
     k = KF[FAMILY][b]
-    return (6, k, cin, cout, s) if l == 0 else (6, k, cout, cout, 1)
+    return (6, k, cin, cout, s, CT[b], CT[b + 1]) if l == 0 else (6, k, cout, cout, 1, CT[b + 1], CT[b + 1])
 
 
 def student_layer(b: int, l: int, c: int):
-    """dict(kind, k, e, E, cin, cout, stride, res) of candidate c of student layer l."""
+    """dict(kind, k, e, E, cin, cout, stride, res, Et, cin_t, cout_t) of candidate c of student layer l
+    (stored widths E / cin / cout, true widths *_t; residual by the true widths)."""
     if b == 0 and l == 0:
-        return dict(kind="stem", k=3, e=0, E=32, cin=3, cout=32, stride=2, res=False)
-    t, _, cin, cout, s = teacher_layer(b, l - 1 if b == 0 else l)
+        return dict(kind="stem", k=3, e=0, E=32, cin=3, cout=32, stride=2, res=False, Et=32, cin_t=3, cout_t=32)
+    t, _, cin, cout, s, cin_t, cout_t = teacher_layer_t(b, l - 1 if b == 0 else l)
     if b == 0 and l == 1:
         k, e = 3, 1
     else:
         k, e = KS[c % 3], ES[c // 3]
     E = cin if e == 1 else round_ch(cin * e)
-    return dict(kind="mb", k=k, e=e, E=E, cin=cin, cout=cout, stride=s, res=(s == 1 and cin == cout))
+    Et = cin_t if e == 1 else cin_t * e
+    return dict(kind="mb", k=k, e=e, E=E, cin=cin, cout=cout, stride=s, res=(s == 1 and cin_t == cout_t), Et=Et,
+                cin_t=cin_t, cout_t=cout_t)
 
 
 def candidate_layout(b: int, l: int, c: int) -> Dict[str, tuple]:

@@ -20,15 +20,22 @@ static inline int mask6(float a) { return a > 0.0f && a < 6.0f; }
 
 /* ------------------------------------------------------------------ architecture */
 typedef struct {
-  int t, k, cin, cout, stride; /* teacher: expansion t (1 = no expand conv), kernel k */
+  int t, k, cin, cout, stride; /* teacher: expansion t (1 = no expand conv), kernel k; stored widths */
+  int cin_t, cout_t;           /* the architecture's true widths (<= stored; the rest are zero channels) */
 } mb_layer;
 
 /* teacher families: 0 = MobileNetV2 (ReLU6), 1 = EfficientNet-B0 (swish + squeeze-excite) */
 static int FAM = 0;
+/* boundary widths: stored (tensor-tile granularity) and true (MobileNetV2-1.0 / EfficientNet-B0).
+ * Channels beyond the true width are stored but identically zero: their weights are initialised to
+ * zero and receive zero gradients, so the model computed is exactly the true-width network
+ * (DESIGN.md §10). */
 static const int CHF[2][7] = {{3, 32, 32, 64, 128, 192, 320}, {3, 32, 64, 128, 128, 192, 320}};
+static const int CTF[2][7] = {{3, 24, 32, 64, 96, 160, 320}, {3, 24, 40, 80, 112, 192, 320}};
 static const int NLF[2][6] = {{3, 3, 4, 3, 3, 1}, {3, 2, 3, 3, 4, 1}}; /* teacher MBConv layers per block */
 static const int KF[2][6] = {{3, 3, 3, 3, 3, 3}, {3, 5, 3, 5, 5, 3}};  /* teacher kernel per block */
 #define CH (CHF[FAM])
+#define CT (CTF[FAM])
 #define NL (NLF[FAM])
 static const int DIV[7] = {1, 4, 8, 16, 16, 32, 32};
 
@@ -36,7 +43,7 @@ void mbo_set_family(int f) { FAM = (f == 1) ? 1 : 0; }
 int mbo_family(void) { return FAM; }
 
 static int teacher_layer(int b, int l, mb_layer* o) {
-  static const mb_layer B0[3] = {{1, 3, 32, 16, 1}, {6, 3, 16, 32, 2}, {6, 3, 32, 32, 1}};
+  static const mb_layer B0[3] = {{1, 3, 32, 16, 1, 32, 16}, {6, 3, 16, 32, 2, 16, 24}, {6, 3, 32, 32, 1, 24, 24}};
   if (l < 0 || l >= NL[b]) return 0;
   if (b == 0) {
     *o = B0[l];
@@ -45,12 +52,15 @@ static int teacher_layer(int b, int l, mb_layer* o) {
   const int cin = CH[b], cout = CH[b + 1];
   const int s = DIV[b + 1] / DIV[b];
   const int k = KF[FAM][b];
-  *o = l == 0 ? (mb_layer){6, k, cin, cout, s} : (mb_layer){6, k, cout, cout, 1};
+  *o = l == 0 ? (mb_layer){6, k, cin, cout, s, CT[b], CT[b + 1]} : (mb_layer){6, k, cout, cout, 1, CT[b + 1], CT[b + 1]};
   return 1;
 }
 
-/* squeeze-excite width of an EfficientNet layer (0.25 x the layer's input channels) */
+/* squeeze-excite width of an EfficientNet layer (0.25 x the layer's input channels): stored / true */
 static int se_ch(const mb_layer* m) { return FAM == 1 ? (m->cin / 4 > 0 ? m->cin / 4 : 1) : 0; }
+static int se_ch_t(const mb_layer* m) { return FAM == 1 ? (m->cin_t / 4 > 0 ? m->cin_t / 4 : 1) : 0; }
+/* a residual joins input and output when the stride is 1 and the TRUE widths agree */
+static int has_res(const mb_layer* m) { return m->stride == 1 && m->cin_t == m->cout_t; }
 static inline float swishf(float z) { return z / (1.0f + expf(-z)); }
 static inline float sigmoidf(float z) { return 1.0f / (1.0f + expf(-z)); }
 /* the teacher's activation: ReLU6 (MobileNetV2) or swish (EfficientNet-B0) */
@@ -61,8 +71,10 @@ static inline float tact(float z) {
 
 static int round_ch(int c) { return c <= 16 ? 16 : c <= 32 ? 32 : (c + 63) / 64 * 64; }
 static int expand_ch(int cin, int t) { return t == 1 ? cin : round_ch(cin * t); }
+static int expand_ch_t(int cin_t, int t) { return t == 1 ? cin_t : cin_t * t; }
 
 int mbo_channels(int b) { return CH[b]; }
+int mbo_true_channels(int b) { return CT[b]; }
 int mbo_hw(int b, int S) { return S / DIV[b]; }
 
 /* student layers: block 0 = [stem, MBConv1 (fixed), searchable...]; others all searchable */
@@ -90,6 +102,7 @@ static mb_layer student_mb(int b, int l) {
 typedef struct {
   size_t we, wd, wp, g1, b1, g2, b2, g3, b3, total;
   int E, k, e;
+  int Et; /* true expanded width */
 } cand_layout;
 
 static cand_layout cand_lay(int b, int l, int c) {
@@ -101,6 +114,7 @@ static cand_layout cand_lay(int b, int l, int c) {
     L.b2 = L.g2 + 32;
     L.total = L.b2 + 32;
     L.E = 32;
+    L.Et = 32;
     L.k = 3;
     L.e = 0;
     return L;
@@ -108,6 +122,7 @@ static cand_layout cand_lay(int b, int l, int c) {
   const mb_layer m = student_mb(b, l);
   cand_ke(b, l, c, &L.k, &L.e);
   L.E = expand_ch(m.cin, L.e);
+  L.Et = expand_ch_t(m.cin_t, L.e);
   size_t o = 0;
   if (L.e != 1) {
     L.we = o;
@@ -185,15 +200,16 @@ void mbo_input(int n, int64_t first, int S, uint32_t seed, float* out, int bf16)
     }
 }
 
-/* dst[k][r][s][cs] = c < ct ? U(-1,1)*bound : 0, Philox counter (flat unpadded index, tensor id) —
- * the product's pbdk_init_uniform */
-static void fill(float* dst, int K, int R, int cs, int ct, uint32_t seed, uint32_t tid, float bound, int bf16) {
+/* dst[k][r][s][cs] = (k < kt && c < ct) ? U(-1,1)*bound : 0, Philox counter (flat index of the true
+ * [kt][r][s][ct] tensor, tensor id) — the product's pbdk_init_uniform */
+static void fill(float* dst, int K, int kt, int R, int cs, int ct, uint32_t seed, uint32_t tid, float bound,
+                 int bf16) {
   const uint32_t key[2] = {seed, 0xB200B200u};
   for (int k = 0; k < K; ++k)
     for (int rs = 0; rs < R * R; ++rs)
       for (int c = 0; c < cs; ++c) {
         float v = 0.0f;
-        if (c < ct) {
+        if (k < kt && c < ct) {
           const uint32_t i = (uint32_t)(((size_t)k * R * R + rs) * ct + c);
           const uint32_t ctr[4] = {i, tid, 0u, 0u};
           uint32_t o[4];
@@ -210,46 +226,46 @@ static float kaiming(int fan_in, float gain) { return sqrtf(6.0f / (float)fan_in
 void mbo_teacher_init(int b, uint32_t seed, float* p, int bf16) {
   int j = 0;
   if (b == 0) {
-    fill(p, 32, 3, 16, 3, seed, 20000u + 10u * j, kaiming(27, 1.0f), bf16);
+    fill(p, 32, 32, 3, 16, 3, seed, 20000u + 10u * j, kaiming(27, 1.0f), bf16);
     p += 32 * 9 * 16;
-    fill(p, 32, 1, 1, 1, seed, 20000u + 10u * j + 1u, 0.1f, 0);
+    fill(p, 32, 32, 1, 1, 1, seed, 20000u + 10u * j + 1u, 0.1f, 0);
     p += 32;
     ++j;
   }
   for (int l = 0; l < NL[b]; ++l) {
     mb_layer m;
     teacher_layer(b, l, &m);
-    const int E = expand_ch(m.cin, m.t);
+    const int E = expand_ch(m.cin, m.t), Et = expand_ch_t(m.cin_t, m.t);
     const uint32_t base = 20000u + 1000u * (uint32_t)b;
     if (m.t != 1) {
-      fill(p, E, 1, m.cin, m.cin, seed, base + 10u * j, kaiming(m.cin, 1.0f), bf16);
+      fill(p, E, Et, 1, m.cin, m.cin_t, seed, base + 10u * j, kaiming(m.cin_t, 1.0f), bf16);
       p += (size_t)E * m.cin;
-      fill(p, E, 1, 1, 1, seed, base + 10u * j + 1u, 0.1f, 0);
+      fill(p, E, Et, 1, 1, 1, seed, base + 10u * j + 1u, 0.1f, 0);
       p += E;
       ++j;
     }
-    fill(p, E, m.k, 1, 1, seed, base + 10u * j, kaiming(m.k * m.k, 1.0f), bf16);
+    fill(p, E, Et, m.k, 1, 1, seed, base + 10u * j, kaiming(m.k * m.k, 1.0f), bf16);
     p += (size_t)E * m.k * m.k;
-    fill(p, E, 1, 1, 1, seed, base + 10u * j + 1u, 0.1f, 0);
+    fill(p, E, Et, 1, 1, 1, seed, base + 10u * j + 1u, 0.1f, 0);
     p += E;
     ++j;
-    const int cs = se_ch(&m);
+    const int cs = se_ch(&m), cst = se_ch_t(&m);
     if (cs) { /* squeeze-excite: W1 [cs][E] + b1, W2 [E][cs] + b2 */
-      fill(p, cs, 1, E, E, seed, base + 10u * j, kaiming(E, 1.0f), bf16);
+      fill(p, cs, cst, 1, E, Et, seed, base + 10u * j, kaiming(Et, 1.0f), bf16);
       p += (size_t)cs * E;
-      fill(p, cs, 1, 1, 1, seed, base + 10u * j + 1u, 0.1f, 0);
+      fill(p, cs, cst, 1, 1, 1, seed, base + 10u * j + 1u, 0.1f, 0);
       p += cs;
       ++j;
-      fill(p, E, 1, cs, cs, seed, base + 10u * j, kaiming(cs, 1.0f), bf16);
+      fill(p, E, Et, 1, cs, cst, seed, base + 10u * j, kaiming(cst, 1.0f), bf16);
       p += (size_t)E * cs;
-      fill(p, E, 1, 1, 1, seed, base + 10u * j + 1u, 0.1f, 0);
+      fill(p, E, Et, 1, 1, 1, seed, base + 10u * j + 1u, 0.1f, 0);
       p += E;
       ++j;
     }
-    const int res = m.stride == 1 && m.cin == m.cout;
-    fill(p, m.cout, 1, E, E, seed, base + 10u * j, kaiming(E, res ? 0.5f : 1.0f), bf16);
+    const int res = has_res(&m);
+    fill(p, m.cout, m.cout_t, 1, E, Et, seed, base + 10u * j, kaiming(Et, res ? 0.5f : 1.0f), bf16);
     p += (size_t)m.cout * E;
-    fill(p, m.cout, 1, 1, 1, seed, base + 10u * j + 1u, 0.1f, 0);
+    fill(p, m.cout, m.cout_t, 1, 1, 1, seed, base + 10u * j + 1u, 0.1f, 0);
     p += m.cout;
     ++j;
   }
@@ -263,7 +279,7 @@ void mbo_student_init(int b, uint32_t seed, float* p) {
       float* q = p + mbo_candidate_offset(b, l, c, NULL);
       const uint32_t tid = 40000u + 1000u * (uint32_t)b + 100u * (uint32_t)l + 10u * (uint32_t)c;
       if (b == 0 && l == 0) {
-        fill(q, 32, 3, 16, 3, seed, tid, kaiming(27, 1.0f), 0);
+        fill(q, 32, 32, 3, 16, 3, seed, tid, kaiming(27, 1.0f), 0);
         for (int i = 0; i < 32; ++i) {
           q[L.g2 + i] = 1.0f;
           q[L.b2 + i] = 0.0f;
@@ -271,9 +287,9 @@ void mbo_student_init(int b, uint32_t seed, float* p) {
         continue;
       }
       const mb_layer m = student_mb(b, l);
-      if (L.e != 1) fill(q + L.we, L.E, 1, m.cin, m.cin, seed, tid, kaiming(m.cin, 1.0f), 0);
-      fill(q + L.wd, L.E, L.k, 1, 1, seed, tid + 1u, kaiming(L.k * L.k, 1.0f), 0);
-      fill(q + L.wp, m.cout, 1, L.E, L.E, seed, tid + 2u, kaiming(L.E, 1.0f), 0);
+      if (L.e != 1) fill(q + L.we, L.E, L.Et, 1, m.cin, m.cin_t, seed, tid, kaiming(m.cin_t, 1.0f), 0);
+      fill(q + L.wd, L.E, L.Et, L.k, 1, 1, seed, tid + 1u, kaiming(L.k * L.k, 1.0f), 0);
+      fill(q + L.wp, m.cout, m.cout_t, 1, L.E, L.Et, seed, tid + 2u, kaiming(L.Et, 1.0f), 0);
       for (int i = 0; i < L.E; ++i) {
         if (L.e != 1) {
           q[L.g1 + i] = 1.0f;
@@ -562,7 +578,7 @@ int mbo_teacher_fwd(int b, const float* tp, int n, int S, const float* in, float
     if (cs) se_apply(e2, n, P * P, E, cs, tp, bf16);
     if (cs) tp += (size_t)cs * E + cs + (size_t)E * cs + E;
     conv1x1(e2, (size_t)n * P * P, E, tp, m.cout, o);
-    const int res = m.stride == 1 && m.cin == m.cout;
+    const int res = has_res(&m);
     bias_act(o, (size_t)n * P * P, m.cout, tp + (size_t)m.cout * E, res ? x : NULL, 0, bf16);
     tp += (size_t)m.cout * E + m.cout;
     memcpy(x, o, sizeof(float) * (size_t)n * P * P * m.cout);
@@ -712,7 +728,7 @@ int mbo_student_fwd_bwd(int b, const float* sp, const int* path, int n, int S, c
     s->k = s->L.k;
     s->e = s->L.e;
     s->P = (H + 2 * (s->k / 2) - s->k) / s->stride + 1;
-    s->res = m.stride == 1 && m.cin == m.cout;
+    s->res = has_res(&m);
     const size_t off = mbo_candidate_offset(b, l, path[l], NULL);
     s->p = sp + off;
     s->gr = grads + off;

@@ -9,8 +9,9 @@
  * There is no executable reference for this path (SPEC.md:15 excludes training):
  * it restates Algorithm 1 with the block pairs of PAPER.md:192-194, the
  * ProxylessNAS supernet + MobileNetV2 teacher of PAPER.md:409-414 (Table 2 row, :533-534), SGD as PAPER.md:428-429.  The
- * tensor shapes are ours (the reference defines none): MobileNetV2-1.0 topology with
- * channel widths rounded to the tensor-tile granularity.  Numerics contract =
+ * tensor shapes are ours (the reference defines none): MobileNetV2-1.0 / EfficientNet-B0
+ * with their true channel widths, stored rounded up to the tensor-tile granularity with the extra
+ * channels identically zero (zero weights, zero gradients).  Numerics contract =
  * the GPU path and this oracle round to bf16 at the same points; depthwise and stem
  * convolutions accumulate in the same fmaf order on both sides, 1x1 convolutions (tensor cores)
  * differ only in fp32 accumulation order.  Deterministic for any OpenMP thread count.
@@ -35,7 +36,8 @@ void mbo_set_family(int family);
 int mbo_family(void);
 
 /* geometry (image side S, e.g. 224): boundary b in 0..6 (0 = the image, stored as 16 channels) */
-int mbo_channels(int boundary);                 /* 3, 32, 32, 64, 128, 192, 320 */
+int mbo_channels(int boundary);                 /* stored: 3, 32, 32, 64, 128, 192, 320 */
+int mbo_true_channels(int boundary);            /* the architecture's: 3, 24, 32, 64, 96, 160, 320 (MBv2) */
 int mbo_hw(int boundary, int S);                /* S, S/4, S/8, S/16, S/16, S/32, S/32 */
 int mbo_student_layers(int block);              /* incl. block 0's stem and fixed MBConv1 */
 int mbo_layer_candidates(int block, int layer); /* 1 (fixed) or MBO_CANDIDATES */

@@ -42,16 +42,21 @@ constexpr int DIV[7] = {1, 4, 8, 16, 16, 32, 32};
 
 // Teacher families: MobileNetV2 (ReLU6; configs[2]) and EfficientNet-B0 (swish,
 // squeeze-excite, k5 stages; configs[3]); the student is the same ProxylessNAS supernet over the
-// family's block / layer structure.  Channel widths rounded to the tensor-tile granularity.
+// family's block / layer structure.  Channels are stored rounded up to the tensor-tile granularity
+// (CH); the architecture's true widths (CT) are the only non-zero ones — the extra stored channels
+// have zero weights and receive zero gradients, so the network computed is the true-width one.
 struct Family {
   int CH[7];
+  int CT[7];
   int NL[6];
   int K[6];
   int act;  // teacher activation code (mb_kernels.hpp): 1 ReLU6, 2 swish
   bool se;  // squeeze-excite in every teacher MBConv
 };
-constexpr Family kMbv2{{3, 32, 32, 64, 128, 192, 320}, {3, 3, 4, 3, 3, 1}, {3, 3, 3, 3, 3, 3}, 1, false};
-constexpr Family kEffb0{{3, 32, 64, 128, 128, 192, 320}, {3, 2, 3, 3, 4, 1}, {3, 5, 3, 5, 5, 3}, 2, true};
+constexpr Family kMbv2{{3, 32, 32, 64, 128, 192, 320}, {3, 24, 32, 64, 96, 160, 320}, {3, 3, 4, 3, 3, 1},
+                      {3, 3, 3, 3, 3, 3}, 1, false};
+constexpr Family kEffb0{{3, 32, 64, 128, 128, 192, 320}, {3, 24, 40, 80, 112, 192, 320}, {3, 2, 3, 3, 4, 1},
+                       {3, 5, 3, 5, 5, 3}, 2, true};
 const Family& family(int model) { return model == PBDX_MODEL_EFFB0_PROXYLESS ? kEffb0 : kMbv2; }
 
 // the family in effect for the layout helpers below (set by every public entry point)
@@ -62,24 +67,30 @@ struct FamScope {
   ~FamScope() { g_fam = prev; }
 };
 #define CH (g_fam->CH)
+#define CT (g_fam->CT)
 #define NL (g_fam->NL)
 
 struct MbLayer {
-  int t, k, cin, cout, stride;
+  int t, k, cin, cout, stride;  // stored widths
+  int cin_t, cout_t;            // true widths
 };
 
 MbLayer teacher_layer(int b, int l) {
-  static const MbLayer B0[3] = {{1, 3, 32, 16, 1}, {6, 3, 16, 32, 2}, {6, 3, 32, 32, 1}};
+  static const MbLayer B0[3] = {{1, 3, 32, 16, 1, 32, 16}, {6, 3, 16, 32, 2, 16, 24}, {6, 3, 32, 32, 1, 24, 24}};
   if (b == 0) return B0[l];
   const int cin = CH[b], cout = CH[b + 1];
   const int s = DIV[b + 1] / DIV[b];
   const int k = g_fam->K[b];
-  return l == 0 ? MbLayer{6, k, cin, cout, s} : MbLayer{6, k, cout, cout, 1};
+  return l == 0 ? MbLayer{6, k, cin, cout, s, CT[b], CT[b + 1]} : MbLayer{6, k, cout, cout, 1, CT[b + 1], CT[b + 1]};
 }
 
 int se_ch(const MbLayer& m) { return g_fam->se ? std::max(1, m.cin / 4) : 0; }
+int se_ch_t(const MbLayer& m) { return g_fam->se ? std::max(1, m.cin_t / 4) : 0; }
 int round_ch(int c) { return c <= 16 ? 16 : c <= 32 ? 32 : (c + 63) / 64 * 64; }
 int expand_ch(int cin, int t) { return t == 1 ? cin : round_ch(cin * t); }
+int expand_ch_t(int cin_t, int t) { return t == 1 ? cin_t : cin_t * t; }
+// a residual joins input and output when the stride is 1 and the TRUE widths agree
+bool has_res(const MbLayer& m) { return m.stride == 1 && m.cin_t == m.cout_t; }
 int student_layers(int b) { return NL[b] + (b == 0 ? 1 : 0); }
 int layer_cands(int b, int l) { return (b == 0 && l < 2) ? 1 : kCands; }
 bool is_stem(int b, int l) { return b == 0 && l == 0; }
@@ -88,6 +99,7 @@ bool is_stem(int b, int l) { return b == 0 && l == 0; }
 struct CandLayout {
   size_t we = 0, wd = 0, wp = 0, g1 = 0, b1 = 0, g2 = 0, b2 = 0, g3 = 0, b3 = 0, total = 0;
   int E = 0, k = 0, e = 0;
+  int Et = 0;  // true expanded width
 };
 
 MbLayer student_mb(int b, int l) { return teacher_layer(b, b == 0 ? l - 1 : l); }
@@ -99,6 +111,7 @@ CandLayout cand_layout(int b, int l, int c) {
     L.b2 = L.g2 + 32;
     L.total = L.b2 + 32;
     L.E = 32;
+    L.Et = 32;
     L.k = 3;
     return L;
   }
@@ -112,6 +125,7 @@ CandLayout cand_layout(int b, int l, int c) {
     L.e = ES[c / 3];
   }
   L.E = expand_ch(m.cin, L.e);
+  L.Et = expand_ch_t(m.cin_t, L.e);
   size_t o = 0;
   if (L.e != 1) {
     L.we = o;
@@ -168,6 +182,7 @@ pbdk_conv_desc pw_desc(size_t m, int cin, int cout) {
 struct TOp {
   enum Kind { STEM, PW, DW, SE } kind;
   int cs = 0;                                  // SE width
+  int cin_t = 0, cout_t = 0, cs_t = 0;         // true widths (weights beyond them are zero)
   bf16 *w2 = nullptr;                          // SE: w = W1 [cs][E], w2 = W2 [E][cs]
   float* b2 = nullptr;                         // SE: bias = b1 [cs], b2 [E]
   int cin = 0, cout = 0, k = 0, stride = 1, hin = 0, hout = 0, epi = 0;
@@ -200,6 +215,7 @@ struct SCand {
 
 struct SLayer {
   int cin = 0, cout = 0, stride = 1, hin = 0, hout = 0, Emax = 0;
+  int cin_t = 0, cout_t = 0;  // true widths
   bool res = false, stem = false, need_dx = false, last = false;
   std::vector<SCand> cands;
   int active = 0;
@@ -262,29 +278,33 @@ class MbPartition final : public PartitionBase {
     for (TBlock& tb : tblocks_)
       for (TOp& op : tb.ops) {
         if (op.kind == TOp::SE) {
-          check(pbdk::init_uniform(op.w, 1, op.cs, 1, 1, op.cout, op.cout, d_.seed_teacher, op.tensor,
-                                   kaiming(op.cout, 1.0f), st),
+          check(pbdk::init_uniform(op.w, 1, op.cs, 1, 1, op.cout, op.cout_t, d_.seed_teacher, op.tensor,
+                                   kaiming(op.cout_t, 1.0f), st, op.cs_t),
                 "init");
-          check(pbdk::init_uniform(op.bias, 0, op.cs, 1, 1, 1, 1, d_.seed_teacher, op.tensor + 1, 0.1f, st), "init");
-          check(pbdk::init_uniform(op.w2, 1, op.cout, 1, 1, op.cs, op.cs, d_.seed_teacher, op.tensor + 10,
-                                   kaiming(op.cs, 1.0f), st),
+          check(pbdk::init_uniform(op.bias, 0, op.cs, 1, 1, 1, 1, d_.seed_teacher, op.tensor + 1, 0.1f, st, op.cs_t),
                 "init");
-          check(pbdk::init_uniform(op.b2, 0, op.cout, 1, 1, 1, 1, d_.seed_teacher, op.tensor + 11, 0.1f, st), "init");
+          check(pbdk::init_uniform(op.w2, 1, op.cout, 1, 1, op.cs, op.cs_t, d_.seed_teacher, op.tensor + 10,
+                                   kaiming(op.cs_t, 1.0f), st, op.cout_t),
+                "init");
+          check(pbdk::init_uniform(op.b2, 0, op.cout, 1, 1, 1, 1, d_.seed_teacher, op.tensor + 11, 0.1f, st, op.cout_t),
+                "init");
           continue;
         }
         if (op.kind == TOp::STEM) {
           check(pbdk::init_uniform(op.w, 1, 32, 3, 3, 16, 3, d_.seed_teacher, op.tensor, kaiming(27, 1.0f), st), "init");
         } else if (op.kind == TOp::PW) {
-          check(pbdk::init_uniform(op.w, 1, op.cout, 1, 1, op.cin, op.cin, d_.seed_teacher, op.tensor,
-                                   kaiming(op.cin, op.gain), st),
+          check(pbdk::init_uniform(op.w, 1, op.cout, 1, 1, op.cin, op.cin_t, d_.seed_teacher, op.tensor,
+                                   kaiming(op.cin_t, op.gain), st, op.cout_t),
                 "init");
         } else {
           check(pbdk::init_uniform(op.w, 1, op.cout, op.k, op.k, 1, 1, d_.seed_teacher, op.tensor,
-                                   kaiming(op.k * op.k, 1.0f), st),
+                                   kaiming(op.k * op.k, 1.0f), st, op.cout_t),
                 "init");
           check(pbdk_weight_flip(op.w, op.wflip, op.cout, op.k, op.k, 1, st), "flip");
         }
-        check(pbdk::init_uniform(op.bias, 0, op.cout, 1, 1, 1, 1, d_.seed_teacher, op.tensor + 1, 0.1f, st), "init");
+        check(pbdk::init_uniform(op.bias, 0, op.cout, 1, 1, 1, 1, d_.seed_teacher, op.tensor + 1, 0.1f, st,
+                                 op.cout_t),
+              "init");
       }
     for (SBlock& sb : sblocks_)
       for (size_t l = 0; l < sb.layers.size(); ++l) {
@@ -301,14 +321,14 @@ class MbPartition final : public PartitionBase {
             continue;
           }
           if (C.L.e != 1)
-            check(pbdk::init_uniform(q + C.L.we, 0, C.L.E, 1, 1, L.cin, L.cin, d_.seed_student, tid,
-                                     kaiming(L.cin, 1.0f), st),
+            check(pbdk::init_uniform(q + C.L.we, 0, C.L.E, 1, 1, L.cin, L.cin_t, d_.seed_student, tid,
+                                     kaiming(L.cin_t, 1.0f), st, C.L.Et),
                   "init");
           check(pbdk::init_uniform(q + C.L.wd, 0, C.L.E, C.L.k, C.L.k, 1, 1, d_.seed_student, tid + 1u,
-                                   kaiming(C.L.k * C.L.k, 1.0f), st),
+                                   kaiming(C.L.k * C.L.k, 1.0f), st, C.L.Et),
                 "init");
-          check(pbdk::init_uniform(q + C.L.wp, 0, L.cout, 1, 1, C.L.E, C.L.E, d_.seed_student, tid + 2u,
-                                   kaiming(C.L.E, 1.0f), st),
+          check(pbdk::init_uniform(q + C.L.wp, 0, L.cout, 1, 1, C.L.E, C.L.Et, d_.seed_student, tid + 2u,
+                                   kaiming(C.L.Et, 1.0f), st, L.cout_t),
                 "init");
           if (C.L.e != 1) {
             check(pbdk::fill(q + C.L.g1, C.L.E, 1.0f, st), "fill");
@@ -556,7 +576,7 @@ class MbPartition final : public PartitionBase {
                                  static_cast<long long>(mo), L.cout, 0, st),
               "bn3 apply");
       } else {
-        const double norm = static_cast<double>(d_.global_batch) * L.cout * L.hout * L.hout;
+        const double norm = static_cast<double>(d_.global_batch) * L.cout_t * L.hout * L.hout;  // true widths
         check(pbdk::mse_affine(L.y3, L.st3, p + C.L.g3, p + C.L.b3, L.res ? L.x : nullptr, sb.target,
                                static_cast<long long>(mo), L.cout, static_cast<float>(2.0 / norm), norm, L.gz, sb.lws,
                                losses_ + i, st),
@@ -630,6 +650,8 @@ class MbPartition final : public PartitionBase {
         op.kind = TOp::STEM;
         op.cin = 3;
         op.cout = 32;
+        op.cin_t = 3;
+        op.cout_t = 32;
         op.k = 3;
         op.stride = 2;
         op.hin = S_;
@@ -645,7 +667,7 @@ class MbPartition final : public PartitionBase {
       }
       for (int l = 0; l < NL[b]; ++l) {
         const MbLayer m = teacher_layer(b, l);
-        const int E = expand_ch(m.cin, m.t);
+        const int E = expand_ch(m.cin, m.t), Et = expand_ch_t(m.cin_t, m.t);
         const int ho = (hw + 2 * (m.k / 2) - m.k) / m.stride + 1;
         const bf16* a = x;
         if (m.t != 1) {
@@ -653,6 +675,8 @@ class MbPartition final : public PartitionBase {
           e.kind = TOp::PW;
           e.cin = m.cin;
           e.cout = E;
+          e.cin_t = m.cin_t;
+          e.cout_t = Et;
           e.hin = e.hout = hw;
           e.epi = fam_.act == 2 ? PBDK_EPI_BIAS_SWISH : PBDK_EPI_BIAS_RELU6;
           e.tensor = base + 10u * j++;
@@ -666,6 +690,7 @@ class MbPartition final : public PartitionBase {
         TOp d{};
         d.kind = TOp::DW;
         d.cin = d.cout = E;
+        d.cin_t = d.cout_t = Et;
         d.k = m.k;
         d.stride = m.stride;
         d.hin = hw;
@@ -682,6 +707,8 @@ class MbPartition final : public PartitionBase {
           q.kind = TOp::SE;
           q.cout = E;
           q.cs = cs;
+          q.cout_t = Et;
+          q.cs_t = se_ch_t(m);
           q.hin = q.hout = ho;
           q.tensor = base + 10u * j;
           j += 2;
@@ -693,11 +720,13 @@ class MbPartition final : public PartitionBase {
           tb.ops.push_back(q);
           se_elems = std::max(se_elems, static_cast<size_t>(N) * E);
         }
-        const bool res = m.stride == 1 && m.cin == m.cout;
+        const bool res = has_res(m);
         TOp pj{};
         pj.kind = TOp::PW;
         pj.cin = E;
         pj.cout = m.cout;
+        pj.cin_t = Et;
+        pj.cout_t = m.cout_t;
         pj.hin = pj.hout = ho;
         pj.epi = res ? PBDK_EPI_BIAS_RES : PBDK_EPI_BIAS;
         pj.gain = res ? 0.5f : 1.0f;
@@ -739,6 +768,8 @@ class MbPartition final : public PartitionBase {
         if (L.stem) {
           L.cin = 3;
           L.cout = 32;
+          L.cin_t = 3;
+          L.cout_t = 32;
           L.stride = 2;
           L.hin = S_;
           L.hout = S_ / 2;
@@ -747,10 +778,12 @@ class MbPartition final : public PartitionBase {
           const MbLayer m = student_mb(b, l);
           L.cin = m.cin;
           L.cout = m.cout;
+          L.cin_t = m.cin_t;
+          L.cout_t = m.cout_t;
           L.stride = m.stride;
           L.hin = hw;
           L.hout = (hw - 1) / m.stride + 1;
-          L.res = m.stride == 1 && m.cin == m.cout;
+          L.res = has_res(m);
         }
         L.need_dx = l > 0;
         const size_t mi = rows_max(L.hin), mo = rows_max(L.hout);

@@ -164,16 +164,17 @@ __global__ void image_split_kernel(float* __restrict__ x, int n, int npix, long 
   }
 }
 
-// dst[k][r][s][c_stored] = c < c_true ? U(-1,1)[counter=((k*r+..)*c_true+c, tensor)] * bound : 0
+// dst[k][r][s][c_stored] = (k < k_true && c < c_true) ? U(-1,1)[counter=((k*r+..)*c_true+c, tensor)] * bound : 0
+// (the counter is the flat index of the true [k_true][r][s][c_true] tensor)
 __global__ void init_uniform_kernel(void* dst, int bf16_out, int k, int r, int s, int cs, int ct, uint32_t seed,
-                                    uint32_t tensor, float bound) {
+                                    uint32_t tensor, float bound, int kt) {
   const long long total = static_cast<long long>(k) * r * s * cs;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int c = static_cast<int>(i % cs);
     const long long krs = i / cs;
     float v = 0.0f;
-    if (c < ct) {
+    if (c < ct && krs / (r * s) < kt) {
       const long long j = krs * ct + c;
       uint32_t o;
       philox10(static_cast<uint32_t>(j), tensor, 0u, 0u, seed, 0xB200B200u, o);
@@ -1208,10 +1209,10 @@ int pack_image_parity(const float* s0, const float* s1, const long long* counter
 }
 
 int init_uniform(void* dst, int bf16_out, int k, int r, int s, int cs, int ct, uint32_t seed, uint32_t tensor,
-                 float bound, cudaStream_t st) {
+                 float bound, cudaStream_t st, int kt) {
   init_uniform_kernel<<<grid_for(static_cast<long long>(k) * r * s * cs), kThreads, 0, st>>>(dst, bf16_out, k, r, s,
                                                                                               cs, ct, seed, tensor,
-                                                                                              bound);
+                                                                                              bound, kt < 0 ? k : kt);
   return ok(cudaGetLastError());
 }
 

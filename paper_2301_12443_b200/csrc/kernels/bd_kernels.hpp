@@ -53,7 +53,7 @@ int pack_image_parity(const float* s0, const float* s1, const long long* counter
                       int side = 32, int prec = 0);
 // bf16_out: 0 fp32, 1 bf16, 2 split fp32 [k][r][s][2cs]
 int init_uniform(void* dst, int bf16_out, int k, int r, int s, int cs, int ct, uint32_t seed, uint32_t tensor,
-                 float bound, cudaStream_t st);
+                 float bound, cudaStream_t st, int kt = -1);  // kt: true output channels (rows >= kt zero)
 int fill(float* dst, size_t n, float v, cudaStream_t st);
 // prec 1 (fp32 workload): fp32 inputs; outputs that feed convolutions are split fp32
 int bn_stats(const void* y, int m, int c, float* ws, float* mean_rstd, cudaStream_t st, int prec = 0);

@@ -11,19 +11,23 @@ from __future__ import annotations
 from typing import Dict, List, Sequence, Tuple
 
 FAMILIES = {
-    # channels per boundary, teacher MBConv layers per block, teacher kernel per block, squeeze-excite
-    "mbv2": ((3, 32, 32, 64, 128, 192, 320), (3, 3, 4, 3, 3, 1), (3, 3, 3, 3, 3, 3), False),
-    "effb0": ((3, 32, 64, 128, 128, 192, 320), (3, 2, 3, 3, 4, 1), (3, 5, 3, 5, 5, 3), True),
+    # stored channels per boundary, teacher MBConv layers per block, teacher kernel per block,
+    # squeeze-excite, true channels per boundary (MobileNetV2-1.0 / EfficientNet-B0; the stored extra
+    # channels are identically zero)
+    "mbv2": ((3, 32, 32, 64, 128, 192, 320), (3, 3, 4, 3, 3, 1), (3, 3, 3, 3, 3, 3), False,
+             (3, 24, 32, 64, 96, 160, 320)),
+    "effb0": ((3, 32, 64, 128, 128, 192, 320), (3, 2, 3, 3, 4, 1), (3, 5, 3, 5, 5, 3), True,
+              (3, 24, 40, 80, 112, 192, 320)),
 }
-CH, NL, KT, SE = FAMILIES["mbv2"]
+CH, NL, KT, SE, CT = FAMILIES["mbv2"]
 DIV = (1, 4, 8, 16, 16, 32, 32)
 KS, ES = (3, 5, 7), (3, 6)
 
 
 def set_family(model: str):
     """Select the teacher family the helpers below describe ("mbv2" | "effb0")."""
-    global CH, NL, KT, SE
-    CH, NL, KT, SE = FAMILIES[model]
+    global CH, NL, KT, SE, CT
+    CH, NL, KT, SE, CT = FAMILIES[model]
 
 
 BF, F4 = 2, 4
@@ -34,12 +38,36 @@ def round_ch(c: int) -> int:
 
 
 def teacher_layer(b: int, l: int) -> Tuple[int, int, int, int, int]:
+    """(t, k, cin, cout, stride), stored widths."""
+    return teacher_layer_t(b, l)[:5]
+
+
+def teacher_layer_t(b: int, l: int) -> Tuple[int, int, int, int, int, int, int]:
+    """(t, k, cin, cout, stride, cin_true, cout_true)."""
     if b == 0:
-        return ((1, 3, 32, 16, 1), (6, 3, 16, 32, 2), (6, 3, 32, 32, 1))[l]
+        return ((1, 3, 32, 16, 1, 32, 16), (6, 3, 16, 32, 2, 16, 24), (6, 3, 32, 32, 1, 24, 24))[l]
     cin, cout = CH[b], CH[b + 1]
     s = DIV[b + 1] // DIV[b]
     k = KT[b]
-    return (6, k, cin, cout, s) if l == 0 else (6, k, cout, cout, 1)
+    return (6, k, cin, cout, s, CT[b], CT[b + 1]) if l == 0 else (6, k, cout, cout, 1, CT[b + 1], CT[b + 1])
+
+
+def teacher_true_macs(S: int = 224) -> float:
+    """Multiply-accumulates of the teacher body (stem + every MBConv) at its true widths."""
+    macs = (S // 2) ** 2 * 32 * 27.0
+    for b in range(6):
+        hw = S // DIV[b] if b else S // 2
+        for l in range(NL[b]):
+            t, k, _, _, st, ci, co = teacher_layer_t(b, l)
+            E = ci * t
+            ho = (hw - 1) // st + 1
+            if t != 1:
+                macs += hw * hw * ci * E
+            macs += ho * ho * E * k * k + ho * ho * E * co
+            if SE:
+                macs += 2 * E * max(1, ci // 4)
+            hw = ho
+    return macs
 
 
 def _mb(acc, n, hin, cin, E, k, stride, cout, res, expand, train, last):
@@ -94,9 +122,9 @@ def block_work(b: int, n: int, S: int, path: Sequence[int]) -> Tuple[float, floa
         hw = P
     hs = hw
     for l in range(NL[b]):
-        tt, k, cin, cout, st = teacher_layer(b, l)
+        tt, k, cin, cout, st, cin_t, cout_t = teacher_layer_t(b, l)
         E = cin if tt == 1 else round_ch(cin * tt)
-        res = st == 1 and cin == cout
+        res = st == 1 and cin_t == cout_t  # residual by the true widths
         hw = _mb(t, n, hw, cin, E, k, st, cout, res, tt != 1, False, False)
         sl = l + 1 if b == 0 else l
         if b == 0 and l == 0:

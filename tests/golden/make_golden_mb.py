@@ -1,7 +1,10 @@
 """Generate tests/golden/mb_torch_fp64.npz — pins the MBConv C oracle (oracle/mb_oracle.c) against an
 independent implementation: the MobileNetV2 teacher / ProxylessNAS student blockwise-distillation
 step written with torch ops + autograd (PyTorch is the paper's framework), in
-float64 so the fixture is a clean reference for the oracle's fp32 mode.  Inputs (data, teacher and
+float64 so the fixture is a clean reference for the oracle's fp32 mode.  The torch model runs at the
+architectures' TRUE channel widths (MobileNetV2-1.0: 24/32/64/96/160/320, EfficientNet-B0:
+24/40/80/112/192/320), slicing the oracle's zero-padded storage — so the fixture also pins that the
+padded layout computes exactly the true-width network.  Inputs (data, teacher and
 student weights, the sampled path) come from the oracle's Philox generators; everything computed
 here is torch's (F.conv2d with groups for depthwise, F.batch_norm in training mode, hardtanh as
 ReLU6, autograd).  Run from the repo root:  python tests/golden/make_golden_mb.py [0|1]   (1 = EfficientNet-B0 teacher:
@@ -46,6 +49,9 @@ def tact(x):
 
 
 def teacher_fwd(b, tp, x):
+    """The teacher at its TRUE widths (MobileNetV2-1.0 / EfficientNet-B0): the stored parameter
+    vector is sliced to the true channels, the stored extra channels of x are ignored and the output
+    is zero-padded back to the stored width (the layout the oracle uses)."""
     p = torch.from_numpy(tp).to(DT)
     off = [0]
 
@@ -56,33 +62,39 @@ def teacher_fwd(b, tp, x):
 
     if b == 0:
         w = take(32 * 9 * 16).reshape(32, 3, 3, 16)[..., :3].permute(0, 3, 1, 2)
-        x = tact(F.conv2d(x, w, take(32), stride=2, padding=1))
+        x = tact(F.conv2d(x[:, :3], w, take(32), stride=2, padding=1))
+    else:
+        x = x[:, :mb.CT[b]]
     for l in range(mb.NL[b]):
-        t, k, cin, cout, s = mb.teacher_layer(b, l)
+        t, k, cin, cout, s, ci, co = mb.teacher_layer_t(b, l)
         E = cin if t == 1 else mb.round_ch(cin * t)
+        Et = ci * t
         h = x
         if t != 1:
-            w = take(E * cin).reshape(E, cin, 1, 1)
-            h = tact(F.conv2d(h, w, take(E)))
-        wd = take(E * k * k).reshape(E, 1, k, k)
-        h = tact(F.conv2d(h, wd, take(E), stride=s, padding=k // 2, groups=E))
+            w = take(E * cin).reshape(E, cin)[:Et, :ci].reshape(Et, ci, 1, 1)
+            h = tact(F.conv2d(h, w, take(E)[:Et]))
+        wd = take(E * k * k).reshape(E, 1, k, k)[:Et]
+        h = tact(F.conv2d(h, wd, take(E)[:Et], stride=s, padding=k // 2, groups=Et))
         cs = mb.se_ch(cin)
-        if cs:  # squeeze-excite
-            w1, b1 = take(cs * E).reshape(cs, E), take(cs)
-            w2, b2 = take(E * cs).reshape(E, cs), take(E)
+        if cs:  # squeeze-excite, reduce width 0.25 x the true input channels
+            cst = mb.se_ch(ci)
+            w1, b1 = take(cs * E).reshape(cs, E)[:cst, :Et], take(cs)[:cst]
+            w2, b2 = take(E * cs).reshape(E, cs)[:Et, :cst], take(E)[:Et]
             z = h.mean(dim=(2, 3))
             z = z @ w1.T + b1
             z = z * torch.sigmoid(z)
             gate = torch.sigmoid(z @ w2.T + b2)
             h = h * gate[:, :, None, None]
-        wp = take(cout * E).reshape(cout, E, 1, 1)
-        y = F.conv2d(h, wp, take(cout))
-        x = y + x if (s == 1 and cin == cout) else y
-    return x
+        wp = take(cout * E).reshape(cout, E)[:co, :Et].reshape(co, Et, 1, 1)
+        y = F.conv2d(h, wp, take(cout)[:co])
+        x = y + x if (s == 1 and ci == co) else y
+    return F.pad(x, (0, 0, 0, 0, 0, mb.CH[b + 1] - x.shape[1]))
 
 
 def student(b, sp, path, x, t, norm):
-    """loss, {(layer, tensor): grad} of the active path."""
+    """loss, {(layer, tensor): grad} of the active path.  The network runs at the TRUE widths: every
+    parameter is a leaf in the stored layout and enters through its true-width slice, so the stored
+    extra entries get exactly zero gradient (as in the oracle / product)."""
     params = {}
     for l in range(mb.layers(b)):
         c = int(path[l])
@@ -90,25 +102,28 @@ def student(b, sp, path, x, t, norm):
         for name, (o, n) in mb.candidate_layout(b, l, c).items():
             params[(l, name)] = torch.tensor(sp[off + o: off + o + n], dtype=DT, requires_grad=True)
 
-    def bn(y, l, g, be):
-        return F.batch_norm(y, None, None, params[(l, g)], params[(l, be)], training=True, eps=1e-5)
+    def bn(y, l, g, be, n):
+        return F.batch_norm(y, None, None, params[(l, g)][:n], params[(l, be)][:n], training=True, eps=1e-5)
 
-    h = x
+    h = x[:, :3] if b == 0 else x[:, :mb.CT[b]]
     for l in range(mb.layers(b)):
         g = mb.student_layer(b, l, int(path[l]))
         if g["kind"] == "stem":
             w = params[(l, "w")].reshape(32, 3, 3, 16)[..., :3].permute(0, 3, 1, 2)
-            h = relu6(bn(F.conv2d(h, w, stride=2, padding=1), l, "g2", "b2"))
+            h = relu6(bn(F.conv2d(h, w, stride=2, padding=1), l, "g2", "b2", 32))
             continue
         E, k, cin, cout = g["E"], g["k"], g["cin"], g["cout"]
+        Et, ci, co = g["Et"], g["cin_t"], g["cout_t"]
         a = h
         if g["e"] != 1:
-            a = relu6(bn(F.conv2d(h, params[(l, "we")].reshape(E, cin, 1, 1)), l, "g1", "b1"))
-        a = relu6(bn(F.conv2d(a, params[(l, "wd")].reshape(E, 1, k, k), stride=g["stride"], padding=k // 2,
-                              groups=E), l, "g2", "b2"))
-        z = bn(F.conv2d(a, params[(l, "wp")].reshape(cout, E, 1, 1)), l, "g3", "b3")
+            we = params[(l, "we")].reshape(E, cin)[:Et, :ci].reshape(Et, ci, 1, 1)
+            a = relu6(bn(F.conv2d(h, we), l, "g1", "b1", Et))
+        wd = params[(l, "wd")].reshape(E, 1, k, k)[:Et]
+        a = relu6(bn(F.conv2d(a, wd, stride=g["stride"], padding=k // 2, groups=Et), l, "g2", "b2", Et))
+        wp = params[(l, "wp")].reshape(cout, E)[:co, :Et].reshape(co, Et, 1, 1)
+        z = bn(F.conv2d(a, wp), l, "g3", "b3", co)
         h = z + h if g["res"] else z
-    loss = ((h - t) ** 2).sum() / norm
+    loss = ((h - t[:, :h.shape[1]]) ** 2).sum() / norm
     loss.backward()
     return float(loss), {key: v.grad.numpy() for key, v in params.items()}
 
@@ -127,7 +142,7 @@ def main():
     for b in range(mb.BLOCKS):
         sp = mb.student_params(b)
         path = mb.sample_path(b, DRAW)
-        c, hh = mb.channels(b + 1), mb.hw(b + 1, S)
+        c, hh = mb.true_channels(b + 1), mb.hw(b + 1, S)
         norm = float(B) * c * hh * hh
         loss, grads = student(b, sp, path, nchw(acts[b]), nchw(acts[b + 1]), norm)
         out[f"s{b}_path"] = path

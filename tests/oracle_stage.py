@@ -138,7 +138,7 @@ class MbOracleStage(OracleStage):
         mb = self.mb
         parts = []
         for i, k in enumerate(self.blocks):
-            norm = float(self.b) * mb.channels(k + 1) * mb.hw(k + 1, self.S) ** 2
+            norm = float(self.b) * mb.true_channels(k + 1) * mb.hw(k + 1, self.S) ** 2
             g, loss = mb.student_fwd_bwd(k, self.sp[k], self.paths[k], self.acts[i], self.acts[i + 1], self.S, norm)
             self._losses[i] = loss
             parts.append(g)

@@ -83,7 +83,7 @@ def test_per_stage_parity_on_identical_inputs(ex, fam, b, draw):
         want_t = mb.teacher_fwd(k, mb.teacher_params(k), prev, S)
         depth = (3 if fam == "mbv2" else 4) * mb.NL[k] + (1 if k == 0 else 0)
         compare_bf16_tensors(gpu_t, want_t, depth=depth)
-        norm = float(b) * mb.channels(k + 1) * mb.hw(k + 1, S) ** 2
+        norm = float(b) * mb.true_channels(k + 1) * mb.hw(k + 1, S) ** 2
         sp = mb.student_params(k)
         g, loss = mb.student_fwd_bwd(k, sp, paths[k], prev, gpu_t, S, norm, bf16=True)
         g32, _ = mb.student_fwd_bwd(k, sp, paths[k], prev, gpu_t, S, norm, bf16=False)

@@ -184,7 +184,7 @@ def test_mbconv_224_b32_per_stage(ex, mbfam):
         want_t = mb.teacher_fwd(k, mb.teacher_params(k), prev, S224)
         depth = (3 if fam == "mbv2" else 4) * mb.NL[k] + (1 if k == 0 else 0)
         compare_bf16_tensors(gpu_t, want_t, depth=depth)
-        norm = float(b) * mb.channels(k + 1) * mb.hw(k + 1, S224) ** 2
+        norm = float(b) * mb.true_channels(k + 1) * mb.hw(k + 1, S224) ** 2
         sp = mb.student_params(k)
         g, loss = mb.student_fwd_bwd(k, sp, paths[k], prev, gpu_t, S224, norm, bf16=True)
         g32, _ = mb.student_fwd_bwd(k, sp, paths[k], prev, gpu_t, S224, norm, bf16=False)

@@ -56,7 +56,7 @@ def test_student_matches_torch(gold, chain):
         sp = mb.student_params(b)
         path = mb.sample_path(b, DRAW)
         assert (path == gold[f"s{b}_path"]).all()
-        c, hh = mb.channels(b + 1), mb.hw(b + 1, S)
+        c, hh = mb.true_channels(b + 1), mb.hw(b + 1, S)
         norm = float(B) * c * hh * hh
         g, loss = mb.student_fwd_bwd(b, sp, path, chain[b], chain[b + 1], S, norm, bf16=False)
         assert loss == pytest.approx(float(gold[f"s{b}_loss"]), rel=1e-5)
@@ -122,7 +122,61 @@ def test_oracle_bf16_mode_close_to_fp32(chain):
     b = 1
     sp = mb.student_params(b)
     path = mb.sample_path(b, 3)
-    norm = float(B) * mb.channels(b + 1) * mb.hw(b + 1, S) ** 2
+    norm = float(B) * mb.true_channels(b + 1) * mb.hw(b + 1, S) ** 2
     _, l32 = mb.student_fwd_bwd(b, sp, path, chain[b], chain[b + 1], S, norm, bf16=False)
     _, l16 = mb.student_fwd_bwd(b, sp, path, chain[b], chain[b + 1], S, norm, bf16=True)
     assert l16 == pytest.approx(l32, rel=2e-2)
+
+
+def test_true_widths_extra_channels_stay_zero():
+    """The stored extra channels (tensor-tile rounding) are identically zero: teacher activations,
+    student gradients and, after SGD, student weights — so the network is the true-width one."""
+    for fam in (0, 1):
+        mb.set_family(fam)
+        try:
+            x = mb.image(2, 0, S)
+            acts = [x]
+            for k in range(mb.BLOCKS):
+                acts.append(mb.teacher_fwd(k, mb.teacher_params(k), acts[-1], S))
+                ct, cs = mb.true_channels(k + 1), mb.channels(k + 1)
+                assert cs >= ct
+                assert not acts[-1][..., ct:].any(), (fam, k)
+                assert np.abs(acts[-1][..., :ct]).max() > 0
+            for b in range(mb.BLOCKS):
+                sp = mb.student_params(b)
+                path = mb.sample_path(b, 4)
+                g, _ = mb.student_fwd_bwd(b, sp, path, acts[b], acts[b + 1], S, 1.0)
+                for l in range(mb.layers(b)):
+                    geo = mb.student_layer(b, l, int(path[l]))
+                    if geo["kind"] == "stem":
+                        continue
+                    off, _ = mb.candidate_span(b, l, int(path[l]))
+                    lay = mb.candidate_layout(b, l, int(path[l]))
+                    E, Et, cin, ci, cout, co = geo["E"], geo["Et"], geo["cin"], geo["cin_t"], geo["cout"], geo["cout_t"]
+                    wp = sp[off + lay["wp"][0]: off + sum(lay["wp"])].reshape(cout, E)
+                    gp = g[off + lay["wp"][0]: off + sum(lay["wp"])].reshape(cout, E)
+                    assert not wp[co:].any() and not wp[:, Et:].any()
+                    assert not gp[co:].any() and not gp[:, Et:].any()
+                    assert np.abs(gp[:co, :Et]).max() > 0
+                    if "we" in lay:
+                        ge = g[off + lay["we"][0]: off + sum(lay["we"])].reshape(E, cin)
+                        assert not ge[Et:].any() and not ge[:, ci:].any()
+                    for bn in ("b2", "g2"):
+                        gb = g[off + lay[bn][0]: off + sum(lay[bn])]
+                        assert not gb[Et:].any()
+        finally:
+            mb.set_family(0)
+
+
+def test_teacher_is_mobilenetv2_1_0():
+    """The MobileNetV2 teacher body at its true widths has the published MobileNetV2-1.0 cost:
+    300.77 M MACs at 224^2 = body + final 1x1 conv 320->1280 at 7^2 + 1280->1000 FC."""
+    from paper_2301_12443_b200 import mb_models
+    mb_models.set_family("mbv2")
+    head = 7 * 7 * 320 * 1280 + 1280 * 1000
+    assert mb_models.teacher_true_macs(224) + head == pytest.approx(300.77e6, abs=0.01e6)
+    mb_models.set_family("effb0")
+    try:  # EfficientNet-B0: 0.39 B FLOPs (multiply-adds) in its paper, incl. the same head
+        assert (mb_models.teacher_true_macs(224) + head) / 1e9 == pytest.approx(0.39, abs=0.005)
+    finally:
+        mb_models.set_family("mbv2")
