@@ -165,6 +165,8 @@ typedef struct pbdx_relay_msg {
   void* remote_flag;
 } pbdx_relay_msg;
 int pbdx_relay_set_recv(void* handle, int nsenders, void* const* remote_consumed_flags);
+/* bytes per sample of the relayed activation (teacher output of block_hi) */
+size_t pbdx_relay_row_bytes(void* handle);
 int pbdx_relay_set_send(void* handle, int nmsgs, const pbdx_relay_msg* msgs);
 /* DP group over peer memory (share_gradient; AHD partitions with |G| > 1): instead of an
  * NCCL allreduce, every member announces its gradients after S_i.backward (device-side flag into each

@@ -49,6 +49,8 @@ int pbdx_create(const pbdx_desc* d, void** handle) {
 
 void pbdx_destroy(void* handle) { delete P(handle); }
 
+size_t pbdx_relay_row_bytes(void* h) { return h == nullptr ? 0 : P(h)->relay_row_bytes(); }
+
 int pbdx_init_params(void* h, void* st) { return guard([&] { P(h)->init_params(S(st)); }); }
 int pbdx_set_shard(void* h, int n, int first) { return guard([&] { P(h)->set_shard(n, first); }); }
 int pbdx_set_input_mode(void* h, int external) { return guard([&] { P(h)->set_external_input(external); }); }

@@ -13,9 +13,14 @@
 //               [--devices N] [--global-batch N] [--reference-batch N] [--load-ms X] [--mem-bytes X]
 //               [--out F]
 //   pbd report <report.json> [--gantt F.svg] [--profile P --schedule S]   (measured runs, §8f)
+//   pbd run <schedule|-> --global-batch N [--steps N] [--warmup N] [--devices d0,d1,..]
+//           [--model resnet|resnet_fp32|mbv2|effb0] [--image S] [--eager]
+//       runs the schedule on the GPUs of this node in ONE process through the C++ driver
+//       (include/pbdr.h): rank r of the schedule on CUDA device d_r (default: rank r % #devices),
+//       peer relay + peer DP exchange, one CUDA graph per rank; prints ms/step and block losses.
 //
-// The GPU-side commands (measure a profile on the device, run a schedule) live in
-// `python -m paper_2301_12443_b200.cli` because they drive torch.distributed.
+// The torch.distributed flavour (one process per GPU, measured profiles, checkpoints) is
+// `python -m paper_2301_12443_b200.cli profile|run`.
 #include <charconv>
 #include <cstdio>
 #include <cstdlib>
@@ -29,8 +34,12 @@
 #include <string>
 #include <vector>
 
+#include <chrono>
+
 #include "pbd/core.hpp"
 #include "pbd/report.hpp"
+#include "pbdr.h"
+#include "pbdx.h"
 
 namespace {
 
@@ -277,8 +286,57 @@ int cmd_report(const Args& a) {
   return kOk;
 }
 
+int cmd_run(const Args& a) {
+  if (a.pos.size() != 1 || !a.has("global-batch"))
+    throw pbd::ValidationError("usage: pbd run <schedule|-> --global-batch N [--steps N] [--devices d0,d1,..]");
+  const std::string text = read_doc(a.pos[0]);
+  const auto sched = pbd::load_schedule(text).first;
+  int nranks = 0;
+  for (const auto& p : sched.partitions) nranks += p.group_size();
+  const int ndev = pbdr_device_count();
+  if (ndev < 1) throw pbd::IoError("no CUDA device");
+  std::vector<int> dev(static_cast<size_t>(nranks));
+  for (int r = 0; r < nranks; ++r) dev[static_cast<size_t>(r)] = r % ndev;
+  if (a.has("devices")) {
+    std::stringstream ss(a.get("devices"));
+    std::string item;
+    for (int r = 0; std::getline(ss, item, ','); ++r) {
+      if (r >= nranks) throw pbd::ValidationError("--devices: more entries than schedule ranks");
+      dev[static_cast<size_t>(r)] = static_cast<int>(num(item, "--devices"));
+    }
+  }
+  const std::string model = a.get("model", "resnet");
+  const int m = model == "resnet" ? PBDX_MODEL_RESNET_CIFAR : model == "resnet_fp32" ? PBDX_MODEL_RESNET_CIFAR_FP32
+              : model == "mbv2" ? PBDX_MODEL_MBV2_PROXYLESS : model == "effb0" ? PBDX_MODEL_EFFB0_PROXYLESS : -1;
+  if (m < 0) throw pbd::ValidationError("--model resnet|resnet_fp32|mbv2|effb0");
+  const int image = a.has("image") ? static_cast<int>(num(a.get("image"), "--image"))
+                                   : (m == PBDX_MODEL_RESNET_CIFAR || m == PBDX_MODEL_RESNET_CIFAR_FP32 ? 32 : 224);
+  const pbdr_desc d{static_cast<int>(num(a.get("global-batch"), "--global-batch")), m, image, 1234u, 1u, 2u, 0.1f,
+                    0.9f, a.flags.count("eager") ? 0 : 1};
+  void* h = nullptr;
+  if (pbdr_create(text.c_str(), &d, dev.data(), nranks, &h) != 0) throw pbd::IoError("driver setup failed (device)");
+  const int steps = static_cast<int>(num(a.get("steps", "20"), "--steps"));
+  const int warmup = static_cast<int>(num(a.get("warmup", "3"), "--warmup"));
+  int rc = 0;
+  for (int i = 0; i < warmup && rc == 0; ++i) rc = pbdr_step(h);
+  if (rc == 0) rc = pbdr_sync(h);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int i = 0; i < steps && rc == 0; ++i) rc = pbdr_step(h);
+  if (rc == 0) rc = pbdr_sync(h);
+  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  std::vector<double> losses(static_cast<size_t>(std::max(1, pbdr_num_blocks(h))));
+  if (rc == 0) rc = pbdr_block_losses(h, losses.data());
+  pbdr_destroy(h);
+  if (rc != 0) throw pbd::IoError("device step failed");
+  std::cout << "ranks: " << nranks << "\nms/step: " << ms / std::max(1, steps) << " (host wall clock, " << steps
+            << " steps)\nsamples/s: " << d.global_batch * std::max(1, steps) / (ms * 1e-3) << "\nblock losses:";
+  for (double l : losses) std::cout << " " << l;
+  std::cout << "\n";
+  return kOk;
+}
+
 void usage() {
-  std::cerr << "usage: pbd <schedule|simulate|compare|profile-gen|report> ...  (see the header of csrc/tools/pbd_cli.cpp)\n";
+  std::cerr << "usage: pbd <schedule|simulate|compare|profile-gen|report|run> ...  (see the header of csrc/tools/pbd_cli.cpp)\n";
 }
 
 }  // namespace
@@ -295,6 +353,7 @@ int main(int argc, char** argv) {
     if (cmd == "compare") return cmd_compare(parse(argc, argv, 2, {}));
     if (cmd == "profile-gen") return cmd_profile_gen(parse(argc, argv, 2, {}));
     if (cmd == "report") return cmd_report(parse(argc, argv, 2, {}));
+    if (cmd == "run") return cmd_run(parse(argc, argv, 2, {"eager"}));
     if (cmd == "-h" || cmd == "--help") {
       usage();
       return kOk;
