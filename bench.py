@@ -525,6 +525,25 @@ def run_ours_mbv2(args, dev, local_rank):
     t0 = time.perf_counter()
     run_e2e(n_e2e)
     e2e_ms = (time.perf_counter() - t0) / n_e2e * 1e3
+    # ProxylessNAS step (nas.py): architecture round + weight round, paths resampled from softmax(alpha)
+    # every round (eager launches: a new path invalidates the captured graphs), host alpha update
+    from paper_2301_12443_b200 import nas
+    part.set_external_input(0)
+    arch = nas.ArchParams(range(6))
+    for s_ in range(2):
+        nas.nas_step(part, arch, s_)
+    torch.cuda.synchronize()
+    n_nas = 10
+    t0 = time.perf_counter()
+    for s_ in range(n_nas):
+        nas.nas_step(part, arch, 2 + s_)
+    torch.cuda.synchronize()
+    nas_ms = (time.perf_counter() - t0) / n_nas * 1e3
+    nas_line = {"ms_per_step": nas_ms, "samples_per_s": b / nas_ms * 1e3, "rounds": 2, "steps": n_nas,
+                "alpha_entropy": [round(arch.entropy(k), 4) for k in range(6)],
+                "note": "host wall clock; one NAS step = teacher fwd + architecture round (student fwd/bwd, "
+                        "REINFORCE alpha update from the block losses) + weight round (student fwd/bwd + SGD), "
+                        "paths ~ softmax(alpha) each round, eager launches"}
     peaks = measured_peaks()
     flops, nbytes = mb_models.step_work(b, S, paths)
     t_roof = max(flops / (peaks["bf16_tflops_sustained"] * 1e12), nbytes / (peaks["hbm_gbs"] * 1e9))
@@ -563,7 +582,7 @@ def run_ours_mbv2(args, dev, local_rank):
             "e2e": {"value": b / e2e_ms * 1e3, "unit": UNIT, "h2d_bytes_per_step": b * S * S * 3 * 4,
                     "d2h_bytes_per_step": 48, "ms_per_step": e2e_ms},
             "roofline": roof, "cpu_baseline": cpu, "gpu_launches": part.launches_per_step() * args.steps,
-            "clocks": clocks.summary(), "losses_last_step": losses}
+            "clocks": clocks.summary(), "losses_last_step": losses, "nas_step": nas_line}
     print(json.dumps(line), flush=True)
 
 
