@@ -235,8 +235,9 @@ struct SBlock {
   std::vector<SLayer> layers;
   const bf16* in = nullptr;
   const bf16* target = nullptr;
-  float* rws = nullptr;  // BN / loss reductions
+  float* rws = nullptr;  // loss reductions
   size_t rws_floats = 0;
+  pbdk::FixScratch fx{};  // self-finalizing BN reductions of this block's stream (sequential: one scratch)
   float* dws = nullptr;  // depthwise / stem wgrad partials
   size_t dws_floats = 0;
   void* wws = nullptr;  // 1x1 wgrad split-K partials
@@ -485,13 +486,13 @@ class MbPartition final : public PartitionBase {
       for (const SLayer& L : sblocks_[bi].layers) {
         const SCand& C = L.cands[static_cast<size_t>(L.active)];
         if (L.stem) {
-          n += (1 + 2 + 1) + (3 + 2) + 1;  // conv, stats, apply | bn bwd, wgrad | sgd
+          n += (1 + 1 + 1) + (2 + 2) + 1;  // conv, stats, apply | bn bwd, wgrad | sgd
           continue;
         }
         const bool e = C.L.e != 1;
-        n += (e ? 4 : 0) + 1 + 2 + 1 + 1 + 2 + (L.last ? 2 : 1);                      // forward
-        n += 3 + (C.w_proj.splits > 1 ? 2 : 1) + 1 + 3 + 2;                            // bn3, wgrad, dgrad, bn2, dw wgrad
-        n += e ? (1 + 3 + (C.w_exp.splits > 1 ? 2 : 1) + (L.need_dx ? 1 : 0)) : (L.need_dx ? 1 : 0);
+        n += (e ? 3 : 0) + 1 + 1 + 1 + 1 + 1 + (L.last ? 2 : 1);                      // forward
+        n += 2 + (C.w_proj.splits > 1 ? 2 : 1) + 1 + 2 + 2;                            // bn3, wgrad, dgrad, bn2, dw wgrad
+        n += e ? (1 + 2 + (C.w_exp.splits > 1 ? 2 : 1) + (L.need_dx ? 1 : 0)) : (L.need_dx ? 1 : 0);
         n += 1 + (e ? 2 : 1) + 1;                                                      // sgd, transposes, flip
       }
     }
@@ -548,7 +549,7 @@ class MbPartition final : public PartitionBase {
       const size_t mi = act_rows_hw(L.hin), mo = act_rows_hw(L.hout);
       if (L.stem) {
         check(pbdk::stem_fwd(L.x, shadow_ + C.off, nullptr, L.y2, n_, S_, 0, st), "student stem");
-        check(pbdk::bn_stats(L.y2, static_cast<int>(mo), 32, sb.rws, L.st2, st), "stem stats");
+        check(pbdk::bn_stats_fix(L.y2, nullptr, static_cast<int>(mo), 32, sb.fx, L.st2, nullptr, st), "stem stats");
         check(pbdk::bn_apply_act(L.y2, L.st2, p + C.L.g2, p + C.L.b2, nullptr, L.a2, static_cast<long long>(mo), 32,
                                  1, st),
               "stem apply");
@@ -557,7 +558,7 @@ class MbPartition final : public PartitionBase {
       const bf16* a_in = L.x;
       if (C.L.e != 1) {
         check(pbdk::fprop_run(C.p_exp, st), "expand");
-        check(pbdk::bn_stats(L.y1, static_cast<int>(mi), C.L.E, sb.rws, L.st1, st), "bn1 stats");
+        check(pbdk::bn_stats_fix(L.y1, nullptr, static_cast<int>(mi), C.L.E, sb.fx, L.st1, nullptr, st), "bn1 stats");
         check(pbdk::bn_apply_act(L.y1, L.st1, p + C.L.g1, p + C.L.b1, nullptr, L.a1, static_cast<long long>(mi), C.L.E,
                                  1, st),
               "bn1 apply");
@@ -565,12 +566,12 @@ class MbPartition final : public PartitionBase {
       }
       const pbdk::DwArgs dw{n_, L.hin, L.hin, C.L.E, C.L.k, L.stride, L.hout, L.hout};
       check(pbdk::dw_fwd(dw, a_in, C.wdF, nullptr, L.y2, 0, st), "dw");
-      check(pbdk::bn_stats(L.y2, static_cast<int>(mo), C.L.E, sb.rws, L.st2, st), "bn2 stats");
+      check(pbdk::bn_stats_fix(L.y2, nullptr, static_cast<int>(mo), C.L.E, sb.fx, L.st2, nullptr, st), "bn2 stats");
       check(pbdk::bn_apply_act(L.y2, L.st2, p + C.L.g2, p + C.L.b2, nullptr, L.a2, static_cast<long long>(mo), C.L.E, 1,
                                st),
             "bn2 apply");
       check(pbdk::fprop_run(C.p_proj, st), "project");
-      check(pbdk::bn_stats(L.y3, static_cast<int>(mo), L.cout, sb.rws, L.st3, st), "bn3 stats");
+      check(pbdk::bn_stats_fix(L.y3, nullptr, static_cast<int>(mo), L.cout, sb.fx, L.st3, nullptr, st), "bn3 stats");
       if (!L.last) {
         check(pbdk::bn_apply_act(L.y3, L.st3, p + C.L.g3, p + C.L.b3, L.res ? L.x : nullptr, L.z,
                                  static_cast<long long>(mo), L.cout, 0, st),
@@ -591,18 +592,18 @@ class MbPartition final : public PartitionBase {
       float* g = grads_ + C.off;
       const size_t mi = act_rows_hw(L.hin), mo = act_rows_hw(L.hout);
       if (L.stem) {
-        check(pbdk::bn_bwd(L.gz, L.y2, L.st2, p + C.L.g2, static_cast<int>(mo), 32, sb.rws, L.red2, g + C.L.g2,
+        check(pbdk::bn_bwd_fix(L.gz, L.y2, L.st2, p + C.L.g2, static_cast<int>(mo), 32, sb.fx, L.red2, g + C.L.g2,
                            g + C.L.b2, L.dy2, st),
               "stem bn bwd");
         check(pbdk::stem_wgrad(L.x, L.dy2, n_, S_, sb.dws, sb.dws_floats, g, st), "stem wgrad");
         continue;
       }
-      check(pbdk::bn_bwd(L.gz, L.y3, L.st3, p + C.L.g3, static_cast<int>(mo), L.cout, sb.rws, L.red3, g + C.L.g3,
+      check(pbdk::bn_bwd_fix(L.gz, L.y3, L.st3, p + C.L.g3, static_cast<int>(mo), L.cout, sb.fx, L.red3, g + C.L.g3,
                          g + C.L.b3, L.dy3, st),
             "bn3 bwd");
       check(pbdk::wgrad_run(C.w_proj, st), "wgrad project");
       check(pbdk::fprop_run(C.p_proj_dgrad, st), "dgrad project");
-      check(pbdk::bn_bwd(L.g2, L.y2, L.st2, p + C.L.g2, static_cast<int>(mo), C.L.E, sb.rws, L.red2, g + C.L.g2,
+      check(pbdk::bn_bwd_fix(L.g2, L.y2, L.st2, p + C.L.g2, static_cast<int>(mo), C.L.E, sb.fx, L.red2, g + C.L.g2,
                          g + C.L.b2, L.dy2, st),
             "bn2 bwd");
       const pbdk::DwArgs dw{n_, L.hin, L.hin, C.L.E, C.L.k, L.stride, L.hout, L.hout};
@@ -610,7 +611,7 @@ class MbPartition final : public PartitionBase {
       check(pbdk::dw_wgrad(dw, a_in, L.dy2, sb.dws, sb.dws_floats, g + C.L.wd, st), "dw wgrad");
       if (C.L.e != 1) {
         check(pbdk::dw_dgrad(dw, L.dy2, C.wdF, L.a1, L.g1, st), "dw dgrad");
-        check(pbdk::bn_bwd(L.g1, L.y1, L.st1, p + C.L.g1, static_cast<int>(mi), C.L.E, sb.rws, L.red1, g + C.L.g1,
+        check(pbdk::bn_bwd_fix(L.g1, L.y1, L.st1, p + C.L.g1, static_cast<int>(mi), C.L.E, sb.fx, L.red1, g + C.L.g1,
                            g + C.L.b1, L.dy1, st),
               "bn1 bwd");
         check(pbdk::wgrad_run(C.w_exp, st), "wgrad expand");
@@ -848,6 +849,15 @@ class MbPartition final : public PartitionBase {
       for (int l = 1; l < nl; ++l) sb.layers[static_cast<size_t>(l)].gx = sb.layers[static_cast<size_t>(l - 1)].gz;
       sb.rws_floats = rws;
       sb.rws = arena_.get<float>(rws * sizeof(float));
+      {  // zero-initialised once; every reduction's last CTA re-zeroes it
+        int cmax = 32;
+        for (const SLayer& L : sb.layers) cmax = std::max({cmax, L.Emax, L.cout});
+        const size_t words = pbdk::fix_acc_words(cmax);
+        sb.fx.acc = arena_.get<unsigned long long>(words * sizeof(unsigned long long));
+        sb.fx.ticket = arena_.get<unsigned int>(sizeof(unsigned int));
+        cuda(cudaMemset(sb.fx.acc, 0, words * sizeof(unsigned long long)), "memset");
+        cuda(cudaMemset(sb.fx.ticket, 0, sizeof(unsigned int)), "memset");
+      }
       sb.dws_floats = dws;
       sb.dws = arena_.get<float>(dws * sizeof(float));
       sb.wws_bytes = wws;
