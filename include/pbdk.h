@@ -147,6 +147,17 @@ typedef struct pbdk_mse_args {
 } pbdk_mse_args;
 int pbdk_mse_bn_loss(const pbdk_mse_args* a, void* stream);
 
+/* ------------------------------------------------------------------ K8: depthwise convolution */
+/* y[n,p,q,c] = act(sum_{r,s} x[n, p*stride+r-k/2, q*stride+s-k/2, c] * w[c][r][s] (+ bias[c])), NHWC bf16,
+ * fmaf over (r, s) ascending; wt = the flipped tap-major filter [k][k][c] (pbdk_weight_flip with c = 1).
+ * act: 0 none, 1 ReLU6, 2 swish.  variant: 0 per-strip register kernel, 1 shared-memory staged tiles,
+ * -1 the product's choice — both variants are bit-identical. */
+typedef struct pbdk_dw_desc {
+  int n, h, w, c, k, stride, p, q;
+} pbdk_dw_desc;
+int pbdk_dw_fwd(const pbdk_dw_desc* d, const void* x, const void* wt, const float* bias, void* y, int act,
+                int variant, void* stream);
+
 /* ------------------------------------------------------------------ K10: SGD-momentum update */
 /* v = mu*v + g; w = w - lr*v (fmaf); w_bf16 (may be NULL) = bf16(w); ++*step_counter (may be NULL).
  * n must be a multiple of 4. */

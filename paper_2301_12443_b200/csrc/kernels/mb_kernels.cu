@@ -21,6 +21,8 @@
 #include "knobs.hpp"
 #include "mb_kernels.hpp"
 #include "pbdk.h"
+#include "sm100.cuh"
+#include "tmap.hpp"
 
 namespace pbdk {
 
@@ -147,6 +149,129 @@ __global__ void __launch_bounds__(kT) dw_fwd_kernel(const __nv_bfloat16* __restr
       }
       st8(y + ((static_cast<size_t>(row) * Q) + q0 + u) * C + c0, o);
     }
+  }
+}
+
+// ------------------------------------------------------------------ depthwise forward, shared-memory tiles
+// Tile = (image n, TP output rows, all Q columns, CT channels).  ONE 4D TMA box per tile stages the
+// input window — (TP-1)*ST + K rows x (Q-1)*ST + K columns x CT channels, the padding zero-filled by
+// the TMA out-of-bounds handling — plus a 2D box of the filter slice [K*K][CT], double-buffered across
+// the CTA's tiles on mbarriers; every input vector leaves HBM/L2 once per tile instead of once per
+// (filter row, output strip) as in dw_fwd_kernel, which was memory-latency bound (ncu: 1.7 TB/s,
+// long-scoreboard stalls at 33 % occupancy).  Thread item = (output row, strip of kQTT = 7 columns —
+// the MBConv maps are 7 * 2^i wide — , 8-channel group); TP is chosen so a tile holds a whole number
+// of 256-item rounds where the shared-memory budget allows.  Per output the fmaf order is (r, s)
+// ascending — bit-identical to dw_fwd_kernel and the oracle (padding taps add +-0 products to an
+// accumulator that is never -0).
+constexpr int kQTT = 7;
+constexpr int kDwStages = 2;
+constexpr int kDwTileBytes = 64 * 1024;  // one stage (input window + filter)
+
+template <int K, int ST, int CT>
+__global__ void __launch_bounds__(kT) dw_fwd_tiled_kernel(const __grid_constant__ CUtensorMap tmx,
+                                                          const __grid_constant__ CUtensorMap tmw,
+                                                          const float* __restrict__ bias,
+                                                          __nv_bfloat16* __restrict__ y, int N, int C, int P, int Q,
+                                                          int act, int TP) {
+  constexpr int PAD = K / 2;
+  constexpr int G = CT / 8;
+  constexpr int WIN = (kQTT - 1) * ST + K;
+  extern __shared__ __align__(128) uint8_t dsm_base[];
+  uint8_t* dsm_raw = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_base) + 127) & ~uintptr_t(127));
+  __shared__ uint64_t full[kDwStages];
+  const int cols_in = (Q - 1) * ST + K;
+  const int rows_in = (TP - 1) * ST + K;
+  const uint32_t x_bytes = static_cast<uint32_t>(rows_in) * cols_in * CT * 2;
+  const uint32_t x_off = (x_bytes + 127) / 128 * 128;  // the filter box starts 128-B aligned
+  const uint32_t w_bytes = K * K * CT * 2;
+  const uint32_t stage_bytes = (x_off + w_bytes + 127) / 128 * 128;
+  const int pblocks = (P + TP - 1) / TP;
+  const int cblocks = C / CT;
+  const int ntiles = N * pblocks * cblocks;
+  const int strips = (Q + kQTT - 1) / kQTT;
+
+  auto tile_of = [&](int t, int& n, int& p0, int& c0) {
+    const int cb = t % cblocks;
+    const int rest = t / cblocks;
+    p0 = (rest % pblocks) * TP;
+    n = rest / pblocks;
+    c0 = cb * CT;
+  };
+  auto issue = [&](int t, int slot) {
+    int n, p0, c0;
+    tile_of(t, n, p0, c0);
+    uint8_t* buf = dsm_raw + slot * stage_bytes;
+    mbar_arrive_expect_tx(&full[slot], x_bytes + w_bytes);
+    tma_load_4d(buf, &tmx, &full[slot], c0, -PAD, p0 * ST - PAD, n);
+    tma_load_2d(buf + x_off, &tmw, &full[slot], c0, 0);
+  };
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kDwStages; ++i) mbar_init(&full[i], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int s = 0; s < kDwStages; ++s)
+      if (blockIdx.x + s * gridDim.x < ntiles) issue(blockIdx.x + s * gridDim.x, s);
+  int it = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const int slot = it % kDwStages;
+    mbar_wait(&full[slot], (it / kDwStages) & 1);
+    const uint4* cur = reinterpret_cast<const uint4*>(dsm_raw + slot * stage_bytes);
+    const uint4* wsm = reinterpret_cast<const uint4*>(dsm_raw + slot * stage_bytes + x_off);
+    int n, p0, c0;
+    tile_of(t, n, p0, c0);
+    const int rows = min(TP, P - p0);
+    const int items = rows * strips * G;
+    for (int i = threadIdx.x; i < items; i += blockDim.x) {
+      const int g = i % G;
+      const int rest = i / G;
+      const int q0 = (rest % strips) * kQTT;
+      const int pr = rest / strips;
+      float acc[kQTT][8];
+#pragma unroll
+      for (int u = 0; u < kQTT; ++u)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[u][j] = 0.0f;
+#pragma unroll
+      for (int r = 0; r < K; ++r) {
+        float wr[K][8];  // w[c][r][s] = wt[K-1-r][K-1-s][c]
+#pragma unroll
+        for (int sidx = 0; sidx < K; ++sidx)
+          ld8(reinterpret_cast<const __nv_bfloat16*>(wsm + ((K - 1 - r) * K + (K - 1 - sidx)) * G + g), wr[sidx]);
+        const uint4* xrow = cur + ((pr * ST + r) * cols_in + q0 * ST) * G + g;
+#pragma unroll
+        for (int j = 0; j < WIN; ++j) {
+          if (q0 * ST + j >= cols_in) break;
+          float xv[8];
+          ld8(reinterpret_cast<const __nv_bfloat16*>(xrow + j * G), xv);
+#pragma unroll
+          for (int u = 0; u < kQTT; ++u) {
+            const int sidx = j - u * ST;
+            if (sidx < 0 || sidx >= K) continue;
+            fma8(acc[u], xv, wr[sidx]);
+          }
+        }
+      }
+      const size_t orow = (static_cast<size_t>(n) * P + p0 + pr) * Q;
+      float bv[8];
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) bv[jj] = bias != nullptr ? bias[c0 + 8 * g + jj] : 0.0f;
+#pragma unroll
+      for (int u = 0; u < kQTT; ++u) {
+        if (q0 + u >= Q) break;
+        float o[8];
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          float v = acc[u][jj];
+          if (bias != nullptr) v = v + bv[jj];
+          o[jj] = act_fn(act, v);
+        }
+        st8(y + (orow + q0 + u) * C + c0 + 8 * g, o);
+      }
+    }
+    __syncthreads();  // slot fully read: refill it with the tile kDwStages ahead
+    if (threadIdx.x == 0 && t + kDwStages * gridDim.x < ntiles) issue(t + kDwStages * gridDim.x, slot);
   }
 }
 
@@ -676,8 +801,99 @@ size_t dw_wgrad_workspace_floats(const DwArgs& d) {
   return static_cast<size_t>(dw_wgrad_tiling(d).chunks) * d.c * d.k * d.k;
 }
 
-int dw_fwd(const DwArgs& d, const void* x, const void* wt, const float* bias, void* y, int relu6, cudaStream_t s) {
+// staged-tile plan of dw_fwd_tiled_kernel: CT channels per tile (64 / 128 for narrow maps), TP output rows
+// = the largest that fits kDwTileBytes, rounded down to a whole number of 256-item rounds when possible
+struct DwTilePlan {
+  int ct = 0, tp = 0;
+  size_t smem = 0;
+};
+DwTilePlan dw_tile_plan(const DwArgs& d) {
+  DwTilePlan t;
+  if (pbd::knob_env("PBDK_DW_TILED") != nullptr && std::atoi(pbd::knob_env("PBDK_DW_TILED")) == 0) return t;
+  int ct = d.q <= 7 && d.c % 128 == 0 ? 128 : d.q <= 14 && d.c % 64 == 0 ? 64 : d.c % 32 == 0 ? 32 : 0;
+  if (ct == 0) return t;
+  const int cols_in = (d.q - 1) * d.stride + d.k;
+  if (cols_in > 256) return t;  // TMA box extent
+  const size_t row_bytes = static_cast<size_t>(cols_in) * ct * 2;
+  const size_t w_bytes = static_cast<size_t>(d.k) * d.k * ct * 2;
+  const int rows_max = static_cast<int>((kDwTileBytes - w_bytes) / row_bytes);
+  if (rows_max < d.k) return t;
+  const int tp_max = std::min({d.p, (rows_max - d.k) / d.stride + 1, (256 - d.k) / d.stride + 1});
+  const int per_row = ((d.q + kQTT - 1) / kQTT) * (ct / 8);
+  int tp = tp_max;
+  for (int c = tp_max; c >= 1; --c)  // prefer whole 256-item rounds (no idle half-round at the barrier)
+    if ((c * per_row) % kT == 0) {
+      tp = c;
+      break;
+    }
+  if (tp < tp_max / 2) tp = tp_max;
+  t.ct = ct;
+  t.tp = tp;
+  const size_t rows_in = static_cast<size_t>(tp - 1) * d.stride + d.k;
+  t.smem = kDwStages * ((((rows_in * row_bytes + 127) / 128 * 128) + w_bytes + 127) / 128 * 128) + 128;
+  return t;
+}
+
+template <int K, int ST, int CT>
+cudaError_t launch_dw_fwd_tiled(const DwArgs& d, const DwTilePlan& t, const void* x, const void* wt,
+                                const float* bias, void* y, int act, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e = cudaFuncSetAttribute(dw_fwd_tiled_kernel<K, ST, CT>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               kDwStages * (kDwTileBytes + 256) + 128);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  CUtensorMap tmx, tmw;
+  {
+    const int cols_in = (d.q - 1) * d.stride + d.k, rows_in = (t.tp - 1) * d.stride + d.k;
+    const uint64_t dims[4] = {static_cast<uint64_t>(d.c), static_cast<uint64_t>(d.w), static_cast<uint64_t>(d.h),
+                              static_cast<uint64_t>(d.n)};
+    const uint64_t strides[3] = {static_cast<uint64_t>(d.c) * 2, static_cast<uint64_t>(d.w) * d.c * 2,
+                                 static_cast<uint64_t>(d.h) * d.w * d.c * 2};
+    const uint32_t box[4] = {static_cast<uint32_t>(CT), static_cast<uint32_t>(cols_in),
+                             static_cast<uint32_t>(rows_in), 1};
+    const uint32_t es[4] = {1, 1, 1, 1};
+    if (!encode_tmap_bf16(&tmx, x, 4, dims, strides, box, es, 0)) return cudaErrorInvalidValue;
+    const uint64_t wd[2] = {static_cast<uint64_t>(d.c), static_cast<uint64_t>(K * K)};
+    const uint64_t ws[1] = {static_cast<uint64_t>(d.c) * 2};
+    const uint32_t wb[2] = {static_cast<uint32_t>(CT), static_cast<uint32_t>(K * K)};
+    const uint32_t we[2] = {1, 1};
+    if (!encode_tmap_bf16(&tmw, wt, 2, wd, ws, wb, we, 0)) return cudaErrorInvalidValue;
+  }
+  const long long tiles = static_cast<long long>(d.n) * ((d.p + t.tp - 1) / t.tp) * (d.c / CT);
+  const int per_sm = t.smem * 2 <= 200 * 1024 ? 2 : 1;
+  const int grid = static_cast<int>(std::min<long long>(tiles, 148LL * per_sm));
+  dw_fwd_tiled_kernel<K, ST, CT><<<grid, kT, t.smem, s>>>(tmx, tmw, bias, static_cast<__nv_bfloat16*>(y), d.n, d.c,
+                                                         d.p, d.q, act, t.tp);
+  return cudaGetLastError();
+}
+
+template <int K>
+cudaError_t dw_fwd_tiled(const DwArgs& d, const DwTilePlan& t, const void* x, const void* wt, const float* bias,
+                         void* y, int act, cudaStream_t s) {
+  if (d.stride == 1)
+    return t.ct == 128 ? launch_dw_fwd_tiled<K, 1, 128>(d, t, x, wt, bias, y, act, s)
+           : t.ct == 64 ? launch_dw_fwd_tiled<K, 1, 64>(d, t, x, wt, bias, y, act, s)
+                        : launch_dw_fwd_tiled<K, 1, 32>(d, t, x, wt, bias, y, act, s);
+  return t.ct == 128 ? launch_dw_fwd_tiled<K, 2, 128>(d, t, x, wt, bias, y, act, s)
+         : t.ct == 64 ? launch_dw_fwd_tiled<K, 2, 64>(d, t, x, wt, bias, y, act, s)
+                      : launch_dw_fwd_tiled<K, 2, 32>(d, t, x, wt, bias, y, act, s);
+}
+
+int dw_fwd(const DwArgs& d, const void* x, const void* wt, const float* bias, void* y, int relu6, cudaStream_t s,
+           int variant) {
   if (!dw_ok(d)) return PBDK_EINVAL;
+  const DwTilePlan t = dw_tile_plan(d);
+  if (variant == 1 && t.ct == 0) return PBDK_EINVAL;
+  if (variant != 0 && t.ct != 0) {
+    switch (d.k) {
+      case 3: return ok(dw_fwd_tiled<3>(d, t, x, wt, bias, y, relu6, s));
+      case 5: return ok(dw_fwd_tiled<5>(d, t, x, wt, bias, y, relu6, s));
+      default: return ok(dw_fwd_tiled<7>(d, t, x, wt, bias, y, relu6, s));
+    }
+  }
   switch (d.k) {
     case 3: return ok(launch_dw_fwd<3>(d.stride, d, x, wt, bias, y, relu6, s));
     case 5: return ok(launch_dw_fwd<5>(d.stride, d, x, wt, bias, y, relu6, s));
@@ -775,3 +991,13 @@ int mse_affine(const void* y, const float* mean_rstd, const float* gamma, const 
 }
 
 }  // namespace pbdk
+
+// ------------------------------------------------------------------ C ABI
+extern "C" int pbdk_dw_fwd(const pbdk_dw_desc* d, const void* x, const void* wt, const float* bias, void* y, int act,
+                           int variant, void* stream) {
+  if (d == nullptr || x == nullptr || wt == nullptr || y == nullptr || act < 0 || act > 2 || variant < -1 ||
+      variant > 1)
+    return PBDK_EINVAL;
+  const pbdk::DwArgs a{d->n, d->h, d->w, d->c, d->k, d->stride, d->p, d->q};
+  return pbdk::dw_fwd(a, x, wt, bias, y, act, static_cast<cudaStream_t>(stream), variant);
+}

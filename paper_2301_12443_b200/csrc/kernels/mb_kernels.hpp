@@ -16,7 +16,9 @@ struct DwArgs {
 
 // activation codes of dw_fwd / stem_fwd: 0 none, 1 ReLU6, 2 swish
 // y = act(dw(x) [+ bias]); wt = flipped tap-major weights wt[r'][s'][c]
-int dw_fwd(const DwArgs& d, const void* x, const void* wt, const float* bias, void* y, int relu6, cudaStream_t s);
+// variant: -1 product choice (staged tiles where they fit), 0 per-strip kernel, 1 staged tiles (bit-identical)
+int dw_fwd(const DwArgs& d, const void* x, const void* wt, const float* bias, void* y, int relu6, cudaStream_t s,
+           int variant = -1);
 // dx = dw^T(dy) [masked by 0 < act < 6]
 int dw_dgrad(const DwArgs& d, const void* dy, const void* wt, const void* act, void* dx, cudaStream_t s);
 // dw[c][r][s] (fp32, the parameter layout) = sum dy * shifted a
