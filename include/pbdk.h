@@ -157,6 +157,10 @@ typedef struct pbdk_dw_desc {
 } pbdk_dw_desc;
 int pbdk_dw_fwd(const pbdk_dw_desc* d, const void* x, const void* wt, const float* bias, void* y, int act,
                 int variant, void* stream);
+/* dx[n,h,w,c] = fmaf chain over (r, s) ascending of dy[n,(h+k/2-r)/stride,(w+k/2-s)/stride,c] * w[c][r][s],
+ * then the ReLU6 mask of `act` (0 < a < 6; NULL: none).  variant as pbdk_dw_fwd (staged tiles: stride 1). */
+int pbdk_dw_dgrad(const pbdk_dw_desc* d, const void* dy, const void* wt, const void* act, void* dx, int variant,
+                  void* stream);
 
 /* ------------------------------------------------------------------ K10: SGD-momentum update */
 /* v = mu*v + g; w = w - lr*v (fmaf); w_bf16 (may be NULL) = bf16(w); ++*step_counter (may be NULL).

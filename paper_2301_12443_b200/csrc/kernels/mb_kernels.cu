@@ -167,12 +167,16 @@ constexpr int kQTT = 7;
 constexpr int kDwStages = 2;
 constexpr int kDwTileBytes = 64 * 1024;  // one stage (input window + filter)
 
-template <int K, int ST, int CT>
+// DG: the stride-1 depthwise DATA gradient on the same tiles — dx = the correlation of dy with the
+// spatially flipped filter, taps visited in descending window order so every output's fmaf chain is
+// dw_dgrad_kernel's (r, s) ascending; epilogue = the ReLU6 mask of the stored activation `amask`.
+template <int K, int ST, int CT, bool DG = false>
 __global__ void __launch_bounds__(kT) dw_fwd_tiled_kernel(const __grid_constant__ CUtensorMap tmx,
                                                           const __grid_constant__ CUtensorMap tmw,
                                                           const float* __restrict__ bias,
                                                           __nv_bfloat16* __restrict__ y, int N, int C, int P, int Q,
-                                                          int act, int TP) {
+                                                          int act, int TP,
+                                                          const __nv_bfloat16* __restrict__ amask = nullptr) {
   constexpr int PAD = K / 2;
   constexpr int G = CT / 8;
   constexpr int WIN = (kQTT - 1) * ST + K;
@@ -234,15 +238,19 @@ __global__ void __launch_bounds__(kT) dw_fwd_tiled_kernel(const __grid_constant_
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[u][j] = 0.0f;
 #pragma unroll
-      for (int r = 0; r < K; ++r) {
-        float wr[K][8];  // w[c][r][s] = wt[K-1-r][K-1-s][c]
+      for (int ri = 0; ri < K; ++ri) {
+        const int r = DG ? K - 1 - ri : ri;  // window row
+        float wr[K][8];  // forward: w[c][r][s] = wt[K-1-r][K-1-s][c]; data gradient: w[c][K-1-r][K-1-s] = wt[r][s][c]
 #pragma unroll
         for (int sidx = 0; sidx < K; ++sidx)
-          ld8(reinterpret_cast<const __nv_bfloat16*>(wsm + ((K - 1 - r) * K + (K - 1 - sidx)) * G + g), wr[sidx]);
+          ld8(reinterpret_cast<const __nv_bfloat16*>(
+                  wsm + (DG ? r * K + sidx : (K - 1 - r) * K + (K - 1 - sidx)) * G + g),
+              wr[sidx]);
         const uint4* xrow = cur + ((pr * ST + r) * cols_in + q0 * ST) * G + g;
 #pragma unroll
-        for (int j = 0; j < WIN; ++j) {
-          if (q0 * ST + j >= cols_in) break;
+        for (int jj = 0; jj < WIN; ++jj) {
+          const int j = DG ? WIN - 1 - jj : jj;
+          if (q0 * ST + j >= cols_in) continue;
           float xv[8];
           ld8(reinterpret_cast<const __nv_bfloat16*>(xrow + j * G), xv);
 #pragma unroll
@@ -261,11 +269,23 @@ __global__ void __launch_bounds__(kT) dw_fwd_tiled_kernel(const __grid_constant_
       for (int u = 0; u < kQTT; ++u) {
         if (q0 + u >= Q) break;
         float o[8];
+        if constexpr (DG) {
+          if (amask != nullptr) {
+            float av[8];
+            ld8(amask + (orow + q0 + u) * C + c0 + 8 * g, av);
 #pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-          float v = acc[u][jj];
-          if (bias != nullptr) v = v + bv[jj];
-          o[jj] = act_fn(act, v);
+            for (int jj = 0; jj < 8; ++jj) o[jj] = (av[jj] > 0.0f && av[jj] < 6.0f) ? acc[u][jj] : 0.0f;
+          } else {
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) o[jj] = acc[u][jj];
+          }
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            float v = acc[u][jj];
+            if (bias != nullptr) v = v + bv[jj];
+            o[jj] = act_fn(act, v);
+          }
         }
         st8(y + (orow + q0 + u) * C + c0 + 8 * g, o);
       }
@@ -834,12 +854,12 @@ DwTilePlan dw_tile_plan(const DwArgs& d) {
   return t;
 }
 
-template <int K, int ST, int CT>
+template <int K, int ST, int CT, bool DG = false>
 cudaError_t launch_dw_fwd_tiled(const DwArgs& d, const DwTilePlan& t, const void* x, const void* wt,
-                                const float* bias, void* y, int act, cudaStream_t s) {
+                                const float* bias, void* y, int act, cudaStream_t s, const void* amask = nullptr) {
   static bool attr = false;
   if (!attr) {
-    const cudaError_t e = cudaFuncSetAttribute(dw_fwd_tiled_kernel<K, ST, CT>,
+    const cudaError_t e = cudaFuncSetAttribute(dw_fwd_tiled_kernel<K, ST, CT, DG>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                kDwStages * (kDwTileBytes + 256) + 128);
     if (e != cudaSuccess) return e;
@@ -865,8 +885,9 @@ cudaError_t launch_dw_fwd_tiled(const DwArgs& d, const DwTilePlan& t, const void
   const long long tiles = static_cast<long long>(d.n) * ((d.p + t.tp - 1) / t.tp) * (d.c / CT);
   const int per_sm = t.smem * 2 <= 200 * 1024 ? 2 : 1;
   const int grid = static_cast<int>(std::min<long long>(tiles, 148LL * per_sm));
-  dw_fwd_tiled_kernel<K, ST, CT><<<grid, kT, t.smem, s>>>(tmx, tmw, bias, static_cast<__nv_bfloat16*>(y), d.n, d.c,
-                                                         d.p, d.q, act, t.tp);
+  dw_fwd_tiled_kernel<K, ST, CT, DG><<<grid, kT, t.smem, s>>>(tmx, tmw, bias, static_cast<__nv_bfloat16*>(y), d.n,
+                                                             d.c, d.p, d.q, act, t.tp,
+                                                             static_cast<const __nv_bfloat16*>(amask));
   return cudaGetLastError();
 }
 
@@ -901,8 +922,30 @@ int dw_fwd(const DwArgs& d, const void* x, const void* wt, const float* bias, vo
   }
 }
 
-int dw_dgrad(const DwArgs& d, const void* dy, const void* wt, const void* act, void* dx, cudaStream_t s) {
+// stride-1 data gradient on the staged tiles: the tile geometry of the forward over dy (H = P, W = Q)
+template <int K>
+cudaError_t dw_dgrad_tiled(const DwArgs& d, const DwTilePlan& t, const void* dy, const void* wt, const void* act,
+                           void* dx, cudaStream_t s) {
+  const DwArgs g{d.n, d.p, d.q, d.c, d.k, 1, d.h, d.w};
+  return t.ct == 128 ? launch_dw_fwd_tiled<K, 1, 128, true>(g, t, dy, wt, nullptr, dx, 0, s, act)
+         : t.ct == 64 ? launch_dw_fwd_tiled<K, 1, 64, true>(g, t, dy, wt, nullptr, dx, 0, s, act)
+                      : launch_dw_fwd_tiled<K, 1, 32, true>(g, t, dy, wt, nullptr, dx, 0, s, act);
+}
+
+int dw_dgrad(const DwArgs& d, const void* dy, const void* wt, const void* act, void* dx, cudaStream_t s,
+             int variant) {
   if (!dw_ok(d)) return PBDK_EINVAL;
+  if (variant != 0 && d.stride == 1) {
+    const DwTilePlan t = dw_tile_plan(d);  // stride 1: the same geometry as the forward
+    if (t.ct != 0) {
+      switch (d.k) {
+        case 3: return ok(dw_dgrad_tiled<3>(d, t, dy, wt, act, dx, s));
+        case 5: return ok(dw_dgrad_tiled<5>(d, t, dy, wt, act, dx, s));
+        default: return ok(dw_dgrad_tiled<7>(d, t, dy, wt, act, dx, s));
+      }
+    }
+  }
+  if (variant == 1) return PBDK_EINVAL;
   switch (d.k) {
     case 3: return ok(launch_dw_dgrad<3>(d.stride, d, dy, wt, act, dx, s));
     case 5: return ok(launch_dw_dgrad<5>(d.stride, d, dy, wt, act, dx, s));
@@ -993,6 +1036,14 @@ int mse_affine(const void* y, const float* mean_rstd, const float* gamma, const 
 }  // namespace pbdk
 
 // ------------------------------------------------------------------ C ABI
+extern "C" int pbdk_dw_dgrad(const pbdk_dw_desc* d, const void* dy, const void* wt, const void* act, void* dx,
+                             int variant, void* stream) {
+  if (d == nullptr || dy == nullptr || wt == nullptr || dx == nullptr || variant < -1 || variant > 1)
+    return PBDK_EINVAL;
+  const pbdk::DwArgs a{d->n, d->h, d->w, d->c, d->k, d->stride, d->p, d->q};
+  return pbdk::dw_dgrad(a, dy, wt, act, dx, static_cast<cudaStream_t>(stream), variant);
+}
+
 extern "C" int pbdk_dw_fwd(const pbdk_dw_desc* d, const void* x, const void* wt, const float* bias, void* y, int act,
                            int variant, void* stream) {
   if (d == nullptr || x == nullptr || wt == nullptr || y == nullptr || act < 0 || act > 2 || variant < -1 ||

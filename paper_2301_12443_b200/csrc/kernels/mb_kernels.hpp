@@ -20,7 +20,9 @@ struct DwArgs {
 int dw_fwd(const DwArgs& d, const void* x, const void* wt, const float* bias, void* y, int relu6, cudaStream_t s,
            int variant = -1);
 // dx = dw^T(dy) [masked by 0 < act < 6]
-int dw_dgrad(const DwArgs& d, const void* dy, const void* wt, const void* act, void* dx, cudaStream_t s);
+// variant as dw_fwd (the staged tiles serve stride 1)
+int dw_dgrad(const DwArgs& d, const void* dy, const void* wt, const void* act, void* dx, cudaStream_t s,
+             int variant = -1);
 // dw[c][r][s] (fp32, the parameter layout) = sum dy * shifted a
 size_t dw_wgrad_workspace_floats(const DwArgs& d);
 int dw_wgrad(const DwArgs& d, const void* a, const void* dy, float* ws, size_t ws_floats, float* dw, cudaStream_t s);

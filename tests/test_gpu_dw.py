@@ -49,3 +49,33 @@ def test_staged_tiles_bitwise_equal_per_strip(L, n, h, c, k, st, act):
     if act == 1:
         ref = ref.clamp(0.0, 6.0)
     assert (ys[1].float() - ref).abs().max().item() <= 2e-2 * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("n,h,c,k", [(2, 112, 32, 3), (2, 56, 192, 5), (3, 28, 384, 7), (3, 14, 576, 3),
+                                     (4, 7, 1152, 5), (2, 30, 64, 3)])
+@pytest.mark.parametrize("masked", [False, True])
+def test_dgrad_staged_tiles_bitwise_equal_per_pixel(L, n, h, c, k, masked):
+    L.pbdk_dw_dgrad.argtypes = [ctypes.POINTER(DwDesc), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+    torch.manual_seed(n + h + c + k)
+    d = DwDesc(n, h, h, c, k, 1, h, h)
+    dy = torch.randn(n, h, h, c, device="cuda").bfloat16()
+    w = (torch.randn(c, k, k, device="cuda") * 0.3).bfloat16()
+    wt = w.permute(1, 2, 0).flip(0, 1).contiguous()
+    act = (torch.rand(n, h, h, c, device="cuda") * 9.0 - 1.5).bfloat16() if masked else None
+    outs = []
+    for variant in (0, 1):
+        dx = torch.full((n, h, h, c), 7.0, device="cuda").bfloat16()
+        s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        assert L.pbdk_dw_dgrad(ctypes.byref(d), dy.data_ptr(), wt.data_ptr(),
+                               act.data_ptr() if masked else None, dx.data_ptr(), variant, s) == 0
+        outs.append(dx)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16))
+    # dx = correlation of dy with the spatially flipped filter (stride 1, pad k // 2)
+    ref = F.conv2d(dy.float().permute(0, 3, 1, 2), w.float().flip(1, 2)[:, None], padding=k // 2, groups=c)
+    ref = ref.permute(0, 2, 3, 1)
+    if masked:
+        a = act.float()
+        ref = torch.where((a > 0) & (a < 6), ref, torch.zeros_like(ref))
+    assert (outs[1].float() - ref).abs().max().item() <= 2e-2 * ref.abs().max().item()
