@@ -30,6 +30,15 @@ for (n, h, c, k, r, st) in [(96, 32, 16, 32, 3, 1), (96, 32, 32, 64, 3, 1), (128
     assert L.pbdk_conv_wgrad(ctypes.byref(d), x.data_ptr(), dy.data_ptr(), dw.data_ptr(), ws.data_ptr(), wsb,
                              ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)) == 0
 torch.cuda.synchronize()
+# round 2: the ProxylessNAS step (the path changes between its two rounds)
+from paper_2301_12443_b200 import nas, mb_models
+mb_models.set_family("mbv2")
+arch = nas.ArchParams(range(6))
+for s_ in range(2):
+    nas.nas_step(m, arch, s_)
+# (the multi-rank C++ driver is not run here: its ranks wait on each other's device-side flags from
+# concurrent streams, and the sanitizer serialises kernels — the first spin wait would time out)
+torch.cuda.synchronize()
 print("ok", p.losses(), m.losses(), e.losses(), q.losses())
 PY
 for tool in memcheck racecheck synccheck; do
