@@ -164,6 +164,9 @@ __global__ void __launch_bounds__(kT) dw_fwd_kernel(const __nv_bfloat16* __restr
 // ascending — bit-identical to dw_fwd_kernel and the oracle (padding taps add +-0 products to an
 // accumulator that is never -0).
 constexpr int kQTT = 7;
+// output columns per thread item: 7 for 3x3 filters; 4 for 5x5 / 7x7, whose filter rows and input
+// windows would otherwise push the kernel to one CTA per SM (ncu: 154-158 registers at kQTT = 7)
+__host__ __device__ constexpr int dw_qt(int k) { return k == 3 ? kQTT : 4; }
 constexpr int kDwStages = 2;
 constexpr int kDwTileBytes = 64 * 1024;  // one stage (input window + filter)
 
@@ -179,7 +182,8 @@ __global__ void __launch_bounds__(kT) dw_fwd_tiled_kernel(const __grid_constant_
                                                           const __nv_bfloat16* __restrict__ amask = nullptr) {
   constexpr int PAD = K / 2;
   constexpr int G = CT / 8;
-  constexpr int WIN = (kQTT - 1) * ST + K;
+  constexpr int QT = dw_qt(K);
+  constexpr int WIN = (QT - 1) * ST + K;
   extern __shared__ __align__(128) uint8_t dsm_base[];
   uint8_t* dsm_raw = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_base) + 127) & ~uintptr_t(127));
   __shared__ uint64_t full[kDwStages];
@@ -192,7 +196,7 @@ __global__ void __launch_bounds__(kT) dw_fwd_tiled_kernel(const __grid_constant_
   const int pblocks = (P + TP - 1) / TP;
   const int cblocks = C / CT;
   const int ntiles = N * pblocks * cblocks;
-  const int strips = (Q + kQTT - 1) / kQTT;
+  const int strips = (Q + QT - 1) / QT;
 
   auto tile_of = [&](int t, int& n, int& p0, int& c0) {
     const int cb = t % cblocks;
@@ -230,11 +234,11 @@ __global__ void __launch_bounds__(kT) dw_fwd_tiled_kernel(const __grid_constant_
     for (int i = threadIdx.x; i < items; i += blockDim.x) {
       const int g = i % G;
       const int rest = i / G;
-      const int q0 = (rest % strips) * kQTT;
+      const int q0 = (rest % strips) * QT;
       const int pr = rest / strips;
-      float acc[kQTT][8];
+      float acc[QT][8];
 #pragma unroll
-      for (int u = 0; u < kQTT; ++u)
+      for (int u = 0; u < QT; ++u)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[u][j] = 0.0f;
 #pragma unroll
@@ -254,7 +258,7 @@ __global__ void __launch_bounds__(kT) dw_fwd_tiled_kernel(const __grid_constant_
           float xv[8];
           ld8(reinterpret_cast<const __nv_bfloat16*>(xrow + j * G), xv);
 #pragma unroll
-          for (int u = 0; u < kQTT; ++u) {
+          for (int u = 0; u < QT; ++u) {
             const int sidx = j - u * ST;
             if (sidx < 0 || sidx >= K) continue;
             fma8(acc[u], xv, wr[sidx]);
@@ -266,7 +270,7 @@ __global__ void __launch_bounds__(kT) dw_fwd_tiled_kernel(const __grid_constant_
 #pragma unroll
       for (int jj = 0; jj < 8; ++jj) bv[jj] = bias != nullptr ? bias[c0 + 8 * g + jj] : 0.0f;
 #pragma unroll
-      for (int u = 0; u < kQTT; ++u) {
+      for (int u = 0; u < QT; ++u) {
         if (q0 + u >= Q) break;
         float o[8];
         if constexpr (DG) {
@@ -839,7 +843,7 @@ DwTilePlan dw_tile_plan(const DwArgs& d) {
   const int rows_max = static_cast<int>((kDwTileBytes - w_bytes) / row_bytes);
   if (rows_max < d.k) return t;
   const int tp_max = std::min({d.p, (rows_max - d.k) / d.stride + 1, (256 - d.k) / d.stride + 1});
-  const int per_row = ((d.q + kQTT - 1) / kQTT) * (ct / 8);
+  const int per_row = ((d.q + dw_qt(d.k) - 1) / dw_qt(d.k)) * (ct / 8);
   int tp = tp_max;
   for (int c = tp_max; c >= 1; --c)  // prefer whole 256-item rounds (no idle half-round at the barrier)
     if ((c * per_row) % kT == 0) {
