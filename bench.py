@@ -146,12 +146,17 @@ def ncu_traffic(kernel_key):
 
 def time_dominant_kernel(torch, batch):
     """CUDA-event timing of the dominant kernel (teacher block-0 3x3 conv, 64->64 @32x32 with the
-    bias+ReLU epilogue, tcgen05) launched alone: 50 back-to-back launches replayed from a CUDA graph
-    on the current stream (so host-side plan building and ctypes overhead stay out of the device
-    timing); algorithmic FLOPs = 2*M*N*K."""
+    bias+ReLU epilogue, tcgen05 — the single conv shape with the largest time per step, 4 launches)
+    launched alone with the step's own plan settings (two epilogue warps per TMEM lane quarter, the
+    ResNet executor's ConvGridScope): 50 back-to-back launches replayed from a CUDA graph on the
+    current stream (so host-side plan building and ctypes overhead stay out of the device timing);
+    algorithmic FLOPs = 2*M*N*K."""
     import ctypes
     from paper_2301_12443_b200 import _lib
     L = _lib.lib()
+    L.pbdk_conv_scope.argtypes = [ctypes.c_int, ctypes.c_int]
+    L.pbdk_conv_scope.restype = None
+    L.pbdk_conv_scope(0, 2)
     d = _lib.ConvDesc(batch, 32, 32, 64, 64, 3, 3, 1, 1, 32, 32)
     x = torch.randn(batch, 32, 32, 64, device="cuda").bfloat16()
     w = (torch.randn(64, 3, 3, 64, device="cuda") * 0.05).bfloat16()
@@ -180,6 +185,7 @@ def time_dominant_kernel(torch, batch):
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
+    L.pbdk_conv_scope(0, 0)
     flops = 2.0 * batch * 32 * 32 * 64 * 9 * 64
     return "conv_fprop_bn64_bkc64", flops, ms
 

@@ -60,6 +60,10 @@ const char* pbdk_build_info(void);
 
 /* y[n,p,q,k] = epi( sum_{r,s,c} x[n, p*st+r-pad, q*st+s-pad, c] * w[k,r,s,c] )
  * tcgen05 implicit GEMM: M = n*p*q pixels (128 per tile), N = k, K = r*s*c. */
+/* Plans built by later pbdk_conv_fprop calls on this thread use at most `sms` SMs (0 = all) and, with
+ * epw = 2, two epilogue warps per TMEM lane quarter — the settings the ResNet executor builds its
+ * plans with (ConvGridScope); pbdk_conv_scope(0, 0) restores the shape defaults. */
+void pbdk_conv_scope(int sms, int epw);
 int pbdk_conv_fprop(const pbdk_conv_desc* d, const void* x, const void* w, void* y, const float* bias,
                     const void* aux, int epilogue, void* stream);
 

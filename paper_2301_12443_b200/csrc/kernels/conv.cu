@@ -1969,6 +1969,11 @@ extern "C" {
 
 const char* pbdk_build_info(void) { return "pbdk sm_100a tcgen05"; }
 
+void pbdk_conv_scope(int sms, int epw) {
+  pbdk::t_grid_sms = sms > 0 ? sms : 0;
+  pbdk::t_epw = epw == 2 ? 2 : 0;
+}
+
 int pbdk_conv_fprop(const pbdk_conv_desc* d, const void* x, const void* w, void* y, const float* bias,
                     const void* aux, int epilogue, void* stream) {
   if (d == nullptr) return PBDK_EINVAL;

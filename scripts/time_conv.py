@@ -5,6 +5,10 @@ from paper_2301_12443_b200 import _lib
 n, h, c, k, r, st = (int(v) for v in sys.argv[1:7])
 epi = int(sys.argv[7]) if len(sys.argv) > 7 else 0
 L = _lib.lib()
+if os.environ.get("STEP_SCOPE"):  # the ResNet executor's plan settings (two epilogue warps per lane quarter)
+    L.pbdk_conv_scope.argtypes = [ctypes.c_int, ctypes.c_int]
+    L.pbdk_conv_scope.restype = None
+    L.pbdk_conv_scope(0, 2)
 p = (h + 2 * (r // 2) - r) // st + 1
 d = _lib.ConvDesc(n, h, h, c, k, r, r, st, r // 2, p, p)
 x = torch.randn(n, h, h, c, device="cuda").bfloat16()
