@@ -438,11 +438,34 @@ __global__ void __launch_bounds__(kT) dw_wgrad_partial_kernel(const __nv_bfloat1
 }
 
 // Pass 2: dw[o] = sum over chunks (chunk order, fp64) of partial[chunk][o].
-__global__ void chunk_sum_kernel(const float* __restrict__ partial, int chunks, size_t n, float* __restrict__ out) {
-  for (size_t o = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; o < n;
-       o += static_cast<size_t>(gridDim.x) * blockDim.x) {
+// out[o] = sum over chunks of partial[chunk][o] in fp64, fixed order: CTA = 32 consecutive outputs
+// (threadIdx.x, coalesced) x 32 chunk lanes (threadIdx.y sums chunks y, y + 32, ...), the 32 lane sums
+// added in lane order.  (A thread walking all chunks serially was latency bound: 25 us per launch.)
+constexpr int kSumLanes = 32;
+__global__ void __launch_bounds__(32 * kSumLanes) chunk_sum_kernel(const float* __restrict__ partial, int chunks,
+                                                                   size_t n, float* __restrict__ out) {
+  __shared__ double part[kSumLanes][33];
+  const size_t o = blockIdx.x * static_cast<size_t>(32) + threadIdx.x;
+  double acc = 0.0;
+  if (o < n) {
+    int c = threadIdx.y;
+    for (; c + 3 * kSumLanes < chunks; c += 4 * kSumLanes) {  // four independent loads in flight
+      const float a0 = partial[static_cast<size_t>(c) * n + o];
+      const float a1 = partial[static_cast<size_t>(c + kSumLanes) * n + o];
+      const float a2 = partial[static_cast<size_t>(c + 2 * kSumLanes) * n + o];
+      const float a3 = partial[static_cast<size_t>(c + 3 * kSumLanes) * n + o];
+      acc += a0;
+      acc += a1;
+      acc += a2;
+      acc += a3;
+    }
+    for (; c < chunks; c += kSumLanes) acc += partial[static_cast<size_t>(c) * n + o];
+  }
+  part[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && o < n) {
     double s = 0.0;
-    for (int c = 0; c < chunks; ++c) s += partial[c * n + o];
+    for (int l = 0; l < kSumLanes; ++l) s += part[l][threadIdx.x];
     out[o] = static_cast<float>(s);
   }
 }
@@ -799,7 +822,7 @@ cudaError_t launch_dw_wgrad(int st, const DwArgs& d, const void* a, const void* 
                                                       static_cast<const __nv_bfloat16*>(dy), partial, d.n, d.h, d.w,
                                                       d.c, d.p, d.q, t.lanes_c, t.per_chunk);
   const size_t n = static_cast<size_t>(d.c) * K * K;
-  chunk_sum_kernel<<<grid_for(static_cast<long long>(n)), kT, 0, s>>>(partial, t.chunks, n, dw);
+  chunk_sum_kernel<<<static_cast<int>((n + 31) / 32), dim3(32, kSumLanes), 0, s>>>(partial, t.chunks, n, dw);
   return cudaGetLastError();
 }
 
@@ -988,7 +1011,7 @@ int stem_wgrad(const void* x, const void* dy, int n, int S, float* ws, size_t ws
   const int chunks = (rows + per - 1) / per;
   stem_wgrad_partial_kernel<<<chunks, kT, 0, s>>>(static_cast<const __nv_bfloat16*>(x),
                                                   static_cast<const __nv_bfloat16*>(dy), ws, n, S, per);
-  chunk_sum_kernel<<<grid_for(32 * 9 * 16), kT, 0, s>>>(ws, chunks, 32 * 9 * 16, dw);
+  chunk_sum_kernel<<<(32 * 9 * 16 + 31) / 32, dim3(32, kSumLanes), 0, s>>>(ws, chunks, 32 * 9 * 16, dw);
   return ok(cudaGetLastError());
 }
 
