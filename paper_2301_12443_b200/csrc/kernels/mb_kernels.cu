@@ -470,6 +470,92 @@ __global__ void __launch_bounds__(32 * kSumLanes) chunk_sum_kernel(const float* 
   }
 }
 
+// ------------------------------------------------------------------ stem weight gradient, staged rows
+// dw[k][r][s][c] = sum_{n,p,q} dy[n,p,q,k] x[n, 2p+r-1, 2q+s-1, c] (c < 3).  A CTA walks its chunk of
+// output rows one at a time: the dy row (Q x 32, bf16 -> fp32) and the three input rows (3 real
+// channels, fp32, zero outside the image) are staged in shared memory, then thread (4-channel group of
+// k, tap) sweeps the row's q with 12 fp32 fmas per 2 shared loads.  (The register kernel re-read 9
+// broadcast 8-byte x vectors per q from L1/L2 and was latency bound: 588 GB/s.)  Per-thread fp32
+// partials over the chunk's rows, CTA partial -> fixed-order chunk sum (as before).
+constexpr int kStemLanes = 3;  // q-lanes per CTA: 72 (k4, tap) threads each
+
+__global__ void __launch_bounds__(kT) stem_wgrad_staged_kernel(const __nv_bfloat16* __restrict__ x,
+                                                               const __nv_bfloat16* __restrict__ dy,
+                                                               float* __restrict__ partial, int N, int S,
+                                                               int rows_per_chunk) {
+  extern __shared__ float4 ssm[];
+  const int P = S / 2;
+  float4* xs = ssm;                             // [3][S + 2] pixels (c0, c1, c2, 0), column -1 .. S
+  float4* gs = ssm + 3 * (S + 2);               // [P][8] = 32 k as 8 float4
+  __shared__ float red[kStemLanes][72][4];
+  const int t = threadIdx.x;
+  const int lane_q = t / 72;                    // q-lane
+  const int pair = t - lane_q * 72;             // (k4, tap)
+  const int k4 = pair / 9, tap = pair - k4 * 9;
+  const int r = tap / 3, sc = tap - r * 3;
+  float acc[4][3] = {};
+  const int r0 = blockIdx.x * rows_per_chunk;
+  const int r1 = min(N * P, r0 + rows_per_chunk);
+  for (int row = r0; row < r1; ++row) {
+    const int p = row % P, n = row / P;
+    __syncthreads();  // previous row's compute done
+    for (int i = t; i < 3 * (S + 2); i += blockDim.x) {
+      const int rr = i / (S + 2), w = i - rr * (S + 2) - 1;
+      const int h = 2 * p + rr - 1;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (h >= 0 && h < S && w >= 0 && w < S) {
+        const uint2 u = *reinterpret_cast<const uint2*>(x + ((static_cast<size_t>(n) * S + h) * S + w) * 16);
+        v = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u), __uint_as_float(u.y << 16),
+                        0.f);
+      }
+      xs[i] = v;
+    }
+    const __nv_bfloat16* grow = dy + static_cast<size_t>(row) * P * 32;
+    for (int i = t; i < P * 8; i += blockDim.x) {
+      const uint2 u = *reinterpret_cast<const uint2*>(grow + 4 * static_cast<size_t>(i));
+      gs[i] = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u), __uint_as_float(u.y << 16),
+                          __uint_as_float(u.y & 0xFFFF0000u));
+    }
+    __syncthreads();
+    if (lane_q < kStemLanes) {
+      const float4* xr = xs + r * (S + 2) + sc;  // column 2q + sc - 1 -> index 2q + sc
+      for (int q = lane_q; q < P; q += kStemLanes) {
+        const float4 g = gs[q * 8 + k4];
+        const float4 xv = xr[2 * q];
+        const float gg[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          acc[j][0] = fmaf(gg[j], xv.x, acc[j][0]);
+          acc[j][1] = fmaf(gg[j], xv.y, acc[j][1]);
+          acc[j][2] = fmaf(gg[j], xv.z, acc[j][2]);
+        }
+      }
+    }
+  }
+  // CTA partial: lanes added in lane order; layout = the weight layout [32][3][3][16] (pad channels 0)
+  float* out = partial + static_cast<size_t>(blockIdx.x) * (32 * 9 * 16);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    __syncthreads();
+    if (lane_q < kStemLanes)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) red[lane_q][pair][j] = acc[j][c];
+    __syncthreads();
+    for (int o = t; o < 72 * 4; o += blockDim.x) {
+      const int pr = o / 4, j = o - pr * 4;
+      float v = 0.f;
+#pragma unroll
+      for (int l = 0; l < kStemLanes; ++l) v += red[l][pr][j];
+      const int kk = (pr / 9) * 4 + j, tp = pr % 9;
+      out[(kk * 9 + tp) * 16 + c] = v;
+    }
+  }
+  for (int o = t; o < 32 * 9 * 13; o += blockDim.x) {
+    const int k = o / (9 * 13), rem = o % (9 * 13);
+    out[(k * 9 + rem / 13) * 16 + 3 + rem % 13] = 0.0f;
+  }
+}
+
 // ------------------------------------------------------------------ stem 3x3 / stride 2 (3 -> 32)
 // x: [N][S][S][16] bf16 (channels 3..15 zero), w: [32][3][3][16] bf16 (the product layout);
 // y[n,p,q,k] = fmaf chain over (r, s, c < 3).  Thread = (output pixel, 8 output channels).
@@ -1009,8 +1095,18 @@ int stem_wgrad(const void* x, const void* dy, int n, int S, float* ws, size_t ws
   const int rows = n * (S / 2);
   const int per = stem_chunk_rows(n, S);
   const int chunks = (rows + per - 1) / per;
-  stem_wgrad_partial_kernel<<<chunks, kT, 0, s>>>(static_cast<const __nv_bfloat16*>(x),
-                                                  static_cast<const __nv_bfloat16*>(dy), ws, n, S, per);
+  const size_t smem = (3 * static_cast<size_t>(S + 2) + static_cast<size_t>(S / 2) * 8) * sizeof(float4);
+  static const bool staged = [] {  // PBDK_STEM_STAGED=0: the register kernel (A/B runs)
+    const char* e = pbd::knob_env("PBDK_STEM_STAGED");
+    return e == nullptr || e[0] != '0';
+  }();
+  if (staged && smem <= 48 * 1024) {
+    stem_wgrad_staged_kernel<<<chunks, kT, smem, s>>>(static_cast<const __nv_bfloat16*>(x),
+                                                      static_cast<const __nv_bfloat16*>(dy), ws, n, S, per);
+  } else {
+    stem_wgrad_partial_kernel<<<chunks, kT, 0, s>>>(static_cast<const __nv_bfloat16*>(x),
+                                                    static_cast<const __nv_bfloat16*>(dy), ws, n, S, per);
+  }
   chunk_sum_kernel<<<(32 * 9 * 16 + 31) / 32, dim3(32, kSumLanes), 0, s>>>(ws, chunks, 32 * 9 * 16, dw);
   return ok(cudaGetLastError());
 }
