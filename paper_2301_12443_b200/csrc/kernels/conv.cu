@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncwarp();  // warp 0 reconverges after the lane-0 barrier init (aligned barrier below)
   if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();  // (a cluster-wide barrier also covers the CTA: the split CTAs start in step)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
