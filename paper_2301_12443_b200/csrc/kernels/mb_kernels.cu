@@ -811,11 +811,16 @@ __global__ void __launch_bounds__(kT) se_fc_kernel(const float* __restrict__ poo
   const int n = blockIdx.x;
   for (int c = threadIdx.x; c < E; c += kT) pl[c] = pooled[static_cast<size_t>(n) * E + c];
   __syncthreads();
-  for (int j = threadIdx.x; j < cs; j += kT) {
-    float acc = b1[j];
+  // FC1: one warp per hidden unit, lanes stride the E inputs (coalesced weight rows), fixed xor tree
+  // (a thread walking E serially left the SM idle: 47 us per launch)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = warp; j < cs; j += kT / 32) {
     const __nv_bfloat16* wr = w1 + static_cast<size_t>(j) * E;
-    for (int c = 0; c < E; ++c) acc = fmaf(__bfloat162float(wr[c]), pl[c], acc);
-    h[j] = swishf(acc);
+    float acc = 0.0f;
+    for (int c = lane; c < E; c += 32) acc = fmaf(__bfloat162float(wr[c]), pl[c], acc);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) h[j] = swishf(acc + b1[j]);
   }
   __syncthreads();
   for (int c = threadIdx.x; c < E; c += kT) {

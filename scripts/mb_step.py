@@ -14,8 +14,10 @@ S = int(sys.argv[2]) if len(sys.argv) > 2 else 224
 draw = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 steps = int(os.environ.get("STEPS", "20"))
 from oracle import mb  # noqa: E402  (path sampler only)
+if os.environ.get("MODEL") == "effb0":
+    mb.set_family(1)
 
-p = ex.Partition(0, 5, b, b, model="mbv2", image=S)
+p = ex.Partition(0, 5, b, b, model=os.environ.get("MODEL", "mbv2"), image=S)
 p.init_params()
 for k in range(6):
     p.set_path(k, mb.sample_path(k, draw))
