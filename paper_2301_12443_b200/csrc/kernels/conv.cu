@@ -85,7 +85,7 @@ __device__ __forceinline__ float epi_aux(const EpiFlags& f, float v, float r) {
 __device__ __forceinline__ float epi_act(const EpiFlags& f, float v) {
   if (f.relu) return fmaxf(v, 0.f);
   if (f.relu6) return fminf(fmaxf(v, 0.f), 6.f);
-  if (f.swish) return v / (1.0f + expf(-v));
+  if (f.swish) return __fdividef(v, 1.0f + __expf(-v));  // fast-math swish (mb_kernels.cu swishf)
   return v;
 }
 

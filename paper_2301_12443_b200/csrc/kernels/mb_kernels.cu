@@ -66,8 +66,12 @@ __device__ __forceinline__ void fma8(float (&acc)[8], const float (&x)[8], const
 }
 
 __device__ __forceinline__ float relu6f(float z) { return fminf(fmaxf(z, 0.0f), 6.0f); }
-__device__ __forceinline__ float swishf(float z) { return z / (1.0f + expf(-z)); }
-__device__ __forceinline__ float sigmoidf(float z) { return 1.0f / (1.0f + expf(-z)); }
+// EfficientNet's swish / sigmoid in fast math (ex2.approx + approximate division, a few ulp of fp32):
+// the libm expf + IEEE division made the swish epilogues compute-bound (the 3x3/s2 depthwise of the
+// EfficientNet teacher ran at 1.0 TB/s vs 3.1 TB/s with ReLU6).  Far below one bf16 rounding step; the
+// oracle keeps expf and '/', parity is within the bf16 teacher tolerance (tests/test_gpu_mb.py).
+__device__ __forceinline__ float swishf(float z) { return __fdividef(z, 1.0f + __expf(-z)); }
+__device__ __forceinline__ float sigmoidf(float z) { return __fdividef(1.0f, 1.0f + __expf(-z)); }
 // activation codes (mb_kernels.hpp): 0 none, 1 ReLU6, 2 swish
 __device__ __forceinline__ float act_fn(int act, float v) {
   return act == 1 ? relu6f(v) : act == 2 ? swishf(v) : v;

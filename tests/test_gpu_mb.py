@@ -8,7 +8,7 @@ tcgen05 tensor cores (different fp32 accumulation order), which flips an occasio
   * synthetic image and every initial student parameter: bit-exact;
   * teacher block k on the GPU's own input: bf16 values within depth * 2^-7 max / depth * 2^-11 mean
     of the output scale (depth = convolutions [+ squeeze-excite] in the block; the EfficientNet
-    teacher's swish/sigmoid use expf on both sides, equal to ~1 ulp);
+    teacher's swish/sigmoid: libm expf in the oracle, fast math on the GPU — a few fp32 ulp);
   * student fwd/bwd of block k on the GPU's own (t_{k-1}, t_k): loss 1e-3 relative; every gradient
     tensor of the active path within max(2e-2 relative, 2x the oracle's own bf16-vs-fp32 distance);
     inactive candidates exactly zero;
