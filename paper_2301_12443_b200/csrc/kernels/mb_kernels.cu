@@ -775,31 +775,39 @@ __global__ void loss_sum_kernel(const double* __restrict__ part, int n, double n
 // ------------------------------------------------------------------ squeeze-excite (EfficientNet teacher)
 // pooled[n][c] = (sum_q y[n][q][c]) / hw: CTA per (n, 8-channel group window of 32 groups); threads
 // stride over q in double, fixed-order tree over the CTA.
+// pooled[n][c] = mean over the hw pixels of y[n][.][c].  CTA = (sample, 32 channel groups):
+// a warp reads 32 consecutive 16-byte channel vectors of one pixel (coalesced), 8 pixel slots per CTA.
+// (One CTA per 8-channel group strided the pixels at E*2 bytes: 32 sectors per warp load, 1.9 TB/s.)
+constexpr int kPoolSlots = kT / 32;
 __global__ void __launch_bounds__(kT) se_pool_kernel(const __nv_bfloat16* __restrict__ y, int hw, int E,
                                                      float* __restrict__ pooled) {
-  __shared__ double red[kT / 32][8];
+  __shared__ double red[kPoolSlots][32][8];
   const int n = blockIdx.x;
-  const int g = blockIdx.y;  // 8-channel group
-  const __nv_bfloat16* base = y + static_cast<size_t>(n) * hw * E + g * 8;
-  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int q = threadIdx.x; q < hw; q += kT) {
-    float f[8];
-    ld8(base + static_cast<size_t>(q) * E, f);
+  const int gl = threadIdx.x & 31, slot = threadIdx.x >> 5;
+  const int g = blockIdx.y * 32 + gl;  // 8-channel group
+  const bool live = g < E / 8;
+  // per-thread fp32 sums over its pixel slot (the fp64 adds were the limit), fp64 across slots
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (live) {
+    const __nv_bfloat16* base = y + static_cast<size_t>(n) * hw * E + g * 8;
+#pragma unroll 4
+    for (int q = slot; q < hw; q += kPoolSlots) {
+      float f[8];
+      ld8(base + static_cast<size_t>(q) * E, f);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] += f[j];
+      for (int j = 0; j < 8; ++j) acc[j] += f[j];
+    }
   }
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    double v = acc[j];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][j] = v;
-  }
+  for (int j = 0; j < 8; ++j) red[slot][gl][j] = acc[j];
   __syncthreads();
-  if (threadIdx.x < 8) {
+  for (int o = threadIdx.x; o < 32 * 8; o += kT) {
+    const int gg = o / 8, j = o % 8;
+    const int go = blockIdx.y * 32 + gg;
+    if (go >= E / 8) continue;
     double t = 0.0;
-    for (int w = 0; w < kT / 32; ++w) t += red[w][threadIdx.x];
-    pooled[static_cast<size_t>(n) * E + g * 8 + threadIdx.x] = static_cast<float>(t / hw);
+    for (int sl = 0; sl < kPoolSlots; ++sl) t += red[sl][gg][j];
+    pooled[static_cast<size_t>(n) * E + go * 8 + j] = static_cast<float>(t / hw);
   }
 }
 
@@ -1142,7 +1150,7 @@ int bn_apply_act(const void* y, const float* mean_rstd, const float* gamma, cons
 int se_apply(void* y, int n, int hw, int E, int cs, const void* w1, const float* b1, const void* w2,
              const float* b2, float* pooled, float* gate, cudaStream_t s) {
   if (E % 8 != 0 || cs < 1 || n < 1 || static_cast<long long>(n) * hw * E >= (1LL << 31)) return PBDK_EINVAL;
-  se_pool_kernel<<<dim3(n, E / 8), kT, 0, s>>>(static_cast<const __nv_bfloat16*>(y), hw, E, pooled);
+  se_pool_kernel<<<dim3(n, (E / 8 + 31) / 32), kT, 0, s>>>(static_cast<const __nv_bfloat16*>(y), hw, E, pooled);
   se_fc_kernel<<<n, kT, (E + cs) * sizeof(float), s>>>(pooled, static_cast<const __nv_bfloat16*>(w1), b1,
                                                         static_cast<const __nv_bfloat16*>(w2), b2, E, cs, gate);
   const int total = n * hw * (E / 8);
