@@ -918,8 +918,15 @@ class MbPartition final : public PartitionBase {
           check(pbdk::fprop_plan(pw_desc(mo, L.cout, C.L.E), L.dy3, C.wpT, L.g2, nullptr, L.a2, PBDK_EPI_RELU6_MASK,
                                  &C.p_proj_dgrad),
                 "project dgrad plan");
+          if (pbd::pdl_enabled())
+            for (pbdk::FpropPlan* f : {&C.p_exp, &C.p_exp_dgrad, &C.p_proj, &C.p_proj_dgrad}) f->pdl = true;
+          if (pbd::pdl_enabled()) C.w_exp.pdl = C.w_proj.pdl = true;
         }
       }
+    if (pbd::pdl_enabled())
+      for (TBlock& tb : tblocks_)
+        for (TOp& op : tb.ops)
+          if (op.kind == TOp::PW) op.plan.pdl = true;
   }
 
   const Family& fam_;

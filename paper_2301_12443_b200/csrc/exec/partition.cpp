@@ -606,6 +606,15 @@ class ResNetPartition final : public PartitionBase {
       check(pbdk::wgrad_plan(sc_desc(s, n_), s.in, s.dys, g + s.lay.wsc, ws2, s.wws_bytes, &s.p_wsc), "wgradsc plan");
       check(pbdk::wgrad_plan(conv1_desc(s, n_), s.in, s.dy1, g + s.lay.w1, s.wws, s.wws_bytes, &s.p_w1), "wgrad1 plan");
     }
+    // programmatic dependent launch for every conv: its prologue overlaps the previous kernel's tail
+    if (pbd::pdl_enabled()) {
+      for (TBlock& tb : tblocks_)
+        for (TConv& c : tb.convs) c.plan.pdl = true;
+      for (SBlock& s : sblocks_) {
+        for (pbdk::FpropPlan* f : {&s.p_conv1, &s.p_sc, &s.p_conv2, &s.p_dgrad}) f->pdl = true;
+        for (pbdk::WgradPlan* w : {&s.p_w2, &s.p_wsc, &s.p_w1}) w->pdl = true;
+      }
+    }
   }
 
   cudaEvent_t fork_ = nullptr;

@@ -61,6 +61,36 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
 
+// Launch with optional thread-block clusters and programmatic dependent launch (PDL: the kernel may
+// start — prologue: barriers, TMEM, tensor-map prefetch — while the previous kernel in the stream
+// drains; it calls grid_dep_wait() before touching global memory).
+template <class... KArgs, class... Args>
+cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, bool pdl,
+                      unsigned cluster, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  unsigned n = 0;
+  if (cluster > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = cluster;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  if (pdl) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // Epilogue semantics (pbdk.h PBDK_EPI_*): y = act(aux_op(acc + bias, aux)), fp32, one bf16 rounding.
 struct EpiFlags {
   bool bias, aux, add, mask0, mask6, relu, relu6, swish;
@@ -242,6 +272,7 @@ __global__ void __launch_bounds__(epi_threads(EPW), 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  grid_dep_wait();  // PDL: the prologue above overlapped the previous kernel; its outputs are visible now
 
   if (warp == 0) {
     if (lane == 0) {
@@ -419,6 +450,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   cluster_sync();  // (a cluster-wide barrier also covers the CTA: the split CTAs start in step)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  grid_dep_wait();  // PDL: the prologue above overlapped the previous kernel; its outputs are visible now
 
   if (warp == 0) {
     if (lane == 0) {
@@ -530,19 +562,8 @@ cudaError_t launch_fprop_splitk(const FpropPlan& p, cudaStream_t stream) {
     return cudaFuncSetAttribute(conv_fprop_splitk_kernel<BN, BKC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 F::SMEM);
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = p.grid;
-  cfg.blockDim = dim3(kThreads, 1, 1);
-  cfg.dynamicSmemBytes = F::SMEM;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = p.grid.x;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, conv_fprop_splitk_kernel<BN, BKC>, p.tmx, p.tmw, p.args);
+  return launch_ex(conv_fprop_splitk_kernel<BN, BKC>, p.grid, dim3(kThreads, 1, 1), F::SMEM, stream, p.pdl, p.grid.x,
+                   p.tmx, p.tmw, p.args);
 }
 
 // ------------------------------------------------------------------ 2-CTA fprop (cta_group::2)
@@ -603,6 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  grid_dep_wait();  // PDL: the prologue above overlapped the previous kernel; its outputs are visible now
 
   if (warp == 0) {
     if (lane == 0) {
@@ -699,19 +721,8 @@ cudaError_t launch_fprop_pair(const FpropPlan& p, cudaStream_t stream) {
     return cudaFuncSetAttribute(conv_fprop_pair_kernel<BN, BKC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 C::SMEM);
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = p.grid;
-  cfg.blockDim = dim3(kThreads, 1, 1);
-  cfg.dynamicSmemBytes = C::SMEM;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, conv_fprop_pair_kernel<BN, BKC>, p.tmx, p.tmw, p.args);
+  return launch_ex(conv_fprop_pair_kernel<BN, BKC>, p.grid, dim3(kThreads, 1, 1), C::SMEM, stream, p.pdl, 2u, p.tmx,
+                   p.tmw, p.args);
 }
 
 // ------------------------------------------------------------------ halo fprop (3x3, stride 1, pad 1)
@@ -782,6 +793,7 @@ __global__ void __launch_bounds__(epi_threads(EPW), 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  grid_dep_wait();  // PDL: the prologue above overlapped the previous kernel; its outputs are visible now
 
   if (warp == 0) {
     if (lane == 0) {
@@ -935,6 +947,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  grid_dep_wait();  // PDL: the prologue above overlapped the previous kernel; its outputs are visible now
 
   if (warp == 0) {
     if (lane == 0) {
@@ -1044,8 +1057,8 @@ cudaError_t launch_fprop_m2(const FpropPlan& p, cudaStream_t stream) {
   if (stream == reinterpret_cast<cudaStream_t>(-1)) {
     return cudaFuncSetAttribute(conv_fprop_m2_kernel<BN, BKC>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   }
-  conv_fprop_m2_kernel<BN, BKC><<<p.grid, kThreads, C::SMEM, stream>>>(p.tmx, p.tmw, p.args);
-  return cudaGetLastError();
+  return launch_ex(conv_fprop_m2_kernel<BN, BKC>, p.grid, dim3(kThreads, 1, 1), C::SMEM, stream, p.pdl, 1u, p.tmx,
+                   p.tmw, p.args);
 }
 
 template <int BN, int BKC, int WP, int EPW = 1>
@@ -1055,8 +1068,8 @@ cudaError_t launch_fprop_halo(const FpropPlan& p, cudaStream_t stream) {
     return cudaFuncSetAttribute(conv_fprop_halo_kernel<BN, BKC, WP, EPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 C::SMEM);
   }
-  conv_fprop_halo_kernel<BN, BKC, WP, EPW><<<p.grid, epi_threads(EPW), C::SMEM, stream>>>(p.tmx, p.tmw, p.args);
-  return cudaGetLastError();
+  return launch_ex(conv_fprop_halo_kernel<BN, BKC, WP, EPW>, p.grid, dim3(epi_threads(EPW), 1, 1), C::SMEM, stream,
+                   p.pdl, 1u, p.tmx, p.tmw, p.args);
 }
 
 template <int BN, int BKC, bool BRES, int EPW = 1>
@@ -1066,8 +1079,8 @@ cudaError_t launch_fprop(const FpropPlan& p, cudaStream_t stream) {
     return cudaFuncSetAttribute(conv_fprop_kernel<BN, BKC, BRES, EPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 C::SMEM);
   }
-  conv_fprop_kernel<BN, BKC, BRES, EPW><<<p.grid, epi_threads(EPW), C::SMEM, stream>>>(p.tmx, p.tmw, p.args);
-  return cudaGetLastError();
+  return launch_ex(conv_fprop_kernel<BN, BKC, BRES, EPW>, p.grid, dim3(epi_threads(EPW), 1, 1), C::SMEM, stream,
+                   p.pdl, 1u, p.tmx, p.tmw, p.args);
 }
 
 // ------------------------------------------------------------------ wgrad
@@ -1129,6 +1142,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  grid_dep_wait();  // PDL: the prologue above overlapped the previous kernel; its outputs are visible now
 
   if (warp == 0) {
     if (lane == 0) {
@@ -1270,6 +1284,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  grid_dep_wait();  // PDL: the prologue above overlapped the previous kernel; its outputs are visible now
 
   if (warp == 0) {
     if (lane == 0) {
@@ -1363,8 +1378,8 @@ cudaError_t launch_wgrad_mt(const WgradPlan& p, cudaStream_t stream) {
     return cudaFuncSetAttribute(conv_wgrad_mt_kernel<CB, SWA, AAT, TAPS>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   }
-  conv_wgrad_mt_kernel<CB, SWA, AAT, TAPS><<<p.grid, kThreads, C::SMEM, stream>>>(p.tmdy, p.tmx, p.args);
-  return cudaGetLastError();
+  return launch_ex(conv_wgrad_mt_kernel<CB, SWA, AAT, TAPS>, p.grid, dim3(kThreads, 1, 1), C::SMEM, stream, p.pdl, 1u,
+                   p.tmdy, p.tmx, p.args);
 }
 
 template <int BN, int SWA, int SWB>
@@ -1374,8 +1389,8 @@ cudaError_t launch_wgrad(const WgradPlan& p, cudaStream_t stream) {
     return cudaFuncSetAttribute(conv_wgrad_kernel<BN, SWA, SWB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 C::SMEM);
   }
-  conv_wgrad_kernel<BN, SWA, SWB><<<p.grid, kThreads, C::SMEM, stream>>>(p.tmdy, p.tmx, p.args);
-  return cudaGetLastError();
+  return launch_ex(conv_wgrad_kernel<BN, SWA, SWB>, p.grid, dim3(kThreads, 1, 1), C::SMEM, stream, p.pdl, 1u, p.tmdy,
+                   p.tmx, p.args);
 }
 
 // Fixed-order split reduction: dw[i] = sum_s ws[s][i]  (deterministic).  CTA = 32 float4 lanes x 8

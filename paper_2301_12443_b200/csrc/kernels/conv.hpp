@@ -50,6 +50,7 @@ struct FpropPlan {
   int bn_tile = 0;
   int bkc = 0;
   int smem_bytes = 0;
+  bool pdl = false;  // launch with programmatic dependent launch (the kernels call griddepcontrol.wait)
   cudaError_t (*launch)(const FpropPlan&, cudaStream_t) = nullptr;
 };
 
@@ -88,6 +89,7 @@ struct WgradPlan {
   int smem_bytes = 0;
   float* dw = nullptr;
   size_t slab = 0;  // elements of dw
+  bool pdl = false;  // as FpropPlan::pdl (the split reduction after it is a plain launch)
   cudaError_t (*launch)(const WgradPlan&, cudaStream_t) = nullptr;
 };
 

@@ -17,4 +17,10 @@ constexpr bool kExperiments = false;
 
 inline const char* knob_env(const char* name) { return kExperiments ? std::getenv(name) : nullptr; }
 
+// Programmatic dependent launch for the executors' convolutions (on; PBD_PDL=0 for A/B runs).
+inline bool pdl_enabled() {
+  const char* e = knob_env("PBD_PDL");
+  return e == nullptr || e[0] != '0';
+}
+
 }  // namespace pbd
