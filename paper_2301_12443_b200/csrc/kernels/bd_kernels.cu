@@ -1330,7 +1330,31 @@ bool apply_pipe() {  // PBDK_APPLY_PIPE=0: the register-loop apply kernels (A/B 
   static const bool on = env_int("PBDK_APPLY_PIPE", 1) != 0;
   return on;
 }
-RowTiling apply_tiling(int m, int c, int v) { return tiling_for(m, c, v, std::max(1, apply_cap() / apply_pipe_div())); }
+// Staged passes over small [M][C] streams: a CTA that streams only a few tens of KB is latency bound
+// (prologue, pipeline fill, reduction tail) while it holds an SM's shared memory against the other
+// student streams' convs, so the grid is also capped at one CTA per `min_bytes` of input.  The
+// fixed-point partials are exact, so the chunk count never changes a result.
+int cap_chunks(int target, long long bytes, int min_bytes) {
+  if (min_bytes <= 0) return target;
+  const long long need = (bytes + min_bytes - 1) / min_bytes;
+  return static_cast<int>(std::max(1LL, std::min<long long>(target, need)));
+}
+int fix_min_bytes() {  // PBDK_FIX_MIN_BYTES: reduction passes (CIFAR step 0.891 -> 0.873 ms at 256 KB; 128 KB-512 KB
+                       // within 1 %, 1 MB 0.94 ms; r02_ab_minbytes.txt)
+  static const int b = env_int("PBDK_FIX_MIN_BYTES", 256 << 10);
+  return b;
+}
+int apply_min_bytes() {  // PBDK_APPLY_MIN_BYTES: elementwise passes (off: 256 KB measured neutral)
+  static const int b = env_int("PBDK_APPLY_MIN_BYTES", 0);
+  return b;
+}
+RowTiling fix_tiling(int m, int c, int v, int nin) {
+  return tiling_for(m, c, v, cap_chunks(red_target(), 2LL * m * c * nin, fix_min_bytes()));
+}
+RowTiling apply_tiling(int m, int c, int v, int nin) {
+  return tiling_for(m, c, v,
+                    cap_chunks(std::max(1, apply_cap() / apply_pipe_div()), 2LL * m * c * nin, apply_min_bytes()));
+}
 
 template <class K, class... Args>
 cudaError_t launch_pipe(K kernel, int grid, size_t smem, cudaStream_t st, Args... args) {
@@ -1350,8 +1374,8 @@ cudaError_t launch_pipe(K kernel, int grid, size_t smem, cudaStream_t st, Args..
 int bn_stats_fix(const void* y0, const void* y1, int m, int c, FixScratch fx, float* mr0, float* mr1,
                  cudaStream_t st) {
   if (c % 8 != 0 || c / 8 > kThreads) return PBDK_EINVAL;
-  const RowTiling t = tiling_for(m, c, 8);
   const int nin = y1 != nullptr ? 2 : 1;
+  const RowTiling t = fix_tiling(m, c, 8, nin);
   const int tr = pipe_tile_rows(nin, c, t.rpp);
   const size_t smem = pipe_smem(nin, c, tr);
   if (y1 != nullptr)
@@ -1367,7 +1391,7 @@ int bn_apply_relu_fix(const void* y, const float* mean_rstd, const float* gamma,
                       int c, cudaStream_t st) {
   if (c % 8 != 0 || c / 8 > kThreads) return PBDK_EINVAL;
   if (!apply_pipe()) return bn_apply_relu(y, mean_rstd, gamma, beta, a, m, c, st);
-  const RowTiling t = apply_tiling(m, c, 8);
+  const RowTiling t = apply_tiling(m, c, 8, 2);
   const int tr = pipe_tile_rows(1, c, t.rpp);
   return ok(launch_pipe(bn_apply_relu_pipe_kernel<8>, t.chunks, pipe_smem(1, c, tr), st,
                         PipeIn<1>{{static_cast<const __nv_bfloat16*>(y)}}, mean_rstd, gamma, beta,
@@ -1379,7 +1403,7 @@ int mse_bn_loss_fix(const MseArgs& a, FixScratch fx, cudaStream_t st) {
   LossParams p{a.y2, a.ysc, a.t, a.stats2, a.statssc, a.gamma2, a.beta2, a.gammasc, a.betasc, a.m, a.c, a.gscale};
   const PipeIn<3> in{{static_cast<const __nv_bfloat16*>(a.y2), static_cast<const __nv_bfloat16*>(a.ysc),
                       static_cast<const __nv_bfloat16*>(a.t)}};
-  const RowTiling t = tiling_for(a.m, a.c, kLossPartialV, kLossChunks);
+  const RowTiling t = fix_tiling(a.m, a.c, kLossPartialV, 3);
   const int tr = pipe_tile_rows(3, a.c, t.rpp);
   const LossOut o{a.norm, fx.acc, fx.ticket, a.red, a.dgamma2, a.dbeta2, a.dgammasc, a.dbetasc, a.loss};
   cudaError_t e = launch_pipe(loss_partial_fix_kernel, t.chunks, pipe_smem(3, a.c, tr), st, p, in, t.rows_per_chunk,
@@ -1392,7 +1416,7 @@ int mse_bn_loss_fix(const MseArgs& a, FixScratch fx, cudaStream_t st) {
                                                                         static_cast<__nv_bfloat16*>(a.dysc));
     return ok(cudaGetLastError());
   }
-  const RowTiling ta = apply_tiling(a.m, a.c, kLossApplyV);
+  const RowTiling ta = apply_tiling(a.m, a.c, kLossApplyV, 5);
   const int tra = pipe_tile_rows(3, a.c, ta.rpp);
   e = launch_pipe(loss_bwd_apply_pipe_kernel, ta.chunks, pipe_smem(3, a.c, tra), st, p, in,
                   static_cast<const float*>(a.red), ta.rows_per_chunk, ta.cg, ta.rpp, tra,
@@ -1404,7 +1428,7 @@ int bn_bwd_fix(const void* g, const void* y, const float* mean_rstd, const float
                float* red, float* dgamma, float* dbeta, void* dy, cudaStream_t st) {
   if (c % 8 != 0 || c / 8 > kThreads) return PBDK_EINVAL;
   const PipeIn<2> in{{static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(y)}};
-  const RowTiling t = tiling_for(m, c, 8);
+  const RowTiling t = fix_tiling(m, c, 8, 2);
   const int tr = pipe_tile_rows(2, c, t.rpp);
   cudaError_t e = launch_pipe(bn_bwd_fix_partial_kernel<8>, t.chunks, pipe_smem(2, c, tr), st, in, m, c,
                               t.rows_per_chunk, t.cg, t.rpp, tr, fx.acc, fx.ticket, mean_rstd, gamma, red, dgamma,
@@ -1416,7 +1440,7 @@ int bn_bwd_fix(const void* g, const void* y, const float* mean_rstd, const float
         t.rpp, static_cast<__nv_bfloat16*>(dy));
     return ok(cudaGetLastError());
   }
-  const RowTiling ta = apply_tiling(m, c, 8);
+  const RowTiling ta = apply_tiling(m, c, 8, 3);
   const int tra = pipe_tile_rows(2, c, ta.rpp);
   e = launch_pipe(bn_bwd_apply_pipe_kernel<8>, ta.chunks, pipe_smem(2, c, tra), st, in, mean_rstd, gamma,
                   static_cast<const float*>(red), m, c, ta.rows_per_chunk, ta.cg, ta.rpp, tra,
