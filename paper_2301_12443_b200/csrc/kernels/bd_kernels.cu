@@ -773,9 +773,11 @@ struct PipeIn {
 };
 
 // f(row, s) with s[k] = this thread's V-channel group of row `row` of input k in shared memory.
-template <int NIN, int V, class F>
+// pre() runs once per thread after the first tiles are requested: per-channel parameter loads placed
+// there overlap the tiles' latency instead of delaying the requests.
+template <int NIN, int V, class P, class F>
 __device__ __forceinline__ void row_pipe(const PipeIn<NIN>& in, int C, int r0, int r1, int tr, int g, int slot,
-                                         int rpp, F&& f) {
+                                         int rpp, P&& pre, F&& f) {
   extern __shared__ __align__(128) uint8_t pipe_smem_raw[];
   __shared__ uint64_t full[kPipeStages];
   const int tile_elems = tr * C;
@@ -797,6 +799,7 @@ __device__ __forceinline__ void row_pipe(const PipeIn<NIN>& in, int C, int r0, i
   __syncthreads();
   if (threadIdx.x == 0)
     for (int t = 0; t < min(ntiles, kPipeStages); ++t) issue(t);
+  pre();
   for (int t = 0; t < ntiles; ++t) {
     const int st = t % kPipeStages;
     mbar_wait(&full[st], (t / kPipeStages) & 1);
@@ -816,6 +819,12 @@ __device__ __forceinline__ void row_pipe(const PipeIn<NIN>& in, int C, int r0, i
     __syncthreads();  // stage st fully read before it is refilled
     if (threadIdx.x == 0 && t + kPipeStages < ntiles) issue(t + kPipeStages);
   }
+}
+
+template <int NIN, int V, class F>
+__device__ __forceinline__ void row_pipe(const PipeIn<NIN>& in, int C, int r0, int r1, int tr, int g, int slot,
+                                         int rpp, F&& f) {
+  row_pipe<NIN, V>(in, C, r0, r1, tr, g, slot, rpp, [] {}, f);
 }
 
 template <int V>
@@ -873,13 +882,14 @@ __global__ void __launch_bounds__(kThreads) bn_apply_relu_pipe_kernel(const Pipe
   const int slot = threadIdx.x / cg;
   const int c0 = g * V;
   float A[V], B[V];
-#pragma unroll
-  for (int j = 0; j < V; ++j) {
-    A[j] = gamma[c0 + j] * mean_rstd[C + c0 + j];
-    B[j] = fmaf(-A[j], mean_rstd[c0 + j], beta[c0 + j]);
-  }
   const int r0 = blockIdx.x * rows_per_chunk;
-  row_pipe<1, V>(in, C, r0, min(m, r0 + rows_per_chunk), tr, g, slot, rpp, [&](int r, const __nv_bfloat16* const* s) {
+  row_pipe<1, V>(in, C, r0, min(m, r0 + rows_per_chunk), tr, g, slot, rpp, [&] {
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      A[j] = gamma[c0 + j] * mean_rstd[C + c0 + j];
+      B[j] = fmaf(-A[j], mean_rstd[c0 + j], beta[c0 + j]);
+    }
+  }, [&](int r, const __nv_bfloat16* const* s) {
     float f[V];
     ld_smem<V>(s[0], f);
 #pragma unroll
@@ -910,9 +920,9 @@ __global__ void __launch_bounds__(kThreads) loss_partial_fix_kernel(const LossPa
   float acc[3][V] = {};
   float lsum = 0.0f;
   float A2[V], As[V], Bz[V];
-  loss_affine<V>(p, gi * V, A2, As, Bz);
   const int r0 = blockIdx.x * rows_per_chunk;
   row_pipe<3, V>(in, p.C, r0, min(p.m, r0 + rows_per_chunk), tr, gi, slot, rpp,
+                 [&] { loss_affine<V>(p, gi * V, A2, As, Bz); },
                  [&](int, const __nv_bfloat16* const* s) {
                    float y2[V], ys[V], t[V];
                    ld_smem<V>(s[0], y2);
@@ -974,16 +984,18 @@ __global__ void __launch_bounds__(kThreads) loss_bwd_apply_pipe_kernel(const Los
   const int slot = threadIdx.x / cg;
   const int c0 = gi * V;
   float A2[V], As[V], Bz[V], Q2[V], R2[V], Qs[V], Rs[V];
-  loss_affine<V>(p, c0, A2, As, Bz);
-#pragma unroll
-  for (int j = 0; j < V; ++j) {
-    Q2[j] = coef[c0 + j];
-    R2[j] = coef[p.C + c0 + j];
-    Qs[j] = coef[2 * p.C + c0 + j];
-    Rs[j] = coef[3 * p.C + c0 + j];
-  }
   const int r0 = blockIdx.x * rows_per_chunk;
   row_pipe<3, V>(in, p.C, r0, min(p.m, r0 + rows_per_chunk), tr, gi, slot, rpp,
+                 [&] {
+                   loss_affine<V>(p, c0, A2, As, Bz);
+#pragma unroll
+                   for (int j = 0; j < V; ++j) {
+                     Q2[j] = coef[c0 + j];
+                     R2[j] = coef[p.C + c0 + j];
+                     Qs[j] = coef[2 * p.C + c0 + j];
+                     Rs[j] = coef[3 * p.C + c0 + j];
+                   }
+                 },
                  [&](int r, const __nv_bfloat16* const* s) {
                    float y2[V], ys[V], t[V], o2[V], os[V];
                    ld_smem<V>(s[0], y2);
@@ -1053,14 +1065,15 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_apply_pipe_kernel(const PipeI
   const int slot = threadIdx.x / cg;
   const int c0 = gi * V;
   float A[V], Q[V], R[V];
-#pragma unroll
-  for (int j = 0; j < V; ++j) {
-    A[j] = gamma[c0 + j] * st[C + c0 + j];
-    Q[j] = coef[c0 + j];
-    R[j] = coef[C + c0 + j];
-  }
   const int r0 = blockIdx.x * rows_per_chunk;
-  row_pipe<2, V>(in, C, r0, min(m, r0 + rows_per_chunk), tr, gi, slot, rpp, [&](int r, const __nv_bfloat16* const* s) {
+  row_pipe<2, V>(in, C, r0, min(m, r0 + rows_per_chunk), tr, gi, slot, rpp, [&] {
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      A[j] = gamma[c0 + j] * st[C + c0 + j];
+      Q[j] = coef[c0 + j];
+      R[j] = coef[C + c0 + j];
+    }
+  }, [&](int r, const __nv_bfloat16* const* s) {
     float fg[V], fy[V], o[V];
     ld_smem<V>(s[0], fg);
     ld_smem<V>(s[1], fy);
@@ -1333,7 +1346,7 @@ bool apply_pipe() {  // PBDK_APPLY_PIPE=0: the register-loop apply kernels (A/B 
 // Staged passes over small [M][C] streams: a CTA that streams only a few tens of KB is latency bound
 // (prologue, pipeline fill, reduction tail) while it holds an SM's shared memory against the other
 // student streams' convs, so the grid is also capped at one CTA per `min_bytes` of input.  The
-// fixed-point partials are exact, so the chunk count never changes a result.
+// cap is a function of the shape only, so a block's numerics stay independent of its placement.
 int cap_chunks(int target, long long bytes, int min_bytes) {
   if (min_bytes <= 0) return target;
   const long long need = (bytes + min_bytes - 1) / min_bytes;
