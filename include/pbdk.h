@@ -171,6 +171,17 @@ int pbdk_dw_dgrad(const pbdk_dw_desc* d, const void* dy, const void* wt, const v
  * n must be a multiple of 4. */
 int pbdk_sgd_momentum(float* w, float* v, const float* g, void* w_bf16, size_t n, float lr, float momentum,
                       long long* step_counter, void* stream);
+/* The same update, also storing the flipped bf16 dgrad operand of up to 4 filters inside w: region i
+ * covers w[off, off + k*r*s*c) laid out [k][r][s][c]; dst[c'][r-1-r'][s-1-s'][k'] = w_bf16 of that
+ * element (bit-identical to pbdk_weight_flip of the updated w_bf16, without its launch).  w_bf16 must be
+ * non-NULL. */
+typedef struct {
+  size_t off;
+  int k, r, s, c;
+  void* dst;
+} pbdk_flip_region;
+int pbdk_sgd_momentum_flip(float* w, float* v, const float* g, void* w_bf16, size_t n, float lr, float momentum,
+                           long long* step_counter, const pbdk_flip_region* regions, int count, void* stream);
 
 #ifdef __cplusplus
 }

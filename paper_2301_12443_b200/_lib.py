@@ -23,6 +23,11 @@ class ConvDesc(ctypes.Structure):
     _fields_ = [(n, c_int) for n in ("n", "h", "w", "c", "k", "r", "s", "stride", "pad", "p", "q")]
 
 
+class FlipRegion(ctypes.Structure):
+    """pbdk_flip_region (include/pbdk.h)."""
+    _fields_ = [("off", c_size_t), ("k", c_int), ("r", c_int), ("s", c_int), ("c", c_int), ("dst", c_void_p)]
+
+
 _lib = None
 
 
@@ -74,6 +79,12 @@ def lib() -> ctypes.CDLL:
     L.pbdk_conv3x_wgrad_workspace_bytes.restype = c_size_t
     L.pbdk_conv3x_wgrad.argtypes = [ctypes.POINTER(ConvDesc), c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
                                     c_void_p]
+    L.pbdk_sgd_momentum.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, ctypes.c_float,
+                                    ctypes.c_float, c_void_p, c_void_p]
+    L.pbdk_sgd_momentum.restype = c_int
+    L.pbdk_sgd_momentum_flip.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, ctypes.c_float,
+                                         ctypes.c_float, c_void_p, ctypes.POINTER(FlipRegion), c_int, c_void_p]
+    L.pbdk_sgd_momentum_flip.restype = c_int
     L.pbdk_split_tf32.argtypes = [c_void_p, c_void_p, c_size_t, c_int, c_void_p]
     L.pbdk_weight_flip_split.argtypes = [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p]
     for name in ("pbdk_conv_fprop", "pbdk_conv_wgrad", "pbdk_weight_flip", "pbdk_conv3x_fprop", "pbdk_conv3x_wgrad",

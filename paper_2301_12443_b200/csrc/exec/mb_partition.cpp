@@ -433,11 +433,16 @@ class MbPartition final : public PartitionBase {
       SBlock& sb = sblocks_[i];
       for (SLayer& L : sb.layers) {
         SCand& C = L.cands[static_cast<size_t>(L.active)];
-        check(pbdk::sgd_momentum(params_ + C.off, mom_ + C.off, grads_ + C.off, shadow_ + C.off, C.L.total, d_.lr,
-                                 d_.momentum, counter, st),
-              "sgd");
+        if (L.stem) {
+          check(pbdk::sgd_momentum(params_ + C.off, mom_ + C.off, grads_ + C.off, shadow_ + C.off, C.L.total,
+                                   d_.lr, d_.momentum, counter, st),
+                "sgd");
+        } else {  // one launch: update + shadow + the three derived dgrad operands (refresh_derived)
+          check(pbdk::sgd_momentum_flip(params_ + C.off, mom_ + C.off, grads_ + C.off, shadow_ + C.off, C.L.total,
+                                        d_.lr, d_.momentum, counter, derived_regions(L, C), st),
+                "sgd");
+        }
         counter = nullptr;  // advance the step counter once
-        refresh_derived(L, C, st);
       }
     }
   }
@@ -493,7 +498,7 @@ class MbPartition final : public PartitionBase {
         n += (e ? 3 : 0) + 1 + 1 + 1 + 1 + 1 + (L.last ? 2 : 1);                      // forward
         n += 2 + (C.w_proj.splits > 1 ? 2 : 1) + 1 + 2 + 2;                            // bn3, wgrad, dgrad, bn2, dw wgrad
         n += e ? (1 + 2 + (C.w_exp.splits > 1 ? 2 : 1) + (L.need_dx ? 1 : 0)) : (L.need_dx ? 1 : 0);
-        n += 1 + (e ? 2 : 1) + 1;                                                      // sgd, transposes, flip
+        n += dp_active() ? 1 + (e ? 2 : 1) + 1 : 1;  // sgd (+ transposes, flip unless fused into it)
       }
     }
     return n;
@@ -515,6 +520,15 @@ class MbPartition final : public PartitionBase {
                                                 (static_cast<size_t>(S_ / DIV[boundary]) * (S_ / DIV[boundary])); }
   // bf16 buffer of (m rows padded to 128) x c
   bf16* act(size_t m, int c) { return arena_.get<bf16>(pad128(m) * static_cast<size_t>(c) * sizeof(bf16)); }
+
+  // refresh_derived's three transposes / flips as regions of the candidate's slice (offsets from C.off)
+  static pbdk::FlipSet derived_regions(const SLayer& L, const SCand& C) {
+    pbdk::FlipSet fs;
+    if (C.L.e != 1) fs.reg[fs.count++] = pbdk::FlipRegion{C.L.we, C.L.E, 1, 1, L.cin, C.weT};
+    fs.reg[fs.count++] = pbdk::FlipRegion{C.L.wp, L.cout, 1, 1, C.L.E, C.wpT};
+    fs.reg[fs.count++] = pbdk::FlipRegion{C.L.wd, C.L.E, C.L.k, C.L.k, 1, C.wdF};
+    return fs;
+  }
 
   void refresh_derived(SLayer& L, SCand& C, cudaStream_t st) {
     if (L.stem) return;

@@ -283,6 +283,13 @@ class ResNetPartition final : public PartitionBase {
       refresh_flips(st);
       return;
     }
+    if (all_train() && fused_flips()) {  // one launch: update + shadows + flipped dgrad filters
+      pbdk::FlipSet fs;
+      for (const SBlock& s : sblocks_) fs.reg[fs.count++] = flip_region(s, s.base);
+      check(pbdk::sgd_momentum_flip(params_, mom_, grads_, shadow_, total_, d_.lr, d_.momentum, step_, fs, st),
+            "sgd");
+      return;
+    }
     if (all_train()) {
       check(pbdk::sgd_momentum(params_, mom_, grads_, shadow_, total_, d_.lr, d_.momentum, step_, st), "sgd");
       refresh_flips(st);
@@ -292,11 +299,12 @@ class ResNetPartition final : public PartitionBase {
     for (size_t i = 0; i < sblocks_.size(); ++i) {
       if (!trains(static_cast<int>(i))) continue;
       const SBlock& s = sblocks_[i];
-      check(pbdk::sgd_momentum(params_ + s.base, mom_ + s.base, grads_ + s.base, shadow_ + s.base, s.lay.total,
-                               d_.lr, d_.momentum, counter, st),
+      pbdk::FlipSet fs;
+      fs.reg[fs.count++] = flip_region(s, 0);
+      check(pbdk::sgd_momentum_flip(params_ + s.base, mom_ + s.base, grads_ + s.base, shadow_ + s.base,
+                                    s.lay.total, d_.lr, d_.momentum, counter, fs, st),
             "sgd");
       counter = nullptr;
-      check(pbdk_weight_flip(shadow_ + s.base + s.lay.w2, s.w2flip, s.cout, 3, 3, s.mid, st), "flip");
     }
   }
 
@@ -334,7 +342,10 @@ class ResNetPartition final : public PartitionBase {
       n += 3 + 2 + 1 + 2 + 1 + 2;  // convs, bn1 stats+apply, bn2+bnsc stats, mse(2), dgrad, bn_bwd(2)
       n += (s.p_w2.splits > 1 ? 2 : 1) + (s.p_wsc.splits > 1 ? 2 : 1) + (s.p_w1.splits > 1 ? 2 : 1);
     }
-    n += all_train() ? 1 + static_cast<int>(sblocks_.size()) : 2 * trained;  // sgd + flips
+    if (dp_active() || (all_train() && !fused_flips()))
+      n += all_train() ? 1 + static_cast<int>(sblocks_.size()) : 2 * trained;  // sgd + flips
+    else
+      n += all_train() ? 1 : trained;  // sgd with the flips fused (sgd_momentum_flip)
     return n;
   }
 
@@ -359,6 +370,13 @@ class ResNetPartition final : public PartitionBase {
   }
 
  private:
+  bool fused_flips() const { return sblocks_.size() <= static_cast<size_t>(pbdk::FlipSet::kMax); }
+
+  // conv2's filter [cout][3][3][mid] at offset base + lay.w2 of the updated vector -> w2flip
+  static pbdk::FlipRegion flip_region(const SBlock& s, size_t base) {
+    return pbdk::FlipRegion{base + s.lay.w2, s.cout, 3, 3, s.mid, s.w2flip};
+  }
+
   void refresh_flips(cudaStream_t st) {
     for (SBlock& s : sblocks_)
       check(pbdk_weight_flip(shadow_ + s.base + s.lay.w2, s.w2flip, s.cout, 3, 3, s.mid, st), "flip");

@@ -1106,6 +1106,53 @@ __global__ void sgd_kernel(float4* __restrict__ w, float4* __restrict__ v, const
   if (counter != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *counter += 1;
 }
 
+// sgd_kernel + the flipped bf16 dgrad filters (FlipSet) scattered from the same registers: the flip
+// launches that followed the update on the step's critical path are gone; values are bit-identical
+// (same round-to-nearest bf16 of the same fp32 weight).
+__global__ void sgd_flip_kernel(float4* __restrict__ w, float4* __restrict__ v, const float4* __restrict__ g,
+                                uint2* __restrict__ shadow, size_t n4, float lr, float mu, long long* counter,
+                                const FlipSet fs) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    float4 vv = v[i];
+    const float4 gg = g[i];
+    float4 ww = w[i];
+    vv.x = fmaf(mu, vv.x, gg.x);
+    vv.y = fmaf(mu, vv.y, gg.y);
+    vv.z = fmaf(mu, vv.z, gg.z);
+    vv.w = fmaf(mu, vv.w, gg.w);
+    ww.x = fmaf(-lr, vv.x, ww.x);
+    ww.y = fmaf(-lr, vv.y, ww.y);
+    ww.z = fmaf(-lr, vv.z, ww.z);
+    ww.w = fmaf(-lr, vv.w, ww.w);
+    v[i] = vv;
+    w[i] = ww;
+    shadow[i] = make_uint2(pack2(ww.x, ww.y), pack2(ww.z, ww.w));
+    const size_t e0 = 4 * i;
+    for (int q = 0; q < fs.count; ++q) {
+      const FlipRegion& R = fs.reg[q];
+      const size_t len = static_cast<size_t>(R.k) * R.r * R.s * R.c;
+      if (e0 + 4 <= R.off || e0 >= R.off + len) continue;
+      const float f[4] = {ww.x, ww.y, ww.z, ww.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const size_t e = e0 + j;
+        if (e < R.off || e >= R.off + len) continue;
+        size_t t = e - R.off;  // [co][r][s][ci]
+        const int ci = static_cast<int>(t % R.c);
+        t /= R.c;
+        const int ss = static_cast<int>(t % R.s);
+        t /= R.s;
+        const int rr = static_cast<int>(t % R.r);
+        const int co = static_cast<int>(t / R.r);
+        const size_t o = ((static_cast<size_t>(ci) * R.r + (R.r - 1 - rr)) * R.s + (R.s - 1 - ss)) * R.k + co;
+        static_cast<__nv_bfloat16*>(R.dst)[o] = __float2bfloat16_rn(f[j]);
+      }
+    }
+  }
+  if (counter != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *counter += 1;
+}
+
 // share_gradient + update_weight fused for a DP group: g = sum of the G members'
 // gradient slabs read straight from their device memory (NVLink peer loads; CUDA IPC mappings across
 // processes), added in member order on every member — so all members compute bit-identical weights
@@ -1470,6 +1517,21 @@ int sgd_momentum(float* w, float* v, const float* g, void* shadow, size_t n, flo
   return ok(cudaGetLastError());
 }
 
+int sgd_momentum_flip(float* w, float* v, const float* g, void* shadow, size_t n, float lr, float mu,
+                      long long* counter, const FlipSet& flips, cudaStream_t st) {
+  if (n % 4 != 0 || shadow == nullptr || flips.count < 0 || flips.count > FlipSet::kMax) return PBDK_EINVAL;
+  for (int q = 0; q < flips.count; ++q) {
+    const FlipRegion& R = flips.reg[q];
+    if (R.dst == nullptr || R.k < 1 || R.r < 1 || R.s < 1 || R.c < 1 ||
+        R.off + static_cast<size_t>(R.k) * R.r * R.s * R.c > n)
+      return PBDK_EINVAL;
+  }
+  sgd_flip_kernel<<<grid_for(static_cast<long long>(n / 4)), kThreads, 0, st>>>(
+      reinterpret_cast<float4*>(w), reinterpret_cast<float4*>(v), reinterpret_cast<const float4*>(g),
+      static_cast<uint2*>(shadow), n / 4, lr, mu, counter, flips);
+  return ok(cudaGetLastError());
+}
+
 int dp_gather(float* w, void* shadow, const float* const* peer_w, int count, int me, size_t n, cudaStream_t st) {
   if (n % 4 != 0 || count < 1 || count > 8 || me < 0 || me >= count) return PBDK_EINVAL;
   GradSources src{};
@@ -1544,6 +1606,19 @@ int pbdk_sgd_momentum(float* w, float* v, const float* g, void* w_bf16, size_t n
                       long long* step_counter, void* stream) {
   if (w == nullptr || v == nullptr || g == nullptr) return PBDK_EINVAL;
   return pbdk::sgd_momentum(w, v, g, w_bf16, n, lr, momentum, step_counter, static_cast<cudaStream_t>(stream));
+}
+
+int pbdk_sgd_momentum_flip(float* w, float* v, const float* g, void* w_bf16, size_t n, float lr, float momentum,
+                           long long* step_counter, const pbdk_flip_region* regions, int count, void* stream) {
+  if (w == nullptr || v == nullptr || g == nullptr || (count > 0 && regions == nullptr) || count < 0 ||
+      count > pbdk::FlipSet::kMax)
+    return PBDK_EINVAL;
+  pbdk::FlipSet fs;
+  for (int i = 0; i < count; ++i)
+    fs.reg[fs.count++] = pbdk::FlipRegion{regions[i].off, regions[i].k, regions[i].r, regions[i].s, regions[i].c,
+                                          regions[i].dst};
+  return pbdk::sgd_momentum_flip(w, v, g, w_bf16, n, lr, momentum, step_counter, fs,
+                                 static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

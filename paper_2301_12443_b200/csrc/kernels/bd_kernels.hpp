@@ -67,6 +67,21 @@ int bn_bwd(const void* g, const void* y, const float* mean_rstd, const float* ga
            float* red, float* dgamma, float* dbeta, void* dy, cudaStream_t st, int prec = 0);
 int sgd_momentum(float* w, float* v, const float* g, void* shadow, size_t n, float lr, float mu, long long* counter,
                  cudaStream_t st);
+// Flipped dgrad copies written by the update itself: region i covers elements [off, off + k*r*s*c) of
+// the updated vector (a [k][r][s][c] filter); its bf16 value (the shadow's rounding) is also stored at
+// dst[c'][r-1-r'][s-1-s'][k'] — what pbdk_weight_flip would produce from the shadow, without the launch.
+struct FlipRegion {
+  size_t off;
+  int k, r, s, c;
+  void* dst;
+};
+struct FlipSet {
+  static constexpr int kMax = 4;
+  int count = 0;
+  FlipRegion reg[kMax];
+};
+int sgd_momentum_flip(float* w, float* v, const float* g, void* shadow, size_t n, float lr, float mu,
+                      long long* counter, const FlipSet& flips, cudaStream_t st);
 
 // ---- self-finalizing variants of bn_stats / bn_stats2 / mse_bn_loss / bn_bwd (bf16 rows): one partial
 // launch per reduction instead of partial + finalize; every pass streams its rows through a TMA-staged

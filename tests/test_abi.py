@@ -94,6 +94,9 @@ def test_device_entry_points_validate_without_gpu():
     assert L.pbdk_conv_fprop(ctypes.byref(bad), None, None, None, None, None, 0, None) == 1
     assert L.pbdk_conv_wgrad_workspace_bytes(ctypes.byref(bad)) == 0
     assert L.pbdk_weight_flip(None, None, 1, 1, 1, 1, None) == 1
+    regs = (_lib.FlipRegion * 5)()
+    assert L.pbdk_sgd_momentum_flip(None, None, None, None, 4, 0.1, 0.9, None, regs, 1, None) == 1
+    assert L.pbdk_sgd_momentum_flip(None, None, None, None, 4, 0.1, 0.9, None, regs, 5, None) == 1
 
 
 def test_mb_supernet_layout_matches_oracle():

@@ -119,6 +119,47 @@ def test_weight_flip(L):
     assert torch.equal(wt, w.flip(1, 2).permute(3, 1, 2, 0).contiguous())
 
 
+def test_sgd_momentum_flip_equals_sgd_then_flip(L):
+    """The update with fused flips == pbdk_sgd_momentum followed by pbdk_weight_flip of the shadow
+    (bitwise: same fp32 update, same bf16 rounding), for the ResNet conv2 filter and the MBConv
+    transposes / depthwise flip, regions at unaligned offsets inside one vector."""
+    import ctypes as C
+
+    torch.manual_seed(5)
+    regs = [(12, 64, 3, 3, 32), (12 + 64 * 9 * 32 + 8, 96, 1, 1, 24), (40000, 48, 5, 5, 1), (52000, 20, 1, 1, 96)]
+    n = 56000
+    w0 = torch.randn(n, device="cuda")
+    v0 = torch.randn(n, device="cuda")
+    g = torch.randn(n, device="cuda")
+    ref_w, ref_v = w0.clone(), v0.clone()
+    ref_sh = torch.empty(n, device="cuda", dtype=torch.bfloat16)
+    assert L.lib().pbdk_sgd_momentum(ref_w.data_ptr(), ref_v.data_ptr(), g.data_ptr(), ref_sh.data_ptr(), n,
+                                     C.c_float(0.05), C.c_float(0.9), None, stream()) == 0
+    want = []
+    for off, k, r, s, c in regs:
+        wt = torch.empty(k * r * s * c, device="cuda", dtype=torch.bfloat16)
+        assert L.lib().pbdk_weight_flip(ref_sh[off:].data_ptr(), wt.data_ptr(), k, r, s, c, stream()) == 0
+        want.append(wt)
+    got = [torch.full_like(t, float("nan")) for t in want]
+    arr = (L.FlipRegion * len(regs))(*[L.FlipRegion(off, k, r, s, c, t.data_ptr())
+                                       for (off, k, r, s, c), t in zip(regs, got)])
+    w, v = w0.clone(), v0.clone()
+    sh = torch.empty(n, device="cuda", dtype=torch.bfloat16)
+    cnt = torch.zeros(1, device="cuda", dtype=torch.int64)
+    assert L.lib().pbdk_sgd_momentum_flip(w.data_ptr(), v.data_ptr(), g.data_ptr(), sh.data_ptr(), n,
+                                          C.c_float(0.05), C.c_float(0.9), cnt.data_ptr(), arr, len(regs),
+                                          stream()) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(w, ref_w) and torch.equal(v, ref_v) and torch.equal(sh, ref_sh)
+    assert int(cnt.item()) == 1
+    for a, b in zip(got, want):
+        assert torch.equal(a, b)
+    # ResNet conv2 region == the torch restatement of the flip
+    off, k, r, s, c = regs[0]
+    ref0 = ref_sh[off:off + k * r * s * c].view(k, r, s, c).flip(1, 2).permute(3, 1, 2, 0).reshape(-1)
+    assert torch.equal(got[0], ref0)
+
+
 def test_unsupported_shapes_fail_loudly(L):
     d = L.ConvDesc(2, 30, 30, 64, 64, 3, 3, 1, 1, 30, 30)  # 30x30 output does not tile 128 rows
     x = torch.zeros(2, 30, 30, 64, device="cuda", dtype=torch.bfloat16)
