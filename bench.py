@@ -9,8 +9,9 @@ ResNet-18-CIFAR 4-block teacher -> slim residual student, bf16 operands / fp32
 accumulation and master weights, global batch 256 per GPU.  At N=1 the whole
 chain runs on one GPU (the IR point of the AHD space, schedule.cpp:305-317).
 Under torchrun (N>1) every rank runs the schedule best_schedule() picks on a
-device-measured profile (weak scaling: global batch 256*N), with NCCL relays
-between pipeline stages and NCCL allreduce inside DP groups (runtime.py).
+device-measured profile (weak scaling: global batch 256*N), with K11 peer-memory
+relays between pipeline stages (--relay nccl: NCCL send/recv) and the DP exchange
+as a reduce-scatter + all-gather over peer memory fused into the update (runtime.py).
 
 One JSON line on rank 0; see DESIGN.md §5 for every field.
 """

@@ -51,10 +51,13 @@ struct FpropCfg {
   static constexpr int B_RES_MAX = 96 * 1024;  // resident filter budget
   static constexpr int STAGE = round_up(A_BYTES + (BRES ? 0 : B_BYTES), 1024);
   static constexpr int RING = (BRES ? kFpropBudget - B_RES_MAX : kFpropBudget);
-  static constexpr int STAGES = (RING / STAGE) > 8 ? 8 : (RING / STAGE);
+  // small stages (16 / 32-channel inputs: 32 / 64-byte box rows) need more of them in flight
+  static constexpr int MAX_STAGES = STAGE <= 4096 ? 24 : STAGE <= 8192 ? 16 : 8;
+  static constexpr int STAGES = (RING / STAGE) > MAX_STAGES ? MAX_STAGES : (RING / STAGE);
   static constexpr int ACC_COLS = BN < 32 ? 32 : BN;
   static constexpr int TMEM_COLS = tmem_cols_for(2 * ACC_COLS);
-  static constexpr int SMEM = STAGES * STAGE + (BRES ? B_RES_MAX : 0) + 1024 + 256;
+  static constexpr int BAR_BYTES = round_up(2 * STAGES * 8 + 5 * 8 + 4, 256);
+  static constexpr int SMEM = STAGES * STAGE + (BRES ? B_RES_MAX : 0) + 1024 + BAR_BYTES;
 };
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
