@@ -394,9 +394,12 @@ class MbPartition final : public PartitionBase {
   }
 
   void student_body(cudaStream_t caller, bool fork) override {
-    static const int red = [] { const char* e = pbd::knob_env("PBDK_MB_RED"); return e ? std::atoi(e) : 0; }();
-    static const int app = [] { const char* e = pbd::knob_env("PBDK_MB_APPLY"); return e ? std::atoi(e) : 0; }();
-    const pbdk::GridScope grids(red, app);
+    // measured (scripts/ab_mb_grids2.sh, profiles/r02_ab_mb_grids.txt): one reduction CTA per SM, 296-CTA
+    // applies and >= 1 MB per reduction CTA beside the six concurrent student streams: MobileNetV2 step
+    // 16.20 -> 15.81 ms, EfficientNet-B0 19.90 -> 19.58 ms
+    static const int red = [] { const char* e = pbd::knob_env("PBDK_MB_RED"); return e ? std::atoi(e) : 148; }();
+    static const int app = [] { const char* e = pbd::knob_env("PBDK_MB_APPLY"); return e ? std::atoi(e) : 296; }();
+    const pbdk::GridScope grids(red, app, 1 << 20);
     if (fork) cuda(cudaEventRecord(fork_, caller), "event");
     for (size_t i = 0; i < sblocks_.size(); ++i) {
       SBlock& sb = sblocks_[i];

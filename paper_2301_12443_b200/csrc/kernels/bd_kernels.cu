@@ -308,7 +308,7 @@ int env_int(const char* name, int dflt) {
 // and applies 1184 -> 296 CTAs took the step from 0.997 to 0.932 ms although each kernel alone is
 // slower — a one-CTA-per-SM wave leaves the other streams' convs their SMs.  The MBConv step (passes
 // mostly alone) prefers 296 / 1184 (19.74 vs 20.17 ms).  PBDK_RED_TARGET / PBDK_APPLY_CTAS override.
-thread_local int t_red = 0, t_apply = 0;
+thread_local int t_red = 0, t_apply = 0, t_fix_min = 0;
 int red_target() {
   static const int e = env_int("PBDK_RED_TARGET", 0);
   return e > 0 ? e : (t_red > 0 ? t_red : 148 * 2);
@@ -1216,13 +1216,16 @@ inline int ok(cudaError_t e) { return e == cudaSuccess ? PBDK_OK : PBDK_ECUDA; }
 
 }  // namespace
 
-GridScope::GridScope(int red_ctas, int apply_ctas) : saved_red(t_red), saved_apply(t_apply) {
+GridScope::GridScope(int red_ctas, int apply_ctas, int fix_min_bytes)
+    : saved_red(t_red), saved_apply(t_apply), saved_fix_min(t_fix_min) {
   t_red = red_ctas;
   t_apply = apply_ctas;
+  t_fix_min = fix_min_bytes;
 }
 GridScope::~GridScope() {
   t_red = saved_red;
   t_apply = saved_apply;
+  t_fix_min = saved_fix_min;
 }
 
 size_t reduce_workspace_floats(int m, int c, int nv) {
@@ -1401,8 +1404,8 @@ int cap_chunks(int target, long long bytes, int min_bytes) {
 }
 int fix_min_bytes() {  // PBDK_FIX_MIN_BYTES: reduction passes (CIFAR step 0.891 -> 0.873 ms at 256 KB; 128 KB-512 KB
                        // within 1 %, 1 MB 0.94 ms; r02_ab_minbytes.txt)
-  static const int b = env_int("PBDK_FIX_MIN_BYTES", 256 << 10);
-  return b;
+  static const int b = env_int("PBDK_FIX_MIN_BYTES", -1);  // experiments: 0 = no cap
+  return b >= 0 ? b : (t_fix_min > 0 ? t_fix_min : 256 << 10);
 }
 int apply_min_bytes() {  // PBDK_APPLY_MIN_BYTES: elementwise passes (off: 256 KB measured neutral)
   static const int b = env_int("PBDK_APPLY_MIN_BYTES", 0);

@@ -40,9 +40,9 @@ size_t reduce_workspace_floats(int m, int c, int nv);
 // passes run mostly alone (MBConv step).  The ResNet step runs them beside the conv kernels of the
 // other student streams and uses GridScope(148, 296) (see bd_kernels.cu).
 struct GridScope {
-  GridScope(int red_ctas, int apply_ctas);
+  GridScope(int red_ctas, int apply_ctas, int fix_min_bytes = 0);  // 0: the default
   ~GridScope();
-  int saved_red, saved_apply;
+  int saved_red, saved_apply, saved_fix_min;
 };
 // synthetic / host images of side x side pixels, stored [n][side][side][16] bf16
 // prec 1: split fp32 [n][side][side][2*32] (conv_tf32.hpp) instead

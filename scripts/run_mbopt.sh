@@ -1,7 +1,7 @@
 #!/bin/bash
 # MB kernel changes: bitwise A/B vs the pre-change build (lib-exp), GPU MB tests, MB benches, MB launch list
 mkdir -p gpurun_out
-PBD_LIB_VARIANT=exp timeout 300 python scripts/ab_bitwise_mb.py a > gpurun_out/abmb.log 2>&1
+env PBD_LIB_VARIANT=exp $AB_ENV timeout 300 python scripts/ab_bitwise_mb.py a > gpurun_out/abmb.log 2>&1
 timeout 300 python scripts/ab_bitwise_mb.py b >> gpurun_out/abmb.log 2>&1
 python scripts/ab_bitwise_mb.py cmp >> gpurun_out/abmb.log 2>&1
 timeout 900 python -m pytest tests/test_gpu_mb.py tests/test_gpu_dw.py tests/test_gpu_nas.py tests/test_gpu_parity_full.py -x -q > gpurun_out/pytest_mb.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_mb.log
