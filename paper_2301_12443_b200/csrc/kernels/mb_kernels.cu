@@ -245,6 +245,17 @@ __global__ void __launch_bounds__(kT) dw_fwd_tiled_kernel(const __grid_constant_
       for (int u = 0; u < QT; ++u)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[u][j] = 0.0f;
+      const size_t orow = (static_cast<size_t>(n) * P + p0 + pr) * Q;
+      // data gradient: the ReLU6 mask rows requested before the taps (latency hidden); not for 5x5, whose
+      // 128 registers (two CTAs per SM) the prefetch would exceed
+      constexpr bool PF = DG && K != 5;
+      uint4 am[PF ? QT : 1];
+      if constexpr (PF) {
+#pragma unroll
+        for (int u = 0; u < QT; ++u)
+          if (amask != nullptr && q0 + u < Q)
+            am[u] = __ldg(reinterpret_cast<const uint4*>(amask + (orow + q0 + u) * C + c0 + 8 * g));
+      }
 #pragma unroll
       for (int ri = 0; ri < K; ++ri) {
         const int r = DG ? K - 1 - ri : ri;  // window row
@@ -269,7 +280,6 @@ __global__ void __launch_bounds__(kT) dw_fwd_tiled_kernel(const __grid_constant_
           }
         }
       }
-      const size_t orow = (static_cast<size_t>(n) * P + p0 + pr) * Q;
       float bv[8];
 #pragma unroll
       for (int jj = 0; jj < 8; ++jj) bv[jj] = bias != nullptr ? bias[c0 + 8 * g + jj] : 0.0f;
@@ -280,7 +290,16 @@ __global__ void __launch_bounds__(kT) dw_fwd_tiled_kernel(const __grid_constant_
         if constexpr (DG) {
           if (amask != nullptr) {
             float av[8];
-            ld8(amask + (orow + q0 + u) * C + c0 + 8 * g, av);
+            if constexpr (PF) {
+              const uint32_t w4[4] = {am[u].x, am[u].y, am[u].z, am[u].w};
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) {
+                av[2 * jj] = __uint_as_float(w4[jj] << 16);
+                av[2 * jj + 1] = __uint_as_float(w4[jj] & 0xFFFF0000u);
+              }
+            } else {
+              ld8(amask + (orow + q0 + u) * C + c0 + 8 * g, av);
+            }
 #pragma unroll
             for (int jj = 0; jj < 8; ++jj) o[jj] = (av[jj] > 0.0f && av[jj] < 6.0f) ? acc[u][jj] : 0.0f;
           } else {
@@ -339,6 +358,8 @@ __global__ void __launch_bounds__(kT) dw_dgrad_kernel(const __nv_bfloat16* __res
     }
     const int c0 = g * 8;
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint4 am = make_uint4(0u, 0u, 0u, 0u);  // the ReLU6 mask row, requested before the taps
+    if (act != nullptr) am = __ldg(reinterpret_cast<const uint4*>(act + static_cast<size_t>(pix) * C + c0));
 #pragma unroll
     for (int r = 0; r < K; ++r) {
       const int pn = h + PAD - r;
@@ -356,10 +377,13 @@ __global__ void __launch_bounds__(kT) dw_dgrad_kernel(const __nv_bfloat16* __res
       }
     }
     if (act != nullptr) {
-      float av[8];
-      ld8(act + static_cast<size_t>(pix) * C + c0, av);
+      const uint32_t w4[4] = {am.x, am.y, am.z, am.w};
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[j] = (av[j] > 0.0f && av[j] < 6.0f) ? acc[j] : 0.0f;
+      for (int jj = 0; jj < 4; ++jj) {
+        const float a0 = __uint_as_float(w4[jj] << 16), a1 = __uint_as_float(w4[jj] & 0xFFFF0000u);
+        acc[2 * jj] = (a0 > 0.0f && a0 < 6.0f) ? acc[2 * jj] : 0.0f;
+        acc[2 * jj + 1] = (a1 > 0.0f && a1 < 6.0f) ? acc[2 * jj + 1] : 0.0f;
+      }
     }
     st8(dx + static_cast<size_t>(pix) * C + c0, acc);
   }
@@ -370,7 +394,7 @@ __global__ void __launch_bounds__(kT) dw_dgrad_kernel(const __nv_bfloat16* __res
 // filter row r = blockIdx.z; every thread accumulates K x 8 fp32 sums over its pixels, then the
 // CTA adds the pixel lanes in lane order -> partial[chunk][c][r][s].
 template <int K, int ST>
-__global__ void __launch_bounds__(kT) dw_wgrad_partial_kernel(const __nv_bfloat16* __restrict__ a,
+__global__ void __launch_bounds__(kT, K >= 7 ? 2 : 1) dw_wgrad_partial_kernel(const __nv_bfloat16* __restrict__ a,
                                                               const __nv_bfloat16* __restrict__ dy,
                                                               float* __restrict__ partial, int N, int H, int W, int C,
                                                               int P, int Q, int lanes_c, int rows_per_chunk) {
