@@ -14,3 +14,8 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/bench_ncu.log 2>&1
 tail -3 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log
 cat gpurun_out/bench*.json
+python scripts/launch_summary.py gpurun_out/launches.csv > gpurun_out/launch_summary.txt 2>&1
+bash scripts/ncu_dominant.sh
+ncu -i gpurun_out/dominant.ncu-rep --page raw --csv > gpurun_out/dominant_raw.csv 2>&1
+timeout 300 python scripts/conv_shape_shares.py > gpurun_out/conv_shapes.txt 2>&1
+head -12 gpurun_out/launch_summary.txt
