@@ -797,6 +797,7 @@ __device__ __forceinline__ void row_pipe(const PipeIn<NIN>& in, int C, int r0, i
     fence_barrier_init();
   }
   __syncthreads();
+  grid_dep_wait();  // PDL (launch_pipe): every global access of the pass kernels comes after this point
   if (threadIdx.x == 0)
     for (int t = 0; t < min(ntiles, kPipeStages); ++t) issue(t);
   pre();
@@ -1419,6 +1420,11 @@ RowTiling apply_tiling(int m, int c, int v, int nin) {
                     cap_chunks(std::max(1, apply_cap() / apply_pipe_div()), 2LL * m * c * nin, apply_min_bytes()));
 }
 
+bool pipe_pdl() {  // PBD_PDL=0 / PBDK_PIPE_PDL=0: plain launches (experiments build, A/B runs)
+  static const bool on = pbd::pdl_enabled() && env_int("PBDK_PIPE_PDL", 1) != 0;
+  return on;
+}
+
 template <class K, class... Args>
 cudaError_t launch_pipe(K kernel, int grid, size_t smem, cudaStream_t st, Args... args) {
   constexpr size_t kMax = 2 * kPipeStages * kPipeStageBytes;  // tiles rounded up to rpp rows stay below
@@ -1430,8 +1436,19 @@ cudaError_t launch_pipe(K kernel, int grid, size_t smem, cudaStream_t st, Args..
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  kernel<<<grid, kThreads, smem, st>>>(args...);
-  return cudaGetLastError();
+  // programmatic dependent launch: the pass's CTAs are scheduled while the previous kernel of the stream
+  // drains; row_pipe waits (griddepcontrol.wait) before its first global access
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pipe_pdl() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
 int bn_stats_fix(const void* y0, const void* y1, int m, int c, FixScratch fx, float* mr0, float* mr1,
