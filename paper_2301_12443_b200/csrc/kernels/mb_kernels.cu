@@ -441,6 +441,8 @@ __global__ void __launch_bounds__(kT, K >= 7 ? 2 : 1) dw_wgrad_partial_kernel(co
       // (ST*u + s) % K, and the ST vectors loaded after step u replace the slots of taps 0..ST-1 —
       // no register moves; the fmaf order per sum (q ascending) is unchanged.
       constexpr int U = K >= 5 ? K : 1;  // K = 3: the plain shift (2 x 8 moves) measured faster
+      // K = 3, stride 1: four q-steps unrolled so the next steps' loads are issued ahead of this step's fmas
+#pragma unroll(K >= 5 || ST != 1 ? 1 : 4)
       for (int q0 = 0; q0 < Q; q0 += U) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
