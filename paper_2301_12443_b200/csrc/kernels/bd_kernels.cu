@@ -1107,14 +1107,75 @@ __global__ void sgd_kernel(float4* __restrict__ w, float4* __restrict__ v, const
   if (counter != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *counter += 1;
 }
 
-// sgd_kernel + the flipped bf16 dgrad filters (FlipSet) scattered from the same registers: the flip
-// launches that followed the update on the step's critical path are gone; values are bit-identical
-// (same round-to-nearest bf16 of the same fp32 weight).
-__global__ void sgd_flip_kernel(float4* __restrict__ w, float4* __restrict__ v, const float4* __restrict__ g,
-                                uint2* __restrict__ shadow, size_t n4, float lr, float mu, long long* counter,
-                                const FlipSet fs) {
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n4;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+// sgd_kernel + the flipped bf16 dgrad filters (FlipSet) written by the same launch: the flip launches
+// that followed the update on the step's critical path are gone; values are bit-identical (same
+// round-to-nearest bf16 of the same fp32 weight).  Regions whose k and c are multiples of 32 (and whose
+// offset is float4-aligned) are updated by the trailing "tile" CTAs as 32x32 (k, c) tiles per tap —
+// coalesced fp32 reads / writes along c, a shared-memory transpose, coalesced bf16 stores of the flipped
+// copy along k — and skipped by the flat loop; any other region is scattered element by element.
+struct FlipTiles {
+  int count;                         // regions handled by tiles
+  int region[FlipSet::kMax];         // FlipSet index of each tiled region
+  int base[FlipSet::kMax + 1];       // first tile of each tiled region (prefix sums)
+  // the flat loop's float4 index space: the gaps between the tiled regions, compacted
+  int nseg;
+  unsigned long long seg_lo[FlipSet::kMax + 1], seg_base[FlipSet::kMax + 2];
+};
+
+__device__ __forceinline__ void sgd1(float& w, float& v, float g, float lr, float mu) {
+  v = fmaf(mu, v, g);
+  w = fmaf(-lr, v, w);
+}
+
+__global__ void __launch_bounds__(kThreads) sgd_flip_kernel(float4* __restrict__ w, float4* __restrict__ v,
+                                                           const float4* __restrict__ g, uint2* __restrict__ shadow,
+                                                           size_t n4, float lr, float mu, long long* counter,
+                                                           const FlipSet fs, const FlipTiles ft) {
+  const int ntiles = ft.base[ft.count];
+  if (static_cast<int>(blockIdx.x) < ntiles) {  // ---- tile part (first, so it starts early): one 32x32 (k, c) tile of one tap
+    __shared__ __nv_bfloat16 tile[32][34];
+    const int t = blockIdx.x;
+    int q = 0;
+    while (q + 1 < ft.count && t >= ft.base[q + 1]) ++q;
+    const FlipRegion& R = fs.reg[ft.region[q]];
+    const int taps = R.r * R.s;
+    int rest = t - ft.base[q];
+    const int tap = rest % taps;
+    rest /= taps;
+    const int cb = rest % (R.c / 32);
+    const int kb = rest / (R.c / 32);
+    const int rr = tap / R.s, ss = tap - rr * R.s;
+    float* wf = reinterpret_cast<float*>(w);
+    float* vf = reinterpret_cast<float*>(v);
+    const float* gf = reinterpret_cast<const float*>(g);
+    __nv_bfloat16* sh = reinterpret_cast<__nv_bfloat16*>(shadow);
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    for (int kk = wp; kk < 32; kk += kThreads / 32) {  // row = output channel k, lanes along c
+      const int k = kb * 32 + kk, c = cb * 32 + lane;
+      const size_t e = R.off + (static_cast<size_t>(k) * taps + tap) * R.c + c;
+      float ww = wf[e], vv = vf[e];
+      sgd1(ww, vv, gf[e], lr, mu);
+      wf[e] = ww;
+      vf[e] = vv;
+      const __nv_bfloat16 b = __float2bfloat16_rn(ww);
+      sh[e] = b;
+      tile[kk][lane] = b;
+    }
+    __syncthreads();
+    __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(R.dst);
+    const int ftap = (R.r - 1 - rr) * R.s + (R.s - 1 - ss);
+    for (int cc = wp; cc < 32; cc += kThreads / 32) {  // row = input channel c, lanes along k
+      const int c = cb * 32 + cc, k = kb * 32 + lane;
+      dst[(static_cast<size_t>(c) * taps + ftap) * R.k + k] = tile[lane][cc];
+    }
+    return;
+  }
+  const unsigned long long total = ft.seg_base[ft.nseg];
+  for (unsigned long long ci = (blockIdx.x - ntiles) * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+       ci < total; ci += static_cast<unsigned long long>(gridDim.x - ntiles) * blockDim.x) {
+    int j = 0;
+    while (j + 1 < ft.nseg && ci >= ft.seg_base[j + 1]) ++j;
+    const size_t i = ft.seg_lo[j] + (ci - ft.seg_base[j]);
     float4 vv = v[i];
     const float4 gg = g[i];
     float4 ww = w[i];
@@ -1151,7 +1212,7 @@ __global__ void sgd_flip_kernel(float4* __restrict__ w, float4* __restrict__ v, 
       }
     }
   }
-  if (counter != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *counter += 1;
+  if (counter != nullptr && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *counter += 1;
 }
 
 // share_gradient + update_weight fused for a DP group: g = sum of the G members'
@@ -1546,9 +1607,48 @@ int sgd_momentum_flip(float* w, float* v, const float* g, void* shadow, size_t n
         R.off + static_cast<size_t>(R.k) * R.r * R.s * R.c > n)
       return PBDK_EINVAL;
   }
-  sgd_flip_kernel<<<grid_for(static_cast<long long>(n / 4)), kThreads, 0, st>>>(
+  // tiled regions (k, c multiples of 32, float4-aligned offset) first, then the scattered ones; the
+  // flat loop skips the tiled regions' float4 ranges (their length is a multiple of 4)
+  FlipTiles ft{};
+  FlipSet packed;
+  int tiles = 0;
+  std::pair<size_t, size_t> cut[FlipSet::kMax];  // tiled float4 ranges
+  for (int pass = 0; pass < 2; ++pass)
+    for (int q = 0; q < flips.count; ++q) {
+      const FlipRegion& R = flips.reg[q];
+      const bool tiled = R.k % 32 == 0 && R.c % 32 == 0 && R.off % 4 == 0;
+      if (tiled != (pass == 0)) continue;
+      if (tiled) {
+        const size_t len = static_cast<size_t>(R.k) * R.r * R.s * R.c;
+        cut[ft.count] = {R.off / 4, (R.off + len) / 4};
+        ft.region[ft.count] = packed.count;
+        ft.base[ft.count] = tiles;
+        tiles += R.r * R.s * (R.k / 32) * (R.c / 32);
+        ++ft.count;
+      }
+      packed.reg[packed.count++] = R;
+    }
+  ft.base[ft.count] = tiles;
+  for (int a = 1; a < ft.count; ++a)  // sort the (at most kMax) ranges by offset
+    for (int b = a; b > 0 && cut[b].first < cut[b - 1].first; --b) std::swap(cut[b], cut[b - 1]);
+  size_t at = 0, base = 0;
+  for (int u = 0; u <= ft.count; ++u) {  // gaps [at, next cut) and the tail [at, n4)
+    const size_t end = u < ft.count ? cut[u].first : n / 4;
+    if (end < at) return PBDK_EINVAL;  // overlapping regions
+    if (end > at) {
+      ft.seg_lo[ft.nseg] = at;
+      ft.seg_base[ft.nseg] = base;
+      base += end - at;
+      ++ft.nseg;
+    }
+    if (u < ft.count) at = cut[u].second;
+  }
+  if (ft.nseg == 0) ft.seg_lo[ft.nseg++] = 0;  // empty flat space: one empty segment
+  ft.seg_base[ft.nseg] = base;
+  const int flat = grid_for(static_cast<long long>(std::max<size_t>(base, 1)));
+  sgd_flip_kernel<<<tiles + flat, kThreads, 0, st>>>(
       reinterpret_cast<float4*>(w), reinterpret_cast<float4*>(v), reinterpret_cast<const float4*>(g),
-      static_cast<uint2*>(shadow), n / 4, lr, mu, counter, flips);
+      static_cast<uint2*>(shadow), n / 4, lr, mu, counter, packed, ft);
   return ok(cudaGetLastError());
 }
 

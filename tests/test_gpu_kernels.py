@@ -119,15 +119,22 @@ def test_weight_flip(L):
     assert torch.equal(wt, w.flip(1, 2).permute(3, 1, 2, 0).contiguous())
 
 
-def test_sgd_momentum_flip_equals_sgd_then_flip(L):
+@pytest.mark.parametrize("regs", [
+    # ResNet conv2 filter (32x32-tiled transpose) + MBConv transposes / depthwise flip (scattered)
+    [(12, 64, 3, 3, 32), (12 + 64 * 9 * 32 + 8, 96, 1, 1, 24), (40000, 48, 5, 5, 1), (52000, 20, 1, 1, 96)],
+    # tiled only: the four student conv2 shapes of the CIFAR step at their executor offsets' alignment
+    [(4, 64, 3, 3, 32), (20000, 128, 3, 3, 64), (96000, 256, 3, 3, 128), (400000, 64, 1, 1, 96)],
+    # unaligned offset: a k, c multiple of 32 that must still take the scatter path
+    [(6, 64, 3, 3, 32)],
+], ids=["mixed", "tiled", "unaligned"])
+def test_sgd_momentum_flip_equals_sgd_then_flip(L, regs):
     """The update with fused flips == pbdk_sgd_momentum followed by pbdk_weight_flip of the shadow
-    (bitwise: same fp32 update, same bf16 rounding), for the ResNet conv2 filter and the MBConv
-    transposes / depthwise flip, regions at unaligned offsets inside one vector."""
+    (bitwise: same fp32 update, same bf16 rounding), for the ResNet conv2 filters (tiled transpose)
+    and the MBConv transposes / depthwise flip (scattered), regions at unaligned offsets too."""
     import ctypes as C
 
     torch.manual_seed(5)
-    regs = [(12, 64, 3, 3, 32), (12 + 64 * 9 * 32 + 8, 96, 1, 1, 24), (40000, 48, 5, 5, 1), (52000, 20, 1, 1, 96)]
-    n = 56000
+    n = 420000
     w0 = torch.randn(n, device="cuda")
     v0 = torch.randn(n, device="cuda")
     g = torch.randn(n, device="cuda")
