@@ -1129,8 +1129,8 @@ __device__ __forceinline__ void sgd1(float& w, float& v, float g, float lr, floa
 
 __global__ void __launch_bounds__(kThreads) sgd_flip_kernel(float4* __restrict__ w, float4* __restrict__ v,
                                                            const float4* __restrict__ g, uint2* __restrict__ shadow,
-                                                           size_t n4, float lr, float mu, long long* counter,
-                                                           const FlipSet fs, const FlipTiles ft) {
+                                                           float lr, float mu, long long* counter, const FlipSet fs,
+                                                           const FlipTiles ft) {
   const int ntiles = ft.base[ft.count];
   if (static_cast<int>(blockIdx.x) < ntiles) {  // ---- tile part (first, so it starts early): one 32x32 (k, c) tile of one tap
     __shared__ __nv_bfloat16 tile[32][34];
@@ -1648,7 +1648,7 @@ int sgd_momentum_flip(float* w, float* v, const float* g, void* shadow, size_t n
   const int flat = grid_for(static_cast<long long>(std::max<size_t>(base, 1)));
   sgd_flip_kernel<<<tiles + flat, kThreads, 0, st>>>(
       reinterpret_cast<float4*>(w), reinterpret_cast<float4*>(v), reinterpret_cast<const float4*>(g),
-      static_cast<uint2*>(shadow), n / 4, lr, mu, counter, packed, ft);
+      static_cast<uint2*>(shadow), lr, mu, counter, packed, ft);
   return ok(cudaGetLastError());
 }
 
