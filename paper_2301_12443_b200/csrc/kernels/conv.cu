@@ -55,8 +55,10 @@ struct FpropCfg {
   static constexpr int MAX_STAGES = STAGE <= 4096 ? 24 : STAGE <= 8192 ? 16 : 8;
   static constexpr int STAGES = (RING / STAGE) > MAX_STAGES ? MAX_STAGES : (RING / STAGE);
   static constexpr int ACC_COLS = BN < 32 ? 32 : BN;
-  static constexpr int TMEM_COLS = tmem_cols_for(2 * ACC_COLS);
-  static constexpr int BAR_BYTES = round_up(2 * STAGES * 8 + 5 * 8 + 4, 256);
+  // TMEM accumulators in rotation (conv_fprop_kernel): four for N <= 64 tiles (256 columns), two above
+  static constexpr int NACC = ACC_COLS <= 64 ? 4 : 2;
+  static constexpr int TMEM_COLS = tmem_cols_for(NACC * ACC_COLS);
+  static constexpr int BAR_BYTES = round_up(2 * STAGES * 8 + (2 * NACC + 1) * 8 + 4, 256);
   static constexpr int SMEM = STAGES * STAGE + (BRES ? B_RES_MAX : 0) + 1024 + BAR_BYTES;
 };
 
@@ -246,9 +248,9 @@ __global__ void __launch_bounds__(epi_threads(EPW), 1)
   uint8_t* bres = smem + C::STAGES * C::STAGE;  // resident filter (BRES)
   uint64_t* full = reinterpret_cast<uint64_t*>(bres + (BRES ? C::B_RES_MAX : 0));
   uint64_t* empty = full + C::STAGES;
-  uint64_t* tfull = empty + C::STAGES;  // [2]
-  uint64_t* tempty = tfull + 2;         // [2]
-  uint64_t* bfull = tempty + 2;
+  uint64_t* tfull = empty + C::STAGES;  // [NACC]
+  uint64_t* tempty = tfull + C::NACC;   // [NACC]
+  uint64_t* bfull = tempty + C::NACC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
 
   const int warp = warp_id();
@@ -263,7 +265,7 @@ __global__ void __launch_bounds__(epi_threads(EPW), 1)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < C::NACC; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 4 * EPW);
     }
@@ -317,8 +319,8 @@ __global__ void __launch_bounds__(epi_threads(EPW), 1)
       if (BRES) mbar_wait(bfull, 0);
       int it = 0, lt = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
-        const int acc = lt & 1;
-        if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
+        const int acc = lt % C::NACC;
+        if (lt >= C::NACC) mbar_wait(&tempty[acc], ((lt / C::NACC) - 1) & 1);
         tc_fence_after();
         const uint32_t dacc = tmem + static_cast<uint32_t>(acc * C::ACC_COLS);
         for (int kb = 0; kb < num_kb; ++kb, ++it) {
@@ -345,7 +347,7 @@ __global__ void __launch_bounds__(epi_threads(EPW), 1)
     const int c_lo = ((warp - 2) >> 2) * CW;
     int lt = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
-      const int acc = lt & 1;
+      const int acc = lt % C::NACC;
       const int m_tile = t / a.n_tiles;
       const int k0 = (t - m_tile * a.n_tiles) * BN;
       const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * C::ACC_COLS);
@@ -353,7 +355,7 @@ __global__ void __launch_bounds__(epi_threads(EPW), 1)
       const int t2 = m_tile / a.tiles_q;
       const TileRows rows{&a, (t2 / a.tiles_p) * a.bn, (t2 % a.tiles_p) * a.bh, tq * a.bw};
       fprop_epilogue<CW>(a, trow + c_lo, quarter * 32 + lane, k0 + c_lo, rows, [&] {
-        mbar_wait(&tfull[acc], (lt >> 1) & 1);
+        mbar_wait(&tfull[acc], (lt / C::NACC) & 1);
         tc_fence_after();
       });
       tc_fence_before();
@@ -748,7 +750,9 @@ struct HaloCfg {
   static constexpr int B_BYTES = BN * SW;
   static constexpr int B_RES_MAX = 96 * 1024;
   static constexpr int ACC_COLS = BN < 32 ? 32 : BN;
-  static constexpr int TMEM_COLS = tmem_cols_for(2 * ACC_COLS);
+  // TMEM accumulators in rotation: the MMA warp may run up to NACC-1 tiles ahead of the epilogue
+  static constexpr int NACC = ACC_COLS <= 64 ? 4 : 2;
+  static constexpr int TMEM_COLS = tmem_cols_for(NACC * ACC_COLS);
   static constexpr int ROWS = 3 + (129 + WP - 1) / WP;  // padded rows one 128-row tile touches
   static constexpr int BOX_BYTES = ROWS * WP * SW;
   static constexpr int STAGE = round_up(BOX_BYTES, 1024);
@@ -768,8 +772,8 @@ __global__ void __launch_bounds__(epi_threads(EPW), 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(bres + C::B_RES_MAX);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* bfull = tempty + 2;
+  uint64_t* tempty = tfull + C::NACC;
+  uint64_t* bfull = tempty + C::NACC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
 
   const int warp = warp_id();
@@ -784,7 +788,7 @@ __global__ void __launch_bounds__(epi_threads(EPW), 1)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < C::NACC; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 4 * EPW);
     }
@@ -836,8 +840,8 @@ __global__ void __launch_bounds__(epi_threads(EPW), 1)
       int lt = 0, st = 0;
       uint32_t ph = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
-        const int acc = lt & 1;
-        if (lt >= 2 && !DBG_IS(a, 8)) mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
+        const int acc = lt % C::NACC;
+        if (lt >= C::NACC && !DBG_IS(a, 8)) mbar_wait(&tempty[acc], ((lt / C::NACC) - 1) & 1);
         tc_fence_after();
         const uint32_t dacc = tmem + static_cast<uint32_t>(acc * C::ACC_COLS);
         const int j0 = (t % a.tiles_img) * 128 % WP;
@@ -870,12 +874,12 @@ __global__ void __launch_bounds__(epi_threads(EPW), 1)
     const int c_lo = ((warp - 2) >> 2) * CW;
     int lt = 0;
     for (int t = blockIdx.x; t < (DBG_IS(a, 8) ? 0 : total); t += gridDim.x, ++lt) {
-      const int acc = lt & 1;
+      const int acc = lt % C::NACC;
       const int img = t / a.tiles_img;
       const HaloRows rows{&a, img, (t - img * a.tiles_img) * 128, WP};
       const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * C::ACC_COLS);
       fprop_epilogue<CW>(a, trow + c_lo, quarter * 32 + lane, c_lo, rows, [&] {
-        mbar_wait(&tfull[acc], (lt >> 1) & 1);
+        mbar_wait(&tfull[acc], (lt / C::NACC) & 1);
         tc_fence_after();
       });
       tc_fence_before();
