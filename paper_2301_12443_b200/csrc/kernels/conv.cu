@@ -55,8 +55,9 @@ struct FpropCfg {
   static constexpr int MAX_STAGES = STAGE <= 4096 ? 24 : STAGE <= 8192 ? 16 : 8;
   static constexpr int STAGES = (RING / STAGE) > MAX_STAGES ? MAX_STAGES : (RING / STAGE);
   static constexpr int ACC_COLS = BN < 32 ? 32 : BN;
-  // TMEM accumulators in rotation (conv_fprop_kernel): four for N <= 64 tiles (256 columns), two above
-  static constexpr int NACC = ACC_COLS <= 64 ? 4 : 2;
+  // TMEM accumulators in rotation (conv_fprop_kernel): four for N <= 128 tiles (up to all 512 columns:
+  // every TMEM-using kernel needs > 114 KB of shared memory, so no two of their CTAs share an SM), two above
+  static constexpr int NACC = ACC_COLS <= 128 ? 4 : 2;
   static constexpr int TMEM_COLS = tmem_cols_for(NACC * ACC_COLS);
   static constexpr int BAR_BYTES = round_up(2 * STAGES * 8 + (2 * NACC + 1) * 8 + 4, 256);
   static constexpr int SMEM = STAGES * STAGE + (BRES ? B_RES_MAX : 0) + 1024 + BAR_BYTES;
@@ -751,7 +752,7 @@ struct HaloCfg {
   static constexpr int B_RES_MAX = 96 * 1024;
   static constexpr int ACC_COLS = BN < 32 ? 32 : BN;
   // TMEM accumulators in rotation: the MMA warp may run up to NACC-1 tiles ahead of the epilogue
-  static constexpr int NACC = ACC_COLS <= 64 ? 4 : 2;
+  static constexpr int NACC = ACC_COLS <= 128 ? 4 : 2;
   static constexpr int TMEM_COLS = tmem_cols_for(NACC * ACC_COLS);
   static constexpr int ROWS = 3 + (129 + WP - 1) / WP;  // padded rows one 128-row tile touches
   static constexpr int BOX_BYTES = ROWS * WP * SW;
