@@ -913,9 +913,11 @@ struct FpropM2Cfg {
   static constexpr int STAGE = round_up(2 * A_BYTES + B_BYTES, 1024);
   static constexpr int STAGES = (kFpropBudget / STAGE) > 8 ? 8 : (kFpropBudget / STAGE);
   static constexpr int ACC_COLS = BN < 32 ? 32 : BN;
-  static constexpr int TMEM_COLS = tmem_cols_for(4 * ACC_COLS);
+  // accumulator pairs in rotation: four for BN = 64 (all 512 columns), two for BN = 128
+  static constexpr int NBUF = 2 * 4 * ACC_COLS <= 512 ? 4 : 2;
+  static constexpr int TMEM_COLS = tmem_cols_for(2 * NBUF * ACC_COLS);
   static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
-  static_assert(4 * ACC_COLS <= 512, "two double-buffered accumulators must fit TMEM");
+  static_assert(2 * NBUF * ACC_COLS <= 512, "the accumulator pairs must fit TMEM");
 };
 
 template <int BN, int BKC>
@@ -927,9 +929,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = align1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
   uint64_t* empty = full + C::STAGES;
-  uint64_t* tfull = empty + C::STAGES;  // [2]
-  uint64_t* tempty = tfull + 2;         // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tfull = empty + C::STAGES;  // [NBUF]
+  uint64_t* tempty = tfull + C::NBUF;   // [NBUF]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + C::NBUF);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -944,7 +946,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < C::NBUF; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 4);
     }
@@ -998,8 +1000,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
         const int mp = t / a.n_tiles;
         const int nval = (2 * mp + 1 < a.m_tiles) ? 2 : 1;
-        const int acc = lt & 1;
-        if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
+        const int acc = lt % C::NBUF;
+        if (lt >= C::NBUF) mbar_wait(&tempty[acc], ((lt / C::NBUF) - 1) & 1);
         tc_fence_after();
         const uint32_t d0 = tmem + static_cast<uint32_t>(acc * 2 * C::ACC_COLS);
         const uint32_t d1 = d0 + static_cast<uint32_t>(C::ACC_COLS);
@@ -1026,7 +1028,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quarter = warp & 3;
     int lt = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
-      const int acc = lt & 1;
+      const int acc = lt % C::NBUF;
       const int mp = t / a.n_tiles;
       const int k0 = (t - mp * a.n_tiles) * BN;
       const int nval = (2 * mp + 1 < a.m_tiles) ? 2 : 1;
@@ -1039,7 +1041,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const TileRows rows{&a, (t2 / a.tiles_p) * a.bn, (t2 % a.tiles_p) * a.bh, tq * a.bw};
         if (u == 0) {
           fprop_epilogue<BN>(a, trow, quarter * 32 + lane, k0, rows, [&] {
-            mbar_wait(&tfull[acc], (lt >> 1) & 1);
+            mbar_wait(&tfull[acc], (lt / C::NBUF) & 1);
             tc_fence_after();
           });
         } else {
