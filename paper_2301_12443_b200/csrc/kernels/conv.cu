@@ -1413,6 +1413,7 @@ __global__ void __launch_bounds__(kRedLanes * kRedSplitLanes)
   __shared__ float4 part[kRedSplitLanes][kRedLanes];
   const int e = threadIdx.x % kRedLanes;
   const int sl = threadIdx.x / kRedLanes;
+  grid_dep_wait();  // PDL (launched with the wgrad plan's pdl flag): the split slabs are complete after this
   for (size_t base = static_cast<size_t>(blockIdx.x) * kRedLanes; base < n4;
        base += static_cast<size_t>(gridDim.x) * kRedLanes) {
     const size_t i = base + e;
@@ -1980,9 +1981,10 @@ int wgrad_run(const WgradPlan& plan, cudaStream_t stream) {
     const size_t n4 = plan.slab / 4;
     const int blocks =
         static_cast<int>(std::max<size_t>(1, std::min<size_t>((n4 + kRedLanes - 1) / kRedLanes, split_reduce_cap())));
-    split_reduce_kernel<<<blocks, kRedLanes * kRedSplitLanes, 0, stream>>>(reinterpret_cast<const float4*>(plan.args.out),
-                                                    reinterpret_cast<float4*>(plan.dw), n4, plan.splits);
-    if (cudaGetLastError() != cudaSuccess) return PBDK_ECUDA;
+    if (launch_ex(split_reduce_kernel, dim3(blocks, 1, 1), dim3(kRedLanes * kRedSplitLanes, 1, 1), 0, stream, plan.pdl,
+                  1u, reinterpret_cast<const float4*>(plan.args.out), reinterpret_cast<float4*>(plan.dw), n4,
+                  plan.splits) != cudaSuccess)
+      return PBDK_ECUDA;
   }
   return PBDK_OK;
 }
