@@ -86,6 +86,28 @@ int grid_for(long long work) {
   return static_cast<int>(std::max<long long>(1, std::min<long long>(b, cap)));
 }
 
+// Programmatic dependent launch for the MBConv kernels (every kernel calls grid_dep_wait() first): a
+// kernel's CTAs are scheduled while its predecessor in the stream drains.  PBD_PDL=0 / PBDK_MB_PDL=0
+// (experiments build): plain launches.
+template <class... KArgs, class... Args>
+cudaError_t mb_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  static const bool pdl = [] {
+    const char* e = pbd::knob_env("PBDK_MB_PDL");
+    return pbd::pdl_enabled() && (e == nullptr || e[0] != '0');
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 inline int ok(cudaError_t e) { return e == cudaSuccess ? PBDK_OK : PBDK_ECUDA; }
 
 // ------------------------------------------------------------------ depthwise forward
@@ -100,6 +122,7 @@ __global__ void __launch_bounds__(kT) dw_fwd_kernel(const __nv_bfloat16* __restr
                                                     const __nv_bfloat16* __restrict__ wt,
                                                     const float* __restrict__ bias, __nv_bfloat16* __restrict__ y,
                                                     int N, int H, int W, int C, int P, int Q, int relu6) {
+  grid_dep_wait();  // PDL (mb_launch): every global access comes after this
   constexpr int PAD = K / 2;
   constexpr int WIN = (kQT - 1) * ST + K;
   const int G = C / 8;
@@ -184,6 +207,7 @@ __global__ void __launch_bounds__(kT) dw_fwd_tiled_kernel(const __grid_constant_
                                                           __nv_bfloat16* __restrict__ y, int N, int C, int P, int Q,
                                                           int act, int TP,
                                                           const __nv_bfloat16* __restrict__ amask = nullptr) {
+  grid_dep_wait();  // PDL (mb_launch): every global access comes after this
   constexpr int PAD = K / 2;
   constexpr int G = CT / 8;
   constexpr int QT = dw_qt(K);
@@ -334,6 +358,7 @@ __global__ void __launch_bounds__(kT) dw_dgrad_kernel(const __nv_bfloat16* __res
                                                       const __nv_bfloat16* __restrict__ act,
                                                       __nv_bfloat16* __restrict__ dx, int N, int H, int W, int C, int P,
                                                       int Q, bool par) {
+  grid_dep_wait();  // PDL (mb_launch): every global access comes after this
   constexpr int PAD = K / 2;
   const int G = C / 8;
   const int total = N * H * W * G;
@@ -398,6 +423,7 @@ __global__ void __launch_bounds__(kT, K >= 7 ? 2 : 1) dw_wgrad_partial_kernel(co
                                                               const __nv_bfloat16* __restrict__ dy,
                                                               float* __restrict__ partial, int N, int H, int W, int C,
                                                               int P, int Q, int lanes_c, int rows_per_chunk) {
+  grid_dep_wait();  // PDL (mb_launch): every global access comes after this
   // Thread = (channel group, row lane): walks whole output rows (n, p) of its chunk, q ascending, with the
   // K input vectors of filter row r the current q touches held in a register window that slides by ST
   // per q — one dy load and ST activation loads per pixel instead of 1 + K.
@@ -501,6 +527,7 @@ __global__ void __launch_bounds__(kT, K >= 7 ? 2 : 1) dw_wgrad_partial_kernel(co
 constexpr int kSumLanes = 32;
 __global__ void __launch_bounds__(32 * kSumLanes) chunk_sum_kernel(const float* __restrict__ partial, int chunks,
                                                                    size_t n, float* __restrict__ out) {
+  grid_dep_wait();  // PDL (mb_launch): every global access comes after this
   __shared__ double part[kSumLanes][33];
   const size_t o = blockIdx.x * static_cast<size_t>(32) + threadIdx.x;
   double acc = 0.0;
@@ -540,6 +567,7 @@ __global__ void __launch_bounds__(kT) stem_wgrad_staged_kernel(const __nv_bfloat
                                                                const __nv_bfloat16* __restrict__ dy,
                                                                float* __restrict__ partial, int N, int S,
                                                                int rows_per_chunk) {
+  grid_dep_wait();  // PDL (mb_launch): every global access comes after this
   extern __shared__ float4 ssm[];
   const int P = S / 2;
   float4* xs = ssm;                             // [3][S + 2] pixels (c0, c1, c2, 0), column -1 .. S
@@ -623,6 +651,7 @@ __global__ void __launch_bounds__(kT) stem_fwd_kernel(const __nv_bfloat16* __res
                                                       const __nv_bfloat16* __restrict__ w,
                                                       const float* __restrict__ bias, __nv_bfloat16* __restrict__ y,
                                                       int N, int S, int relu6) {
+  grid_dep_wait();  // PDL (mb_launch): every global access comes after this
   __shared__ __align__(16) float ws[27][32];  // [r*9 + s*3 + c][k]
   for (int i = threadIdx.x; i < 27 * 32; i += blockDim.x) {
     const int k = i % 32, t = i / 32;
@@ -687,6 +716,7 @@ __global__ void __launch_bounds__(kT) stem_wgrad_partial_kernel(const __nv_bfloa
                                                                 const __nv_bfloat16* __restrict__ dy,
                                                                 float* __restrict__ partial, int N, int S,
                                                                 int rows_per_chunk) {
+  grid_dep_wait();  // PDL (mb_launch): every global access comes after this
   __shared__ float red[8][27][32];
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const int P = S / 2;
@@ -753,6 +783,7 @@ __global__ void __launch_bounds__(kT) bn_apply_act_kernel(const __nv_bfloat16* _
                                                           const float* __restrict__ beta,
                                                           const __nv_bfloat16* __restrict__ res,
                                                           __nv_bfloat16* __restrict__ out, int m, int C) {
+  grid_dep_wait();  // PDL (mb_launch): every global access comes after this
   const int cg = C / 8;
   const int rpp = kT / cg;
   const int g = threadIdx.x % cg;
@@ -792,6 +823,7 @@ __global__ void __launch_bounds__(kT) mse_affine_partial_kernel(const __nv_bfloa
                                                                 const __nv_bfloat16* __restrict__ t, long long m,
                                                                 int C, float gscale, __nv_bfloat16* __restrict__ g,
                                                                 double* __restrict__ loss_partial) {
+  grid_dep_wait();  // PDL (mb_launch): every global access comes after this
   __shared__ double sm[kT / 32];
   const int G = C / 8;
   const long long total = m * G;
@@ -830,6 +862,7 @@ __global__ void __launch_bounds__(kT) mse_affine_partial_kernel(const __nv_bfloa
 
 // one CTA: strided per-thread sums, xor-shuffle tree per warp, warps added in order (deterministic)
 __global__ void loss_sum_kernel(const double* __restrict__ part, int n, double norm, double* __restrict__ loss) {
+  grid_dep_wait();  // PDL (mb_launch): every global access comes after this
   __shared__ double sm[kT / 32];
   double s = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
@@ -853,6 +886,7 @@ __global__ void loss_sum_kernel(const double* __restrict__ part, int n, double n
 constexpr int kPoolSlots = kT / 32;
 __global__ void __launch_bounds__(kT) se_pool_kernel(const __nv_bfloat16* __restrict__ y, int hw, int E,
                                                      float* __restrict__ pooled) {
+  grid_dep_wait();  // PDL (mb_launch): every global access comes after this
   __shared__ double red[kPoolSlots][32][8];
   const int n = blockIdx.x;
   const int gl = threadIdx.x & 31, slot = threadIdx.x >> 5;
@@ -889,6 +923,7 @@ __global__ void __launch_bounds__(kT) se_fc_kernel(const float* __restrict__ poo
                                                    const float* __restrict__ b1, const __nv_bfloat16* __restrict__ w2,
                                                    const float* __restrict__ b2, int E, int cs,
                                                    float* __restrict__ gate) {
+  grid_dep_wait();  // PDL (mb_launch): every global access comes after this
   extern __shared__ float sm[];  // pooled[E], h[cs]
   float* pl = sm;
   float* h = sm + E;
@@ -918,6 +953,7 @@ __global__ void __launch_bounds__(kT) se_fc_kernel(const float* __restrict__ poo
 // y[n][q][c] = bf16(y * gate[n][c]) in place
 __global__ void __launch_bounds__(kT) se_scale_kernel(__nv_bfloat16* __restrict__ y, const float* __restrict__ gate,
                                                       int hw, int E, int total) {
+  grid_dep_wait();  // PDL (mb_launch): every global access comes after this
   const int G = E / 8;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const int g = i % G;
@@ -938,11 +974,11 @@ cudaError_t launch_dw_fwd(int st, const DwArgs& d, const void* x, const void* wt
                           int relu6, cudaStream_t s) {
   const int g = grid_for(static_cast<long long>(d.n) * d.p * ((d.q + kQT - 1) / kQT) * (d.c / 8));
   if (st == 1)
-    dw_fwd_kernel<K, 1><<<g, kT, 0, s>>>(static_cast<const __nv_bfloat16*>(x),
+    mb_launch(dw_fwd_kernel<K, 1>, dim3(g), dim3(kT), 0, s, static_cast<const __nv_bfloat16*>(x),
                                          static_cast<const __nv_bfloat16*>(wt), bias,
                                          static_cast<__nv_bfloat16*>(y), d.n, d.h, d.w, d.c, d.p, d.q, relu6);
   else
-    dw_fwd_kernel<K, 2><<<g, kT, 0, s>>>(static_cast<const __nv_bfloat16*>(x),
+    mb_launch(dw_fwd_kernel<K, 2>, dim3(g), dim3(kT), 0, s, static_cast<const __nv_bfloat16*>(x),
                                          static_cast<const __nv_bfloat16*>(wt), bias,
                                          static_cast<__nv_bfloat16*>(y), d.n, d.h, d.w, d.c, d.p, d.q, relu6);
   return cudaGetLastError();
@@ -954,11 +990,11 @@ cudaError_t launch_dw_dgrad(int st, const DwArgs& d, const void* dy, const void*
   const int g = grid_for(static_cast<long long>(d.n) * d.h * d.w * (d.c / 8));
   auto* a = static_cast<const __nv_bfloat16*>(act);
   if (st == 1)
-    dw_dgrad_kernel<K, 1><<<g, kT, 0, s>>>(static_cast<const __nv_bfloat16*>(dy),
+    mb_launch(dw_dgrad_kernel<K, 1>, dim3(g), dim3(kT), 0, s, static_cast<const __nv_bfloat16*>(dy),
                                            static_cast<const __nv_bfloat16*>(wt), a,
                                            static_cast<__nv_bfloat16*>(dx), d.n, d.h, d.w, d.c, d.p, d.q, false);
   else
-    dw_dgrad_kernel<K, 2><<<g, kT, 0, s>>>(static_cast<const __nv_bfloat16*>(dy),
+    mb_launch(dw_dgrad_kernel<K, 2>, dim3(g), dim3(kT), 0, s, static_cast<const __nv_bfloat16*>(dy),
                                            static_cast<const __nv_bfloat16*>(wt), a,
                                            static_cast<__nv_bfloat16*>(dx), d.n, d.h, d.w, d.c, d.p, d.q,
                                            d.h % 2 == 0 && d.w % 2 == 0);
@@ -990,15 +1026,15 @@ cudaError_t launch_dw_wgrad(int st, const DwArgs& d, const void* a, const void* 
   const WgradTiling t = dw_wgrad_tiling(d);
   const dim3 grid(t.chunks, t.cwin, K);
   if (st == 1)
-    dw_wgrad_partial_kernel<K, 1><<<grid, kT, 0, s>>>(static_cast<const __nv_bfloat16*>(a),
+    mb_launch(dw_wgrad_partial_kernel<K, 1>, dim3(grid), dim3(kT), 0, s, static_cast<const __nv_bfloat16*>(a),
                                                       static_cast<const __nv_bfloat16*>(dy), partial, d.n, d.h, d.w,
                                                       d.c, d.p, d.q, t.lanes_c, t.per_chunk);
   else
-    dw_wgrad_partial_kernel<K, 2><<<grid, kT, 0, s>>>(static_cast<const __nv_bfloat16*>(a),
+    mb_launch(dw_wgrad_partial_kernel<K, 2>, dim3(grid), dim3(kT), 0, s, static_cast<const __nv_bfloat16*>(a),
                                                       static_cast<const __nv_bfloat16*>(dy), partial, d.n, d.h, d.w,
                                                       d.c, d.p, d.q, t.lanes_c, t.per_chunk);
   const size_t n = static_cast<size_t>(d.c) * K * K;
-  chunk_sum_kernel<<<static_cast<int>((n + 31) / 32), dim3(32, kSumLanes), 0, s>>>(partial, t.chunks, n, dw);
+  mb_launch(chunk_sum_kernel, dim3(static_cast<int>((n + 31) / 32)), dim3(dim3(32, kSumLanes)), 0, s, partial, t.chunks, n, dw);
   return cudaGetLastError();
 }
 
@@ -1088,7 +1124,7 @@ cudaError_t launch_dw_fwd_tiled(const DwArgs& d, const DwTilePlan& t, const void
   const long long tiles = static_cast<long long>(d.n) * ((d.p + t.tp - 1) / t.tp) * (d.c / CT);
   const int per_sm = t.smem * 2 <= 200 * 1024 ? 2 : 1;
   const int grid = static_cast<int>(std::min<long long>(tiles, 148LL * per_sm));
-  dw_fwd_tiled_kernel<K, ST, CT, DG><<<grid, kT, t.smem, s>>>(tmx, tmw, bias, static_cast<__nv_bfloat16*>(y), d.n,
+  mb_launch(dw_fwd_tiled_kernel<K, ST, CT, DG>, dim3(grid), dim3(kT), t.smem, s, tmx, tmw, bias, static_cast<__nv_bfloat16*>(y), d.n,
                                                              d.c, d.p, d.q, act, t.tp,
                                                              static_cast<const __nv_bfloat16*>(amask));
   return cudaGetLastError();
@@ -1167,7 +1203,7 @@ int dw_wgrad(const DwArgs& d, const void* a, const void* dy, float* ws, size_t w
 
 int stem_fwd(const void* x, const void* w, const float* bias, void* y, int n, int S, int relu6, cudaStream_t s) {
   if (n < 1 || S < 2 || S % 2 != 0 || static_cast<long long>(n) * S * S >= (1LL << 29)) return PBDK_EINVAL;
-  stem_fwd_kernel<<<grid_for((static_cast<long long>(n) * (S / 2) * (S / 2) + 31) / 32 * 64), kT, 0, s>>>(
+  mb_launch(stem_fwd_kernel, dim3(grid_for((static_cast<long long>(n) * (S / 2) * (S / 2) + 31) / 32 * 64)), dim3(kT), 0, s, 
       static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(w), bias,
       static_cast<__nv_bfloat16*>(y), n, S, relu6);
   return ok(cudaGetLastError());
@@ -1191,13 +1227,13 @@ int stem_wgrad(const void* x, const void* dy, int n, int S, float* ws, size_t ws
     return e == nullptr || e[0] != '0';
   }();
   if (staged && smem <= 48 * 1024) {
-    stem_wgrad_staged_kernel<<<chunks, kT, smem, s>>>(static_cast<const __nv_bfloat16*>(x),
+    mb_launch(stem_wgrad_staged_kernel, dim3(chunks), dim3(kT), smem, s, static_cast<const __nv_bfloat16*>(x),
                                                       static_cast<const __nv_bfloat16*>(dy), ws, n, S, per);
   } else {
-    stem_wgrad_partial_kernel<<<chunks, kT, 0, s>>>(static_cast<const __nv_bfloat16*>(x),
+    mb_launch(stem_wgrad_partial_kernel, dim3(chunks), dim3(kT), 0, s, static_cast<const __nv_bfloat16*>(x),
                                                     static_cast<const __nv_bfloat16*>(dy), ws, n, S, per);
   }
-  chunk_sum_kernel<<<(32 * 9 * 16 + 31) / 32, dim3(32, kSumLanes), 0, s>>>(ws, chunks, 32 * 9 * 16, dw);
+  mb_launch(chunk_sum_kernel, dim3((32 * 9 * 16 + 31) / 32), dim3(dim3(32, kSumLanes)), 0, s, ws, chunks, 32 * 9 * 16, dw);
   return ok(cudaGetLastError());
 }
 
@@ -1210,11 +1246,11 @@ int bn_apply_act(const void* y, const float* mean_rstd, const float* gamma, cons
   auto* rr = static_cast<const __nv_bfloat16*>(res);
   auto* oo = static_cast<__nv_bfloat16*>(out);
   if (relu6 && res == nullptr)
-    bn_apply_act_kernel<6, false><<<g, kT, 0, s>>>(yy, mean_rstd, gamma, beta, rr, oo, static_cast<int>(m), c);
+    mb_launch(bn_apply_act_kernel<6, false>, dim3(g), dim3(kT), 0, s, yy, mean_rstd, gamma, beta, rr, oo, static_cast<int>(m), c);
   else if (!relu6 && res == nullptr)
-    bn_apply_act_kernel<0, false><<<g, kT, 0, s>>>(yy, mean_rstd, gamma, beta, rr, oo, static_cast<int>(m), c);
+    mb_launch(bn_apply_act_kernel<0, false>, dim3(g), dim3(kT), 0, s, yy, mean_rstd, gamma, beta, rr, oo, static_cast<int>(m), c);
   else if (!relu6)
-    bn_apply_act_kernel<0, true><<<g, kT, 0, s>>>(yy, mean_rstd, gamma, beta, rr, oo, static_cast<int>(m), c);
+    mb_launch(bn_apply_act_kernel<0, true>, dim3(g), dim3(kT), 0, s, yy, mean_rstd, gamma, beta, rr, oo, static_cast<int>(m), c);
   else
     return PBDK_EINVAL;
   return ok(cudaGetLastError());
@@ -1223,11 +1259,11 @@ int bn_apply_act(const void* y, const float* mean_rstd, const float* gamma, cons
 int se_apply(void* y, int n, int hw, int E, int cs, const void* w1, const float* b1, const void* w2,
              const float* b2, float* pooled, float* gate, cudaStream_t s) {
   if (E % 8 != 0 || cs < 1 || n < 1 || static_cast<long long>(n) * hw * E >= (1LL << 31)) return PBDK_EINVAL;
-  se_pool_kernel<<<dim3(n, (E / 8 + 31) / 32), kT, 0, s>>>(static_cast<const __nv_bfloat16*>(y), hw, E, pooled);
-  se_fc_kernel<<<n, kT, (E + cs) * sizeof(float), s>>>(pooled, static_cast<const __nv_bfloat16*>(w1), b1,
+  mb_launch(se_pool_kernel, dim3(dim3(n, (E / 8 + 31) / 32)), dim3(kT), 0, s, static_cast<const __nv_bfloat16*>(y), hw, E, pooled);
+  mb_launch(se_fc_kernel, dim3(n), dim3(kT), (E + cs) * sizeof(float), s, pooled, static_cast<const __nv_bfloat16*>(w1), b1,
                                                         static_cast<const __nv_bfloat16*>(w2), b2, E, cs, gate);
   const int total = n * hw * (E / 8);
-  se_scale_kernel<<<grid_for(total), kT, 0, s>>>(static_cast<__nv_bfloat16*>(y), gate, hw, E, total);
+  mb_launch(se_scale_kernel, dim3(grid_for(total)), dim3(kT), 0, s, static_cast<__nv_bfloat16*>(y), gate, hw, E, total);
   return ok(cudaGetLastError());
 }
 
@@ -1238,11 +1274,11 @@ int mse_affine(const void* y, const float* mean_rstd, const float* gamma, const 
                cudaStream_t s) {
   if (c % 8 != 0 || m < 1) return PBDK_EINVAL;
   const int grid = grid_for(m * (c / 8));
-  mse_affine_partial_kernel<<<grid, kT, 0, s>>>(static_cast<const __nv_bfloat16*>(y), mean_rstd, gamma, beta,
+  mb_launch(mse_affine_partial_kernel, dim3(grid), dim3(kT), 0, s, static_cast<const __nv_bfloat16*>(y), mean_rstd, gamma, beta,
                                                 static_cast<const __nv_bfloat16*>(res),
                                                 static_cast<const __nv_bfloat16*>(t), m, c, gscale,
                                                 static_cast<__nv_bfloat16*>(g), ws);
-  loss_sum_kernel<<<1, kT, 0, s>>>(ws, grid, norm, loss);
+  mb_launch(loss_sum_kernel, dim3(1), dim3(kT), 0, s, ws, grid, norm, loss);
   return ok(cudaGetLastError());
 }
 
