@@ -17,10 +17,30 @@
 #include <algorithm>
 
 #include "conv.hpp"
+#include "knobs.hpp"
 #include "sm100.cuh"
 #include "tmap.hpp"
 
 namespace pbdk {
+
+namespace {
+// programmatic dependent launch for the fp32 workload's tcgen05 convs and split sums (the kernels wait
+// with griddepcontrol.wait before touching global memory); PBD_PDL=0 in the experiments build: plain
+template <class... KArgs, class... Args>
+cudaError_t f3_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pbd::pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+}  // namespace
 
 namespace {
 
@@ -82,6 +102,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  grid_dep_wait();  // PDL (f3_launch): the prologue above overlapped the previous kernel
 
   if (warp == 0) {
     if (lane == 0) {
@@ -213,7 +234,7 @@ cudaError_t launch_fprop(const F3FpropPlan& p, cudaStream_t st) {
   using C = F3FpropCfg<BN, CK>;
   if (st == reinterpret_cast<cudaStream_t>(-1))  // plan-time attribute setup
     return cudaFuncSetAttribute(conv3x_fprop_kernel<BN, CK>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-  conv3x_fprop_kernel<BN, CK><<<p.grid, kThreads, C::SMEM, st>>>(p.tmx, p.tmw, p.args);
+  f3_launch(conv3x_fprop_kernel<BN, CK>, p.grid, dim3(kThreads), C::SMEM, st, p.tmx, p.tmw, p.args);
   return cudaGetLastError();
 }
 
@@ -279,6 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  grid_dep_wait();  // PDL (f3_launch): the prologue above overlapped the previous kernel
 
   if (warp == 0) {
     if (lane == 0) {
@@ -365,12 +387,13 @@ cudaError_t launch_wgrad(const F3WgradPlan& p, cudaStream_t st) {
   using C = F3WgradCfg<BN>;
   if (st == reinterpret_cast<cudaStream_t>(-1))
     return cudaFuncSetAttribute(conv3x_wgrad_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-  conv3x_wgrad_kernel<BN><<<p.grid, kThreads, C::SMEM, st>>>(p.tmdy, p.tmx, p.args);
+  f3_launch(conv3x_wgrad_kernel<BN>, p.grid, dim3(kThreads), C::SMEM, st, p.tmdy, p.tmx, p.args);
   return cudaGetLastError();
 }
 
 // dw[i] = sum_s ws[s][i] in split order
 __global__ void f3_split_sum_kernel(const float4* __restrict__ ws, float4* __restrict__ dw, size_t n4, int splits) {
+  grid_dep_wait();  // PDL (f3_launch): the split slabs are complete after this
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n4;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     float4 acc = ws[i];
@@ -555,9 +578,10 @@ int f3_wgrad_run(const F3WgradPlan& plan, cudaStream_t st) {
   if (plan.launch(plan, st) != cudaSuccess) return PBDK_ECUDA;
   if (plan.splits > 1) {
     const size_t n4 = plan.slab / 4;
-    f3_split_sum_kernel<<<grid_for(n4), 256, 0, st>>>(reinterpret_cast<const float4*>(plan.args.out),
-                                                      reinterpret_cast<float4*>(plan.dw), n4, plan.splits);
-    if (cudaGetLastError() != cudaSuccess) return PBDK_ECUDA;
+    if (f3_launch(f3_split_sum_kernel, dim3(grid_for(n4)), dim3(256), 0, st,
+                  reinterpret_cast<const float4*>(plan.args.out), reinterpret_cast<float4*>(plan.dw), n4,
+                  plan.splits) != cudaSuccess)
+      return PBDK_ECUDA;
   }
   return PBDK_OK;
 }
